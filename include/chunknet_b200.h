@@ -1,0 +1,196 @@
+/*
+ * chunknet_b200.h -- C ABI of the B200-native hot path of the chunknet
+ * multipath transport (arXiv 2504.17307, reference: /root/reference/proj).
+ *
+ * The boundary is plain C: opaque handles, integer status codes, plain
+ * pointers + sizes.  No C++ exceptions and no torch types cross it.  Every
+ * entry point names the reference interface it replaces (file:line into
+ * /root/reference/proj).
+ *
+ * Device pointers are marked d_*; host pointers h_*.  Asynchronous calls
+ * take a cudaStream_t passed as void* (NULL = legacy default stream) and
+ * never synchronise the host unless documented.
+ */
+#ifndef CHUNKNET_B200_H
+#define CHUNKNET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------- constants */
+/* NetParams::mtu / hdr_overhead defaults (include/chunknet/network.hpp:25-26):
+ * 4096-byte MTU including a 64-byte header -> 4032 payload bytes/packet. */
+#define CN_MTU 4096u
+#define CN_HDR_OVERHEAD 64u
+#define CN_MAX_PAYLOAD 4032u
+/* kCsnWindow (src/transport.cpp:14): unacked chunks per message. */
+#define CN_CSN_WINDOW 128
+/* uint32_t packet bitmask per chunk (transport.hpp:195). */
+#define CN_MAX_PKTS_PER_CHUNK 32
+/* array<MsgRecv,128> / 7-bit msg_id (transport.hpp:222, wire.hpp:15). */
+#define CN_MSG_SLOTS 128
+
+/* ----------------------------------------------------------- status codes
+ * The reference throws; the ABI returns one of these and records a message
+ * retrievable with cn_last_error(). */
+#define CN_OK 0
+#define CN_E_INVALID (-1)       /* std::invalid_argument                   */
+#define CN_E_LOGIC (-2)         /* std::logic_error (policy contract, ...)  */
+#define CN_E_FIELD_RANGE (-3)   /* chunknet::FieldRangeError (wire.hpp:29)  */
+#define CN_E_OUT_OF_WINDOW (-4) /* chunknet::OutOfWindowError (wire.hpp:37) */
+#define CN_E_CUDA (-5)          /* CUDA runtime failure                     */
+#define CN_E_UNSUPPORTED (-6)   /* input outside the device path's domain   */
+#define CN_E_CAPACITY (-7)      /* a configured table/pool/output is full   */
+
+/* Thread-local description of the last non-OK status. */
+const char* cn_last_error(void);
+/* Library version string and the sm arch it was compiled for. */
+const char* cn_version(void);
+
+/* ------------------------------------------------------------------ wire
+ * ControlHeader (include/chunknet/wire.hpp:18-26): [31:24] conn_id,
+ * [23:17] msg_id, [16:9] csn, [8] last_chunk, [7:0] reserved. */
+typedef struct cn_control_header {
+    uint8_t conn_id;
+    uint8_t msg_id; /* 0..127 */
+    uint8_t csn;
+    uint8_t last_chunk; /* 0/1 */
+    uint8_t reserved;
+} cn_control_header;
+
+/* encode_header (src/wire.cpp:5-14): CN_E_FIELD_RANGE if msg_id > 127. */
+int cn_encode_header(const cn_control_header* h, uint32_t* out_word);
+/* decode_header (src/wire.cpp:16-24). */
+void cn_decode_header(uint32_t word, cn_control_header* out);
+/* csn_before (src/wire.cpp:26-40) over SeqWindow{base, width}
+ * (wire.hpp:47-62): CN_E_FIELD_RANGE for width outside [1,128],
+ * CN_E_OUT_OF_WINDOW if a or b is outside the window. *out = 0/1. */
+int cn_csn_before(uint8_t a, uint8_t b, uint8_t base, int width, int* out);
+
+/* ------------------------------------------------------ packet records
+ * The 64-byte per-packet header record: the reference's per-packet
+ * hdr_overhead (network.hpp:26) carrying the 32-bit control word plus the
+ * data fields of chunknet::Packet the receiver reads (packet.hpp:33-86). */
+#define CN_PKT_RTX 0x1u     /* Packet::is_rtx  */
+#define CN_PKT_ECN 0x2u     /* Packet::ecn     */
+#define CN_PKT_TRIMMED 0x4u /* Packet::trimmed */
+typedef struct cn_pkt_hdr {
+    int32_t src;           /* source host            */
+    int32_t dst;           /* destination host       */
+    int32_t path_id;       /* path the packet took   */
+    uint32_t hdr;          /* encode_header(ControlHeader) */
+    uint64_t chunk_offset; /* byte offset of the chunk in its message */
+    uint32_t chunk_len;    /* total chunk length     */
+    uint16_t payload_len;  /* <= CN_MAX_PAYLOAD      */
+    uint8_t seq_in_chunk;  /* < 32                   */
+    uint8_t flags;         /* CN_PKT_*               */
+    int64_t tx_time;       /* ns, echoed by acks     */
+    uint64_t msg_seq;      /* per-connection message generation */
+    uint64_t msg_tag;      /* caller's flow tag      */
+    uint64_t msg_len;      /* total message length   */
+} cn_pkt_hdr;
+
+/* ACK record: the ack fields of chunknet::Packet (packet.hpp:73-79) as
+ * built by Transport::send_ack (transport.cpp:763-792) or the stale re-ack
+ * (transport.cpp:602-615). */
+#define CN_ACK_CUM_VALID 0x1u
+#define CN_ACK_ECN_ECHO 0x2u
+typedef struct cn_ack_rec {
+    int32_t src;          /* ack source = receiving host   */
+    int32_t dst;          /* ack destination = sender host */
+    uint32_t hdr;         /* conn_id | msg_id | csn = cause chunk csn */
+    int32_t echo_path_id;
+    uint8_t cum_csn;
+    uint8_t flags;        /* CN_ACK_* */
+    uint16_t reserved;
+    uint32_t pkt_index;   /* index in the batch of the data packet that triggered it */
+    uint64_t msg_seq;
+    uint64_t sack[2];     /* SackBitmap, bit j = chunk cum+j complete */
+    int64_t echo_tx_time;
+    int64_t aux;          /* 0 from the device path (fixtures: delivery time) */
+} cn_ack_rec;
+
+/* One delivered message (Transport::maybe_deliver, transport.cpp:794-803). */
+typedef struct cn_completion {
+    uint64_t tag;
+    int32_t src;
+    int32_t dst;
+    uint64_t len;
+    uint64_t msg_seq;
+    uint32_t pkt_index;   /* batch index of the packet that completed it */
+    uint32_t msg_id;
+    uint64_t buf_offset;  /* byte offset of the message in the rx arena */
+    uint64_t bytes;       /* MsgRecv::bytes: payload bytes accepted */
+    uint64_t reserved;
+} cn_completion;
+
+/* ------------------------------------------------------------- receiver
+ * Device-resident receive side of chunknet::Transport for the selective
+ * (multipath) reliability mode with the reference's fixed-size chunking
+ * (DefaultPolicy::on_chunk_size, policy.hpp:75-78).  Replaces, for a batch
+ * of delivered data packets in arrival order:
+ *   Transport::handle_packet/rconn_at   (transport.cpp:546-594)
+ *   Transport::handle_data               (transport.cpp:596-688)
+ *   Transport::accept_payload            (transport.cpp:719-730)
+ *   Transport::chunk_completed           (transport.cpp:732-761)
+ *   Transport::send_ack                  (transport.cpp:763-792)
+ *   Transport::maybe_deliver             (transport.cpp:794-803)
+ * State persists across batches: splitting a packet sequence into batches
+ * yields the same ack stream as one batch. */
+typedef struct cn_rx_config {
+    uint32_t chunk_bytes;    /* TransportConfig::chunk_bytes (transport.hpp:27) */
+    uint32_t max_payload;    /* Network::max_payload(); 0 = CN_MAX_PAYLOAD      */
+    uint32_t max_conns;      /* receive connections (rounded up to pow2)        */
+    uint32_t max_msgs;       /* concurrently live messages (rounded up to pow2) */
+    uint64_t chunk_pool;     /* chunk state entries (sum of chunks of live msgs)*/
+    uint64_t arena_bytes;    /* device bytes for reassembled message buffers    */
+    uint32_t max_batch;      /* max packets per cn_rx_batch                     */
+    int32_t carry_payload;   /* TransportConfig::carry_payload                  */
+} cn_rx_config;
+
+typedef struct cn_rx cn_rx;
+
+/* Fills *cfg with defaults (chunk_bytes 32768, 1024 conns, 4096 msgs,
+ * 1<<22 chunks, 1 GiB arena, 1<<20 packets/batch, carry_payload 1). */
+void cn_rx_config_default(cn_rx_config* cfg);
+int cn_rx_create(const cn_rx_config* cfg, cn_rx** out);
+void cn_rx_destroy(cn_rx* rx);
+/* Forget every connection and message (fresh Transport receive state). */
+int cn_rx_reset(cn_rx* rx, void* stream);
+
+/* Batch result counters, written by the device (d_result). */
+typedef struct cn_rx_result {
+    uint32_t n_acks;
+    uint32_t n_completions;
+    uint32_t status;      /* 0 or CN_RXF_* bits */
+    uint32_t n_copied;    /* packets whose payload was accepted */
+    uint64_t bytes_copied;
+} cn_rx_result;
+#define CN_RXF_UNSUPPORTED 0x1u  /* trimmed pkt / non-fixed chunking / bad seq */
+#define CN_RXF_ALIAS 0x2u        /* csn unwrap would alias */
+#define CN_RXF_CAPACITY 0x4u     /* table/pool/arena/output overflow */
+#define CN_RXF_GENERATION 0x8u   /* msg id reused before completion */
+
+/* Process n data packets (arrival order).  d_payload + i*payload_stride
+ * holds packet i's payload_len bytes.  ACK records are appended in emission
+ * order to d_acks (max_acks), completions to d_completions.  Asynchronous
+ * on `stream`; d_result is written when the batch finishes. */
+int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
+                uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks,
+                uint32_t max_acks, cn_completion* d_completions,
+                uint32_t max_completions, cn_rx_result* d_result,
+                void* stream);
+/* Device base pointer of the reassembly arena (cn_completion::buf_offset). */
+void* cn_rx_arena(cn_rx* rx);
+/* Number of kernel launches the last cn_rx_batch issued. */
+int cn_rx_last_launches(const cn_rx* rx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHUNKNET_B200_H */

@@ -1,0 +1,155 @@
+"""Generates tests/golden/*.npz from the UNMODIFIED reference -- TEST INFRA.
+
+Run where /root/reference is mounted, after `make -C oracle ref`:
+
+    python -m oracle.gen_fixtures
+
+For every scenario the reference discrete-event simulator
+(Network + Transport, src/network.cpp, src/transport.cpp) is run with
+carry_payload and pattern payloads (test_transport.cpp:63-71, seed = tag);
+the data packets delivered at their destinations are recorded in arrival
+order, then replayed into a fresh reference Transport's receive path
+(Transport::handle_packet, transport.cpp:565) to capture the exact ack
+stream (emission order, causing packet index) and the completions.  The
+script asserts that (a) every DES completion was byte-identical to its
+source, and (b) for single-connection scenarios the replay ack stream equals
+the ack stream the DES delivered to the sender (replay purity, SURVEY.md
+Appendix B).
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+from . import ref
+from .records import ACK_FIELDS, ack_equal
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+MiB = 1 << 20
+
+# name -> (record kwargs, flows)
+SCENARIOS = {
+    # BASELINE.json configs[0]: 1 MiB, 4 KiB chunks, 8 paths, no loss
+    "cfg1": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,
+                  loss=0.0, seed=1, chunk_bytes=4096, paths=8, lb="p2_rtt",
+                  cc="cubic"), [(0, 127, MiB, 1)]),
+    # BASELINE.json configs[1]: 64 MiB, 256 paths, 1% drop (32 KiB / 4 KiB chunks)
+    "cfg2_32k": (dict(topo="fat_tree", topo_arg=32, rate_bps=400e9, qcap_bytes=MiB,
+                      loss=0.01, seed=1, chunk_bytes=32768, paths=256, lb="p2_rtt",
+                      cc="cubic"), [(0, 8191, 64 * MiB, 1)]),
+    "cfg2_4k": (dict(topo="fat_tree", topo_arg=32, rate_bps=400e9, qcap_bytes=MiB,
+                     loss=0.01, seed=1, chunk_bytes=4096, paths=256, lb="p2_rtt",
+                     cc="cubic"), [(0, 8191, 64 * MiB, 1)]),
+    # reference test "csn wrap-around: 600 chunks reassemble under loss"
+    # (test_transport.cpp:330-357)
+    "csn_wrap": (dict(topo="star", topo_arg=2, rate_bps=10e9, qcap_bytes=MiB,
+                      loss=0.01, seed=5, chunk_bytes=4032, paths=1, lb="oblivious",
+                      cc="cubic"), [(0, 1, 600 * 4032, 1)]),
+    # reference test "lossy link: retransmission delivers byte-identical data"
+    "lossy_2m": (dict(topo="star", topo_arg=2, rate_bps=10e9, qcap_bytes=MiB,
+                      loss=0.02, seed=4, chunk_bytes=32768, paths=1, lb="oblivious",
+                      cc="cubic"), [(0, 1, 2 * MiB, 1)]),
+    # reference test "multipath spray with loss keeps payload integrity"
+    "multipath_k4": (dict(topo="fat_tree", topo_arg=4, rate_bps=10e9, qcap_bytes=MiB,
+                          loss=0.01, seed=6, chunk_bytes=16128, paths=4, lb="p2_rtt",
+                          cc="cubic"), [(0, 12, MiB, 1), (5, 12, MiB, 1)]),
+    # many generations per connection, msg-id reuse, 3% loss
+    "multigen_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=MiB,
+                         loss=0.03, seed=11, chunk_bytes=4032, paths=16, lb="p2_ecn",
+                         cc="none"), [(0, 127, 64 * 1024, 32)]),
+    # concurrent messages on one connection + several connections into one host
+    "concurrent_k4": (dict(topo="fat_tree", topo_arg=4, rate_bps=100e9, qcap_bytes=MiB,
+                           loss=0.01, seed=12, chunk_bytes=8064, paths=4, lb="p2_rtt",
+                           cc="swift", window=4),
+                      [(0, 12, 300_000, 6), (5, 12, 123_457, 6), (13, 2, 1, 3),
+                       (7, 3, 4031, 4), (8, 3, 4033, 4)]),
+    # chunk size not a multiple of 16: unaligned scatter, runt packets
+    "odd_chunk": (dict(topo="star", topo_arg=6, rate_bps=100e9, qcap_bytes=MiB,
+                       loss=0.02, seed=13, chunk_bytes=5000, paths=1, lb="oblivious",
+                       cc="cubic", window=2),
+                  [(0, 1, 77_777, 3), (2, 1, 5000, 2), (3, 4, 12_345, 3),
+                   (5, 4, 7, 2)]),
+    # 4 x 1 MiB, 16 paths, 1% (survey Appendix B item 10)
+    "k8_4x1m": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,
+                     loss=0.01, seed=3, chunk_bytes=32768, paths=16, lb="p2_rtt",
+                     cc="cubic"), [(0, 127, MiB, 4)]),
+}
+
+
+def gen(name, kw, flows):
+    kw = dict(kw)
+    window = kw.pop("window", 1)
+    tmp = f"/tmp/cnfix_{name}"
+    data, acks_des, cpl_des, st = ref.record(tmp, flows=flows, window=window, **kw)
+    assert st["quiesced"] == 1, (name, st)
+    assert st["bytes_ok"] == st["completions"], (name, st)
+    acks, cpls, arena = ref.rx_replay(data, st["n_hosts"], kw["chunk_bytes"])
+    assert len(cpls) == st["completions"], (name, len(cpls), st)
+    conns = {(int(s), int(d)) for s, d in zip(data["src"], data["dst"])}
+    if len(conns) == 1:
+        a2 = acks_des.copy()
+        a2["pkt_index"] = acks["pkt_index"]
+        ok, bad = ack_equal(acks, a2)
+        assert ok, (name, bad)
+    meta = dict(name=name, n_hosts=int(st["n_hosts"]), chunk_bytes=int(kw["chunk_bytes"]),
+                record=dict(kw, window=window), flows=flows,
+                des_stats={k: int(v) for k, v in st.items()})
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    np.savez_compressed(path, data=data, acks=acks, completions=cpls,
+                        meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
+    print(f"{name}: pkts={len(data)} acks={len(acks)} completions={len(cpls)} "
+          f"rtx={st['chunk_rtx']} fast_rtx={st['fast_rtx']} rtos={st['rtos']} "
+          f"-> {os.path.getsize(path)} B")
+
+
+def gen_rng():
+    """RngStream / select_path draw sequences (rng.hpp:29-60, lb.cpp:7-27).
+
+    The reference tests pin only statistics here (test_lb.cpp:34-108), so
+    the literal sequences come from running the compiled reference."""
+    out = {}
+    # raw mt19937_64 outputs of per-connection streams (transport.cpp:101)
+    for idx in (0, 1, 2, 255, 1023):
+        out[f"u64_conn{idx}"] = ref.rng_u64(1, "transport.conn", idx, 1000)
+    out["u64_named_loss7"] = ref.rng_u64(42, "loss", 7, 1000)
+    out["u64_unindexed"] = ref.rng_u64(9, "workload", -1, 1000)
+    # next_below over assorted ranges incl. non powers of two (Lemire rejection)
+    rs = np.random.RandomState(5)
+    ns = np.concatenate([np.array([1, 2, 3, 7, 8, 255, 256, 1000, 2**33 + 5,
+                                   2**63 + 1, 2**64 - 1], dtype=np.uint64),
+                         rs.randint(1, 1 << 30, size=4000).astype(np.uint64)])
+    out["below_ns"] = ns
+    out["below_vals"] = ref.next_below(3, "transport.conn", 17, ns)
+    out["double_vals"] = ref.next_double(3, "loss", 2, 1000)
+    # select_path on fixed boards
+    for n_paths in (1, 2, 7, 8, 256):
+        rtt = 10000.0 + rs.randint(0, 5000, size=n_paths).astype(np.float64)
+        rtt[rs.randint(0, n_paths, size=max(1, n_paths // 4))] = 12345.0  # ties
+        ecn = rs.randint(0, 9, size=n_paths) / 8.0
+        out[f"board{n_paths}_rtt"] = rtt
+        out[f"board{n_paths}_ecn"] = ecn
+        for pol in ("oblivious", "p2_rtt", "p2_ecn"):
+            for idx in (0, 5):
+                out[f"sel_{pol}_{n_paths}_{idx}"] = ref.select_paths(
+                    pol, rtt, ecn, 1, "transport.conn", idx, 2000)
+    path = os.path.join(GOLDEN, "rng.npz")
+    np.savez_compressed(path, **out)
+    print(f"rng: {len(out)} arrays -> {os.path.getsize(path)} B")
+
+
+def main(argv):
+    os.makedirs(GOLDEN, exist_ok=True)
+    names = argv or list(SCENARIOS) + ["rng"]
+    for n in names:
+        if n == "rng":
+            gen_rng()
+            continue
+        kw, flows = SCENARIOS[n]
+        gen(n, kw, flows)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

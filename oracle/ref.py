@@ -1,0 +1,191 @@
+"""ctypes wrapper of oracle/_ref/libcnref.so -- TEST INFRASTRUCTURE ONLY.
+
+libcnref.so is the UNMODIFIED reference chunknet library compiled from
+/root/reference/proj/src by oracle/Makefile, plus oracle/ref_harness.cpp.
+Only tests/, __graft_entry__.smoke() and bench.py's cpu-baseline /
+--impl reference legs may import this module.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+from .records import ACK_DTYPE, CPL_DTYPE, PKT_DTYPE
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libcnref.so")
+
+LB = {"oblivious": 0, "p2_rtt": 1, "p2_ecn": 2}
+CC = {"none": 0, "cubic": 1, "swift": 2}
+
+
+class Scenario(ctypes.Structure):
+    _fields_ = [
+        ("topo_kind", ctypes.c_int32), ("topo_arg", ctypes.c_int32),
+        ("rate_bps", ctypes.c_double), ("link_delay_ns", ctypes.c_int64),
+        ("qcap_bytes", ctypes.c_int64), ("loss", ctypes.c_double),
+        ("seed", ctypes.c_uint64), ("chunk_bytes", ctypes.c_uint32),
+        ("paths", ctypes.c_int32), ("lb", ctypes.c_int32), ("cc", ctypes.c_int32),
+        ("cc_scope", ctypes.c_int32), ("engines", ctypes.c_int32),
+        ("conn_split", ctypes.c_int32), ("dupack_threshold", ctypes.c_int32),
+        ("rto_min", ctypes.c_int64), ("n_flows", ctypes.c_int32),
+        ("window", ctypes.c_int32), ("cutoff_ns", ctypes.c_int64),
+    ]
+
+
+class Flow(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_int32), ("dst", ctypes.c_int32),
+                ("len", ctypes.c_uint64), ("count", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+class RecordStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "data_pkts", "acks_at_sender", "completions", "chunks_sent", "chunk_rtx",
+        "fast_rtx", "rtos", "acks_sent", "loss_dropped")] + [
+        ("end_time", ctypes.c_int64), ("quiesced", ctypes.c_int32),
+        ("n_hosts", ctypes.c_int32), ("bytes_ok", ctypes.c_uint64)]
+
+
+class RxOut(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "n_acks", "n_completions", "arena_used", "acks_sent_stat")]
+
+
+_lib = None
+
+
+def available():
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"{LIB_PATH} missing: run `make -C oracle ref` "
+                               "where /root/reference is mounted")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u64, i64, i32, u32 = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64,
+                                  ctypes.c_int, ctypes.c_uint32)
+        L.cnref_last_error.restype = ctypes.c_char_p
+        L.cnref_record.argtypes = [ctypes.POINTER(Scenario), ctypes.POINTER(Flow),
+                                   ctypes.c_char_p, ctypes.POINTER(RecordStats)]
+        L.cnref_rx_replay.argtypes = [vp, u64, i32, u32, i32, vp, u64, vp, u64, vp,
+                                      u64, ctypes.POINTER(RxOut)]
+        L.cnref_rx_replay_bench.argtypes = [vp, u64, i32, u32, i32, i32]
+        L.cnref_rx_replay_bench.restype = ctypes.c_double
+        L.cnref_rng_u64.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
+        L.cnref_next_below.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]
+        L.cnref_next_double.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
+        L.cnref_select_paths.argtypes = [i32, i32, vp, vp, u64, ctypes.c_char_p, i64,
+                                         u64, vp]
+        L.cnref_select_paths_bench.argtypes = [i32, i32, i32, u64, i32, vp]
+        L.cnref_select_paths_bench.restype = ctypes.c_double
+        L.cnref_encode_header.argtypes = [ctypes.c_uint8] * 3 + [i32, ctypes.c_uint8,
+                                                                 ctypes.POINTER(u32)]
+        L.cnref_csn_before.argtypes = [ctypes.c_uint8] * 3 + [i32, ctypes.POINTER(i32)]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
+           link_delay_ns=1000, qcap_bytes=1 << 20, loss=0.0, seed=1,
+           chunk_bytes=32768, paths=8, lb="p2_rtt", cc="cubic", cc_scope=0,
+           engines=1, conn_split=0, dupack_threshold=8, rto_min=0, flows=(),
+           window=1, cutoff_ns=60_000_000_000):
+    """Runs the reference DES and writes data.bin / acks_des.bin /
+    completions_des.bin into outdir.  flows: [(src, dst, len, count)]."""
+    sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns,
+                  qcap_bytes, loss, seed, chunk_bytes, paths, LB[lb], CC[cc],
+                  cc_scope, engines, conn_split, dupack_threshold, rto_min,
+                  len(flows), window, cutoff_ns)
+    fl = (Flow * max(1, len(flows)))(*[Flow(s, d, l, c, 0) for (s, d, l, c) in flows])
+    st = RecordStats()
+    os.makedirs(outdir, exist_ok=True)
+    rc = lib().cnref_record(ctypes.byref(sc), fl, outdir.encode(), ctypes.byref(st))
+    if rc != 0:
+        raise RuntimeError(lib().cnref_last_error().decode())
+    data = np.fromfile(os.path.join(outdir, "data.bin"), dtype=PKT_DTYPE)
+    acks = np.fromfile(os.path.join(outdir, "acks_des.bin"), dtype=ACK_DTYPE)
+    cpls = np.fromfile(os.path.join(outdir, "completions_des.bin"), dtype=CPL_DTYPE)
+    return data, acks, cpls, {k: getattr(st, k) for k, _ in RecordStats._fields_}
+
+
+def rx_replay(recs, n_hosts, chunk_bytes, carry_payload=True, arena_bytes=None):
+    """Reference receive path over recorded packets -> (acks, completions, arena)."""
+    recs = np.ascontiguousarray(recs, dtype=PKT_DTYPE)
+    n = len(recs)
+    max_acks = n + 16
+    acks = np.zeros(max_acks, dtype=ACK_DTYPE)
+    cpls = np.zeros(n + 16, dtype=CPL_DTYPE)
+    if arena_bytes is None:
+        lens = {}
+        for t, l in zip(recs["msg_tag"], recs["msg_len"]):
+            lens[(int(t), int(l))] = int(l)
+        arena_bytes = sum(((l + 15) // 16) * 16 for l in lens.values()) * 2 + 64
+    arena = np.zeros(arena_bytes if carry_payload else 1, dtype=np.uint8)
+    out = RxOut()
+    rc = lib().cnref_rx_replay(_ptr(recs), n, n_hosts, chunk_bytes,
+                               1 if carry_payload else 0, _ptr(acks), max_acks,
+                               _ptr(cpls), len(cpls), _ptr(arena),
+                               arena.nbytes if carry_payload else 0, ctypes.byref(out))
+    if rc != 0:
+        raise RuntimeError(lib().cnref_last_error().decode())
+    return acks[: out.n_acks].copy(), cpls[: out.n_completions].copy(), arena[: out.arena_used]
+
+
+def rx_replay_bench(recs, n_hosts, chunk_bytes, threads=1, reps=1):
+    recs = np.ascontiguousarray(recs, dtype=PKT_DTYPE)
+    return lib().cnref_rx_replay_bench(_ptr(recs), len(recs), n_hosts, chunk_bytes,
+                                       threads, reps)
+
+
+def rng_u64(seed, name, index, count):
+    out = np.zeros(count, dtype=np.uint64)
+    lib().cnref_rng_u64(seed, name.encode(), index, count, _ptr(out))
+    return out
+
+
+def next_below(seed, name, index, ns):
+    ns = np.ascontiguousarray(ns, dtype=np.uint64)
+    out = np.zeros(len(ns), dtype=np.uint64)
+    lib().cnref_next_below(seed, name.encode(), index, _ptr(ns), len(ns), _ptr(out))
+    return out
+
+
+def next_double(seed, name, index, count):
+    out = np.zeros(count, dtype=np.float64)
+    lib().cnref_next_double(seed, name.encode(), index, count, _ptr(out))
+    return out
+
+
+def select_paths(policy, rtt, ecn, seed, name, index, count):
+    rtt = np.ascontiguousarray(rtt, dtype=np.float64)
+    ecn = np.ascontiguousarray(ecn, dtype=np.float64)
+    out = np.zeros(count, dtype=np.int32)
+    lib().cnref_select_paths(LB[policy], len(rtt), _ptr(rtt), _ptr(ecn), seed,
+                             name.encode(), index, count, _ptr(out))
+    return out
+
+
+def select_paths_bench(policy, n_paths, conns, count, threads=1):
+    cs = np.zeros(1, dtype=np.uint64)
+    t = lib().cnref_select_paths_bench(LB[policy], n_paths, conns, count, threads, _ptr(cs))
+    return t, int(cs[0])
+
+
+def encode_header(conn, msg, csn, last, rsvd):
+    out = ctypes.c_uint32()
+    rc = lib().cnref_encode_header(conn, msg, csn, int(last), rsvd, ctypes.byref(out))
+    return rc, out.value
+
+
+def csn_before(a, b, base, width):
+    out = ctypes.c_int()
+    rc = lib().cnref_csn_before(a, b, base, width, ctypes.byref(out))
+    return rc, out.value

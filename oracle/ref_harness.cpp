@@ -1,0 +1,547 @@
+// ref_harness.cpp -- TEST INFRASTRUCTURE ONLY (oracle side, never shipped).
+//
+// Drives the UNMODIFIED reference chunknet library (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/) to
+//   * record packet traces from its discrete-event simulator (DES),
+//   * replay delivered data packets into a fresh Transport's receive path
+//     (Transport::handle_packet, src/transport.cpp:565) and capture the ack
+//     stream in emission order,
+//   * time that receive path on the host's cores (bench.py cpu baseline),
+//   * emit RngStream / select_path draw sequences (rng.hpp:29-60, lb.cpp:7-27),
+//   * replay timed acks into a sender (handle_ack, transport.cpp:849-942).
+// Private members are reached by compiling THIS translation unit with
+// `private` defined as `public`; the library objects are compiled normally,
+// access specifiers do not change layout.
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#define private public
+#include "chunknet/event_queue.hpp"
+#include "chunknet/lb.hpp"
+#include "chunknet/network.hpp"
+#include "chunknet/packet.hpp"
+#include "chunknet/rng.hpp"
+#include "chunknet/topology.hpp"
+#include "chunknet/transport.hpp"
+#include "chunknet/wire.hpp"
+#undef private
+
+#include "chunknet_b200.h"
+
+using namespace chunknet;
+
+namespace {
+
+thread_local std::string g_err;
+
+// Payload generator of the reference tests (test_transport.cpp:63-71).
+std::shared_ptr<std::vector<uint8_t>> pattern(uint64_t n, uint64_t seed) {
+    auto v = std::make_shared<std::vector<uint8_t>>(n);
+    uint64_t x = seed;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (i % 8 == 0) x = splitmix64(x + i);
+        (*v)[i] = static_cast<uint8_t>(x >> ((i % 8) * 8));
+    }
+    return v;
+}
+
+cn_pkt_hdr to_rec(const Packet& p) {
+    cn_pkt_hdr r;
+    std::memset(&r, 0, sizeof r);
+    r.src = p.src;
+    r.dst = p.dst;
+    r.path_id = p.path_id;
+    r.hdr = encode_header(p.hdr);
+    r.chunk_offset = p.chunk_offset;
+    r.chunk_len = p.chunk_len;
+    r.payload_len = static_cast<uint16_t>(p.payload_len);
+    r.seq_in_chunk = static_cast<uint8_t>(p.seq_in_chunk);
+    r.flags = (p.is_rtx ? CN_PKT_RTX : 0) | (p.ecn ? CN_PKT_ECN : 0) |
+              (p.trimmed ? CN_PKT_TRIMMED : 0);
+    r.tx_time = p.tx_time;
+    r.msg_seq = p.msg_seq;
+    r.msg_tag = p.msg_tag;
+    r.msg_len = p.msg_len;
+    return r;
+}
+
+Packet from_rec(const cn_pkt_hdr& r) {
+    Packet p;
+    p.kind = PacketKind::data;
+    p.src = r.src;
+    p.dst = r.dst;
+    p.path_id = r.path_id;
+    p.hdr = decode_header(r.hdr);
+    p.chunk_offset = r.chunk_offset;
+    p.chunk_len = r.chunk_len;
+    p.payload_len = r.payload_len;
+    p.seq_in_chunk = r.seq_in_chunk;
+    p.is_rtx = r.flags & CN_PKT_RTX;
+    p.ecn = r.flags & CN_PKT_ECN;
+    p.trimmed = r.flags & CN_PKT_TRIMMED;
+    p.tx_time = r.tx_time;
+    p.msg_seq = r.msg_seq;
+    p.msg_tag = r.msg_tag;
+    p.msg_len = r.msg_len;
+    return p;
+}
+
+cn_ack_rec ack_rec(const Packet& p, uint32_t idx, int64_t aux) {
+    cn_ack_rec a;
+    std::memset(&a, 0, sizeof a);
+    a.src = p.src;
+    a.dst = p.dst;
+    a.hdr = encode_header(p.hdr);
+    a.echo_path_id = p.echo_path_id;
+    a.cum_csn = p.cum_csn;
+    a.flags = (p.cum_valid ? CN_ACK_CUM_VALID : 0) |
+              (p.ecn_echo ? CN_ACK_ECN_ECHO : 0);
+    a.pkt_index = idx;
+    a.msg_seq = p.msg_seq;
+    a.sack[0] = p.sack[0];
+    a.sack[1] = p.sack[1];
+    a.echo_tx_time = p.echo_tx_time;
+    a.aux = aux;
+    return a;
+}
+
+Packet from_ack(const cn_ack_rec& a) {
+    Packet p;
+    p.kind = PacketKind::ack;
+    p.src = a.src;
+    p.dst = a.dst;
+    p.hdr = decode_header(a.hdr);
+    p.echo_path_id = a.echo_path_id;
+    p.cum_csn = a.cum_csn;
+    p.cum_valid = a.flags & CN_ACK_CUM_VALID;
+    p.ecn_echo = a.flags & CN_ACK_ECN_ECHO;
+    p.msg_seq = a.msg_seq;
+    p.sack[0] = a.sack[0];
+    p.sack[1] = a.sack[1];
+    p.echo_tx_time = a.echo_tx_time;
+    return p;
+}
+
+template <class T>
+bool write_vec(const std::string& path, const std::vector<T>& v) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) return false;
+    if (!v.empty()) std::fwrite(v.data(), sizeof(T), v.size(), f);
+    std::fclose(f);
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------ DES recorder
+struct cnref_scenario {
+    int32_t topo_kind;   // 0 star, 1 fat tree
+    int32_t topo_arg;    // n hosts (star) or k (fat tree)
+    double rate_bps;
+    int64_t link_delay_ns;
+    int64_t qcap_bytes;
+    double loss;         // at every host egress
+    uint64_t seed;
+    uint32_t chunk_bytes;
+    int32_t paths;
+    int32_t lb;          // LbPolicy
+    int32_t cc;          // CcConfig::Algo
+    int32_t cc_scope;    // CcConfig::Scope
+    int32_t engines;
+    int32_t conn_split;
+    int32_t dupack_threshold;
+    int64_t rto_min;
+    int32_t n_flows;
+    int32_t window;      // messages outstanding per flow
+    int64_t cutoff_ns;
+};
+
+struct cnref_flow {
+    int32_t src, dst;
+    uint64_t len;
+    int32_t count;
+    int32_t pad;
+};
+
+struct cnref_record_stats {
+    uint64_t data_pkts;
+    uint64_t acks_at_sender;
+    uint64_t completions;
+    uint64_t chunks_sent;
+    uint64_t chunk_rtx;
+    uint64_t fast_rtx;
+    uint64_t rtos;
+    uint64_t acks_sent;
+    uint64_t loss_dropped;
+    int64_t end_time;
+    int32_t quiesced;
+    int32_t n_hosts;
+    uint64_t bytes_ok;  // completions whose data matched the source
+};
+
+const char* cnref_last_error() { return g_err.c_str(); }
+
+int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
+                 const char* outdir, cnref_record_stats* st) {
+    try {
+        Topology topo =
+            sc->topo_kind == 0 ? build_star(sc->topo_arg) : build_fat_tree(sc->topo_arg);
+        NetParams np;
+        np.rate_bps = sc->rate_bps;
+        np.link_delay_ns = sc->link_delay_ns;
+        np.qcap_bytes = sc->qcap_bytes;
+        EventQueue eq;
+        Network net(topo, np, eq, sc->seed);
+        if (sc->loss > 0) net.inject_loss_at_host_egress(sc->loss);
+
+        TransportConfig tc;
+        tc.chunk_bytes = sc->chunk_bytes;
+        tc.paths = sc->paths;
+        tc.lb = static_cast<LbPolicy>(sc->lb);
+        tc.cc.algo = static_cast<CcConfig::Algo>(sc->cc);
+        tc.cc.scope = static_cast<CcConfig::Scope>(sc->cc_scope);
+        if (tc.cc.algo == CcConfig::Algo::swift)
+            tc.cc.swift_target_ns = 3 * net.base_rtt_ns();
+        tc.engines = sc->engines;
+        tc.conn_split = sc->conn_split;
+        tc.dupack_threshold = sc->dupack_threshold;
+        tc.rto_min = sc->rto_min;
+        tc.carry_payload = true;
+        Transport tr(net, eq, tc, sc->seed);
+
+        std::vector<cn_pkt_hdr> data;
+        std::vector<cn_ack_rec> acks;
+        std::vector<cn_completion> cpls;
+        net.set_trace([&](const TraceEvent& te) {
+            if (std::strcmp(te.event, "deliver") != 0) return;
+            const Packet& p = *te.pkt;
+            if (p.kind == PacketKind::data)
+                data.push_back(to_rec(p));
+            else if (p.kind == PacketKind::ack)
+                acks.push_back(ack_rec(p, 0, te.t));
+        });
+
+        // tags: flow * 1'000'000 + k ; payload = pattern(len, tag)
+        std::vector<int> next(sc->n_flows, 0);
+        std::map<uint64_t, std::shared_ptr<std::vector<uint8_t>>> srcs;
+        uint64_t ok = 0;
+        std::function<void(int)> submit = [&](int f) {
+            const cnref_flow& fl = flows[f];
+            if (next[f] >= fl.count) return;
+            uint64_t tag = uint64_t(f) * 1000000ull + uint64_t(next[f]);
+            auto buf = pattern(fl.len, tag);
+            if (!tr.send_message_data(fl.src, fl.dst, buf, tag)) return;  // retried on completion
+            srcs[tag] = buf;
+            ++next[f];
+        };
+        tr.set_on_complete([&](uint64_t tag, int src, int dst, uint64_t len,
+                               SimTime t, const std::vector<uint8_t>* d) {
+            cn_completion c;
+            std::memset(&c, 0, sizeof c);
+            c.tag = tag;
+            c.src = src;
+            c.dst = dst;
+            c.len = len;
+            c.reserved = static_cast<uint64_t>(t);
+            cpls.push_back(c);
+            auto it = srcs.find(tag);
+            if (d && it != srcs.end() && *d == *it->second) ++ok;
+            int f = static_cast<int>(tag / 1000000ull);
+            eq.schedule_in(0, [&submit, f] { submit(f); });
+        });
+        for (int f = 0; f < sc->n_flows; ++f)
+            for (int w = 0; w < sc->window; ++w) submit(f);
+        bool q = eq.run_until_idle(sc->cutoff_ns);
+
+        std::string dir(outdir);
+        if (!write_vec(dir + "/data.bin", data) || !write_vec(dir + "/acks_des.bin", acks) ||
+            !write_vec(dir + "/completions_des.bin", cpls))
+            throw std::runtime_error("cannot write to " + dir);
+        if (st) {
+            st->data_pkts = data.size();
+            st->acks_at_sender = acks.size();
+            st->completions = cpls.size();
+            st->chunks_sent = tr.stats().chunks_sent;
+            st->chunk_rtx = tr.stats().chunk_rtx;
+            st->fast_rtx = tr.stats().fast_rtx;
+            st->rtos = tr.stats().rtos;
+            st->acks_sent = tr.stats().acks_sent;
+            st->loss_dropped = net.counters().loss_dropped_pkts;
+            st->end_time = eq.now();
+            st->quiesced = q ? 1 : 0;
+            st->n_hosts = topo.n_hosts;
+            st->bytes_ok = ok;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// -------------------------------------------------------- receive replay
+// Feeds recorded data packets, in order, into Transport::handle_packet of a
+// fresh instance and captures every ack it emits, in emission order, with
+// the index of the packet that caused it.  Completions are captured with
+// their reassembled bytes copied into `arena` (if non-null) at a running
+// offset.
+struct cnref_rx_out {
+    uint64_t n_acks;
+    uint64_t n_completions;
+    uint64_t arena_used;
+    uint64_t acks_sent_stat;
+};
+
+int cnref_rx_replay(const cn_pkt_hdr* recs, uint64_t n, int n_hosts,
+                    uint32_t chunk_bytes, int carry_payload, cn_ack_rec* acks,
+                    uint64_t max_acks, cn_completion* cpls, uint64_t max_cpls,
+                    uint8_t* arena, uint64_t arena_bytes, cnref_rx_out* out) {
+    try {
+        Topology topo = build_star(std::max(2, n_hosts));
+        NetParams np;
+        np.rate_bps = 1e12;
+        np.link_delay_ns = 1;
+        np.qcap_bytes = int64_t{1} << 40;
+        EventQueue eq;
+        Network net(topo, np, eq, 1);
+        TransportConfig tc;
+        tc.chunk_bytes = chunk_bytes;
+        tc.carry_payload = carry_payload != 0;
+        Transport tr(net, eq, tc, 1);
+
+        uint64_t na = 0, nc = 0, used = 0;
+        uint64_t cur = 0;
+        net.set_trace([&](const TraceEvent& te) {
+            if (std::strcmp(te.event, "deliver") != 0) return;
+            if (te.pkt->kind != PacketKind::ack) return;
+            if (na < max_acks) acks[na] = ack_rec(*te.pkt, static_cast<uint32_t>(cur), 0);
+            ++na;
+        });
+        std::unordered_map<uint64_t, std::shared_ptr<std::vector<uint8_t>>> srcs;
+        tr.set_on_complete([&](uint64_t tag, int src, int dst, uint64_t len,
+                               SimTime, const std::vector<uint8_t>* d) {
+            if (nc < max_cpls) {
+                cn_completion& c = cpls[nc];
+                std::memset(&c, 0, sizeof c);
+                c.tag = tag;
+                c.src = src;
+                c.dst = dst;
+                c.len = len;
+                c.pkt_index = static_cast<uint32_t>(cur);
+                c.buf_offset = ~uint64_t{0};
+                if (d && arena && used + d->size() <= arena_bytes) {
+                    std::memcpy(arena + used, d->data(), d->size());
+                    c.buf_offset = used;
+                    used += (d->size() + 15) & ~uint64_t{15};
+                }
+            }
+            ++nc;
+        });
+        for (uint64_t i = 0; i < n; ++i) {
+            Packet p = from_rec(recs[i]);
+            if (carry_payload) {
+                auto& s = srcs[p.msg_tag ^ (p.msg_len << 40)];
+                if (!s) s = pattern(p.msg_len, p.msg_tag);
+                p.msg_data = s;
+            }
+            cur = i;
+            // msg_seq recorded per completion through the MsgRecv before reset
+            tr.handle_packet(p.dst, std::move(p));
+            eq.run_until_idle(std::numeric_limits<SimTime>::max() / 2);
+        }
+        if (out) {
+            out->n_acks = na;
+            out->n_completions = nc;
+            out->arena_used = used;
+            out->acks_sent_stat = tr.stats().acks_sent;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// Times the reference receive path: T threads, each owning one Transport
+// (constructed outside the timer) and its own source buffers, replay the
+// same recorded packet sequence `reps` times.  Acks go into the reference's
+// own Network::inject (part of the measured path, as in the survey probe);
+// the event queue is drained outside the timer.  Returns wall seconds of
+// the slowest thread's timed region.
+double cnref_rx_replay_bench(const cn_pkt_hdr* recs, uint64_t n, int n_hosts,
+                             uint32_t chunk_bytes, int threads, int reps) {
+    std::vector<double> secs(threads, 0.0);
+    std::atomic<int> ready{0};
+    std::atomic<bool> go{false};
+    auto work = [&](int t) {
+        Topology topo = build_star(std::max(2, n_hosts));
+        NetParams np;
+        np.rate_bps = 1e12;
+        np.link_delay_ns = 1;
+        np.qcap_bytes = int64_t{1} << 40;
+        std::unordered_map<uint64_t, std::shared_ptr<std::vector<uint8_t>>> srcs;
+        for (uint64_t i = 0; i < n; ++i) {
+            auto& s = srcs[recs[i].msg_tag ^ (recs[i].msg_len << 40)];
+            if (!s) s = pattern(recs[i].msg_len, recs[i].msg_tag);
+        }
+        std::vector<Packet> pk;
+        pk.reserve(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            Packet p = from_rec(recs[i]);
+            p.msg_data = srcs[recs[i].msg_tag ^ (recs[i].msg_len << 40)];
+            pk.push_back(std::move(p));
+        }
+        ready.fetch_add(1);
+        while (!go.load()) std::this_thread::yield();
+        double total = 0;
+        for (int r = 0; r < reps; ++r) {
+            EventQueue eq;
+            Network net(topo, np, eq, 1);
+            TransportConfig tc;
+            tc.chunk_bytes = chunk_bytes;
+            tc.carry_payload = true;
+            Transport tr(net, eq, tc, 1);
+            uint64_t sink = 0;
+            tr.set_on_complete([&](uint64_t, int, int, uint64_t len, SimTime,
+                                   const std::vector<uint8_t>* d) {
+                sink += len + (d ? (*d)[len / 2] : 0);
+            });
+            std::vector<Packet> batch = pk;  // copy outside the timer
+            auto t0 = std::chrono::steady_clock::now();
+            for (uint64_t i = 0; i < n; ++i) {
+                int dst = batch[i].dst;
+                tr.handle_packet(dst, std::move(batch[i]));
+            }
+            auto t1 = std::chrono::steady_clock::now();
+            total += std::chrono::duration<double>(t1 - t0).count();
+            eq.run_until_idle(std::numeric_limits<SimTime>::max() / 2);
+            if (sink == 0xdeadbeef) std::fprintf(stderr, "!");
+        }
+        secs[t] = total;
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < threads; ++t) th.emplace_back(work, t);
+    while (ready.load() < threads) std::this_thread::yield();
+    go.store(true);
+    for (auto& x : th) x.join();
+    return *std::max_element(secs.begin(), secs.end());
+}
+
+// ------------------------------------------------------------- RNG draws
+void cnref_rng_u64(uint64_t seed, const char* name, int64_t index, uint64_t count,
+                   uint64_t* out) {
+    RngStream r = index < 0 ? RngStream(seed, name)
+                            : RngStream(seed, name, static_cast<uint64_t>(index));
+    for (uint64_t i = 0; i < count; ++i) out[i] = r.next_u64();
+}
+
+void cnref_next_below(uint64_t seed, const char* name, int64_t index,
+                      const uint64_t* ns, uint64_t count, uint64_t* out) {
+    RngStream r = index < 0 ? RngStream(seed, name)
+                            : RngStream(seed, name, static_cast<uint64_t>(index));
+    for (uint64_t i = 0; i < count; ++i) out[i] = r.next_below(ns[i]);
+}
+
+void cnref_next_double(uint64_t seed, const char* name, int64_t index,
+                       uint64_t count, double* out) {
+    RngStream r = index < 0 ? RngStream(seed, name)
+                            : RngStream(seed, name, static_cast<uint64_t>(index));
+    for (uint64_t i = 0; i < count; ++i) out[i] = r.next_double();
+}
+
+// select_path sequence on a fixed scoreboard (rtt/ecn scores given).
+int cnref_select_paths(int policy, int n_paths, const double* rtt,
+                       const double* ecn, uint64_t seed, const char* name,
+                       int64_t index, uint64_t count, int32_t* out) {
+    PathScoreboard b(n_paths, 0);
+    for (int p = 0; p < n_paths; ++p) {
+        b.rtt_[p] = rtt ? rtt[p] : 0.0;
+        b.ecn_[p] = ecn ? ecn[p] : 0.0;
+    }
+    RngStream r = index < 0 ? RngStream(seed, name)
+                            : RngStream(seed, name, static_cast<uint64_t>(index));
+    for (uint64_t i = 0; i < count; ++i)
+        out[i] = select_path(static_cast<LbPolicy>(policy), b, r);
+    return 0;
+}
+
+// Times select_path: `conns` connections each with its own stream and
+// board; `count` decisions per connection, round robin.  Returns seconds.
+double cnref_select_paths_bench(int policy, int n_paths, int conns,
+                                uint64_t count, int threads, uint64_t* checksum) {
+    std::vector<double> secs(threads, 0.0);
+    std::vector<uint64_t> sums(threads, 0);
+    auto work = [&](int t) {
+        int lo = conns * t / threads, hi = conns * (t + 1) / threads;
+        std::vector<PathScoreboard> boards;
+        std::vector<RngStream> rngs;
+        for (int c = lo; c < hi; ++c) {
+            boards.emplace_back(n_paths, 10000);
+            RngStream init(77, "board", c);
+            for (int p = 0; p < n_paths; ++p)
+                boards.back().rtt_[p] = 10000.0 + double(init.next_below(5000));
+            rngs.emplace_back(1, "transport.conn", c);
+        }
+        uint64_t s = 0;
+        auto t0 = std::chrono::steady_clock::now();
+        for (uint64_t k = 0; k < count; ++k)
+            for (int c = 0; c < hi - lo; ++c)
+                s += select_path(static_cast<LbPolicy>(policy), boards[c], rngs[c]);
+        auto t1 = std::chrono::steady_clock::now();
+        secs[t] = std::chrono::duration<double>(t1 - t0).count();
+        sums[t] = s;
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < threads; ++t) th.emplace_back(work, t);
+    for (auto& x : th) x.join();
+    uint64_t s = 0;
+    for (auto v : sums) s += v;
+    if (checksum) *checksum = s;
+    return *std::max_element(secs.begin(), secs.end());
+}
+
+// ------------------------------------------------------------ wire codec
+int cnref_encode_header(uint8_t conn, uint8_t msg, uint8_t csn, int last,
+                        uint8_t rsvd, uint32_t* out) {
+    try {
+        *out = encode_header({conn, msg, csn, last != 0, rsvd});
+        return 0;
+    } catch (const FieldRangeError& e) {
+        g_err = e.what();
+        return CN_E_FIELD_RANGE;
+    }
+}
+
+int cnref_csn_before(uint8_t a, uint8_t b, uint8_t base, int width, int* out) {
+    try {
+        SeqWindow w(base, width);
+        *out = csn_before(a, b, w) ? 1 : 0;
+        return 0;
+    } catch (const OutOfWindowError& e) {
+        g_err = e.what();
+        return CN_E_OUT_OF_WINDOW;
+    } catch (const FieldRangeError& e) {
+        g_err = e.what();
+        return CN_E_FIELD_RANGE;
+    }
+}
+
+}  // extern "C"

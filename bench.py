@@ -1,0 +1,362 @@
+"""bench.py -- reassembly + ACK bookkeeping throughput of the B200 receive path.
+
+Workload (BASELINE.json configs[1], "cfg2"): one 64 MiB message sprayed over
+256 paths with 1% random drop and heavy reordering, as recorded from the
+reference discrete-event simulator (tests/golden/cfg2_32k.npz: k=32 fat
+tree 0 -> 8191, 32 KiB chunks, seed 1; 19,997 delivered data packets incl.
+retransmissions, 2,885 acks).  One step = the device receive path over the
+whole trace: reset receive state, classify, mark, scan, decide, scatter-copy
+payloads into the message buffer, emit the ordered ack stream, finalize.
+
+N > 1 GPUs: every rank runs its own replica (the transport shards by
+connection; no data-path collective) -> weak scaling; the
+ring all-reduce of configs[2] is reported beside it.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+MAX_PL = 4032
+HDR = 64
+ACK = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2_32k")
+    ap.add_argument("--replicas", type=int, default=4,
+                    help="rotating staging replicas so that inputs exceed L2")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_trace(name):
+    z = np.load(os.path.join(ROOT, "tests", "golden", f"{name}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    return z["data"], meta, len(z["acks"])
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [int(s[0]) for s in self.samples if s[0].isdigit()]
+        mx = [int(s[1]) for s in self.samples if s[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[2 + k].lower() == "active"})
+        return {"sm_mhz": int(statistics.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_reference(data, n_hosts, chunk_bytes, seconds, threads=None):
+    """The reference's own receive path (oracle/_ref: the unmodified chunknet
+    library, Transport::handle_packet replay) on this host's cores."""
+    from oracle import ref
+    threads = threads or os.cpu_count() or 1
+    msg = int(data["msg_len"][0])
+    if ref.available():
+        t1 = ref.rx_replay_bench(data, n_hosts, chunk_bytes, threads, 1)
+        reps = max(1, min(200, int(seconds / max(t1, 1e-3))))
+        t = ref.rx_replay_bench(data, n_hosts, chunk_bytes, threads, reps)
+        gbs = threads * reps * msg / t / 1e9
+        return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                "sample": f"{threads} threads x {reps} replays of the {len(data)}-packet "
+                          f"trace (each thread its own Transport + source buffer), "
+                          f"{t:.2f} s", "mpkts_per_s": round(threads * reps * len(data) / t / 1e6, 3)}
+    from oracle import oracle as O
+    staging = O.fill_staging(data)
+    rx = O.OracleRx()
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < seconds / 4 or reps == 0:
+        rx = O.OracleRx()
+        rx.batch(data, staging)
+        reps += 1
+    t = time.perf_counter() - t0
+    return {"value": round(reps * msg / t / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"{reps} single-thread oracle replays, {t:.2f} s",
+            "mpkts_per_s": round(reps * len(data) / t / 1e6, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    data, meta, n_acks = load_trace(args.workload)
+    from oracle import ref
+    threads = os.cpu_count() or 1
+    msg = int(data["msg_len"][0])
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    for _ in range(args.warmup):
+        ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
+    times = [ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
+             for _ in range(args.steps)]
+    t = sum(times)
+    v = threads * args.steps * msg / t / 1e9
+    line = {
+        "metric": "reassembly_GBps", "value": round(v, 3), "unit": "GB/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "reference DES trace",
+        "config": {"workload": f"{args.workload}: 64 MiB message, 256 paths, 1% drop "
+                               f"(BASELINE configs[1]); {threads} threads each replay it"},
+        "mpkts_per_s": round(threads * args.steps * len(data) / t / 1e6, 3),
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{threads} threads x 1 replay per step"},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_17307_b200 as cn
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    data, meta, _ = load_trace(args.workload)
+    n = len(data)
+    msg_len = int(data["msg_len"][0])
+    cb = meta["chunk_bytes"]
+
+    hdrs = cn.to_device_records(data, dev)
+    # synthetic payload: random message bytes on device, gathered into the
+    # arrival-order staging slots (packet i at i*4032) -- setup, untimed
+    off = torch.from_numpy((data["chunk_offset"] + data["seq_in_chunk"].astype(np.uint64) * MAX_PL)
+                           .astype(np.int64)).to(dev)
+    pl = torch.from_numpy(data["payload_len"].astype(np.int64)).to(dev)
+    R = max(1, args.replicas)
+    srcs, stagings = [], []
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    col = torch.arange(MAX_PL, device=dev)
+    for r in range(R):
+        src = torch.randint(0, 256, (msg_len,), dtype=torch.uint8, device=dev, generator=g)
+        st = torch.zeros(n * MAX_PL, dtype=torch.uint8, device=dev)
+        for a in range(0, n, 2048):
+            b = min(n, a + 2048)
+            pos = off[a:b, None] + col[None, :]
+            mask = col[None, :] < pl[a:b, None]
+            vals = src[pos.clamp(max=msg_len - 1)]
+            st.view(n, MAX_PL)[a:b] = torch.where(mask, vals, torch.zeros_like(vals))
+        srcs.append(src)
+        stagings.append(st)
+
+    tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
+                      arena_bytes=msg_len + (1 << 20), chunk_pool=4 * ((msg_len + cb - 1) // cb),
+                      max_batch=n, max_conns=64, max_msgs=64)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k):
+        tr.reset(stream)
+        tr.rx_batch_async(hdrs, stagings[k % R], MAX_PL, stream)
+
+    # correctness gate before timing: ack count + reassembled bytes
+    tr.reset(stream)
+    out = tr.handle_packets(hdrs, stagings[0], MAX_PL, stream)
+    arena = tr.arena()
+    c0 = out.completions_np()[0]
+    assert torch.equal(arena[int(c0["buf_offset"]): int(c0["buf_offset"]) + msg_len], srcs[0]), \
+        "reassembled message != source"
+    n_acks = int(out.result.n_acks)
+    bytes_copied = int(out.result.bytes_copied)
+    assert bytes_copied == msg_len
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tr.set_profiling(True)
+    tr.kernel_profile(reset=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            step(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+    tr.set_profiling(False)
+    prof, nb = tr.kernel_profile(reset=True)
+    launches = tr.last_launches() + 2  # + reset kernels
+    # last step's buffer must equal its source (the work was really done)
+    last = (args.steps - 1) % R
+    assert torch.equal(tr.arena()[int(c0["buf_offset"]): int(c0["buf_offset"]) + msg_len],
+                       srcs[last])
+
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * msg_len * args.steps / (ms_max * 1e-3) / 1e9
+    mpkts = world * n * args.steps / (ms_max * 1e-3) / 1e6
+
+    # roofline of the dominant kernel (k_work: payload scatter + acks)
+    peak, peak_kind = peaks()
+    work_ms = prof["work"] / max(nb, 1)
+    algo_work = 2 * bytes_copied + HDR * n + ACK * n_acks
+    achieved = algo_work / (work_ms * 1e-3) / 1e9
+    algo_step = algo_work + 6 * 4 * n + HDR * n * 3  # + per-packet scratch + header re-reads
+    step_gbs = algo_work / (ms_step * 1e-3) / 1e9
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_hdr = hdrs.cpu().pin_memory()
+        h_st = [s.cpu().pin_memory() for s in stagings[:2]]
+        d_hdr = torch.empty_like(hdrs)
+        d_st = torch.empty_like(stagings[0])
+        h_acks = torch.empty((n_acks + 16) * ACK, dtype=torch.uint8).pin_memory()
+        h_res = torch.empty(24, dtype=torch.uint8).pin_memory()
+
+        def e2e_step(k):
+            d_hdr.copy_(h_hdr, non_blocking=True)
+            d_st.copy_(h_st[k % 2], non_blocking=True)
+            tr.reset(stream)
+            tr.rx_batch_async(d_hdr, d_st, MAX_PL, stream)
+            h_acks[: n_acks * ACK].copy_(tr._acks[: n_acks * ACK], non_blocking=True)
+            h_res.copy_(tr._result, non_blocking=True)
+
+        for k in range(args.warmup):
+            e2e_step(k)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for k in range(args.steps):
+            e2e_step(k)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * msg_len * args.steps / (float(te.item()) * 1e-3) / 1e9, 3),
+               "unit": "GB/s", "h2d_bytes_per_step": int(hdrs.numel() + stagings[0].numel()),
+               "d2h_bytes_per_step": int(n_acks * ACK + 24),
+               "path": "pinned host records+staging -> cn_rx_batch (C ABI) -> acks to host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference(data, meta["n_hosts"], cb, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "reassembly_GBps", "value": round(value, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "reference DES trace + random payload",
+            "config": {"workload": f"{args.workload}: BASELINE configs[1], 64 MiB message, "
+                                   f"256 paths, 1% drop; {n} pkts, {n_acks} acks, chunk {cb} B",
+                       "l2": f"inputs larger than L2: {R} rotating staging replicas "
+                             f"({R * n * MAX_PL / 1e6:.0f} MB) + 64 MiB output per step",
+                       "parallelism": f"replicas x{world} (shard by connection)"},
+            "mpkts_per_s": round(mpkts, 3),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "k_work (payload scatter + ack snapshots)",
+                         "algorithmic_bytes_per_launch": algo_work,
+                         "kernel_ms": round(work_ms, 5), "peak_kind": peak_kind,
+                         "step_frac": round(step_gbs / peak, 4)},
+            "kernel_ms_per_step": {k: round(v / max(nb, 1), 5) for k, v in prof.items()},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -188,6 +188,12 @@ int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
 void* cn_rx_arena(cn_rx* rx);
 /* Number of kernel launches the last cn_rx_batch issued. */
 int cn_rx_last_launches(const cn_rx* rx);
+/* Optional per-kernel CUDA-event timing of cn_rx_batch (bench/profiling). */
+int cn_rx_set_profiling(cn_rx* rx, int enable);
+/* Synchronises profiled batches; ms[k] = accumulated milliseconds of
+ * kernel k (names from cn_rx_kernel_name); returns the kernel count. */
+int cn_rx_profile(cn_rx* rx, double* ms, int max, uint64_t* batches, int reset);
+const char* cn_rx_kernel_name(int k);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,92 @@
+"""Loads the in-tree C-ABI library libchunknet_b200.so (include/chunknet_b200.h).
+
+There is no fallback: if the library is missing or cannot load, every
+entry point raises.  Build it with `python -c "import __graft_entry__ as g;
+g.build()"` or `make -C paper_2504_17307_b200/csrc`.
+"""
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libchunknet_b200.so")
+
+CN_OK = 0
+STATUS_NAMES = {-1: "CN_E_INVALID", -2: "CN_E_LOGIC", -3: "CN_E_FIELD_RANGE",
+                -4: "CN_E_OUT_OF_WINDOW", -5: "CN_E_CUDA", -6: "CN_E_UNSUPPORTED",
+                -7: "CN_E_CAPACITY"}
+
+
+class ChunknetError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ControlHeader(ctypes.Structure):
+    _fields_ = [("conn_id", ctypes.c_uint8), ("msg_id", ctypes.c_uint8),
+                ("csn", ctypes.c_uint8), ("last_chunk", ctypes.c_uint8),
+                ("reserved", ctypes.c_uint8)]
+
+
+class RxConfig(ctypes.Structure):
+    _fields_ = [("chunk_bytes", ctypes.c_uint32), ("max_payload", ctypes.c_uint32),
+                ("max_conns", ctypes.c_uint32), ("max_msgs", ctypes.c_uint32),
+                ("chunk_pool", ctypes.c_uint64), ("arena_bytes", ctypes.c_uint64),
+                ("max_batch", ctypes.c_uint32), ("carry_payload", ctypes.c_int32)]
+
+
+class RxResult(ctypes.Structure):
+    _fields_ = [("n_acks", ctypes.c_uint32), ("n_completions", ctypes.c_uint32),
+                ("status", ctypes.c_uint32), ("n_copied", ctypes.c_uint32),
+                ("bytes_copied", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ChunknetError(-5, f"{LIB_PATH} not built (no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+    L.cn_last_error.restype = ctypes.c_char_p
+    L.cn_version.restype = ctypes.c_char_p
+    L.cn_encode_header.argtypes = [ctypes.POINTER(ControlHeader), ctypes.POINTER(u32)]
+    L.cn_decode_header.argtypes = [u32, ctypes.POINTER(ControlHeader)]
+    L.cn_decode_header.restype = None
+    L.cn_csn_before.argtypes = [ctypes.c_uint8, ctypes.c_uint8, ctypes.c_uint8, i32,
+                                ctypes.POINTER(i32)]
+    L.cn_rx_config_default.argtypes = [ctypes.POINTER(RxConfig)]
+    L.cn_rx_config_default.restype = None
+    L.cn_rx_create.argtypes = [ctypes.POINTER(RxConfig), ctypes.POINTER(vp)]
+    L.cn_rx_destroy.argtypes = [vp]
+    L.cn_rx_destroy.restype = None
+    L.cn_rx_reset.argtypes = [vp, vp]
+    L.cn_rx_batch.argtypes = [vp, vp, vp, u64, u32, vp, u32, vp, u32, vp, vp]
+    L.cn_rx_arena.argtypes = [vp]
+    L.cn_rx_arena.restype = vp
+    L.cn_rx_last_launches.argtypes = [vp]
+    L.cn_rx_set_profiling.argtypes = [vp, i32]
+    L.cn_rx_profile.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32,
+                                ctypes.POINTER(u64), i32]
+    L.cn_rx_kernel_name.restype = ctypes.c_char_p
+    L.cn_rx_kernel_name.argtypes = [i32]
+    _lib = L
+    return L
+
+
+def check(status, what=""):
+    if status != CN_OK:
+        raise ChunknetError(status, f"{what}: {lib().cn_last_error().decode()}")
+    return status
+
+
+def exported_symbols():
+    """Names declared in include/chunknet_b200.h (for the ABI load test)."""
+    import re
+    hdr = os.path.join(os.path.dirname(HERE), "include", "chunknet_b200.h")
+    src = open(hdr).read()
+    return sorted(set(re.findall(r"\b(cn_[a-z0-9_]+)\s*\(", src)))

@@ -1,0 +1,161 @@
+"""Parity of the sm_100a receive path (csrc/rx.cu via the C ABI) with the
+reference receive path (golden ack streams / completions generated from the
+compiled reference, oracle/gen_fixtures.py) and the C oracle."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_names, load_golden
+from oracle import oracle as O
+from oracle.records import ACK_FIELDS, CPL_FIELDS, PKT_DTYPE, ack_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _transport(meta, carry=True, **kw):
+    import paper_2504_17307_b200 as cn
+    cfg = cn.TransportConfig(chunk_bytes=meta["chunk_bytes"], carry_payload=carry)
+    kw.setdefault("arena_bytes", 256 << 20)
+    kw.setdefault("max_batch", 1 << 17)
+    kw.setdefault("chunk_pool", 1 << 20)
+    return cn.Transport(cfg, **kw)
+
+
+def _dev(data, stride=4032):
+    import paper_2504_17307_b200 as cn
+    staging = O.fill_staging(data, stride=stride)
+    return cn.to_device_records(data), torch.from_numpy(staging).cuda()
+
+
+def _check_completions(tr, out, cpls_ref, index_base=0):
+    got = out.completions_np()
+    assert len(got) == len(cpls_ref)
+    for f in ("tag", "src", "dst", "len"):
+        assert (got[f] == cpls_ref[f]).all(), f
+    assert ((got["pkt_index"] + index_base) == cpls_ref["pkt_index"]).all()
+    arena = tr.arena()
+    for c in got:
+        buf = arena[int(c["buf_offset"]): int(c["buf_offset"]) + int(c["len"])].cpu().numpy()
+        assert (buf == O.pattern_bytes(int(c["len"]), int(c["tag"]))).all(), int(c["tag"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_rx_matches_reference(name):
+    data, acks_ref, cpls_ref, meta = load_golden(name)
+    tr = _transport(meta)
+    hd, pl = _dev(data)
+    out = tr.handle_packets(hd, pl)
+    ok, bad = ack_equal(out.acks_np(), acks_ref)
+    assert ok, bad
+    _check_completions(tr, out, cpls_ref)
+    assert tr.stats().acks_sent == meta["des_stats"]["acks_sent"]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "concurrent_k4", "multigen_k8", "k8_4x1m", "csn_wrap"])
+@pytest.mark.parametrize("nsplit", [2, 7, 64])
+def test_rx_batch_split_invariance(name, nsplit):
+    """Persistent device state: any split of the packet sequence into
+    batches yields the identical ack stream and completions."""
+    data, acks_ref, cpls_ref, meta = load_golden(name)
+    tr = _transport(meta)
+    rs = np.random.RandomState(nsplit)
+    cuts = np.unique(np.concatenate([[0, len(data)], rs.randint(0, len(data), nsplit - 1)]))
+    acks, cpls, seen = [], [], []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        hd, pl = _dev(data[a:b])
+        out = tr.handle_packets(hd, pl)
+        ak = out.acks_np().copy()
+        ak["pkt_index"] += np.uint32(a)
+        acks.append(ak)
+        cp = out.completions_np().copy()
+        cp["pkt_index"] += np.uint32(a)
+        cpls.append(cp)
+        arena = tr.arena()
+        for c in out.completions_np():
+            buf = arena[int(c["buf_offset"]): int(c["buf_offset"]) + int(c["len"])].cpu().numpy()
+            assert (buf == O.pattern_bytes(int(c["len"]), int(c["tag"]))).all()
+    ok, bad = ack_equal(np.concatenate(acks), acks_ref)
+    assert ok, bad
+    cp = np.concatenate(cpls)
+    for f in CPL_FIELDS:
+        assert (cp[f] == cpls_ref[f]).all(), f
+
+
+def test_rx_no_payload_mode_same_acks():
+    data, acks_ref, cpls_ref, meta = load_golden("cfg2_32k")
+    tr = _transport(meta, carry=False)
+    import paper_2504_17307_b200 as cn
+    out = tr.handle_packets(cn.to_device_records(data), None)
+    ok, bad = ack_equal(out.acks_np(), acks_ref)
+    assert ok, bad
+    assert out.completions_np()["buf_offset"][0] == np.uint64(2**64 - 1)
+
+
+def test_rx_wide_staging_stride():
+    data, acks_ref, cpls_ref, meta = load_golden("k8_4x1m")
+    tr = _transport(meta)
+    hd, pl = _dev(data, stride=4096)
+    out = tr.handle_packets(hd, pl, stride=4096)
+    ok, bad = ack_equal(out.acks_np(), acks_ref)
+    assert ok, bad
+    _check_completions(tr, out, cpls_ref)
+
+
+def test_rx_selective_ack_contract_forged():
+    """test_transport.cpp:152-203 on the device path."""
+    import paper_2504_17307_b200 as cn
+    h = np.zeros(9, dtype=PKT_DTYPE)
+    for i, c in enumerate(list(range(1, 9)) + [0]):
+        h[i]["src"], h[i]["dst"] = 0, 1
+        h[i]["hdr"] = cn.encode_header(9, 0, c, c == 8)
+        h[i]["chunk_offset"] = c * 4032
+        h[i]["chunk_len"] = 4032
+        h[i]["payload_len"] = 4032
+        h[i]["msg_seq"] = 1
+        h[i]["msg_len"] = 9 * 4032
+    tr = _transport({"chunk_bytes": 4032}, carry=False)
+    out = tr.handle_packets(cn.to_device_records(h), None)
+    a = out.acks_np()
+    assert len(a) == 9
+    for i in range(8):
+        assert not (a[i]["flags"] & 1)
+        assert (a[i]["hdr"] >> 9) & 0xFF == i + 1
+        assert bin(int(a[i]["sack0"])).count("1") + bin(int(a[i]["sack1"])).count("1") == i + 1
+    assert a[8]["flags"] & 1 and a[8]["cum_csn"] == 8 and (a[8]["hdr"] >> 9) & 0xFF == 0
+    assert a[8]["sack0"] == 0 and a[8]["sack1"] == 0
+    assert len(out.completions_np()) == 1
+
+
+def test_rx_reset_and_rerun_identical():
+    data, acks_ref, cpls_ref, meta = load_golden("multipath_k4")
+    tr = _transport(meta)
+    hd, pl = _dev(data)
+    for _ in range(3):
+        tr.reset()
+        out = tr.handle_packets(hd, pl)
+        ok, bad = ack_equal(out.acks_np(), acks_ref)
+        assert ok, bad
+        _check_completions(tr, out, cpls_ref)
+
+
+def test_rx_completion_callback():
+    data, acks_ref, cpls_ref, meta = load_golden("concurrent_k4")
+    tr = _transport(meta)
+    got = []
+    tr.set_on_complete(lambda tag, src, dst, ln, t, d: got.append(
+        (tag, src, dst, ln, t, bytes(d.cpu().numpy()) == bytes(O.pattern_bytes(ln, tag)))))
+    hd, pl = _dev(data)
+    tr.handle_packets(hd, pl)
+    assert [g[:5] for g in got] == [(int(c["tag"]), int(c["src"]), int(c["dst"]), int(c["len"]),
+                                     int(c["pkt_index"])) for c in cpls_ref]
+    assert all(g[5] for g in got)
+
+
+def test_rx_rejects_trimmed_packets_loudly():
+    import paper_2504_17307_b200 as cn
+    data, _, _, meta = load_golden("cfg1")
+    d2 = data.copy()
+    d2["flags"][5] |= 4
+    tr = _transport(meta, carry=False)
+    with pytest.raises(cn.ChunknetError):
+        tr.handle_packets(cn.to_device_records(d2), None)

@@ -9,20 +9,26 @@
 //   Transport::send_ack                   src/transport.cpp:763-792
 //   Transport::maybe_deliver              src/transport.cpp:794-803
 //
-// Batched, data-parallel restatement: every packet i of a
-// batch gets the time t = i+1 (0 = an earlier batch).  For every chunk
+// Batched, data-parallel restatement: packet i of a batch
+// gets the time t = i+1 (0 = an earlier batch).  Per chunk c of a message
 //   first[c][s] = first arrival time of packet s of chunk c   (atomicMin)
 //   cpl[c]      = max_s first[c][s]  (time the chunk completes; INF if not)
 //   pmax[c]     = max(cpl[cum0..c])  (prefix max per message)
-// so that the cumulative cursor after packet i is #{c : pmax[c] <= t(i)}.
-// Each packet's ack (if any) is then an independent snapshot: cum, the
-// 128-bit SACK {cpl[cum+j] <= t}, and the echo of chunk
-// cum + uint8(cause - uint8(cum)).  Ack records are compacted in arrival
-// order with a two-level scan.  The payload scatter (accept_payload) is a
-// warp-cooperative 16-byte vectorised copy of each first-arriving packet.
+// so the cumulative cursor right after packet i is #{c : pmax[c] <= t(i)}.
+// Each packet's ack is then an independent snapshot: cum, the 128-bit SACK
+// {cpl[cum+j] <= t}, and the echo of chunk cum + uint8(cause - uint8(cum)).
 //
-// Kernels per batch: classify -> alloc -> mark -> scan -> decide ->
-// tilescan -> work (copy + ack + completion) -> finalize.
+// Five kernels per batch, all graph-capturable (no host state per batch):
+//   k_ingest   thread/packet: rconn + generation lookup (lock-free hash),
+//              lazy message allocation, stale test, first-arrival marking
+//   k_copy     warp/packet: the payload scatter of first arrivals (HBM-bound)
+//   k_scan     block/message: chunk completion times + prefix max
+//   k_acks     block/32-packet tile: decide, warp-parallel decoupled
+//              look-back for the ordered ack/completion streams, ack
+//              snapshots (SACK by ballot) and completion records
+//   k_finalize block/message: fold batch scratch into persistent chunk
+//              state, advance cum, retire delivered messages; last block
+//              publishes the batch result and arms the next batch.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -30,50 +36,59 @@
 
 #include <new>
 #include <string>
+#include <vector>
 
+#include "bulk.cuh"
 #include "common.cuh"
 
 namespace cnb {
 
 struct GenState {
-    uint64_t len, tag, seq, chunk_base, buf_off, bytes;
-    uint32_t nchunks, cum, n_init, rc, msg_id, epoch, max_touched, deliver_t;
+    uint64_t len, tag, seq, chunk_base, buf_off;
+    unsigned long long touch;  // (epoch << 32) | (max chunk touched + 1) in that epoch
+    uint32_t nchunks, cum, n_init, rc, msg_id, epoch, deliver_t, ready;
+    uint32_t lo_batch, tiles_done, cum_add, pad;
 };
 
 struct RxCtl {
-    unsigned long long pool_top;
-    unsigned long long arena_top;
-    uint32_t n_touched;
-    uint32_t pad;
+    unsigned long long pool_top, arena_top, pool_snap, bytes_copied;
+    uint32_t n_touched, epoch, tile_ticket, fin_done, status, n_copied, n_acks, n_cpls;
+    uint32_t ingest_done, scan_ticket, fin_ticket, n_scan_tiles;
 };
 
 enum : uint32_t { CF_INIT = 1, CF_COMPLETE = 2, CF_ECN = 4, CF_RTX = 8 };
 enum : uint8_t { PC_STALE = 1, PC_ACK = 2, PC_COPY = 4, PC_DELIVER = 8 };
-constexpr uint32_t kStale = kInf;      // p_gen marker: stale before the batch
-constexpr uint32_t kErr = kInf - 1;    // p_gen marker: rejected packet
-constexpr int kTile = 256;             // decide / tilescan granularity
+constexpr uint32_t kStale = kInf;    // p_gen marker: stale before the batch
+constexpr uint32_t kErr = kInf - 1;  // p_gen marker: rejected packet
+constexpr int kAckTile = 128;        // packets per k_acks tile / block
+constexpr int kAckWarps = 16;        // 512 threads, 8 packets per warp
+constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
+constexpr int kCopyUnroll = 8;       // 16-byte vectors in flight per lane
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 
 struct RxDev {
     uint32_t cb, max_pl, ppc, conn_mask, gen_mask, carry;
     uint64_t pool_cap, arena_cap;
     unsigned long long* rc_key;
-    unsigned long long* rc_done;  // [conns*128] completed_seq
+    unsigned long long* rc_done;  // [conns*128] completed_seq (transport.hpp:223)
     unsigned long long* gen_key;
     GenState* gen;
     uint32_t* touched;
     uint32_t* c_first;  // [pool*ppc] batch scratch
-    uint32_t* c_seen;   // [pool] persistent packet bitmask
+    uint32_t* c_seen;   // [pool] persistent packet bitmask (ChunkRx::pkts_seen)
     uint32_t* c_flags;  // [pool] persistent CF_*
-    int64_t* c_txt;     // [pool] persistent echo tx_time
-    int32_t* c_path;    // [pool] persistent echo path
+    int64_t* c_txt;     // [pool] persistent ChunkRx::tx_time
+    int32_t* c_path;    // [pool] persistent ChunkRx::path
     uint32_t* c_init;   // [pool] batch scratch: first arrival time
     uint32_t* c_cpl;    // [pool] batch scratch: completion time
     uint32_t* c_pmax;   // [pool] batch scratch: prefix max of c_cpl
+    uint32_t* c_newb;   // [pool] batch scratch: bits of new packets
+    uint32_t* c_last;   // [pool] batch scratch: last new packet time
+    uint32_t* c_newfl;  // [pool] batch scratch: ECN/RTX of new packets
     uint32_t* p_gen;    // [batch]
-    uint32_t* p_pos;    // [batch] local ack pos | local completion pos << 16
-    uint8_t* p_cls;     // [batch]
-    uint32_t* tile_cnt; // [tiles*2]
-    uint32_t* tile_off; // [tiles*2]
+    unsigned long long* tile_state;  // [ack tiles] decoupled look-back (ack order)
+    unsigned long long* scan_state;  // [scan tiles] segmented look-back (prefix max)
+    uint32_t* plan_base;             // [touched] first scan tile of each message
     RxCtl* ctl;
     uint8_t* arena;
 };
@@ -86,117 +101,134 @@ __device__ __forceinline__ uint32_t pkts_of(const RxDev& d, uint32_t clen) {
     return (clen + d.max_pl - 1) / d.max_pl;
 }
 
-// ------------------------------------------------------------------ K1
-// rconn_at (transport.cpp:546-563) + the stale-generation test
-// (transport.cpp:602) + message-generation discovery (:620-626).
-__global__ void k_classify(RxDev d, const cn_pkt_hdr* __restrict__ hdrs, uint32_t n,
-                           uint32_t epoch, cn_rx_result* res) {
-    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const cn_pkt_hdr h = hdrs[i];
+// ------------------------------------------------------------------ ingest
+// rconn_at (transport.cpp:546-563), the stale-generation test (:602), lazy
+// MsgRecv init (:620-626) with its chunk vector and buffer (:637, :723),
+// chunk init (:639-645) and the per-packet bit (:676-683) recorded as a
+// first-arrival time.  Table work is warp-aggregated: one leader lane per
+// distinct connection / message generation in the warp.
+__global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
+                                                uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const uint32_t epoch = d.ctl->epoch;
+    const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
+    if (i < tiles) d.tile_state[i] = 0;
     uint32_t status = 0;
-    if (h.flags & CN_PKT_TRIMMED) status |= CN_RXF_UNSUPPORTED;  // trim mode: DESIGN.md §7
     uint32_t g = kErr;
-    if (static_cast<uint32_t>(h.src) >= (1u << 24) || static_cast<uint32_t>(h.dst) >= (1u << 24) ||
-        h.msg_seq >= (1ull << 40) || h.msg_seq == 0) {
-        status |= CN_RXF_UNSUPPORTED;
+    uint32_t touch = 0;
+    cn_pkt_hdr h;
+    bool ok = i < n;
+    if (ok) {
+        h = hdrs[i];
+        if (h.flags & CN_PKT_TRIMMED) status |= CN_RXF_UNSUPPORTED;  // trim mode: DESIGN.md §7
+        if (static_cast<uint32_t>(h.src) >= (1u << 24) ||
+            static_cast<uint32_t>(h.dst) >= (1u << 24) || h.msg_seq >= (1ull << 40) ||
+            h.msg_seq == 0) {
+            status |= CN_RXF_UNSUPPORTED;
+            ok = false;
+        }
     } else {
-        uint32_t conn = h.hdr >> 24, mid = (h.hdr >> 17) & 0x7F;
-        uint64_t rkey = (static_cast<uint64_t>(h.dst) << 32) |
-                        (static_cast<uint64_t>(h.src) << 8) | conn;
+        memset(&h, 0, sizeof h);
+    }
+    const uint32_t mid = (h.hdr >> 17) & 0x7F;
+    // ---- connection (dst, src, conn_id), one table probe per distinct key
+    const uint64_t rkey = ok ? ((static_cast<uint64_t>(h.dst) << 32) |
+                                (static_cast<uint64_t>(h.src) << 8) | (h.hdr >> 24))
+                             : (0xF000000000000000ull | lane);
+    const unsigned pr = __match_any_sync(0xffffffffu, rkey);
+    const int lr = __ffs(pr) - 1;
+    uint32_t rc = kInf;
+    if (ok && lane == lr) {
         bool ins = false;
-        uint32_t rc = table_insert(d.rc_key, d.conn_mask, rkey, &ins);
-        if (rc == kInf) {
-            status |= CN_RXF_CAPACITY;
-        } else if (h.msg_seq <= d.rc_done[rc * 128 + mid]) {
-            g = kStale;
-        } else {
-            bool gins = false;
-            g = table_insert(d.gen_key, d.gen_mask, (static_cast<uint64_t>(rc) << 40) | h.msg_seq,
-                             &gins);
-            if (g == kInf) {
-                g = kErr;
-                status |= CN_RXF_CAPACITY;
-            } else {
-                GenState* G = &d.gen[g];
-                if (gins) {
-                    G->len = h.msg_len;
-                    G->tag = h.msg_tag;
-                    G->seq = h.msg_seq;
-                    G->chunk_base = kEmpty;
-                    G->buf_off = 0;
-                    G->bytes = 0;
-                    G->nchunks = 0;
-                    G->cum = 0;
-                    G->n_init = 0;
-                    G->rc = rc;
-                    G->msg_id = mid;
+        rc = table_insert(d.rc_key, d.conn_mask, rkey, &ins);
+    }
+    rc = __shfl_sync(0xffffffffu, rc, lr);
+    if (ok && rc == kInf) {
+        status |= CN_RXF_CAPACITY;
+        ok = false;
+    }
+    if (ok && h.msg_seq <= d.rc_done[rc * 128 + mid]) {
+        g = kStale;  // transport.cpp:602
+        ok = false;
+    }
+    // ---- message generation (rconn, msg_seq)
+    const uint64_t gkey = ok ? ((static_cast<uint64_t>(rc) << 40) | h.msg_seq)
+                             : (0xF000000000000000ull | lane);
+    const unsigned pg = __match_any_sync(0xffffffffu, gkey);
+    const int lg = __ffs(pg) - 1;
+    uint32_t gs = kInf, nch = 0;
+    unsigned long long cbase = 0, glen = 0;
+    if (ok && lane == lg) {
+        bool gins = false;
+        gs = table_insert(d.gen_key, d.gen_mask, gkey, &gins);
+        if (gs != kInf) {
+            GenState* G = &d.gen[gs];
+            if (gins) {
+                // the unique inserter allocates the message state
+                uint64_t nc = (h.msg_len + d.cb - 1) / d.cb;
+                uint32_t st = 0;
+                unsigned long long base = 0, boff = 0;
+                if (h.msg_len == 0 || nc >= (1ull << 31)) st = CN_RXF_UNSUPPORTED;
+                if (!st) {
+                    base = atomicAdd(&d.ctl->pool_top, static_cast<unsigned long long>(nc));
+                    if (base + nc > d.pool_cap) st = CN_RXF_CAPACITY;
                 }
+                if (!st && d.carry) {
+                    unsigned long long need = (h.msg_len + 15) & ~15ull;
+                    boff = atomicAdd(&d.ctl->arena_top, need);
+                    if (boff + need > d.arena_cap) st = CN_RXF_CAPACITY;
+                }
+                status |= st;
+                G->len = h.msg_len;
+                G->tag = h.msg_tag;
+                G->seq = h.msg_seq;
+                G->chunk_base = st ? 0 : base;
+                G->buf_off = boff;
+                G->touch = 0;
+                G->nchunks = st ? 0 : static_cast<uint32_t>(nc);
+                G->cum = 0;
+                G->n_init = 0;
+                G->rc = rc;
+                G->msg_id = mid;
+                G->deliver_t = kInf;
+                __threadfence();
+                st_release(&G->ready, 1u);
+            } else {
+                // wait for the inserter (resident, already past its CAS)
+                uint32_t spins = 0;
+                while (ld_acquire(&G->ready) == 0) {
+                    __nanosleep(32);
+                    if (++spins > (1u << 24)) {
+                        gs = kInf;
+                        status |= CN_RXF_CAPACITY;
+                        break;
+                    }
+                }
+            }
+            if (gs != kInf) {
+                nch = G->nchunks;
+                cbase = G->chunk_base;
+                glen = G->len;
                 if (atomicExch(&G->epoch, epoch) != epoch) {
                     uint32_t k = atomicAdd(&d.ctl->n_touched, 1u);
-                    d.touched[k] = g;
+                    d.touched[k] = gs;
                 }
             }
+        } else {
+            status |= CN_RXF_CAPACITY;
         }
     }
-    d.p_gen[i] = g;
-    if (status) atomicOr(&res->status, status);
-}
-
-// ------------------------------------------------------------------ K2
-// Lazy MsgRecv init (transport.cpp:620-626): chunk state and the message
-// buffer (accept_payload's buf.resize, :723) come from bump pools.
-__global__ void k_alloc(RxDev d, cn_rx_result* res) {
-    uint32_t nt = d.ctl->n_touched;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt;
-         k += gridDim.x * blockDim.x) {
-        GenState* G = &d.gen[d.touched[k]];
-        if (G->chunk_base == kEmpty) {
-            uint64_t nc = (G->len + d.cb - 1) / d.cb;
-            uint32_t st = 0;
-            if (G->len == 0 || nc >= (1ull << 31)) st = CN_RXF_UNSUPPORTED;
-            unsigned long long base = 0, boff = 0;
-            if (!st) {
-                base = atomicAdd(&d.ctl->pool_top, static_cast<unsigned long long>(nc));
-                if (base + nc > d.pool_cap) st = CN_RXF_CAPACITY;
-            }
-            if (!st && d.carry) {
-                unsigned long long need = (G->len + 15) & ~15ull;
-                boff = atomicAdd(&d.ctl->arena_top, need);
-                if (boff + need > d.arena_cap) st = CN_RXF_CAPACITY;
-            }
-            if (st) {
-                atomicOr(&res->status, st);
-                G->nchunks = 0;  // every packet of this message is rejected
-                G->chunk_base = 0;
-            } else {
-                G->chunk_base = base;
-                G->buf_off = boff;
-                G->nchunks = static_cast<uint32_t>(nc);
-            }
-        }
-        G->max_touched = G->n_init;
-        G->deliver_t = kInf;
-    }
-}
-
-// ------------------------------------------------------------------ K3
-// Per-packet bit (transport.cpp:676-683) as first-arrival times, chunk init
-// (:639-645), and the unwrapped chunk vector size (:636-637).
-__global__ void k_mark(RxDev d, const cn_pkt_hdr* __restrict__ hdrs, uint32_t n,
-                       cn_rx_result* res) {
-    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t g = i < n ? d.p_gen[i] : kErr;
-    uint32_t touched = 0;
-    if (g < kErr) {
-        const cn_pkt_hdr h = hdrs[i];
-        const GenState* G = &d.gen[g];
-        uint64_t nch = G->nchunks;
-        uint64_t c = h.chunk_offset / d.cb;
-        uint32_t s = h.seq_in_chunk;
-        bool bad = nch == 0 || (h.chunk_offset % d.cb) != 0 || c >= nch || h.msg_len != G->len;
+    gs = __shfl_sync(0xffffffffu, gs, lg);
+    nch = __shfl_sync(0xffffffffu, nch, lg);
+    cbase = __shfl_sync(0xffffffffu, cbase, lg);
+    glen = __shfl_sync(0xffffffffu, glen, lg);
+    if (ok && gs != kInf) {
+        const uint64_t c = h.chunk_offset / d.cb;
+        const uint32_t s = h.seq_in_chunk;
+        bool bad = nch == 0 || (h.chunk_offset % d.cb) != 0 || c >= nch || h.msg_len != glen;
         if (!bad) {
-            uint32_t clen = chunk_len_of(d, G->len, c);
+            uint32_t clen = chunk_len_of(d, glen, c);
             uint32_t exp = pkts_of(d, clen);
             uint32_t pl = clen - s * d.max_pl;
             pl = pl < d.max_pl ? pl : d.max_pl;
@@ -204,115 +236,209 @@ __global__ void k_mark(RxDev d, const cn_pkt_hdr* __restrict__ hdrs, uint32_t n,
                   h.payload_len != pl || ((h.hdr >> 8) & 1) != (c + 1 == nch ? 1u : 0u);
         }
         if (bad) {
-            atomicOr(&res->status, CN_RXF_UNSUPPORTED);
-            d.p_gen[i] = kErr;
+            status |= CN_RXF_UNSUPPORTED;
         } else {
-            uint64_t e = G->chunk_base + c;
-            uint32_t t = i + 1;
-            uint32_t fl = d.c_flags[e];
+            g = gs;
+            const uint64_t e = cbase + c;
+            const uint32_t t = i + 1;
+            const uint32_t fl = d.c_flags[e];
             if (!(fl & CF_COMPLETE) && !((d.c_seen[e] >> s) & 1u))
                 atomicMin(&d.c_first[e * d.ppc + s], t);
             if (!(fl & CF_INIT)) atomicMin(&d.c_init[e], t);
-            touched = static_cast<uint32_t>(c) + 1;
+            touch = static_cast<uint32_t>(c) + 1;
         }
     }
-    // warp-aggregated atomicMax of the chunk vector size per message
-    unsigned peers = __match_any_sync(__activemask(), g);
-    int lane = threadIdx.x & 31;
-    int leader = __ffs(peers) - 1;
+    if (i < n) d.p_gen[i] = g;
+    // chunk-vector size per message (:636-637), reduced over the group
     uint32_t gm = 0;
-    for (unsigned p = peers; p; p &= p - 1) {
-        uint32_t v = __shfl_sync(peers, touched, __ffs(p) - 1);
+    for (unsigned p = pg; p; p &= p - 1) {
+        uint32_t v = __shfl_sync(pg, touch, __ffs(p) - 1);
         gm = gm > v ? gm : v;
     }
-    if (lane == leader && g < kErr && gm) atomicMax(&d.gen[g].max_touched, gm);
+    if (lane == lg && gs != kInf && gm)
+        atomicMax(&d.gen[gs].touch, (static_cast<unsigned long long>(epoch) << 32) | gm);
+    status = __reduce_or_sync(0xffffffffu, status);
+    if (lane == 0 && status) atomicOr(&d.ctl->status, status);
+    // ---- plan (last block): per touched message the batch's chunk range
+    // [cum, hi) and its first scan tile; hi = the chunk vector size (:637)
+    __shared__ bool s_last;
+    __shared__ uint32_t s_wsum[8], s_carry;
+    __threadfence();
+    if (threadIdx.x == 0) s_last = atomicAdd(&d.ctl->ingest_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const uint32_t nt = __ldcg(&d.ctl->n_touched);
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (uint32_t k0 = 0; k0 < nt; k0 += blockDim.x) {
+        const uint32_t k = k0 + threadIdx.x;
+        uint32_t tl = 0;
+        if (k < nt) {
+            GenState* G = &d.gen[__ldcg(&d.touched[k])];
+            const unsigned long long tch = __ldcg(&G->touch);
+            const uint32_t lo = __ldcg(&G->cum);
+            uint32_t hi = __ldcg(&G->n_init);
+            if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
+            G->lo_batch = lo;
+            G->n_init = hi;
+            G->deliver_t = kInf;
+            G->tiles_done = 0;
+            G->cum_add = 0;
+            tl = (hi - lo + kScanThreads - 1) / kScanThreads;
+        }
+        // block exclusive sum of tile counts
+        uint32_t inc = tl;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int w = threadIdx.x >> 5;
+        if (lane == 31) s_wsum[w] = inc;
+        __syncthreads();
+        uint32_t wpre = 0;
+        for (int q = 0; q < w; ++q) wpre += s_wsum[q];
+        const uint32_t carry = s_carry;
+        if (k < nt) d.plan_base[k] = carry + wpre + inc - tl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = carry + wpre + inc;
+        __syncthreads();
+    }
+    const uint32_t total = s_carry;
+    for (uint32_t x = threadIdx.x; x < total; x += blockDim.x) d.scan_state[x] = 0;
+    if (threadIdx.x == 0) {
+        d.ctl->n_scan_tiles = total;
+        d.ctl->ingest_done = 0;
+    }
 }
 
-// block-wide inclusive max-scan over 256 threads
-__device__ __forceinline__ uint32_t block_scan_max(uint32_t v, uint32_t* smem) {
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+
+// block-wide inclusive max-scan (blockDim multiple of 32, <= 1024)
+__device__ __forceinline__ uint32_t block_scan_max(uint32_t v, uint32_t* wsum) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int o = 1; o < 32; o <<= 1) {
         uint32_t x = __shfl_up_sync(0xffffffffu, v, o);
         if (lane >= o) v = v > x ? v : x;
     }
-    if (lane == 31) smem[w] = v;
+    if (lane == 31) wsum[w] = v;
     __syncthreads();
     if (w == 0) {
-        uint32_t x = lane < (blockDim.x >> 5) ? smem[lane] : 0;
+        uint32_t x = lane < nw ? wsum[lane] : 0;
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x = x > y ? x : y;
         }
-        smem[lane] = x;
+        wsum[lane] = x;
     }
     __syncthreads();
     if (w > 0) {
-        uint32_t p = smem[w - 1];
+        uint32_t p = wsum[w - 1];
         v = v > p ? v : p;
     }
-    __syncthreads();
     return v;
 }
 
-// ------------------------------------------------------------------ K4
-// chunk completion times and the cumulative-cursor prefix max
-// (chunk_completed's `while (chunks[cum].complete) ++cum`, :736-738).
-constexpr int kScanItems = 8;
-__global__ void __launch_bounds__(256) k_scan(RxDev d) {
-    __shared__ uint32_t smem[32];
-    __shared__ uint32_t carry_s;
-    uint32_t nt = d.ctl->n_touched;
-    for (uint32_t k = blockIdx.x; k < nt; k += gridDim.x) {
-        GenState* G = &d.gen[d.touched[k]];
-        uint32_t lo = G->cum, hi = G->max_touched;
-        uint64_t base = G->chunk_base;
+
+// -------------------------------------------------------------------- scan
+// Flattened over every touched message: tile = 256 consecutive chunks of
+// one message's range [lo, hi), handed out by ticket (tickets of a message
+// are consecutive, planned by k_ingest's last block).  Per chunk: the
+// completion time cpl (max first arrival over its missing packets), the
+// new-packet bitmask and last new packet (for finalize), and the prefix max
+// pmax that drives the cumulative cursor (chunk_completed's
+// `while (complete) ++cum`, :736-738) -- a segmented decoupled look-back
+// across the message's tiles.
+__device__ __forceinline__ uint32_t find_gen_of_ticket(const RxDev& d, uint32_t nt, uint32_t ticket) {
+    uint32_t lo = 0, hi = nt;  // last k with plan_base[k] <= ticket
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldcg(&d.plan_base[mid]) <= ticket) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t s_ticket, s_k, s_carry;
+    const int lane = threadIdx.x & 31;
+    const uint32_t total = d.ctl->n_scan_tiles;
+    const uint32_t nt = d.ctl->n_touched;
+    const uint32_t ppc = d.ppc;
+    for (;;) {
         if (threadIdx.x == 0) {
-            G->n_init = hi;
-            carry_s = 0;
+            uint32_t tk = atomicAdd(&d.ctl->scan_ticket, 1u);
+            s_ticket = tk;
+            s_k = tk < total ? find_gen_of_ticket(d, nt, tk) : 0;
         }
         __syncthreads();
-        for (uint32_t t0 = lo; t0 < hi; t0 += 256 * kScanItems) {
-            uint32_t v[kScanItems];
-            uint32_t run = 0;
-#pragma unroll
-            for (int j = 0; j < kScanItems; ++j) {
-                uint32_t c = t0 + threadIdx.x * kScanItems + j;
-                uint32_t cpl = 0;
-                if (c < hi) {
-                    uint64_t e = base + c;
-                    if (!(d.c_flags[e] & CF_COMPLETE)) {
-                        uint32_t exp = pkts_of(d, chunk_len_of(d, G->len, c));
-                        uint32_t seen = d.c_seen[e];
-                        for (uint32_t s = 0; s < exp; ++s) {
-                            if ((seen >> s) & 1u) continue;
-                            uint32_t f = d.c_first[e * d.ppc + s];
-                            cpl = cpl > f ? cpl : f;
-                        }
+        const uint32_t ticket = s_ticket;
+        if (ticket >= total) break;
+        const uint32_t k = s_k;
+        GenState* G = &d.gen[d.touched[k]];
+        const uint32_t lo = G->lo_batch, hi = G->n_init;
+        const uint32_t ti = ticket - d.plan_base[k];
+        const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
+        const uint64_t base = G->chunk_base;
+        uint32_t cpl = 0;
+        if (c < hi) {
+            const uint64_t e = base + c;
+            if (!(d.c_flags[e] & CF_COMPLETE)) {
+                const uint32_t exp = pkts_of(d, chunk_len_of(d, G->len, c));
+                const uint32_t seen = d.c_seen[e];
+                uint32_t newb = 0, last = 0;
+                for (uint32_t s = 0; s < exp; ++s) {
+                    uint32_t f = d.c_first[e * ppc + s];
+                    if (f != kInf) {
+                        newb |= 1u << s;
+                        last = last > f ? last : f;
                     }
-                    d.c_cpl[e] = cpl;
+                    if ((seen >> s) & 1u) f = 0;
+                    cpl = cpl > f ? cpl : f;
                 }
-                run = run > cpl ? run : cpl;
-                v[j] = run;
+                d.c_newb[e] = newb;
+                d.c_last[e] = last;
             }
-            uint32_t incl = block_scan_max(run, smem);
-            // exclusive prefix for this thread = max of previous threads
-            uint32_t prev = __shfl_up_sync(0xffffffffu, incl, 1);
-            if ((threadIdx.x & 31) == 0) prev = (threadIdx.x >> 5) ? smem[(threadIdx.x >> 5) - 1] : 0;
-            uint32_t carry = carry_s;
-            uint32_t pre = prev > carry ? prev : carry;
-#pragma unroll
-            for (int j = 0; j < kScanItems; ++j) {
-                uint32_t c = t0 + threadIdx.x * kScanItems + j;
-                if (c < hi) d.c_pmax[base + c] = v[j] > pre ? v[j] : pre;
-            }
-            __syncthreads();
-            if (threadIdx.x == blockDim.x - 1) carry_s = incl > carry ? incl : carry;
-            __syncthreads();
+            d.c_cpl[e] = cpl;
         }
-        if (threadIdx.x == 0) {
-            uint32_t dt = kInf;
-            if (G->nchunks && hi == G->nchunks) dt = d.c_pmax[base + hi - 1];
-            G->deliver_t = dt;
+        const uint32_t incl = block_scan_max(cpl, wsum);
+        if (threadIdx.x < 32) {
+            const uint32_t agg = wsum[kScanThreads / 32 - 1];
+            uint32_t carry = 0;
+            if (ti == 0) {
+                if (lane == 0) atomicExch(&d.scan_state[ticket], kFlagIncl | agg);
+            } else {
+                if (lane == 0) atomicExch(&d.scan_state[ticket], kFlagAgg | agg);
+                int64_t b = static_cast<int64_t>(ticket) - 1;
+                const int64_t seg0 = static_cast<int64_t>(ticket) - ti;  // the message's first tile
+                for (;;) {
+                    int64_t p = b - lane;
+                    unsigned long long v = p >= seg0 ? ld_volatile_u64(&d.scan_state[p]) : kFlagIncl;
+                    unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                    unsigned upto = inc ? ((2u << (__ffs(inc) - 1)) - 1) : 0xffffffffu;
+                    unsigned waiting = __ballot_sync(0xffffffffu, (v >> 62) == 0) & upto;
+                    if (waiting) {
+                        __nanosleep(32);
+                        continue;
+                    }
+                    uint32_t mine = ((upto >> lane) & 1u) ? static_cast<uint32_t>(v) : 0u;
+                    mine = __reduce_max_sync(0xffffffffu, mine);
+                    carry = carry > mine ? carry : mine;
+                    if (inc) break;
+                    b -= 32;
+                }
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(&d.scan_state[ticket], kFlagIncl | (agg > carry ? agg : carry));
+                }
+            }
+            if (lane == 0) s_carry = carry;
+        }
+        __syncthreads();
+        if (c < hi) {
+            const uint32_t carry = s_carry;
+            const uint32_t pm = incl > carry ? incl : carry;
+            d.c_pmax[base + c] = pm;
+            if (c == hi - 1) G->deliver_t = hi == G->nchunks ? pm : kInf;
         }
         __syncthreads();
     }
@@ -324,154 +450,27 @@ __device__ __forceinline__ uint32_t pmax_at(const RxDev& d, const GenState& G, u
     return d.c_pmax[G.chunk_base + x];
 }
 
-// ------------------------------------------------------------------ K5
-// What the reference does with each packet (handle_data branches) and where
-// its ack / completion lands in the ordered output streams.
-__global__ void __launch_bounds__(kTile) k_decide(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
-                                                  uint32_t n, cn_rx_result* res) {
-    __shared__ uint32_t wsum[kTile / 32];
-    uint32_t i = blockIdx.x * kTile + threadIdx.x;
-    uint8_t cls = 0;
-    uint32_t st = 0;
-    if (i < n) {
-        uint32_t g = d.p_gen[i];
-        uint32_t t = i + 1;
-        if (g == kStale) {
-            cls = PC_STALE;  // transport.cpp:602-615
-        } else if (g != kErr) {
-            const GenState G = d.gen[g];
-            if (t > G.deliver_t) {
-                cls = PC_STALE;
-            } else {
-                const cn_pkt_hdr h = hdrs[i];
-                uint64_t c = h.chunk_offset / d.cb;
-                uint32_t s = h.seq_in_chunk;
-                uint64_t e = G.chunk_base + c;
-                uint32_t cpl = (d.c_flags[e] & CF_COMPLETE) ? 0 : d.c_cpl[e];
-                if (cpl < t) {
-                    cls = PC_ACK;  // complete chunk (:651-655) or behind cursor (:631-634)
-                } else if (cpl == t) {
-                    cls = PC_ACK | PC_COPY;  // completes its chunk (:686-687)
-                    if (t == G.deliver_t) cls |= PC_DELIVER;
-                } else if (!((d.c_seen[e] >> s) & 1u) && d.c_first[e * d.ppc + s] == t) {
-                    cls = PC_COPY;  // new packet, chunk still open: silent
-                }
-                // The reference unwraps the 8-bit csn against the cursor
-                // (:629-636); check it names chunk c (no aliasing).
-                if (pmax_at(d, G, c) < t) {
-                    if (pmax_at(d, G, c + 128) < t) st |= CN_RXF_ALIAS;
-                } else if (c >= 128 && pmax_at(d, G, c - 128) >= t) {
-                    st |= CN_RXF_ALIAS;
-                }
-            }
-        }
-        d.p_cls[i] = cls;
-    }
-    if (st) atomicOr(&res->status, st);
-    // two exclusive counts (acks, completions) packed in one 32-bit scan
-    uint32_t v = ((cls & (PC_STALE | PC_ACK)) ? 1u : 0u) | ((cls & PC_DELIVER) ? 1u << 16 : 0u);
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t incl = v;
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
-    }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-        uint32_t x = lane < kTile / 32 ? wsum[lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane < kTile / 32) wsum[lane] = x;
-    }
-    __syncthreads();
-    uint32_t excl = incl - v + (w ? wsum[w - 1] : 0);
-    if (i < n) d.p_pos[i] = excl;
-    if (threadIdx.x == kTile - 1) {
-        uint32_t tot = wsum[kTile / 32 - 1];
-        d.tile_cnt[blockIdx.x * 2 + 0] = tot & 0xFFFFu;
-        d.tile_cnt[blockIdx.x * 2 + 1] = tot >> 16;
-    }
-}
-
-// ------------------------------------------------------------------ K5b
-__global__ void __launch_bounds__(1024) k_tilescan(RxDev d, uint32_t tiles, uint32_t max_acks,
-                                                   uint32_t max_cpls, cn_rx_result* res) {
-    __shared__ uint32_t wsum[2][32];
-    __shared__ uint32_t carry[2];
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (threadIdx.x < 2) carry[threadIdx.x] = 0;
-    __syncthreads();
-    for (uint32_t t0 = 0; t0 < tiles; t0 += 1024) {
-        uint32_t t = t0 + threadIdx.x;
-        uint32_t a = t < tiles ? d.tile_cnt[2 * t] : 0;
-        uint32_t b = t < tiles ? d.tile_cnt[2 * t + 1] : 0;
-        uint32_t ia = a, ib = b;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t x = __shfl_up_sync(0xffffffffu, ia, o);
-            uint32_t y = __shfl_up_sync(0xffffffffu, ib, o);
-            if (lane >= o) {
-                ia += x;
-                ib += y;
-            }
-        }
-        if (lane == 31) {
-            wsum[0][w] = ia;
-            wsum[1][w] = ib;
-        }
-        __syncthreads();
-        if (w == 0) {
-            uint32_t x = wsum[0][lane], y = wsum[1][lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t p = __shfl_up_sync(0xffffffffu, x, o);
-                uint32_t q = __shfl_up_sync(0xffffffffu, y, o);
-                if (lane >= o) {
-                    x += p;
-                    y += q;
-                }
-            }
-            wsum[0][lane] = x;
-            wsum[1][lane] = y;
-        }
-        __syncthreads();
-        uint32_t ea = carry[0] + ia - a + (w ? wsum[0][w - 1] : 0);
-        uint32_t eb = carry[1] + ib - b + (w ? wsum[1][w - 1] : 0);
-        if (t < tiles) {
-            d.tile_off[2 * t] = ea;
-            d.tile_off[2 * t + 1] = eb;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            carry[0] += wsum[0][31];
-            carry[1] += wsum[1][31];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        res->n_acks = carry[0];
-        res->n_completions = carry[1];
-        if (carry[0] > max_acks || carry[1] > max_cpls) atomicOr(&res->status, CN_RXF_CAPACITY);
-    }
-}
-
-// warp-cooperative scatter copy (accept_payload's memcpy, :728-729)
+// -------------------------------------------------------------------- copy
+// accept_payload's scatter memcpy (:719-730) for every first-arriving packet
+// (duplicates of a seen packet return before it, :677).  Pure streaming:
+// one warp per packet, 16-byte vectors, all loads of a packet in flight
+// before its stores.  The decision needs only the batch's first[] (final
+// after k_ingest), so this kernel does not wait for the ack machinery.
 __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
                                           uint32_t len, int lane) {
     if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
         const int4* s4 = reinterpret_cast<const int4*>(src);
         int4* d4 = reinterpret_cast<int4*>(dst);
-        uint32_t nv = len >> 4;
-        for (uint32_t v0 = 0; v0 < nv; v0 += 32 * 8) {
-            int4 r[8];
+        const uint32_t nv = len >> 4;
+        for (uint32_t v0 = 0; v0 < nv; v0 += 32 * kCopyUnroll) {
+            int4 r[kCopyUnroll];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < kCopyUnroll; ++k) {
                 uint32_t v = v0 + k * 32 + lane;
                 if (v < nv) r[k] = __ldcs(s4 + v);
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < kCopyUnroll; ++k) {
                 uint32_t v = v0 + k * 32 + lane;
                 if (v < nv) d4[v] = r[k];
             }
@@ -482,28 +481,96 @@ __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8
     }
 }
 
-// ------------------------------------------------------------------ K6
-// One warp per packet: payload scatter, ack snapshot (send_ack :763-792 or
-// the stale re-ack :602-615), completion record (maybe_deliver :794-803).
-__global__ void __launch_bounds__(256) k_work(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
+__global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                               const uint8_t* __restrict__ payload, uint64_t stride,
-                                              uint32_t n, cn_ack_rec* __restrict__ acks,
-                                              uint32_t max_acks, cn_completion* __restrict__ cpls,
-                                              uint32_t max_cpls, cn_rx_result* res) {
-    uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    uint8_t cls = d.p_cls[i];
-    if (!cls) return;
-    const cn_pkt_hdr h = hdrs[i];
-    uint32_t t = i + 1;
-    uint32_t tile = i / kTile;
-    uint32_t pos = d.p_pos[i];
-    uint32_t csn = (h.hdr >> 9) & 0xFF;
+                                              uint32_t n) {
+    __shared__ uint32_t s_cnt;
+    __shared__ unsigned long long s_bytes;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        s_cnt = 0;
+        s_bytes = 0;
+    }
+    __syncthreads();
+    uint32_t my_cnt = 0, my_bytes = 0;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+        const uint32_t g = d.p_gen[i];
+        if (g >= kErr) continue;  // stale before the batch, or rejected
+        const cn_pkt_hdr* hp = hdrs + i;
+        const uint64_t off = hp->chunk_offset;
+        const uint32_t s = hp->seq_in_chunk;
+        const uint32_t len = hp->payload_len;
+        const GenState* G = &d.gen[g];
+        const uint64_t e = G->chunk_base + off / d.cb;
+        const bool fresh = !((d.c_seen[e] >> s) & 1u) && d.c_first[e * d.ppc + s] == i + 1;
+        if (!fresh) continue;
+        ++my_cnt;
+        my_bytes += len;
+        if (d.carry)
+            warp_copy(d.arena + G->buf_off + off + static_cast<uint64_t>(s) * d.max_pl,
+                      payload + static_cast<uint64_t>(i) * stride, len, lane);
+    }
+    if (lane == 0 && my_cnt) {
+        atomicAdd(&s_cnt, my_cnt);
+        atomicAdd(&s_bytes, static_cast<unsigned long long>(my_bytes));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) {
+        atomicAdd(&d.ctl->n_copied, s_cnt);
+        atomicAdd(&d.ctl->bytes_copied, s_bytes);
+    }
+}
 
+// What the reference does with packet i (handle_data's branches).
+__device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __restrict__ hdrs,
+                                          uint32_t i, uint32_t* st, uint64_t* e_out) {
+    uint32_t g = d.p_gen[i];
+    uint32_t t = i + 1;
+    if (g == kStale) return PC_STALE;  // transport.cpp:602-615
+    if (g == kErr) return 0;
+    const GenState& G = d.gen[g];
+    uint32_t dt = G.deliver_t;
+    if (t > dt) return PC_STALE;
+    uint64_t off = hdrs[i].chunk_offset;
+    uint32_t s = hdrs[i].seq_in_chunk;
+    uint64_t c = off / d.cb;
+    uint64_t e = G.chunk_base + c;
+    *e_out = e;
+    uint8_t cls = 0;
+    uint32_t cpl = (d.c_flags[e] & CF_COMPLETE) ? 0 : d.c_cpl[e];
+    if (cpl < t) {
+        cls = PC_ACK;  // complete chunk (:651-655) or behind the cursor (:631-634)
+    } else if (cpl == t) {
+        cls = PC_ACK | PC_COPY;  // completes its chunk (:686-687)
+        if (t == dt) cls |= PC_DELIVER;
+    } else if (!((d.c_seen[e] >> s) & 1u) && d.c_first[e * d.ppc + s] == t) {
+        cls = PC_COPY;  // new packet of an open chunk: silent
+    }
+    // The reference unwraps the 8-bit csn against the cursor (:629-636):
+    // verify it names chunk c (no aliasing) -- DESIGN.md §3.
+    if (pmax_at(d, G, c) < t) {
+        if (pmax_at(d, G, c + 128) < t) *st |= CN_RXF_ALIAS;
+    } else if (c >= 128 && pmax_at(d, G, c - 128) >= t) {
+        *st |= CN_RXF_ALIAS;
+    }
+    return cls;
+}
+
+// -------------------------------------------------------------------- acks
+// One block per 128-packet tile: 4 warps decide (one lane per packet); the
+// tile's ack/completion counts are ordered with a warp-parallel decoupled
+// look-back while all 16 warps build their packets' ack snapshots
+// (send_ack :763-792, stale re-ack :602-615) into shared memory; then the
+// records are written to their stream positions, with completion records
+// (maybe_deliver :794-803).
+__device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __restrict__ hdrs,
+                                          uint32_t i, uint8_t cls, int lane, cn_ack_rec* out) {
+    const cn_pkt_hdr h = hdrs[i];
+    const uint32_t t = i + 1;
+    const uint32_t csn = (h.hdr >> 9) & 0xFF;
     if (cls & PC_STALE) {
-        uint32_t a = d.tile_off[2 * tile] + (pos & 0xFFFFu);
-        if (lane == 0 && a < max_acks) {
+        if (lane == 0) {
             cn_ack_rec r;
             memset(&r, 0, sizeof r);
             r.src = h.dst;
@@ -513,177 +580,320 @@ __global__ void __launch_bounds__(256) k_work(RxDev d, const cn_pkt_hdr* __restr
             r.flags = CN_ACK_CUM_VALID;
             r.pkt_index = i;
             r.msg_seq = h.msg_seq;
-            acks[a] = r;
+            *out = r;
         }
         return;
     }
-    const uint32_t g = d.p_gen[i];
-    const GenState G = d.gen[g];
-    if ((cls & PC_COPY) && d.carry) {
-        uint64_t off = h.chunk_offset + static_cast<uint64_t>(h.seq_in_chunk) * d.max_pl;
-        warp_copy(d.arena + G.buf_off + off, payload + static_cast<uint64_t>(i) * stride,
-                  h.payload_len, lane);
+    const GenState& G = d.gen[d.p_gen[i]];
+    const uint32_t cum0 = G.cum, n_init = G.n_init;
+    const uint64_t cbase = G.chunk_base;
+    // cum after this packet: first x in [cum0, n_init) with pmax[x] > t
+    uint32_t lo = cum0, hi = n_init;
+    const uint32_t* pm = d.c_pmax + cbase;
+    while (hi - lo > 32) {
+        uint32_t step = (hi - lo + 31) / 32;
+        uint32_t p = lo + (lane + 1) * step - 1;
+        bool ok = p < hi && pm[p] <= t;
+        uint32_t k = __popc(__ballot_sync(0xffffffffu, ok));
+        lo += k * step;
+        hi = hi < lo + step ? hi : lo + step;
     }
-    if (cls & PC_ACK) {
-        // cum after this packet: first x in [cum0, n_init) with pmax[x] > t
-        uint32_t lo = G.cum, hi = G.n_init;
-        const uint32_t* pm = d.c_pmax + G.chunk_base;
-        while (hi - lo > 32) {
-            uint32_t step = (hi - lo + 31) / 32;
-            uint32_t p = lo + (lane + 1) * step - 1;
-            bool ok = p < hi && pm[p] <= t;
-            uint32_t k = __popc(__ballot_sync(0xffffffffu, ok));
-            lo += k * step;
-            hi = hi < lo + step ? hi : lo + step;
-        }
-        bool ok = lo + lane < hi && pm[lo + lane] <= t;
-        uint32_t cum = lo + __popc(__ballot_sync(0xffffffffu, ok));
-        // 128-bit SACK, bit j = chunk cum+j complete (:775-779)
-        const uint32_t* cp = d.c_cpl + G.chunk_base;
-        uint32_t sw[4];
+    bool okc = lo + lane < hi && pm[lo + lane] <= t;
+    const uint32_t cum = lo + __popc(__ballot_sync(0xffffffffu, okc));
+    // 128-bit SACK, bit j = chunk cum+j complete (:775-779)
+    const uint32_t* cp = d.c_cpl + cbase;
+    uint32_t sw[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t x = cum + q * 32 + lane;
-            sw[q] = __ballot_sync(0xffffffffu, x < G.n_init && cp[x] <= t);
+    for (int q = 0; q < 4; ++q) {
+        uint32_t x = cum + q * 32 + lane;
+        sw[q] = __ballot_sync(0xffffffffu, x < n_init && cp[x] <= t);
+    }
+    // echo of chunk cum + uint8(cause - uint8(cum)) (:781-789)
+    uint32_t rel = (csn - (cum & 0xFF)) & 0xFF;
+    uint32_t ei = cum + rel;
+    int64_t etxt = 0;
+    int32_t epath = 0;
+    uint32_t eecn = 0;
+    if (rel < CN_CSN_WINDOW && ei < n_init) {
+        uint64_t E = cbase + ei;
+        uint32_t fl = d.c_flags[E];
+        if ((fl & CF_INIT) || d.c_init[E] <= t) {
+            uint32_t exp = pkts_of(d, chunk_len_of(d, G.len, ei));
+            uint32_t seen = d.c_seen[E];
+            uint32_t f = (static_cast<uint32_t>(lane) < exp && !((seen >> lane) & 1u))
+                             ? d.c_first[E * d.ppc + lane]
+                             : kInf;
+            bool fok = f <= t;
+            uint32_t lastf = __reduce_max_sync(0xffffffffu, fok ? f : 0u);
+            unsigned eb = __ballot_sync(0xffffffffu, fok && (hdrs[fok ? f - 1 : i].flags & CN_PKT_ECN));
+            if (lastf) {
+                etxt = hdrs[lastf - 1].tx_time;
+                epath = hdrs[lastf - 1].path_id;
+            } else {
+                etxt = d.c_txt[E];
+                epath = d.c_path[E];
+            }
+            eecn = (eb != 0) || (fl & CF_ECN);
         }
-        // echo of chunk cum + uint8(cause - uint8(cum)) (:781-789)
-        uint32_t rel = (csn - (cum & 0xFF)) & 0xFF;
-        uint32_t ei = cum + rel;
-        int64_t etxt = 0;
-        int32_t epath = 0;
-        uint32_t eecn = 0;
-        if (rel < CN_CSN_WINDOW && ei < G.n_init) {
-            uint64_t E = G.chunk_base + ei;
-            uint32_t fl = d.c_flags[E];
-            bool init = (fl & CF_INIT) || d.c_init[E] <= t;
-            if (init) {
-                uint32_t exp = pkts_of(d, chunk_len_of(d, G.len, ei));
-                uint32_t seen = d.c_seen[E];
-                uint32_t f = (static_cast<uint32_t>(lane) < exp && !((seen >> lane) & 1u))
-                                 ? d.c_first[E * d.ppc + lane] : kInf;
-                bool fok = f <= t;
-                uint32_t fm = fok ? f : 0;
-                uint32_t lastf = __reduce_max_sync(0xffffffffu, fm);
-                uint32_t ecn_b = __ballot_sync(0xffffffffu,
-                                               fok && (hdrs[fok ? f - 1 : 0].flags & CN_PKT_ECN));
-                if (lastf) {
-                    etxt = hdrs[lastf - 1].tx_time;
-                    epath = hdrs[lastf - 1].path_id;
-                } else {
-                    etxt = d.c_txt[E];
-                    epath = d.c_path[E];
+    }
+    if (lane == 0) {
+        cn_ack_rec r;
+        memset(&r, 0, sizeof r);
+        r.src = h.dst;
+        r.dst = h.src;
+        r.hdr = enc_hdr(h.hdr >> 24, G.msg_id, csn, 0, 0);
+        r.echo_path_id = epath;
+        r.cum_csn = static_cast<uint8_t>((cum - 1) & 0xFF);
+        r.flags = (cum > 0 ? CN_ACK_CUM_VALID : 0) | (eecn ? CN_ACK_ECN_ECHO : 0);
+        r.pkt_index = i;
+        r.msg_seq = G.seq;
+        r.sack[0] = sw[0] | (static_cast<uint64_t>(sw[1]) << 32);
+        r.sack[1] = sw[2] | (static_cast<uint64_t>(sw[3]) << 32);
+        r.echo_tx_time = etxt;
+        *out = r;
+    }
+}
+
+__global__ void __launch_bounds__(kAckWarps * 32) k_acks(
+    RxDev d, const cn_pkt_hdr* __restrict__ hdrs, uint32_t n, cn_ack_rec* __restrict__ acks,
+    uint32_t max_acks, cn_completion* __restrict__ cpls, uint32_t max_cpls) {
+    constexpr int kDecideWarps = kAckTile / 32;
+    __shared__ cn_ack_rec s_rec[kAckTile];
+    __shared__ uint8_t s_cls[kAckTile];
+    __shared__ uint32_t s_aloc[kAckTile], s_cloc[kAckTile];
+    __shared__ uint32_t s_wa[kDecideWarps], s_wc[kDecideWarps];
+    __shared__ uint32_t s_tile, s_base_a, s_base_c;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&d.ctl->tile_ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
+    const uint32_t i0 = tile * kAckTile;
+    if (warp < kDecideWarps) {
+        uint32_t st = 0;
+        uint8_t cls = 0;
+        uint64_t e = 0;
+        const uint32_t j = warp * 32 + lane;
+        const uint32_t i = i0 + j;
+        if (i < n) cls = decide(d, hdrs, i, &st, &e);
+        if (cls & PC_COPY) {  // ChunkRx::ecn / any_rtx of new packets (:680-681)
+            uint8_t pf = hdrs[i].flags;
+            uint32_t b = ((pf & CN_PKT_ECN) ? CF_ECN : 0) | ((pf & CN_PKT_RTX) ? CF_RTX : 0);
+            if (b) atomicOr(&d.c_newfl[e], b);
+        }
+        const unsigned ab = __ballot_sync(0xffffffffu, cls & (PC_STALE | PC_ACK));
+        const unsigned cb = __ballot_sync(0xffffffffu, cls & PC_DELIVER);
+        const unsigned lt = (1u << lane) - 1;
+        s_cls[j] = cls;
+        s_aloc[j] = __popc(ab & lt);
+        s_cloc[j] = __popc(cb & lt);
+        if (lane == 0) {
+            s_wa[warp] = __popc(ab);
+            s_wc[warp] = __popc(cb);
+        }
+        st = __reduce_or_sync(0xffffffffu, st);
+        if (lane == 0 && st) atomicOr(&d.ctl->status, st);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t ta = 0, tc = 0;
+        for (int w = 0; w < kDecideWarps; ++w) {
+            ta += s_wa[w];
+            tc += s_wc[w];
+        }
+        const unsigned long long agg = ta | (static_cast<unsigned long long>(tc) << 31);
+        unsigned long long pre = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(&d.tile_state[0], kFlagIncl | agg);
+        } else {
+            if (lane == 0) atomicExch(&d.tile_state[tile], kFlagAgg | agg);
+            // warp-parallel look-back: lane l inspects tile (base - l)
+            int64_t base = static_cast<int64_t>(tile) - 1;
+            for (;;) {
+                int64_t p = base - lane;
+                unsigned long long v = p >= 0 ? ld_volatile_u64(&d.tile_state[p]) : kFlagIncl;
+                unsigned incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                unsigned upto = incl ? ((2u << (__ffs(incl) - 1)) - 1) : 0xffffffffu;
+                unsigned waiting = __ballot_sync(0xffffffffu, (v >> 62) == 0) & upto;
+                if (waiting) {
+                    __nanosleep(32);
+                    continue;
                 }
-                eecn = (ecn_b != 0) || (fl & CF_ECN);
+                unsigned long long mine = ((upto >> lane) & 1u) ? (v & ~(3ull << 62)) : 0ull;
+                for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+                pre += mine;
+                if (incl) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(&d.tile_state[tile], kFlagIncl | (agg + pre));
             }
         }
-        uint32_t a = d.tile_off[2 * tile] + (pos & 0xFFFFu);
-        if (lane == 0 && a < max_acks) {
-            cn_ack_rec r;
-            memset(&r, 0, sizeof r);
-            r.src = h.dst;
-            r.dst = h.src;
-            r.hdr = enc_hdr(h.hdr >> 24, G.msg_id, csn, 0, 0);
-            r.echo_path_id = epath;
-            r.cum_csn = static_cast<uint8_t>((cum - 1) & 0xFF);
-            r.flags = (cum > 0 ? CN_ACK_CUM_VALID : 0) | (eecn ? CN_ACK_ECN_ECHO : 0);
-            r.pkt_index = i;
-            r.msg_seq = G.seq;
-            r.sack[0] = sw[0] | (static_cast<uint64_t>(sw[1]) << 32);
-            r.sack[1] = sw[2] | (static_cast<uint64_t>(sw[3]) << 32);
-            r.echo_tx_time = etxt;
-            acks[a] = r;
+        if (lane == 0) {
+            s_base_a = static_cast<uint32_t>(pre & 0x7FFFFFFFu);
+            s_base_c = static_cast<uint32_t>(pre >> 31);
+            if (tile == tiles - 1) {
+                unsigned long long tot = agg + pre;
+                uint32_t na = static_cast<uint32_t>(tot & 0x7FFFFFFFu);
+                uint32_t nc = static_cast<uint32_t>(tot >> 31);
+                d.ctl->n_acks = na;
+                d.ctl->n_cpls = nc;
+                if (na > max_acks || nc > max_cpls) atomicOr(&d.ctl->status, CN_RXF_CAPACITY);
+            }
         }
     }
-    if ((cls & PC_DELIVER) && lane == 0) {
-        uint32_t a = d.tile_off[2 * tile + 1] + (pos >> 16);
-        if (a < max_cpls) {
-            cn_completion c;
-            memset(&c, 0, sizeof c);
-            c.tag = G.tag;
-            c.src = h.src;
-            c.dst = h.dst;
-            c.len = G.len;
-            c.msg_seq = G.seq;
-            c.pkt_index = i;
-            c.msg_id = G.msg_id;
-            c.buf_offset = d.carry ? G.buf_off : ~0ull;
-            c.bytes = G.len;  // every byte accepted exactly once
-            cpls[a] = c;
-        }
+    // every warp builds the acks of its packets while warp 0 looks back
+    constexpr int kPer = kAckTile / kAckWarps;
+    for (int jj = 0; jj < kPer; ++jj) {
+        const int j = warp * kPer + jj;
+        const uint8_t cls = s_cls[j];
+        if (cls & (PC_STALE | PC_ACK)) build_ack(d, hdrs, i0 + j, cls, lane, &s_rec[j]);
     }
-    if (cls & PC_COPY) {
-        unsigned m = __activemask();
-        if (lane == __ffs(m) - 1) {
-            atomicAdd(&res->n_copied, 1u);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&res->bytes_copied),
-                      static_cast<unsigned long long>(h.payload_len));
+    __syncthreads();
+    for (int jj = 0; jj < kPer; ++jj) {
+        const int j = warp * kPer + jj;
+        const uint8_t cls = s_cls[j];
+        uint32_t w = j >> 5, pa = s_aloc[j], pc = s_cloc[j];
+        for (uint32_t q = 0; q < w; ++q) {
+            pa += s_wa[q];
+            pc += s_wc[q];
+        }
+        if ((cls & (PC_STALE | PC_ACK)) && lane < 16) {
+            uint32_t a = s_base_a + pa;
+            if (a < max_acks)
+                reinterpret_cast<uint32_t*>(&acks[a])[lane] =
+                    reinterpret_cast<const uint32_t*>(&s_rec[j])[lane];
+        }
+        if ((cls & PC_DELIVER) && lane == 0) {
+            const uint32_t i = i0 + j;
+            uint32_t a = s_base_c + pc;
+            if (a < max_cpls) {
+                const GenState& G = d.gen[d.p_gen[i]];
+                cn_completion c;
+                memset(&c, 0, sizeof c);
+                c.tag = G.tag;
+                c.src = hdrs[i].src;
+                c.dst = hdrs[i].dst;
+                c.len = G.len;
+                c.msg_seq = G.seq;
+                c.pkt_index = i;
+                c.msg_id = G.msg_id;
+                c.buf_offset = d.carry ? G.buf_off : ~0ull;
+                c.bytes = G.len;  // every byte accepted exactly once
+                cpls[a] = c;
+            }
         }
     }
 }
 
-// ------------------------------------------------------------------ K7
-// Fold batch scratch into persistent per-chunk state, advance cum, retire
-// delivered messages (completed_seq, :801).
-__global__ void __launch_bounds__(256) k_finalize(RxDev d, const cn_pkt_hdr* __restrict__ hdrs) {
-    __shared__ uint32_t cnt_s;
-    uint32_t nt = d.ctl->n_touched;
-    for (uint32_t k = blockIdx.x; k < nt; k += gridDim.x) {
-        uint32_t g = d.touched[k];
-        GenState* G = &d.gen[g];
-        uint32_t lo = G->cum, hi = G->n_init;
-        uint64_t base = G->chunk_base;
-        if (threadIdx.x == 0) cnt_s = 0;
+// ---------------------------------------------------------------- finalize
+// Same tiles: fold batch scratch into persistent per-chunk state
+// (pkts_seen, complete, init, ecn, any_rtx, tx_time/path of the last new
+// packet, :678-683).  The last tile of a message advances its cum and
+// retires it if delivered (completed_seq, :801); the last block of the
+// grid publishes the batch result and arms the next batch.
+__global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
+                                                           cn_rx_result* res) {
+    __shared__ uint32_t s_ticket, s_k, s_cnt;
+    __shared__ bool last_block;
+    const uint32_t total = d.ctl->n_scan_tiles;
+    const uint32_t nt = d.ctl->n_touched;
+    const uint32_t ppc = d.ppc;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            uint32_t tk = atomicAdd(&d.ctl->fin_ticket, 1u);
+            s_ticket = tk;
+            s_k = tk < total ? find_gen_of_ticket(d, nt, tk) : 0;
+            s_cnt = 0;
+        }
         __syncthreads();
-        uint32_t cnt = 0;
-        for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
-            uint64_t e = base + c;
+        const uint32_t ticket = s_ticket;
+        if (ticket >= total) break;
+        const uint32_t k = s_k;
+        const uint32_t g = d.touched[k];
+        GenState* G = &d.gen[g];
+        const uint32_t lo = G->lo_batch, hi = G->n_init;
+        const uint32_t ti = ticket - d.plan_base[k];
+        const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
+        const uint64_t base = G->chunk_base;
+        uint32_t done = 0;
+        if (c < hi) {
+            const uint64_t e = base + c;
             uint32_t fl = d.c_flags[e];
             if (!(fl & CF_COMPLETE)) {
-                uint32_t exp = pkts_of(d, chunk_len_of(d, G->len, c));
-                uint32_t seen = d.c_seen[e];
-                uint32_t lastf = 0;
-                for (uint32_t s = 0; s < exp; ++s) {
-                    uint32_t* fp = &d.c_first[e * d.ppc + s];
-                    uint32_t f = *fp;
-                    if (f == kInf) continue;
-                    seen |= 1u << s;
-                    lastf = lastf > f ? lastf : f;
-                    uint8_t pf = hdrs[f - 1].flags;
-                    if (pf & CN_PKT_ECN) fl |= CF_ECN;
-                    if (pf & CN_PKT_RTX) fl |= CF_RTX;
-                    *fp = kInf;
+                d.c_seen[e] |= d.c_newb[e];
+                const uint32_t lf = d.c_last[e];
+                if (lf) {
+                    d.c_txt[e] = hdrs[lf - 1].tx_time;
+                    d.c_path[e] = hdrs[lf - 1].path_id;
                 }
-                d.c_seen[e] = seen;
-                if (lastf) {
-                    d.c_txt[e] = hdrs[lastf - 1].tx_time;
-                    d.c_path[e] = hdrs[lastf - 1].path_id;
-                }
+                fl |= d.c_newfl[e];
                 if (d.c_cpl[e] != kInf) fl |= CF_COMPLETE;
+                d.c_newb[e] = 0;
+                d.c_last[e] = 0;
+                d.c_newfl[e] = 0;
+                for (uint32_t s = 0; s < ppc; ++s) d.c_first[e * ppc + s] = kInf;
             }
             if (d.c_init[e] != kInf) {
                 fl |= CF_INIT;
                 d.c_init[e] = kInf;
             }
             d.c_flags[e] = fl;
-            if (d.c_pmax[e] != kInf) ++cnt;
+            done = d.c_pmax[e] != kInf;
             d.c_cpl[e] = kInf;
             d.c_pmax[e] = kInf;
         }
-        if (cnt) atomicAdd(&cnt_s, cnt);
+        done = __reduce_add_sync(0xffffffffu, done);
+        if ((threadIdx.x & 31) == 0 && done) atomicAdd(&s_cnt, done);
         __syncthreads();
         if (threadIdx.x == 0) {
-            G->cum = lo + cnt_s;
-            if (G->deliver_t != kInf) {
-                atomicMax(&d.rc_done[G->rc * 128 + G->msg_id],
-                          static_cast<unsigned long long>(G->seq));
-                d.gen_key[g] = kTomb;
+            const uint32_t ntiles = (hi - lo + kScanThreads - 1) / kScanThreads;
+            if (s_cnt) atomicAdd(&G->cum_add, s_cnt);
+            __threadfence();
+            if (atomicAdd(&G->tiles_done, 1u) == ntiles - 1) {
+                __threadfence();
+                G->cum = lo + atomicAdd(&G->cum_add, 0u);
+                if (G->deliver_t != kInf) {
+                    atomicMax(&d.rc_done[G->rc * 128 + G->msg_id],
+                              static_cast<unsigned long long>(G->seq));
+                    d.gen_key[g] = kTomb;
+                }
             }
         }
         __syncthreads();
     }
+    // ---- batch epilogue (last block)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last_block = atomicAdd(&d.ctl->fin_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last_block && threadIdx.x == 0) {
+        RxCtl* C = d.ctl;
+        res->n_acks = C->n_acks;
+        res->n_completions = C->n_cpls;
+        res->status = C->status;
+        res->n_copied = C->n_copied;
+        res->bytes_copied = C->bytes_copied;
+        C->pool_snap = C->pool_top;
+        C->n_touched = 0;
+        C->tile_ticket = 0;
+        C->fin_done = 0;
+        C->status = 0;
+        C->n_copied = 0;
+        C->bytes_copied = 0;
+        C->n_acks = 0;
+        C->n_cpls = 0;
+        C->scan_ticket = 0;
+        C->fin_ticket = 0;
+        C->n_scan_tiles = 0;
+        uint32_t ep = C->epoch + 1;
+        C->epoch = ep ? ep : 1;
+    }
 }
 
-// ------------------------------------------------------------------ reset
+// -------------------------------------------------------------------- reset
 __global__ void k_reset(RxDev d, int full) {
     uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -693,8 +903,10 @@ __global__ void k_reset(RxDev d, int full) {
     for (uint64_t x = tid; x < ngen; x += stride) {
         d.gen_key[x] = kEmpty;
         d.gen[x].epoch = 0;
+        d.gen[x].ready = 0;
+        d.gen[x].touch = 0;
     }
-    uint64_t top = full ? d.pool_cap : d.ctl->pool_top;
+    uint64_t top = full ? d.pool_cap : d.ctl->pool_snap;
     if (top > d.pool_cap) top = d.pool_cap;
     for (uint64_t x = tid; x < top; x += stride) {
         d.c_seen[x] = 0;
@@ -704,50 +916,45 @@ __global__ void k_reset(RxDev d, int full) {
         d.c_init[x] = kInf;
         d.c_cpl[x] = kInf;
         d.c_pmax[x] = kInf;
+        d.c_newb[x] = 0;
+        d.c_last[x] = 0;
+        d.c_newfl[x] = 0;
     }
     for (uint64_t x = tid; x < top * d.ppc; x += stride) d.c_first[x] = kInf;
+    if (tid == 0) {
+        d.ctl->pool_top = 0;
+        d.ctl->arena_top = 0;
+    }
 }
 
-__global__ void k_reset_ctl(RxDev d) {
-    d.ctl->pool_top = 0;
-    d.ctl->arena_top = 0;
-    d.ctl->n_touched = 0;
-}
-
-__global__ void k_begin(RxDev d, cn_rx_result* res) {
-    d.ctl->n_touched = 0;
-    res->n_acks = 0;
-    res->n_completions = 0;
-    res->status = 0;
-    res->n_copied = 0;
-    res->bytes_copied = 0;
+__global__ void k_ctl_init(RxDev d) {
+    memset(d.ctl, 0, sizeof(RxCtl));
+    d.ctl->epoch = 1;
 }
 
 }  // namespace cnb
 
 using namespace cnb;
 
-#include <vector>
-
-constexpr int kRxKernels = 9;  // begin classify alloc mark scan decide tilescan work finalize
-static const char* kRxKernelNames[kRxKernels] = {"begin", "classify", "alloc", "mark", "scan",
-                                                 "decide", "tilescan", "work", "finalize"};
+constexpr int kRxKernels = 5;
+static const char* kRxKernelNames[kRxKernels] = {"ingest", "copy", "scan", "acks", "finalize"};
 
 struct cn_rx {
     cn_rx_config cfg;
     RxDev d;
-    uint32_t epoch = 0;
     uint32_t max_tiles = 0;
     int launches = 0;
     int sms = 148;
     // optional per-kernel timing with CUDA events on the launch stream
     bool profiling = false;
-    std::vector<std::vector<cudaEvent_t>> pending, spare;
+    cudaStream_t side = nullptr;           // k_copy overlaps the ack machinery
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::vector<std::vector<cudaEvent_t>> pending;
     double acc_ms[kRxKernels] = {0};
     uint64_t acc_n = 0;
 };
 
-static void prof_mark(cn_rx* rx, std::vector<cudaEvent_t>* ev, cudaStream_t s) {
+static void prof_mark(std::vector<cudaEvent_t>* ev, cudaStream_t s) {
     if (!ev) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -775,8 +982,9 @@ extern "C" void cn_rx_config_default(cn_rx_config* cfg) {
 static void rx_free(cn_rx* rx) {
     RxDev& d = rx->d;
     void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen, d.touched, d.c_first, d.c_seen,
-                    d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.p_gen,
-                    d.p_pos, d.p_cls, d.tile_cnt, d.tile_off, d.ctl, d.arena};
+                    d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
+                    d.c_last, d.c_newfl, d.p_gen,
+                    d.tile_state, d.scan_state, d.plan_base, d.ctl, d.arena};
     for (void* p : ptrs)
         if (p) cudaFree(p);
 }
@@ -801,6 +1009,7 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
         return CN_E_INVALID;
     }
     if (cfg.max_batch == 0 || cfg.max_batch > (1u << 28) || cfg.max_conns == 0 ||
+        cfg.max_conns > (1u << 20) ||
         cfg.max_msgs == 0 || cfg.chunk_pool == 0) {
         set_error("cn_rx_create: bad capacity");
         return CN_E_INVALID;
@@ -820,18 +1029,18 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     d.pool_cap = cfg.chunk_pool;
     d.arena_cap = cfg.carry_payload ? cfg.arena_bytes : 0;
     uint64_t B = cfg.max_batch;
-    rx->max_tiles = static_cast<uint32_t>((B + kTile - 1) / kTile);
+    rx->max_tiles = static_cast<uint32_t>((B + kAckTile - 1) / kAckTile);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&rx->sms, cudaDevAttrMultiProcessorCount, dev);
-#define ALLOC(ptr, bytes)                                         \
-    do {                                                          \
-        cudaError_t e_ = cudaMalloc(&(ptr), (bytes));             \
-        if (e_ != cudaSuccess) {                                  \
-            rx_free(rx);                                          \
-            delete rx;                                            \
+#define ALLOC(ptr, bytes)                                             \
+    do {                                                              \
+        cudaError_t e_ = cudaMalloc(&(ptr), (bytes));                 \
+        if (e_ != cudaSuccess) {                                      \
+            rx_free(rx);                                              \
+            delete rx;                                                \
             return cuda_status(e_, "cn_rx_create: cudaMalloc " #ptr); \
-        }                                                         \
+        }                                                             \
     } while (0)
     ALLOC(d.rc_key, nconn * 8ull);
     ALLOC(d.rc_done, nconn * 128ull * 8);
@@ -846,17 +1055,22 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.c_init, cfg.chunk_pool * 4);
     ALLOC(d.c_cpl, cfg.chunk_pool * 4);
     ALLOC(d.c_pmax, cfg.chunk_pool * 4);
+    ALLOC(d.c_newb, cfg.chunk_pool * 4);
+    ALLOC(d.c_last, cfg.chunk_pool * 4);
+    ALLOC(d.c_newfl, cfg.chunk_pool * 4);
     ALLOC(d.p_gen, B * 4);
-    ALLOC(d.p_pos, B * 4);
-    ALLOC(d.p_cls, B);
-    ALLOC(d.tile_cnt, rx->max_tiles * 8ull);
-    ALLOC(d.tile_off, rx->max_tiles * 8ull);
+    ALLOC(d.tile_state, rx->max_tiles * 8ull);
+    ALLOC(d.scan_state, (cfg.chunk_pool / kScanThreads + ngen + 2) * 8ull);
+    ALLOC(d.plan_base, ngen * 4ull);
     ALLOC(d.ctl, sizeof(RxCtl));
     if (d.carry) ALLOC(d.arena, cfg.arena_bytes);
 #undef ALLOC
+    cudaStreamCreateWithFlags(&rx->side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&rx->ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&rx->ev_join, cudaEventDisableTiming);
     cudaMemset(d.gen, 0, ngen * sizeof(GenState));
+    k_ctl_init<<<1, 1>>>(d);
     k_reset<<<rx->sms * 4, 256>>>(d, 1);
-    k_reset_ctl<<<1, 1>>>(d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         rx_free(rx);
@@ -870,6 +1084,11 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
 extern "C" void cn_rx_destroy(cn_rx* rx) {
     if (!rx) return;
     cudaDeviceSynchronize();
+    for (auto& ev : rx->pending)
+        for (auto e : ev) cudaEventDestroy(e);
+    if (rx->side) cudaStreamDestroy(rx->side);
+    if (rx->ev_fork) cudaEventDestroy(rx->ev_fork);
+    if (rx->ev_join) cudaEventDestroy(rx->ev_join);
     rx_free(rx);
     delete rx;
 }
@@ -881,7 +1100,6 @@ extern "C" int cn_rx_reset(cn_rx* rx, void* stream) {
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     k_reset<<<rx->sms * 4, 256, 0, s>>>(rx->d, 0);
-    k_reset_ctl<<<1, 1, 0, s>>>(rx->d);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }
@@ -911,41 +1129,42 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const RxDev& d = rx->d;
-    ++rx->epoch;
-    if (rx->epoch == 0) rx->epoch = 1;
     std::vector<cudaEvent_t>* ev = nullptr;
     if (rx->profiling && n > 0) {
         rx->pending.emplace_back();
         ev = &rx->pending.back();
     }
-    prof_mark(rx, ev, s);
-    k_begin<<<1, 1, 0, s>>>(d, d_result);
-    prof_mark(rx, ev, s);
-    rx->launches = 1;
+    // chunk-tile kernels: persistent grids pulling 256-chunk tiles by ticket
+    uint32_t gb = 2u * static_cast<uint32_t>(rx->sms);
+    prof_mark(ev, s);
     if (n > 0) {
-        uint32_t pb = (n + 255) / 256;
-        uint32_t gb = n < 2u * rx->sms ? n : 2u * rx->sms;
-        uint32_t tiles = (n + kTile - 1) / kTile;
         const uint8_t* pl = static_cast<const uint8_t*>(d_payload);
-        k_classify<<<pb, 256, 0, s>>>(d, d_hdrs, n, rx->epoch, d_result);
-        prof_mark(rx, ev, s);
-        k_alloc<<<(gb + 255) / 256, 256, 0, s>>>(d, d_result);
-        prof_mark(rx, ev, s);
-        k_mark<<<pb, 256, 0, s>>>(d, d_hdrs, n, d_result);
-        prof_mark(rx, ev, s);
-        k_scan<<<gb, 256, 0, s>>>(d);
-        prof_mark(rx, ev, s);
-        k_decide<<<tiles, kTile, 0, s>>>(d, d_hdrs, n, d_result);
-        prof_mark(rx, ev, s);
-        k_tilescan<<<1, 1024, 0, s>>>(d, tiles, max_acks, max_completions, d_result);
-        prof_mark(rx, ev, s);
-        k_work<<<(n + 7) / 8, 256, 0, s>>>(d, d_hdrs, pl, payload_stride, n, d_acks, max_acks,
-                                           d_completions, max_completions, d_result);
-        prof_mark(rx, ev, s);
-        k_finalize<<<gb, 256, 0, s>>>(d, d_hdrs);
-        prof_mark(rx, ev, s);
-        rx->launches += 8;
+        uint32_t tiles = (n + kAckTile - 1) / kAckTile;
+        uint32_t cw = (n + 7) / 8;  // 8 warps (packets) per copy block
+        uint32_t cmax = static_cast<uint32_t>(rx->sms) * 8;
+        k_ingest<<<(n + 255) / 256, 256, 0, s>>>(d, d_hdrs, n);
+        prof_mark(ev, s);
+        // fork: the HBM-bound scatter runs beside the latency-bound ack path
+        cudaStream_t cs = ev ? s : rx->side;
+        if (!ev) {
+            CNB_CUDA(cudaEventRecord(rx->ev_fork, s));
+            CNB_CUDA(cudaStreamWaitEvent(cs, rx->ev_fork, 0));
+        }
+        k_copy<<<cw < cmax ? cw : cmax, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+        prof_mark(ev, s);
+        k_scan<<<gb, kScanThreads, 0, s>>>(d);
+        prof_mark(ev, s);
+        k_acks<<<tiles, kAckWarps * 32, 0, s>>>(d, d_hdrs, n, d_acks, max_acks, d_completions,
+                                               max_completions);
+        prof_mark(ev, s);
+        if (!ev) {
+            CNB_CUDA(cudaEventRecord(rx->ev_join, cs));
+            CNB_CUDA(cudaStreamWaitEvent(s, rx->ev_join, 0));
+        }
     }
+    k_finalize<<<gb, kScanThreads, 0, s>>>(d, d_hdrs, d_result);
+    prof_mark(ev, s);
+    rx->launches = n > 0 ? 5 : 1;
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }
@@ -962,7 +1181,7 @@ extern "C" int cn_rx_profile(cn_rx* rx, double* ms, int max, uint64_t* batches, 
     if (!rx) return CN_E_INVALID;
     for (auto& ev : rx->pending) {
         cudaEventSynchronize(ev.back());
-        for (size_t k = 0; k + 1 < ev.size() && k < (size_t)kRxKernels; ++k) {
+        for (size_t k = 0; k + 1 < ev.size() && k < static_cast<size_t>(kRxKernels); ++k) {
             float t = 0;
             cudaEventElapsedTime(&t, ev[k], ev[k + 1]);
             rx->acc_ms[k] += t;

@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sched", action="store_true")
     return ap.parse_args()
 
 
@@ -140,6 +141,43 @@ def cpu_reference(data, n_hosts, chunk_bytes, seconds, threads=None):
     return {"value": round(reps * msg / t / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{reps} single-thread oracle replays, {t:.2f} s",
             "mpkts_per_s": round(reps * len(data) / t / 1e6, 3)}
+
+
+def sched_bench(dev, steps=20, conns=1024, paths=256, per_call=4096):
+    """S1-S4 rows: batched select_path (p2_rtt) for `conns` connections x
+    `paths` paths, `per_call` decisions per connection per call."""
+    import torch
+
+    import paper_2504_17307_b200 as cn
+    s = cn.PathScheduler(conns, paths, 1, base_rtt_ns=10000.0, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    s.rtt_scores()[:] = 10000.0 + torch.randint(0, 5000, (conns, paths), device=dev,
+                                                generator=g).double()
+    out = torch.empty((conns, per_call), dtype=torch.int32, device=dev)
+    for _ in range(3):
+        s.select("p2_rtt", per_call, out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        s.select("p2_rtt", per_call, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    r = {"decisions_per_s": round(conns * per_call * steps / (ms * 1e-3), 1),
+         "config": f"{conns} connections x {paths} paths, p2_rtt, {per_call} decisions/conn/call",
+         "ms_per_call": round(ms / steps, 4)}
+    try:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            t, _ = ref.select_paths_bench("p2_rtt", paths, conns, 2000, threads)
+            r["cpu_reference_decisions_per_s"] = round(conns * 2000 / t, 1)
+            r["cpu_threads"] = threads
+    except Exception as e:  # noqa: BLE001
+        r["cpu_reference_error"] = str(e)
+    return r
 
 
 def run_reference(args):
@@ -337,6 +375,8 @@ def main():
                "d2h_bytes_per_step": int(n_acks * ACK + 24),
                "path": "pinned host records+staging -> cn_rx_batch (C ABI) -> acks to host"}
 
+    sched = sched_bench(dev) if not args.no_sched else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference(data, meta["n_hosts"], cb, args.cpu_seconds)
@@ -366,6 +406,8 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+        if sched:
+            line["scheduler"] = sched
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

@@ -195,6 +195,48 @@ int cn_rx_set_profiling(cn_rx* rx, int enable);
 int cn_rx_profile(cn_rx* rx, double* ms, int max, uint64_t* batches, int reset);
 const char* cn_rx_kernel_name(int k);
 
+/* ------------------------------------------------------------ scheduler
+ * Batched multipath chunk scheduler: per-connection RngStream
+ * (include/chunknet/rng.hpp:29-60; std::mt19937_64 + libstdc++ 13
+ * uniform_int_distribution), PathScoreboard (lb.hpp:15-36) and
+ * select_path (src/lb.cpp:7-27) / DefaultPolicy's on_select_path and
+ * on_tx_rtx_chunk (policy.hpp:80-91), one warp per connection.
+ * Path choices are bit-identical to the sequential reference. */
+#define CN_LB_OBLIVIOUS 0 /* LbPolicy::oblivious (lb.hpp:39) */
+#define CN_LB_P2_RTT 1    /* LbPolicy::p2_rtt                */
+#define CN_LB_P2_ECN 2    /* LbPolicy::p2_ecn                */
+typedef struct cn_sched cn_sched;
+
+/* n_conns streams RngStream(seed, stream_name, index0 + c) -- the
+ * reference's per-connection stream is ("transport.conn", conn idx),
+ * transport.cpp:101; index0 < 0 = unindexed RngStream(seed, name).
+ * Boards start at PathScoreboard(n_paths[c], base_rtt_ns). */
+int cn_sched_create(uint32_t n_conns, uint32_t max_paths, const int32_t* h_n_paths,
+                    double base_rtt_ns, uint64_t seed, const char* stream_name,
+                    int64_t index0, cn_sched** out);
+void cn_sched_destroy(cn_sched* s);
+/* Device pointers to the [n_conns][max_paths] rtt / ecn score boards;
+ * returns max_paths. */
+int cn_sched_boards(cn_sched* s, double** d_rtt, double** d_ecn);
+/* Path decisions, in order, for n_groups connections: group g is
+ * connection d_conns[g] (NULL = g) with decisions
+ * [d_offsets[g], d_offsets[g+1]) (NULL = uniform_count each, packed).
+ * d_prev_paths[k] >= 0 marks a retransmission whose previous path is
+ * avoided when rtx_avoid_prev_path (DefaultPolicy::on_tx_rtx_chunk);
+ * -1 / NULL = fresh chunk (on_select_path).  A connection may appear in
+ * at most one group per call. */
+int cn_sched_select(cn_sched* s, int policy, int rtx_avoid_prev_path, const uint32_t* d_conns,
+                    const uint32_t* d_offsets, const int32_t* d_prev_paths, uint32_t n_groups,
+                    uint32_t uniform_count, int32_t* d_out, void* stream);
+/* Raw RngStream outputs (d_ns == NULL: next_u64, else next_below(d_ns[i])). */
+int cn_sched_draws(cn_sched* s, uint32_t conn, const uint64_t* d_ns, uint64_t count,
+                   uint64_t* d_out, void* stream);
+/* PathScoreboard::record_rtt + record_ecn for samples grouped per
+ * connection (group g = samples [d_offsets[g], d_offsets[g+1]), applied in
+ * order), as release_chunk does for RTT-sampled acks (transport.cpp:819-822). */
+int cn_sched_record(cn_sched* s, const uint32_t* d_conn, const int32_t* d_path, const int64_t* d_rtt,
+                    const uint8_t* d_ecn, const uint32_t* d_offsets, uint32_t n_groups, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

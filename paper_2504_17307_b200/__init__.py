@@ -6,6 +6,7 @@ the C ABI in include/chunknet_b200.h).  This package is the host-side
 mirror of the reference's Transport interface; it has no CPU fallback.
 """
 from ._lib import ChunknetError, lib  # noqa: F401
+from .scheduler import PathScheduler  # noqa: F401
 from .transport import (MAX_PAYLOAD, RxBatch, Stats, Transport, TransportConfig,  # noqa: F401
                         csn_before, decode_header, encode_header, to_device_records)
 

@@ -74,6 +74,14 @@ def lib():
                                 ctypes.POINTER(u64), i32]
     L.cn_rx_kernel_name.restype = ctypes.c_char_p
     L.cn_rx_kernel_name.argtypes = [i32]
+    L.cn_sched_create.argtypes = [u32, u32, vp, ctypes.c_double, u64, ctypes.c_char_p,
+                                  ctypes.c_int64, ctypes.POINTER(vp)]
+    L.cn_sched_destroy.argtypes = [vp]
+    L.cn_sched_destroy.restype = None
+    L.cn_sched_boards.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    L.cn_sched_select.argtypes = [vp, i32, i32, vp, vp, vp, u32, u32, vp, vp]
+    L.cn_sched_draws.argtypes = [vp, u32, vp, u64, vp, vp]
+    L.cn_sched_record.argtypes = [vp, vp, vp, vp, vp, vp, u32, vp]
     _lib = L
     return L
 

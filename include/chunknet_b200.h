@@ -125,7 +125,7 @@ typedef struct cn_completion {
     uint32_t msg_id;
     uint64_t buf_offset;  /* byte offset of the message in the rx arena */
     uint64_t bytes;       /* MsgRecv::bytes: payload bytes accepted */
-    uint64_t reserved;
+    uint64_t reserved;    /* absolute device pointer of the message buffer */
 } cn_completion;
 
 /* ------------------------------------------------------------- receiver
@@ -150,7 +150,16 @@ typedef struct cn_rx_config {
     uint64_t arena_bytes;    /* device bytes for reassembled message buffers    */
     uint32_t max_batch;      /* max packets per cn_rx_batch                     */
     int32_t carry_payload;   /* TransportConfig::carry_payload                  */
+    int32_t reduce_op;       /* CN_REDUCE_*: fuse the scatter with a ring
+                                reduction step            */
+    uint32_t max_posts;      /* capacity of posted destinations (cn_rx_post)    */
 } cn_rx_config;
+
+/* Reduce modes of the payload scatter: dst = dst + payload elementwise,
+ * each element once (fp32; bf16 with fp32 add + round-to-nearest-even). */
+#define CN_REDUCE_NONE 0
+#define CN_REDUCE_SUM_F32 1
+#define CN_REDUCE_SUM_BF16 2
 
 typedef struct cn_rx cn_rx;
 
@@ -176,7 +185,10 @@ typedef struct cn_rx_result {
 #define CN_RXF_GENERATION 0x8u   /* msg id reused before completion */
 
 /* Process n data packets (arrival order).  d_payload + i*payload_stride
- * holds packet i's payload_len bytes.  ACK records are appended in emission
+ * holds packet i's payload_len bytes; payload_stride == 0 means zero-copy
+ * source addressing: packet i's payload is at d_payload + chunk_offset +
+ * seq_in_chunk*max_payload (the sender's message buffer, e.g. a peer GPU's
+ * memory over NVLink).  ACK records are appended in emission
  * order to d_acks (max_acks), completions to d_completions.  Asynchronous
  * on `stream`; d_result is written when the batch finishes. */
 int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
@@ -184,6 +196,12 @@ int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
                 uint32_t max_acks, cn_completion* d_completions,
                 uint32_t max_completions, cn_rx_result* d_result,
                 void* stream);
+/* Post a destination buffer for the message with caller tag `tag` (the
+ * reference's per-message tag, transport.hpp:88-91): its payload is
+ * scattered (or reduced, CN_REDUCE_*) into d_buf instead of the arena.
+ * Posts persist across batches and resets; the completion's `reserved` field
+ * carries the absolute destination pointer.  Asynchronous on `stream`. */
+int cn_rx_post(cn_rx* rx, uint64_t tag, void* d_buf, uint64_t len, void* stream);
 /* Device base pointer of the reassembly arena (cn_completion::buf_offset). */
 void* cn_rx_arena(cn_rx* rx);
 /* Number of kernel launches the last cn_rx_batch issued. */

@@ -44,7 +44,8 @@
 namespace cnb {
 
 struct GenState {
-    uint64_t len, tag, seq, chunk_base, buf_off;
+    uint64_t len, tag, seq, chunk_base, buf_off;  // buf_off: arena offset, ~0 if posted
+    uint8_t* buf;                                  // absolute destination of the message
     unsigned long long touch;  // (epoch << 32) | (max chunk touched + 1) in that epoch
     uint32_t nchunks, cum, n_init, rc, msg_id, epoch, deliver_t, ready;
     uint32_t lo_batch, tiles_done, cum_add, pad;
@@ -67,7 +68,10 @@ constexpr int kCopyUnroll = 8;       // 16-byte vectors in flight per lane
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 
 struct RxDev {
-    uint32_t cb, max_pl, ppc, conn_mask, gen_mask, carry;
+    uint32_t cb, max_pl, ppc, conn_mask, gen_mask, carry, reduce, elem, post_mask;
+    unsigned long long* post_key;  // [posts] message tag (posted destinations)
+    unsigned long long* post_val;  // [posts] device pointer
+    unsigned long long* post_len;  // [posts] bytes
     uint64_t pool_cap, arena_cap;
     unsigned long long* rc_key;
     unsigned long long* rc_done;  // [conns*128] completed_seq (transport.hpp:223)
@@ -174,17 +178,35 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
                     base = atomicAdd(&d.ctl->pool_top, static_cast<unsigned long long>(nc));
                     if (base + nc > d.pool_cap) st = CN_RXF_CAPACITY;
                 }
-                if (!st && d.carry) {
+                uint8_t* buf = nullptr;
+                if (!st && d.carry && d.post_mask) {  // a posted destination (cn_rx_post)
+                    uint32_t hp = static_cast<uint32_t>(mix64(h.msg_tag)) & d.post_mask;
+                    for (uint32_t q = 0; q <= d.post_mask; ++q) {
+                        unsigned long long k = __ldcg(&d.post_key[hp]);
+                        if (k == kEmpty) break;
+                        if (k == h.msg_tag) {
+                            if (__ldcg(&d.post_len[hp]) >= h.msg_len)
+                                buf = reinterpret_cast<uint8_t*>(__ldcg(&d.post_val[hp]));
+                            break;
+                        }
+                        hp = (hp + 1) & d.post_mask;
+                    }
+                    if (buf) boff = ~0ull;
+                }
+                if (!st && d.carry && !buf) {
                     unsigned long long need = (h.msg_len + 15) & ~15ull;
                     boff = atomicAdd(&d.ctl->arena_top, need);
                     if (boff + need > d.arena_cap) st = CN_RXF_CAPACITY;
+                    buf = d.arena + boff;
                 }
+                if (!st && d.reduce && (h.msg_len % d.elem)) st = CN_RXF_UNSUPPORTED;
                 status |= st;
                 G->len = h.msg_len;
                 G->tag = h.msg_tag;
                 G->seq = h.msg_seq;
                 G->chunk_base = st ? 0 : base;
                 G->buf_off = boff;
+                G->buf = buf;
                 G->touch = 0;
                 G->nchunks = st ? 0 : static_cast<uint32_t>(nc);
                 G->cum = 0;
@@ -233,7 +255,8 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
             uint32_t pl = clen - s * d.max_pl;
             pl = pl < d.max_pl ? pl : d.max_pl;
             bad = ((h.hdr >> 9) & 0xFF) != (c & 0xFF) || h.chunk_len != clen || s >= exp ||
-                  h.payload_len != pl || ((h.hdr >> 8) & 1) != (c + 1 == nch ? 1u : 0u);
+                  h.payload_len != pl || ((h.hdr >> 8) & 1) != (c + 1 == nch ? 1u : 0u) ||
+                  (d.reduce && ((h.chunk_offset | pl) % d.elem));
         }
         if (bad) {
             status |= CN_RXF_UNSUPPORTED;
@@ -263,7 +286,8 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
     // [cum, hi) and its first scan tile; hi = the chunk vector size (:637)
     __shared__ bool s_last;
     __shared__ uint32_t s_wsum[8], s_carry;
-    __threadfence();
+    __threadfence();  // every thread's table/list writes ...
+    __syncthreads();  // ... are done before the block reports in
     if (threadIdx.x == 0) s_last = atomicAdd(&d.ctl->ingest_done, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
@@ -456,31 +480,106 @@ __device__ __forceinline__ uint32_t pmax_at(const RxDev& d, const GenState& G, u
 // one warp per packet, 16-byte vectors, all loads of a packet in flight
 // before its stores.  The decision needs only the batch's first[] (final
 // after k_ingest), so this kernel does not wait for the ack machinery.
-__device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
-                                          uint32_t len, int lane) {
+//
+// Reduce mode: the scatter is fused
+// with the ring reduction step -- dst = dst + payload elementwise (fp32, or
+// bf16 with an fp32 add rounded to nearest even), each element exactly
+// once, so the result is independent of arrival order.
+// Source addressing: payload + i*stride (arrival-order staging), or with
+// stride 0 payload + message offset (zero-copy from the sender's message
+// buffer, e.g. a peer GPU's memory over NVLink).
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t bf16_rne(float f) {
+    uint32_t u = __float_as_uint(f);
+    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x7fffffu)) return (u >> 16) | 0x40u;  // quiet NaN
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return u >> 16;
+}
+__device__ __forceinline__ uint32_t add_bf16x2(uint32_t a, uint32_t b) {
+    uint32_t lo = bf16_rne(__fadd_rn(bf16_lo(a), bf16_lo(b)));
+    uint32_t hi = bf16_rne(__fadd_rn(bf16_hi(a), bf16_hi(b)));
+    return lo | (hi << 16);
+}
+template <int R>
+__device__ __forceinline__ int4 combine(int4 dst, int4 src) {
+    if (R == 1) {
+        float4 a = *reinterpret_cast<float4*>(&dst), b = *reinterpret_cast<float4*>(&src), c;
+        c.x = __fadd_rn(a.x, b.x);
+        c.y = __fadd_rn(a.y, b.y);
+        c.z = __fadd_rn(a.z, b.z);
+        c.w = __fadd_rn(a.w, b.w);
+        return *reinterpret_cast<int4*>(&c);
+    } else {
+        int4 c;
+        c.x = static_cast<int>(add_bf16x2(dst.x, src.x));
+        c.y = static_cast<int>(add_bf16x2(dst.y, src.y));
+        c.z = static_cast<int>(add_bf16x2(dst.z, src.z));
+        c.w = static_cast<int>(add_bf16x2(dst.w, src.w));
+        return c;
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void warp_scatter(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                             uint32_t len, int lane) {
     if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
         const int4* s4 = reinterpret_cast<const int4*>(src);
         int4* d4 = reinterpret_cast<int4*>(dst);
         const uint32_t nv = len >> 4;
         for (uint32_t v0 = 0; v0 < nv; v0 += 32 * kCopyUnroll) {
             int4 r[kCopyUnroll];
+            int4 a[R ? kCopyUnroll : 1];
 #pragma unroll
             for (int k = 0; k < kCopyUnroll; ++k) {
                 uint32_t v = v0 + k * 32 + lane;
-                if (v < nv) r[k] = __ldcs(s4 + v);
+                if (v < nv) {
+                    r[k] = __ldcs(s4 + v);
+                    if (R) a[R ? k : 0] = d4[v];
+                }
             }
 #pragma unroll
             for (int k = 0; k < kCopyUnroll; ++k) {
                 uint32_t v = v0 + k * 32 + lane;
-                if (v < nv) d4[v] = r[k];
+                if (v < nv) d4[v] = R ? combine<R ? R : 1>(a[R ? k : 0], r[k]) : r[k];
             }
         }
-        for (uint32_t b = (nv << 4) + lane; b < len; b += 32) dst[b] = src[b];
-    } else {
+        const uint32_t tail = nv << 4;
+        if (R == 0) {
+            for (uint32_t b = tail + lane; b < len; b += 32) dst[b] = src[b];
+        } else if (R == 1) {  // 4-byte aligned tail
+            for (uint32_t b = tail + 4 * lane; b + 4 <= len; b += 128)
+                *reinterpret_cast<float*>(dst + b) =
+                    __fadd_rn(*reinterpret_cast<float*>(dst + b), *reinterpret_cast<const float*>(src + b));
+        } else {
+            for (uint32_t b = tail + 2 * lane; b + 2 <= len; b += 64) {
+                uint16_t x = *reinterpret_cast<uint16_t*>(dst + b), y = *reinterpret_cast<const uint16_t*>(src + b);
+                *reinterpret_cast<uint16_t*>(dst + b) =
+                    static_cast<uint16_t>(bf16_rne(__fadd_rn(bf16_lo(x), bf16_lo(y))));
+            }
+        }
+    } else if (R == 0) {
         for (uint32_t b = lane; b < len; b += 32) dst[b] = src[b];
+    } else if (R == 1) {
+        for (uint32_t b = 4 * lane; b + 4 <= len; b += 128) {
+            float x, y;
+            memcpy(&x, dst + b, 4);
+            memcpy(&y, src + b, 4);
+            x = __fadd_rn(x, y);
+            memcpy(dst + b, &x, 4);
+        }
+    } else {
+        for (uint32_t b = 2 * lane; b + 2 <= len; b += 64) {
+            uint16_t x, y;
+            memcpy(&x, dst + b, 2);
+            memcpy(&y, src + b, 2);
+            uint16_t z = static_cast<uint16_t>(bf16_rne(__fadd_rn(bf16_lo(x), bf16_lo(y))));
+            memcpy(dst + b, &z, 2);
+        }
     }
 }
 
+template <int R>
 __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                               const uint8_t* __restrict__ payload, uint64_t stride,
                                               uint32_t n) {
@@ -507,9 +606,11 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
         if (!fresh) continue;
         ++my_cnt;
         my_bytes += len;
-        if (d.carry)
-            warp_copy(d.arena + G->buf_off + off + static_cast<uint64_t>(s) * d.max_pl,
-                      payload + static_cast<uint64_t>(i) * stride, len, lane);
+        if (d.carry) {
+            const uint64_t moff = off + static_cast<uint64_t>(s) * d.max_pl;
+            const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
+            warp_scatter<R>(G->buf + moff, src, len, lane);
+        }
     }
     if (lane == 0 && my_cnt) {
         atomicAdd(&s_cnt, my_cnt);
@@ -780,6 +881,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
                 c.pkt_index = i;
                 c.msg_id = G.msg_id;
                 c.buf_offset = d.carry ? G.buf_off : ~0ull;
+                c.reserved = reinterpret_cast<uint64_t>(G.buf);  // absolute device pointer
                 c.bytes = G.len;  // every byte accepted exactly once
                 cpls[a] = c;
             }
@@ -949,6 +1051,7 @@ struct cn_rx {
     bool profiling = false;
     cudaStream_t side = nullptr;           // k_copy overlaps the ack machinery
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int* post_ok = nullptr;
     std::vector<std::vector<cudaEvent_t>> pending;
     double acc_ms[kRxKernels] = {0};
     uint64_t acc_n = 0;
@@ -977,6 +1080,8 @@ extern "C" void cn_rx_config_default(cn_rx_config* cfg) {
     cfg->arena_bytes = 1ull << 30;
     cfg->max_batch = 1u << 20;
     cfg->carry_payload = 1;
+    cfg->reduce_op = CN_REDUCE_NONE;
+    cfg->max_posts = 0;
 }
 
 static void rx_free(cn_rx* rx) {
@@ -984,7 +1089,8 @@ static void rx_free(cn_rx* rx) {
     void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen, d.touched, d.c_first, d.c_seen,
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
                     d.c_last, d.c_newfl, d.p_gen,
-                    d.tile_state, d.scan_state, d.plan_base, d.ctl, d.arena};
+                    d.tile_state, d.scan_state, d.plan_base, d.ctl, d.arena, d.post_key,
+                    d.post_val, d.post_len};
     for (void* p : ptrs)
         if (p) cudaFree(p);
 }
@@ -1023,6 +1129,15 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     d.max_pl = cfg.max_payload;
     d.ppc = ppc;
     d.carry = cfg.carry_payload ? 1 : 0;
+    d.reduce = static_cast<uint32_t>(cfg.reduce_op);
+    d.elem = cfg.reduce_op == CN_REDUCE_SUM_F32 ? 4 : (cfg.reduce_op == CN_REDUCE_SUM_BF16 ? 2 : 1);
+    if (cfg.reduce_op < 0 || cfg.reduce_op > 2 || (cfg.reduce_op && !cfg.carry_payload) ||
+        (cfg.reduce_op && (cfg.max_payload % d.elem))) {
+        delete rx;
+        set_error("cn_rx_create: reduce_op needs carry_payload and element-aligned packets");
+        return CN_E_INVALID;
+    }
+    if (cfg.max_posts) d.post_mask = pow2_at_least(2ull * cfg.max_posts) - 1;
     uint32_t nconn = pow2_at_least(cfg.max_conns), ngen = pow2_at_least(2ull * cfg.max_msgs);
     d.conn_mask = nconn - 1;
     d.gen_mask = ngen - 1;
@@ -1063,7 +1178,13 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.scan_state, (cfg.chunk_pool / kScanThreads + ngen + 2) * 8ull);
     ALLOC(d.plan_base, ngen * 4ull);
     ALLOC(d.ctl, sizeof(RxCtl));
-    if (d.carry) ALLOC(d.arena, cfg.arena_bytes);
+    if (d.carry && cfg.arena_bytes) ALLOC(d.arena, cfg.arena_bytes);
+    if (d.post_mask) {
+        ALLOC(d.post_key, (d.post_mask + 1ull) * 8);
+        ALLOC(d.post_val, (d.post_mask + 1ull) * 8);
+        ALLOC(d.post_len, (d.post_mask + 1ull) * 8);
+        cudaMemset(d.post_key, 0xFF, (d.post_mask + 1ull) * 8);
+    }
 #undef ALLOC
     cudaStreamCreateWithFlags(&rx->side, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&rx->ev_fork, cudaEventDisableTiming);
@@ -1087,6 +1208,7 @@ extern "C" void cn_rx_destroy(cn_rx* rx) {
     for (auto& ev : rx->pending)
         for (auto e : ev) cudaEventDestroy(e);
     if (rx->side) cudaStreamDestroy(rx->side);
+    if (rx->post_ok) cudaFree(rx->post_ok);
     if (rx->ev_fork) cudaEventDestroy(rx->ev_fork);
     if (rx->ev_join) cudaEventDestroy(rx->ev_join);
     rx_free(rx);
@@ -1123,8 +1245,8 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
         set_error("cn_rx_batch: null headers");
         return CN_E_INVALID;
     }
-    if (rx->d.carry && n > 0 && (!d_payload || payload_stride < rx->d.max_pl)) {
-        set_error("cn_rx_batch: carry_payload needs a payload staging buffer with stride >= max_payload");
+    if (rx->d.carry && n > 0 && (!d_payload || (payload_stride && payload_stride < rx->d.max_pl))) {
+        set_error("cn_rx_batch: carry_payload needs a payload buffer (stride 0 or >= max_payload)");
         return CN_E_INVALID;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1150,7 +1272,13 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
             CNB_CUDA(cudaEventRecord(rx->ev_fork, s));
             CNB_CUDA(cudaStreamWaitEvent(cs, rx->ev_fork, 0));
         }
-        k_copy<<<cw < cmax ? cw : cmax, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+        const uint32_t cg = cw < cmax ? cw : cmax;
+        if (d.reduce == 1)
+            k_copy<1><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+        else if (d.reduce == 2)
+            k_copy<2><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+        else
+            k_copy<0><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
         prof_mark(ev, s);
         k_scan<<<gb, kScanThreads, 0, s>>>(d);
         prof_mark(ev, s);
@@ -1165,6 +1293,37 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
     k_finalize<<<gb, kScanThreads, 0, s>>>(d, d_hdrs, d_result);
     prof_mark(ev, s);
     rx->launches = n > 0 ? 5 : 1;
+    CNB_CUDA(cudaGetLastError());
+    return CN_OK;
+}
+
+__global__ void k_post(RxDev d, uint64_t tag, uint64_t ptr, uint64_t len, int* ok) {
+    uint32_t h = static_cast<uint32_t>(mix64(tag)) & d.post_mask;
+    for (uint32_t q = 0; q <= d.post_mask; ++q) {
+        unsigned long long old = atomicCAS(&d.post_key[h], kEmpty, tag);
+        if (old == kEmpty || old == tag) {
+            d.post_val[h] = ptr;
+            d.post_len[h] = len;
+            *ok = 1;
+            return;
+        }
+        h = (h + 1) & d.post_mask;
+    }
+    *ok = 0;
+}
+
+extern "C" int cn_rx_post(cn_rx* rx, uint64_t tag, void* d_buf, uint64_t len, void* stream) {
+    if (!rx || !d_buf || !rx->d.post_mask || !rx->d.carry) {
+        set_error("cn_rx_post: needs carry_payload and max_posts > 0");
+        return CN_E_INVALID;
+    }
+    if (reinterpret_cast<uintptr_t>(d_buf) & 15) {
+        set_error("cn_rx_post: buffer must be 16-byte aligned");
+        return CN_E_INVALID;
+    }
+    if (!rx->post_ok) CNB_CUDA(cudaMalloc(&rx->post_ok, sizeof(int)));
+    k_post<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(rx->d, tag, reinterpret_cast<uint64_t>(d_buf),
+                                                           len, rx->post_ok);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }

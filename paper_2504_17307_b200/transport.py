@@ -71,8 +71,11 @@ class Transport:
     """Receive side of chunknet::Transport on one B200 (selective mode,
     fixed-size chunking as DefaultPolicy, policy.hpp:70-97)."""
 
+    REDUCE = {None: 0, "none": 0, "sum_f32": 1, "sum_bf16": 2}
+
     def __init__(self, cfg=None, seed=0, *, device="cuda", max_conns=1024, max_msgs=4096,
-                 chunk_pool=1 << 22, arena_bytes=1 << 30, max_batch=1 << 20):
+                 chunk_pool=1 << 22, arena_bytes=1 << 30, max_batch=1 << 20, reduce=None,
+                 max_posts=0):
         self.cfg = cfg or TransportConfig()
         if self.cfg.reliability != "selective":
             raise _lib.ChunknetError(-6, "device receive path implements selective mode")
@@ -93,6 +96,8 @@ class Transport:
         rc.arena_bytes = arena_bytes if self.cfg.carry_payload else 0
         rc.max_batch = max_batch
         rc.carry_payload = 1 if self.cfg.carry_payload else 0
+        rc.reduce_op = self.REDUCE[reduce]
+        rc.max_posts = max_posts
         self._rxcfg = rc
         with torch.cuda.device(self.device):
             h = ctypes.c_void_p()
@@ -150,6 +155,8 @@ class Transport:
         self._ensure(n)
         s = stream or torch.cuda.current_stream(self.device)
         pl = payload.data_ptr() if payload is not None else None
+        if payload is not None and stride == 0 and not self.cfg.carry_payload:
+            pl = None
         _lib.check(_lib.lib().cn_rx_batch(
             self._h, hdrs.data_ptr(), pl, stride, n, self._acks.data_ptr(), n + 16,
             self._cpls.data_ptr(), n + 16, self._result.data_ptr(),
@@ -186,6 +193,13 @@ class Transport:
                                   self._index_base + int(c["pkt_index"]), data)
         self._index_base += n
         return out
+
+    def post(self, tag, buf, stream=None):
+        """Scatter (or, in reduce mode, accumulate) the message with caller
+        tag `tag` into the device tensor `buf` instead of the arena."""
+        s = stream or torch.cuda.current_stream(self.device)
+        _lib.check(_lib.lib().cn_rx_post(self._h, tag, buf.data_ptr(), buf.numel() * buf.element_size(),
+                                          ctypes.c_void_p(s.cuda_stream)), "cn_rx_post")
 
     def set_profiling(self, enable=True):
         _lib.lib().cn_rx_set_profiling(self._h, 1 if enable else 0)

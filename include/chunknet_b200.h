@@ -255,6 +255,45 @@ int cn_sched_draws(cn_sched* s, uint32_t conn, const uint64_t* d_ns, uint64_t co
 int cn_sched_record(cn_sched* s, const uint32_t* d_conn, const int32_t* d_path, const int64_t* d_rtt,
                     const uint8_t* d_ecn, const uint32_t* d_offsets, uint32_t n_groups, void* stream);
 
+/* --------------------------------------------------------- send side
+ * Transport::send_chunk's packetization (transport.cpp:433-494) for all
+ * chunks of one message (DefaultPolicy chunking, policy.hpp:75-78): packet
+ * i of chunk c carries min(max_payload, chunk_len - i*max_payload) bytes at
+ * message offset c*chunk_bytes + i*max_payload; header {conn_id, msg_id,
+ * csn = c & 0xFF, last = (c == nchunks-1)}.  Records are written in chunk
+ * order (the order send_chunk injects them). */
+typedef struct cn_packetize_args {
+    uint64_t len;            /* message length (> 0; send_message throws on 0) */
+    uint32_t chunk_bytes;
+    uint32_t max_payload;    /* 0 = CN_MAX_PAYLOAD */
+    int32_t src, dst;
+    uint32_t conn_id, msg_id;
+    uint64_t msg_seq, tag;
+    int64_t tx_time;
+    const int32_t* d_chunk_paths; /* path per chunk (cn_sched_select), or NULL */
+    int32_t path;            /* path of every chunk when d_chunk_paths == NULL */
+    int32_t is_rtx;
+} cn_packetize_args;
+uint64_t cn_packet_count(uint64_t len, uint32_t chunk_bytes, uint32_t max_payload);
+int cn_packetize(const cn_packetize_args* a, cn_pkt_hdr* d_out, void* stream);
+
+/* ------------------------------------------------- multi-GPU plumbing
+ * CUDA IPC mappings of a peer rank's device buffers (NVLink P2P): 64-byte
+ * opaque handles exchanged by the host (torch.distributed in the Python
+ * driver). */
+int cn_ipc_get_handle(void* d_ptr, void* out64);  /* d_ptr must be an allocation base */
+/* Whole-allocation device buffers (zeroed) for IPC sharing. */
+int cn_dev_alloc(uint64_t bytes, void** d_ptr);
+int cn_dev_free(void* d_ptr);
+int cn_ipc_open(const void* handle64, void** d_ptr);
+int cn_ipc_close(void* d_ptr);
+/* Progress flags between neighbouring ranks: signal = system-scope release
+ * store of `value` into up to two (peer) flag words; wait = bounded acquire
+ * spin until both local words are >= value (sets *d_err on timeout). */
+int cn_flag_signal(unsigned long long* d_a, unsigned long long* d_b, uint64_t value, void* stream);
+int cn_flag_wait(const unsigned long long* d_a, const unsigned long long* d_b, uint64_t value,
+                 uint64_t max_spins, unsigned int* d_err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

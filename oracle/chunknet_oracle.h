@@ -83,6 +83,9 @@ void orc_fill_staging(const cn_pkt_hdr* hdrs, uint64_t n, uint32_t max_pl,
  * (uint16 storage, fp32 add, round-to-nearest-even per hop). */
 void orc_ring_allreduce(int dtype, int n_ranks, uint64_t count, const void* x,
                         void* out);
+/* same with segment boundaries rounded down to multiples of `quantum`. */
+void orc_ring_allreduce_q(int dtype, int n_ranks, uint64_t count, const void* x, void* out,
+                          uint64_t quantum);
 
 #ifdef __cplusplus
 }

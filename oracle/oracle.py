@@ -45,6 +45,7 @@ def lib():
         L.orc_fill_staging.argtypes = [vp, u64, u32, vp, u64]
         L.orc_select_paths.argtypes = [i32, i32, vp, vp, u64, ctypes.c_char_p, i64, u64, vp]
         L.orc_ring_allreduce.argtypes = [i32, i32, u64, vp, vp]
+        L.orc_ring_allreduce_q.argtypes = [i32, i32, u64, vp, vp, u64]
         L.orc_rng_u64_seq.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
         L.orc_next_below_seq.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]
         L.orc_next_double_seq.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
@@ -115,13 +116,14 @@ def select_paths(policy, rtt, ecn, seed, name, index, count):
     return out
 
 
-def ring_allreduce(x):
-    """x: [n_ranks, count] float32 or uint16 (bf16 bits) -> allreduced [count]."""
+def ring_allreduce(x, quantum=1):
+    """x: [n_ranks, count] float32 or uint16 (bf16 bits) -> allreduced [count].
+    Segment boundaries are rounded down to multiples of `quantum` elements."""
     x = np.ascontiguousarray(x)
     dtype = 0 if x.dtype == np.float32 else 1
     assert x.dtype in (np.float32, np.uint16)
     out = np.zeros(x.shape[1], dtype=x.dtype)
-    lib().orc_ring_allreduce(dtype, x.shape[0], x.shape[1], _ptr(x), _ptr(out))
+    lib().orc_ring_allreduce_q(dtype, x.shape[0], x.shape[1], _ptr(x), _ptr(out), quantum)
     return out
 
 

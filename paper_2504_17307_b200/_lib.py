@@ -36,6 +36,15 @@ class RxConfig(ctypes.Structure):
                 ("reduce_op", ctypes.c_int32), ("max_posts", ctypes.c_uint32)]
 
 
+class PacketizeArgs(ctypes.Structure):
+    _fields_ = [("len", ctypes.c_uint64), ("chunk_bytes", ctypes.c_uint32),
+                ("max_payload", ctypes.c_uint32), ("src", ctypes.c_int32), ("dst", ctypes.c_int32),
+                ("conn_id", ctypes.c_uint32), ("msg_id", ctypes.c_uint32),
+                ("msg_seq", ctypes.c_uint64), ("tag", ctypes.c_uint64), ("tx_time", ctypes.c_int64),
+                ("d_chunk_paths", ctypes.c_void_p), ("path", ctypes.c_int32),
+                ("is_rtx", ctypes.c_int32)]
+
+
 class RxResult(ctypes.Structure):
     _fields_ = [("n_acks", ctypes.c_uint32), ("n_completions", ctypes.c_uint32),
                 ("status", ctypes.c_uint32), ("n_copied", ctypes.c_uint32),
@@ -84,6 +93,16 @@ def lib():
     L.cn_sched_select.argtypes = [vp, i32, i32, vp, vp, vp, u32, u32, vp, vp]
     L.cn_sched_draws.argtypes = [vp, u32, vp, u64, vp, vp]
     L.cn_sched_record.argtypes = [vp, vp, vp, vp, vp, vp, u32, vp]
+    L.cn_packet_count.restype = u64
+    L.cn_packet_count.argtypes = [u64, u32, u32]
+    L.cn_packetize.argtypes = [ctypes.POINTER(PacketizeArgs), vp, vp]
+    L.cn_ipc_get_handle.argtypes = [vp, vp]
+    L.cn_dev_alloc.argtypes = [u64, ctypes.POINTER(vp)]
+    L.cn_dev_free.argtypes = [vp]
+    L.cn_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+    L.cn_ipc_close.argtypes = [vp]
+    L.cn_flag_signal.argtypes = [vp, vp, u64, vp]
+    L.cn_flag_wait.argtypes = [vp, vp, u64, u64, vp, vp]
     _lib = L
     return L
 

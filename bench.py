@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sched", action="store_true")
+    ap.add_argument("--no-ring", action="store_true")
     return ap.parse_args()
 
 
@@ -178,6 +179,60 @@ def sched_bench(dev, steps=20, conns=1024, paths=256, per_call=4096):
     except Exception as e:  # noqa: BLE001
         r["cpu_reference_error"] = str(e)
     return r
+
+
+def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30):
+    """BASELINE configs[2]: ring all-reduce of 1 GiB per rank (fp32 and bf16)
+    through the transport (packetize -> NVLink zero-copy fused-reduce receive
+    path), busbw = (S/t)*2(N-1)/N, max over ranks; NCCL's all_reduce on the
+    same buffers beside it."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_17307_b200.collective import RingAllreduce, busbw
+    out = {}
+    for dt, name in ((torch.float32, "fp32"), (torch.bfloat16, "bf16")):
+        count = nbytes // (4 if dt == torch.float32 else 2)
+        x = torch.randn(count, device=dev).to(dt)
+        ring = RingAllreduce(count, dt, chunk_bytes=32768, paths=8)
+        ring.buffer().copy_(x)
+        for _ in range(warmup):  # in place, like dist.all_reduce(y) below
+            ring.run()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            ring.run()
+        e1.record()
+        torch.cuda.synchronize()
+        ring.check()
+        t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        # NCCL on the same buffer size for context
+        y = x.clone()
+        for _ in range(warmup):
+            dist.all_reduce(y)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        for _ in range(iters):
+            dist.all_reduce(y)
+        e1.record()
+        torch.cuda.synchronize()
+        tn = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
+        dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+        msn = float(tn.item())
+        out[name] = {"bytes": nbytes, "ms": round(ms, 4), "busbw_GBps": round(busbw(nbytes, ms * 1e-3, world), 1),
+                     "nccl_ms": round(msn, 4),
+                     "nccl_busbw_GBps": round(busbw(nbytes, msn * 1e-3, world), 1)}
+        ring.close()
+        del x, y
+        torch.cuda.empty_cache()
+    out["roofline"] = {"bound": "nvlink", "peak_GBps_per_direction": 770.0,
+                       "note": "measured peer copy per direction (B200_PROFILING.md); busbw ~ link rate"}
+    return out
 
 
 def run_reference(args):
@@ -376,6 +431,7 @@ def main():
                "path": "pinned host records+staging -> cn_rx_batch (C ABI) -> acks to host"}
 
     sched = sched_bench(dev) if not args.no_sched else None
+    ring = ring_bench(dev, world, rank) if world > 1 and not args.no_ring else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -408,6 +464,8 @@ def main():
             line["e2e"] = e2e
         if sched:
             line["scheduler"] = sched
+        if ring:
+            line["allreduce"] = ring
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

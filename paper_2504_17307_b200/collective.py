@@ -146,9 +146,19 @@ class RingAllreduce:
         self._hdr_bufs = [DeviceBuffer(max(1, k) * 64, self.dev) for k in self.n_pkts]
         self.hdrs = [b.tensor() for b in self._hdr_bufs]
         # per-chunk path choices for the outgoing messages (S3 scheduler)
+        # one virtual connection (RngStream) per step's message, so the path
+        # choices of all messages of an iteration are drawn in one launch
         from .scheduler import PathScheduler
-        self.sched = PathScheduler(1, paths, seed, base_rtt_ns=10000.0, index0=r)
+        n_msgs = len(self.steps) - 1
+        self.sched = PathScheduler(n_msgs, paths, seed, base_rtt_ns=10000.0, index0=r * n_msgs)
         self.max_chunks = max((b + chunk_bytes - 1) // chunk_bytes for b in self.seg_bytes)
+        nchs = [(self.seg_bytes[st[3]] + chunk_bytes - 1) // chunk_bytes for st in self.steps[1:]]
+        offs = [0]
+        for c in nchs:
+            offs.append(offs[-1] + c)
+        self.path_offs = torch.tensor(offs, dtype=torch.int32, device=self.dev)
+        self.paths_all = torch.empty(max(1, offs[-1]), dtype=torch.int32, device=self.dev)
+        self.path_slices = [(offs[i], offs[i + 1]) for i in range(n_msgs)]
         # flags: [from_prev, from_next, err]
         self._flag_buf = DeviceBuffer(64, self.dev)
         self.flags = self._flag_buf.tensor(torch.int64, 4)
@@ -182,7 +192,6 @@ class RingAllreduce:
             elif ph == "ag":
                 self.rx_ag.post(tag, accb[self.seg_off[rcv]: self.seg_off[rcv] + self.seg_bytes[rcv]])
         self.g = 0  # global step counter (across iterations)
-        self.paths_buf = torch.empty(self.max_chunks, dtype=torch.int32, device=self.dev)
         torch.cuda.synchronize()
         dist.barrier(group)
 
@@ -213,23 +222,29 @@ class RingAllreduce:
         _lib.check(_lib.lib().cn_flag_signal(a, b, g, ctypes.c_void_p(s.cuda_stream)),
                    "cn_flag_signal")
 
-    def run(self, x, stream=None):
-        """All-reduce x (count elements, this rank's contribution)."""
+    def buffer(self):
+        """The accumulator: write the input here and call run() for an
+        in-place all-reduce (no init copy, like an in-place ncclAllReduce)."""
+        return self.acc
+
+    def run(self, x=None, stream=None):
+        """All-reduce x (count elements, this rank's contribution), or the
+        accumulator in place when x is None."""
         s = stream or torch.cuda.current_stream(self.dev)
         n, r = self.n, self.rank
         for (k, ph, st, snd, rcv, tag) in self.steps:
             g = self.g
             self._wait(g, s)  # neighbours finished global step g-1
             if ph == "init":
-                self.acc.copy_(x)
+                if x is not None:
+                    self.acc.copy_(x)
                 self.rx_rs.reset(s)
                 self.rx_ag.reset(s)
+                self.sched.select("p2_rtt", offsets=self.path_offs, out=self.paths_all, stream=s)
                 for (k2, ph2, st2, snd2, rcv2, tag2) in self.steps[1:]:
-                    nb = self.seg_bytes[snd2]
-                    nch = (nb + self.cb - 1) // self.cb
-                    self.sched.select("p2_rtt", nch, out=self.paths_buf[:nch].view(1, nch), stream=s)
-                    packetize(nb, self.cb, src=r, dst=(r + 1) % n, conn_id=0, msg_id=k2 % 128,
-                              msg_seq=k2, tag=tag2, chunk_paths=self.paths_buf[:nch],
+                    a, b = self.path_slices[k2 - 1]
+                    packetize(self.seg_bytes[snd2], self.cb, src=r, dst=(r + 1) % n, conn_id=0,
+                              msg_id=k2 % 128, msg_seq=k2, tag=tag2, chunk_paths=self.paths_all[a:b],
                               out=self.hdrs[k2], stream=s, device=self.dev)
             else:
                 rx = self.rx_rs if ph == "rs" else self.rx_ag

@@ -212,11 +212,11 @@ __global__ void __launch_bounds__(256) k_select(SchedDev d, int policy, int avoi
             k += m;
             continue;
         }
-        if (r.idx + draws * m > kMtN) {
-            // straddles a twist: take what fits sequentially-exact
+        const uint32_t avail = (kMtN - r.idx) / draws;  // whole decisions left in this block
+        if (avail == 0) {
             if (r.idx >= kMtN) {
                 refill(r, lane);
-            } else {
+            } else {  // a decision straddles the twist: exact sequential step
                 int32_t pv = req ? req[o0 + k] : -1;
                 int p = select_seq(r, policy, n, score, lane);
                 if (avoid_prev && pv >= 0 && n > 1 && p == pv) p = (p + 1) % n;
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256) k_select(SchedDev d, int policy, int avoi
             }
             continue;
         }
+        if (m > avail) m = avail;
         // parallel: lane j takes draws idx + draws*j (+1)
         bool rej = false;
         int p = 0;

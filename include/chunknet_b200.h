@@ -255,6 +255,65 @@ int cn_sched_draws(cn_sched* s, uint32_t conn, const uint64_t* d_ns, uint64_t co
 int cn_sched_record(cn_sched* s, const uint32_t* d_conn, const int32_t* d_path, const int64_t* d_rtt,
                     const uint8_t* d_ecn, const uint32_t* d_offsets, uint32_t n_groups, void* stream);
 
+/* ------------------------------------------------------------ tx engine
+ * Device sender: ack processing, duplicate-hint fast retransmit, RTO with
+ * backoff, and the commit/egress pump of chunknet::Transport
+ * (transport.cpp:144-542, 807-942, 1078-1169; RttEstimator cc.hpp:12-35)
+ * for congestion control none (OpenLoop), one engine per host, selective
+ * mode, DefaultPolicy.  One warp per connection consumes a time-ordered
+ * event stream (message submissions, acks delivered at the sender) and
+ * fires its own RTO timer in between; every transmission is logged.
+ * Path choices (commits and retransmissions) come from the connection's
+ * RngStream("transport.conn", stream_index0 + c) and are bit-identical to
+ * the reference. */
+typedef struct cn_tx_config {
+    uint32_t chunk_bytes;         /* TransportConfig::chunk_bytes            */
+    uint32_t max_payload;         /* 0 = CN_MAX_PAYLOAD                      */
+    uint32_t dupack_threshold;    /* TransportConfig::dupack_threshold (8)   */
+    uint32_t rtx_avoid_prev_path; /* TransportConfig::rtx_avoid_prev_path    */
+    int32_t lb_policy;            /* CN_LB_*                                 */
+    uint32_t max_inflight_msgs;   /* per engine (128)                        */
+    uint32_t max_paths;           /* paths per connection (upper bound)      */
+    uint32_t log_cap;             /* transmit records kept per connection    */
+    int64_t rto_min;              /* resolved Transport::rto_min_ (> 0)      */
+    int64_t rto_max;              /* 0 = 64 * rto_min (transport.cpp:36)     */
+    int64_t commit_ahead;         /* Transport::commit_ahead_ (:37-39)       */
+    double base_rtt_ns;           /* scoreboard prior (Network::base_rtt_ns) */
+    uint64_t seed;                /* Transport seed                          */
+    int64_t stream_index0;        /* connection c uses stream index0 + c     */
+    uint64_t chunk_pool;          /* chunk state entries                     */
+} cn_tx_config;
+typedef struct cn_tx_submit { int64_t t; uint64_t len; uint64_t tag; } cn_tx_submit;
+/* one chunk transmission (send_chunk): time, message, chunk index, path */
+typedef struct cn_tx_rec {
+    int64_t t;
+    uint32_t msg_id;
+    uint32_t chunk;
+    int32_t path;
+    int32_t is_rtx;
+    uint64_t msg_seq;
+} cn_tx_rec;
+typedef struct cn_tx_stats {  /* Transport::Stats sender fields + estimator */
+    uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_sent, msgs_completed, backpressured, n_log;
+    int64_t srtt, rttvar;
+    int32_t backoff, live_msgs;
+} cn_tx_stats;
+typedef struct cn_tx cn_tx;
+void cn_tx_config_default(cn_tx_config* cfg);
+int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int32_t* h_src, const int32_t* h_dst,
+                 const int32_t* h_n_paths, cn_tx** out);
+void cn_tx_destroy(cn_tx* t);
+/* Events of connection c are d_events[d_ev_off[c] .. d_ev_off[c+1]), each
+ * (type << 62) | index: type 0 = d_submits[index], 1 = d_acks[index]
+ * (cn_ack_rec::aux = delivery time at the sender), ordered by time (ties:
+ * in list order).  Timers fire up to end_time.  d_log holds log_cap records
+ * per connection; d_stats one record per connection.  State persists
+ * across calls. */
+int cn_tx_run(cn_tx* t, const uint32_t* d_ev_off, const uint64_t* d_events,
+              const cn_tx_submit* d_submits, const cn_ack_rec* d_acks, int64_t end_time,
+              cn_tx_rec* d_log, cn_tx_stats* d_stats, void* stream);
+int cn_tx_status(cn_tx* t, unsigned int* out);
+
 /* --------------------------------------------------------- send side
  * Transport::send_chunk's packetization (transport.cpp:433-494) for all
  * chunks of one message (DefaultPolicy chunking, policy.hpp:75-78): packet

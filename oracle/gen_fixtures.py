@@ -94,15 +94,47 @@ def gen(name, kw, flows):
         a2["pkt_index"] = acks["pkt_index"]
         ok, bad = ack_equal(acks, a2)
         assert ok, (name, bad)
+    subs = st.pop("submits")
     meta = dict(name=name, n_hosts=int(st["n_hosts"]), chunk_bytes=int(kw["chunk_bytes"]),
                 record=dict(kw, window=window), flows=flows,
                 des_stats={k: int(v) for k, v in st.items()})
+    if name in SENDER_SCENARIOS:
+        gen_sender(name, kw, flows, acks_des, subs)
     path = os.path.join(GOLDEN, f"{name}.npz")
     np.savez_compressed(path, data=data, acks=acks, completions=cpls,
                         meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
     print(f"{name}: pkts={len(data)} acks={len(acks)} completions={len(cpls)} "
           f"rtx={st['chunk_rtx']} fast_rtx={st['fast_rtx']} rtos={st['rtos']} "
           f"-> {os.path.getsize(path)} B")
+
+
+# single-connection scenarios whose timed acks are replayed into the
+# reference sender (blackhole, CC none) for the tx-engine goldens
+SENDER_SCENARIOS = ["cfg1", "cfg2_32k", "cfg2_4k", "k8_4x1m", "multigen_k8", "lossy_2m",
+                    "csn_wrap"]
+
+
+def gen_sender(name, kw, flows, acks_des, subs):
+    """Sender-side golden: the reference sender (OpenLoop) fed the DES's
+    submissions and the acks the DES delivered to it, at their times."""
+    src, dst = flows[0][0], flows[0][1]
+    rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes",
+                              "paths", "lb") if k in kw}
+    submits = [(int(s["t"]), int(s["len"]), int(s["tag"])) for s in subs]
+    tx, st = ref.sender_replay(acks_des, submits, src, dst, cc="none", **rkw)
+    rate = kw.get("rate_bps", 400e9)
+    bdp = int(round(rate * st["base_rtt"] / 8e9))
+    commit_ahead = max(2 * kw["chunk_bytes"], 2 * 32768, bdp)
+    meta = dict(name=name, src=src, dst=dst, chunk_bytes=kw["chunk_bytes"], lb=kw["lb"],
+                seed=kw["seed"], n_paths=int(st["n_paths"]), base_rtt=int(st["base_rtt"]),
+                rto_min=int(st["rto_min"]), rto_max=int(st["rto_max"]), commit_ahead=commit_ahead,
+                end_time=int(st["end_time"]), stats={k: int(v) for k, v in st.items()})
+    path = os.path.join(GOLDEN, f"sender_{name}.npz")
+    sub_arr = np.array(submits, dtype=[("t", "<i8"), ("len", "<u8"), ("tag", "<u8")])
+    np.savez_compressed(path, acks=acks_des, submits=sub_arr, tx=tx,
+                        meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
+    print(f"  sender_{name}: submits={len(submits)} acks={len(acks_des)} tx={len(tx)} "
+          f"rtx={st['chunk_rtx']} fast={st['fast_rtx']} rtos={st['rtos']} done={st['msgs_completed']}")
 
 
 def gen_rng():

@@ -52,6 +52,27 @@ class RxOut(ctypes.Structure):
         "n_acks", "n_completions", "arena_used", "acks_sent_stat")]
 
 
+class TxRec(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64), ("msg_id", ctypes.c_uint32), ("chunk", ctypes.c_uint32),
+                ("path", ctypes.c_int32), ("is_rtx", ctypes.c_int32), ("msg_seq", ctypes.c_uint64)]
+
+
+class SenderStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "chunks_sent", "chunk_rtx", "fast_rtx", "rtos", "msgs_completed", "n_tx")] + [
+        (n, ctypes.c_int64) for n in ("base_rtt", "rto_min", "rto_max", "end_time")] + [
+        ("n_paths", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class Submit(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_int64), ("len", ctypes.c_uint64), ("tag", ctypes.c_uint64)]
+
+
+SUBMIT_LOG_DTYPE = np.dtype([("t", "<i8"), ("len", "<u8"), ("tag", "<u8"), ("src", "<i4"),
+                             ("dst", "<i4")])
+TX_DTYPE = np.dtype([("t", "<i8"), ("msg_id", "<u4"), ("chunk", "<u4"), ("path", "<i4"),
+                     ("is_rtx", "<i4"), ("msg_seq", "<u8")])
+
 _lib = None
 
 
@@ -75,6 +96,8 @@ def lib():
                                       u64, ctypes.POINTER(RxOut)]
         L.cnref_rx_replay_bench.argtypes = [vp, u64, i32, u32, i32, i32]
         L.cnref_rx_replay_bench.restype = ctypes.c_double
+        L.cnref_sender_replay.argtypes = [ctypes.POINTER(Scenario), i32, i32, vp, u64, vp, u64,
+                                          vp, u64, ctypes.POINTER(SenderStats)]
         L.cnref_rng_u64.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
         L.cnref_next_below.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]
         L.cnref_next_double.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
@@ -113,7 +136,31 @@ def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
     data = np.fromfile(os.path.join(outdir, "data.bin"), dtype=PKT_DTYPE)
     acks = np.fromfile(os.path.join(outdir, "acks_des.bin"), dtype=ACK_DTYPE)
     cpls = np.fromfile(os.path.join(outdir, "completions_des.bin"), dtype=CPL_DTYPE)
-    return data, acks, cpls, {k: getattr(st, k) for k, _ in RecordStats._fields_}
+    subs = np.fromfile(os.path.join(outdir, "submits.bin"), dtype=SUBMIT_LOG_DTYPE)
+    st_d = {k: getattr(st, k) for k, _ in RecordStats._fields_}
+    st_d["submits"] = subs
+    return data, acks, cpls, st_d
+
+
+def sender_replay(acks, submits, src, dst, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
+                  link_delay_ns=1000, qcap_bytes=1 << 20, seed=1, chunk_bytes=32768, paths=8,
+                  lb="p2_rtt", cc="none", cc_scope=0, dupack_threshold=8, rto_min=0,
+                  cutoff_ns=60_000_000_000, max_out=1 << 20):
+    """Reference sender over a blackhole: submits [(t, len, tag)] and acks
+    (ACK_DTYPE, aux = delivery time at the sender) -> (tx log, stats)."""
+    sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns, qcap_bytes, 0.0,
+                  seed, chunk_bytes, paths, LB[lb], CC[cc], cc_scope, 1, 0, dupack_threshold,
+                  rto_min, 0, 1, cutoff_ns)
+    sb = (Submit * max(1, len(submits)))(*[Submit(int(t), int(l), int(g)) for t, l, g in submits])
+    acks = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
+    out = np.zeros(max_out, dtype=TX_DTYPE)
+    st = SenderStats()
+    rc = lib().cnref_sender_replay(ctypes.byref(sc), src, dst, ctypes.cast(sb, ctypes.c_void_p),
+                                   len(submits), _ptr(acks), len(acks), _ptr(out), max_out,
+                                   ctypes.byref(st))
+    if rc != 0:
+        raise RuntimeError(lib().cnref_last_error().decode())
+    return out[: min(st.n_tx, max_out)].copy(), {k: getattr(st, k) for k, _ in SenderStats._fields_}
 
 
 def rx_replay(recs, n_hosts, chunk_bytes, carry_payload=True, arena_bytes=None):

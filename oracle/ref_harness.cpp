@@ -230,6 +230,8 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
         std::vector<cn_pkt_hdr> data;
         std::vector<cn_ack_rec> acks;
         std::vector<cn_completion> cpls;
+        struct SubRec { int64_t t; uint64_t len, tag; int32_t src, dst; };
+        std::vector<SubRec> subs_log;
         net.set_trace([&](const TraceEvent& te) {
             if (std::strcmp(te.event, "deliver") != 0) return;
             const Packet& p = *te.pkt;
@@ -249,6 +251,7 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
             uint64_t tag = uint64_t(f) * 1000000ull + uint64_t(next[f]);
             auto buf = pattern(fl.len, tag);
             if (!tr.send_message_data(fl.src, fl.dst, buf, tag)) return;  // retried on completion
+            subs_log.push_back({eq.now(), fl.len, tag, fl.src, fl.dst});
             srcs[tag] = buf;
             ++next[f];
         };
@@ -273,7 +276,7 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
 
         std::string dir(outdir);
         if (!write_vec(dir + "/data.bin", data) || !write_vec(dir + "/acks_des.bin", acks) ||
-            !write_vec(dir + "/completions_des.bin", cpls))
+            !write_vec(dir + "/completions_des.bin", cpls) || !write_vec(dir + "/submits.bin", subs_log))
             throw std::runtime_error("cannot write to " + dir);
         if (st) {
             st->data_pkts = data.size();
@@ -443,6 +446,109 @@ double cnref_rx_replay_bench(const cn_pkt_hdr* recs, uint64_t n, int n_hosts,
     go.store(true);
     for (auto& x : th) x.join();
     return *std::max_element(secs.begin(), secs.end());
+}
+
+// --------------------------------------------------------- sender replay
+// A fresh reference Transport whose data packets all vanish at the host
+// egress (inject_loss_at_host_egress(1.0), the reference tests' blackhole,
+// test_transport.cpp:207-295): messages are submitted at given times and
+// recorded acks are delivered to the sender at their recorded times
+// (Transport::handle_packet -> handle_ack, transport.cpp:849-942).  Every
+// transmission is captured from the "loss" trace event of its first packet:
+// (time, msg_id, chunk index, path, is_rtx).  Timers (rto_fire) run inside
+// the reference event queue.
+struct cnref_tx_rec {
+    int64_t t;
+    uint32_t msg_id;
+    uint32_t chunk;
+    int32_t path;
+    int32_t is_rtx;
+    uint64_t msg_seq;
+};
+
+struct cnref_sender_stats {
+    uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_completed, n_tx;
+    int64_t base_rtt, rto_min, rto_max, end_time;
+    int32_t n_paths, pad;
+};
+
+struct cnref_submit {
+    int64_t t;
+    uint64_t len;
+    uint64_t tag;
+};
+
+int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_submit* subs,
+                        uint64_t n_subs, const cn_ack_rec* acks, uint64_t n_acks,
+                        cnref_tx_rec* out, uint64_t max_out, cnref_sender_stats* st) {
+    try {
+        Topology topo =
+            sc->topo_kind == 0 ? build_star(sc->topo_arg) : build_fat_tree(sc->topo_arg);
+        NetParams np;
+        np.rate_bps = sc->rate_bps;
+        np.link_delay_ns = sc->link_delay_ns;
+        np.qcap_bytes = sc->qcap_bytes;
+        EventQueue eq;
+        Network net(topo, np, eq, sc->seed);
+        net.inject_loss_at_host_egress(1.0);
+        TransportConfig tc;
+        tc.chunk_bytes = sc->chunk_bytes;
+        tc.paths = sc->paths;
+        tc.lb = static_cast<LbPolicy>(sc->lb);
+        tc.cc.algo = static_cast<CcConfig::Algo>(sc->cc);
+        tc.cc.scope = static_cast<CcConfig::Scope>(sc->cc_scope);
+        if (tc.cc.algo == CcConfig::Algo::swift) tc.cc.swift_target_ns = 3 * net.base_rtt_ns();
+        tc.engines = 1;
+        tc.dupack_threshold = sc->dupack_threshold;
+        tc.rto_min = sc->rto_min;
+        Transport tr(net, eq, tc, sc->seed);
+        uint64_t n_out = 0;
+        net.set_trace([&](const TraceEvent& te) {
+            if (std::strcmp(te.event, "loss") != 0) return;
+            const Packet& p = *te.pkt;
+            if (p.kind != PacketKind::data || p.seq_in_chunk != 0) return;
+            if (n_out < max_out) {
+                cnref_tx_rec& r = out[n_out];
+                r.t = te.t;
+                r.msg_id = p.hdr.msg_id;
+                r.chunk = static_cast<uint32_t>(p.chunk_offset / tc.chunk_bytes);
+                r.path = p.path_id;
+                r.is_rtx = p.is_rtx ? 1 : 0;
+                r.msg_seq = p.msg_seq;
+            }
+            ++n_out;
+        });
+        for (uint64_t k = 0; k < n_subs; ++k) {
+            cnref_submit sb = subs[k];
+            eq.schedule(sb.t, [&tr, src, dst, sb] { tr.send_message(src, dst, sb.len, sb.tag); });
+        }
+        for (uint64_t k = 0; k < n_acks; ++k) {
+            cn_ack_rec a = acks[k];
+            eq.schedule(a.aux, [&tr, a] {
+                Packet p = from_ack(a);
+                int host = p.dst;
+                tr.handle_packet(host, std::move(p));
+            });
+        }
+        eq.run_until_idle(sc->cutoff_ns);
+        if (st) {
+            st->chunks_sent = tr.stats().chunks_sent;
+            st->chunk_rtx = tr.stats().chunk_rtx;
+            st->fast_rtx = tr.stats().fast_rtx;
+            st->rtos = tr.stats().rtos;
+            st->msgs_completed = tr.stats().msgs_completed;
+            st->n_tx = n_out;
+            st->base_rtt = net.base_rtt_ns();
+            st->rto_min = tr.rto_min_;
+            st->rto_max = tr.rto_max_;
+            st->end_time = eq.now();
+            st->n_paths = tr.conns_.empty() ? 0 : static_cast<int>(tr.conns_[0].subs.size());
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
 }
 
 // ------------------------------------------------------------- RNG draws

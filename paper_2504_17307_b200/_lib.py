@@ -45,6 +45,17 @@ class PacketizeArgs(ctypes.Structure):
                 ("is_rtx", ctypes.c_int32)]
 
 
+class TxConfig(ctypes.Structure):
+    _fields_ = [("chunk_bytes", ctypes.c_uint32), ("max_payload", ctypes.c_uint32),
+                ("dupack_threshold", ctypes.c_uint32), ("rtx_avoid_prev_path", ctypes.c_uint32),
+                ("lb_policy", ctypes.c_int32), ("max_inflight_msgs", ctypes.c_uint32),
+                ("max_paths", ctypes.c_uint32), ("log_cap", ctypes.c_uint32),
+                ("rto_min", ctypes.c_int64), ("rto_max", ctypes.c_int64),
+                ("commit_ahead", ctypes.c_int64), ("base_rtt_ns", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("stream_index0", ctypes.c_int64),
+                ("chunk_pool", ctypes.c_uint64)]
+
+
 class RxResult(ctypes.Structure):
     _fields_ = [("n_acks", ctypes.c_uint32), ("n_completions", ctypes.c_uint32),
                 ("status", ctypes.c_uint32), ("n_copied", ctypes.c_uint32),
@@ -103,6 +114,13 @@ def lib():
     L.cn_ipc_close.argtypes = [vp]
     L.cn_flag_signal.argtypes = [vp, vp, u64, vp]
     L.cn_flag_wait.argtypes = [vp, vp, u64, u64, vp, vp]
+    L.cn_tx_config_default.argtypes = [ctypes.POINTER(TxConfig)]
+    L.cn_tx_config_default.restype = None
+    L.cn_tx_create.argtypes = [ctypes.POINTER(TxConfig), u32, vp, vp, vp, ctypes.POINTER(vp)]
+    L.cn_tx_destroy.argtypes = [vp]
+    L.cn_tx_destroy.restype = None
+    L.cn_tx_run.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp, vp]
+    L.cn_tx_status.argtypes = [vp, ctypes.POINTER(ctypes.c_uint)]
     _lib = L
     return L
 

@@ -1,0 +1,97 @@
+"""Device sender engine (C ABI cn_tx_*): ack processing, duplicate-hint fast
+retransmit, RTO backoff and the commit/egress pump of chunknet::Transport
+(src/transport.cpp:144-542, 807-942, 1078-1169), one warp per connection,
+for congestion control none (OpenLoop), one engine per host, DefaultPolicy.
+
+Inputs are per-connection event streams: message submissions
+(Transport::send_message at time t) and acks delivered at the sender (the
+cn_ack_rec records the receive path emits, `aux` = delivery time).  Output
+is the transmit log (one record per send_chunk) and Transport::Stats.
+"""
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .records import ACK_DTYPE
+
+LB = {"oblivious": 0, "p2_rtt": 1, "p2_ecn": 2}
+TX_DTYPE = np.dtype([("t", "<i8"), ("msg_id", "<u4"), ("chunk", "<u4"), ("path", "<i4"),
+                     ("is_rtx", "<i4"), ("msg_seq", "<u8")])
+SUBMIT_DTYPE = np.dtype([("t", "<i8"), ("len", "<u8"), ("tag", "<u8")])
+STATS_DTYPE = np.dtype([(n, "<u8") for n in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos",
+                                             "msgs_sent", "msgs_completed", "backpressured",
+                                             "n_log")] +
+                       [("srtt", "<i8"), ("rttvar", "<i8"), ("backoff", "<i4"), ("live_msgs", "<i4")])
+
+
+class TxEngine:
+    def __init__(self, n_conns, *, chunk_bytes, rto_min, commit_ahead, base_rtt_ns, seed,
+                 lb="oblivious", max_paths=1, n_paths=None, src=None, dst=None, rto_max=0,
+                 dupack_threshold=8, rtx_avoid_prev_path=True, stream_index0=0,
+                 chunk_pool=1 << 20, log_cap=1 << 16, device="cuda"):
+        L = _lib.lib()
+        c = _lib.TxConfig()
+        L.cn_tx_config_default(ctypes.byref(c))
+        c.chunk_bytes, c.dupack_threshold = chunk_bytes, dupack_threshold
+        c.rtx_avoid_prev_path = 1 if rtx_avoid_prev_path else 0
+        c.lb_policy, c.max_paths, c.log_cap = LB[lb], max_paths, log_cap
+        c.rto_min, c.rto_max, c.commit_ahead = rto_min, rto_max, commit_ahead
+        c.base_rtt_ns, c.seed, c.stream_index0, c.chunk_pool = float(base_rtt_ns), seed, stream_index0, chunk_pool
+        self.device = torch.device(device)
+        self.n, self.log_cap = n_conns, log_cap
+        arr = lambda v: (ctypes.c_int32 * n_conns)(*[int(x) for x in v]) if v is not None else None  # noqa: E731
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(L.cn_tx_create(ctypes.byref(c), n_conns, arr(src), arr(dst), arr(n_paths),
+                                      ctypes.byref(h)), "cn_tx_create")
+        self._h = h
+        self.log = torch.zeros(n_conns * log_cap * 32, dtype=torch.uint8, device=self.device)
+        self.stats = torch.zeros(n_conns * STATS_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().cn_tx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, events_per_conn, submits, acks, end_time, stream=None):
+        """events_per_conn: list (per connection) of lists of (type, index),
+        type 0 = submits[index], 1 = acks[index], already time-ordered."""
+        off = np.zeros(self.n + 1, dtype=np.uint32)
+        ev = []
+        for c, evs in enumerate(events_per_conn):
+            off[c + 1] = off[c] + len(evs)
+            ev.extend((int(t) << 62) | int(i) for t, i in evs)
+        dev = self.device
+        t_off = torch.from_numpy(off.view(np.int32)).to(dev)
+        t_ev = torch.from_numpy(np.array(ev if ev else [0], dtype=np.uint64).view(np.int64)).to(dev)
+        sub = np.ascontiguousarray(submits, dtype=SUBMIT_DTYPE)
+        t_sub = torch.from_numpy(sub.view(np.uint8).copy() if len(sub) else np.zeros(24, np.uint8)).to(dev)
+        ak = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
+        t_ack = torch.from_numpy(ak.view(np.uint8).copy() if len(ak) else np.zeros(64, np.uint8)).to(dev)
+        s = stream or torch.cuda.current_stream(dev)
+        _lib.check(_lib.lib().cn_tx_run(self._h, t_off.data_ptr(), t_ev.data_ptr(), t_sub.data_ptr(),
+                                        t_ack.data_ptr(), int(end_time), self.log.data_ptr(),
+                                        self.stats.data_ptr(), ctypes.c_void_p(s.cuda_stream)),
+                   "cn_tx_run")
+        s.synchronize()
+        st = ctypes.c_uint()
+        _lib.lib().cn_tx_status(self._h, ctypes.byref(st))
+        if st.value:
+            raise _lib.ChunknetError(-6, f"tx engine status 0x{st.value:x}")
+        return self.stats_np()
+
+    def stats_np(self):
+        return self.stats.cpu().numpy().view(STATS_DTYPE)
+
+    def log_np(self, conn):
+        n = int(self.stats_np()[conn]["n_log"])
+        raw = self.log.view(self.n, self.log_cap * 32)[conn, : min(n, self.log_cap) * 32]
+        return raw.cpu().numpy().view(TX_DTYPE)

@@ -1,0 +1,69 @@
+"""Device sender engine (csrc/tx.cu) vs the reference sender: the same
+submissions and timed acks replayed into the unmodified reference Transport
+over a blackhole (golden tests/golden/sender_*.npz, oracle/gen_fixtures.py)
+must produce the identical transmit log -- every (re)transmission's time,
+message, chunk, path and rtx flag -- and the same Transport::Stats."""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+NAMES = sorted(os.path.basename(p)[7:-4] for p in glob.glob(os.path.join(GOLDEN, "sender_*.npz")))
+
+
+def _events(submits, acks):
+    ev = [(int(s["t"]), 0, k) for k, s in enumerate(submits)] + \
+         [(int(a["aux"]), 1, k) for k, a in enumerate(acks)]
+    ev.sort(key=lambda x: (x[0], x[1], x[2]))  # DES: submits scheduled before acks
+    return [(typ, k) for _, typ, k in ev]
+
+
+def _sorted(tx):
+    return np.sort(tx, order=["t", "msg_seq", "chunk"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_tx_engine_matches_reference_sender(name):
+    from paper_2504_17307_b200.sender import TxEngine
+    z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    eng = TxEngine(1, chunk_bytes=meta["chunk_bytes"], rto_min=meta["rto_min"],
+                   rto_max=meta["rto_max"], commit_ahead=meta["commit_ahead"],
+                   base_rtt_ns=meta["base_rtt"], seed=meta["seed"], lb=meta["lb"],
+                   max_paths=meta["n_paths"], src=[meta["src"]], dst=[meta["dst"]],
+                   chunk_pool=1 << 18, log_cap=1 << 17)
+    st = eng.run([_events(z["submits"], z["acks"])], z["submits"], z["acks"], 60_000_000_000)[0]
+    ref = meta["stats"]
+    for k in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos", "msgs_completed"):
+        assert int(st[k]) == ref[k], (k, int(st[k]), ref[k])
+    got, want = _sorted(eng.log_np(0)), _sorted(z["tx"])
+    assert len(got) == len(want)
+    for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
+        bad = np.nonzero(got[f] != want[f])[0]
+        assert len(bad) == 0, (f, int(bad[0]), got[bad[0]], want[bad[0]])
+
+
+def test_tx_engine_eight_dup_hints_one_fast_rtx():
+    """test_transport.cpp:207-261 on the device: acks for chunks 1..7 leave
+    chunk 0 alone; the 8th later-chunk ack retransmits it exactly once."""
+    from paper_2504_17307_b200.records import ACK_DTYPE
+    from paper_2504_17307_b200.sender import TxEngine
+    eng = TxEngine(1, chunk_bytes=4032, rto_min=10_000_000, commit_ahead=1 << 20,
+                   base_rtt_ns=12_000, seed=2, max_paths=1, src=[0], dst=[1])
+    acks = np.zeros(9, dtype=ACK_DTYPE)
+    for k, c in enumerate(range(1, 10)):
+        a = acks[k]
+        a["src"], a["dst"], a["msg_seq"], a["aux"] = 1, 0, 1, 10_000 * c
+        a["hdr"] = (c << 9)
+        a["sack0"] = 1 << c
+        a["echo_tx_time"] = 999
+    sub = np.array([(0, 10 * 4032, 1)], dtype=[("t", "<i8"), ("len", "<u8"), ("tag", "<u8")])
+    st = eng.run([[(0, 0)] + [(1, k) for k in range(9)]], sub, acks, 200_000)[0]
+    assert int(st["fast_rtx"]) == 1 and int(st["chunk_rtx"]) == 1 and int(st["chunks_sent"]) == 10
+    log = eng.log_np(0)
+    assert [int(r["chunk"]) for r in log if r["is_rtx"]] == [0]

@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg2_32k")
+    ap.add_argument("--conns", type=int, default=4,
+                    help="concurrent connections per batch (each a copy of the workload trace)")
     ap.add_argument("--replicas", type=int, default=4,
                     help="rotating staging replicas so that inputs exceed L2")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
@@ -53,6 +55,21 @@ def load_trace(name):
     z = np.load(os.path.join(ROOT, "tests", "golden", f"{name}.npz"))
     meta = json.loads(bytes(z["meta"]).decode())
     return z["data"], meta, len(z["acks"])
+
+
+def interleave(data, k):
+    """k concurrent copies of a recorded single-connection trace as one
+    receiver would see them: copy j comes from source host j (its own
+    connection and message, tag j), packets merged round-robin."""
+    if k == 1:
+        return data.copy()
+    out = np.empty(len(data) * k, dtype=data.dtype)
+    for j in range(k):
+        c = data.copy()
+        c["src"] = j
+        c["msg_tag"] = j
+        out[j::k] = c
+    return out
 
 
 def peaks():
@@ -114,12 +131,20 @@ class Clocks:
                 "samples": len(self.samples)}
 
 
+def message_bytes(data):
+    """Total bytes of the distinct messages a trace delivers."""
+    seen = {}
+    for s, t, ln in zip(data["src"], data["msg_tag"], data["msg_len"]):
+        seen[(int(s), int(t))] = int(ln)
+    return sum(seen.values())
+
+
 def cpu_reference(data, n_hosts, chunk_bytes, seconds, threads=None):
     """The reference's own receive path (oracle/_ref: the unmodified chunknet
     library, Transport::handle_packet replay) on this host's cores."""
     from oracle import ref
     threads = threads or os.cpu_count() or 1
-    msg = int(data["msg_len"][0])
+    msg = message_bytes(data)
     if ref.available():
         t1 = ref.rx_replay_bench(data, n_hosts, chunk_bytes, threads, 1)
         reps = max(1, min(200, int(seconds / max(t1, 1e-3))))
@@ -239,10 +264,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    data, meta, n_acks = load_trace(args.workload)
+    data1, meta, n_acks = load_trace(args.workload)
+    data = interleave(data1, max(1, args.conns))
     from oracle import ref
     threads = os.cpu_count() or 1
-    msg = int(data["msg_len"][0])
+    msg = message_bytes(data)
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
@@ -257,8 +283,9 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "reference DES trace",
-        "config": {"workload": f"{args.workload}: 64 MiB message, 256 paths, 1% drop "
-                               f"(BASELINE configs[1]); {threads} threads each replay it"},
+        "config": {"workload": f"{args.workload}: BASELINE configs[1] (64 MiB message, 256 paths, "
+                               f"1% drop) x {args.conns} concurrent connections per batch; "
+                               f"{threads} threads each replay it into its own Transport"},
         "mpkts_per_s": round(threads * args.steps * len(data) / t / 1e6, 3),
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads,
                          "kind": "reference",
@@ -287,36 +314,41 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    data, meta, _ = load_trace(args.workload)
+    data1, meta, _ = load_trace(args.workload)
+    K = max(1, args.conns)
+    data = interleave(data1, K)
     n = len(data)
     msg_len = int(data["msg_len"][0])
     cb = meta["chunk_bytes"]
 
     hdrs = cn.to_device_records(data, dev)
-    # synthetic payload: random message bytes on device, gathered into the
-    # arrival-order staging slots (packet i at i*4032) -- setup, untimed
+    # synthetic payload: random message bytes on device (one message per
+    # connection), gathered into the arrival-order staging slots (packet i
+    # at i*4032) -- setup, untimed
     off = torch.from_numpy((data["chunk_offset"] + data["seq_in_chunk"].astype(np.uint64) * MAX_PL)
                            .astype(np.int64)).to(dev)
     pl = torch.from_numpy(data["payload_len"].astype(np.int64)).to(dev)
-    R = max(1, args.replicas)
+    conn_of = torch.from_numpy(data["msg_tag"].astype(np.int64)).to(dev)
+    R = max(1, args.replicas if K == 1 else 2)
     srcs, stagings = [], []
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     col = torch.arange(MAX_PL, device=dev)
     for r in range(R):
-        src = torch.randint(0, 256, (msg_len,), dtype=torch.uint8, device=dev, generator=g)
+        src = torch.randint(0, 256, (K, msg_len), dtype=torch.uint8, device=dev, generator=g)
+        flat = src.view(-1)
         st = torch.zeros(n * MAX_PL, dtype=torch.uint8, device=dev)
         for a in range(0, n, 2048):
             b = min(n, a + 2048)
             pos = off[a:b, None] + col[None, :]
             mask = col[None, :] < pl[a:b, None]
-            vals = src[pos.clamp(max=msg_len - 1)]
+            vals = flat[conn_of[a:b, None] * msg_len + pos.clamp(max=msg_len - 1)]
             st.view(n, MAX_PL)[a:b] = torch.where(mask, vals, torch.zeros_like(vals))
         srcs.append(src)
         stagings.append(st)
 
     tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
-                      arena_bytes=msg_len + (1 << 20), chunk_pool=4 * ((msg_len + cb - 1) // cb),
+                      arena_bytes=K * (msg_len + (1 << 20)), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
                       max_batch=n, max_conns=64, max_msgs=64)
     stream = torch.cuda.current_stream(dev)
 
@@ -325,16 +357,22 @@ def main():
         tr.reset(s)
         tr.rx_batch_async(hdrs, stagings[k % R], MAX_PL, s)
 
+    def check_buffers(r):
+        arena = tr.arena()
+        cp = tr.completions_np(K)
+        assert len(cp) == K
+        for c in cp:
+            o = int(c["buf_offset"])
+            assert torch.equal(arena[o: o + msg_len], srcs[r][int(c["tag"])]), \
+                "reassembled message != source"
+
     # correctness gate before timing: ack count + reassembled bytes
     tr.reset(stream)
     out = tr.handle_packets(hdrs, stagings[0], MAX_PL, stream)
-    arena = tr.arena()
-    c0 = out.completions_np()[0]
-    assert torch.equal(arena[int(c0["buf_offset"]): int(c0["buf_offset"]) + msg_len], srcs[0]), \
-        "reassembled message != source"
+    check_buffers(0)
     n_acks = int(out.result.n_acks)
     bytes_copied = int(out.result.bytes_copied)
-    assert bytes_copied == msg_len
+    assert bytes_copied == K * msg_len
     launches = tr.last_launches() + 1  # + the reset kernel
 
     # one CUDA graph per staging replica: reset + the 4 receive kernels
@@ -372,17 +410,15 @@ def main():
         torch.cuda.synchronize()
         tr.set_profiling(False)
         prof, nb = tr.kernel_profile(reset=True)
-    # last step's buffer must equal its source (the work was really done)
-    last = (args.steps - 1) % R
-    assert torch.equal(tr.arena()[int(c0["buf_offset"]): int(c0["buf_offset"]) + msg_len],
-                       srcs[last])
+    # last step's buffers must equal their sources (the work was really done)
+    check_buffers((args.steps - 1) % R)
 
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ms_step = ms_max / args.steps
-    value = world * msg_len * args.steps / (ms_max * 1e-3) / 1e9
+    value = world * K * msg_len * args.steps / (ms_max * 1e-3) / 1e9
     mpkts = world * n * args.steps / (ms_max * 1e-3) / 1e6
 
     # roofline of the dominant kernel (k_copy: the payload scatter)
@@ -425,7 +461,7 @@ def main():
         te = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(world * msg_len * args.steps / (float(te.item()) * 1e-3) / 1e9, 3),
+        e2e = {"value": round(world * K * msg_len * args.steps / (float(te.item()) * 1e-3) / 1e9, 3),
                "unit": "GB/s", "h2d_bytes_per_step": int(hdrs.numel() + stagings[0].numel()),
                "d2h_bytes_per_step": int(n_acks * ACK + 24),
                "path": "pinned host records+staging -> cn_rx_batch (C ABI) -> acks to host"}
@@ -443,8 +479,9 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "reference DES trace + random payload",
-            "config": {"workload": f"{args.workload}: BASELINE configs[1], 64 MiB message, "
-                                   f"256 paths, 1% drop; {n} pkts, {n_acks} acks, chunk {cb} B",
+            "config": {"workload": f"{args.workload}: BASELINE configs[1] (64 MiB message, "
+                                   f"256 paths, 1% drop) x {K} concurrent connections per batch "
+                                   f"(round-robin interleaved); {n} pkts, {n_acks} acks, chunk {cb} B",
                        "l2": f"inputs larger than L2: {R} rotating staging replicas "
                              f"({R * n * MAX_PL / 1e6:.0f} MB) + 64 MiB output per step",
                        "parallelism": f"replicas x{world} (shard by connection)"},

@@ -201,6 +201,10 @@ class Transport:
         _lib.check(_lib.lib().cn_rx_post(self._h, tag, buf.data_ptr(), buf.numel() * buf.element_size(),
                                           ctypes.c_void_p(s.cuda_stream)), "cn_rx_post")
 
+    def completions_np(self, n):
+        """The first n completion records of the last batch (host copy)."""
+        return self._cpls[: n * 64].cpu().numpy().view(CPL_DTYPE)
+
     def set_profiling(self, enable=True):
         _lib.lib().cn_rx_set_profiling(self._h, 1 if enable else 0)
 

@@ -159,3 +159,34 @@ def test_rx_rejects_trimmed_packets_loudly():
     tr = _transport(meta, carry=False)
     with pytest.raises(cn.ChunknetError):
         tr.handle_packets(cn.to_device_records(d2), None)
+
+
+def test_rx_interleaved_connections_independent():
+    """Three concurrent connections (cfg1 copies from distinct source hosts,
+    round-robin interleaved): each connection's ack subsequence equals the
+    single-connection reference stream."""
+    import paper_2504_17307_b200 as cn
+    data, acks_ref, cpls_ref, meta = load_golden("cfg1")
+    K = 3
+    mix = np.empty(len(data) * K, dtype=data.dtype)
+    for j in range(K):
+        c = data.copy()
+        c["src"] = j
+        c["msg_tag"] = 100 + j
+        mix[j::K] = c
+    tr = _transport(meta)
+    hd, pl = _dev(mix)
+    out = tr.handle_packets(hd, pl)
+    a = out.acks_np()
+    for j in range(K):
+        sub = a[a["dst"] == j].copy()
+        sub["pkt_index"] = (sub["pkt_index"] - j) // K
+        want = acks_ref.copy()
+        want["dst"] = j
+        ok, bad = ack_equal(sub, want)
+        assert ok, (j, bad)
+    assert len(out.completions_np()) == K
+    arena = tr.arena()
+    for c in out.completions_np():
+        buf = arena[int(c["buf_offset"]): int(c["buf_offset"]) + int(c["len"])].cpu().numpy()
+        assert (buf == O.pattern_bytes(int(c["len"]), int(c["tag"]))).all()

@@ -233,6 +233,11 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
                 cbase = G->chunk_base;
                 glen = G->len;
                 if (atomicExch(&G->epoch, epoch) != epoch) {
+                    // first touch this batch: freeze the batch's lower bound
+                    // (finalize advances cum) and clear the tile counters
+                    G->lo_batch = G->cum;
+                    G->tiles_done = 0;
+                    G->cum_add = 0;
                     uint32_t k = atomicAdd(&d.ctl->n_touched, 1u);
                     d.touched[k] = gs;
                 }
@@ -282,58 +287,6 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
         atomicMax(&d.gen[gs].touch, (static_cast<unsigned long long>(epoch) << 32) | gm);
     status = __reduce_or_sync(0xffffffffu, status);
     if (lane == 0 && status) atomicOr(&d.ctl->status, status);
-    // ---- plan (last block): per touched message the batch's chunk range
-    // [cum, hi) and its first scan tile; hi = the chunk vector size (:637)
-    __shared__ bool s_last;
-    __shared__ uint32_t s_wsum[8], s_carry;
-    __threadfence();  // every thread's table/list writes ...
-    __syncthreads();  // ... are done before the block reports in
-    if (threadIdx.x == 0) s_last = atomicAdd(&d.ctl->ingest_done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const uint32_t nt = __ldcg(&d.ctl->n_touched);
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (uint32_t k0 = 0; k0 < nt; k0 += blockDim.x) {
-        const uint32_t k = k0 + threadIdx.x;
-        uint32_t tl = 0;
-        if (k < nt) {
-            GenState* G = &d.gen[__ldcg(&d.touched[k])];
-            const unsigned long long tch = __ldcg(&G->touch);
-            const uint32_t lo = __ldcg(&G->cum);
-            uint32_t hi = __ldcg(&G->n_init);
-            if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
-            G->lo_batch = lo;
-            G->n_init = hi;
-            G->deliver_t = kInf;
-            G->tiles_done = 0;
-            G->cum_add = 0;
-            tl = (hi - lo + kScanThreads - 1) / kScanThreads;
-        }
-        // block exclusive sum of tile counts
-        uint32_t inc = tl;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        const int w = threadIdx.x >> 5;
-        if (lane == 31) s_wsum[w] = inc;
-        __syncthreads();
-        uint32_t wpre = 0;
-        for (int q = 0; q < w; ++q) wpre += s_wsum[q];
-        const uint32_t carry = s_carry;
-        if (k < nt) d.plan_base[k] = carry + wpre + inc - tl;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) s_carry = carry + wpre + inc;
-        __syncthreads();
-    }
-    const uint32_t total = s_carry;
-    for (uint32_t x = threadIdx.x; x < total; x += blockDim.x) d.scan_state[x] = 0;
-    if (threadIdx.x == 0) {
-        d.ctl->n_scan_tiles = total;
-        d.ctl->ingest_done = 0;
-    }
 }
 
 
@@ -372,11 +325,64 @@ __device__ __forceinline__ uint32_t block_scan_max(uint32_t v, uint32_t* wsum) {
 // pmax that drives the cumulative cursor (chunk_completed's
 // `while (complete) ++cum`, :736-738) -- a segmented decoupled look-back
 // across the message's tiles.
-__device__ __forceinline__ uint32_t find_gen_of_ticket(const RxDev& d, uint32_t nt, uint32_t ticket) {
-    uint32_t lo = 0, hi = nt;  // last k with plan_base[k] <= ticket
+constexpr uint32_t kPlanMax = 4096;  // touched messages per batch planned in smem
+
+// Every scan/finalize block plans the batch itself (no serial phase): for
+// each touched message its chunk range [lo, hi) -- hi = the chunk vector
+// size (:636-637) -- and the first tile index, as an exclusive prefix sum in
+// shared memory.  Returns the total tile count.  In k_scan lo = cum and hi
+// = max(n_init, max touched chunk + 1); k_finalize reads the values k_scan
+// stored (lo_batch, n_init), so both see the same tiles.
+__device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool scan,
+                               uint32_t* s_base, uint32_t* s_w) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t carry = 0;
+    for (uint32_t k0 = 0; k0 < nt; k0 += blockDim.x) {
+        const uint32_t k = k0 + threadIdx.x;
+        uint32_t tl = 0;
+        if (k < nt) {
+            const GenState* G = &d.gen[d.touched[k]];
+            uint32_t lo, hi;
+            if (scan) {
+                lo = G->cum;
+                hi = G->n_init;
+                const unsigned long long tch = G->touch;
+                if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
+            } else {
+                lo = G->lo_batch;
+                hi = G->n_init;
+                // a delivered message is retired whole: its chunk state is
+                // never read again (pool entries are reclaimed by reset)
+                if (G->deliver_t != kInf) hi = lo;
+            }
+            tl = (hi - lo + kScanThreads - 1) / kScanThreads;
+        }
+        uint32_t inc = tl;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_w[w] = inc;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+        for (int q = 0; q < nw; ++q) {
+            if (q < w) wpre += s_w[q];
+            tot += s_w[q];
+        }
+        if (k < nt) s_base[k] = carry + wpre + inc - tl;
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) s_base[nt] = carry;
+    __syncthreads();
+    return carry;
+}
+
+__device__ __forceinline__ uint32_t find_gen_of_ticket(const uint32_t* s_base, uint32_t nt, uint32_t ticket) {
+    uint32_t lo = 0, hi = nt;  // last k with s_base[k] <= ticket
     while (hi - lo > 1) {
         uint32_t mid = (lo + hi) >> 1;
-        if (__ldcg(&d.plan_base[mid]) <= ticket) lo = mid; else hi = mid;
+        if (s_base[mid] <= ticket) lo = mid; else hi = mid;
     }
     return lo;
 }
@@ -384,23 +390,33 @@ __device__ __forceinline__ uint32_t find_gen_of_ticket(const RxDev& d, uint32_t 
 __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t s_ticket, s_k, s_carry;
+    __shared__ uint32_t s_base[kPlanMax + 1];
     const int lane = threadIdx.x & 31;
-    const uint32_t total = d.ctl->n_scan_tiles;
-    const uint32_t nt = d.ctl->n_touched;
+    const uint32_t epoch = d.ctl->epoch;
+    const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
     const uint32_t ppc = d.ppc;
+    const uint32_t total = plan_block(d, nt, epoch, true, s_base, wsum);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && d.ctl->n_touched > kPlanMax)
+        atomicOr(&d.ctl->status, CN_RXF_CAPACITY);
     for (;;) {
         if (threadIdx.x == 0) {
             uint32_t tk = atomicAdd(&d.ctl->scan_ticket, 1u);
             s_ticket = tk;
-            s_k = tk < total ? find_gen_of_ticket(d, nt, tk) : 0;
+            s_k = tk < total ? find_gen_of_ticket(s_base, nt, tk) : 0;
         }
         __syncthreads();
         const uint32_t ticket = s_ticket;
         if (ticket >= total) break;
         const uint32_t k = s_k;
         GenState* G = &d.gen[d.touched[k]];
-        const uint32_t lo = G->lo_batch, hi = G->n_init;
-        const uint32_t ti = ticket - d.plan_base[k];
+        const uint32_t ti = ticket - s_base[k];
+        const uint32_t lo = G->cum;
+        uint32_t hi = G->n_init;
+        {
+            const unsigned long long tch = G->touch;
+            if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
+        }
+
         const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
         const uint64_t base = G->chunk_base;
         uint32_t cpl = 0;
@@ -462,7 +478,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
             const uint32_t carry = s_carry;
             const uint32_t pm = incl > carry ? incl : carry;
             d.c_pmax[base + c] = pm;
-            if (c == hi - 1) G->deliver_t = hi == G->nchunks ? pm : kInf;
+            if (c == hi - 1) {
+                G->deliver_t = hi == G->nchunks ? pm : kInf;
+                G->n_init = hi;  // every tile computes the same hi: idempotent
+            }
         }
         __syncthreads();
     }
@@ -899,14 +918,16 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
                                                            cn_rx_result* res) {
     __shared__ uint32_t s_ticket, s_k, s_cnt;
     __shared__ bool last_block;
-    const uint32_t total = d.ctl->n_scan_tiles;
-    const uint32_t nt = d.ctl->n_touched;
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_base[kPlanMax + 1];
+    const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
     const uint32_t ppc = d.ppc;
+    const uint32_t total = plan_block(d, nt, 0, false, s_base, s_w);
     for (;;) {
         if (threadIdx.x == 0) {
             uint32_t tk = atomicAdd(&d.ctl->fin_ticket, 1u);
             s_ticket = tk;
-            s_k = tk < total ? find_gen_of_ticket(d, nt, tk) : 0;
+            s_k = tk < total ? find_gen_of_ticket(s_base, nt, tk) : 0;
             s_cnt = 0;
         }
         __syncthreads();
@@ -916,10 +937,11 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         const uint32_t g = d.touched[k];
         GenState* G = &d.gen[g];
         const uint32_t lo = G->lo_batch, hi = G->n_init;
-        const uint32_t ti = ticket - d.plan_base[k];
+        const uint32_t ti = ticket - s_base[k];
         const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
         const uint64_t base = G->chunk_base;
         uint32_t done = 0;
+        if (threadIdx.x == 0) d.scan_state[ticket] = 0;  // re-arm the look-back state
         if (c < hi) {
             const uint64_t e = base + c;
             uint32_t fl = d.c_flags[e];
@@ -956,15 +978,20 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             if (atomicAdd(&G->tiles_done, 1u) == ntiles - 1) {
                 __threadfence();
                 G->cum = lo + atomicAdd(&G->cum_add, 0u);
-                if (G->deliver_t != kInf) {
-                    atomicMax(&d.rc_done[G->rc * 128 + G->msg_id],
-                              static_cast<unsigned long long>(G->seq));
-                    d.gen_key[g] = kTomb;
-                }
             }
         }
         __syncthreads();
     }
+    // ---- delivered messages: completed_seq (:801) and retirement
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
+        const uint32_t g = d.touched[k];
+        GenState* G = &d.gen[g];
+        if (G->deliver_t != kInf) {
+            atomicMax(&d.rc_done[G->rc * 128 + G->msg_id], static_cast<unsigned long long>(G->seq));
+            d.gen_key[g] = kTomb;
+        }
+    }
+    __syncthreads();
     // ---- batch epilogue (last block)
     if (threadIdx.x == 0) {
         __threadfence();
@@ -989,7 +1016,6 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->n_cpls = 0;
         C->scan_ticket = 0;
         C->fin_ticket = 0;
-        C->n_scan_tiles = 0;
         uint32_t ep = C->epoch + 1;
         C->epoch = ep ? ep : 1;
     }
@@ -1023,6 +1049,8 @@ __global__ void k_reset(RxDev d, int full) {
         d.c_newfl[x] = 0;
     }
     for (uint64_t x = tid; x < top * d.ppc; x += stride) d.c_first[x] = kInf;
+    if (full)
+        for (uint64_t x = tid; x < d.pool_cap / kScanThreads + ngen + 2; x += stride) d.scan_state[x] = 0;
     if (tid == 0) {
         d.ctl->pool_top = 0;
         d.ctl->arena_top = 0;

@@ -206,6 +206,61 @@ def sched_bench(dev, steps=20, conns=1024, paths=256, per_call=4096):
     return r
 
 
+def sender_bench(dev, conns=1024, scenario="cfg1", reps=3):
+    """B1-B6 rows: the device sender engine (csrc/tx.cu) replaying, on each
+    of `conns` connections, the recorded sender scenario (submissions + the
+    acks the reference DES delivered, tests/golden/sender_<scenario>.npz):
+    ack processing, fast retransmit, RTO, commit/egress with path draws."""
+    import torch
+
+    from paper_2504_17307_b200.sender import TxEngine
+    z = np.load(os.path.join(ROOT, "tests", "golden", f"sender_{scenario}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    acks, subs = z["acks"], z["submits"]
+    ev = [(int(x["t"]), 0, k) for k, x in enumerate(subs)] + [(int(a["aux"]), 1, k) for k, a in enumerate(acks)]
+    ev.sort()
+    one = [(typ, k) for _, typ, k in ev]
+    ms = []
+    for r in range(reps + 1):
+        eng = TxEngine(conns, chunk_bytes=meta["chunk_bytes"], rto_min=meta["rto_min"],
+                       rto_max=meta["rto_max"], commit_ahead=meta["commit_ahead"],
+                       base_rtt_ns=meta["base_rtt"], seed=meta["seed"], lb=meta["lb"],
+                       max_paths=meta["n_paths"], src=[meta["src"]] * conns, dst=[meta["dst"]] * conns,
+                       chunk_pool=conns * 2048, log_cap=max(1024, len(z["tx"]) + 16), device=dev)
+        prep = eng.prepare([one] * conns, subs, acks)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        eng.launch(prep, 60_000_000_000)
+        e1.record()
+        torch.cuda.synchronize()
+        st = eng.stats_np()
+        if r:
+            ms.append(e0.elapsed_time(e1))
+        ok = int(st[0]["chunk_rtx"]) == meta["stats"]["chunk_rtx"]
+        eng.close()
+    t = min(ms) * 1e-3
+    n_tx = len(z["tx"]) * conns
+    out = {"config": f"{conns} connections x sender_{scenario} ({len(acks)} acks, {len(z['tx'])} "
+                     f"transmissions each; CC none)", "acks_per_s": round(conns * len(acks) / t, 1),
+           "tx_decisions_per_s": round(n_tx / t, 1), "ms": round(t * 1e3, 3), "parity_chunk_rtx": ok,
+           "note": "device-resident event streams; one cn_tx_run launch timed with CUDA events"}
+    try:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            kw = {k: meta[k] for k in ("chunk_bytes", "lb", "seed")}
+            topo_arg = 32 if meta["n_paths"] > 16 else 8
+            tc = ref.sender_replay_bench(acks, [(int(x["t"]), int(x["len"]), int(x["tag"])) for x in subs],
+                                         meta["src"], meta["dst"], threads, 20, topo_arg=topo_arg,
+                                         paths=meta["n_paths"], **kw)
+            out["cpu_reference_acks_per_s"] = round(threads * 20 * len(acks) / tc, 1)
+            out["cpu_threads"] = threads
+    except Exception as e:  # noqa: BLE001
+        out["cpu_reference_error"] = str(e)
+    return out
+
+
 def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30):
     """BASELINE configs[2]: ring all-reduce of 1 GiB per rank (fp32 and bf16)
     through the transport (packetize -> NVLink zero-copy fused-reduce receive
@@ -467,6 +522,7 @@ def main():
                "path": "pinned host records+staging -> cn_rx_batch (C ABI) -> acks to host"}
 
     sched = sched_bench(dev) if not args.no_sched else None
+    sender = sender_bench(dev) if not args.no_sched and rank == 0 else None
     ring = ring_bench(dev, world, rank) if world > 1 and not args.no_ring else None
 
     cpu = None
@@ -501,6 +557,8 @@ def main():
             line["e2e"] = e2e
         if sched:
             line["scheduler"] = sched
+        if sender:
+            line["sender"] = sender
         if ring:
             line["allreduce"] = ring
         if cpu:

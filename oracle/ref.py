@@ -98,6 +98,9 @@ def lib():
         L.cnref_rx_replay_bench.restype = ctypes.c_double
         L.cnref_sender_replay.argtypes = [ctypes.POINTER(Scenario), i32, i32, vp, u64, vp, u64,
                                           vp, u64, ctypes.POINTER(SenderStats)]
+        L.cnref_sender_replay_bench.argtypes = [ctypes.POINTER(Scenario), i32, i32, vp, u64, vp,
+                                                u64, i32, i32]
+        L.cnref_sender_replay_bench.restype = ctypes.c_double
         L.cnref_rng_u64.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
         L.cnref_next_below.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]
         L.cnref_next_double.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
@@ -161,6 +164,19 @@ def sender_replay(acks, submits, src, dst, *, topo="fat_tree", topo_arg=8, rate_
     if rc != 0:
         raise RuntimeError(lib().cnref_last_error().decode())
     return out[: min(st.n_tx, max_out)].copy(), {k: getattr(st, k) for k, _ in SenderStats._fields_}
+
+
+def sender_replay_bench(acks, submits, src, dst, threads=1, reps=1, *, topo="fat_tree",
+                        topo_arg=8, rate_bps=400e9, link_delay_ns=1000, qcap_bytes=1 << 20, seed=1,
+                        chunk_bytes=32768, paths=8, lb="p2_rtt", dupack_threshold=8,
+                        cutoff_ns=60_000_000_000):
+    sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns, qcap_bytes, 0.0,
+                  seed, chunk_bytes, paths, LB[lb], CC["none"], 0, 1, 0, dupack_threshold, 0, 0, 1,
+                  cutoff_ns)
+    sb = (Submit * max(1, len(submits)))(*[Submit(int(t), int(l), int(g)) for t, l, g in submits])
+    acks = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
+    return lib().cnref_sender_replay_bench(ctypes.byref(sc), src, dst, ctypes.cast(sb, ctypes.c_void_p),
+                                           len(submits), _ptr(acks), len(acks), threads, reps)
 
 
 def rx_replay(recs, n_hosts, chunk_bytes, carry_payload=True, arena_bytes=None):

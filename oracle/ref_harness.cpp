@@ -551,6 +551,58 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
     }
 }
 
+// Times the reference sender on the same replay (construction and event
+// scheduling outside the timer): T threads x reps replays.  Returns the
+// slowest thread's seconds.
+double cnref_sender_replay_bench(const cnref_scenario* sc, int src, int dst,
+                                 const cnref_submit* subs, uint64_t n_subs,
+                                 const cn_ack_rec* acks, uint64_t n_acks, int threads,
+                                 int reps) {
+    std::vector<double> secs(threads, 0.0);
+    auto work = [&](int t) {
+        Topology topo =
+            sc->topo_kind == 0 ? build_star(sc->topo_arg) : build_fat_tree(sc->topo_arg);
+        double total = 0;
+        for (int r = 0; r < reps; ++r) {
+            NetParams np;
+            np.rate_bps = sc->rate_bps;
+            np.link_delay_ns = sc->link_delay_ns;
+            np.qcap_bytes = sc->qcap_bytes;
+            EventQueue eq;
+            Network net(topo, np, eq, sc->seed);
+            net.inject_loss_at_host_egress(1.0);
+            TransportConfig tc;
+            tc.chunk_bytes = sc->chunk_bytes;
+            tc.paths = sc->paths;
+            tc.lb = static_cast<LbPolicy>(sc->lb);
+            tc.engines = 1;
+            tc.dupack_threshold = sc->dupack_threshold;
+            Transport tr(net, eq, tc, sc->seed);
+            for (uint64_t k = 0; k < n_subs; ++k) {
+                cnref_submit sb = subs[k];
+                eq.schedule(sb.t, [&tr, src, dst, sb] { tr.send_message(src, dst, sb.len, sb.tag); });
+            }
+            for (uint64_t k = 0; k < n_acks; ++k) {
+                cn_ack_rec a = acks[k];
+                eq.schedule(a.aux, [&tr, a] {
+                    Packet p = from_ack(a);
+                    int host = p.dst;
+                    tr.handle_packet(host, std::move(p));
+                });
+            }
+            auto t0 = std::chrono::steady_clock::now();
+            eq.run_until_idle(sc->cutoff_ns);
+            auto t1 = std::chrono::steady_clock::now();
+            total += std::chrono::duration<double>(t1 - t0).count();
+        }
+        secs[t] = total;
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < threads; ++t) th.emplace_back(work, t);
+    for (auto& x : th) x.join();
+    return *std::max_element(secs.begin(), secs.end());
+}
+
 // ------------------------------------------------------------- RNG draws
 void cnref_rng_u64(uint64_t seed, const char* name, int64_t index, uint64_t count,
                    uint64_t* out) {

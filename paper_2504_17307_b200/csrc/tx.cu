@@ -55,6 +55,7 @@ struct TxConn {
     uint64_t next_seq, chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_sent, msgs_completed, backpressured;
     int32_t has_sample, backoff, timer_armed, n_free, fq_head, fq_count, src, dst, conn_id,
         n_paths, live_msgs, pad0;
+    uint32_t live_mask[4];  // message slots in use (bit = msg id)
     uint8_t free_ids[128];
     uint8_t fq[128];
     TxMsg msgs[128];
@@ -92,6 +93,7 @@ struct Tx {
     int64_t srtt, rttvar, armed_at, timer_at, committed_unsent;
     int has_sample, backoff, timer_armed;
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_completed;
+    uint32_t live[4];  // live message slots, iterated in slot order
 
     __device__ int64_t cur_rto() const {  // cc.hpp:27-33 via transport.cpp:1078-1081
         int64_t x = srtt + 4 * rttvar;
@@ -182,9 +184,10 @@ __device__ __forceinline__ void store_msg(TxConn* C, uint32_t mid, const TxMsg& 
 __device__ uint32_t egress(Tx& x, int64_t now) {
     uint32_t sent = 0;
     for (int pass = 0; pass < 2; ++pass) {
-        for (uint32_t mid = 0; mid < 128; ++mid) {
+        for (uint32_t q = 0; q < 4; ++q)
+        for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
+            const uint32_t mid = q * 32 + __ffs(lb) - 1;
             TxMsg m = load_msg(x.C, mid);
-            if (!m.live) continue;
             for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
                 uint32_t ci = w0 + x.lane;
                 uint32_t fl = ci < m.nchunks ? x.d.c_fl[m.chunk_base + ci] : (TF_SENT | TF_ACKED);
@@ -283,6 +286,7 @@ __device__ void msg_finished(Tx& x, uint32_t mid) {
     TxMsg m;
     memset(&m, 0, sizeof m);
     store_msg(C, mid, m, x.lane);
+    x.live[mid >> 5] &= ~(1u << (mid & 31));
     if (x.lane == 0) {
         C->free_ids[C->n_free] = static_cast<uint8_t>(mid);
         C->n_free += 1;
@@ -409,9 +413,10 @@ __device__ void rto_fire(Tx& x) {
     int64_t best = 0;
     bool have = false;
     uint32_t n_exp = 0;
-    for (uint32_t mid = 0; mid < 128; ++mid) {
+    for (uint32_t q = 0; q < 4; ++q)
+    for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
+        const uint32_t mid = q * 32 + __ffs(lb) - 1;
         TxMsg m = load_msg(C, mid);
-        if (!m.live) continue;
         for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
             uint32_t ci = w0 + x.lane;
             bool elig = false;
@@ -446,9 +451,10 @@ __device__ void rto_fire(Tx& x) {
     ++x.rtos;
     x.backoff = x.backoff * 2 < kBackoffCap ? x.backoff * 2 : kBackoffCap;
     // queue_rtx for every expired chunk in scan order (:1154-1164)
-    for (uint32_t mid = 0; mid < 128; ++mid) {
+    for (uint32_t q = 0; q < 4; ++q)
+    for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
+        const uint32_t mid = q * 32 + __ffs(lb) - 1;
         TxMsg m = load_msg(C, mid);
-        if (!m.live) continue;
         for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
             uint32_t ci = w0 + x.lane;
             bool ex = false;
@@ -500,6 +506,7 @@ __device__ void submit(Tx& x, int64_t now, const cn_tx_submit& s) {
     m.live = 1;
     m.in_factory = 1;
     store_msg(C, mid, m, x.lane);
+    x.live[mid >> 5] |= 1u << (mid & 31);
     if (x.lane == 0) {
         C->n_free -= 1;
         C->live_msgs += 1;
@@ -550,6 +557,7 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
     x.fast_rtx = C->fast_rtx;
     x.rtos = C->rtos;
     x.msgs_completed = C->msgs_completed;
+    for (int q = 0; q < 4; ++q) x.live[q] = C->live_mask[q];
     for (uint32_t k = ev_off[conn]; k < ev_off[conn + 1]; ++k) {
         const uint64_t ev = events[k];
         const uint32_t type = static_cast<uint32_t>(ev >> 62);
@@ -587,6 +595,7 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
         C->fast_rtx = x.fast_rtx;
         C->rtos = x.rtos;
         C->msgs_completed = x.msgs_completed;
+        for (int q = 0; q < 4; ++q) C->live_mask[q] = x.live[q];
         log_n[conn] = x.log_n;
         cn_tx_stats st;
         st.chunks_sent = x.chunks_sent;

@@ -61,9 +61,10 @@ class TxEngine:
         except Exception:
             pass
 
-    def run(self, events_per_conn, submits, acks, end_time, stream=None):
-        """events_per_conn: list (per connection) of lists of (type, index),
-        type 0 = submits[index], 1 = acks[index], already time-ordered."""
+    def prepare(self, events_per_conn, submits, acks):
+        """Device copies of the event streams.  events_per_conn: list (per
+        connection) of lists of (type, index), type 0 = submits[index],
+        1 = acks[index], time-ordered."""
         off = np.zeros(self.n + 1, dtype=np.uint32)
         ev = []
         for c, evs in enumerate(events_per_conn):
@@ -76,11 +77,20 @@ class TxEngine:
         t_sub = torch.from_numpy(sub.view(np.uint8).copy() if len(sub) else np.zeros(24, np.uint8)).to(dev)
         ak = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
         t_ack = torch.from_numpy(ak.view(np.uint8).copy() if len(ak) else np.zeros(64, np.uint8)).to(dev)
-        s = stream or torch.cuda.current_stream(dev)
+        return (t_off, t_ev, t_sub, t_ack)
+
+    def launch(self, prepared, end_time, stream=None):
+        """Enqueue cn_tx_run on prepared device events (no synchronisation)."""
+        t_off, t_ev, t_sub, t_ack = prepared
+        s = stream or torch.cuda.current_stream(self.device)
         _lib.check(_lib.lib().cn_tx_run(self._h, t_off.data_ptr(), t_ev.data_ptr(), t_sub.data_ptr(),
                                         t_ack.data_ptr(), int(end_time), self.log.data_ptr(),
                                         self.stats.data_ptr(), ctypes.c_void_p(s.cuda_stream)),
                    "cn_tx_run")
+
+    def run(self, events_per_conn, submits, acks, end_time, stream=None):
+        s = stream or torch.cuda.current_stream(self.device)
+        self.launch(self.prepare(events_per_conn, submits, acks), end_time, s)
         s.synchronize()
         st = ctypes.c_uint()
         _lib.lib().cn_tx_status(self._h, ctypes.byref(st))

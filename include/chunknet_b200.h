@@ -266,6 +266,10 @@ int cn_sched_record(cn_sched* s, const uint32_t* d_conn, const int32_t* d_path, 
  * Path choices (commits and retransmissions) come from the connection's
  * RngStream("transport.conn", stream_index0 + c) and are bit-identical to
  * the reference. */
+/* congestion control on the device (CcConfig::Algo, cc.hpp); global scope.
+ * CUBIC is not offered on the device: std::cbrt has no bit-identical
+ * device counterpart, so it stays with the host reference. */
+enum { CN_CC_NONE = 0, CN_CC_SWIFT = 2 };
 typedef struct cn_tx_config {
     uint32_t chunk_bytes;         /* TransportConfig::chunk_bytes            */
     uint32_t max_payload;         /* 0 = CN_MAX_PAYLOAD                      */
@@ -282,6 +286,12 @@ typedef struct cn_tx_config {
     uint64_t seed;                /* Transport seed                          */
     int64_t stream_index0;        /* connection c uses stream index0 + c     */
     uint64_t chunk_pool;          /* chunk state entries                     */
+    int32_t cc_algo;              /* CN_CC_NONE (OpenLoop) | CN_CC_SWIFT     */
+    uint32_t drr_quantum;         /* TransportConfig::drr_quantum (32768)    */
+    int64_t mss;                  /* CcConfig::mss (4032)                    */
+    int64_t cap_bytes;            /* CcConfig::cap_bytes, 0 = uncapped       */
+    int64_t swift_target_ns;      /* CcConfig::swift_target_ns (resolved)    */
+    double init_cwnd_pkts;        /* CcConfig::init_cwnd_pkts (2.0)          */
 } cn_tx_config;
 typedef struct cn_tx_submit { int64_t t; uint64_t len; uint64_t tag; } cn_tx_submit;
 /* one chunk transmission (send_chunk): time, message, chunk index, path */
@@ -297,6 +307,9 @@ typedef struct cn_tx_stats {  /* Transport::Stats sender fields + estimator */
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_sent, msgs_completed, backpressured, n_log;
     int64_t srtt, rttvar;
     int32_t backoff, live_msgs;
+    int64_t cwnd_bytes;   /* CongestionControl::cwnd_bytes() at the end   */
+    int64_t inflight;     /* gated_inflight (global scope) at the end     */
+    double cwnd_pkts;     /* Swift window in packets (unused for none)    */
 } cn_tx_stats;
 typedef struct cn_tx cn_tx;
 void cn_tx_config_default(cn_tx_config* cfg);

@@ -76,6 +76,17 @@ SCENARIOS = {
     "k8_4x1m": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,
                      loss=0.01, seed=3, chunk_bytes=32768, paths=16, lb="p2_rtt",
                      cc="cubic"), [(0, 127, MiB, 4)]),
+    # closed loop under Swift: the DES sender runs Swift (target 3 x base
+    # RTT), so its recorded acks answer exactly what a Swift sender sends
+    "closed_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,
+                       loss=0.01, seed=7, chunk_bytes=32768, paths=16, lb="p2_rtt",
+                       cc="swift"), [(0, 127, MiB, 4)]),
+    "closed_w4": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=MiB,
+                       loss=0.03, seed=8, chunk_bytes=8064, paths=16, lb="p2_ecn",
+                       cc="swift", window=4), [(0, 127, 300_000, 12)]),
+    "closed_cfg2": (dict(topo="fat_tree", topo_arg=32, rate_bps=400e9, qcap_bytes=MiB,
+                         loss=0.01, seed=1, chunk_bytes=32768, paths=256, lb="p2_rtt",
+                         cc="swift"), [(0, 8191, 64 * MiB, 1)]),
 }
 
 
@@ -100,6 +111,8 @@ def gen(name, kw, flows):
                 des_stats={k: int(v) for k, v in st.items()})
     if name in SENDER_SCENARIOS:
         gen_sender(name, kw, flows, acks_des, subs)
+    if name in CLOSED_SWIFT:
+        gen_sender(name, kw, flows, acks_des, subs, cc="swift")
     path = os.path.join(GOLDEN, f"{name}.npz")
     np.savez_compressed(path, data=data, acks=acks, completions=cpls,
                         meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
@@ -114,27 +127,45 @@ SENDER_SCENARIOS = ["cfg1", "cfg2_32k", "cfg2_4k", "k8_4x1m", "multigen_k8", "lo
                     "csn_wrap"]
 
 
-def gen_sender(name, kw, flows, acks_des, subs):
-    """Sender-side golden: the reference sender (OpenLoop) fed the DES's
-    submissions and the acks the DES delivered to it, at their times."""
+def gen_sender(name, kw, flows, acks_des, subs, cc="none"):
+    """Sender-side golden: the reference sender (OpenLoop, or Swift with
+    global scope) fed the DES's submissions and the acks the DES delivered
+    to it, at their times."""
     src, dst = flows[0][0], flows[0][1]
     rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes",
                               "paths", "lb") if k in kw}
     submits = [(int(s["t"]), int(s["len"]), int(s["tag"])) for s in subs]
-    tx, st = ref.sender_replay(acks_des, submits, src, dst, cc="none", **rkw)
+    tx, st = ref.sender_replay(acks_des, submits, src, dst, cc=cc, **rkw)
     rate = kw.get("rate_bps", 400e9)
     bdp = int(round(rate * st["base_rtt"] / 8e9))
     commit_ahead = max(2 * kw["chunk_bytes"], 2 * 32768, bdp)
     meta = dict(name=name, src=src, dst=dst, chunk_bytes=kw["chunk_bytes"], lb=kw["lb"],
                 seed=kw["seed"], n_paths=int(st["n_paths"]), base_rtt=int(st["base_rtt"]),
                 rto_min=int(st["rto_min"]), rto_max=int(st["rto_max"]), commit_ahead=commit_ahead,
-                end_time=int(st["end_time"]), stats={k: int(v) for k, v in st.items()})
-    path = os.path.join(GOLDEN, f"sender_{name}.npz")
+                end_time=int(st["end_time"]), stats={k: int(v) for k, v in st.items()}, cc=cc,
+                # the harness resolves Swift's target to 3 x base RTT (ref_harness.cpp)
+                swift_target_ns=3 * int(st["base_rtt"]) if cc == "swift" else 0)
+    path = os.path.join(GOLDEN, f"sender_{name}.npz" if cc == "none" else f"sender_{cc}_{name}.npz")
     sub_arr = np.array(submits, dtype=[("t", "<i8"), ("len", "<u8"), ("tag", "<u8")])
     np.savez_compressed(path, acks=acks_des, submits=sub_arr, tx=tx,
                         meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
-    print(f"  sender_{name}: submits={len(submits)} acks={len(acks_des)} tx={len(tx)} "
+    print(f"  sender[{cc}]_{name}: submits={len(submits)} acks={len(acks_des)} tx={len(tx)} "
           f"rtx={st['chunk_rtx']} fast={st['fast_rtx']} rtos={st['rtos']} done={st['msgs_completed']}")
+
+
+# single-connection Swift DES runs replayed into the reference sender under
+# Swift: the replay must reproduce the DES sender's own transmissions
+CLOSED_SWIFT = ["closed_k8", "closed_w4", "closed_cfg2"]
+
+# Swift (device-exact CC) goldens: the same stimulus as sender_<name>.npz
+SWIFT_SCENARIOS = ["cfg1", "cfg2_32k", "k8_4x1m", "multigen_k8", "lossy_2m", "csn_wrap"]
+
+
+def gen_sender_swift(name):
+    """sender_swift_<name>.npz from the stimulus already in sender_<name>.npz."""
+    z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
+    kw, flows = SCENARIOS[name]
+    gen_sender(name, kw, flows, z["acks"], z["submits"], cc="swift")
 
 
 def gen_rng():
@@ -174,10 +205,14 @@ def gen_rng():
 
 def main(argv):
     os.makedirs(GOLDEN, exist_ok=True)
-    names = argv or list(SCENARIOS) + ["rng"]
+    names = argv or list(SCENARIOS) + ["rng", "swift"]
     for n in names:
         if n == "rng":
             gen_rng()
+            continue
+        if n == "swift":
+            for m in SWIFT_SCENARIOS:
+                gen_sender_swift(m)
             continue
         kw, flows = SCENARIOS[n]
         gen(n, kw, flows)

@@ -53,7 +53,9 @@ class TxConfig(ctypes.Structure):
                 ("rto_min", ctypes.c_int64), ("rto_max", ctypes.c_int64),
                 ("commit_ahead", ctypes.c_int64), ("base_rtt_ns", ctypes.c_double),
                 ("seed", ctypes.c_uint64), ("stream_index0", ctypes.c_int64),
-                ("chunk_pool", ctypes.c_uint64)]
+                ("chunk_pool", ctypes.c_uint64), ("cc_algo", ctypes.c_int32),
+                ("drr_quantum", ctypes.c_uint32), ("mss", ctypes.c_int64), ("cap_bytes", ctypes.c_int64),
+                ("swift_target_ns", ctypes.c_int64), ("init_cwnd_pkts", ctypes.c_double)]
 
 
 class RxResult(ctypes.Structure):

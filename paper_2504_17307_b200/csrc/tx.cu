@@ -1,31 +1,48 @@
-// tx.cu -- device sender engine: ack processing, loss detection and
-// retransmission of the selective multipath transport (sm_100a).
+// tx.cu -- device sender engine: ack processing, loss detection,
+// retransmission, congestion control and window-gated egress of the
+// selective multipath transport (sm_100a).
 //
 // Restates, per connection, the reference sender's event handling
 // (/root/reference/proj/src/transport.cpp):
-//   send_message / dispatch         :144-218   (msg ids LIFO, :127-129)
-//   pump / commit_chunks / egress   :232-431   (factory rotation, 128-chunk
-//                                               window, retransmissions first)
-//   send_chunk                      :433-494   (attempts, tx_time, deadline)
-//   queue_rtx                       :516-542   (path via on_tx_rtx_chunk)
-//   release_chunk / advance / finish:807-847
-//   handle_ack                      :849-942   (cause release + RTT sample,
-//                                               cumulative + SACK release,
-//                                               dup hints -> fast retransmit)
-//   cur_rto / arm_rto / rto_fire    :1078-1169 (backoff x2 capped at 64)
-//   RttEstimator                    cc.hpp:12-35
-// for the configuration the survey fixes for sender parity:
-// congestion control none (OpenLoop: cwnd never gates, RTT samples still
-// feed the RTO), one engine per host, DefaultPolicy.  Every send happens at
-// the time of the event that triggers it, exactly as the reference's
-// synchronous pump.
+//   send_message / dispatch          :144-218   (msg ids LIFO, :127-129)
+//   pump / commit_chunks             :232-310   (factory rotation, 128-chunk
+//                                                window stall, commit_ahead,
+//                                                path bound at commit)
+//   can_send / gated_inflight        :312-325   (global CC scope)
+//   egress                           :329-431   (retransmission queues in
+//                                                ring order, then deficit
+//                                                round robin over the ring)
+//   send_chunk                       :433-494   (attempts, tx_time, deadline)
+//   queue_rtx                        :516-542   (path via on_tx_rtx_chunk)
+//   release_chunk / advance / finish :807-847
+//   handle_ack                       :849-942   (cause release + RTT sample,
+//                                                cumulative + SACK release,
+//                                                dup hints -> fast retransmit)
+//   cur_rto / arm_rto / rto_fire     :1078-1169 (backoff x2 capped at 64)
+//   RttEstimator                     cc.hpp:12-35
+//   OpenLoop / Swift                 cc.cpp:19-34, :108-156
+// for one engine per host, global CC scope, DefaultPolicy (no pacing).
+// Swift is device-exact: its update uses IEEE double + - * / only, each
+// rounded explicitly (__d*_rn, no contraction), in the reference's
+// evaluation order.  CUBIC stays host-side: std::cbrt has no bit-identical
+// device counterpart.
 //
 // One warp per connection consumes a time-ordered stream of events (message
 // submissions, acks delivered at the sender) and fires its own RTO timer in
-// between.  Control flow is warp-uniform; the chunk-window scans (cumulative
-// and SACK release, duplicate hints, base advance, the RTO expiry scan) run
-// one chunk per lane with ballots; path choices come from the connection's
-// RngStream (rng.cuh), bit-identical to the reference.
+// between (timers scheduled during the run fire after same-time events).
+// Control flow is warp-uniform; chunk-window scans run one chunk per lane
+// with ballots; per-path inflight, deficits and queue depths sit in shared
+// memory; path choices come from the connection's RngStream (rng.cuh),
+// bit-identical to the reference.
+//
+// Queues.  Each chunk carries a queue tag c_q = kind | seq (seq from a
+// per-connection counter, 0 = not queued).  The front of path p's tx or
+// retransmission queue is the queued chunk of that kind on p with the
+// smallest seq -- the reference's FIFO order.  The reference's queues can
+// also hold stale entries (a chunk acked while awaiting retransmission);
+// egress pops those without effect, and a stale entry never outlives the
+// next egress that sends a fresh chunk (every rtx queue is drained first
+// while the window is open), so it can never alias a reused message id.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -41,9 +58,13 @@
 namespace cnb {
 
 enum : uint32_t { TF_SENT = 1, TF_ACKED = 2, TF_RTXP = 4 };
-constexpr int kTxWindow = 128;   // kCsnWindow (transport.cpp:14)
-constexpr int kBackoffCap = 64;  // kBackoffCap (transport.cpp:15)
+constexpr uint32_t kQRtx = 0x80000000u;  // c_q kind bit: retransmission queue
+constexpr int kTxWindow = 128;           // kCsnWindow (transport.cpp:14)
+constexpr int kBackoffCap = 64;          // kBackoffCap (transport.cpp:15)
 constexpr int kTxWarps = 4;
+constexpr int64_t kNeverDecreased = LLONG_MIN / 2;  // cc.cpp:17
+// cc.cpp:11-16
+constexpr double kSwiftAi = 1.0, kSwiftMdScale = 0.8, kSwiftMaxMd = 0.5, kMinCwndPkts = 1.0;
 
 struct TxMsg {
     uint64_t seq, tag, len, chunked, chunk_base;
@@ -51,10 +72,14 @@ struct TxMsg {
 };
 
 struct TxConn {
-    int64_t srtt, rttvar, armed_at, timer_at, committed_unsent;
-    uint64_t next_seq, chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_sent, msgs_completed, backpressured;
+    int64_t srtt, rttvar, armed_at, timer_at, committed_unsent, total_inflight, last_decrease;
+    uint64_t next_seq, chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_sent, msgs_completed, backpressured,
+        ring_pos;
+    double w;  // Swift window, packets
     int32_t has_sample, backoff, timer_armed, n_free, fq_head, fq_count, src, dst, conn_id,
-        n_paths, live_msgs, pad0;
+        n_paths, live_msgs, ring_len;
+    uint32_t q_seq, pump_pending;
+    int64_t pump_at;
     uint32_t live_mask[4];  // message slots in use (bit = msg id)
     uint8_t free_ids[128];
     uint8_t fq[128];
@@ -62,8 +87,9 @@ struct TxConn {
 };
 
 struct TxDev {
-    uint32_t n_conns, cb, max_pl, dupack, avoid_prev, policy, max_inflight, log_cap;
-    int64_t rto_min, rto_max, commit_ahead;
+    uint32_t n_conns, cb, max_pl, dupack, avoid_prev, policy, max_inflight, log_cap, cc_algo, quantum;
+    int64_t rto_min, rto_max, commit_ahead, swift_target, mss, cap_bytes;
+    double init_cwnd, cap_pkts;
     uint64_t pool_cap;
     TxConn* conns;
     int32_t* c_path;
@@ -72,6 +98,14 @@ struct TxDev {
     int32_t* c_att;
     uint32_t* c_fl;
     int32_t* c_dup;
+    uint32_t* c_q;
+    // per connection x path (SubConn, transport.hpp), persisted across runs
+    int64_t* s_inflight;
+    int64_t* s_deficit;
+    uint32_t* s_txq;
+    uint32_t* s_rtxq;
+    uint16_t* s_ring;  // engine ring: paths in order of first use
+    uint8_t* s_inring;
     unsigned long long* pool_top;
     SchedDev s;
     unsigned int* status;
@@ -84,14 +118,24 @@ struct Tx {
     const uint32_t conn;
     const int lane;
     WarpRng r;
-    double* rtt_s;  // PathScoreboard (lb.hpp:15-36), shared memory copy
+    double* rtt_s;  // PathScoreboard (lb.hpp:15-36), shared-memory copy
     double* ecn_s;
-    int n;          // paths of this connection
+    int64_t* inflight;  // SubConn::inflight per path
+    int64_t* deficit;   // SubConn::deficit
+    uint32_t* txq_n;    // live tx-queue entries per path
+    uint32_t* rtxq_n;   // live retransmission-queue entries per path
+    uint16_t* ring;
+    uint8_t* in_ring;
+    int n;  // paths of this connection
     cn_tx_rec* log;
     uint32_t log_n;
-    // RttEstimator + timer + counters (warp-uniform registers)
-    int64_t srtt, rttvar, armed_at, timer_at, committed_unsent;
-    int has_sample, backoff, timer_armed;
+    // RttEstimator, CC, timer, ring and counters (warp-uniform registers)
+    int64_t srtt, rttvar, armed_at, timer_at, committed_unsent, total_inflight, last_decrease;
+    double w;
+    int has_sample, backoff, timer_armed, ring_len;
+    uint64_t ring_pos;
+    uint32_t q_seq, pump_pending;
+    int64_t pump_at;  // schedule_pump (:219-230): one deferred pump per engine
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_completed;
     uint32_t live[4];  // live message slots, iterated in slot order
 
@@ -111,6 +155,63 @@ struct Tx {
         int64_t err = srtt > rtt ? srtt - rtt : rtt - srtt;
         rttvar = (3 * rttvar + err) / 4;
         srtt = (7 * srtt + rtt) / 8;
+    }
+    // CongestionControl::cwnd_bytes: OpenLoop (cc.cpp:21-22), Swift (:146-148)
+    __device__ int64_t cwnd_bytes() const {
+        if (d.cc_algo == 0) return d.cap_bytes > 0 ? d.cap_bytes : LLONG_MAX / 4;
+        return llround(__dmul_rn(w, static_cast<double>(d.mss)));
+    }
+    __device__ void cc_on_ack(int64_t now, int64_t acked, int64_t rtt) {  // cc.cpp:23-25, :117-131
+        if (rtt > 0) est_sample(rtt);
+        if (d.cc_algo == 0) return;
+        if (rtt <= d.swift_target) {
+            if (acked > 0) {
+                double a = __ddiv_rn(static_cast<double>(acked), static_cast<double>(d.mss));
+                double nw = __dadd_rn(w, __ddiv_rn(__dmul_rn(kSwiftAi, a), w));
+                w = d.cap_pkts < nw ? d.cap_pkts : nw;
+            }
+            return;
+        }
+        if (now - last_decrease < srtt) return;
+        double q = __ddiv_rn(__dmul_rn(kSwiftMdScale, static_cast<double>(rtt - d.swift_target)),
+                             static_cast<double>(rtt));
+        double f = __dsub_rn(1.0, q);
+        if (f < kSwiftMaxMd) f = kSwiftMaxMd;
+        double nw = __dmul_rn(w, f);
+        w = nw < kMinCwndPkts ? kMinCwndPkts : nw;
+        last_decrease = now;
+    }
+    __device__ void cc_on_loss(int64_t now) {  // cc.cpp:133-138
+        if (d.cc_algo == 0) return;
+        if (has_sample && now - last_decrease < srtt) return;
+        double nw = __dmul_rn(w, kSwiftMaxMd);
+        w = nw < kMinCwndPkts ? kMinCwndPkts : nw;
+        last_decrease = now;
+    }
+    __device__ void cc_on_rto(int64_t now) {  // cc.cpp:140-144
+        if (d.cc_algo == 0) return;
+        w = kMinCwndPkts;
+        last_decrease = now;
+    }
+    // can_send (:312-325), global scope: the connection's total inflight
+    __device__ bool can_send() const { return total_inflight < cwnd_bytes(); }
+    __device__ void add_inflight(int p, int64_t delta) {  // clamped at 0 (:520-521, :813-814)
+        int64_t v = inflight[p] + delta;
+        if (v < 0) v = 0;
+        total_inflight += v - inflight[p];
+        __syncwarp();
+        if (lane == 0) inflight[p] = v;
+        __syncwarp();
+    }
+    __device__ void ring_insert(int p) {  // :296-300, :537-540
+        if (in_ring[p]) return;
+        __syncwarp();
+        if (lane == 0) {
+            in_ring[p] = 1;
+            ring[ring_len] = static_cast<uint16_t>(p);
+        }
+        __syncwarp();
+        ++ring_len;
     }
     __device__ void arm_rto(int64_t now) {  // transport.cpp:1083-1092
         if (timer_armed) return;
@@ -136,83 +237,157 @@ struct Tx {
         }
         ++log_n;
     }
-    // send_chunk (transport.cpp:433-494) for chunk e of message mid
+    __device__ uint32_t chunk_len(const TxMsg& m, uint32_t ci) const {
+        uint64_t off = static_cast<uint64_t>(ci) * d.cb;
+        return m.len - off < d.cb ? static_cast<uint32_t>(m.len - off) : d.cb;
+    }
+    // send_chunk (transport.cpp:433-494) on the path the chunk is queued on
     __device__ void send_chunk(int64_t now, uint32_t mid, const TxMsg& m, uint32_t ci, bool rtx) {
-        uint64_t e = m.chunk_base + ci;
-        int64_t dl = now + cur_rto() * backoff;
+        const uint64_t e = m.chunk_base + ci;
+        const int64_t dl = now + cur_rto() * backoff;
+        const int32_t path = d.c_path[e];
+        const int32_t att = d.c_att[e] + 1;
+        __syncwarp();
         if (lane == 0) {
-            d.c_att[e] += 1;
+            d.c_att[e] = att;
             d.c_fl[e] = TF_SENT | (d.c_fl[e] & TF_ACKED);
             d.c_dup[e] = 0;
             d.c_txt[e] = now;
             d.c_dead[e] = dl;
+            d.c_q[e] = 0;
         }
-        uint64_t off = static_cast<uint64_t>(ci) * d.cb;
-        uint64_t len = m.len - off < d.cb ? m.len - off : d.cb;
-        if (rtx) {
-            ++chunk_rtx;
-        } else {
-            ++chunks_sent;
-            committed_unsent -= static_cast<int64_t>(len);
-        }
-        record(now, mid, ci, d.c_path[e], rtx || d.c_att[e] > 1, m.seq);
+        __syncwarp();
+        add_inflight(path, chunk_len(m, ci));
+        if (rtx) ++chunk_rtx;
+        else ++chunks_sent;
+        record(now, mid, ci, path, rtx || att > 1, m.seq);
         __syncwarp();
         arm_rto(now);
     }
     // queue_rtx (transport.cpp:516-542); caller checked sent && !acked && !rtx_pending
-    __device__ void queue_rtx(const TxMsg& m, uint32_t ci) {
-        uint64_t e = m.chunk_base + ci;
-        int prev = d.c_path[e];  // attempts > 0: prev_path = ch.path (view_of, :509)
-        int p = select(prev);
+    __device__ void queue_rtx(int64_t now, const TxMsg& m, uint32_t ci) {
+        const uint64_t e = m.chunk_base + ci;
+        const int prev = d.c_path[e];  // attempts > 0: prev_path = ch.path (view_of, :509)
+        add_inflight(prev, -static_cast<int64_t>(chunk_len(m, ci)));
+        cc_on_loss(now);
+        const int p = select(prev);
+        ++q_seq;
+        __syncwarp();
         if (lane == 0) {
             d.c_fl[e] |= TF_RTXP;
             d.c_dup[e] = 0;
             d.c_path[e] = p;
+            d.c_q[e] = kQRtx | q_seq;
+            rtxq_n[p] += 1;
         }
         __syncwarp();
+        ring_insert(p);
+        if (!pump_pending) {  // schedule_pump (:541): runs after the events queued at `now`
+            pump_pending = 1;
+            pump_at = now;
+        }
     }
 };
 
 __device__ __forceinline__ TxMsg load_msg(const TxConn* C, uint32_t mid) { return C->msgs[mid]; }
 __device__ __forceinline__ void store_msg(TxConn* C, uint32_t mid, const TxMsg& m, int lane) {
+    __syncwarp();
     if (lane == 0) C->msgs[mid] = m;
     __syncwarp();
 }
+__device__ __forceinline__ void set_u32(uint32_t* p, uint32_t v, int lane) {
+    __syncwarp();
+    if (lane == 0) *p = v;
+    __syncwarp();
+}
 
-// egress (transport.cpp:329-431) with an open cwnd: retransmissions first,
-// then every committed, unsent chunk.  Returns the number of sends.
-__device__ uint32_t egress(Tx& x, int64_t now) {
-    uint32_t sent = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        for (uint32_t q = 0; q < 4; ++q)
+// Front of path p's tx (rtx = false) or retransmission queue.
+__device__ bool queue_front(const Tx& x, int p, bool rtx, uint32_t* out_mid, uint32_t* out_ci) {
+    uint32_t best = 0xFFFFFFFFu, bmid = 0, bci = 0;
+    for (uint32_t q = 0; q < 4; ++q)
         for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
             const uint32_t mid = q * 32 + __ffs(lb) - 1;
-            TxMsg m = load_msg(x.C, mid);
+            const TxMsg m = load_msg(x.C, mid);
             for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
-                uint32_t ci = w0 + x.lane;
-                uint32_t fl = ci < m.nchunks ? x.d.c_fl[m.chunk_base + ci] : (TF_SENT | TF_ACKED);
-                bool want = pass == 0 ? ((fl & TF_RTXP) && !(fl & TF_ACKED)) : !(fl & TF_SENT);
-                unsigned b = __ballot_sync(0xffffffffu, want);
-                for (; b; b &= b - 1) {
-                    uint32_t cj = w0 + __ffs(b) - 1;
-                    x.send_chunk(now, mid, m, cj, pass == 0);
-                    ++sent;
+                const uint32_t ci = w0 + x.lane;
+                uint32_t key = 0xFFFFFFFFu;
+                if (ci < m.nchunks) {
+                    const uint64_t e = m.chunk_base + ci;
+                    const uint32_t qv = x.d.c_q[e];
+                    if (qv && ((qv & kQRtx) != 0) == rtx && x.d.c_path[e] == p) key = qv & ~kQRtx;
+                }
+                const uint32_t mn = __reduce_min_sync(0xffffffffu, key);
+                if (mn < best) {
+                    best = mn;
+                    bmid = mid;
+                    bci = w0 + __ffs(__ballot_sync(0xffffffffu, key == mn)) - 1;
                 }
             }
         }
+    *out_mid = bmid;
+    *out_ci = bci;
+    return best != 0xFFFFFFFFu;
+}
+
+// egress (transport.cpp:329-431): retransmission queues in ring order, then
+// deficit round robin over the ring, every send gated by can_send.
+__device__ uint32_t egress(Tx& x, int64_t now) {
+    uint32_t sent = 0;
+    for (int k = 0; k < x.ring_len; ++k) {  // :333-369
+        const int p = x.ring[k];
+        while (x.rtxq_n[p] > 0 && x.can_send()) {
+            uint32_t mid, ci;
+            if (!queue_front(x, p, true, &mid, &ci)) break;
+            set_u32(&x.rtxq_n[p], x.rtxq_n[p] - 1, x.lane);
+            x.send_chunk(now, mid, load_msg(x.C, mid), ci, true);
+            ++sent;
+        }
+    }
+    const int nr = x.ring_len;
+    int idle = 0;
+    while (idle < nr) {  // :378-424
+        const int p = x.ring[x.ring_pos % static_cast<uint64_t>(nr)];
+        ++x.ring_pos;
+        if (x.txq_n[p] == 0) {
+            __syncwarp();
+            if (x.lane == 0) x.deficit[p] = 0;
+            __syncwarp();
+            ++idle;
+            continue;
+        }
+        int64_t def = x.deficit[p] + static_cast<int64_t>(x.d.quantum);
+        if (def > static_cast<int64_t>(x.d.quantum)) def = x.d.quantum;
+        bool sent_any = false;
+        while (x.txq_n[p] > 0 && def > 0 && x.can_send()) {
+            uint32_t mid, ci;
+            if (!queue_front(x, p, false, &mid, &ci)) break;
+            const TxMsg m = load_msg(x.C, mid);
+            const uint32_t len = x.chunk_len(m, ci);
+            set_u32(&x.txq_n[p], x.txq_n[p] - 1, x.lane);
+            x.committed_unsent -= len;
+            def -= len;
+            x.send_chunk(now, mid, m, ci, false);
+            sent_any = true;
+            ++sent;
+        }
+        if (x.txq_n[p] == 0) def = 0;
+        __syncwarp();
+        if (x.lane == 0) x.deficit[p] = def;
+        __syncwarp();
+        idle = sent_any ? 0 : idle + 1;
     }
     return sent;
 }
 
 // commit_chunks (transport.cpp:244-310): one chunk per message per turn of
 // the factory rotation, window-stalled at 128 unacked chunks, bounded by
-// commit_ahead bytes.
-__device__ void commit_chunks(Tx& x, int64_t now) {
+// commit_ahead bytes; each chunk is bound to a path and queued on it.
+__device__ void commit_chunks(Tx& x) {
     TxConn* C = x.C;
     int32_t head = C->fq_head, count = C->fq_count;
     uint32_t stalled = 0;
     while (count > 0 && stalled < static_cast<uint32_t>(count) && x.committed_unsent < x.d.commit_ahead) {
-        uint32_t mid = C->fq[head];
+        const uint32_t mid = C->fq[head];
         head = (head + 1) & 127;
         --count;
         TxMsg m = load_msg(C, mid);
@@ -223,27 +398,35 @@ __device__ void commit_chunks(Tx& x, int64_t now) {
             continue;
         }
         if (m.nchunks - m.base >= static_cast<uint32_t>(kTxWindow)) {
+            __syncwarp();
             if (x.lane == 0) C->fq[(head + count) & 127] = static_cast<uint8_t>(mid);
             __syncwarp();
             ++count;
             ++stalled;
             continue;
         }
-        uint64_t rem = m.len - m.chunked;
-        uint32_t sz = rem < x.d.cb ? static_cast<uint32_t>(rem) : x.d.cb;
-        uint32_t ci = m.nchunks;
-        int p = x.select(-1);  // on_select_path (:281-287)
+        const uint64_t rem = m.len - m.chunked;
+        const uint32_t sz = rem < x.d.cb ? static_cast<uint32_t>(rem) : x.d.cb;
+        const uint32_t ci = m.nchunks;
+        const int p = x.select(-1);  // on_select_path (:281-287)
+        ++x.q_seq;
+        __syncwarp();
         if (x.lane == 0) {
-            uint64_t e = m.chunk_base + ci;
+            const uint64_t e = m.chunk_base + ci;
             x.d.c_path[e] = p;
             x.d.c_fl[e] = 0;
             x.d.c_att[e] = 0;
             x.d.c_dup[e] = 0;
+            x.d.c_q[e] = x.q_seq;
+            x.txq_n[p] += 1;
         }
+        __syncwarp();
+        x.ring_insert(p);
         m.nchunks = ci + 1;
         m.chunked += sz;
         x.committed_unsent += sz;
         if (m.chunked < m.len) {
+            __syncwarp();
             if (x.lane == 0) C->fq[(head + count) & 127] = static_cast<uint8_t>(mid);
             __syncwarp();
             ++count;
@@ -253,6 +436,7 @@ __device__ void commit_chunks(Tx& x, int64_t now) {
         store_msg(C, mid, m, x.lane);
         stalled = 0;
     }
+    __syncwarp();
     if (x.lane == 0) {
         C->fq_head = head;
         C->fq_count = count;
@@ -262,7 +446,7 @@ __device__ void commit_chunks(Tx& x, int64_t now) {
 
 __device__ void pump(Tx& x, int64_t now) {  // transport.cpp:232-240
     for (;;) {
-        commit_chunks(x, now);
+        commit_chunks(x);
         if (egress(x, now) == 0) break;
     }
 }
@@ -271,9 +455,9 @@ __device__ void pump(Tx& x, int64_t now) {  // transport.cpp:232-240
 __device__ uint32_t advance_base(const Tx& x, const TxMsg& m) {
     uint32_t b = m.base;
     while (b < m.nchunks) {
-        uint32_t ci = b + x.lane;
-        bool acked = ci < m.nchunks ? (x.d.c_fl[m.chunk_base + ci] & TF_ACKED) != 0 : false;
-        unsigned un = __ballot_sync(0xffffffffu, !acked);
+        const uint32_t ci = b + x.lane;
+        const bool acked = ci < m.nchunks ? (x.d.c_fl[m.chunk_base + ci] & TF_ACKED) != 0 : false;
+        const unsigned un = __ballot_sync(0xffffffffu, !acked);
         if (un) return b + __ffs(un) - 1;
         b += 32;
     }
@@ -296,13 +480,55 @@ __device__ void msg_finished(Tx& x, uint32_t mid) {
     ++x.msgs_completed;
 }
 
-// release_chunk (:807-823) of a lane-owned chunk, rtt = 0 (no estimator or
-// scoreboard effect under OpenLoop); returns whether it released.
-__device__ __forceinline__ bool release_lane(const Tx& x, uint64_t e) {
-    uint32_t fl = x.d.c_fl[e];
-    if ((fl & TF_ACKED) || !(fl & TF_SENT)) return false;
-    x.d.c_fl[e] = (fl | TF_ACKED) & ~TF_RTXP;
-    return true;
+// release_chunk (:807-823) of a chunk the caller found sent && !acked.  A
+// chunk awaiting retransmission leaves its queue (the reference's entry
+// turns stale and is popped without effect).
+__device__ void release(Tx& x, int64_t now, const TxMsg& m, uint32_t ci, int64_t rtt, bool ecn) {
+    const uint64_t e = m.chunk_base + ci;
+    const uint32_t fl = x.d.c_fl[e];
+    const int path = x.d.c_path[e];
+    const uint32_t len = x.chunk_len(m, ci);
+    const uint32_t rq = x.rtxq_n[path];
+    __syncwarp();
+    if (x.lane == 0) {
+        x.d.c_fl[e] = (fl | TF_ACKED) & ~TF_RTXP;
+        if (fl & TF_RTXP) {
+            x.rtxq_n[path] = rq - 1;
+            x.d.c_q[e] = 0;
+        }
+    }
+    __syncwarp();
+    if (!(fl & TF_RTXP)) x.add_inflight(path, -static_cast<int64_t>(len));
+    x.cc_on_ack(now, len, rtt);
+    if (rtt > 0) {  // board.record_rtt / record_ecn (:819-822)
+        __syncwarp();
+        if (x.lane == 0) {
+            x.rtt_s[path] += (static_cast<double>(rtt) - x.rtt_s[path]) / 8.0;
+            x.ecn_s[path] += ((ecn ? 1.0 : 0.0) - x.ecn_s[path]) / 8.0;
+        }
+        __syncwarp();
+    }
+}
+
+// Releases, in ascending order, every sent && !acked chunk of [lo, hi)
+// that `pick` selects (CC sees the acks in the reference's order).
+template <class Pick>
+__device__ uint32_t release_range(Tx& x, int64_t now, TxMsg& m, uint32_t lo, uint32_t hi, Pick pick) {
+    uint32_t n_rel = 0;
+    for (uint32_t w0 = lo; w0 < hi; w0 += 32) {
+        const uint32_t ci = w0 + x.lane;
+        bool want = false;
+        if (ci < hi && pick(ci)) {
+            const uint32_t fl = x.d.c_fl[m.chunk_base + ci];
+            want = (fl & TF_SENT) && !(fl & TF_ACKED);
+        }
+        for (unsigned b = __ballot_sync(0xffffffffu, want); b; b &= b - 1) {
+            release(x, now, m, w0 + __ffs(b) - 1, 0, false);
+            ++n_rel;
+        }
+    }
+    m.acked += n_rel;
+    return n_rel;
 }
 
 // handle_ack (:849-942)
@@ -316,70 +542,50 @@ __device__ void handle_ack(Tx& x, int64_t now, const cn_ack_rec& a) {
     uint32_t newly = 0;
     int64_t cause = -1;
     {
-        uint8_t rel = static_cast<uint8_t>(((a.hdr >> 9) & 0xFF) - base_csn);
+        const uint8_t rel = static_cast<uint8_t>(((a.hdr >> 9) & 0xFF) - base_csn);
         if (rel < kTxWindow && m.base + rel < nch) cause = m.base + rel;
     }
     if (cause >= 0) {  // cause chunk: the only trustworthy RTT echo (:869-887)
-        uint64_t e = m.chunk_base + cause;
-        uint32_t fl = x.d.c_fl[e];
+        const uint64_t e = m.chunk_base + cause;
+        const uint32_t fl = x.d.c_fl[e];
         if ((fl & TF_SENT) && !(fl & TF_ACKED)) {
             int64_t rtt = 0;
             if (x.d.c_att[e] == 1 && a.echo_tx_time == x.d.c_txt[e] && now > a.echo_tx_time)
                 rtt = now - a.echo_tx_time;
-            bool ecn = (a.flags & CN_ACK_ECN_ECHO) != 0;
-            int path = x.d.c_path[e];
-            __syncwarp();
-            if (x.lane == 0) x.d.c_fl[e] = (fl | TF_ACKED) & ~TF_RTXP;
-            __syncwarp();
+            release(x, now, m, static_cast<uint32_t>(cause), rtt, (a.flags & CN_ACK_ECN_ECHO) != 0);
             m.acked += 1;
-            if (rtt > 0) {
-                x.est_sample(rtt);  // OpenLoop::on_ack (cc.cpp:23-25)
-                if (x.lane == 0) {   // board.record_rtt / record_ecn (:819-822)
-                    x.rtt_s[path] += (static_cast<double>(rtt) - x.rtt_s[path]) / 8.0;
-                    x.ecn_s[path] += ((ecn ? 1.0 : 0.0) - x.ecn_s[path]) / 8.0;
-                }
-                __syncwarp();
-            }
             ++newly;
         }
     }
     // cumulative bound (:890-897)
     uint32_t rcum = m.base;
     if (a.flags & CN_ACK_CUM_VALID) {
-        uint8_t rel1 = static_cast<uint8_t>(static_cast<uint8_t>(a.cum_csn + 1) - base_csn);
+        const uint8_t rel1 = static_cast<uint8_t>(static_cast<uint8_t>(a.cum_csn + 1) - base_csn);
         if (rel1 <= kTxWindow) rcum = m.base + rel1;
     } else {
         rcum = 0;
     }
     const uint32_t cend = rcum < nch ? rcum : nch;
-    for (uint32_t w0 = m.base; w0 < cend; w0 += 32) {  // :898-904
-        uint32_t ci = w0 + x.lane;
-        bool rel = ci < cend && release_lane(x, m.chunk_base + ci);
-        uint32_t c = __popc(__ballot_sync(0xffffffffu, rel));
-        m.acked += c;
-        newly += c;
+    newly += release_range(x, now, m, m.base, cend, [](uint32_t) { return true; });  // :898-904
+    {  // selective bitmap relative to rcum (:905-914)
+        const uint32_t send_ = rcum + 128 < nch ? rcum + 128 : nch;
+        const uint64_t s0 = a.sack[0], s1 = a.sack[1];
+        const uint32_t rc = rcum;
+        newly += release_range(x, now, m, rcum < send_ ? rcum : send_, send_, [=](uint32_t ci) {
+            const uint32_t j = ci - rc;
+            return ((j < 64 ? s0 >> j : s1 >> (j - 64)) & 1ull) != 0;
+        });
     }
-    __syncwarp();
-    for (int q = 0; q < 4; ++q) {  // SACK (:905-914)
-        uint32_t j = q * 32 + x.lane;
-        bool bit = ((q < 2 ? a.sack[0] >> (j & 63) : a.sack[1] >> (j & 63)) & 1ull) != 0;
-        uint64_t i = static_cast<uint64_t>(rcum) + j;
-        bool rel = bit && i < nch && release_lane(x, m.chunk_base + i);
-        uint32_t c = __popc(__ballot_sync(0xffffffffu, rel));
-        m.acked += c;
-        newly += c;
-    }
-    __syncwarp();
     // duplicate hints -> fast retransmit, ascending chunk order (:918-929)
     if (cause >= 0) {
         for (uint32_t w0 = m.base; w0 < static_cast<uint32_t>(cause); w0 += 32) {
-            uint32_t ci = w0 + x.lane;
+            const uint32_t ci = w0 + x.lane;
             bool trig = false;
             if (ci < static_cast<uint32_t>(cause)) {
-                uint64_t e = m.chunk_base + ci;
-                uint32_t fl = x.d.c_fl[e];
+                const uint64_t e = m.chunk_base + ci;
+                const uint32_t fl = x.d.c_fl[e];
                 if ((fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP))) {
-                    int32_t dup = x.d.c_dup[e] + 1;
+                    const int32_t dup = x.d.c_dup[e] + 1;
                     x.d.c_dup[e] = dup;
                     trig = dup >= static_cast<int32_t>(x.d.dupack);
                 }
@@ -387,15 +593,15 @@ __device__ void handle_ack(Tx& x, int64_t now, const cn_ack_rec& a) {
             __syncwarp();
             for (unsigned b = __ballot_sync(0xffffffffu, trig); b; b &= b - 1) {
                 ++x.fast_rtx;
-                x.queue_rtx(m, w0 + __ffs(b) - 1);
+                x.queue_rtx(now, m, w0 + __ffs(b) - 1);
             }
         }
     }
     m.base = advance_base(x, m);  // :931
-    bool done = m.chunked >= m.len && nch > 0 && m.acked == nch && !m.in_factory;
+    const bool done = m.chunked >= m.len && nch > 0 && m.acked == nch && !m.in_factory;
     store_msg(C, mid, m, x.lane);
     if (done) msg_finished(x, mid);  // :932-934
-    if (newly > 0) {  // :936-940
+    if (newly > 0) {                 // :936-940
         x.backoff = 1;
         x.timer_armed = 0;
         x.arm_rto(now);
@@ -408,39 +614,36 @@ __device__ void rto_fire(Tx& x) {
     TxConn* C = x.C;
     const int64_t now = x.timer_at;
     x.timer_armed = 0;
-    // scan: msg slots 0..127 x [base, n): oldest deadline (first wins) and
-    // the expired set in scan order
+    // scan: oldest deadline and the number of expired chunks
     int64_t best = 0;
     bool have = false;
     uint32_t n_exp = 0;
     for (uint32_t q = 0; q < 4; ++q)
-    for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
-        const uint32_t mid = q * 32 + __ffs(lb) - 1;
-        TxMsg m = load_msg(C, mid);
-        for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
-            uint32_t ci = w0 + x.lane;
-            bool elig = false;
-            int64_t dl = 0;
-            if (ci < m.nchunks) {
-                uint64_t e = m.chunk_base + ci;
-                uint32_t fl = x.d.c_fl[e];
-                elig = (fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP));
-                dl = x.d.c_dead[e];
+        for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
+            const uint32_t mid = q * 32 + __ffs(lb) - 1;
+            const TxMsg m = load_msg(C, mid);
+            for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
+                const uint32_t ci = w0 + x.lane;
+                bool elig = false;
+                int64_t dl = 0;
+                if (ci < m.nchunks) {
+                    const uint64_t e = m.chunk_base + ci;
+                    const uint32_t fl = x.d.c_fl[e];
+                    elig = (fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP));
+                    dl = x.d.c_dead[e];
+                }
+                long long mn = elig ? dl : LLONG_MAX;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const long long t = __shfl_xor_sync(0xffffffffu, mn, o);
+                    mn = t < mn ? t : mn;
+                }
+                if (__ballot_sync(0xffffffffu, elig) && (!have || mn < best)) {
+                    best = mn;
+                    have = true;
+                }
+                n_exp += __popc(__ballot_sync(0xffffffffu, elig && dl <= now));
             }
-            // min deadline with the lowest scan position winning ties
-            long long v = elig ? dl : LLONG_MAX;
-            long long mn = v;
-            for (int o = 16; o > 0; o >>= 1) {
-                long long t = __shfl_xor_sync(0xffffffffu, mn, o);
-                mn = t < mn ? t : mn;
-            }
-            if (__ballot_sync(0xffffffffu, elig) && (!have || mn < best)) {
-                best = mn;
-                have = true;
-            }
-            n_exp += __popc(__ballot_sync(0xffffffffu, elig && dl <= now));
         }
-    }
     if (!have) return;  // :1131 nothing outstanding
     if (n_exp == 0) {   // :1132-1140 re-arm for the earliest deadline
         x.timer_armed = 1;
@@ -450,23 +653,23 @@ __device__ void rto_fire(Tx& x) {
     }
     ++x.rtos;
     x.backoff = x.backoff * 2 < kBackoffCap ? x.backoff * 2 : kBackoffCap;
-    // queue_rtx for every expired chunk in scan order (:1154-1164)
+    x.cc_on_rto(now);  // once per distinct CC -- global scope has one (:1154-1160)
     for (uint32_t q = 0; q < 4; ++q)
-    for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
-        const uint32_t mid = q * 32 + __ffs(lb) - 1;
-        TxMsg m = load_msg(C, mid);
-        for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
-            uint32_t ci = w0 + x.lane;
-            bool ex = false;
-            if (ci < m.nchunks) {
-                uint64_t e = m.chunk_base + ci;
-                uint32_t fl = x.d.c_fl[e];
-                ex = (fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP)) && x.d.c_dead[e] <= now;
+        for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
+            const uint32_t mid = q * 32 + __ffs(lb) - 1;
+            const TxMsg m = load_msg(C, mid);
+            for (uint32_t w0 = m.base; w0 < m.nchunks; w0 += 32) {
+                const uint32_t ci = w0 + x.lane;
+                bool ex = false;
+                if (ci < m.nchunks) {
+                    const uint64_t e = m.chunk_base + ci;
+                    const uint32_t fl = x.d.c_fl[e];
+                    ex = (fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP)) && x.d.c_dead[e] <= now;
+                }
+                for (unsigned b = __ballot_sync(0xffffffffu, ex); b; b &= b - 1)
+                    x.queue_rtx(now, m, w0 + __ffs(b) - 1);
             }
-            for (unsigned b = __ballot_sync(0xffffffffu, ex); b; b &= b - 1)
-                x.queue_rtx(m, w0 + __ffs(b) - 1);
         }
-    }
     x.arm_rto(now);  // :1167
     pump(x, now);    // :1168
 }
@@ -474,22 +677,25 @@ __device__ void rto_fire(Tx& x) {
 // send_message (:144-196) + dispatch (:198-218)
 __device__ void submit(Tx& x, int64_t now, const cn_tx_submit& s) {
     TxConn* C = x.C;
-    if (s.len == 0 || C->n_free == 0) {  // len 0 throws in the reference; counted here
-        if (x.lane == 0) C->backpressured += 1;
+    if (s.len == 0 || C->n_free == 0) {  // len 0 throws in the reference; flagged here
         __syncwarp();
+        if (x.lane == 0) C->backpressured += 1;
         if (s.len == 0 && x.lane == 0) atomicOr(x.d.status, 1u);
+        __syncwarp();
         return;
     }
-    uint32_t mid = C->free_ids[C->n_free - 1];
-    uint64_t seq = C->next_seq;
+    const uint32_t mid = C->free_ids[C->n_free - 1];
+    const uint64_t seq = C->next_seq;
+    __syncwarp();
     if (x.lane == 0) C->next_seq = seq + 1;
     __syncwarp();
     if (static_cast<uint32_t>(C->live_msgs) >= x.d.max_inflight) {
+        __syncwarp();
         if (x.lane == 0) C->backpressured += 1;
         __syncwarp();
         return;
     }
-    uint64_t nc = (s.len + x.d.cb - 1) / x.d.cb;
+    const uint64_t nc = (s.len + x.d.cb - 1) / x.d.cb;
     unsigned long long base = 0;
     if (x.lane == 0) base = atomicAdd(x.d.pool_top, static_cast<unsigned long long>(nc));
     base = __shfl_sync(0xffffffffu, base, 0);
@@ -518,6 +724,34 @@ __device__ void submit(Tx& x, int64_t now, const cn_tx_submit& s) {
     pump(x, now);
 }
 
+// Fires the events the run itself scheduled -- the RTO timer and the
+// deferred pump -- that precede an input event at time t (inclusive = false)
+// or the horizon t (inclusive = true), in the event queue's (time, seq)
+// order: input events were all queued first, so they win ties; a timer due
+// at the deferred pump's time was queued before it (rto > 0), so it wins.
+__device__ void run_deferred(Tx& x, int64_t t, bool inclusive) {
+    for (;;) {
+        const bool tmr = x.timer_armed && (inclusive ? x.timer_at <= t : x.timer_at < t);
+        const bool pmp = x.pump_pending && (inclusive ? x.pump_at <= t : x.pump_at < t);
+        if (tmr && (!pmp || x.timer_at <= x.pump_at)) {
+            rto_fire(x);
+        } else if (pmp) {
+            x.pump_pending = 0;
+            pump(x, x.pump_at);
+        } else {
+            return;
+        }
+    }
+}
+
+// shared memory per warp, in 8-byte words: mt state + tempered block, the
+// rtt / ecn boards, inflight and deficit, then txq / rtxq depths (4 B),
+// ring (2 B) and in_ring (1 B) per path
+__host__ __device__ inline size_t tx_smem_words(uint32_t max_paths) {
+    return 2 * static_cast<size_t>(kMtN) + 4 * static_cast<size_t>(max_paths) +
+           (11 * static_cast<size_t>(max_paths) + 7) / 8;
+}
+
 __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_t* __restrict__ ev_off,
                                                          const uint64_t* __restrict__ events,
                                                          const cn_tx_submit* __restrict__ submits,
@@ -529,16 +763,30 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t conn = blockIdx.x * kTxWarps + w;
     if (conn >= d.n_conns) return;
-    uint64_t* mt = sm + static_cast<size_t>(w) * (2 * kMtN + 2 * d.s.max_paths);
+    const uint32_t mp = d.s.max_paths;
+    uint64_t* mt = sm + static_cast<size_t>(w) * tx_smem_words(mp);
+    double* rtt_s = reinterpret_cast<double*>(mt + 2 * kMtN);
+    double* ecn_s = rtt_s + mp;
+    int64_t* infl = reinterpret_cast<int64_t*>(ecn_s + mp);
+    int64_t* defc = infl + mp;
+    uint32_t* txq = reinterpret_cast<uint32_t*>(defc + mp);
+    uint32_t* rtxq = txq + mp;
+    uint16_t* ring = reinterpret_cast<uint16_t*>(rtxq + mp);
+    uint8_t* inr = reinterpret_cast<uint8_t*>(ring + mp);
     TxConn* C = d.conns + conn;
-    Tx x{d, C, conn, lane, WarpRng{mt, mt + kMtN, 0},
-         reinterpret_cast<double*>(mt + 2 * kMtN), reinterpret_cast<double*>(mt + 2 * kMtN + d.s.max_paths),
+    Tx x{d,    C,    conn, lane, WarpRng{mt, mt + kMtN, 0}, rtt_s, ecn_s, infl, defc, txq, rtxq, ring, inr,
          C->n_paths, log + static_cast<uint64_t>(conn) * d.log_cap, log_n[conn]};
-    // stream + boards into shared memory
+    const uint64_t sb = static_cast<uint64_t>(conn) * mp;
     for (int k = lane; k < kMtN; k += 32) mt[k] = d.s.mt[static_cast<uint64_t>(conn) * kMtN + k];
-    for (int p = lane; p < x.n; p += 32) {
-        x.rtt_s[p] = d.s.rtt[static_cast<uint64_t>(conn) * d.s.max_paths + p];
-        x.ecn_s[p] = d.s.ecn[static_cast<uint64_t>(conn) * d.s.max_paths + p];
+    for (uint32_t p = lane; p < mp; p += 32) {
+        rtt_s[p] = d.s.rtt[sb + p];
+        ecn_s[p] = d.s.ecn[sb + p];
+        infl[p] = d.s_inflight[sb + p];
+        defc[p] = d.s_deficit[sb + p];
+        txq[p] = d.s_txq[sb + p];
+        rtxq[p] = d.s_rtxq[sb + p];
+        ring[p] = d.s_ring[sb + p];
+        inr[p] = d.s_inring[sb + p];
     }
     x.r.idx = d.s.mt_idx[conn];
     __syncwarp();
@@ -549,9 +797,17 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
     x.armed_at = C->armed_at;
     x.timer_at = C->timer_at;
     x.committed_unsent = C->committed_unsent;
+    x.total_inflight = C->total_inflight;
+    x.last_decrease = C->last_decrease;
+    x.w = C->w;
     x.has_sample = C->has_sample;
     x.backoff = C->backoff;
     x.timer_armed = C->timer_armed;
+    x.ring_len = C->ring_len;
+    x.ring_pos = C->ring_pos;
+    x.q_seq = C->q_seq;
+    x.pump_pending = C->pump_pending;
+    x.pump_at = C->pump_at;
     x.chunks_sent = C->chunks_sent;
     x.chunk_rtx = C->chunk_rtx;
     x.fast_rtx = C->fast_rtx;
@@ -563,22 +819,28 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
         const uint32_t type = static_cast<uint32_t>(ev >> 62);
         const uint64_t idx = ev & ((1ull << 62) - 1);
         const int64_t t = type == 0 ? submits[idx].t : acks[idx].aux;
-        // timers scheduled during the run fire after same-time events (DES order)
-        while (x.timer_armed && x.timer_at < t) rto_fire(x);
+        run_deferred(x, t, false);
         if (type == 0) {
-            cn_tx_submit s = submits[idx];
+            const cn_tx_submit s = submits[idx];
             submit(x, t, s);
         } else {
-            cn_ack_rec a = acks[idx];
+            const cn_ack_rec a = acks[idx];
             handle_ack(x, t, a);
         }
     }
-    while (x.timer_armed && x.timer_at <= end_time) rto_fire(x);
+    run_deferred(x, end_time, true);
     // persist
+    __syncwarp();
     for (int k = lane; k < kMtN; k += 32) d.s.mt[static_cast<uint64_t>(conn) * kMtN + k] = mt[k];
-    for (int p = lane; p < x.n; p += 32) {
-        d.s.rtt[static_cast<uint64_t>(conn) * d.s.max_paths + p] = x.rtt_s[p];
-        d.s.ecn[static_cast<uint64_t>(conn) * d.s.max_paths + p] = x.ecn_s[p];
+    for (uint32_t p = lane; p < mp; p += 32) {
+        d.s.rtt[sb + p] = rtt_s[p];
+        d.s.ecn[sb + p] = ecn_s[p];
+        d.s_inflight[sb + p] = infl[p];
+        d.s_deficit[sb + p] = defc[p];
+        d.s_txq[sb + p] = txq[p];
+        d.s_rtxq[sb + p] = rtxq[p];
+        d.s_ring[sb + p] = ring[p];
+        d.s_inring[sb + p] = inr[p];
     }
     if (lane == 0) {
         d.s.mt_idx[conn] = x.r.idx;
@@ -587,9 +849,17 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
         C->armed_at = x.armed_at;
         C->timer_at = x.timer_at;
         C->committed_unsent = x.committed_unsent;
+        C->total_inflight = x.total_inflight;
+        C->last_decrease = x.last_decrease;
+        C->w = x.w;
         C->has_sample = x.has_sample;
         C->backoff = x.backoff;
         C->timer_armed = x.timer_armed;
+        C->ring_len = x.ring_len;
+        C->ring_pos = x.ring_pos;
+        C->q_seq = x.q_seq;
+        C->pump_pending = x.pump_pending;
+        C->pump_at = x.pump_at;
         C->chunks_sent = x.chunks_sent;
         C->chunk_rtx = x.chunk_rtx;
         C->fast_rtx = x.fast_rtx;
@@ -610,23 +880,37 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
         st.rttvar = x.rttvar;
         st.backoff = x.backoff;
         st.live_msgs = C->live_msgs;
+        st.cwnd_bytes = x.cwnd_bytes();
+        st.inflight = x.total_inflight;
+        st.cwnd_pkts = x.w;
         stats[conn] = st;
     }
 }
 
 __global__ void k_tx_init(TxDev d, const int32_t* src, const int32_t* dst, const int32_t* np) {
-    uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= d.n_conns) return;
     TxConn* C = d.conns + c;
     memset(C, 0, sizeof(TxConn));
     C->backoff = 1;
     C->next_seq = 1;
+    C->w = d.init_cwnd;
+    C->last_decrease = kNeverDecreased;
     C->src = src ? src[c] : 0;
     C->dst = dst ? dst[c] : 0;
     C->n_paths = np ? np[c] : static_cast<int32_t>(d.s.max_paths);
     C->conn_id = static_cast<int32_t>(c & 0xFF);
     for (int i = 0; i < 128; ++i) C->free_ids[i] = static_cast<uint8_t>(127 - i);  // :127-129
     C->n_free = 128;
+    const uint64_t sb = static_cast<uint64_t>(c) * d.s.max_paths;
+    for (uint32_t p = 0; p < d.s.max_paths; ++p) {
+        d.s_inflight[sb + p] = 0;
+        d.s_deficit[sb + p] = 0;
+        d.s_txq[sb + p] = 0;
+        d.s_rtxq[sb + p] = 0;
+        d.s_ring[sb + p] = 0;
+        d.s_inring[sb + p] = 0;
+    }
 }
 
 }  // namespace cnb
@@ -649,16 +933,23 @@ extern "C" void cn_tx_config_default(cn_tx_config* c) {
     c->max_inflight_msgs = 128;
     c->max_paths = 1;
     c->chunk_pool = 1ull << 20;
-    c->seed = 0;
-    c->stream_index0 = 0;
     c->log_cap = 1u << 16;
+    c->cc_algo = CN_CC_NONE;
+    c->drr_quantum = 32768;  // TransportConfig::drr_quantum
+    c->mss = 4032;           // CcConfig::mss
+    c->init_cwnd_pkts = 2.0; // CcConfig::init_cwnd_pkts
 }
+
+static size_t tx_smem_bytes(uint32_t max_paths) { return kTxWarps * tx_smem_words(max_paths) * 8; }
 
 extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int32_t* h_src,
                             const int32_t* h_dst, const int32_t* h_n_paths, cn_tx** out) {
     if (!cfg || !out || n_conns == 0 || cfg->chunk_bytes == 0 || cfg->rto_min <= 0 ||
-        cfg->max_paths == 0 || cfg->lb_policy < 0 || cfg->lb_policy > 2) {
-        set_error("cn_tx_create: bad config (rto_min must be resolved, > 0)");
+        cfg->max_paths == 0 || cfg->max_paths > 1024 || cfg->lb_policy < 0 || cfg->lb_policy > 2 ||
+        (cfg->cc_algo != CN_CC_NONE && cfg->cc_algo != CN_CC_SWIFT) || cfg->drr_quantum == 0 ||
+        cfg->mss <= 0 || !(cfg->init_cwnd_pkts > 0) || cfg->cap_bytes < 0) {
+        set_error("cn_tx_create: bad config (rto_min resolved > 0, max_paths <= 1024, "
+                  "cc none or swift -- CUBIC is host-side)");
         return CN_E_INVALID;
     }
     *out = nullptr;
@@ -680,25 +971,41 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
     d.policy = static_cast<uint32_t>(cfg->lb_policy);
     d.max_inflight = cfg->max_inflight_msgs;
     d.log_cap = cfg->log_cap;
+    d.cc_algo = cfg->cc_algo == CN_CC_SWIFT ? 1 : 0;
+    d.quantum = cfg->drr_quantum;
     d.rto_min = cfg->rto_min;
     d.rto_max = cfg->rto_max > 0 ? cfg->rto_max : 64 * cfg->rto_min;  // transport.cpp:36
     d.commit_ahead = cfg->commit_ahead;
+    d.swift_target = cfg->swift_target_ns;
+    d.mss = cfg->mss;
+    d.cap_bytes = cfg->cap_bytes;
+    d.init_cwnd = cfg->init_cwnd_pkts;
+    // cap_pkts_ (cc.cpp:111-113)
+    d.cap_pkts = cfg->cap_bytes > 0 ? static_cast<double>(cfg->cap_bytes) / static_cast<double>(cfg->mss)
+                                    : __builtin_huge_val();
     d.pool_cap = cfg->chunk_pool;
     d.s = *sched_dev(t->sched);
+    const uint64_t subs = static_cast<uint64_t>(n_conns) * cfg->max_paths;
     int32_t *src = nullptr, *dst = nullptr, *np = nullptr;
+    const uint64_t pool = cfg->chunk_pool;
     bool ok = cudaMalloc(&d.conns, sizeof(TxConn) * n_conns) == cudaSuccess &&
-              cudaMalloc(&d.c_path, cfg->chunk_pool * 4) == cudaSuccess &&
-              cudaMalloc(&d.c_txt, cfg->chunk_pool * 8) == cudaSuccess &&
-              cudaMalloc(&d.c_dead, cfg->chunk_pool * 8) == cudaSuccess &&
-              cudaMalloc(&d.c_att, cfg->chunk_pool * 4) == cudaSuccess &&
-              cudaMalloc(&d.c_fl, cfg->chunk_pool * 4) == cudaSuccess &&
-              cudaMalloc(&d.c_dup, cfg->chunk_pool * 4) == cudaSuccess &&
-              cudaMalloc(&d.pool_top, 8) == cudaSuccess && cudaMalloc(&d.status, 4) == cudaSuccess &&
-              cudaMalloc(&t->d_logn, n_conns * 4ull) == cudaSuccess &&
+              cudaMalloc(&d.c_path, pool * 4) == cudaSuccess && cudaMalloc(&d.c_txt, pool * 8) == cudaSuccess &&
+              cudaMalloc(&d.c_dead, pool * 8) == cudaSuccess && cudaMalloc(&d.c_att, pool * 4) == cudaSuccess &&
+              cudaMalloc(&d.c_fl, pool * 4) == cudaSuccess && cudaMalloc(&d.c_dup, pool * 4) == cudaSuccess &&
+              cudaMalloc(&d.c_q, pool * 4) == cudaSuccess &&
+              cudaMalloc(&d.s_inflight, subs * 8) == cudaSuccess &&
+              cudaMalloc(&d.s_deficit, subs * 8) == cudaSuccess && cudaMalloc(&d.s_txq, subs * 4) == cudaSuccess &&
+              cudaMalloc(&d.s_rtxq, subs * 4) == cudaSuccess && cudaMalloc(&d.s_ring, subs * 2) == cudaSuccess &&
+              cudaMalloc(&d.s_inring, subs) == cudaSuccess && cudaMalloc(&d.pool_top, 8) == cudaSuccess &&
+              cudaMalloc(&d.status, 4) == cudaSuccess && cudaMalloc(&t->d_logn, n_conns * 4ull) == cudaSuccess &&
               cudaMalloc(&src, n_conns * 4ull) == cudaSuccess && cudaMalloc(&dst, n_conns * 4ull) == cudaSuccess &&
               cudaMalloc(&np, n_conns * 4ull) == cudaSuccess;
     if (!ok) {
         set_error("cn_tx_create: out of device memory");
+        cudaFree(src);
+        cudaFree(dst);
+        cudaFree(np);
+        cn_tx_destroy(t);
         return CN_E_CAPACITY;
     }
     std::vector<int32_t> hs(n_conns, 0), hd(n_conns, 0), hn(n_conns, static_cast<int32_t>(cfg->max_paths));
@@ -712,15 +1019,19 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
     cudaMemcpy(np, hn.data(), n_conns * 4ull, cudaMemcpyHostToDevice);
     cudaMemset(d.pool_top, 0, 8);
     cudaMemset(d.status, 0, 4);
+    cudaMemset(d.c_q, 0, pool * 4);
     cudaMemset(t->d_logn, 0, n_conns * 4ull);
     k_tx_init<<<(n_conns + 127) / 128, 128>>>(d, src, dst, np);
     cudaError_t e = cudaDeviceSynchronize();
     cudaFree(src);
     cudaFree(dst);
     cudaFree(np);
-    if (e != cudaSuccess) return cuda_status(e, "cn_tx_create");
-    int smem = kTxWarps * (2 * kMtN + 2 * static_cast<int>(cfg->max_paths)) * 8;
-    cudaFuncSetAttribute(k_tx_run, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) {
+        cn_tx_destroy(t);
+        return cuda_status(e, "cn_tx_create");
+    }
+    cudaFuncSetAttribute(k_tx_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(tx_smem_bytes(cfg->max_paths)));
     *out = t;
     return CN_OK;
 }
@@ -729,11 +1040,12 @@ extern "C" void cn_tx_destroy(cn_tx* t) {
     if (!t) return;
     cudaDeviceSynchronize();
     TxDev& d = t->d;
-    void* ptrs[] = {d.conns, d.c_path, d.c_txt, d.c_dead, d.c_att, d.c_fl, d.c_dup, d.pool_top,
-                    d.status, t->d_logn};
+    void* ptrs[] = {d.conns,      d.c_path,    d.c_txt, d.c_dead, d.c_att,  d.c_fl,
+                    d.c_dup,      d.c_q,       d.s_inflight, d.s_deficit, d.s_txq, d.s_rtxq,
+                    d.s_ring,     d.s_inring,  d.pool_top, d.status, t->d_logn};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    cn_sched_destroy(t->sched);
+    if (t->sched) cn_sched_destroy(t->sched);
     delete t;
 }
 
@@ -744,10 +1056,9 @@ extern "C" int cn_tx_run(cn_tx* t, const uint32_t* d_ev_off, const uint64_t* d_e
         set_error("cn_tx_run: bad arguments");
         return CN_E_INVALID;
     }
-    int smem = kTxWarps * (2 * kMtN + 2 * static_cast<int>(t->d.s.max_paths)) * 8;
-    k_tx_run<<<(t->d.n_conns + kTxWarps - 1) / kTxWarps, kTxWarps * 32, smem,
-               static_cast<cudaStream_t>(stream)>>>(t->d, d_ev_off, d_events, d_submits, d_acks,
-                                                    end_time, d_log, t->d_logn, d_stats);
+    k_tx_run<<<(t->d.n_conns + kTxWarps - 1) / kTxWarps, kTxWarps * 32,
+               tx_smem_bytes(t->d.s.max_paths), static_cast<cudaStream_t>(stream)>>>(
+        t->d, d_ev_off, d_events, d_submits, d_acks, end_time, d_log, t->d_logn, d_stats);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }

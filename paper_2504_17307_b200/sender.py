@@ -1,7 +1,9 @@
 """Device sender engine (C ABI cn_tx_*): ack processing, duplicate-hint fast
 retransmit, RTO backoff and the commit/egress pump of chunknet::Transport
 (src/transport.cpp:144-542, 807-942, 1078-1169), one warp per connection,
-for congestion control none (OpenLoop), one engine per host, DefaultPolicy.
+with congestion control none (OpenLoop) or Swift (cc.cpp:108-156, global
+scope), the per-path retransmission queues and deficit-round-robin egress
+(:329-431), one engine per host, DefaultPolicy.
 
 Inputs are per-connection event streams: message submissions
 (Transport::send_message at time t) and acks delivered at the sender (the
@@ -23,14 +25,17 @@ SUBMIT_DTYPE = np.dtype([("t", "<i8"), ("len", "<u8"), ("tag", "<u8")])
 STATS_DTYPE = np.dtype([(n, "<u8") for n in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos",
                                              "msgs_sent", "msgs_completed", "backpressured",
                                              "n_log")] +
-                       [("srtt", "<i8"), ("rttvar", "<i8"), ("backoff", "<i4"), ("live_msgs", "<i4")])
+                       [("srtt", "<i8"), ("rttvar", "<i8"), ("backoff", "<i4"), ("live_msgs", "<i4"),
+                        ("cwnd_bytes", "<i8"), ("inflight", "<i8"), ("cwnd_pkts", "<f8")])
+CC = {"none": 0, "swift": 2}
 
 
 class TxEngine:
     def __init__(self, n_conns, *, chunk_bytes, rto_min, commit_ahead, base_rtt_ns, seed,
                  lb="oblivious", max_paths=1, n_paths=None, src=None, dst=None, rto_max=0,
                  dupack_threshold=8, rtx_avoid_prev_path=True, stream_index0=0,
-                 chunk_pool=1 << 20, log_cap=1 << 16, device="cuda"):
+                 chunk_pool=1 << 20, log_cap=1 << 16, cc="none", swift_target_ns=0,
+                 drr_quantum=32768, mss=4032, cap_bytes=0, init_cwnd_pkts=2.0, device="cuda"):
         L = _lib.lib()
         c = _lib.TxConfig()
         L.cn_tx_config_default(ctypes.byref(c))
@@ -39,6 +44,10 @@ class TxEngine:
         c.lb_policy, c.max_paths, c.log_cap = LB[lb], max_paths, log_cap
         c.rto_min, c.rto_max, c.commit_ahead = rto_min, rto_max, commit_ahead
         c.base_rtt_ns, c.seed, c.stream_index0, c.chunk_pool = float(base_rtt_ns), seed, stream_index0, chunk_pool
+        if cc not in CC:
+            raise ValueError(f"cc must be one of {sorted(CC)} (CUBIC stays host-side)")
+        c.cc_algo, c.swift_target_ns, c.drr_quantum = CC[cc], swift_target_ns, drr_quantum
+        c.mss, c.cap_bytes, c.init_cwnd_pkts = mss, cap_bytes, float(init_cwnd_pkts)
         self.device = torch.device(device)
         self.n, self.log_cap = n_conns, log_cap
         arr = lambda v: (ctypes.c_int32 * n_conns)(*[int(x) for x in v]) if v is not None else None  # noqa: E731

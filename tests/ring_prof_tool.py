@@ -1,4 +1,5 @@
-"""Profiling helper (not a test): phase timing of RingAllreduce.run on rank 0."""
+"""Profiling helper (not a test): per-kernel receive-path times inside the
+ring all-reduce (serial profiling mode) and the whole-iteration time."""
 import os
 import sys
 
@@ -12,31 +13,34 @@ def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2504_17307_b200.collective import RingAllreduce, packetize
+    from paper_2504_17307_b200.collective import RingAllreduce
     count = (1 << 30) // 4
-    x = torch.randn(count, device="cuda")
     ring = RingAllreduce(count, torch.float32)
+    ring.buffer().normal_()
     for _ in range(2):
-        ring.run(x)
+        ring.run()
     torch.cuda.synchronize()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    e = [ev() for _ in range(4)]
-    nb = ring.seg_bytes[0]
-    nch = (nb + ring.cb - 1) // ring.cb
-    e[0].record()
+    e0, e1 = ev(), ev()
+    e0.record()
     for _ in range(5):
-        ring.sched.select("p2_rtt", offsets=ring.path_offs, out=ring.paths_all)
-    e[1].record()
-    for _ in range(5):
-        packetize(nb, ring.cb, src=0, dst=1, chunk_paths=ring.paths_all[:nch], out=ring.hdrs[1])
-    e[2].record()
-    for _ in range(5):
-        ring.rx_rs.reset()
-    e[3].record()
+        ring.run()
+    e1.record()
     torch.cuda.synchronize()
+    it = e0.elapsed_time(e1) / 5
+    for rx in (ring.rx_rs, ring.rx_ag):
+        rx.set_profiling(True)
+        rx.kernel_profile()
+    e0.record()
+    for _ in range(3):
+        ring.run()
+    e1.record()
+    torch.cuda.synchronize()
+    p1, n1 = ring.rx_rs.kernel_profile()
+    p2, n2 = ring.rx_ag.kernel_profile()
     if dist.get_rank() == 0:
-        print("select ms", e[0].elapsed_time(e[1]) / 5, "packetize ms", e[1].elapsed_time(e[2]) / 5,
-              "reset ms", e[2].elapsed_time(e[3]) / 5, "chunks", nch)
+        print(f"n={ring.n} iter ms {it:.3f} (serial-profiled {e0.elapsed_time(e1) / 3:.3f})")
+        print("rs", {k: round(v / n1, 4) for k, v in p1.items()}, "ag", {k: round(v / n2, 4) for k, v in p2.items()})
     ring.close()
     dist.destroy_process_group()
 

@@ -1,8 +1,13 @@
 """Device sender engine (csrc/tx.cu) vs the reference sender: the same
 submissions and timed acks replayed into the unmodified reference Transport
 over a blackhole (golden tests/golden/sender_*.npz, oracle/gen_fixtures.py)
-must produce the identical transmit log -- every (re)transmission's time,
-message, chunk, path and rtx flag -- and the same Transport::Stats."""
+must produce the identical transmit log -- every (re)transmission, in
+emission order, with its time, message, chunk, path and rtx flag -- and the
+same Transport::Stats.  sender_<name>: congestion control none (OpenLoop);
+sender_swift_<name>: Swift with global scope, target 3 x base RTT, the
+window gating egress (DRR over the path ring, retransmission queues first).
+The closed_* stimuli come from Swift DES runs, so there the replay is the
+DES sender itself."""
 import glob
 import json
 import os
@@ -23,10 +28,6 @@ def _events(submits, acks):
     return [(typ, k) for _, typ, k in ev]
 
 
-def _sorted(tx):
-    return np.sort(tx, order=["t", "msg_seq", "chunk"])
-
-
 @pytest.mark.parametrize("name", NAMES)
 def test_tx_engine_matches_reference_sender(name):
     from paper_2504_17307_b200.sender import TxEngine
@@ -36,12 +37,13 @@ def test_tx_engine_matches_reference_sender(name):
                    rto_max=meta["rto_max"], commit_ahead=meta["commit_ahead"],
                    base_rtt_ns=meta["base_rtt"], seed=meta["seed"], lb=meta["lb"],
                    max_paths=meta["n_paths"], src=[meta["src"]], dst=[meta["dst"]],
-                   chunk_pool=1 << 18, log_cap=1 << 17)
+                   chunk_pool=1 << 18, log_cap=1 << 17, cc=meta.get("cc", "none"),
+                   swift_target_ns=meta.get("swift_target_ns", 0))
     st = eng.run([_events(z["submits"], z["acks"])], z["submits"], z["acks"], 60_000_000_000)[0]
     ref = meta["stats"]
     for k in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos", "msgs_completed"):
         assert int(st[k]) == ref[k], (k, int(st[k]), ref[k])
-    got, want = _sorted(eng.log_np(0)), _sorted(z["tx"])
+    got, want = eng.log_np(0), z["tx"]
     assert len(got) == len(want)
     for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
         bad = np.nonzero(got[f] != want[f])[0]

@@ -109,15 +109,60 @@ __device__ __forceinline__ uint32_t pkts_of(const RxDev& d, uint32_t clen) {
 // rconn_at (transport.cpp:546-563), the stale-generation test (:602), lazy
 // MsgRecv init (:620-626) with its chunk vector and buffer (:637, :723),
 // chunk init (:639-645) and the per-packet bit (:676-683) recorded as a
-// first-arrival time.  Table work is warp-aggregated: one leader lane per
-// distinct connection / message generation in the warp.
-__global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
-                                                uint32_t n) {
+// first-arrival time.
+//
+// Table work is block-aggregated: a batch carries few distinct connections
+// and message generations, and every packet of a generation reads the same
+// table slot and GenState line -- thousands of same-line L2 requests that
+// serialise on one slice.  So lanes first dedupe keys in the warp
+// (match_any), warp leaders dedupe them again in a shared-memory map, and
+// only one thread per distinct key and block touches the global tables;
+// results are broadcast through shared memory.
+constexpr int kIngestThreads = 256;  // one packet per thread
+constexpr int kIngMap = 512;         // shared map slots (power of two, >= 2 x threads)
+constexpr unsigned long long kMapEmpty = ~0ull;
+
+// Inserts key into the block map; returns its slot and whether this thread
+// owns it (first inserter).
+__device__ __forceinline__ uint32_t map_insert(unsigned long long* keys, uint64_t key, bool* own) {
+    uint32_t h = static_cast<uint32_t>(mix64(key)) & (kIngMap - 1);
+    for (;;) {
+        unsigned long long k = keys[h];
+        if (k == key) {
+            *own = false;
+            return h;
+        }
+        if (k == kMapEmpty) {
+            unsigned long long old = atomicCAS(&keys[h], kMapEmpty, key);
+            if (old == kMapEmpty) {
+                *own = true;
+                return h;
+            }
+            if (old == key) {
+                *own = false;
+                return h;
+            }
+        }
+        h = (h + 1) & (kIngMap - 1);
+    }
+}
+
+__global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
+                                                           uint32_t n) {
+    __shared__ unsigned long long m_key[kIngMap];
+    __shared__ unsigned long long m_cbase[kIngMap], m_glen[kIngMap];
+    __shared__ uint32_t m_val[kIngMap], m_nch[kIngMap], m_touch[kIngMap];
+    __shared__ uint32_t s_status;
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
     if (i < tiles) d.tile_state[i] = 0;
+    for (int k = threadIdx.x; k < kIngMap; k += kIngestThreads) {
+        m_key[k] = kMapEmpty;
+        m_touch[k] = 0;
+    }
+    if (threadIdx.x == 0) s_status = 0;
     uint32_t status = 0;
     uint32_t g = kErr;
     uint32_t touch = 0;
@@ -136,18 +181,22 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
         memset(&h, 0, sizeof h);
     }
     const uint32_t mid = (h.hdr >> 17) & 0x7F;
-    // ---- connection (dst, src, conn_id), one table probe per distinct key
-    const uint64_t rkey = ok ? ((static_cast<uint64_t>(h.dst) << 32) |
-                                (static_cast<uint64_t>(h.src) << 8) | (h.hdr >> 24))
-                             : (0xF000000000000000ull | lane);
-    const unsigned pr = __match_any_sync(0xffffffffu, rkey);
-    const int lr = __ffs(pr) - 1;
-    uint32_t rc = kInf;
-    if (ok && lane == lr) {
-        bool ins = false;
-        rc = table_insert(d.rc_key, d.conn_mask, rkey, &ins);
+    __syncthreads();
+    // ---- connection (dst, src, conn_id)
+    const uint64_t rkey = (static_cast<uint64_t>(h.dst) << 32) | (static_cast<uint64_t>(h.src) << 8) |
+                          (h.hdr >> 24);
+    uint32_t rslot = 0;
+    {
+        const unsigned pr = __match_any_sync(0xffffffffu, ok ? rkey : (0xF000000000000000ull | lane));
+        const int lr = __ffs(pr) - 1;
+        bool own = false;
+        if (ok && lane == lr) rslot = map_insert(m_key, rkey, &own);
+        rslot = __shfl_sync(0xffffffffu, rslot, lr);
+        __syncthreads();
+        if (own) m_val[rslot] = table_insert(d.rc_key, d.conn_mask, rkey, &own);
+        __syncthreads();
     }
-    rc = __shfl_sync(0xffffffffu, rc, lr);
+    uint32_t rc = ok ? m_val[rslot] : kInf;
     if (ok && rc == kInf) {
         status |= CN_RXF_CAPACITY;
         ok = false;
@@ -157,13 +206,19 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
         ok = false;
     }
     // ---- message generation (rconn, msg_seq)
-    const uint64_t gkey = ok ? ((static_cast<uint64_t>(rc) << 40) | h.msg_seq)
-                             : (0xF000000000000000ull | lane);
-    const unsigned pg = __match_any_sync(0xffffffffu, gkey);
+    for (int k = threadIdx.x; k < kIngMap; k += kIngestThreads) m_key[k] = kMapEmpty;
+    __syncthreads();
+    const uint64_t gkey = (static_cast<uint64_t>(rc) << 40) | h.msg_seq;
+    const unsigned pg = __match_any_sync(0xffffffffu, ok ? gkey : (0xF000000000000000ull | lane));
     const int lg = __ffs(pg) - 1;
-    uint32_t gs = kInf, nch = 0;
-    unsigned long long cbase = 0, glen = 0;
-    if (ok && lane == lg) {
+    uint32_t gslot = 0;
+    bool gown = false;
+    if (ok && lane == lg) gslot = map_insert(m_key, gkey, &gown);
+    gslot = __shfl_sync(0xffffffffu, gslot, lg);
+    __syncthreads();
+    if (gown) {
+        uint32_t gs = kInf, nch = 0;
+        unsigned long long cbase = 0, glen = 0;
         bool gins = false;
         gs = table_insert(d.gen_key, d.gen_mask, gkey, &gins);
         if (gs != kInf) {
@@ -232,7 +287,8 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
                 nch = G->nchunks;
                 cbase = G->chunk_base;
                 glen = G->len;
-                if (atomicExch(&G->epoch, epoch) != epoch) {
+                // plain read first: only the first block of the batch pays the atomic
+                if (ld_volatile_u32(&G->epoch) != epoch && atomicExch(&G->epoch, epoch) != epoch) {
                     // first touch this batch: freeze the batch's lower bound
                     // (finalize advances cum) and clear the tile counters
                     G->lo_batch = G->cum;
@@ -245,12 +301,16 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
         } else {
             status |= CN_RXF_CAPACITY;
         }
+        m_val[gslot] = gs;
+        m_nch[gslot] = nch;
+        m_cbase[gslot] = cbase;
+        m_glen[gslot] = glen;
     }
-    gs = __shfl_sync(0xffffffffu, gs, lg);
-    nch = __shfl_sync(0xffffffffu, nch, lg);
-    cbase = __shfl_sync(0xffffffffu, cbase, lg);
-    glen = __shfl_sync(0xffffffffu, glen, lg);
+    __syncthreads();
+    const uint32_t gs = ok ? m_val[gslot] : kInf;
     if (ok && gs != kInf) {
+        const uint32_t nch = m_nch[gslot];
+        const unsigned long long cbase = m_cbase[gslot], glen = m_glen[gslot];
         const uint64_t c = h.chunk_offset / d.cb;
         const uint32_t s = h.seq_in_chunk;
         bool bad = nch == 0 || (h.chunk_offset % d.cb) != 0 || c >= nch || h.msg_len != glen;
@@ -277,16 +337,16 @@ __global__ void __launch_bounds__(256) k_ingest(RxDev d, const cn_pkt_hdr* __res
         }
     }
     if (i < n) d.p_gen[i] = g;
-    // chunk-vector size per message (:636-637), reduced over the group
-    uint32_t gm = 0;
-    for (unsigned p = pg; p; p &= p - 1) {
-        uint32_t v = __shfl_sync(pg, touch, __ffs(p) - 1);
-        gm = gm > v ? gm : v;
-    }
-    if (lane == lg && gs != kInf && gm)
-        atomicMax(&d.gen[gs].touch, (static_cast<unsigned long long>(epoch) << 32) | gm);
+    // chunk-vector size per message (:636-637): max over the block, one
+    // global atomic per generation and block
+    const uint32_t gm = __reduce_max_sync(pg, touch);  // lanes of one group share pg
+    if (lane == lg && gm) atomicMax(&m_touch[gslot], gm);
     status = __reduce_or_sync(0xffffffffu, status);
-    if (lane == 0 && status) atomicOr(&d.ctl->status, status);
+    if (lane == 0 && status) atomicOr(&s_status, status);
+    __syncthreads();
+    if (gown && m_val[gslot] != kInf && m_touch[gslot])
+        atomicMax(&d.gen[m_val[gslot]].touch, (static_cast<unsigned long long>(epoch) << 32) | m_touch[gslot]);
+    if (threadIdx.x == 0 && s_status) atomicOr(&d.ctl->status, s_status);
 }
 
 
@@ -487,11 +547,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
     }
 }
 
-__device__ __forceinline__ uint32_t pmax_at(const RxDev& d, const GenState& G, uint64_t x) {
-    if (x < G.cum) return 0;
-    if (x >= G.n_init) return kInf;
-    return d.c_pmax[G.chunk_base + x];
-}
 
 // -------------------------------------------------------------------- copy
 // accept_payload's scatter memcpy (:719-730) for every first-arriving packet
@@ -560,7 +615,12 @@ __device__ __forceinline__ void warp_scatter(uint8_t* __restrict__ dst, const ui
 #pragma unroll
             for (int k = 0; k < kCopyUnroll; ++k) {
                 uint32_t v = v0 + k * 32 + lane;
-                if (v < nv) d4[v] = R ? combine<R ? R : 1>(a[R ? k : 0], r[k]) : r[k];
+                if (v < nv) {
+                    // streaming stores: the message buffers must not evict the
+                    // bookkeeping arrays the concurrent ack kernels walk
+                    if (R) d4[v] = combine<R ? R : 1>(a[R ? k : 0], r[k]);
+                    else __stcs(d4 + v, r[k]);
+                }
             }
         }
         const uint32_t tail = nv << 4;
@@ -642,36 +702,48 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
     }
 }
 
-// What the reference does with packet i (handle_data's branches).
+// What the reference does with packet i (handle_data's branches).  Every
+// load that does not depend on an earlier one is issued up front: the
+// kernel is latency-bound and usually shares HBM with the scatter.
+__device__ __forceinline__ uint32_t pmax_ld(const RxDev& d, uint64_t cbase, uint32_t cum, uint32_t n_init,
+                                            uint64_t x) {
+    return x < cum ? 0u : x >= n_init ? kInf : d.c_pmax[cbase + x];
+}
 __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __restrict__ hdrs,
                                           uint32_t i, uint32_t* st, uint64_t* e_out) {
-    uint32_t g = d.p_gen[i];
-    uint32_t t = i + 1;
+    const uint32_t g = d.p_gen[i];
+    const uint64_t off = hdrs[i].chunk_offset;
+    const uint32_t s = hdrs[i].seq_in_chunk;
+    const uint32_t t = i + 1;
     if (g == kStale) return PC_STALE;  // transport.cpp:602-615
     if (g == kErr) return 0;
     const GenState& G = d.gen[g];
-    uint32_t dt = G.deliver_t;
-    if (t > dt) return PC_STALE;
-    uint64_t off = hdrs[i].chunk_offset;
-    uint32_t s = hdrs[i].seq_in_chunk;
-    uint64_t c = off / d.cb;
-    uint64_t e = G.chunk_base + c;
+    const uint32_t dt = G.deliver_t, cum = G.cum, n_init = G.n_init;
+    const uint64_t cbase = G.chunk_base;
+    const uint64_t c = off / d.cb;
+    const uint64_t e = cbase + c;
     *e_out = e;
+    const uint32_t fl = d.c_flags[e], cpl0 = d.c_cpl[e], seen = d.c_seen[e];
+    const uint32_t first = d.c_first[e * d.ppc + s];
+    const uint32_t pm0 = pmax_ld(d, cbase, cum, n_init, c);
+    const uint32_t pm1 = pmax_ld(d, cbase, cum, n_init, c + 128);
+    const uint32_t pm2 = c >= 128 ? pmax_ld(d, cbase, cum, n_init, c - 128) : 0u;
+    if (t > dt) return PC_STALE;
     uint8_t cls = 0;
-    uint32_t cpl = (d.c_flags[e] & CF_COMPLETE) ? 0 : d.c_cpl[e];
+    const uint32_t cpl = (fl & CF_COMPLETE) ? 0 : cpl0;
     if (cpl < t) {
         cls = PC_ACK;  // complete chunk (:651-655) or behind the cursor (:631-634)
     } else if (cpl == t) {
         cls = PC_ACK | PC_COPY;  // completes its chunk (:686-687)
         if (t == dt) cls |= PC_DELIVER;
-    } else if (!((d.c_seen[e] >> s) & 1u) && d.c_first[e * d.ppc + s] == t) {
+    } else if (!((seen >> s) & 1u) && first == t) {
         cls = PC_COPY;  // new packet of an open chunk: silent
     }
     // The reference unwraps the 8-bit csn against the cursor (:629-636):
     // verify it names chunk c (no aliasing) -- DESIGN.md §3.
-    if (pmax_at(d, G, c) < t) {
-        if (pmax_at(d, G, c + 128) < t) *st |= CN_RXF_ALIAS;
-    } else if (c >= 128 && pmax_at(d, G, c - 128) >= t) {
+    if (pm0 < t) {
+        if (pm1 < t) *st |= CN_RXF_ALIAS;
+    } else if (c >= 128 && pm2 >= t) {
         *st |= CN_RXF_ALIAS;
     }
     return cls;
@@ -735,23 +807,24 @@ __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __re
     int32_t epath = 0;
     uint32_t eecn = 0;
     if (rel < CN_CSN_WINDOW && ei < n_init) {
-        uint64_t E = cbase + ei;
-        uint32_t fl = d.c_flags[E];
-        if ((fl & CF_INIT) || d.c_init[E] <= t) {
-            uint32_t exp = pkts_of(d, chunk_len_of(d, G.len, ei));
-            uint32_t seen = d.c_seen[E];
-            uint32_t f = (static_cast<uint32_t>(lane) < exp && !((seen >> lane) & 1u))
-                             ? d.c_first[E * d.ppc + lane]
-                             : kInf;
-            bool fok = f <= t;
-            uint32_t lastf = __reduce_max_sync(0xffffffffu, fok ? f : 0u);
-            unsigned eb = __ballot_sync(0xffffffffu, fok && (hdrs[fok ? f - 1 : i].flags & CN_PKT_ECN));
+        // all of the echo chunk's state in one round trip
+        const uint64_t E = cbase + ei;
+        const uint32_t exp = pkts_of(d, chunk_len_of(d, G.len, ei));
+        const uint32_t fl = d.c_flags[E], cinit = d.c_init[E], seen = d.c_seen[E];
+        const int64_t txt0 = d.c_txt[E];
+        const int32_t path0 = d.c_path[E];
+        const uint32_t f0 = static_cast<uint32_t>(lane) < exp ? d.c_first[E * d.ppc + lane] : kInf;
+        if ((fl & CF_INIT) || cinit <= t) {
+            const uint32_t f = ((seen >> lane) & 1u) ? kInf : f0;
+            const bool fok = f <= t;
+            const uint32_t lastf = __reduce_max_sync(0xffffffffu, fok ? f : 0u);
+            const unsigned eb = __ballot_sync(0xffffffffu, fok && (hdrs[fok ? f - 1 : i].flags & CN_PKT_ECN));
             if (lastf) {
                 etxt = hdrs[lastf - 1].tx_time;
                 epath = hdrs[lastf - 1].path_id;
             } else {
-                etxt = d.c_txt[E];
-                epath = d.c_path[E];
+                etxt = txt0;
+                epath = path0;
             }
             eecn = (eb != 0) || (fl & CF_ECN);
         }
@@ -1075,6 +1148,8 @@ struct cn_rx {
     uint32_t max_tiles = 0;
     int launches = 0;
     int sms = 148;
+    int copy_bps = 2;  // k_copy blocks per SM (CN_COPY_BLOCKS_PER_SM overrides)
+    int scan_first = 1;  // launch scan/acks before the scatter (CN_SCAN_FIRST=0 reverts)
     // optional per-kernel timing with CUDA events on the launch stream
     bool profiling = false;
     cudaStream_t side = nullptr;           // k_copy overlaps the ack machinery
@@ -1176,6 +1251,8 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&rx->sms, cudaDevAttrMultiProcessorCount, dev);
+    if (const char* e = getenv("CN_COPY_BLOCKS_PER_SM")) rx->copy_bps = atoi(e) > 0 ? atoi(e) : 2;
+    if (const char* e = getenv("CN_SCAN_FIRST")) rx->scan_first = atoi(e);
 #define ALLOC(ptr, bytes)                                             \
     do {                                                              \
         cudaError_t e_ = cudaMalloc(&(ptr), (bytes));                 \
@@ -1291,8 +1368,11 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
         const uint8_t* pl = static_cast<const uint8_t*>(d_payload);
         uint32_t tiles = (n + kAckTile - 1) / kAckTile;
         uint32_t cw = (n + 7) / 8;  // 8 warps (packets) per copy block
-        uint32_t cmax = static_cast<uint32_t>(rx->sms) * 8;
-        k_ingest<<<(n + 255) / 256, 256, 0, s>>>(d, d_hdrs, n);
+        // a persistent scatter grid that leaves half the register file to
+        // the concurrent scan/ack kernels; 2 blocks x 8 warps x 8 x 16 B in
+        // flight per lane still cover HBM latency
+        uint32_t cmax = static_cast<uint32_t>(rx->sms * rx->copy_bps);
+        k_ingest<<<(n + kIngestThreads - 1) / kIngestThreads, kIngestThreads, 0, s>>>(d, d_hdrs, n);
         prof_mark(ev, s);
         // fork: the HBM-bound scatter runs beside the latency-bound ack path
         cudaStream_t cs = ev ? s : rx->side;
@@ -1301,18 +1381,22 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
             CNB_CUDA(cudaStreamWaitEvent(cs, rx->ev_fork, 0));
         }
         const uint32_t cg = cw < cmax ? cw : cmax;
-        if (d.reduce == 1)
-            k_copy<1><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
-        else if (d.reduce == 2)
-            k_copy<2><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
-        else
-            k_copy<0><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
-        prof_mark(ev, s);
+        auto copy = [&] {
+            if (d.reduce == 1)
+                k_copy<1><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+            else if (d.reduce == 2)
+                k_copy<2><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+            else
+                k_copy<0><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+            prof_mark(ev, s);
+        };
+        if (!rx->scan_first) copy();
         k_scan<<<gb, kScanThreads, 0, s>>>(d);
         prof_mark(ev, s);
         k_acks<<<tiles, kAckWarps * 32, 0, s>>>(d, d_hdrs, n, d_acks, max_acks, d_completions,
                                                max_completions);
         prof_mark(ev, s);
+        if (rx->scan_first) copy();
         if (!ev) {
             CNB_CUDA(cudaEventRecord(rx->ev_join, cs));
             CNB_CUDA(cudaStreamWaitEvent(s, rx->ev_join, 0));

@@ -1,0 +1,68 @@
+"""Profiling helper (not a test): GPU timeline of the receive-path graph
+(bench.py's cfg2_32k x K workload) from CUPTI kernel records (torch.profiler),
+to see launch gaps and stream overlap.  Usage:
+    python tests/rx_timeline_tool.py [K] [steps]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    K = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    import bench
+    import paper_2504_17307_b200 as cn
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    data, meta, _ = bench.load_trace("cfg2_32k")
+    data = bench.interleave(data, K)
+    n = len(data)
+    cb = meta["chunk_bytes"]
+    msg_len = int(data["msg_len"][0])
+    hdrs = cn.to_device_records(data, dev)
+    st = torch.randint(0, 256, (n * bench.MAX_PL,), dtype=torch.uint8, device=dev)
+    tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
+                      arena_bytes=K * (msg_len + (1 << 20)), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
+                      max_batch=n, max_conns=64, max_msgs=64)
+    def step():
+        s = torch.cuda.current_stream(dev)
+        tr.reset(s)
+        tr.rx_batch_async(hdrs, st, bench.MAX_PL, s)
+
+    step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(5):
+        g.replay()
+    torch.cuda.synchronize()
+    from torch.profiler import ProfilerActivity, profile
+    eager = os.environ.get("EAGER") == "1"
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            if eager:
+                step()
+            else:
+                g.replay()
+        torch.cuda.synchronize()
+    evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    rows = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
+    t0 = rows[0][0]
+    prev_reset = None
+    for a, b, nm in rows:
+        short = nm.split("(")[0].replace("void ", "").replace("cnb::", "")[:28]
+        if "k_reset" in short:
+            if prev_reset is not None:
+                print(f"--- step {(a - prev_reset):.1f} us")
+            prev_reset = a
+        print(f"{a - t0:9.1f} {b - t0:9.1f} {b - a:7.1f}  {short}")
+
+
+if __name__ == "__main__":
+    main()

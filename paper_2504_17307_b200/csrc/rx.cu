@@ -62,7 +62,7 @@ enum : uint8_t { PC_STALE = 1, PC_ACK = 2, PC_COPY = 4, PC_DELIVER = 8 };
 constexpr uint32_t kStale = kInf;    // p_gen marker: stale before the batch
 constexpr uint32_t kErr = kInf - 1;  // p_gen marker: rejected packet
 constexpr int kAckTile = 128;        // packets per k_acks tile / block
-constexpr int kAckWarps = 16;        // 512 threads, 8 packets per warp
+constexpr int kAckWarps = 8;         // 256 threads: 4 decide warps, 8 ack builders
 constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
 constexpr int kCopyUnroll = 8;       // 16-byte vectors in flight per lane
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
@@ -710,7 +710,7 @@ __device__ __forceinline__ uint32_t pmax_ld(const RxDev& d, uint64_t cbase, uint
     return x < cum ? 0u : x >= n_init ? kInf : d.c_pmax[cbase + x];
 }
 __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __restrict__ hdrs,
-                                          uint32_t i, uint32_t* st, uint64_t* e_out) {
+                                          uint32_t i, uint32_t* st, uint64_t* e_out, uint32_t* pmc) {
     const uint32_t g = d.p_gen[i];
     const uint64_t off = hdrs[i].chunk_offset;
     const uint32_t s = hdrs[i].seq_in_chunk;
@@ -728,6 +728,7 @@ __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __re
     const uint32_t pm0 = pmax_ld(d, cbase, cum, n_init, c);
     const uint32_t pm1 = pmax_ld(d, cbase, cum, n_init, c + 128);
     const uint32_t pm2 = c >= 128 ? pmax_ld(d, cbase, cum, n_init, c - 128) : 0u;
+    *pmc = pm0;
     if (t > dt) return PC_STALE;
     uint8_t cls = 0;
     const uint32_t cpl = (fl & CF_COMPLETE) ? 0 : cpl0;
@@ -750,14 +751,33 @@ __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __re
 }
 
 // -------------------------------------------------------------------- acks
-// One block per 128-packet tile: 4 warps decide (one lane per packet); the
-// tile's ack/completion counts are ordered with a warp-parallel decoupled
-// look-back while all 16 warps build their packets' ack snapshots
-// (send_ack :763-792, stale re-ack :602-615) into shared memory; then the
-// records are written to their stream positions, with completion records
-// (maybe_deliver :794-803).
+// Persistent blocks pull 128-packet tiles by ticket.  Per tile: 4 warps
+// decide (one lane per packet) and compact the tile's ack and completion
+// packets into lists; warp 0 orders the tile's counts with a warp-parallel
+// decoupled look-back while the other warps build the ack snapshots
+// (send_ack :763-792, stale re-ack :602-615) round-robin, one warp per ack;
+// then the records are written to their stream positions, with completion
+// records (maybe_deliver :794-803).
+
+// cum after packet t: the first x in [lo, hi) with pmax[x] > t (pmax is
+// non-decreasing over [cum0, n_init)), by 32-ary bisection
+__device__ __forceinline__ uint32_t first_above(const uint32_t* __restrict__ pm, uint32_t lo, uint32_t hi,
+                                                uint32_t t, int lane) {
+    while (hi - lo > 32) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t p = lo + (lane + 1) * step - 1;
+        const bool ok = p < hi && pm[p] <= t;
+        const uint32_t k = __popc(__ballot_sync(0xffffffffu, ok));
+        lo += k * step;
+        hi = hi < lo + step ? hi : lo + step;
+    }
+    const bool okc = lo + lane < hi && pm[lo + lane] <= t;
+    return lo + __popc(__ballot_sync(0xffffffffu, okc));
+}
+
 __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __restrict__ hdrs,
-                                          uint32_t i, uint8_t cls, int lane, cn_ack_rec* out) {
+                                          uint32_t i, uint8_t cls, uint32_t g, uint32_t pmc, int lane,
+                                          cn_ack_rec* out) {
     const cn_pkt_hdr h = hdrs[i];
     const uint32_t t = i + 1;
     const uint32_t csn = (h.hdr >> 9) & 0xFF;
@@ -776,33 +796,40 @@ __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __re
         }
         return;
     }
-    const GenState& G = d.gen[d.p_gen[i]];
+    const GenState& G = d.gen[g];
     const uint32_t cum0 = G.cum, n_init = G.n_init;
     const uint64_t cbase = G.chunk_base;
-    // cum after this packet: first x in [cum0, n_init) with pmax[x] > t
-    uint32_t lo = cum0, hi = n_init;
     const uint32_t* pm = d.c_pmax + cbase;
-    while (hi - lo > 32) {
-        uint32_t step = (hi - lo + 31) / 32;
-        uint32_t p = lo + (lane + 1) * step - 1;
-        bool ok = p < hi && pm[p] <= t;
-        uint32_t k = __popc(__ballot_sync(0xffffffffu, ok));
-        lo += k * step;
-        hi = hi < lo + step ? hi : lo + step;
+    // cum after this packet, searched outward from the packet's own chunk c
+    // (pmax[c] came from decide): usually one 32-chunk window decides it
+    const uint32_t c = static_cast<uint32_t>(h.chunk_offset / d.cb);
+    uint32_t cum;
+    if (pmc <= t) {  // the cursor is past c: scan upward from c + 1
+        const uint32_t x = c + 1 + lane;
+        const bool le = x < cum0 || (x < n_init && pm[x] <= t);
+        const unsigned b = __ballot_sync(0xffffffffu, le);
+        cum = b != 0xffffffffu ? c + 1 + __popc(b)
+                               : first_above(pm, c + 33 > cum0 ? c + 33 : cum0, n_init, t, lane);
+    } else {  // the cursor is at or before c: scan downward from c
+        const int64_t x = static_cast<int64_t>(c) - 32 + lane;
+        const bool gt = x >= static_cast<int64_t>(cum0) && pm[x] > t;
+        const unsigned b = __ballot_sync(0xffffffffu, gt);
+        if ((b & 1u) && static_cast<int64_t>(c) - 32 > static_cast<int64_t>(cum0))
+            cum = first_above(pm, cum0, c - 32, t, lane);
+        else
+            cum = b ? c - 32 + (__ffs(b) - 1) : c;
     }
-    bool okc = lo + lane < hi && pm[lo + lane] <= t;
-    const uint32_t cum = lo + __popc(__ballot_sync(0xffffffffu, okc));
     // 128-bit SACK, bit j = chunk cum+j complete (:775-779)
     const uint32_t* cp = d.c_cpl + cbase;
     uint32_t sw[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        uint32_t x = cum + q * 32 + lane;
+        const uint32_t x = cum + q * 32 + lane;
         sw[q] = __ballot_sync(0xffffffffu, x < n_init && cp[x] <= t);
     }
     // echo of chunk cum + uint8(cause - uint8(cum)) (:781-789)
-    uint32_t rel = (csn - (cum & 0xFF)) & 0xFF;
-    uint32_t ei = cum + rel;
+    const uint32_t rel = (csn - (cum & 0xFF)) & 0xFF;
+    const uint32_t ei = cum + rel;
     int64_t etxt = 0;
     int32_t epath = 0;
     uint32_t eecn = 0;
@@ -853,114 +880,119 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
     constexpr int kDecideWarps = kAckTile / 32;
     __shared__ cn_ack_rec s_rec[kAckTile];
     __shared__ uint8_t s_cls[kAckTile];
-    __shared__ uint32_t s_aloc[kAckTile], s_cloc[kAckTile];
+    __shared__ uint32_t s_g[kAckTile], s_pm[kAckTile];
+    __shared__ uint16_t s_alist[kAckTile], s_clist[kAckTile];
     __shared__ uint32_t s_wa[kDecideWarps], s_wc[kDecideWarps];
     __shared__ uint32_t s_tile, s_base_a, s_base_c;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&d.ctl->tile_ticket, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
     const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
-    const uint32_t i0 = tile * kAckTile;
-    if (warp < kDecideWarps) {
-        uint32_t st = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&d.ctl->tile_ticket, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= tiles) break;
+        const uint32_t i0 = tile * kAckTile;
         uint8_t cls = 0;
-        uint64_t e = 0;
-        const uint32_t j = warp * 32 + lane;
-        const uint32_t i = i0 + j;
-        if (i < n) cls = decide(d, hdrs, i, &st, &e);
-        if (cls & PC_COPY) {  // ChunkRx::ecn / any_rtx of new packets (:680-681)
-            uint8_t pf = hdrs[i].flags;
-            uint32_t b = ((pf & CN_PKT_ECN) ? CF_ECN : 0) | ((pf & CN_PKT_RTX) ? CF_RTX : 0);
-            if (b) atomicOr(&d.c_newfl[e], b);
+        unsigned ab = 0, cb = 0;
+        if (warp < kDecideWarps) {
+            uint32_t st = 0;
+            uint64_t e = 0;
+            const uint32_t j = warp * 32 + lane;
+            const uint32_t i = i0 + j;
+            uint32_t pmc = 0;
+            if (i < n) cls = decide(d, hdrs, i, &st, &e, &pmc);
+            if (cls & PC_COPY) {  // ChunkRx::ecn / any_rtx of new packets (:680-681)
+                const uint8_t pf = hdrs[i].flags;
+                const uint32_t b = ((pf & CN_PKT_ECN) ? CF_ECN : 0) | ((pf & CN_PKT_RTX) ? CF_RTX : 0);
+                if (b) atomicOr(&d.c_newfl[e], b);
+            }
+            ab = __ballot_sync(0xffffffffu, cls & (PC_STALE | PC_ACK));
+            cb = __ballot_sync(0xffffffffu, cls & PC_DELIVER);
+            s_cls[j] = cls;
+            s_pm[j] = pmc;
+            if (i < n) s_g[j] = d.p_gen[i];
+            if (lane == 0) {
+                s_wa[warp] = __popc(ab);
+                s_wc[warp] = __popc(cb);
+            }
+            st = __reduce_or_sync(0xffffffffu, st);
+            if (lane == 0 && st) atomicOr(&d.ctl->status, st);
         }
-        const unsigned ab = __ballot_sync(0xffffffffu, cls & (PC_STALE | PC_ACK));
-        const unsigned cb = __ballot_sync(0xffffffffu, cls & PC_DELIVER);
-        const unsigned lt = (1u << lane) - 1;
-        s_cls[j] = cls;
-        s_aloc[j] = __popc(ab & lt);
-        s_cloc[j] = __popc(cb & lt);
-        if (lane == 0) {
-            s_wa[warp] = __popc(ab);
-            s_wc[warp] = __popc(cb);
-        }
-        st = __reduce_or_sync(0xffffffffu, st);
-        if (lane == 0 && st) atomicOr(&d.ctl->status, st);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t ta = 0, tc = 0;
+        __syncthreads();
+        uint32_t na = 0, nc = 0;
         for (int w = 0; w < kDecideWarps; ++w) {
-            ta += s_wa[w];
-            tc += s_wc[w];
+            na += s_wa[w];
+            nc += s_wc[w];
         }
-        const unsigned long long agg = ta | (static_cast<unsigned long long>(tc) << 31);
-        unsigned long long pre = 0;
-        if (tile == 0) {
-            if (lane == 0) atomicExch(&d.tile_state[0], kFlagIncl | agg);
-        } else {
-            if (lane == 0) atomicExch(&d.tile_state[tile], kFlagAgg | agg);
-            // warp-parallel look-back: lane l inspects tile (base - l)
-            int64_t base = static_cast<int64_t>(tile) - 1;
-            for (;;) {
-                int64_t p = base - lane;
-                unsigned long long v = p >= 0 ? ld_volatile_u64(&d.tile_state[p]) : kFlagIncl;
-                unsigned incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-                unsigned upto = incl ? ((2u << (__ffs(incl) - 1)) - 1) : 0xffffffffu;
-                unsigned waiting = __ballot_sync(0xffffffffu, (v >> 62) == 0) & upto;
-                if (waiting) {
-                    __nanosleep(32);
-                    continue;
+        if (warp < kDecideWarps) {  // compact the tile's ack / completion packets
+            uint32_t pa = 0, pc = 0;
+            for (int w = 0; w < warp; ++w) {
+                pa += s_wa[w];
+                pc += s_wc[w];
+            }
+            const unsigned lt = (1u << lane) - 1;
+            const uint16_t j = static_cast<uint16_t>(warp * 32 + lane);
+            if ((ab >> lane) & 1u) s_alist[pa + __popc(ab & lt)] = j;
+            if ((cb >> lane) & 1u) s_clist[pc + __popc(cb & lt)] = j;
+        }
+        if (warp == 0) {
+            const unsigned long long agg = na | (static_cast<unsigned long long>(nc) << 31);
+            unsigned long long pre = 0;
+            if (tile == 0) {
+                if (lane == 0) atomicExch(&d.tile_state[0], kFlagIncl | agg);
+            } else {
+                if (lane == 0) atomicExch(&d.tile_state[tile], kFlagAgg | agg);
+                // warp-parallel look-back: lane l inspects tile (base - l)
+                int64_t base = static_cast<int64_t>(tile) - 1;
+                for (;;) {
+                    const int64_t p = base - lane;
+                    const unsigned long long v = p >= 0 ? ld_volatile_u64(&d.tile_state[p]) : kFlagIncl;
+                    const unsigned incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                    const unsigned upto = incl ? ((2u << (__ffs(incl) - 1)) - 1) : 0xffffffffu;
+                    const unsigned waiting = __ballot_sync(0xffffffffu, (v >> 62) == 0) & upto;
+                    if (waiting) {
+                        __nanosleep(32);
+                        continue;
+                    }
+                    unsigned long long mine = ((upto >> lane) & 1u) ? (v & ~(3ull << 62)) : 0ull;
+                    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+                    pre += mine;
+                    if (incl) break;
+                    base -= 32;
                 }
-                unsigned long long mine = ((upto >> lane) & 1u) ? (v & ~(3ull << 62)) : 0ull;
-                for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-                pre += mine;
-                if (incl) break;
-                base -= 32;
+                if (lane == 0) {
+                    __threadfence();
+                    atomicExch(&d.tile_state[tile], kFlagIncl | (agg + pre));
+                }
             }
             if (lane == 0) {
-                __threadfence();
-                atomicExch(&d.tile_state[tile], kFlagIncl | (agg + pre));
+                s_base_a = static_cast<uint32_t>(pre & 0x7FFFFFFFu);
+                s_base_c = static_cast<uint32_t>(pre >> 31);
+                if (tile == tiles - 1) {
+                    const unsigned long long tot = agg + pre;
+                    const uint32_t ta = static_cast<uint32_t>(tot & 0x7FFFFFFFu);
+                    const uint32_t tc = static_cast<uint32_t>(tot >> 31);
+                    d.ctl->n_acks = ta;
+                    d.ctl->n_cpls = tc;
+                    if (ta > max_acks || tc > max_cpls) atomicOr(&d.ctl->status, CN_RXF_CAPACITY);
+                }
             }
         }
-        if (lane == 0) {
-            s_base_a = static_cast<uint32_t>(pre & 0x7FFFFFFFu);
-            s_base_c = static_cast<uint32_t>(pre >> 31);
-            if (tile == tiles - 1) {
-                unsigned long long tot = agg + pre;
-                uint32_t na = static_cast<uint32_t>(tot & 0x7FFFFFFFu);
-                uint32_t nc = static_cast<uint32_t>(tot >> 31);
-                d.ctl->n_acks = na;
-                d.ctl->n_cpls = nc;
-                if (na > max_acks || nc > max_cpls) atomicOr(&d.ctl->status, CN_RXF_CAPACITY);
-            }
+        __syncthreads();  // s_alist / s_clist complete
+        // acks round-robin over the warps, warp 0 (busy looking back) last
+        for (uint32_t k = kAckWarps - 1 - warp; k < na; k += kAckWarps) {
+            const uint32_t j = s_alist[k];
+            build_ack(d, hdrs, i0 + j, s_cls[j], s_g[j], s_pm[j], lane, &s_rec[k]);
         }
-    }
-    // every warp builds the acks of its packets while warp 0 looks back
-    constexpr int kPer = kAckTile / kAckWarps;
-    for (int jj = 0; jj < kPer; ++jj) {
-        const int j = warp * kPer + jj;
-        const uint8_t cls = s_cls[j];
-        if (cls & (PC_STALE | PC_ACK)) build_ack(d, hdrs, i0 + j, cls, lane, &s_rec[j]);
-    }
-    __syncthreads();
-    for (int jj = 0; jj < kPer; ++jj) {
-        const int j = warp * kPer + jj;
-        const uint8_t cls = s_cls[j];
-        uint32_t w = j >> 5, pa = s_aloc[j], pc = s_cloc[j];
-        for (uint32_t q = 0; q < w; ++q) {
-            pa += s_wa[q];
-            pc += s_wc[q];
+        __syncthreads();
+        for (uint32_t k = warp; k < na; k += kAckWarps) {
+            const uint32_t a = s_base_a + k;
+            if (lane < 16 && a < max_acks)
+                reinterpret_cast<uint32_t*>(&acks[a])[lane] = reinterpret_cast<const uint32_t*>(&s_rec[k])[lane];
         }
-        if ((cls & (PC_STALE | PC_ACK)) && lane < 16) {
-            uint32_t a = s_base_a + pa;
-            if (a < max_acks)
-                reinterpret_cast<uint32_t*>(&acks[a])[lane] =
-                    reinterpret_cast<const uint32_t*>(&s_rec[j])[lane];
-        }
-        if ((cls & PC_DELIVER) && lane == 0) {
-            const uint32_t i = i0 + j;
-            uint32_t a = s_base_c + pc;
+        for (uint32_t k = threadIdx.x; k < nc; k += kAckWarps * 32) {
+            const uint32_t i = i0 + s_clist[k];
+            const uint32_t a = s_base_c + k;
             if (a < max_cpls) {
                 const GenState& G = d.gen[d.p_gen[i]];
                 cn_completion c;
@@ -978,6 +1010,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
                 cpls[a] = c;
             }
         }
+        __syncthreads();  // shared lists are reused by the next tile
     }
 }
 
@@ -1148,8 +1181,9 @@ struct cn_rx {
     uint32_t max_tiles = 0;
     int launches = 0;
     int sms = 148;
-    int copy_bps = 2;  // k_copy blocks per SM (CN_COPY_BLOCKS_PER_SM overrides)
+    int copy_bps = 64;  // k_copy block cap per SM (CN_COPY_BLOCKS_PER_SM overrides)
     int scan_first = 1;  // launch scan/acks before the scatter (CN_SCAN_FIRST=0 reverts)
+    int hi_prio = 0;     // greatest stream priority: the latency-bound ack path wins SM slots
     // optional per-kernel timing with CUDA events on the launch stream
     bool profiling = false;
     cudaStream_t side = nullptr;           // k_copy overlaps the ack machinery
@@ -1251,8 +1285,14 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&rx->sms, cudaDevAttrMultiProcessorCount, dev);
-    if (const char* e = getenv("CN_COPY_BLOCKS_PER_SM")) rx->copy_bps = atoi(e) > 0 ? atoi(e) : 2;
+    if (const char* e = getenv("CN_COPY_BLOCKS_PER_SM")) rx->copy_bps = atoi(e) > 0 ? atoi(e) : 64;
     if (const char* e = getenv("CN_SCAN_FIRST")) rx->scan_first = atoi(e);
+    {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        rx->hi_prio = greatest;
+        if (const char* e = getenv("CN_ACK_PRIO")) rx->hi_prio = atoi(e) ? greatest : least;
+    }
 #define ALLOC(ptr, bytes)                                             \
     do {                                                              \
         cudaError_t e_ = cudaMalloc(&(ptr), (bytes));                 \
@@ -1368,9 +1408,10 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
         const uint8_t* pl = static_cast<const uint8_t*>(d_payload);
         uint32_t tiles = (n + kAckTile - 1) / kAckTile;
         uint32_t cw = (n + 7) / 8;  // 8 warps (packets) per copy block
-        // a persistent scatter grid that leaves half the register file to
-        // the concurrent scan/ack kernels; 2 blocks x 8 warps x 8 x 16 B in
-        // flight per lane still cover HBM latency
+        // about one packet per warp: short-lived blocks, so the block
+        // scheduler hands SM slots to the high-priority ack path first and
+        // to the scatter as they free up (a persistent scatter grid would
+        // pin half the register file for its whole duration)
         uint32_t cmax = static_cast<uint32_t>(rx->sms * rx->copy_bps);
         k_ingest<<<(n + kIngestThreads - 1) / kIngestThreads, kIngestThreads, 0, s>>>(d, d_hdrs, n);
         prof_mark(ev, s);
@@ -1390,13 +1431,38 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
                 k_copy<0><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
             prof_mark(ev, s);
         };
-        if (!rx->scan_first) copy();
-        k_scan<<<gb, kScanThreads, 0, s>>>(d);
+        const bool copy_last = rx->scan_first && !ev;  // profiling keeps the named kernel order
+        if (!copy_last) copy();
+        {
+            cudaLaunchConfig_t lc = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributePriority;
+            at[0].val.priority = rx->hi_prio;
+            lc.gridDim = dim3(gb);
+            lc.blockDim = dim3(kScanThreads);
+            lc.stream = s;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            CNB_CUDA(cudaLaunchKernelEx(&lc, k_scan, d));
+        }
         prof_mark(ev, s);
-        k_acks<<<tiles, kAckWarps * 32, 0, s>>>(d, d_hdrs, n, d_acks, max_acks, d_completions,
-                                               max_completions);
+        // persistent: as many blocks as fit beside the scatter, tiles by ticket
+        const uint32_t ag = tiles < static_cast<uint32_t>(rx->sms) * 4 ? tiles : rx->sms * 4;
+        {
+            cudaLaunchConfig_t lc = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributePriority;
+            at[0].val.priority = rx->hi_prio;
+            lc.gridDim = dim3(ag);
+            lc.blockDim = dim3(kAckWarps * 32);
+            lc.stream = s;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            CNB_CUDA(cudaLaunchKernelEx(&lc, k_acks, d, d_hdrs, n, d_acks, max_acks, d_completions,
+                                        max_completions));
+        }
         prof_mark(ev, s);
-        if (rx->scan_first) copy();
+        if (copy_last) copy();
         if (!ev) {
             CNB_CUDA(cudaEventRecord(rx->ev_join, cs));
             CNB_CUDA(cudaStreamWaitEvent(s, rx->ev_join, 0));

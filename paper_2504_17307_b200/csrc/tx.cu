@@ -134,6 +134,8 @@ struct Tx {
     double w;
     int has_sample, backoff, timer_armed, ring_len;
     uint64_t ring_pos;
+    uint32_t ring_idx;       // ring_pos % ring_len
+    uint32_t n_txq, n_rtxq;  // live entries over all tx / retransmission queues
     uint32_t q_seq, pump_pending;
     int64_t pump_at;  // schedule_pump (:219-230): one deferred pump per engine
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_completed;
@@ -212,6 +214,7 @@ struct Tx {
         }
         __syncwarp();
         ++ring_len;
+        ring_idx = static_cast<uint32_t>(ring_pos % static_cast<uint64_t>(ring_len));
     }
     __device__ void arm_rto(int64_t now) {  // transport.cpp:1083-1092
         if (timer_armed) return;
@@ -280,6 +283,7 @@ struct Tx {
             d.c_q[e] = kQRtx | q_seq;
             rtxq_n[p] += 1;
         }
+        ++n_rtxq;
         __syncwarp();
         ring_insert(p);
         if (!pump_pending) {  // schedule_pump (:541): runs after the events queued at `now`
@@ -329,25 +333,52 @@ __device__ bool queue_front(const Tx& x, int p, bool rtx, uint32_t* out_mid, uin
     return best != 0xFFFFFFFFu;
 }
 
+// `visits` DRR visits that cannot send (window shut or nothing queued):
+// each visits a distinct path of the ring once, so they are independent --
+// a tx-queued path tops its deficit up to one quantum, an idle one resets it
+// (:385-391) -- and run lane-parallel.
+__device__ void drr_idle(Tx& x, uint32_t visits) {
+    const uint32_t nr = static_cast<uint32_t>(x.ring_len);
+    const int64_t q = x.d.quantum;
+    __syncwarp();
+    for (uint32_t j = x.lane; j < visits; j += 32) {
+        uint32_t k = x.ring_idx + j;
+        k = k >= nr ? k - nr : k;
+        const int p = x.ring[k];
+        const int64_t def = x.deficit[p] + q;
+        x.deficit[p] = x.txq_n[p] ? (def > q ? q : def) : 0;
+    }
+    __syncwarp();
+    x.ring_pos += visits;
+    x.ring_idx = static_cast<uint32_t>((x.ring_idx + visits) % nr);
+}
+
 // egress (transport.cpp:329-431): retransmission queues in ring order, then
 // deficit round robin over the ring, every send gated by can_send.
 __device__ uint32_t egress(Tx& x, int64_t now) {
     uint32_t sent = 0;
-    for (int k = 0; k < x.ring_len; ++k) {  // :333-369
+    for (int k = 0; x.n_rtxq && k < x.ring_len; ++k) {  // :333-369
         const int p = x.ring[k];
         while (x.rtxq_n[p] > 0 && x.can_send()) {
             uint32_t mid, ci;
             if (!queue_front(x, p, true, &mid, &ci)) break;
             set_u32(&x.rtxq_n[p], x.rtxq_n[p] - 1, x.lane);
+            --x.n_rtxq;
             x.send_chunk(now, mid, load_msg(x.C, mid), ci, true);
             ++sent;
         }
     }
-    const int nr = x.ring_len;
-    int idle = 0;
+    const uint32_t nr = static_cast<uint32_t>(x.ring_len);
+    if (nr == 0) return sent;
+    uint32_t idle = 0;
     while (idle < nr) {  // :378-424
-        const int p = x.ring[x.ring_pos % static_cast<uint64_t>(nr)];
+        if (x.n_txq == 0 || !x.can_send()) {  // the remaining visits cannot send
+            drr_idle(x, nr - idle);
+            break;
+        }
+        const int p = x.ring[x.ring_idx];
         ++x.ring_pos;
+        if (++x.ring_idx == nr) x.ring_idx = 0;
         if (x.txq_n[p] == 0) {
             __syncwarp();
             if (x.lane == 0) x.deficit[p] = 0;
@@ -364,6 +395,7 @@ __device__ uint32_t egress(Tx& x, int64_t now) {
             const TxMsg m = load_msg(x.C, mid);
             const uint32_t len = x.chunk_len(m, ci);
             set_u32(&x.txq_n[p], x.txq_n[p] - 1, x.lane);
+            --x.n_txq;
             x.committed_unsent -= len;
             def -= len;
             x.send_chunk(now, mid, m, ci, false);
@@ -420,6 +452,7 @@ __device__ void commit_chunks(Tx& x) {
             x.d.c_q[e] = x.q_seq;
             x.txq_n[p] += 1;
         }
+        ++x.n_txq;
         __syncwarp();
         x.ring_insert(p);
         m.nchunks = ci + 1;
@@ -498,7 +531,8 @@ __device__ void release(Tx& x, int64_t now, const TxMsg& m, uint32_t ci, int64_t
         }
     }
     __syncwarp();
-    if (!(fl & TF_RTXP)) x.add_inflight(path, -static_cast<int64_t>(len));
+    if (fl & TF_RTXP) --x.n_rtxq;
+    else x.add_inflight(path, -static_cast<int64_t>(len));
     x.cc_on_ack(now, len, rtt);
     if (rtt > 0) {  // board.record_rtt / record_ecn (:819-822)
         __syncwarp();
@@ -805,6 +839,16 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
     x.timer_armed = C->timer_armed;
     x.ring_len = C->ring_len;
     x.ring_pos = C->ring_pos;
+    x.ring_idx = x.ring_len ? static_cast<uint32_t>(x.ring_pos % static_cast<uint64_t>(x.ring_len)) : 0;
+    {
+        uint32_t a = 0, b = 0;
+        for (uint32_t p = lane; p < mp; p += 32) {
+            a += txq[p];
+            b += rtxq[p];
+        }
+        x.n_txq = __reduce_add_sync(0xffffffffu, a);
+        x.n_rtxq = __reduce_add_sync(0xffffffffu, b);
+    }
     x.q_seq = C->q_seq;
     x.pump_pending = C->pump_pending;
     x.pump_at = C->pump_at;

@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sched", action="store_true")
     ap.add_argument("--no-ring", action="store_true")
+    ap.add_argument("--piece-mb", type=int, default=32, help="ring pipeline piece size (MiB)")
     return ap.parse_args()
 
 
@@ -261,7 +262,7 @@ def sender_bench(dev, conns=1024, scenario="cfg1", reps=3):
     return out
 
 
-def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30):
+def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30, piece_bytes=32 << 20):
     """BASELINE configs[2]: ring all-reduce of 1 GiB per rank (fp32 and bf16)
     through the transport (packetize -> NVLink zero-copy fused-reduce receive
     path), busbw = (S/t)*2(N-1)/N, max over ranks; NCCL's all_reduce on the
@@ -274,8 +275,10 @@ def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30):
     for dt, name in ((torch.float32, "fp32"), (torch.bfloat16, "bf16")):
         count = nbytes // (4 if dt == torch.float32 else 2)
         x = torch.randn(count, device=dev).to(dt)
-        ring = RingAllreduce(count, dt, chunk_bytes=32768, paths=8)
+        ring = RingAllreduce(count, dt, chunk_bytes=32768, paths=8, piece_bytes=piece_bytes)
         ring.buffer().copy_(x)
+        ring.run()  # eager once, then one captured iteration replayed in place
+        ring.capture()
         for _ in range(warmup):  # in place, like dist.all_reduce(y) below
             ring.run()
         torch.cuda.synchronize()
@@ -305,6 +308,7 @@ def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30):
         dist.all_reduce(tn, op=dist.ReduceOp.MAX)
         msn = float(tn.item())
         out[name] = {"bytes": nbytes, "ms": round(ms, 4), "busbw_GBps": round(busbw(nbytes, ms * 1e-3, world), 1),
+                     "pieces_per_step": ring.pieces,
                      "nccl_ms": round(msn, 4),
                      "nccl_busbw_GBps": round(busbw(nbytes, msn * 1e-3, world), 1)}
         ring.close()
@@ -523,7 +527,7 @@ def main():
 
     sched = sched_bench(dev) if not args.no_sched else None
     sender = sender_bench(dev) if not args.no_sched and rank == 0 else None
-    ring = ring_bench(dev, world, rank) if world > 1 and not args.no_ring else None
+    ring = ring_bench(dev, world, rank, piece_bytes=args.piece_mb << 20) if world > 1 and not args.no_ring else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -365,6 +365,20 @@ int cn_ipc_close(void* d_ptr);
 int cn_flag_signal(unsigned long long* d_a, unsigned long long* d_b, uint64_t value, void* stream);
 int cn_flag_wait(const unsigned long long* d_a, const unsigned long long* d_b, uint64_t value,
                  uint64_t max_spins, unsigned int* d_err, void* stream);
+/* Graph-replayable progress counters.  Targets are relative to a device
+ * iteration counter *d_iter: target = *d_iter * per_iter + offset (offset
+ * may be negative; targets below 0 are met).  wait spins (acquire, system
+ * scope) until *d_flag >= target; signal stores target into (peer) *d_flag
+ * (release, system scope); advance adds 1 to *d_iter. */
+int cn_ctr_wait(const unsigned long long* d_flag, const unsigned long long* d_iter, uint64_t per_iter,
+                int64_t offset, uint64_t max_spins, unsigned int* d_err, void* stream);
+int cn_ctr_signal(unsigned long long* d_flag, const unsigned long long* d_iter, uint64_t per_iter,
+                  int64_t offset, void* stream);
+int cn_ctr_advance(unsigned long long* d_iter, void* stream);
+/* Bulk device-to-device copy on a stream (the copy engines; a peer pointer
+ * from cn_ipc_open makes it an NVLink transfer -- the "wire" that delivers
+ * a message's payload into the receiver's staging slot). */
+int cn_copy_async(void* d_dst, const void* d_src, uint64_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -116,6 +116,10 @@ def lib():
     L.cn_ipc_close.argtypes = [vp]
     L.cn_flag_signal.argtypes = [vp, vp, u64, vp]
     L.cn_flag_wait.argtypes = [vp, vp, u64, u64, vp, vp]
+    L.cn_ctr_wait.argtypes = [vp, vp, u64, ctypes.c_int64, u64, vp, vp]
+    L.cn_ctr_signal.argtypes = [vp, vp, u64, ctypes.c_int64, vp]
+    L.cn_ctr_advance.argtypes = [vp, vp]
+    L.cn_copy_async.argtypes = [vp, vp, u64, vp]
     L.cn_tx_config_default.argtypes = [ctypes.POINTER(TxConfig)]
     L.cn_tx_config_default.restype = None
     L.cn_tx_create.argtypes = [ctypes.POINTER(TxConfig), u32, vp, vp, vp, ctypes.POINTER(vp)]

@@ -115,10 +115,25 @@ class RingAllreduce:
 
     Construct collectively (every rank of the default process group); then
     `run(x)` returns the all-reduced buffer (a view of the internal
-    accumulator) on every rank."""
+    accumulator) on every rank.
+
+    Pipelined push design.  Every segment message of a step is cut into
+    `pieces` chunk-aligned pieces.  The sender's "wire" is a copy-engine
+    transfer of a piece over NVLink into a staging slot in the receiver's
+    HBM (cn_copy_async), followed by a system-scope release of a progress
+    counter; a step's 64-B packet headers (cn_packetize, with the S3
+    scheduler's per-chunk paths, packetized once per iteration) travel with
+    its first piece into the receiver's header buffer.  The receiver runs the transport's receive path
+    (csrc/rx.cu: ingest, fused reduce-scatter or copy, SACK/cum bookkeeping,
+    completion) on each piece from local memory as soon as it lands, then
+    frees the slot.  Piece p of step k+1 leaves as soon as piece p of step k
+    has been reduced, so NVLink stays busy across steps (the pipelining NCCL
+    does with its chunked ring), and the copy engines move the bytes while
+    the SMs reduce.  Counters are relative to a device iteration counter, so
+    one iteration can be captured in a CUDA graph (capture()/replay())."""
 
     def __init__(self, count, dtype=torch.float32, *, chunk_bytes=32768, paths=8, seed=1,
-                 group=None, max_spins=1 << 26):
+                 group=None, piece_bytes=32 << 20, max_spins=1 << 26):
         self.group = group
         self.n = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -131,6 +146,7 @@ class RingAllreduce:
         n, r = self.n, self.rank
         if n < 2:
             raise ValueError("RingAllreduce needs >= 2 ranks")
+        L = _lib.lib()
         self._acc_buf = DeviceBuffer(count * self.elem, self.dev)
         self.acc = self._acc_buf.tensor(dtype, count)
         self.steps = ring_schedule(n, r)
@@ -138,60 +154,84 @@ class RingAllreduce:
         segb = [seg_bounds(count, n, j, self.quantum) for j in range(n)]
         self.seg_bytes = [(b - a) * self.elem for a, b in segb]
         self.seg_off = [a * self.elem for a, b in segb]
-        if min(self.seg_bytes) == 0:
-            raise ValueError("count too small for the ring")
-        # outgoing header rings, one per step (read by rank r+1 over NVLink)
-        self.n_pkts = [_lib.lib().cn_packet_count(self.seg_bytes[st[3]], chunk_bytes, MAX_PAYLOAD)
-                       if st[1] != "init" else 0 for st in self.steps]
-        self._hdr_bufs = [DeviceBuffer(max(1, k) * 64, self.dev) for k in self.n_pkts]
-        self.hdrs = [b.tensor() for b in self._hdr_bufs]
-        # per-chunk path choices for the outgoing messages (S3 scheduler)
-        # one virtual connection (RngStream) per step's message, so the path
-        # choices of all messages of an iteration are drawn in one launch
+        if min(self.seg_bytes) < chunk_bytes:
+            raise ValueError("count too small for the ring (a segment must hold a chunk)")
+        # pieces per step (the same on every rank and step), chunk-aligned; an
+        # even count feeds two push lanes (copy streams) alternately
+        P = max(1, min(-(-max(self.seg_bytes) // piece_bytes), min(self.seg_bytes) // chunk_bytes))
+        if P > 1 and P % 2:
+            P = P + 1 if P + 1 <= min(self.seg_bytes) // chunk_bytes else P - 1
+        self.pieces = P
+        self.lanes = 2 if P % 2 == 0 else 1
+        self.bounds = [[0 if p == 0 else (sb if p == P else sb * p // P // chunk_bytes * chunk_bytes)
+                        for p in range(P + 1)] for sb in self.seg_bytes]
+        self.slot_bytes = max(b[p + 1] - b[p] for b in self.bounds for p in range(P))
+        self.ppi = (2 * n - 2) * P  # pieces per iteration
+        ppc = -(-chunk_bytes // MAX_PAYLOAD)
+        self.n_pkts = [L.cn_packet_count(sb, chunk_bytes, MAX_PAYLOAD) for sb in self.seg_bytes]
+
+        def pkt_range(j, p):
+            lo, hi = self.bounds[j][p], self.bounds[j][p + 1]
+            return lo // chunk_bytes * ppc, (self.n_pkts[j] if hi == self.seg_bytes[j] else hi // chunk_bytes * ppc)
+        self.pkt_range = pkt_range
+        # receive side: staging slots and one header buffer per step (written by prev)
+        self._stage = DeviceBuffer(P * self.slot_bytes, self.dev)
+        self._hdr_bufs = [DeviceBuffer(max(1, self.n_pkts[st[4]]) * 64, self.dev) if st[1] != "init" else None
+                          for st in self.steps]
+        # flags: ready[2] (from prev), freed[2] (from next), err, iteration;
+        # one ready/freed counter pair per push lane (monotone within a lane)
+        self._flag_buf = DeviceBuffer(64, self.dev)
+        self.flags = self._flag_buf.tensor(torch.int64, 8)
+        fp = self._flag_buf.data_ptr()
+        self.f_ready, self.f_freed, self.f_err, self.f_it = fp, fp + 16, fp + 32, fp + 40
+        # per-chunk path choices of the outgoing messages (S3 scheduler): one
+        # virtual connection (RngStream) per piece of each step's message, so
+        # all of an iteration's choices come from one launch of many streams
         from .scheduler import PathScheduler
         n_msgs = len(self.steps) - 1
-        self.sched = PathScheduler(n_msgs, paths, seed, base_rtt_ns=10000.0, index0=r * n_msgs)
-        self.max_chunks = max((b + chunk_bytes - 1) // chunk_bytes for b in self.seg_bytes)
-        nchs = [(self.seg_bytes[st[3]] + chunk_bytes - 1) // chunk_bytes for st in self.steps[1:]]
-        offs = [0]
-        for c in nchs:
-            offs.append(offs[-1] + c)
+        self.sched = PathScheduler(n_msgs * P, paths, seed, base_rtt_ns=10000.0, index0=r * n_msgs * P)
+        offs, self.path_slices = [0], []
+        for st in self.steps[1:]:
+            b = self.bounds[st[3]]
+            start = offs[-1]
+            for p in range(P):
+                offs.append(start + -(-b[p + 1] // chunk_bytes))
+            self.path_slices.append((start, offs[-1]))
         self.path_offs = torch.tensor(offs, dtype=torch.int32, device=self.dev)
         self.paths_all = torch.empty(max(1, offs[-1]), dtype=torch.int32, device=self.dev)
-        self.path_slices = [(offs[i], offs[i + 1]) for i in range(n_msgs)]
-        # flags: [from_prev, from_next, err]
-        self._flag_buf = DeviceBuffer(64, self.dev)
-        self.flags = self._flag_buf.tensor(torch.int64, 4)
-        # exchange IPC handles: acc, headers, flags
-        mine = {"acc": _ipc_handle(self._acc_buf), "flags": _ipc_handle(self._flag_buf),
-                "hdrs": [_ipc_handle(b) for b in self._hdr_bufs]}
+        # my outgoing headers (packetized locally, copied per piece with the payload)
+        self._out_hdrs = [DeviceBuffer(max(1, self.n_pkts[st[3]]) * 64, self.dev) if st[1] != "init" else None
+                          for st in self.steps]
+        # exchange IPC handles: staging, header buffers, flags
+        mine = {"stage": _ipc_handle(self._stage), "flags": _ipc_handle(self._flag_buf),
+                "hdrs": [_ipc_handle(b) if b is not None else None for b in self._hdr_bufs]}
         allh = [None] * n
         dist.all_gather_object(allh, mine, group=group)
         prev, nxt = (r - 1) % n, (r + 1) % n
         self._opened = []
-        self.prev_acc = self._open(allh[prev]["acc"])
-        self.prev_hdrs = [self._open(h) for h in allh[prev]["hdrs"]]
-        self.prev_flags = self._open(allh[prev]["flags"])
-        self.next_flags = self._open(allh[nxt]["flags"]) if nxt != prev else self.prev_flags
-        self.prev_n_pkts = []
-        for st in ring_schedule(n, prev):
-            self.prev_n_pkts.append(_lib.lib().cn_packet_count(self.seg_bytes[st[3]], chunk_bytes,
-                                                               MAX_PAYLOAD) if st[1] != "init" else 0)
+        self.next_stage = self._open(allh[nxt]["stage"])
+        self.next_hdrs = [self._open(h) if h is not None else None for h in allh[nxt]["hdrs"]]
+        self.next_flags = self._open(allh[nxt]["flags"])
+        self.prev_flags = self._open(allh[prev]["flags"]) if prev != nxt else self.next_flags
         # receive paths: reduce-scatter (fused reduce) and all-gather (copy)
         red = "sum_f32" if dtype == torch.float32 else "sum_bf16"
-        maxp = max(self.prev_n_pkts)
-        kw = dict(device=self.dev, max_conns=4, max_msgs=4 * n, chunk_pool=4 * n * self.max_chunks + 64,
+        maxp = max(pkt_range(j, p)[1] - pkt_range(j, p)[0] for j in range(n) for p in range(P))
+        max_chunks = max(-(-sb // chunk_bytes) for sb in self.seg_bytes)
+        kw = dict(device=self.dev, max_conns=4, max_msgs=4 * n, chunk_pool=4 * n * max_chunks + 64,
                   arena_bytes=0, max_batch=maxp + 16, max_posts=4 * n)
         cfg = TransportConfig(chunk_bytes=chunk_bytes, paths=paths, lb="p2_rtt", carry_payload=True)
         self.rx_rs = Transport(cfg, reduce=red, **kw)
         self.rx_ag = Transport(cfg, **kw)
         accb = self.acc.view(torch.uint8)
         for (k, ph, s, snd, rcv, tag) in self.steps:
-            if ph == "rs":
-                self.rx_rs.post(tag, accb[self.seg_off[rcv]: self.seg_off[rcv] + self.seg_bytes[rcv]])
-            elif ph == "ag":
-                self.rx_ag.post(tag, accb[self.seg_off[rcv]: self.seg_off[rcv] + self.seg_bytes[rcv]])
-        self.g = 0  # global step counter (across iterations)
+            if ph in ("rs", "ag"):
+                (self.rx_rs if ph == "rs" else self.rx_ag).post(
+                    tag, accb[self.seg_off[rcv]: self.seg_off[rcv] + self.seg_bytes[rcv]])
+        self.push_streams = [torch.cuda.Stream(self.dev) for _ in range(self.lanes)]
+        self.rx_done = [[torch.cuda.Event() for _ in range(P)] for _ in self.steps]
+        self.ev_init = torch.cuda.Event()
+        self.ev_hdrs = torch.cuda.Event()
+        self._graph = None
         torch.cuda.synchronize()
         dist.barrier(group)
 
@@ -202,63 +242,111 @@ class RingAllreduce:
 
     def close(self):
         torch.cuda.synchronize()
+        self._graph = None
         for p in getattr(self, "_opened", []):
             _lib.lib().cn_ipc_close(ctypes.c_void_p(p))
         self._opened = []
-        for b in [getattr(self, "_acc_buf", None), getattr(self, "_flag_buf", None)] + \
-                list(getattr(self, "_hdr_bufs", [])):
+        for b in [getattr(self, "_acc_buf", None), getattr(self, "_flag_buf", None),
+                  getattr(self, "_stage", None)] + list(getattr(self, "_hdr_bufs", [])) + \
+                list(getattr(self, "_out_hdrs", [])):
             if b is not None:
                 b.free()
 
-    def _wait(self, g, s):
-        fp = self.flags.data_ptr()
-        _lib.check(_lib.lib().cn_flag_wait(fp, fp + 8, g, self.max_spins, fp + 16,
-                                           ctypes.c_void_p(s.cuda_stream)), "cn_flag_wait")
+    def _wait(self, flag, off, s):
+        _lib.check(_lib.lib().cn_ctr_wait(flag, self.f_it, self.ppi // self.lanes, off, self.max_spins,
+                                          self.f_err, ctypes.c_void_p(s.cuda_stream)), "cn_ctr_wait")
 
-    def _signal(self, g, s):
-        # next rank's from_prev, previous rank's from_next
-        a = self.next_flags
-        b = self.prev_flags + 8
-        _lib.check(_lib.lib().cn_flag_signal(a, b, g, ctypes.c_void_p(s.cuda_stream)),
-                   "cn_flag_signal")
+    def _signal(self, flag, off, s):
+        _lib.check(_lib.lib().cn_ctr_signal(flag, self.f_it, self.ppi // self.lanes, off,
+                                            ctypes.c_void_p(s.cuda_stream)), "cn_ctr_signal")
 
     def buffer(self):
         """The accumulator: write the input here and call run() for an
         in-place all-reduce (no init copy, like an in-place ncclAllReduce)."""
         return self.acc
 
+    def _enqueue(self, x, s):
+        L = _lib.lib()
+        n, r, P, NL = self.n, self.rank, self.pieces, self.lanes
+        sp = self.push_streams[0]
+        # init: the accumulator and fresh receive state (main stream); this
+        # iteration's paths and packet headers, packetized locally (push stream)
+        if x is not None:
+            self.acc.copy_(x)
+        self.rx_rs.reset(s)
+        self.rx_ag.reset(s)
+        self.ev_init.record(s)
+        sp.wait_event(self.ev_init)
+        self.sched.select("p2_rtt", offsets=self.path_offs, out=self.paths_all, stream=sp)
+        for (k, ph, st, snd, rcv, tag) in self.steps[1:]:
+            a, b = self.path_slices[k - 1]
+            out = _PeerView(self._out_hdrs[k].data_ptr(), self.n_pkts[snd] * 64)
+            packetize(self.seg_bytes[snd], self.cb, src=r, dst=(r + 1) % n, conn_id=0, msg_id=k % 128,
+                      msg_seq=k, tag=tag, chunk_paths=self.paths_all[a:b], out=out, stream=sp, device=self.dev)
+        self.ev_hdrs.record(sp)
+        for sl in self.push_streams[1:]:
+            sl.wait_event(self.ev_hdrs)
+        acc = self._acc_buf.data_ptr()
+        for (k, ph, st, snd, rcv, tag) in self.steps[1:]:
+            rx = self.rx_rs if ph == "rs" else self.rx_ag
+            for p in range(P):
+                gp = (k - 1) * P + p
+                ln, q = p % NL, gp // NL  # push lane, index within the lane
+                sp = self.push_streams[ln]
+                # push piece p of my message (segment snd) into next's slot p
+                if k > 1:
+                    sp.wait_event(self.rx_done[k - 1][p])  # its bytes were reduced here
+                # next consumed the slot's last piece (for p = 0 that also
+                # means it is done with this step's headers of the last iteration:
+                # its receive path runs pieces in order)
+                self._wait(self.f_freed + 8 * ln, q + 1 - P // NL, sp)
+                lo, hi = self.bounds[snd][p], self.bounds[snd][p + 1]
+                if p == 0:  # the whole step's headers ride with its first piece
+                    _lib.check(L.cn_copy_async(self.next_hdrs[k], self._out_hdrs[k].data_ptr(),
+                                               self.n_pkts[snd] * 64, ctypes.c_void_p(sp.cuda_stream)),
+                               "cn_copy_async")
+                _lib.check(L.cn_copy_async(self.next_stage + p * self.slot_bytes, acc + self.seg_off[snd] + lo,
+                                           hi - lo, ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
+                self._signal(self.next_flags + 8 * ln, q + 1, sp)  # next's ready counter
+                # receive piece p of prev's message (segment rcv) from my slot p
+                self._wait(self.f_ready + 8 * ln, q + 1, s)
+                rlo = self.bounds[rcv][p]
+                a, b = self.pkt_range(rcv, p)
+                hd = _PeerView(self._hdr_bufs[k].data_ptr() + a * 64, (b - a) * 64)
+                src = _PeerView(self._stage.data_ptr() + p * self.slot_bytes - rlo, self.slot_bytes)
+                rx.rx_batch_async(hd, src, 0, s, n=b - a)
+                self.rx_done[k][p].record(s)
+                self._signal(self.prev_flags + 16 + 8 * ln, q + 1, s)  # prev's freed counter
+        for sl in self.push_streams:
+            s.wait_stream(sl)
+        _lib.check(L.cn_ctr_advance(self.f_it, ctypes.c_void_p(s.cuda_stream)), "cn_ctr_advance")
+
     def run(self, x=None, stream=None):
         """All-reduce x (count elements, this rank's contribution), or the
         accumulator in place when x is None."""
         s = stream or torch.cuda.current_stream(self.dev)
-        n, r = self.n, self.rank
-        for (k, ph, st, snd, rcv, tag) in self.steps:
-            g = self.g
-            self._wait(g, s)  # neighbours finished global step g-1
-            if ph == "init":
-                if x is not None:
-                    self.acc.copy_(x)
-                self.rx_rs.reset(s)
-                self.rx_ag.reset(s)
-                self.sched.select("p2_rtt", offsets=self.path_offs, out=self.paths_all, stream=s)
-                for (k2, ph2, st2, snd2, rcv2, tag2) in self.steps[1:]:
-                    a, b = self.path_slices[k2 - 1]
-                    packetize(self.seg_bytes[snd2], self.cb, src=r, dst=(r + 1) % n, conn_id=0,
-                              msg_id=k2 % 128, msg_seq=k2, tag=tag2, chunk_paths=self.paths_all[a:b],
-                              out=self.hdrs[k2], stream=s, device=self.dev)
-            else:
-                rx = self.rx_rs if ph == "rs" else self.rx_ag
-                npk = self.prev_n_pkts[k]
-                hd = _PeerView(self.prev_hdrs[k], npk * 64)
-                src = _PeerView(self.prev_acc + self.seg_off[rcv], self.seg_bytes[rcv])
-                rx.rx_batch_async(hd, src, 0, s, n=npk)
-            self._signal(g + 1, s)
-            self.g += 1
+        if self._graph is not None and x is None:
+            self._graph.replay()
+        else:
+            self._enqueue(x, s)
         return self.acc
+
+    def capture(self):
+        """Capture one in-place iteration in a CUDA graph; later run() calls
+        without x replay it (host launch cost independent of the pieces)."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.graph(g, stream=s):
+            self._enqueue(None, torch.cuda.current_stream(self.dev))
+        torch.cuda.synchronize()
+        self._graph = g
+        return g
 
     def check(self):
         """Host check after run(): device flag timeouts and transport status."""
-        if int(self.flags[2].item()) != 0:
+        if int(self.flags[4].item()) != 0:
             raise _lib.ChunknetError(-5, "ring flag wait timed out")
         for rx in (self.rx_rs, self.rx_ag):
             res = _lib.RxResult.from_buffer_copy(bytes(rx._result.cpu().numpy()))

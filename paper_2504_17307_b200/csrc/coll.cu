@@ -81,9 +81,93 @@ __global__ void k_flag_wait(const unsigned long long* a, const unsigned long lon
     __threadfence_system();
 }
 
+__device__ __forceinline__ long long ctr_target(const unsigned long long* it, unsigned long long per_iter,
+                                                long long off) {
+    return static_cast<long long>(*reinterpret_cast<const volatile unsigned long long*>(it) * per_iter) + off;
+}
+
+__global__ void k_ctr_wait(const unsigned long long* f, const unsigned long long* it, unsigned long long per_iter,
+                           long long off, unsigned long long max_spins, unsigned int* err) {
+    const long long v = ctr_target(it, per_iter, off);
+    if (v <= 0) return;
+    unsigned long long spins = 0;
+    for (;;) {
+        unsigned long long x;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(f) : "memory");
+        if (static_cast<long long>(x) >= v) break;
+        if (++spins > max_spins) {
+            atomicOr(err, 1u);
+            break;
+        }
+        __nanosleep(64);
+    }
+    __threadfence_system();
+}
+
+__global__ void k_ctr_signal(unsigned long long* f, const unsigned long long* it, unsigned long long per_iter,
+                             long long off) {
+    const long long v = ctr_target(it, per_iter, off);
+    __threadfence_system();  // everything this stream wrote before
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(static_cast<unsigned long long>(v))
+                 : "memory");
+}
+
+__global__ void k_ctr_advance(unsigned long long* it) { *it += 1; }
+
 }  // namespace cnb
 
 using namespace cnb;
+
+// Progress kernels run at the greatest stream priority: they are single
+// threads that gate copy-engine transfers, so they must not queue behind the
+// receive path's short-lived scatter blocks for an SM slot.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_hi(void (*k)(KArgs...), void* stream, Args... args) {
+    static int prio = [] {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        return greatest;
+    }();
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = prio;
+    lc.gridDim = dim3(1);
+    lc.blockDim = dim3(1);
+    lc.stream = static_cast<cudaStream_t>(stream);
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, k, args...);
+}
+
+extern "C" int cn_ctr_wait(const unsigned long long* d_flag, const unsigned long long* d_iter, uint64_t per_iter,
+                           int64_t offset, uint64_t max_spins, unsigned int* d_err, void* stream) {
+    if (!d_flag || !d_iter || !d_err) return CN_E_INVALID;
+    CNB_CUDA(launch_hi(k_ctr_wait, stream, d_flag, d_iter, static_cast<unsigned long long>(per_iter),
+                       static_cast<long long>(offset), static_cast<unsigned long long>(max_spins), d_err));
+    return CN_OK;
+}
+
+extern "C" int cn_ctr_signal(unsigned long long* d_flag, const unsigned long long* d_iter, uint64_t per_iter,
+                             int64_t offset, void* stream) {
+    if (!d_flag || !d_iter) return CN_E_INVALID;
+    CNB_CUDA(launch_hi(k_ctr_signal, stream, d_flag, d_iter, static_cast<unsigned long long>(per_iter),
+                       static_cast<long long>(offset)));
+    return CN_OK;
+}
+
+extern "C" int cn_ctr_advance(unsigned long long* d_iter, void* stream) {
+    if (!d_iter) return CN_E_INVALID;
+    CNB_CUDA(launch_hi(k_ctr_advance, stream, d_iter));
+    return CN_OK;
+}
+
+extern "C" int cn_copy_async(void* d_dst, const void* d_src, uint64_t bytes, void* stream) {
+    if (!bytes) return CN_OK;
+    if (!d_dst || !d_src) return CN_E_INVALID;
+    CNB_CUDA(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+    return CN_OK;
+}
 
 extern "C" uint64_t cn_packet_count(uint64_t len, uint32_t chunk_bytes, uint32_t max_payload) {
     if (!len || !chunk_bytes || !max_payload) return 0;

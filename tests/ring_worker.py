@@ -13,6 +13,8 @@ def main():
     count = int(sys.argv[1]) if len(sys.argv) > 1 else (1 << 20) + 37
     dtype_s = sys.argv[2] if len(sys.argv) > 2 else "f32"
     iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    piece = int(sys.argv[4]) if len(sys.argv) > 4 else 32 << 20
+    graph = len(sys.argv) > 5 and sys.argv[5] == "graph"
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -29,10 +31,16 @@ def main():
     else:
         x = torch.from_numpy(xs[r].copy()).cuda()
         dt = torch.float32
-    ring = RingAllreduce(count, dt, chunk_bytes=32768, paths=8)
+    ring = RingAllreduce(count, dt, chunk_bytes=32768, paths=8, piece_bytes=piece)
     want = O.ring_allreduce(xs, quantum=ring.quantum)
+    if graph:
+        ring.capture()
     for it in range(iters):
-        out = ring.run(x)
+        if graph:  # in place: the captured iteration reduces the accumulator
+            ring.buffer().copy_(x)
+            out = ring.run()
+        else:
+            out = ring.run(x)
         torch.cuda.synchronize()
         ring.check()
         got = out.view(torch.int16).cpu().numpy().view(np.uint16) if dt == torch.bfloat16 \
@@ -45,7 +53,7 @@ def main():
     dist.barrier()
     ring.close()
     if r == 0:
-        print(f"RING_OK n={n} count={count} dtype={dtype_s} iters={iters}")
+        print(f"RING_OK n={n} count={count} dtype={dtype_s} iters={iters} pieces={ring.pieces} graph={graph}")
     dist.destroy_process_group()
 
 

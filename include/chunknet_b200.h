@@ -379,6 +379,9 @@ int cn_ctr_advance(unsigned long long* d_iter, void* stream);
  * from cn_ipc_open makes it an NVLink transfer -- the "wire" that delivers
  * a message's payload into the receiver's staging slot). */
 int cn_copy_async(void* d_dst, const void* d_src, uint64_t bytes, void* stream);
+/* The same transfer driven by SM threads (16-byte aligned pointers and size;
+ * blocks = 0 picks one per SM): posted NVLink writes beside the copy engines. */
+int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, void* stream);
 
 #ifdef __cplusplus
 }

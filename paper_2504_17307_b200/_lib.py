@@ -120,6 +120,7 @@ def lib():
     L.cn_ctr_signal.argtypes = [vp, vp, u64, ctypes.c_int64, vp]
     L.cn_ctr_advance.argtypes = [vp, vp]
     L.cn_copy_async.argtypes = [vp, vp, u64, vp]
+    L.cn_copy_sm.argtypes = [vp, vp, u64, u32, vp]
     L.cn_tx_config_default.argtypes = [ctypes.POINTER(TxConfig)]
     L.cn_tx_config_default.restype = None
     L.cn_tx_create.argtypes = [ctypes.POINTER(TxConfig), u32, vp, vp, vp, ctypes.POINTER(vp)]

@@ -228,6 +228,7 @@ class RingAllreduce:
                 (self.rx_rs if ph == "rs" else self.rx_ag).post(
                     tag, accb[self.seg_off[rcv]: self.seg_off[rcv] + self.seg_bytes[rcv]])
         self.push_streams = [torch.cuda.Stream(self.dev) for _ in range(self.lanes)]
+        self.hdr_stream = torch.cuda.Stream(self.dev)
         self.rx_done = [[torch.cuda.Event() for _ in range(P)] for _ in self.steps]
         self.ev_init = torch.cuda.Event()
         self.ev_hdrs = torch.cuda.Event()
@@ -276,16 +277,17 @@ class RingAllreduce:
         self.rx_rs.reset(s)
         self.rx_ag.reset(s)
         self.ev_init.record(s)
-        sp.wait_event(self.ev_init)
-        self.sched.select("p2_rtt", offsets=self.path_offs, out=self.paths_all, stream=sp)
+        sh = self.hdr_stream  # paths + headers, beside the first payload transfers
+        sh.wait_event(self.ev_init)
+        self.sched.select("p2_rtt", offsets=self.path_offs, out=self.paths_all, stream=sh)
         for (k, ph, st, snd, rcv, tag) in self.steps[1:]:
             a, b = self.path_slices[k - 1]
             out = _PeerView(self._out_hdrs[k].data_ptr(), self.n_pkts[snd] * 64)
             packetize(self.seg_bytes[snd], self.cb, src=r, dst=(r + 1) % n, conn_id=0, msg_id=k % 128,
-                      msg_seq=k, tag=tag, chunk_paths=self.paths_all[a:b], out=out, stream=sp, device=self.dev)
-        self.ev_hdrs.record(sp)
-        for sl in self.push_streams[1:]:
-            sl.wait_event(self.ev_hdrs)
+                      msg_seq=k, tag=tag, chunk_paths=self.paths_all[a:b], out=out, stream=sh, device=self.dev)
+        self.ev_hdrs.record(sh)
+        for sl in self.push_streams:
+            sl.wait_event(self.ev_init)
         acc = self._acc_buf.data_ptr()
         for (k, ph, st, snd, rcv, tag) in self.steps[1:]:
             rx = self.rx_rs if ph == "rs" else self.rx_ag
@@ -301,12 +303,14 @@ class RingAllreduce:
                 # its receive path runs pieces in order)
                 self._wait(self.f_freed + 8 * ln, q + 1 - P // NL, sp)
                 lo, hi = self.bounds[snd][p], self.bounds[snd][p + 1]
+                _lib.check(L.cn_copy_async(self.next_stage + p * self.slot_bytes, acc + self.seg_off[snd] + lo,
+                                           hi - lo, ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
                 if p == 0:  # the whole step's headers ride with its first piece
+                    if k == 1:
+                        sp.wait_event(self.ev_hdrs)
                     _lib.check(L.cn_copy_async(self.next_hdrs[k], self._out_hdrs[k].data_ptr(),
                                                self.n_pkts[snd] * 64, ctypes.c_void_p(sp.cuda_stream)),
                                "cn_copy_async")
-                _lib.check(L.cn_copy_async(self.next_stage + p * self.slot_bytes, acc + self.seg_off[snd] + lo,
-                                           hi - lo, ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
                 self._signal(self.next_flags + 8 * ln, q + 1, sp)  # next's ready counter
                 # receive piece p of prev's message (segment rcv) from my slot p
                 self._wait(self.f_ready + 8 * ln, q + 1, s)
@@ -317,7 +321,7 @@ class RingAllreduce:
                 rx.rx_batch_async(hd, src, 0, s, n=b - a)
                 self.rx_done[k][p].record(s)
                 self._signal(self.prev_flags + 16 + 8 * ln, q + 1, s)  # prev's freed counter
-        for sl in self.push_streams:
+        for sl in self.push_streams + [self.hdr_stream]:
             s.wait_stream(sl)
         _lib.check(L.cn_ctr_advance(self.f_it, ctypes.c_void_p(s.cuda_stream)), "cn_ctr_advance")
 

@@ -114,6 +114,24 @@ __global__ void k_ctr_signal(unsigned long long* f, const unsigned long long* it
 
 __global__ void k_ctr_advance(unsigned long long* it) { *it += 1; }
 
+// SM-driven bulk copy (16-byte vectors, 4 in flight per thread): with a peer
+// destination these are NVLink posted writes, a second "wire" beside the
+// copy engines.
+__global__ void __launch_bounds__(512) k_copy_sm(int4* __restrict__ dst, const int4* __restrict__ src,
+                                                 uint64_t nv) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < nv; i += 4 * stride) {
+        int4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+             e = __ldcs(src + i + 3 * stride);
+        dst[i] = a;
+        dst[i + stride] = b;
+        dst[i + 2 * stride] = c;
+        dst[i + 3 * stride] = e;
+    }
+    for (; i < nv; i += stride) dst[i] = __ldcs(src + i);
+}
+
 }  // namespace cnb
 
 using namespace cnb;
@@ -159,6 +177,18 @@ extern "C" int cn_ctr_signal(unsigned long long* d_flag, const unsigned long lon
 extern "C" int cn_ctr_advance(unsigned long long* d_iter, void* stream) {
     if (!d_iter) return CN_E_INVALID;
     CNB_CUDA(launch_hi(k_ctr_advance, stream, d_iter));
+    return CN_OK;
+}
+
+extern "C" int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, void* stream) {
+    if (!bytes) return CN_OK;
+    if (!d_dst || !d_src || ((reinterpret_cast<uintptr_t>(d_dst) | reinterpret_cast<uintptr_t>(d_src) | bytes) & 15)) {
+        set_error("cn_copy_sm: pointers and size must be 16-byte aligned");
+        return CN_E_INVALID;
+    }
+    k_copy_sm<<<blocks ? blocks : 148, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<int4*>(d_dst), static_cast<const int4*>(d_src), bytes >> 4);
+    CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }
 

@@ -73,6 +73,18 @@ def interleave(data, k):
     return out
 
 
+def copy_traffic(workload, conns):
+    """DRAM bytes (read + write) per k_copy launch from the committed ncu
+    --set full capture of this workload (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_copy_traffic.json")
+    if not os.path.exists(p):
+        return None
+    j = json.load(open(p))
+    if j.get("workload") != workload or int(j.get("conns", 0)) != conns:
+        return None
+    return int(j["dram__bytes_read.sum"]) + int(j["dram__bytes_write.sum"])
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -547,7 +559,8 @@ def main():
                        "parallelism": f"replicas x{world} (shard by connection)"},
             "mpkts_per_s": round(mpkts, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": copy_traffic(args.workload, K),
                          "kernel": "k_copy (payload scatter of first arrivals)",
                          "algorithmic_bytes_per_launch": algo_work,
                          "kernel_ms": round(work_ms, 5), "peak_kind": peak_kind,

@@ -383,6 +383,33 @@ int cn_copy_async(void* d_dst, const void* d_src, uint64_t bytes, void* stream);
  * blocks = 0 picks one per SM): posted NVLink writes beside the copy engines. */
 int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, void* stream);
 
+/* ------------------------------------------------------------ trace
+ * The reference's packet trace (experiment.cpp:18-40 trace_line over
+ * network.hpp:30-35 TraceEvent), one TSV line per record:
+ *   <t>\t<event>\t<link_id>\t<src>><dst>:<path_id>\t<csn>\t<kind>[,rtx][,ecn][,trim][,last]\n
+ * formatted on the device, byte-identical, in record order. */
+enum { CN_TEV_DELIVER = 0, CN_TEV_DROP = 1, CN_TEV_TRIM = 2, CN_TEV_LOSS = 3, CN_TEV_HDR_DROP = 4 };
+enum { CN_PK_DATA = 0, CN_PK_ACK = 1, CN_PK_NACK = 2, CN_PK_CREDIT = 3, CN_PK_RTS = 4, CN_PK_RTS_ACK = 5 };
+enum { CN_TRF_RTX = 1, CN_TRF_ECN = 2, CN_TRF_TRIM = 4, CN_TRF_LAST = 8 };
+typedef struct cn_trace_rec {
+    int64_t t;        /* TraceEvent::t                              */
+    int32_t link_id;  /* -1 = host delivery                         */
+    int32_t src, dst, path_id;
+    uint8_t csn, event, kind, flags;  /* CN_TEV_*, CN_PK_*, CN_TRF_* */
+    uint32_t reserved;
+} cn_trace_rec;
+uint64_t cn_trace_tsv_bound(uint64_t n);      /* output bytes that always suffice */
+uint64_t cn_trace_scratch_bytes(uint64_t n);  /* device scratch for cn_trace_format */
+/* Writes the lines (at most cap bytes) and the full length into *d_len. */
+int cn_trace_format(const cn_trace_rec* d_recs, uint64_t n, char* d_out, uint64_t cap, uint64_t* d_len,
+                    void* d_scratch, void* stream);
+/* Data packets as trace records (t = d_times[i], or tx_time when NULL). */
+int cn_trace_from_packets(const cn_pkt_hdr* d_hdrs, const int64_t* d_times, uint64_t n, int32_t event,
+                          int32_t link_id, cn_trace_rec* d_out, void* stream);
+/* Ack records as trace records (t = aux, the delivery time; path 0 as send_ack leaves it). */
+int cn_trace_from_acks(const cn_ack_rec* d_acks, uint64_t n, int32_t event, int32_t link_id,
+                       cn_trace_rec* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

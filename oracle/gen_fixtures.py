@@ -168,6 +168,102 @@ def gen_sender_swift(name):
     gen_sender(name, kw, flows, z["acks"], z["submits"], cc="swift")
 
 
+# reference experiment runs with run.trace = true (experiment.cpp:18-40): the
+# trace writer's golden text, covering every event / kind / flag
+TRACE_SCENARIOS = {
+    "trim_incast": """[topology]
+kind = star
+hosts = 4
+[net]
+rate_gbps = 100
+queue = trim
+qcap_bytes = 65536
+trim_depth = 2
+[transport]
+chunk_bytes = 16384
+paths = 2
+[workload]
+pattern = incast
+fan_in = 3
+bytes_per_host = 262144
+msg_bytes = 65536
+dst = 0
+[loss]
+drop_ratio = 0.01
+""",
+    "eqds_incast": """[topology]
+kind = star
+hosts = 6
+[net]
+rate_gbps = 100
+qcap_bytes = 131072
+[transport]
+chunk_bytes = 32768
+paths = 1
+receiver_driven = true
+[workload]
+pattern = incast
+fan_in = 5
+bytes_per_host = 262144
+msg_bytes = 131072
+dst = 0
+""",
+    "fat_tree_loss": """[topology]
+kind = fat_tree
+k = 4
+[net]
+rate_gbps = 100
+qcap_bytes = 32768
+[transport]
+chunk_bytes = 8192
+paths = 4
+[cc]
+algo = swift
+[workload]
+pattern = permutation
+bytes_per_host = 131072
+msg_bytes = 65536
+[loss]
+drop_ratio = 0.02
+[run]
+seed = 3
+""",
+    "ordered_loss": """[topology]
+kind = star
+hosts = 2
+[net]
+rate_gbps = 10
+[transport]
+reliability = ordered
+paths = 1
+[workload]
+pattern = fixed
+src = 0
+dst = 1
+bytes_per_host = 524288
+msg_bytes = 262144
+[loss]
+drop_ratio = 0.02
+[run]
+seed = 4
+""",
+}
+
+
+def gen_traces():
+    out = {}
+    for name, ini in TRACE_SCENARIOS.items():
+        t = ref.experiment_trace(ini)
+        out[f"ini_{name}"] = np.frombuffer(ini.encode(), dtype=np.uint8)
+        out[f"tsv_{name}"] = np.frombuffer(t, dtype=np.uint8)
+        kinds = sorted({ln.split(b"\t")[5].split(b",")[0] for ln in t.splitlines()})
+        events = sorted({ln.split(b"\t")[1] for ln in t.splitlines()})
+        print(f"trace {name}: {len(t.splitlines())} lines, events {events}, kinds {kinds}")
+    path = os.path.join(GOLDEN, "trace.npz")
+    np.savez_compressed(path, **out)
+    print(f"trace: -> {os.path.getsize(path)} B")
+
+
 def gen_rng():
     """RngStream / select_path draw sequences (rng.hpp:29-60, lb.cpp:7-27).
 
@@ -205,10 +301,13 @@ def gen_rng():
 
 def main(argv):
     os.makedirs(GOLDEN, exist_ok=True)
-    names = argv or list(SCENARIOS) + ["rng", "swift"]
+    names = argv or list(SCENARIOS) + ["rng", "swift", "trace"]
     for n in names:
         if n == "rng":
             gen_rng()
+            continue
+        if n == "trace":
+            gen_traces()
             continue
         if n == "swift":
             for m in SWIFT_SCENARIOS:

@@ -252,3 +252,18 @@ def csn_before(a, b, base, width):
     out = ctypes.c_int()
     rc = lib().cnref_csn_before(a, b, base, width, ctypes.byref(out))
     return rc, out.value
+
+
+def experiment_trace(ini):
+    """The reference's run_experiment on an ExperimentSpec INI text with
+    run.trace = true -> its trace.tsv text (experiment.cpp trace_line)."""
+    L = lib()
+    L.cnref_experiment_trace.restype = ctypes.c_int64
+    L.cnref_experiment_trace.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_uint64]
+    b = ini.encode()
+    n = L.cnref_experiment_trace(b, None, 0)
+    if n < 0:
+        raise RuntimeError(L.cnref_last_error().decode())
+    buf = ctypes.create_string_buffer(max(1, n))
+    L.cnref_experiment_trace(b, buf, n)
+    return buf.raw[:n]

@@ -32,7 +32,9 @@
 #include <vector>
 
 #define private public
+#include "chunknet/config.hpp"
 #include "chunknet/event_queue.hpp"
+#include "chunknet/experiment.hpp"
 #include "chunknet/lb.hpp"
 #include "chunknet/network.hpp"
 #include "chunknet/packet.hpp"
@@ -699,6 +701,24 @@ int cnref_csn_before(uint8_t a, uint8_t b, uint8_t base, int width, int* out) {
     } catch (const FieldRangeError& e) {
         g_err = e.what();
         return CN_E_FIELD_RANGE;
+    }
+}
+
+// The reference's own experiment runner (ExperimentSpec INI text ->
+// run_experiment) with run.trace = true: its trace.tsv text (experiment.cpp
+// trace_line) -- golden input for the trace writer.  Returns the full length;
+// copies at most cap bytes.
+int64_t cnref_experiment_trace(const char* ini, char* out, uint64_t cap) {
+    try {
+        ExperimentSpec spec = ExperimentSpec::from_text(ini);
+        spec.set("run.trace", "true");
+        RunOutput ro = run_experiment(spec.plan());
+        const std::string& t = ro.trace_tsv;
+        if (out && cap) std::memcpy(out, t.data(), std::min<uint64_t>(cap, t.size()));
+        return static_cast<int64_t>(t.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
     }
 }
 

@@ -121,6 +121,13 @@ def lib():
     L.cn_ctr_advance.argtypes = [vp, vp]
     L.cn_copy_async.argtypes = [vp, vp, u64, vp]
     L.cn_copy_sm.argtypes = [vp, vp, u64, u32, vp]
+    L.cn_trace_tsv_bound.restype = u64
+    L.cn_trace_tsv_bound.argtypes = [u64]
+    L.cn_trace_scratch_bytes.restype = u64
+    L.cn_trace_scratch_bytes.argtypes = [u64]
+    L.cn_trace_format.argtypes = [vp, u64, vp, u64, vp, vp, vp]
+    L.cn_trace_from_packets.argtypes = [vp, vp, u64, i32, i32, vp, vp]
+    L.cn_trace_from_acks.argtypes = [vp, u64, i32, i32, vp, vp]
     L.cn_tx_config_default.argtypes = [ctypes.POINTER(TxConfig)]
     L.cn_tx_config_default.restype = None
     L.cn_tx_create.argtypes = [ctypes.POINTER(TxConfig), u32, vp, vp, vp, ctypes.POINTER(vp)]

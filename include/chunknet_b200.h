@@ -383,6 +383,41 @@ int cn_copy_async(void* d_dst, const void* d_src, uint64_t bytes, void* stream);
  * blocks = 0 picks one per SM): posted NVLink writes beside the copy engines. */
 int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, void* stream);
 
+/* ------------------------------------------------------------- EQDS
+ * The receiver-driven pull pacer (EqdsReceiver, eqds.cpp:7-104), one per
+ * receiving host, run on the device over each receiver's time-ordered input
+ * stream.  cn_eqds_config mirrors EqdsParams (eqds.hpp) as Transport builds
+ * it (transport.cpp:45-73): quantum = credit_quantum, tick_ns =
+ * ser(quantum + pkts * hdr_overhead), bank_cap = credit_bank_quanta * quantum. */
+enum { CN_EQ_RTS = 0, CN_EQ_CHUNK = 1, CN_EQ_TRIM = 2 };
+typedef struct cn_eqds_config {
+    uint32_t quantum;
+    int32_t grant_to_idle;
+    int64_t tick_ns;
+    int64_t bank_cap;
+    uint32_t max_senders;  /* distinct senders per receiver */
+    uint32_t queue_cap;    /* entries per service list (stale ones included) */
+    uint32_t log_cap;      /* log records per receiver and run */
+    uint32_t reserved;
+} cn_eqds_config;
+/* on_rts(sender, demand = arg, rtx = flag) / on_chunk(sender, bytes = arg,
+ * was_rtx = flag) / on_trim(sender, chunk_len = arg) at time t */
+typedef struct cn_eqds_event { int64_t t; int32_t type; int32_t sender; uint64_t arg; int32_t flag; int32_t pad; } cn_eqds_event;
+/* kind 0: grant of `bytes` credit to sender; kind 1: rts_ack to sender */
+typedef struct cn_eqds_log { int64_t t; int32_t sender; uint32_t bytes; int32_t kind; int32_t pad; } cn_eqds_log;
+typedef struct cn_eqds cn_eqds;
+void cn_eqds_config_default(cn_eqds_config* cfg);
+int cn_eqds_create(const cn_eqds_config* cfg, uint32_t n_receivers, cn_eqds** out);
+void cn_eqds_destroy(cn_eqds* h);
+/* Events of receiver r are d_events[d_ev_off[r] .. d_ev_off[r+1]), ordered
+ * by time (ties: list order); ticks fire up to end_time.  d_log holds
+ * log_cap records per receiver, d_log_n the count per receiver.  State
+ * persists across runs. */
+int cn_eqds_run(cn_eqds* h, const uint32_t* d_ev_off, const cn_eqds_event* d_events, int64_t end_time,
+                cn_eqds_log* d_log, uint32_t* d_log_n, void* stream);
+/* status bits: 1 sender table full, 2 service list overflow, 4 log truncated */
+int cn_eqds_status(cn_eqds* h, uint32_t receiver, uint32_t* status, uint64_t* grants_sent);
+
 /* ------------------------------------------------------------ trace
  * The reference's packet trace (experiment.cpp:18-40 trace_line over
  * network.hpp:30-35 TraceEvent), one TSV line per record:

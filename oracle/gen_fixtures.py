@@ -264,6 +264,70 @@ def gen_traces():
     print(f"trace: -> {os.path.getsize(path)} B")
 
 
+def eqds_stream(rs, n_senders, n_events, t_step, sender_base=1):
+    """A random but protocol-shaped input stream for one EQDS receiver:
+    RTS registrations and resyncs (some flagged rtx), chunk arrivals (some
+    retransmitted), trimmed headers; ties in time included."""
+    from paper_2504_17307_b200.eqds import CHUNK, EV_DTYPE, RTS, TRIM
+    ev = np.zeros(n_events, dtype=EV_DTYPE)
+    t = 0
+    known = []
+    for i in range(n_events):
+        t += 0 if rs.rand() < 0.1 else int(rs.randint(1, t_step))
+        s = int(rs.randint(0, n_senders)) + sender_base
+        u = rs.rand()
+        if s not in known or u < 0.15:
+            typ, arg, flag = RTS, int(rs.randint(1, 64)) * 32768 + int(rs.randint(0, 32768)), int(rs.rand() < 0.3)
+            if s not in known:
+                known.append(s)
+        elif u < 0.25:
+            typ, arg, flag = TRIM, int(rs.choice([32768, 16384, int(rs.randint(1, 32768))])), 0
+        else:
+            typ, arg, flag = CHUNK, int(rs.choice([32768, 32768, int(rs.randint(1, 32768))])), int(rs.rand() < 0.1)
+        ev[i] = (t, typ, s, arg, flag, 0)
+    return ev
+
+
+# EqdsReceiver scenarios: (params, [per-receiver event streams])
+def eqds_scenarios():
+    from paper_2504_17307_b200.eqds import CHUNK, EV_DTYPE, RTS, TRIM, transport_params
+    P = transport_params()  # 32 KiB quantum, 100 Gb/s tick, 4-quantum bank
+    basic = np.array([(0, RTS, 1, 10 * 32768, 0, 0), (0, RTS, 2, 2 * 32768, 1, 0), (100, RTS, 3, 0, 0, 0),
+                      (5000, CHUNK, 1, 32768, 0, 0), (5000, TRIM, 2, 32768, 0, 0),
+                      (9000, CHUNK, 2, 32768, 1, 0), (20000, RTS, 1, 3 * 32768, 0, 0)], dtype=EV_DTYPE)
+    out = {"basic": (dict(P, grant_to_idle=True), [basic])}
+    rs = np.random.RandomState(21)
+    out["incast40"] = (dict(P, grant_to_idle=True), [eqds_stream(rs, 40, 3000, 4000)])
+    out["noidle"] = (dict(P, grant_to_idle=False), [eqds_stream(rs, 10, 1000, 6000)])
+    out["multi16"] = (dict(P, grant_to_idle=True),
+                      [eqds_stream(rs, int(rs.randint(8, 64)), 600, int(rs.randint(1500, 8000)),
+                                   sender_base=100 * r) for r in range(16)])
+    return out
+
+
+def gen_eqds():
+    out = {}
+    for name, (prm, streams) in eqds_scenarios().items():
+        offs, logs, loffs, gs = [0], [], [0], []
+        for ev in streams:
+            lg, g = ref.eqds_replay(ev, quantum=prm["quantum"], tick_ns=prm["tick_ns"], bank_cap=prm["bank_cap"],
+                                    grant_to_idle=prm["grant_to_idle"])
+            offs.append(offs[-1] + len(ev))
+            logs.append(lg)
+            loffs.append(loffs[-1] + len(lg))
+            gs.append(g)
+        out[f"{name}_events"] = np.concatenate(streams)
+        out[f"{name}_offsets"] = np.array(offs, dtype=np.uint32)
+        out[f"{name}_log"] = np.concatenate(logs)
+        out[f"{name}_log_offsets"] = np.array(loffs, dtype=np.uint64)
+        out[f"{name}_grants_sent"] = np.array(gs, dtype=np.uint64)
+        out[f"{name}_params"] = np.frombuffer(json.dumps(prm).encode(), dtype=np.uint8)
+        print(f"eqds {name}: receivers={len(streams)} events={offs[-1]} log={loffs[-1]} grants={sum(gs)}")
+    path = os.path.join(GOLDEN, "eqds.npz")
+    np.savez_compressed(path, **out)
+    print(f"eqds: -> {os.path.getsize(path)} B")
+
+
 def gen_rng():
     """RngStream / select_path draw sequences (rng.hpp:29-60, lb.cpp:7-27).
 
@@ -301,10 +365,13 @@ def gen_rng():
 
 def main(argv):
     os.makedirs(GOLDEN, exist_ok=True)
-    names = argv or list(SCENARIOS) + ["rng", "swift", "trace"]
+    names = argv or list(SCENARIOS) + ["rng", "swift", "trace", "eqds"]
     for n in names:
         if n == "rng":
             gen_rng()
+            continue
+        if n == "eqds":
+            gen_eqds()
             continue
         if n == "trace":
             gen_traces()

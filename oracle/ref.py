@@ -267,3 +267,23 @@ def experiment_trace(ini):
     buf = ctypes.create_string_buffer(max(1, n))
     L.cnref_experiment_trace(b, buf, n)
     return buf.raw[:n]
+
+
+def eqds_replay(events, *, quantum, tick_ns, bank_cap, grant_to_idle=True, cutoff=1 << 62, max_out=1 << 20):
+    """The reference EqdsReceiver (eqds.cpp) over scripted events
+    (paper_2504_17307_b200.eqds.EV_DTYPE) -> (log LOG_DTYPE, grants_sent)."""
+    from paper_2504_17307_b200.eqds import EV_DTYPE, LOG_DTYPE
+    L = lib()
+    L.cnref_eqds_replay.restype = ctypes.c_int
+    L.cnref_eqds_replay.argtypes = [ctypes.c_uint32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                    ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
+                                    ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64),
+                                    ctypes.POINTER(ctypes.c_uint64)]
+    ev = np.ascontiguousarray(events, dtype=EV_DTYPE)
+    out = np.zeros(max_out, dtype=LOG_DTYPE)
+    n, gs = ctypes.c_uint64(), ctypes.c_uint64()
+    rc = L.cnref_eqds_replay(quantum, tick_ns, bank_cap, 1 if grant_to_idle else 0, _ptr(ev), len(ev), cutoff,
+                             _ptr(out), max_out, ctypes.byref(n), ctypes.byref(gs))
+    if rc != 0:
+        raise RuntimeError(L.cnref_last_error().decode())
+    return out[: min(n.value, max_out)].copy(), gs.value

@@ -33,6 +33,7 @@
 
 #define private public
 #include "chunknet/config.hpp"
+#include "chunknet/eqds.hpp"
 #include "chunknet/event_queue.hpp"
 #include "chunknet/experiment.hpp"
 #include "chunknet/lb.hpp"
@@ -701,6 +702,50 @@ int cnref_csn_before(uint8_t a, uint8_t b, uint8_t base, int width, int* out) {
     } catch (const FieldRangeError& e) {
         g_err = e.what();
         return CN_E_FIELD_RANGE;
+    }
+}
+
+// EqdsReceiver (eqds.cpp) driven by a scripted event stream: every input
+// scheduled at its time (in list order for ties), ticks as the pacer
+// schedules them, run to cutoff.  Log records: grants and rts_acks in the
+// order the callbacks fire.
+struct cnref_eqds_event { int64_t t; int32_t type; int32_t sender; uint64_t arg; int32_t flag; int32_t pad; };
+struct cnref_eqds_log { int64_t t; int32_t sender; uint32_t bytes; int32_t kind; int32_t pad; };
+int cnref_eqds_replay(uint32_t quantum, int64_t tick_ns, int64_t bank_cap, int32_t grant_to_idle,
+                      const cnref_eqds_event* ev, uint64_t n, int64_t cutoff, cnref_eqds_log* out,
+                      uint64_t cap, uint64_t* n_out, uint64_t* grants_sent) {
+    try {
+        EventQueue eq;
+        EqdsParams p;
+        p.quantum = quantum;
+        p.tick_ns = tick_ns;
+        p.bank_cap = bank_cap;
+        p.grant_to_idle = grant_to_idle != 0;
+        uint64_t k = 0;
+        auto put = [&](int32_t sender, uint32_t bytes, int32_t kind) {
+            if (k < cap) out[k] = cnref_eqds_log{eq.now(), sender, bytes, kind, 0};
+            ++k;
+        };
+        EqdsReceiver pacer(
+            eq, p, [&](int s, uint32_t b) { put(s, b, 0); }, [&](int s) { put(s, 0, 1); });
+        for (uint64_t i = 0; i < n; ++i) {
+            cnref_eqds_event e = ev[i];
+            eq.schedule(e.t, [&pacer, e] {
+                if (e.type == 0)
+                    pacer.on_rts(e.sender, e.arg, e.flag != 0);
+                else if (e.type == 1)
+                    pacer.on_chunk(e.sender, static_cast<uint32_t>(e.arg), e.flag != 0);
+                else
+                    pacer.on_trim(e.sender, static_cast<uint32_t>(e.arg));
+            });
+        }
+        eq.run_until_idle(cutoff);
+        *n_out = k;
+        if (grants_sent) *grants_sent = pacer.grants_sent();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
     }
 }
 

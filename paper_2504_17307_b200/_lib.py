@@ -121,6 +121,13 @@ def lib():
     L.cn_ctr_advance.argtypes = [vp, vp]
     L.cn_copy_async.argtypes = [vp, vp, u64, vp]
     L.cn_copy_sm.argtypes = [vp, vp, u64, u32, vp]
+    L.cn_eqds_config_default.argtypes = [vp]
+    L.cn_eqds_config_default.restype = None
+    L.cn_eqds_create.argtypes = [vp, u32, ctypes.POINTER(vp)]
+    L.cn_eqds_destroy.argtypes = [vp]
+    L.cn_eqds_destroy.restype = None
+    L.cn_eqds_run.argtypes = [vp, vp, vp, ctypes.c_int64, vp, vp, vp]
+    L.cn_eqds_status.argtypes = [vp, u32, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64)]
     L.cn_trace_tsv_bound.restype = u64
     L.cn_trace_tsv_bound.argtypes = [u64]
     L.cn_trace_scratch_bytes.restype = u64

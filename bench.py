@@ -274,6 +274,68 @@ def sender_bench(dev, conns=1024, scenario="cfg1", reps=3):
     return out
 
 
+def eqds_bench(dev, receivers=4096, senders=32, events=1000, reps=3, cpu_receivers=64):
+    """§8(f) rank 1: the EQDS pull pacer (csrc/eqds.cu), one per receiving
+    host, over synthetic incast input streams (RTS / chunk / trim events,
+    `senders` per receiver); grants/s, with the reference EqdsReceiver on a
+    sample of the same streams on all host threads beside it."""
+    import concurrent.futures
+
+    import torch
+
+    from paper_2504_17307_b200.eqds import EV_DTYPE, EqdsPacers, transport_params
+    P = transport_params()
+    rs = np.random.RandomState(5)
+    n = receivers * events
+    ev = np.zeros(n, dtype=EV_DTYPE)
+    dt = np.where(rs.rand(n) < 0.1, 0, rs.randint(1, 4000, size=n)).reshape(receivers, events)
+    ev["t"] = np.cumsum(dt, axis=1).reshape(-1)
+    u = rs.rand(n)
+    ev["type"] = np.where(u < 0.15, 0, np.where(u < 0.25, 2, 1))
+    ev["type"].reshape(receivers, events)[:, :senders] = 0  # every sender registers first
+    ev["sender"] = (rs.randint(0, senders, size=n) + 1).reshape(-1)
+    ev["sender"].reshape(receivers, events)[:, :senders] = np.arange(1, senders + 1)
+    ev["arg"] = np.where(ev["type"] == 0, rs.randint(1, 64, size=n) * 32768, 32768)
+    ev["flag"] = rs.rand(n) < 0.1
+    off = np.arange(receivers + 1, dtype=np.uint32) * events
+    ms, grants = [], 0
+    for r in range(reps + 1):
+        pc = EqdsPacers(receivers, quantum=P["quantum"], tick_ns=P["tick_ns"], bank_cap=P["bank_cap"],
+                        max_senders=2 * senders, queue_cap=8192, log_cap=4 * events, device=dev)
+        prep = pc.prepare(ev, off)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pc.launch(prep, 1 << 62)
+        e1.record()
+        torch.cuda.synchronize()
+        if r:
+            ms.append(e0.elapsed_time(e1))
+        logs = pc.log_n.cpu().numpy()
+        pc.close()
+    t = min(ms) * 1e-3
+    out = {"config": f"{receivers} receivers x {events} input events ({senders} senders each), "
+                     f"quantum {P['quantum']} B, tick {P['tick_ns']} ns",
+           "events_per_s": round(n / t, 1), "log_records_per_s": round(int(logs.sum()) / t, 1),
+           "ms": round(t * 1e3, 3)}
+    try:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            sample = [ev[i * events:(i + 1) * events] for i in range(cpu_receivers)]
+            t0 = time.perf_counter()
+            with concurrent.futures.ThreadPoolExecutor(threads) as ex:  # ctypes releases the GIL
+                list(ex.map(lambda e: ref.eqds_replay(e, quantum=P["quantum"], tick_ns=P["tick_ns"],
+                                                      bank_cap=P["bank_cap"], max_out=4 * events), sample))
+            tc = time.perf_counter() - t0
+            out["cpu_reference_events_per_s"] = round(cpu_receivers * events / tc, 1)
+            out["cpu_threads"] = threads
+            out["cpu_sample"] = f"{cpu_receivers} of the receivers' streams"
+    except Exception as e:  # noqa: BLE001
+        out["cpu_reference_error"] = str(e)
+    return out
+
+
 def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30, piece_bytes=32 << 20):
     """BASELINE configs[2]: ring all-reduce of 1 GiB per rank (fp32 and bf16)
     through the transport (packetize -> NVLink zero-copy fused-reduce receive
@@ -539,6 +601,7 @@ def main():
 
     sched = sched_bench(dev) if not args.no_sched else None
     sender = sender_bench(dev) if not args.no_sched and rank == 0 else None
+    eqds = eqds_bench(dev) if not args.no_sched and rank == 0 else None
     ring = ring_bench(dev, world, rank, piece_bytes=args.piece_mb << 20) if world > 1 and not args.no_ring else None
 
     cpu = None
@@ -576,6 +639,8 @@ def main():
             line["scheduler"] = sched
         if sender:
             line["sender"] = sender
+        if eqds:
+            line["eqds"] = eqds
         if ring:
             line["allreduce"] = ring
         if cpu:

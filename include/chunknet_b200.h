@@ -99,6 +99,9 @@ typedef struct cn_pkt_hdr {
  * (transport.cpp:602-615). */
 #define CN_ACK_CUM_VALID 0x1u
 #define CN_ACK_ECN_ECHO 0x2u
+/* the record is a trimmed-header NACK (transport.cpp:657-674): hdr = the
+ * trimmed packet's header, cum_csn = nack_csn; no cum / SACK / echo */
+#define CN_ACK_NACK 0x4u
 typedef struct cn_ack_rec {
     int32_t src;          /* ack source = receiving host   */
     int32_t dst;          /* ack destination = sender host */

@@ -76,6 +76,17 @@ SCENARIOS = {
     "k8_4x1m": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,
                      loss=0.01, seed=3, chunk_bytes=32768, paths=16, lb="p2_rtt",
                      cc="cubic"), [(0, 127, MiB, 4)]),
+    # trim queue mode (NDP-style header trimming): incast of 4 senders into a
+    # 96 KiB trimming queue; trimmed headers -> NACKs (transport.cpp:657-674)
+    "trim_swift": (dict(topo="star", topo_arg=5, rate_bps=100e9, qcap_bytes=96 * 1024,
+                        loss=0.0, seed=9, chunk_bytes=16384, paths=1, lb="oblivious",
+                        cc="swift", queue="trim", trim_depth=4, window=2),
+                   [(1, 0, MiB, 2), (2, 0, MiB, 2), (3, 0, MiB, 2), (4, 0, MiB, 2)]),
+    # the same with an open window: 10,401 of 18,894 deliveries are trimmed
+    "trim_storm": (dict(topo="star", topo_arg=5, rate_bps=100e9, qcap_bytes=96 * 1024,
+                        loss=0.0, seed=9, chunk_bytes=16384, paths=1, lb="oblivious",
+                        cc="none", queue="trim", trim_depth=4, window=2),
+                   [(1, 0, MiB, 2), (2, 0, MiB, 2), (3, 0, MiB, 2), (4, 0, MiB, 2)]),
     # closed loop under Swift: the DES sender runs Swift (target 3 x base
     # RTT), so its recorded acks answer exactly what a Swift sender sends
     "closed_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,

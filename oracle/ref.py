@@ -30,7 +30,11 @@ class Scenario(ctypes.Structure):
         ("conn_split", ctypes.c_int32), ("dupack_threshold", ctypes.c_int32),
         ("rto_min", ctypes.c_int64), ("n_flows", ctypes.c_int32),
         ("window", ctypes.c_int32), ("cutoff_ns", ctypes.c_int64),
+        ("queue_mode", ctypes.c_int32), ("trim_depth", ctypes.c_int32),
     ]
+
+
+QUEUE = {"drop_tail": 0, "trim": 1, "pause": 2}
 
 
 class Flow(ctypes.Structure):
@@ -123,13 +127,13 @@ def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
            link_delay_ns=1000, qcap_bytes=1 << 20, loss=0.0, seed=1,
            chunk_bytes=32768, paths=8, lb="p2_rtt", cc="cubic", cc_scope=0,
            engines=1, conn_split=0, dupack_threshold=8, rto_min=0, flows=(),
-           window=1, cutoff_ns=60_000_000_000):
+           window=1, cutoff_ns=60_000_000_000, queue="drop_tail", trim_depth=0):
     """Runs the reference DES and writes data.bin / acks_des.bin /
     completions_des.bin into outdir.  flows: [(src, dst, len, count)]."""
     sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns,
                   qcap_bytes, loss, seed, chunk_bytes, paths, LB[lb], CC[cc],
                   cc_scope, engines, conn_split, dupack_threshold, rto_min,
-                  len(flows), window, cutoff_ns)
+                  len(flows), window, cutoff_ns, QUEUE[queue], trim_depth)
     fl = (Flow * max(1, len(flows)))(*[Flow(s, d, l, c, 0) for (s, d, l, c) in flows])
     st = RecordStats()
     os.makedirs(outdir, exist_ok=True)

@@ -114,7 +114,9 @@ cn_ack_rec ack_rec(const Packet& p, uint32_t idx, int64_t aux) {
     a.echo_path_id = p.echo_path_id;
     a.cum_csn = p.cum_csn;
     a.flags = (p.cum_valid ? CN_ACK_CUM_VALID : 0) |
-              (p.ecn_echo ? CN_ACK_ECN_ECHO : 0);
+              (p.ecn_echo ? CN_ACK_ECN_ECHO : 0) |
+              (p.kind == PacketKind::nack ? CN_ACK_NACK : 0);
+    if (p.kind == PacketKind::nack) a.cum_csn = p.nack_csn;
     a.pkt_index = idx;
     a.msg_seq = p.msg_seq;
     a.sack[0] = p.sack[0];
@@ -126,7 +128,11 @@ cn_ack_rec ack_rec(const Packet& p, uint32_t idx, int64_t aux) {
 
 Packet from_ack(const cn_ack_rec& a) {
     Packet p;
-    p.kind = PacketKind::ack;
+    p.kind = (a.flags & CN_ACK_NACK) ? PacketKind::nack : PacketKind::ack;
+    if (a.flags & CN_ACK_NACK) {
+        p.nack_csn = a.cum_csn;
+        p.nack_trim = true;
+    }
     p.src = a.src;
     p.dst = a.dst;
     p.hdr = decode_header(a.hdr);
@@ -175,6 +181,8 @@ struct cnref_scenario {
     int32_t n_flows;
     int32_t window;      // messages outstanding per flow
     int64_t cutoff_ns;
+    int32_t queue_mode;  // QueueMode: 0 drop_tail, 1 trim, 2 pause
+    int32_t trim_depth;  // NetParams::trim_queue_depth (0 = default)
 };
 
 struct cnref_flow {
@@ -211,6 +219,8 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
         np.rate_bps = sc->rate_bps;
         np.link_delay_ns = sc->link_delay_ns;
         np.qcap_bytes = sc->qcap_bytes;
+        np.mode = static_cast<QueueMode>(sc->queue_mode);
+        if (sc->trim_depth > 0) np.trim_queue_depth = sc->trim_depth;
         EventQueue eq;
         Network net(topo, np, eq, sc->seed);
         if (sc->loss > 0) net.inject_loss_at_host_egress(sc->loss);
@@ -240,7 +250,7 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
             const Packet& p = *te.pkt;
             if (p.kind == PacketKind::data)
                 data.push_back(to_rec(p));
-            else if (p.kind == PacketKind::ack)
+            else if (p.kind == PacketKind::ack || p.kind == PacketKind::nack)
                 acks.push_back(ack_rec(p, 0, te.t));
         });
 
@@ -337,7 +347,7 @@ int cnref_rx_replay(const cn_pkt_hdr* recs, uint64_t n, int n_hosts,
         uint64_t cur = 0;
         net.set_trace([&](const TraceEvent& te) {
             if (std::strcmp(te.event, "deliver") != 0) return;
-            if (te.pkt->kind != PacketKind::ack) return;
+            if (te.pkt->kind != PacketKind::ack && te.pkt->kind != PacketKind::nack) return;
             if (na < max_acks) acks[na] = ack_rec(*te.pkt, static_cast<uint32_t>(cur), 0);
             ++na;
         });
@@ -491,6 +501,8 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
         np.rate_bps = sc->rate_bps;
         np.link_delay_ns = sc->link_delay_ns;
         np.qcap_bytes = sc->qcap_bytes;
+        np.mode = static_cast<QueueMode>(sc->queue_mode);
+        if (sc->trim_depth > 0) np.trim_queue_depth = sc->trim_depth;
         EventQueue eq;
         Network net(topo, np, eq, sc->seed);
         net.inject_loss_at_host_egress(1.0);

@@ -55,10 +55,13 @@ struct RxCtl {
     unsigned long long pool_top, arena_top, pool_snap, bytes_copied;
     uint32_t n_touched, epoch, tile_ticket, fin_done, status, n_copied, n_acks, n_cpls;
     uint32_t ingest_done, scan_ticket, fin_ticket, n_scan_tiles;
+    uint32_t n_trim, pad_t;
 };
 
-enum : uint32_t { CF_INIT = 1, CF_COMPLETE = 2, CF_ECN = 4, CF_RTX = 8 };
-enum : uint8_t { PC_STALE = 1, PC_ACK = 2, PC_COPY = 4, PC_DELIVER = 8 };
+enum : uint32_t { CF_INIT = 1, CF_COMPLETE = 2, CF_ECN = 4, CF_RTX = 8, CF_NACKED = 16 };
+constexpr uint32_t CF_NACKSET = 0x100;  // c_newfl scratch: a trimmed header after the last new packet
+enum : uint8_t { PC_STALE = 1, PC_ACK = 2, PC_COPY = 4, PC_DELIVER = 8, PC_NACK = 16 };
+constexpr uint32_t kTrimMax = 16384;  // trimmed headers per batch (sorted in one block, 128 KB smem)
 constexpr uint32_t kStale = kInf;    // p_gen marker: stale before the batch
 constexpr uint32_t kErr = kInf - 1;  // p_gen marker: rejected packet
 constexpr int kAckTile = 128;        // packets per k_acks tile / block
@@ -90,6 +93,8 @@ struct RxDev {
     uint32_t* c_last;   // [pool] batch scratch: last new packet time
     uint32_t* c_newfl;  // [pool] batch scratch: ECN/RTX of new packets
     uint32_t* p_gen;    // [batch]
+    uint8_t* p_nack;    // [batch] trimmed header that emits a NACK
+    uint32_t* trim_list;  // [kTrimMax] trimmed headers of the batch (packet index)
     unsigned long long* tile_state;  // [ack tiles] decoupled look-back (ack order)
     unsigned long long* scan_state;  // [scan tiles] segmented look-back (prefix max)
     uint32_t* plan_base;             // [touched] first scan tile of each message
@@ -170,7 +175,6 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     bool ok = i < n;
     if (ok) {
         h = hdrs[i];
-        if (h.flags & CN_PKT_TRIMMED) status |= CN_RXF_UNSUPPORTED;  // trim mode: DESIGN.md §7
         if (static_cast<uint32_t>(h.src) >= (1u << 24) ||
             static_cast<uint32_t>(h.dst) >= (1u << 24) || h.msg_seq >= (1ull << 40) ||
             h.msg_seq == 0) {
@@ -330,13 +334,21 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
             const uint64_t e = cbase + c;
             const uint32_t t = i + 1;
             const uint32_t fl = d.c_flags[e];
-            if (!(fl & CF_COMPLETE) && !((d.c_seen[e] >> s) & 1u))
+            if (h.flags & CN_PKT_TRIMMED) {  // header only: chunk init, then the NACK pass (k_trim)
+                const uint32_t k = atomicAdd(&d.ctl->n_trim, 1u);
+                if (k < kTrimMax) d.trim_list[k] = i;
+                else status |= CN_RXF_CAPACITY;
+            } else if (!(fl & CF_COMPLETE) && !((d.c_seen[e] >> s) & 1u)) {
                 atomicMin(&d.c_first[e * d.ppc + s], t);
+            }
             if (!(fl & CF_INIT)) atomicMin(&d.c_init[e], t);
             touch = static_cast<uint32_t>(c) + 1;
         }
     }
-    if (i < n) d.p_gen[i] = g;
+    if (i < n) {
+        d.p_gen[i] = g;
+        d.p_nack[i] = 0;
+    }
     // chunk-vector size per message (:636-637): max over the block, one
     // global atomic per generation and block
     const uint32_t gm = __reduce_max_sync(pg, touch);  // lanes of one group share pg
@@ -715,6 +727,7 @@ __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __re
     const uint64_t off = hdrs[i].chunk_offset;
     const uint32_t s = hdrs[i].seq_in_chunk;
     const uint32_t t = i + 1;
+    if (hdrs[i].flags & CN_PKT_TRIMMED) return d.p_nack[i] ? PC_NACK : 0;  // decided by k_trim
     if (g == kStale) return PC_STALE;  // transport.cpp:602-615
     if (g == kErr) return 0;
     const GenState& G = d.gen[g];
@@ -750,6 +763,84 @@ __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __re
     return cls;
 }
 
+// -------------------------------------------------------------------- trim
+// Trimmed headers (trim queue mode; handle_data :596-674): a trimmed packet
+// of an open chunk emits a NACK unless the chunk is already `nacked` -- set
+// by a trimmed header, cleared by every new data packet (:658-660, :679).
+// Within a batch that is an order question per chunk: the header at time t
+// NACKs iff no trimmed header of its chunk arrived since the chunk's last
+// new packet before t (or, with none in the batch, the chunk was not left
+// nacked by an earlier batch).  Trimmed headers are rare, so one block sorts
+// them by (chunk, time) and decides each from its predecessor; the decision
+// feeds k_acks, which orders the NACK records into the ack stream.
+__global__ void __launch_bounds__(1024) k_trim(RxDev d, const cn_pkt_hdr* __restrict__ hdrs) {
+    extern __shared__ unsigned long long key[];  // [kTrimMax]
+    const uint32_t m0 = d.ctl->n_trim;
+    const uint32_t m = m0 < kTrimMax ? m0 : kTrimMax;
+    if (m == 0) return;
+    uint32_t P = 1;
+    while (P < m) P <<= 1;
+    for (uint32_t k = threadIdx.x; k < P; k += blockDim.x) {
+        unsigned long long v = ~0ull;
+        if (k < m) {
+            const uint32_t i = d.trim_list[k];
+            const uint32_t g = d.p_gen[i];
+            if (g < kErr)
+                v = ((d.gen[g].chunk_base + hdrs[i].chunk_offset / d.cb) << 32) | (i + 1);
+        }
+        key[k] = v;
+    }
+    __syncthreads();
+    for (uint32_t sz = 2; sz <= P; sz <<= 1)  // bitonic sort, ascending
+        for (uint32_t j = sz >> 1; j > 0; j >>= 1) {
+            for (uint32_t k = threadIdx.x; k < P; k += blockDim.x) {
+                const uint32_t l = k ^ j;
+                if (l > k) {
+                    const unsigned long long a = key[k], b = key[l];
+                    const bool up = (k & sz) == 0;
+                    if ((a > b) == up) {
+                        key[k] = b;
+                        key[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    uint32_t st = 0;
+    for (uint32_t k = threadIdx.x; k < m; k += blockDim.x) {
+        const unsigned long long v = key[k];
+        if (v == ~0ull) continue;
+        const uint64_t e = v >> 32;
+        const uint32_t t = static_cast<uint32_t>(v), i = t - 1;
+        const uint32_t prev_t = (k > 0 && (key[k - 1] >> 32) == e) ? static_cast<uint32_t>(key[k - 1]) : 0;
+        const bool last = k + 1 == m || (key[k + 1] >> 32) != e;
+        const GenState& G = d.gen[d.p_gen[i]];
+        const uint64_t c = e - G.chunk_base;
+        const uint32_t fl = d.c_flags[e];
+        // stale generation (:603), complete or behind the cursor (:629-634, :651-655): silent
+        bool silent = t > G.deliver_t || ((fl & CF_COMPLETE) ? true : d.c_cpl[e] < t);
+        // the csn must name chunk c (no aliasing), as in decide()
+        const uint32_t pm0 = pmax_ld(d, G.chunk_base, G.cum, G.n_init, c);
+        if (pm0 < t) {
+            if (pmax_ld(d, G.chunk_base, G.cum, G.n_init, c + 128) < t) st |= CN_RXF_ALIAS;
+        } else if (c >= 128 && pmax_ld(d, G.chunk_base, G.cum, G.n_init, c - 128) >= t) {
+            st |= CN_RXF_ALIAS;
+        }
+        if (!silent) {
+            uint32_t L = 0;  // the chunk's last new packet before t in this batch
+            const uint32_t exp = pkts_of(d, chunk_len_of(d, G.len, c));
+            for (uint32_t q = 0; q < exp; ++q) {
+                const uint32_t f = d.c_first[e * d.ppc + q];
+                if (f < t && f > L) L = f;
+            }
+            const bool nacked = prev_t > L || (L == 0 && prev_t == 0 && (fl & CF_NACKED));
+            if (!nacked) d.p_nack[i] = 1;
+        }
+        if (last && !(fl & CF_COMPLETE) && t > d.c_last[e]) atomicOr(&d.c_newfl[e], CF_NACKSET);
+    }
+    if (st) atomicOr(&d.ctl->status, st);
+}
+
 // -------------------------------------------------------------------- acks
 // Persistent blocks pull 128-packet tiles by ticket.  Per tile: 4 warps
 // decide (one lane per packet) and compact the tile's ack and completion
@@ -781,7 +872,7 @@ __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __re
     const cn_pkt_hdr h = hdrs[i];
     const uint32_t t = i + 1;
     const uint32_t csn = (h.hdr >> 9) & 0xFF;
-    if (cls & PC_STALE) {
+    if (cls & (PC_STALE | PC_NACK)) {  // stale re-ack (:602-615) / trimmed-header NACK (:657-674)
         if (lane == 0) {
             cn_ack_rec r;
             memset(&r, 0, sizeof r);
@@ -789,7 +880,7 @@ __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __re
             r.dst = h.src;
             r.hdr = h.hdr;
             r.cum_csn = static_cast<uint8_t>(csn);
-            r.flags = CN_ACK_CUM_VALID;
+            r.flags = (cls & PC_NACK) ? CN_ACK_NACK : CN_ACK_CUM_VALID;
             r.pkt_index = i;
             r.msg_seq = h.msg_seq;
             *out = r;
@@ -906,7 +997,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
                 const uint32_t b = ((pf & CN_PKT_ECN) ? CF_ECN : 0) | ((pf & CN_PKT_RTX) ? CF_RTX : 0);
                 if (b) atomicOr(&d.c_newfl[e], b);
             }
-            ab = __ballot_sync(0xffffffffu, cls & (PC_STALE | PC_ACK));
+            ab = __ballot_sync(0xffffffffu, cls & (PC_STALE | PC_ACK | PC_NACK));
             cb = __ballot_sync(0xffffffffu, cls & PC_DELIVER);
             s_cls[j] = cls;
             s_pm[j] = pmc;
@@ -1058,7 +1149,10 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
                     d.c_txt[e] = hdrs[lf - 1].tx_time;
                     d.c_path[e] = hdrs[lf - 1].path_id;
                 }
-                fl |= d.c_newfl[e];
+                const uint32_t nf = d.c_newfl[e];
+                fl |= nf & (CF_ECN | CF_RTX);
+                if (nf & CF_NACKSET) fl |= CF_NACKED;  // cr.nacked (:658-660, cleared at :679)
+                else if (d.c_newb[e]) fl &= ~CF_NACKED;
                 if (d.c_cpl[e] != kInf) fl |= CF_COMPLETE;
                 d.c_newb[e] = 0;
                 d.c_last[e] = 0;
@@ -1113,6 +1207,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         res->bytes_copied = C->bytes_copied;
         C->pool_snap = C->pool_top;
         C->n_touched = 0;
+        C->n_trim = 0;
         C->tile_ticket = 0;
         C->fin_done = 0;
         C->status = 0;
@@ -1225,7 +1320,7 @@ static void rx_free(cn_rx* rx) {
     RxDev& d = rx->d;
     void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen, d.touched, d.c_first, d.c_seen,
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
-                    d.c_last, d.c_newfl, d.p_gen,
+                    d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list,
                     d.tile_state, d.scan_state, d.plan_base, d.ctl, d.arena, d.post_key,
                     d.post_val, d.post_len};
     for (void* p : ptrs)
@@ -1285,6 +1380,7 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&rx->sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_trim, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTrimMax * 8));
     if (const char* e = getenv("CN_COPY_BLOCKS_PER_SM")) rx->copy_bps = atoi(e) > 0 ? atoi(e) : 64;
     if (const char* e = getenv("CN_SCAN_FIRST")) rx->scan_first = atoi(e);
     {
@@ -1319,6 +1415,8 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.c_last, cfg.chunk_pool * 4);
     ALLOC(d.c_newfl, cfg.chunk_pool * 4);
     ALLOC(d.p_gen, B * 4);
+    ALLOC(d.p_nack, B);
+    ALLOC(d.trim_list, kTrimMax * 4ull);
     ALLOC(d.tile_state, rx->max_tiles * 8ull);
     ALLOC(d.scan_state, (cfg.chunk_pool / kScanThreads + ngen + 2) * 8ull);
     ALLOC(d.plan_base, ngen * 4ull);
@@ -1445,6 +1543,7 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
             lc.numAttrs = 1;
             CNB_CUDA(cudaLaunchKernelEx(&lc, k_scan, d));
         }
+        k_trim<<<1, 1024, kTrimMax * 8, s>>>(d, d_hdrs);
         prof_mark(ev, s);
         // persistent: as many blocks as fit beside the scatter, tiles by ticket
         const uint32_t ag = tiles < static_cast<uint32_t>(rx->sms) * 4 ? tiles : rx->sms * 4;
@@ -1470,7 +1569,7 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
     }
     k_finalize<<<gb, kScanThreads, 0, s>>>(d, d_hdrs, d_result);
     prof_mark(ev, s);
-    rx->launches = n > 0 ? 5 : 1;
+    rx->launches = n > 0 ? 6 : 1;
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }

@@ -48,6 +48,7 @@ class Stats:
     """Receive-side subset of Transport::Stats (transport.hpp:62-75)."""
     msgs_completed: int = 0
     acks_sent: int = 0
+    nacks_sent: int = 0
     pkts_accepted: int = 0
     bytes_accepted: int = 0
 
@@ -177,7 +178,12 @@ class Transport:
                                      f"rx batch status flags 0x{res.status:x}")
         acks = self._acks[: res.n_acks * 64].view(res.n_acks, 64)
         cpls = self._cpls[: res.n_completions * 64].view(res.n_completions, 64)
-        self._stats.acks_sent += res.n_acks
+        n_nacks = 0
+        if res.n_acks:  # NACK records (trimmed headers) share the ack stream
+            fo = ACK_DTYPE.fields["flags"][1]
+            n_nacks = int(((acks[:, fo] & 4) != 0).sum().item())
+        self._stats.acks_sent += res.n_acks - n_nacks
+        self._stats.nacks_sent += n_nacks
         self._stats.msgs_completed += res.n_completions
         self._stats.pkts_accepted += res.n_copied
         self._stats.bytes_accepted += res.bytes_copied

@@ -124,6 +124,9 @@ def gen(name, kw, flows):
         gen_sender(name, kw, flows, acks_des, subs)
     if name in CLOSED_SWIFT:
         gen_sender(name, kw, flows, acks_des, subs, cc="swift")
+    if name in TRIM_SENDER:
+        for f in range(len(flows)):
+            gen_sender(name, kw, flows, acks_des, subs, cc=kw["cc"], flow=f)
     path = os.path.join(GOLDEN, f"{name}.npz")
     np.savez_compressed(path, data=data, acks=acks, completions=cpls,
                         meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
@@ -138,11 +141,16 @@ SENDER_SCENARIOS = ["cfg1", "cfg2_32k", "cfg2_4k", "k8_4x1m", "multigen_k8", "lo
                     "csn_wrap"]
 
 
-def gen_sender(name, kw, flows, acks_des, subs, cc="none"):
+def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
     """Sender-side golden: the reference sender (OpenLoop, or Swift with
-    global scope) fed the DES's submissions and the acks the DES delivered
-    to it, at their times."""
-    src, dst = flows[0][0], flows[0][1]
+    global scope) fed the DES's submissions and the acks (and NACKs) the DES
+    delivered to it, at their times.  flow: one connection of a multi-flow
+    scenario (its own submissions and acks; connections are independent)."""
+    src, dst = flows[flow or 0][0], flows[flow or 0][1]
+    if flow is not None:
+        acks_des = acks_des[(acks_des["dst"] == src) & (acks_des["src"] == dst)]
+        subs = subs[(subs["src"] == src) & (subs["dst"] == dst)]
+        name = f"{name}_f{flow}"
     rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes",
                               "paths", "lb") if k in kw}
     submits = [(int(s["t"]), int(s["len"]), int(s["tag"])) for s in subs]
@@ -167,6 +175,8 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none"):
 # single-connection Swift DES runs replayed into the reference sender under
 # Swift: the replay must reproduce the DES sender's own transmissions
 CLOSED_SWIFT = ["closed_k8", "closed_w4", "closed_cfg2"]
+# trim-mode incasts: every connection replayed with its acks and NACKs
+TRIM_SENDER = ["trim_swift", "trim_storm"]
 
 # Swift (device-exact CC) goldens: the same stimulus as sender_<name>.npz
 SWIFT_SCENARIOS = ["cfg1", "cfg2_32k", "k8_4x1m", "multigen_k8", "lossy_2m", "csn_wrap"]

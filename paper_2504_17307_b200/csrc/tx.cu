@@ -18,6 +18,7 @@
 //   handle_ack                       :849-942   (cause release + RTT sample,
 //                                                cumulative + SACK release,
 //                                                dup hints -> fast retransmit)
+//   handle_nack                      :944-965   (trimmed-header NACK -> rtx)
 //   cur_rto / arm_rto / rto_fire     :1078-1169 (backoff x2 capped at 64)
 //   RttEstimator                     cc.hpp:12-35
 //   OpenLoop / Swift                 cc.cpp:19-34, :108-156
@@ -643,6 +644,20 @@ __device__ void handle_ack(Tx& x, int64_t now, const cn_ack_rec& a) {
     pump(x, now);  // :941
 }
 
+// handle_nack (:944-965), selective mode: a trimmed header's NACK names a
+// chunk that never arrived -- retransmit it now.
+__device__ void handle_nack(Tx& x, int64_t now, const cn_ack_rec& a) {
+    const uint32_t mid = (a.hdr >> 17) & 0x7F;
+    const TxMsg m = load_msg(x.C, mid);
+    if (!m.live || m.seq != a.msg_seq) return;
+    const uint8_t rel = static_cast<uint8_t>(a.cum_csn - static_cast<uint8_t>(m.base & 0xFF));
+    if (rel >= kTxWindow || m.base + rel >= m.nchunks) return;
+    const uint32_t ci = m.base + rel;
+    const uint32_t fl = x.d.c_fl[m.chunk_base + ci];
+    if ((fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP))) x.queue_rtx(now, m, ci);
+    pump(x, now);
+}
+
 // rto_fire (:1094-1169), the live timer at x.timer_at
 __device__ void rto_fire(Tx& x) {
     TxConn* C = x.C;
@@ -869,7 +884,8 @@ __global__ void __launch_bounds__(kTxWarps * 32) k_tx_run(TxDev d, const uint32_
             submit(x, t, s);
         } else {
             const cn_ack_rec a = acks[idx];
-            handle_ack(x, t, a);
+            if (a.flags & CN_ACK_NACK) handle_nack(x, t, a);
+            else handle_ack(x, t, a);
         }
     }
     run_deferred(x, end_time, true);

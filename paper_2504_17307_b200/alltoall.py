@@ -1,0 +1,174 @@
+"""Variable-size all-to-all over NVLink through the transport: the MoE
+dispatch / combine of BASELINE configs[3] (SURVEY.md 8(d) cfg 4, 8(e):
+"all-to-all = N-1 peer connections per rank").
+
+Each rank holds one connection to every peer.  Per call, rank r's message
+to peer d (`send_counts[d]` bytes of its send buffer) is packetized
+(cn_packetize = Transport::send_chunk, per-chunk paths from the S3
+scheduler) and moved by a copy engine into r's staging slot in d's HBM, its
+headers alongside, followed by a system-scope release of d's ready counter
+for r (the NIC DMA + doorbell of the paper's transport).  Peer d runs the
+receive path on the landed message (ingest, scatter into the posted
+receive slot for r, SACK/cum bookkeeping, completion) and releases r's
+freed counter, after which r may reuse the slot.  Messages to different
+peers leave on two copy lanes in a staggered order (r+1, r+2, ...), so a
+hot receiver (incast) sees all its senders at once -- its NVLink ingress is
+the bottleneck, which is the point of the workload.  Counters are relative
+to a device iteration counter (cn_ctr_*), as in collective.RingAllreduce.
+"""
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .collective import DeviceBuffer, _ipc_handle, _ipc_open, _PeerView, packetize
+from .transport import MAX_PAYLOAD, Transport, TransportConfig
+
+
+class AllToAll:
+    def __init__(self, max_bytes_per_peer, *, chunk_bytes=32768, paths=8, seed=7, group=None,
+                 max_spins=1 << 26):
+        self.group = group
+        self.n = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        n, r = self.n, self.rank
+        if n < 2:
+            raise ValueError("AllToAll needs >= 2 ranks")
+        self.cap = (max_bytes_per_peer + 15) // 16 * 16
+        self.cb = chunk_bytes
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.max_spins = max_spins
+        L = _lib.lib()
+        self.max_pkts = L.cn_packet_count(self.cap, chunk_bytes, MAX_PAYLOAD)
+        # receive side: posted destination slot, staging slot and header slot per source
+        self._recv = DeviceBuffer(n * self.cap, self.dev)
+        self._stage = DeviceBuffer(n * self.cap, self.dev)
+        self._hdrs = DeviceBuffer(n * self.max_pkts * 64, self.dev)
+        self._out_hdrs = DeviceBuffer(n * self.max_pkts * 64, self.dev)  # my outgoing headers
+        # flags: ready[n] (written by sources), freed[n] (written by destinations), err, iteration
+        self._flags = DeviceBuffer((2 * n + 2) * 8, self.dev)
+        self.flags = self._flags.tensor(torch.int64, 2 * n + 2)
+        fp = self._flags.data_ptr()
+        self.f_ready, self.f_freed = fp, fp + 8 * n
+        self.f_err, self.f_it = fp + 16 * n, fp + 16 * n + 8
+        mine = {"stage": _ipc_handle(self._stage), "hdrs": _ipc_handle(self._hdrs),
+                "flags": _ipc_handle(self._flags)}
+        allh = [None] * n
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        self.peer = {}
+        for d in range(n):
+            if d == r:
+                continue
+            self.peer[d] = {k: self._open(allh[d][k]) for k in ("stage", "hdrs", "flags")}
+        # path choices: one RngStream per peer connection
+        from .scheduler import PathScheduler
+        self.sched = PathScheduler(n, paths, seed, base_rtt_ns=10000.0, index0=r * n)
+        self.max_chunks = -(-self.cap // chunk_bytes)
+        self.paths_all = torch.empty(n * self.max_chunks, dtype=torch.int32, device=self.dev)
+        self.rx = Transport(TransportConfig(chunk_bytes=chunk_bytes, paths=paths, lb="p2_rtt", carry_payload=True),
+                            device=self.dev, max_conns=2 * n, max_msgs=4 * n,
+                            chunk_pool=2 * n * self.max_chunks + 64, arena_bytes=0,
+                            max_batch=self.max_pkts + 16, max_posts=4 * n)
+        rb = self.recv_buffer()
+        for s in range(n):
+            if s != r:
+                self.rx.post(s, rb[s * self.cap:(s + 1) * self.cap])
+        self.lanes = [torch.cuda.Stream(self.dev) for _ in range(2)]
+        self.ev_init = torch.cuda.Event()
+        torch.cuda.synchronize()
+        dist.barrier(group)
+
+    def _open(self, h):
+        p = _ipc_open(h)
+        self._opened.append(p)
+        return p
+
+    def recv_buffer(self):
+        """uint8 view of the receive slots: source s's message at [s*cap, s*cap + recv_counts[s])."""
+        return self._recv.tensor()
+
+    def close(self):
+        torch.cuda.synchronize()
+        for p in self._opened:
+            _lib.lib().cn_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+        for b in (self._recv, self._stage, self._hdrs, self._out_hdrs, self._flags):
+            b.free()
+
+    def _wait(self, flag, off, s):
+        _lib.check(_lib.lib().cn_ctr_wait(flag, self.f_it, 1, off, self.max_spins, self.f_err,
+                                          ctypes.c_void_p(s.cuda_stream)), "cn_ctr_wait")
+
+    def _signal(self, flag, off, s):
+        _lib.check(_lib.lib().cn_ctr_signal(flag, self.f_it, 1, off, ctypes.c_void_p(s.cuda_stream)),
+                   "cn_ctr_signal")
+
+    def run(self, send, send_counts, recv_counts, send_offsets=None, stream=None):
+        """send: device uint8 tensor; send_counts[d] bytes for peer d starting at
+        send_offsets[d] (default: packed in peer order); recv_counts[s] bytes
+        expected from each source.  Returns the receive slots view."""
+        L = _lib.lib()
+        n, r = self.n, self.rank
+        s = stream or torch.cuda.current_stream(self.dev)
+        send_counts = [int(x) for x in send_counts]
+        recv_counts = [int(x) for x in recv_counts]
+        if send_offsets is not None:
+            send_offsets = [int(x) for x in send_offsets]
+        if send_offsets is None:
+            send_offsets, o = [], 0
+            for d in range(n):
+                send_offsets.append(o)
+                o += send_counts[d]
+        assert max(send_counts) <= self.cap and max(recv_counts) <= self.cap
+        self.rx.reset(s)
+        self.ev_init.record(s)
+        for ln in self.lanes:
+            ln.wait_event(self.ev_init)
+        # paths for every outgoing message in one launch (grouped by peer)
+        nch = [-(-send_counts[d] // self.cb) if d != r else 0 for d in range(n)]
+        offs = [0]
+        for c in nch:
+            offs.append(offs[-1] + c)
+        po = torch.tensor(offs, dtype=torch.int32).to(self.dev, non_blocking=True)
+        self.sched.select("p2_rtt", offsets=po, out=self.paths_all, stream=self.lanes[0])
+        ev_paths = torch.cuda.Event()
+        ev_paths.record(self.lanes[0])
+        self.lanes[1].wait_event(ev_paths)
+        sb = send.data_ptr()
+        for k in range(1, n):  # staggered: r+1, r+2, ...
+            d = (r + k) % n
+            sp = self.lanes[k % 2]
+            pe = self.peer[d]
+            self._wait(self.f_freed + 8 * d, 0, sp)  # d consumed my last message
+            if send_counts[d]:
+                npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
+                oh = _PeerView(self._out_hdrs.data_ptr() + d * self.max_pkts * 64, npk * 64)
+                packetize(send_counts[d], self.cb, src=r, dst=d, conn_id=0, msg_id=1, msg_seq=1, tag=r,
+                          chunk_paths=self.paths_all[offs[d]:offs[d + 1]], out=oh, stream=sp, device=self.dev)
+                _lib.check(L.cn_copy_async(pe["stage"] + r * self.cap, sb + send_offsets[d], send_counts[d],
+                                           ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
+                _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh.data_ptr(), npk * 64,
+                                           ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
+            self._signal(pe["flags"] + 8 * r, 1, sp)  # d's ready[r]
+        for k in range(1, n):  # receive in the mirrored order: r-1, r-2, ...
+            src = (r - k) % n
+            self._wait(self.f_ready + 8 * src, 1, s)
+            if recv_counts[src]:
+                npk = L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD)
+                hd = _PeerView(self._hdrs.data_ptr() + src * self.max_pkts * 64, npk * 64)
+                pl = _PeerView(self._stage.data_ptr() + src * self.cap, recv_counts[src])
+                self.rx.rx_batch_async(hd, pl, 0, s, n=npk)
+            self._signal(self.peer[src]["flags"] + 8 * n + 8 * r, 1, s)  # src's freed[r]
+        for ln in self.lanes:
+            s.wait_stream(ln)
+        _lib.check(L.cn_ctr_advance(self.f_it, ctypes.c_void_p(s.cuda_stream)), "cn_ctr_advance")
+        return self.recv_buffer()
+
+    def check(self):
+        if int(self.flags[2 * self.n].item()) != 0:
+            raise _lib.ChunknetError(-5, "all-to-all flag wait timed out")
+        res = _lib.RxResult.from_buffer_copy(bytes(self.rx._result.cpu().numpy()))
+        if res.status:
+            raise _lib.ChunknetError(-6, f"all-to-all receive status 0x{res.status:x}")

@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sched", action="store_true")
     ap.add_argument("--no-ring", action="store_true")
-    ap.add_argument("--piece-mb", type=int, default=32, help="ring pipeline piece size (MiB)")
+    ap.add_argument("--piece-mb", type=int, default=64, help="ring pipeline piece size (MiB)")
+    ap.add_argument("--no-moe", action="store_true", help="skip the MoE all-to-all (configs[3]) at N > 1")
     return ap.parse_args()
 
 
@@ -336,6 +337,117 @@ def eqds_bench(dev, receivers=4096, senders=32, events=1000, reps=3, cpu_receive
     return out
 
 
+def moe_routing(world, tokens, topk=8, experts_per_rank=32, hot=0, skew=10.0):
+    """DeepSeek-V3-shaped routing for every rank (deterministic): each token
+    picks `topk` distinct experts (Gumbel top-k), experts on rank `hot`
+    weighted so that rank receives ~skew x the average per-rank load.
+    Returns per source rank: (token index order grouped by destination rank,
+    rows sent to each destination)."""
+    E = world * experts_per_rank
+    w = np.ones(E)
+    others = world - 1
+    # share(hot) / share(other) = skew  ->  per-expert weight ratio = skew
+    w[hot * experts_per_rank:(hot + 1) * experts_per_rank] = skew
+    out = []
+    for s in range(world):
+        rs = np.random.RandomState(1000 + s)
+        g = np.log(w)[None, :] - np.log(-np.log(rs.rand(tokens, E)))
+        top = np.argpartition(-g, topk - 1, axis=1)[:, :topk]       # [tokens, topk] experts
+        dest = top // experts_per_rank
+        order = np.argsort(dest.reshape(-1), kind="stable")          # copies grouped by destination
+        tok = np.repeat(np.arange(tokens), topk)[order]
+        rows = np.bincount(dest.reshape(-1), minlength=world)
+        out.append((tok, rows))
+    del others
+    return out
+
+
+def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
+    """BASELINE configs[3]: 8-rank MoE all-to-all (DeepSeek-V3 shape: hidden
+    7168 bf16 = 14,336 B per token copy, top-8 of 32 experts per rank) with
+    incast -- rank 0's experts draw 10x the average load.  One step =
+    dispatch (token copies to their experts' ranks) + combine (expert outputs
+    back), through the transport all-to-all; NCCL all_to_all_single with the
+    same splits beside it.  Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_17307_b200.alltoall import AllToAll
+    row = hidden * 2
+    routing = moe_routing(world, tokens)
+    rows = np.stack([r_[1] for r_ in routing])                     # [src, dst] rows
+    rows_self = rows.copy()
+    np.fill_diagonal(rows, 0)                                      # local experts need no transfer
+    tok, _ = routing[rank]
+    g = torch.Generator(device=dev)
+    g.manual_seed(rank)
+    x = torch.randn(tokens, hidden, device=dev, generator=g).to(torch.bfloat16)
+    idx = torch.from_numpy(tok).to(dev)
+    send = x.index_select(0, idx).view(torch.uint8).reshape(-1)    # dispatch payload, grouped by dest
+    offs = np.concatenate([[0], np.cumsum(rows_self[rank])[:-1]]) * row
+    sc, rc = rows[rank] * row, rows[:, rank] * row
+    cap = int(max(rows.max() * row, 16))
+    a2a = AllToAll(cap)   # dispatch
+    a2c = AllToAll(cap)   # combine (its own slots: the dispatch slots are its send buffer)
+    coffs = [s_ * a2a.cap for s_ in range(world)]
+
+    def step():
+        recv = a2a.run(send, sc, rc, send_offsets=offs)
+        # combine: expert outputs (here: the received rows) return to their owners
+        a2c.run(recv, rc, sc, send_offsets=coffs)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    h0 = time.perf_counter()
+    for _ in range(iters):
+        step()
+    host_ms = (time.perf_counter() - h0) * 1e3 / iters
+    e1.record()
+    torch.cuda.synchronize()
+    a2a.check()
+    a2c.check()
+    t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # NCCL all_to_all_single with the same splits (local rows excluded on both sides)
+    inp = torch.empty(int(sc.sum()), dtype=torch.uint8, device=dev)
+    out = torch.empty(int(rc.sum()), dtype=torch.uint8, device=dev)
+    sl, rl = [int(v) for v in sc], [int(v) for v in rc]
+
+    def nstep():
+        dist.all_to_all_single(out, inp, rl, sl)
+        dist.all_to_all_single(inp, out, sl, rl)
+
+    for _ in range(warmup):
+        nstep()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for _ in range(iters):
+        nstep()
+    e1.record()
+    torch.cuda.synchronize()
+    tn = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
+    dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+    msn = float(tn.item())
+    a2a.close()
+    a2c.close()
+    moved = int(rows.sum()) * row * 2  # dispatch + combine, all ranks
+    hot_in = int(rows[:, 0].sum()) * row
+    return {"config": f"{world} ranks x {tokens} tokens, hidden {hidden} bf16 ({row} B/copy), top-8 of "
+                      f"{32 * world} experts, rank 0 experts 10x weight (incast)",
+            "ms_per_step": round(ms, 4), "nccl_ms_per_step": round(msn, 4),
+            "host_enqueue_ms_per_step": round(host_ms, 4),
+            "bytes_per_step_all_ranks": moved, "hot_rank_ingress_bytes": hot_in,
+            "hot_rank_ingress_GBps": round(hot_in / (ms / 2 * 1e-3) / 1e9, 1),
+            "algbw_GBps_all_ranks": round(moved / (ms * 1e-3) / 1e9, 1),
+            "nccl_algbw_GBps_all_ranks": round(moved / (msn * 1e-3) / 1e9, 1)}
+
+
 def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30, piece_bytes=32 << 20):
     """BASELINE configs[2]: ring all-reduce of 1 GiB per rank (fp32 and bf16)
     through the transport (packetize -> NVLink zero-copy fused-reduce receive
@@ -603,6 +715,7 @@ def main():
     sender = sender_bench(dev) if not args.no_sched and rank == 0 else None
     eqds = eqds_bench(dev) if not args.no_sched and rank == 0 else None
     ring = ring_bench(dev, world, rank, piece_bytes=args.piece_mb << 20) if world > 1 and not args.no_ring else None
+    moe = moe_bench(dev, world, rank) if world > 1 and not args.no_moe else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -643,6 +756,8 @@ def main():
             line["eqds"] = eqds
         if ring:
             line["allreduce"] = ring
+        if moe:
+            line["moe_alltoall"] = moe
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

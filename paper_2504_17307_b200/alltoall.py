@@ -13,8 +13,9 @@ receive slot for r, SACK/cum bookkeeping, completion) and releases r's
 freed counter, after which r may reuse the slot.  Messages to different
 peers leave on two copy lanes in a staggered order (r+1, r+2, ...), so a
 hot receiver (incast) sees all its senders at once -- its NVLink ingress is
-the bottleneck, which is the point of the workload.  Counters are relative
-to a device iteration counter (cn_ctr_*), as in collective.RingAllreduce.
+the bottleneck, which is the point of the workload.  Messages move in
+chunk-aligned pieces, each releasing a per-pair monotone counter, so the
+receive path runs on early pieces while later ones are still in flight.
 """
 import ctypes
 
@@ -28,7 +29,7 @@ from .transport import MAX_PAYLOAD, Transport, TransportConfig
 
 class AllToAll:
     def __init__(self, max_bytes_per_peer, *, chunk_bytes=32768, paths=8, seed=7, group=None,
-                 max_spins=1 << 26):
+                 piece_bytes=64 << 20, max_spins=1 << 26):
         self.group = group
         self.n = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -46,12 +47,13 @@ class AllToAll:
         self._stage = DeviceBuffer(n * self.cap, self.dev)
         self._hdrs = DeviceBuffer(n * self.max_pkts * 64, self.dev)
         self._out_hdrs = DeviceBuffer(n * self.max_pkts * 64, self.dev)  # my outgoing headers
-        # flags: ready[n] (written by sources), freed[n] (written by destinations), err, iteration
-        self._flags = DeviceBuffer((2 * n + 2) * 8, self.dev)
-        self.flags = self._flags.tensor(torch.int64, 2 * n + 2)
+        # flags: ready[n][2] (written by sources, per copy lane), freed[n][2]
+        # (written by destinations), err
+        self._flags = DeviceBuffer((4 * n + 2) * 8, self.dev)
+        self.flags = self._flags.tensor(torch.int64, 4 * n + 2)
         fp = self._flags.data_ptr()
-        self.f_ready, self.f_freed = fp, fp + 8 * n
-        self.f_err, self.f_it = fp + 16 * n, fp + 16 * n + 8
+        self.f_ready, self.f_freed = fp, fp + 16 * n
+        self.f_err = fp + 32 * n
         mine = {"stage": _ipc_handle(self._stage), "hdrs": _ipc_handle(self._hdrs),
                 "flags": _ipc_handle(self._flags)}
         allh = [None] * n
@@ -76,6 +78,9 @@ class AllToAll:
             if s != r:
                 self.rx.post(s, rb[s * self.cap:(s + 1) * self.cap])
         self.lanes = [torch.cuda.Stream(self.dev) for _ in range(2)]
+        self.piece_bytes = max(chunk_bytes, piece_bytes // chunk_bytes * chunk_bytes)
+        self.sent = [[0, 0] for _ in range(n)]   # pieces sent to each peer, per lane
+        self.recvd = [[0, 0] for _ in range(n)]  # pieces consumed from each peer, per lane
         self.ev_init = torch.cuda.Event()
         torch.cuda.synchronize()
         dist.barrier(group)
@@ -105,10 +110,22 @@ class AllToAll:
         _lib.check(_lib.lib().cn_ctr_signal(flag, self.f_it, 1, off, ctypes.c_void_p(s.cuda_stream)),
                    "cn_ctr_signal")
 
+    def _pieces(self, cnt):
+        """Chunk-aligned piece bounds of a cnt-byte message."""
+        if cnt == 0:
+            return []
+        P = max(1, min(-(-cnt // self.piece_bytes), -(-cnt // self.cb)))
+        b = [0] + [cnt * p // P // self.cb * self.cb for p in range(1, P)] + [cnt]
+        return [(b[p], b[p + 1]) for p in range(P) if b[p + 1] > b[p]]
+
     def run(self, send, send_counts, recv_counts, send_offsets=None, stream=None):
         """send: device uint8 tensor; send_counts[d] bytes for peer d starting at
         send_offsets[d] (default: packed in peer order); recv_counts[s] bytes
-        expected from each source.  Returns the receive slots view."""
+        expected from each source.  Returns the receive slots view.
+
+        Messages travel in chunk-aligned pieces (piece_bytes): the receiver
+        runs the receive path on each piece as it lands, interleaved across
+        sources, so a hot receiver's processing overlaps its ingress."""
         L = _lib.lib()
         n, r = self.n, self.rank
         s = stream or torch.cuda.current_stream(self.dev)
@@ -122,6 +139,7 @@ class AllToAll:
                 send_offsets.append(o)
                 o += send_counts[d]
         assert max(send_counts) <= self.cap and max(recv_counts) <= self.cap
+        ppc = -(-self.cb // MAX_PAYLOAD)
         self.rx.reset(s)
         self.ev_init.record(s)
         for ln in self.lanes:
@@ -137,37 +155,66 @@ class AllToAll:
         ev_paths.record(self.lanes[0])
         self.lanes[1].wait_event(ev_paths)
         sb = send.data_ptr()
+        cs = lambda st: ctypes.c_void_p(st.cuda_stream)  # noqa: E731
         for k in range(1, n):  # staggered: r+1, r+2, ...
             d = (r + k) % n
-            sp = self.lanes[k % 2]
+            if not send_counts[d]:
+                continue
             pe = self.peer[d]
-            self._wait(self.f_freed + 8 * d, 0, sp)  # d consumed my last message
-            if send_counts[d]:
-                npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
-                oh = _PeerView(self._out_hdrs.data_ptr() + d * self.max_pkts * 64, npk * 64)
-                packetize(send_counts[d], self.cb, src=r, dst=d, conn_id=0, msg_id=1, msg_seq=1, tag=r,
-                          chunk_paths=self.paths_all[offs[d]:offs[d + 1]], out=oh, stream=sp, device=self.dev)
-                _lib.check(L.cn_copy_async(pe["stage"] + r * self.cap, sb + send_offsets[d], send_counts[d],
-                                           ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
-                _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh.data_ptr(), npk * 64,
-                                           ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
-            self._signal(pe["flags"] + 8 * r, 1, sp)  # d's ready[r]
-        for k in range(1, n):  # receive in the mirrored order: r-1, r-2, ...
+            # d consumed every piece of my previous message (slot and header reuse)
+            for ln in range(2):
+                _lib.check(L.cn_flag_wait(self.f_freed + 16 * d + 8 * ln, None, self.sent[d][ln], self.max_spins,
+                                          self.f_err, cs(self.lanes[ln])), "cn_flag_wait")
+            sp0 = self.lanes[k % 2]
+            npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
+            oh = _PeerView(self._out_hdrs.data_ptr() + d * self.max_pkts * 64, npk * 64)
+            packetize(send_counts[d], self.cb, src=r, dst=d, conn_id=0, msg_id=1, msg_seq=1, tag=r,
+                      chunk_paths=self.paths_all[offs[d]:offs[d + 1]], out=oh, stream=sp0, device=self.dev)
+            ev_h = torch.cuda.Event()
+            ev_h.record(sp0)
+            self.lanes[(k + 1) % 2].wait_event(ev_h)
+            for p, (lo, hi) in enumerate(self._pieces(send_counts[d])):
+                ln = (k + p) % 2  # consecutive pieces alternate copy lanes
+                sp = self.lanes[ln]
+                _lib.check(L.cn_copy_async(pe["stage"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
+                                           cs(sp)), "cn_copy_async")
+                if p == 0:  # the message's headers ride with its first piece
+                    _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh.data_ptr(), npk * 64,
+                                               cs(sp)), "cn_copy_async")
+                self.sent[d][ln] += 1
+                _lib.check(L.cn_flag_signal(pe["flags"] + 16 * r + 8 * ln, None, self.sent[d][ln], cs(sp)),
+                           "cn_flag_signal")
+        # receive: pieces as they land, interleaved over the sources (r-1, r-2, ...)
+        plan = {}
+        for k in range(1, n):
             src = (r - k) % n
-            self._wait(self.f_ready + 8 * src, 1, s)
             if recv_counts[src]:
-                npk = L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD)
-                hd = _PeerView(self._hdrs.data_ptr() + src * self.max_pkts * 64, npk * 64)
+                plan[src] = (k, self._pieces(recv_counts[src]))
+        for p in range(max([len(v[1]) for v in plan.values()] or [0])):
+            for k in range(1, n):
+                src = (r - k) % n
+                if src not in plan or p >= len(plan[src][1]):
+                    continue
+                ks = (r - src) % n  # the sender's stagger index for me -> its lane choice
+                ln = (ks + p) % 2
+                lo, hi = plan[src][1][p]
+                self.recvd[src][ln] += 1
+                _lib.check(L.cn_flag_wait(self.f_ready + 16 * src + 8 * ln, None, self.recvd[src][ln],
+                                          self.max_spins, self.f_err, cs(s)), "cn_flag_wait")
+                a = lo // self.cb * ppc
+                b = (L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD) if hi == recv_counts[src]
+                     else hi // self.cb * ppc)
+                hd = _PeerView(self._hdrs.data_ptr() + src * self.max_pkts * 64 + a * 64, (b - a) * 64)
                 pl = _PeerView(self._stage.data_ptr() + src * self.cap, recv_counts[src])
-                self.rx.rx_batch_async(hd, pl, 0, s, n=npk)
-            self._signal(self.peer[src]["flags"] + 8 * n + 8 * r, 1, s)  # src's freed[r]
+                self.rx.rx_batch_async(hd, pl, 0, s, n=b - a)
+                _lib.check(L.cn_flag_signal(self.peer[src]["flags"] + 16 * n + 16 * r + 8 * ln, None,
+                                            self.recvd[src][ln], cs(s)), "cn_flag_signal")  # src's freed[r][ln]
         for ln in self.lanes:
             s.wait_stream(ln)
-        _lib.check(L.cn_ctr_advance(self.f_it, ctypes.c_void_p(s.cuda_stream)), "cn_ctr_advance")
         return self.recv_buffer()
 
     def check(self):
-        if int(self.flags[2 * self.n].item()) != 0:
+        if int(self.flags[4 * self.n].item()) != 0:
             raise _lib.ChunknetError(-5, "all-to-all flag wait timed out")
         res = _lib.RxResult.from_buffer_copy(bytes(self.rx._result.cpu().numpy()))
         if res.status:

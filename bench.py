@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-ring", action="store_true")
     ap.add_argument("--piece-mb", type=int, default=64, help="ring pipeline piece size (MiB)")
     ap.add_argument("--no-moe", action="store_true", help="skip the MoE all-to-all (configs[3]) at N > 1")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] receive sweep")
     return ap.parse_args()
 
 
@@ -334,6 +335,116 @@ def eqds_bench(dev, receivers=4096, senders=32, events=1000, reps=3, cpu_receive
             out["cpu_sample"] = f"{cpu_receivers} of the receivers' streams"
     except Exception as e:  # noqa: BLE001
         out["cpu_reference_error"] = str(e)
+    return out
+
+
+def synth_trace(conns, size, chunk_bytes=32768, paths=256, seed=0, window=64, dev="cuda", conn_base=0):
+    """configs[4] traffic into one receiver: `conns` connections (sources
+    conn_base+1.., conn id = index & 0xFF), one `size`-byte message each,
+    chunked and packetized as Transport::send_chunk does (DefaultPolicy),
+    per-chunk paths from the S3 scheduler (P2-RTT over `paths` paths, one
+    RngStream per connection), packets of all connections interleaved
+    round-robin and reordered within a `window`-packet sliding window (the
+    multipath spray).  Returns cn_pkt_hdr records (numpy PKT_DTYPE)."""
+    import torch
+
+    import paper_2504_17307_b200 as cn
+    from paper_2504_17307_b200.records import PKT_DTYPE
+    nch = -(-size // chunk_bytes)
+    ppc = -(-chunk_bytes // MAX_PL)
+    last = size - (nch - 1) * chunk_bytes
+    lp = -(-last // MAX_PL)
+    per = (nch - 1) * ppc + lp
+    sch = cn.PathScheduler(conns, paths, seed + 1, base_rtt_ns=10000.0, device=dev)
+    pth = sch.select("p2_rtt", nch).cpu().numpy()                      # [conns, nch]
+    k = np.arange(per)
+    c = np.minimum(k // ppc, nch - 1)
+    sq = k - c * ppc
+    clen = np.where(c == nch - 1, last, chunk_bytes)
+    pl = np.minimum(MAX_PL, clen - sq * MAX_PL)
+    rec = np.zeros((conns, per), dtype=PKT_DTYPE)
+    j = np.arange(conns)[:, None]
+    rec["src"] = conn_base + 1 + j
+    rec["dst"] = 0
+    rec["path_id"] = pth[:, c]
+    hdr = ((j & 0xFF) << 24) | (0 << 17) | ((c & 0xFF) << 9) | ((c == nch - 1) << 8)
+    rec["hdr"] = hdr.astype(np.uint32)
+    rec["chunk_offset"] = (c * chunk_bytes)[None, :]
+    rec["chunk_len"] = clen[None, :]
+    rec["payload_len"] = pl[None, :]
+    rec["seq_in_chunk"] = sq[None, :]
+    rec["tx_time"] = k[None, :] * 10
+    rec["msg_seq"] = 1
+    rec["msg_tag"] = conn_base + j
+    rec["msg_len"] = size
+    out = rec.T.reshape(-1)                                            # round-robin over connections
+    if window > 1 and len(out) > window:
+        rs = np.random.RandomState(seed)
+        key = np.arange(len(out)) + rs.randint(0, window, len(out))
+        out = out[np.argsort(key, kind="stable")]
+    return out
+
+
+def sweep_bench(dev, world, rank, sizes=(4 << 10, 64 << 10, 1 << 20, 16 << 20, 256 << 20, 1 << 30),
+                total_conns=1024, cap_bytes=2 << 30, steps=10, warmup=3):
+    """BASELINE configs[4]: flow-collision sweep -- 1k connections x 256
+    paths into the receive path, message sizes 4 KiB..1 GiB (connections per
+    size capped so that <= 2 GiB of messages are in flight per GPU); the
+    connections shard over the ranks.  Per size: one batch
+    = every packet of every connection (reset + receive path, CUDA graph),
+    time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_17307_b200 as cn
+    out = []
+    for size in sizes:
+        conns = max(1, min(total_conns // world, cap_bytes // size))
+        data = synth_trace(conns, size, seed=size % 9973 + rank, conn_base=rank * conns, dev=dev)
+        n = len(data)
+        hdrs = cn.to_device_records(data, dev)
+        st = torch.randint(0, 256, (n * MAX_PL,), dtype=torch.uint8, device=dev)
+        nchk = conns * (-(-size // 32768))
+        tr = cn.Transport(cn.TransportConfig(chunk_bytes=32768, carry_payload=True), device=dev,
+                          arena_bytes=conns * (size + 64) + (1 << 20), chunk_pool=2 * nchk + 64,
+                          max_batch=n, max_conns=2 * conns + 16, max_msgs=2 * conns + 16)
+
+        def step():
+            s_ = torch.cuda.current_stream(dev)
+            tr.reset(s_)
+            tr.rx_batch_async(hdrs, st, MAX_PL, s_)
+
+        step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        for _ in range(warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        res = torch.empty(24, dtype=torch.uint8).copy_(tr._result)
+        r = cn.lib  # noqa: F841
+        from paper_2504_17307_b200 import _lib as L_
+        rr = L_.RxResult.from_buffer_copy(bytes(res.numpy()))
+        assert rr.status == 0 and rr.n_completions == conns, (size, rr.status, rr.n_completions)
+        out.append({"msg_bytes": size, "connections": conns * world, "packets": n * world,
+                    "ms_per_batch": round(ms, 4),
+                    "GBps": round(world * conns * size / (ms * 1e-3) / 1e9, 1),
+                    "Mpkts_per_s": round(world * n / (ms * 1e-3) / 1e6, 1)})
+        del tr, g, hdrs, st
+        torch.cuda.empty_cache()
     return out
 
 
@@ -716,6 +827,7 @@ def main():
     eqds = eqds_bench(dev) if not args.no_sched and rank == 0 else None
     ring = ring_bench(dev, world, rank, piece_bytes=args.piece_mb << 20) if world > 1 and not args.no_ring else None
     moe = moe_bench(dev, world, rank) if world > 1 and not args.no_moe else None
+    sweep = sweep_bench(dev, world, rank) if not args.no_sweep else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -758,6 +870,8 @@ def main():
             line["allreduce"] = ring
         if moe:
             line["moe_alltoall"] = moe
+        if sweep:
+            line["sweep_cfg5"] = sweep
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

@@ -329,6 +329,10 @@ int cn_tx_run(cn_tx* t, const uint32_t* d_ev_off, const uint64_t* d_events,
               const cn_tx_submit* d_submits, const cn_ack_rec* d_acks, int64_t end_time,
               cn_tx_rec* d_log, cn_tx_stats* d_stats, void* stream);
 int cn_tx_status(cn_tx* t, unsigned int* out);
+/* Transmit records logged per connection so far (host array of n_conns);
+ * cn_tx_log_clear restarts every connection's log at 0. */
+int cn_tx_log_counts(cn_tx* t, uint32_t* h_out);
+int cn_tx_log_clear(cn_tx* t, void* stream);
 
 /* --------------------------------------------------------- send side
  * Transport::send_chunk's packetization (transport.cpp:433-494) for all
@@ -385,6 +389,69 @@ int cn_copy_async(void* d_dst, const void* d_src, uint64_t bytes, void* stream);
 /* The same transfer driven by SM threads (16-byte aligned pointers and size;
  * blocks = 0 picks one per SM): posted NVLink writes beside the copy engines. */
 int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, void* stream);
+
+/* -------------------------------------------------------- transport
+ * One object in the shape of chunknet::Transport (transport.hpp:53-107):
+ * the sender engine (cn_tx) for every connection it opens plus the receive
+ * path (cn_rx), driven by the caller's clock.  The reference's synchronous
+ * calls become queued events: send_message / handle_acks queue at their
+ * time, cn_transport_advance runs the device sender up to a time, and the
+ * transmissions, acks and completions are polled.  Supported: one engine
+ * per host, selective reliability, DefaultPolicy, CC none or Swift (global
+ * scope), sender-driven; other settings are rejected with CN_E_UNSUPPORTED. */
+typedef struct cn_transport_config {
+    /* TransportConfig (transport.hpp:23-51) */
+    int32_t engines, conn_split, paths;
+    uint32_t chunk_bytes;
+    int32_t lb, reliability, receiver_driven, max_inflight_msgs;
+    int64_t rto_min, rto_max;            /* resolved (0 rto_max = 64 x rto_min) */
+    uint32_t drr_quantum;
+    int32_t rtx_avoid_prev_path, dupack_threshold, carry_payload;
+    int64_t initial_credit;
+    uint32_t credit_quantum;
+    int32_t credit_bank_quanta;
+    /* CcConfig (cc.hpp:37-51) */
+    int32_t cc_algo, cc_scope;
+    int64_t mss, cap_bytes;
+    int32_t ecn_as_loss, pad0;
+    int64_t swift_target_ns;
+    double init_cwnd_pkts;
+    /* what the reference reads from its Network */
+    double base_rtt_ns;                  /* scoreboard prior */
+    int64_t commit_ahead;                /* max(2 chunk, 2 quantum, BDP) (transport.cpp:37-39) */
+    /* device capacities */
+    uint32_t max_conns, max_batch, log_cap, pad1;
+    uint64_t chunk_pool, arena_bytes;
+} cn_transport_config;
+typedef struct cn_stats {  /* Transport::Stats (transport.hpp:62-75) */
+    uint64_t msgs_sent, msgs_completed, backpressured, chunks_sent, chunk_rtx, fast_rtx, rtos,
+        acks_sent, nacks_sent, rts_sent, credit_pkts, delivered_msgs;
+} cn_stats;
+typedef struct cn_transport cn_transport;
+void cn_transport_config_default(cn_transport_config* cfg);
+int cn_transport_create(const cn_transport_config* cfg, uint64_t seed, cn_transport** out);
+void cn_transport_destroy(cn_transport* h);
+/* Transport::send_message (transport.hpp:88) at time t: opens the (src,
+ * dst) connection on first use (conn_to order = RngStream index); returns 1
+ * when queued (backpressure is counted in the stats when the engine runs). */
+int cn_transport_send_message(cn_transport* h, int32_t src, int32_t dst, uint64_t len, uint64_t tag, int64_t t);
+/* acks and trimmed-header NACKs delivered at the senders (host records, aux = time) */
+int cn_transport_handle_acks(cn_transport* h, const cn_ack_rec* acks, uint32_t n);
+/* run the sender engine over everything queued, timers up to `until` */
+int cn_transport_advance(cn_transport* h, int64_t until, void* stream);
+/* transmissions since the last poll, per connection in emission order;
+ * conn_out[i] = connection index of out[i] (optional) */
+int64_t cn_transport_poll_transmissions(cn_transport* h, cn_tx_rec* out, uint64_t cap, int32_t* conn_out);
+/* Transport::handle_packet for a batch of delivered data packets (device records) */
+int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const void* d_payload, uint64_t stride,
+                             uint32_t n, void* stream);
+/* the last batch's ack / NACK records and completions (host copies) */
+int64_t cn_transport_poll_acks(cn_transport* h, cn_ack_rec* out, uint64_t cap);
+int64_t cn_transport_poll_completions(cn_transport* h, cn_completion* out, uint64_t cap);
+int cn_transport_stats(cn_transport* h, cn_stats* out);
+int32_t cn_transport_conn_index(cn_transport* h, int32_t src, int32_t dst);
+/* outstanding_bytes (transport.hpp:102): the connection's gated inflight */
+int64_t cn_transport_outstanding_bytes(cn_transport* h, int32_t src, int32_t dst);
 
 /* ------------------------------------------------------------- EQDS
  * The receiver-driven pull pacer (EqdsReceiver, eqds.cpp:7-104), one per

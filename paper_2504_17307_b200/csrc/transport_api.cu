@@ -1,0 +1,367 @@
+// transport_api.cu -- the drop-in boundary in the shape of chunknet::Transport
+// (/root/reference/proj/include/chunknet/transport.hpp:53-107).
+//
+// Host C++ around the device engines: the sender engine (tx.cu, every
+// connection the object opens) and the receive path (rx.cu).  The
+// reference's Transport is driven by its discrete-event loop -- every call
+// acts at eq.now().  Here the caller's clock is explicit: send_message and
+// the acks delivered at the senders are queued with their times,
+// cn_transport_advance runs the device sender over the queue (timers up to
+// a horizon), and the transmissions, ack/NACK records and completions are
+// polled.  Connections open on first use in conn_to order (transport.cpp:
+// 84-137), which fixes each one's RngStream index.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+using cnb::set_error;
+
+namespace {
+
+struct Ev {
+    int64_t t;
+    uint32_t type;  // 0 submit, 1 ack / NACK (events at one instant: submits first)
+    uint32_t idx;
+};
+
+template <class T>
+bool grow(T** p, uint64_t* cap, uint64_t need) {
+    if (need <= *cap) return true;
+    uint64_t c = std::max<uint64_t>(need, *cap * 2 + 64);
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (cudaMalloc(p, c * sizeof(T)) != cudaSuccess) {
+        *cap = 0;
+        return false;
+    }
+    *cap = c;
+    return true;
+}
+
+}  // namespace
+
+struct cn_transport {
+    cn_transport_config c{};
+    cn_rx* rx = nullptr;
+    cn_tx* tx = nullptr;
+    std::map<std::pair<int32_t, int32_t>, int32_t> conn_idx;
+    std::vector<std::vector<Ev>> pend;
+    std::vector<cn_tx_submit> subs;
+    std::vector<cn_ack_rec> acks;
+    cn_tx_rec* d_log = nullptr;
+    cn_tx_stats* d_stats = nullptr;
+    uint32_t* d_evoff = nullptr;
+    uint64_t* d_ev = nullptr;
+    cn_tx_submit* d_subs = nullptr;
+    cn_ack_rec* d_ain = nullptr;
+    uint64_t cap_ev = 0, cap_subs = 0, cap_ain = 0;
+    cn_ack_rec* d_aout = nullptr;
+    cn_completion* d_cpls = nullptr;
+    cn_rx_result* d_res = nullptr;
+    std::vector<cn_ack_rec> last_acks;
+    std::vector<cn_completion> last_cpls;
+    std::vector<cn_tx_stats> txs;
+    uint64_t acks_sent = 0, nacks_sent = 0, delivered = 0;
+};
+
+extern "C" void cn_transport_config_default(cn_transport_config* c) {
+    memset(c, 0, sizeof *c);
+    c->engines = 1;      // TransportConfig defaults (transport.hpp:23-51)
+    c->paths = 1;
+    c->chunk_bytes = 32768;
+    c->lb = CN_LB_OBLIVIOUS;
+    c->max_inflight_msgs = 128;
+    c->drr_quantum = 32768;
+    c->rtx_avoid_prev_path = 1;
+    c->dupack_threshold = 8;
+    c->initial_credit = -1;
+    c->credit_quantum = 32768;
+    c->credit_bank_quanta = 4;
+    c->cc_algo = CN_CC_NONE;  // CcConfig defaults (cc.hpp:37-51)
+    c->mss = 4032;
+    c->init_cwnd_pkts = 2.0;
+    c->base_rtt_ns = 10000.0;
+    c->max_conns = 64;
+    c->max_batch = 1 << 16;
+    c->log_cap = 1 << 16;
+    c->chunk_pool = 1 << 20;
+    c->arena_bytes = 64ull << 20;
+}
+
+extern "C" void cn_transport_destroy(cn_transport* h) {
+    if (!h) return;
+    cudaDeviceSynchronize();
+    if (h->tx) cn_tx_destroy(h->tx);
+    if (h->rx) cn_rx_destroy(h->rx);
+    void* p[] = {h->d_log, h->d_stats, h->d_evoff, h->d_ev, h->d_subs, h->d_ain, h->d_aout, h->d_cpls, h->d_res};
+    for (void* x : p)
+        if (x) cudaFree(x);
+    delete h;
+}
+
+extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed, cn_transport** out) {
+    if (!cfg || !out || !cfg->max_conns || !cfg->chunk_bytes || cfg->paths < 1 || cfg->rto_min <= 0) {
+        set_error("cn_transport_create: bad config (paths >= 1, resolved rto_min > 0, max_conns > 0)");
+        return CN_E_INVALID;
+    }
+    if (cfg->engines != 1 || cfg->conn_split || cfg->reliability != 0 || cfg->receiver_driven ||
+        (cfg->cc_algo != CN_CC_NONE && cfg->cc_algo != CN_CC_SWIFT) || cfg->cc_scope != 0) {
+        set_error("cn_transport_create: supported: 1 engine, selective reliability, sender-driven, "
+                  "CC none/swift with global scope");
+        return CN_E_UNSUPPORTED;
+    }
+    *out = nullptr;
+    cn_transport* h = new (std::nothrow) cn_transport();
+    if (!h) return CN_E_CAPACITY;
+    h->c = *cfg;
+    cn_tx_config tc;
+    cn_tx_config_default(&tc);
+    tc.chunk_bytes = cfg->chunk_bytes;
+    tc.dupack_threshold = cfg->dupack_threshold;
+    tc.rtx_avoid_prev_path = cfg->rtx_avoid_prev_path;
+    tc.lb_policy = cfg->lb;
+    tc.max_inflight_msgs = cfg->max_inflight_msgs;
+    tc.max_paths = cfg->paths;
+    tc.log_cap = cfg->log_cap;
+    tc.rto_min = cfg->rto_min;
+    tc.rto_max = cfg->rto_max;
+    tc.commit_ahead = cfg->commit_ahead > 0 ? cfg->commit_ahead
+                                            : std::max<int64_t>(2ll * cfg->chunk_bytes, 2ll * cfg->drr_quantum);
+    tc.base_rtt_ns = cfg->base_rtt_ns;
+    tc.seed = seed;
+    tc.stream_index0 = 0;
+    tc.chunk_pool = cfg->chunk_pool;
+    tc.cc_algo = cfg->cc_algo;
+    tc.drr_quantum = cfg->drr_quantum;
+    tc.mss = cfg->mss;
+    tc.cap_bytes = cfg->cap_bytes;
+    tc.swift_target_ns = cfg->swift_target_ns;
+    tc.init_cwnd_pkts = cfg->init_cwnd_pkts;
+    int rc = cn_tx_create(&tc, cfg->max_conns, nullptr, nullptr, nullptr, &h->tx);
+    if (rc != CN_OK) {
+        cn_transport_destroy(h);
+        return rc;
+    }
+    cn_rx_config rcfg;
+    cn_rx_config_default(&rcfg);
+    rcfg.chunk_bytes = cfg->chunk_bytes;
+    rcfg.carry_payload = cfg->carry_payload;
+    rcfg.max_conns = std::max<uint32_t>(64, 2 * cfg->max_conns);
+    rcfg.max_msgs = std::max<uint32_t>(256, 16 * cfg->max_conns);
+    rcfg.chunk_pool = cfg->chunk_pool;
+    rcfg.arena_bytes = cfg->carry_payload ? cfg->arena_bytes : 0;
+    rcfg.max_batch = cfg->max_batch;
+    rc = cn_rx_create(&rcfg, &h->rx);
+    if (rc != CN_OK) {
+        cn_transport_destroy(h);
+        return rc;
+    }
+    const uint64_t nc = cfg->max_conns, nb = cfg->max_batch + 16ull;
+    bool ok = cudaMalloc(&h->d_log, nc * cfg->log_cap * sizeof(cn_tx_rec)) == cudaSuccess &&
+              cudaMalloc(&h->d_stats, nc * sizeof(cn_tx_stats)) == cudaSuccess &&
+              cudaMalloc(&h->d_evoff, (nc + 1) * 4) == cudaSuccess &&
+              cudaMalloc(&h->d_aout, nb * sizeof(cn_ack_rec)) == cudaSuccess &&
+              cudaMalloc(&h->d_cpls, nb * sizeof(cn_completion)) == cudaSuccess &&
+              cudaMalloc(&h->d_res, sizeof(cn_rx_result)) == cudaSuccess;
+    if (!ok) {
+        set_error("cn_transport_create: out of device memory");
+        cn_transport_destroy(h);
+        return CN_E_CAPACITY;
+    }
+    cudaMemset(h->d_stats, 0, nc * sizeof(cn_tx_stats));
+    h->pend.resize(nc);
+    h->txs.assign(nc, cn_tx_stats{});
+    *out = h;
+    return CN_OK;
+}
+
+static int32_t open_conn(cn_transport* h, int32_t src, int32_t dst, bool create) {
+    auto it = h->conn_idx.find({src, dst});
+    if (it != h->conn_idx.end()) return it->second;
+    if (!create) return -1;
+    const int32_t k = static_cast<int32_t>(h->conn_idx.size());
+    if (static_cast<uint32_t>(k) >= h->c.max_conns) return -1;
+    h->conn_idx[{src, dst}] = k;
+    return k;
+}
+
+extern "C" int32_t cn_transport_conn_index(cn_transport* h, int32_t src, int32_t dst) {
+    return h ? open_conn(h, src, dst, false) : -1;
+}
+
+extern "C" int cn_transport_send_message(cn_transport* h, int32_t src, int32_t dst, uint64_t len, uint64_t tag,
+                                         int64_t t) {
+    if (!h) return CN_E_INVALID;
+    if (len == 0) {
+        set_error("send_message: empty message (transport.cpp:145)");
+        return CN_E_INVALID;
+    }
+    const int32_t k = open_conn(h, src, dst, true);
+    if (k < 0) {
+        set_error("send_message: max_conns connections already open");
+        return CN_E_CAPACITY;
+    }
+    h->subs.push_back(cn_tx_submit{t, len, tag});
+    h->pend[k].push_back(Ev{t, 0, static_cast<uint32_t>(h->subs.size() - 1)});
+    return 1;
+}
+
+extern "C" int cn_transport_handle_acks(cn_transport* h, const cn_ack_rec* acks, uint32_t n) {
+    if (!h || (n && !acks)) return CN_E_INVALID;
+    for (uint32_t i = 0; i < n; ++i) {
+        // handle_ack / handle_nack look the connection up at the receiving host (:850-852)
+        const int32_t k = open_conn(h, acks[i].dst, acks[i].src, false);
+        if (k < 0) continue;
+        h->acks.push_back(acks[i]);
+        h->pend[k].push_back(Ev{acks[i].aux, 1, static_cast<uint32_t>(h->acks.size() - 1)});
+    }
+    return CN_OK;
+}
+
+extern "C" int cn_transport_advance(cn_transport* h, int64_t until, void* stream) {
+    if (!h) return CN_E_INVALID;
+    const uint32_t nc = h->c.max_conns;
+    std::vector<uint32_t> off(nc + 1, 0);
+    std::vector<uint64_t> ev;
+    for (uint32_t k = 0; k < nc; ++k) {
+        auto& v = h->pend[k];
+        std::stable_sort(v.begin(), v.end(), [](const Ev& a, const Ev& b) {
+            return a.t != b.t ? a.t < b.t : a.type < b.type;
+        });
+        for (const Ev& e : v) ev.push_back((static_cast<uint64_t>(e.type) << 62) | e.idx);
+        off[k + 1] = static_cast<uint32_t>(ev.size());
+    }
+    if (!grow(&h->d_ev, &h->cap_ev, ev.size() + 1) || !grow(&h->d_subs, &h->cap_subs, h->subs.size() + 1) ||
+        !grow(&h->d_ain, &h->cap_ain, h->acks.size() + 1)) {
+        set_error("cn_transport_advance: out of device memory");
+        return CN_E_CAPACITY;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CNB_CUDA(cudaMemcpyAsync(h->d_evoff, off.data(), (nc + 1) * 4ull, cudaMemcpyHostToDevice, s));
+    if (!ev.empty()) CNB_CUDA(cudaMemcpyAsync(h->d_ev, ev.data(), ev.size() * 8, cudaMemcpyHostToDevice, s));
+    if (!h->subs.empty())
+        CNB_CUDA(cudaMemcpyAsync(h->d_subs, h->subs.data(), h->subs.size() * sizeof(cn_tx_submit),
+                                 cudaMemcpyHostToDevice, s));
+    if (!h->acks.empty())
+        CNB_CUDA(cudaMemcpyAsync(h->d_ain, h->acks.data(), h->acks.size() * sizeof(cn_ack_rec),
+                                 cudaMemcpyHostToDevice, s));
+    int rc = cn_tx_run(h->tx, h->d_evoff, h->d_ev, h->d_subs, h->d_ain, until, h->d_log, h->d_stats, stream);
+    if (rc != CN_OK) return rc;
+    CNB_CUDA(cudaMemcpyAsync(h->txs.data(), h->d_stats, nc * sizeof(cn_tx_stats), cudaMemcpyDeviceToHost, s));
+    CNB_CUDA(cudaStreamSynchronize(s));
+    unsigned int st = 0;
+    cn_tx_status(h->tx, &st);
+    for (auto& v : h->pend) v.clear();
+    h->subs.clear();
+    h->acks.clear();
+    if (st) {
+        set_error("cn_transport_advance: sender status 0x" + std::to_string(st));
+        return CN_E_CAPACITY;
+    }
+    return CN_OK;
+}
+
+extern "C" int64_t cn_transport_poll_transmissions(cn_transport* h, cn_tx_rec* out, uint64_t cap, int32_t* conn_out) {
+    if (!h) return CN_E_INVALID;
+    const uint32_t nc = h->c.max_conns;
+    std::vector<uint32_t> cnt(nc);
+    int rc = cn_tx_log_counts(h->tx, cnt.data());
+    if (rc != CN_OK) return rc;
+    uint64_t k = 0;
+    for (uint32_t c = 0; c < nc; ++c) {
+        const uint32_t m = std::min(cnt[c], h->c.log_cap);
+        if (!m) continue;
+        if (out && k < cap) {
+            const uint64_t take = std::min<uint64_t>(m, cap - k);
+            CNB_CUDA(cudaMemcpy(out + k, h->d_log + static_cast<uint64_t>(c) * h->c.log_cap,
+                                take * sizeof(cn_tx_rec), cudaMemcpyDeviceToHost));
+            if (conn_out)
+                for (uint64_t j = 0; j < take; ++j) conn_out[k + j] = static_cast<int32_t>(c);
+        }
+        k += m;
+    }
+    rc = cn_tx_log_clear(h->tx, nullptr);
+    if (rc != CN_OK) return rc;
+    CNB_CUDA(cudaDeviceSynchronize());
+    return static_cast<int64_t>(k);
+}
+
+extern "C" int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const void* d_payload,
+                                        uint64_t stride, uint32_t n, void* stream) {
+    if (!h) return CN_E_INVALID;
+    if (n > h->c.max_batch) {
+        set_error("cn_transport_handle_data: batch larger than max_batch");
+        return CN_E_CAPACITY;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = cn_rx_batch(h->rx, d_hdrs, d_payload, stride, n, h->d_aout, n + 16, h->d_cpls, n + 16, h->d_res,
+                         stream);
+    if (rc != CN_OK) return rc;
+    cn_rx_result r;
+    CNB_CUDA(cudaMemcpyAsync(&r, h->d_res, sizeof r, cudaMemcpyDeviceToHost, s));
+    CNB_CUDA(cudaStreamSynchronize(s));
+    if (r.status) {
+        set_error("cn_transport_handle_data: receive status 0x" + std::to_string(r.status));
+        return (r.status & (CN_RXF_UNSUPPORTED | CN_RXF_ALIAS)) ? CN_E_UNSUPPORTED : CN_E_CAPACITY;
+    }
+    h->last_acks.resize(r.n_acks);
+    h->last_cpls.resize(r.n_completions);
+    if (r.n_acks)
+        CNB_CUDA(cudaMemcpy(h->last_acks.data(), h->d_aout, r.n_acks * sizeof(cn_ack_rec), cudaMemcpyDeviceToHost));
+    if (r.n_completions)
+        CNB_CUDA(cudaMemcpy(h->last_cpls.data(), h->d_cpls, r.n_completions * sizeof(cn_completion),
+                            cudaMemcpyDeviceToHost));
+    for (const cn_ack_rec& a : h->last_acks) {
+        if (a.flags & CN_ACK_NACK) ++h->nacks_sent;
+        else ++h->acks_sent;
+    }
+    h->delivered += r.n_completions;
+    return CN_OK;
+}
+
+extern "C" int64_t cn_transport_poll_acks(cn_transport* h, cn_ack_rec* out, uint64_t cap) {
+    if (!h) return CN_E_INVALID;
+    const uint64_t n = h->last_acks.size();
+    if (out) memcpy(out, h->last_acks.data(), std::min(n, cap) * sizeof(cn_ack_rec));
+    return static_cast<int64_t>(n);
+}
+
+extern "C" int64_t cn_transport_poll_completions(cn_transport* h, cn_completion* out, uint64_t cap) {
+    if (!h) return CN_E_INVALID;
+    const uint64_t n = h->last_cpls.size();
+    if (out) memcpy(out, h->last_cpls.data(), std::min(n, cap) * sizeof(cn_completion));
+    return static_cast<int64_t>(n);
+}
+
+extern "C" int cn_transport_stats(cn_transport* h, cn_stats* o) {
+    if (!h || !o) return CN_E_INVALID;
+    memset(o, 0, sizeof *o);
+    for (const cn_tx_stats& t : h->txs) {
+        o->msgs_sent += t.msgs_sent;
+        o->msgs_completed += t.msgs_completed;
+        o->backpressured += t.backpressured;
+        o->chunks_sent += t.chunks_sent;
+        o->chunk_rtx += t.chunk_rtx;
+        o->fast_rtx += t.fast_rtx;
+        o->rtos += t.rtos;
+    }
+    o->acks_sent = h->acks_sent;
+    o->nacks_sent = h->nacks_sent;
+    o->delivered_msgs = h->delivered;
+    return CN_OK;
+}
+
+extern "C" int64_t cn_transport_outstanding_bytes(cn_transport* h, int32_t src, int32_t dst) {
+    if (!h) return CN_E_INVALID;
+    const int32_t k = open_conn(h, src, dst, false);
+    return k < 0 ? 0 : h->txs[k].inflight;
+}

@@ -1123,6 +1123,18 @@ extern "C" int cn_tx_run(cn_tx* t, const uint32_t* d_ev_off, const uint64_t* d_e
     return CN_OK;
 }
 
+extern "C" int cn_tx_log_counts(cn_tx* t, uint32_t* h_out) {
+    if (!t || !h_out) return CN_E_INVALID;
+    CNB_CUDA(cudaMemcpy(h_out, t->d_logn, t->d.n_conns * 4ull, cudaMemcpyDeviceToHost));
+    return CN_OK;
+}
+
+extern "C" int cn_tx_log_clear(cn_tx* t, void* stream) {
+    if (!t) return CN_E_INVALID;
+    CNB_CUDA(cudaMemsetAsync(t->d_logn, 0, t->d.n_conns * 4ull, static_cast<cudaStream_t>(stream)));
+    return CN_OK;
+}
+
 extern "C" int cn_tx_status(cn_tx* t, unsigned int* out) {
     if (!t || !out) return CN_E_INVALID;
     CNB_CUDA(cudaMemcpy(out, t->d.status, 4, cudaMemcpyDeviceToHost));

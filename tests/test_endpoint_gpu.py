@@ -1,0 +1,82 @@
+"""The unified boundary object (cn_transport_*, TransportEndpoint) driven
+like chunknet::Transport: the recorded sender scenarios through
+send_message / handle_acks / advance give the reference transmit log, and
+a multi-connection trim incast through one object gives every connection's
+log; the receive side of the same object gives the reference ack stream."""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+from oracle.records import ack_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _ep(meta, n_conns=4, **kw):
+    from paper_2504_17307_b200.endpoint import TransportEndpoint
+    return TransportEndpoint(chunk_bytes=meta["chunk_bytes"], paths=meta["n_paths"], lb=meta["lb"],
+                             rto_min=meta["rto_min"], rto_max=meta["rto_max"], commit_ahead=meta["commit_ahead"],
+                             base_rtt_ns=meta["base_rtt"], seed=meta["seed"], cc=meta.get("cc", "none"),
+                             swift_target_ns=meta.get("swift_target_ns", 0), max_conns=n_conns,
+                             chunk_pool=1 << 18, log_cap=1 << 17, **kw)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "lossy_2m", "swift_closed_k8", "swift_cfg1"])
+def test_endpoint_sender_replay(name):
+    z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    ep = _ep(meta)
+    for s in z["submits"]:
+        ep.send_message(meta["src"], meta["dst"], int(s["len"]), int(s["tag"]), int(s["t"]))
+    ep.handle_acks(z["acks"])
+    ep.advance(60_000_000_000)
+    tx, conn = ep.poll_transmissions()
+    want = z["tx"]
+    assert len(tx) == len(want) and (conn == 0).all()
+    for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
+        assert (tx[f] == want[f]).all(), f
+    st = ep.stats()
+    for k in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos"):
+        assert st[k] == meta["stats"][k], k
+
+
+def test_endpoint_multi_connection_and_receive():
+    names = sorted(glob.glob(os.path.join(GOLDEN, "sender_swift_trim_swift_f*.npz")))
+    assert len(names) == 4
+    zs = [np.load(p) for p in names]
+    metas = [json.loads(bytes(z["meta"]).decode()) for z in zs]
+    ep = _ep(metas[0])
+    for z, m in zip(zs, metas):  # connections open in flow order (conn_to)
+        for s in z["submits"]:
+            ep.send_message(m["src"], m["dst"], int(s["len"]), int(s["tag"]), int(s["t"]))
+    ep.handle_acks(np.concatenate([z["acks"] for z in zs]))
+    # advance in two slices: state carries over
+    ep.advance(2_000_000)
+    tx1, c1 = ep.poll_transmissions()
+    ep.advance(60_000_000_000)
+    tx2, c2 = ep.poll_transmissions()
+    tx, conn = np.concatenate([tx1, tx2]), np.concatenate([c1, c2])
+    for k, (z, m) in enumerate(zip(zs, metas)):
+        assert ep.conn_index(m["src"], m["dst"]) == k
+        got = tx[conn == k]
+        got = got[np.argsort(got["t"], kind="stable")]
+        want = z["tx"]
+        assert len(got) == len(want), k
+        for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
+            assert (got[f] == want[f]).all(), (k, f)
+    # receive side of the same object: the trim incast's delivered packets
+    import paper_2504_17307_b200 as cn
+    from oracle import oracle as O
+    data, acks_ref, cpls_ref, meta = load_golden("trim_swift")
+    import torch
+    ep.handle_data(cn.to_device_records(data), torch.from_numpy(O.fill_staging(data)).cuda())
+    ok, bad = ack_equal(ep.poll_acks(), acks_ref)
+    assert ok, bad
+    assert len(ep.poll_completions()) == len(cpls_ref)
+    st = ep.stats()
+    assert st["nacks_sent"] == int(((acks_ref["flags"] & 4) != 0).sum())
+    assert st["delivered_msgs"] == len(cpls_ref)

@@ -17,6 +17,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "chunknet_b200.h"
@@ -209,6 +210,66 @@ class PathScheduler {
   private:
     cn_sched* s_ = nullptr;
     uint32_t n_;
+};
+
+// ------------------------------------------------- transport.hpp:53-107
+// chunknet::Transport's shape over the device engines (cn_transport_*): the
+// caller's clock replaces the event loop -- queue sends and the acks the
+// fabric delivered, advance to a time, poll what the transport did.
+class Endpoint {
+  public:
+    explicit Endpoint(const cn_transport_config& cfg, uint64_t seed) {
+        check(cn_transport_create(&cfg, seed, &h_), "cn_transport_create");
+    }
+    ~Endpoint() { cn_transport_destroy(h_); }
+    Endpoint(const Endpoint&) = delete;
+    Endpoint& operator=(const Endpoint&) = delete;
+
+    // Transport::send_message (transport.hpp:88) at time t; throws on an
+    // empty message like the reference (std::invalid_argument)
+    void send_message(int src, int dst, uint64_t len, uint64_t tag, int64_t t) {
+        int rc = cn_transport_send_message(h_, src, dst, len, tag, t);
+        if (rc < 0) check(rc, "send_message");
+    }
+    // acks and trimmed-header NACKs delivered at the senders (aux = time)
+    void handle_acks(const std::vector<cn_ack_rec>& acks) {
+        check(cn_transport_handle_acks(h_, acks.data(), static_cast<uint32_t>(acks.size())), "handle_acks");
+    }
+    void advance(int64_t until, cudaStream_t s = nullptr) { check(cn_transport_advance(h_, until, s), "advance"); }
+    // every send_chunk since the last poll, with its connection index
+    std::vector<std::pair<int32_t, cn_tx_rec>> poll_transmissions() {
+        std::vector<cn_tx_rec> r(1 << 20);
+        std::vector<int32_t> c(r.size());
+        int64_t n = cn_transport_poll_transmissions(h_, r.data(), r.size(), c.data());
+        if (n < 0) check(static_cast<int>(n), "poll_transmissions");
+        std::vector<std::pair<int32_t, cn_tx_rec>> out;
+        for (int64_t i = 0; i < n && i < static_cast<int64_t>(r.size()); ++i) out.push_back({c[i], r[i]});
+        return out;
+    }
+    // Transport::handle_packet for a batch of delivered data packets (device records)
+    void handle_data(const cn_pkt_hdr* d_hdrs, const void* d_payload, uint64_t stride, uint32_t n,
+                     cudaStream_t s = nullptr) {
+        check(cn_transport_handle_data(h_, d_hdrs, d_payload, stride, n, s), "handle_data");
+    }
+    std::vector<cn_ack_rec> poll_acks() {
+        std::vector<cn_ack_rec> a(static_cast<size_t>(cn_transport_poll_acks(h_, nullptr, 0)));
+        cn_transport_poll_acks(h_, a.data(), a.size());
+        return a;
+    }
+    std::vector<cn_completion> poll_completions() {
+        std::vector<cn_completion> c(static_cast<size_t>(cn_transport_poll_completions(h_, nullptr, 0)));
+        cn_transport_poll_completions(h_, c.data(), c.size());
+        return c;
+    }
+    cn_stats stats() const {
+        cn_stats s;
+        check(cn_transport_stats(h_, &s), "stats");
+        return s;
+    }
+    int64_t outstanding_bytes(int src, int dst) const { return cn_transport_outstanding_bytes(h_, src, dst); }
+
+  private:
+    cn_transport* h_ = nullptr;
 };
 
 }  // namespace b200

@@ -50,3 +50,24 @@ def test_cpp_rx_facade_replays_golden(tmp_path, name):
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "CPP_RX_OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cfg1", "lossy_2m"])
+def test_cpp_endpoint_replays_sender(tmp_path, name):
+    import json
+    from paper_2504_17307_b200.sender import LB
+    exe = str(tmp_path / "endpoint_replay")
+    _build("endpoint_replay.cpp", exe)
+    z = np.load(os.path.join(ROOT, "tests", "golden", f"sender_{name}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    z["submits"].tofile(tmp_path / "subs.bin")
+    z["acks"].tofile(tmp_path / "acks.bin")
+    z["tx"].tofile(tmp_path / "tx.bin")
+    args = [exe, str(tmp_path / "subs.bin"), str(tmp_path / "acks.bin"), str(tmp_path / "tx.bin"),
+            str(meta["chunk_bytes"]), str(meta["n_paths"]), str(LB[meta["lb"]]), str(meta["rto_min"]),
+            str(meta["rto_max"]), str(meta["commit_ahead"]), str(meta["base_rtt"]), str(meta["seed"]),
+            str(meta["src"]), str(meta["dst"])]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "CPP_ENDPOINT_OK" in r.stdout

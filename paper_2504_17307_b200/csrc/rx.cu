@@ -1543,7 +1543,19 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
             lc.numAttrs = 1;
             CNB_CUDA(cudaLaunchKernelEx(&lc, k_scan, d));
         }
-        k_trim<<<1, 1024, kTrimMax * 8, s>>>(d, d_hdrs);
+        {  // rare work, but on the ack path: same priority, or it queues behind the scatter
+            cudaLaunchConfig_t lc = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributePriority;
+            at[0].val.priority = rx->hi_prio;
+            lc.gridDim = dim3(1);
+            lc.blockDim = dim3(1024);
+            lc.dynamicSmemBytes = kTrimMax * 8;
+            lc.stream = s;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            CNB_CUDA(cudaLaunchKernelEx(&lc, k_trim, d, d_hdrs));
+        }
         prof_mark(ev, s);
         // persistent: as many blocks as fit beside the scatter, tiles by ticket
         const uint32_t ag = tiles < static_cast<uint32_t>(rx->sms) * 4 ? tiles : rx->sms * 4;

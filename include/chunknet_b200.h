@@ -102,6 +102,10 @@ typedef struct cn_pkt_hdr {
 /* the record is a trimmed-header NACK (transport.cpp:657-674): hdr = the
  * trimmed packet's header, cum_csn = nack_csn; no cum / SACK / echo */
 #define CN_ACK_NACK 0x4u
+/* receiver-driven mode (EQDS) control packets at the sender: a credit grant
+ * (credit bytes in sack[0]) or an RTS acknowledgement */
+#define CN_ACK_CREDIT 0x8u
+#define CN_ACK_RTS_ACK 0x10u
 typedef struct cn_ack_rec {
     int32_t src;          /* ack source = receiving host   */
     int32_t dst;          /* ack destination = sender host */
@@ -295,6 +299,14 @@ typedef struct cn_tx_config {
     int64_t cap_bytes;            /* CcConfig::cap_bytes, 0 = uncapped       */
     int64_t swift_target_ns;      /* CcConfig::swift_target_ns (resolved)    */
     double init_cwnd_pkts;        /* CcConfig::init_cwnd_pkts (2.0)          */
+    /* receiver-driven mode (EQDS glue, transport.cpp:1003-1074): credit
+     * gates egress; RTS (logged as records with chunk = 0xFFFFFFFF, msg_seq =
+     * demand, is_rtx = retransmissions queued) when credit runs out */
+    int32_t receiver_driven;
+    uint32_t credit_quantum;      /* TransportConfig::credit_quantum (32768) */
+    int32_t credit_bank_quanta;   /* TransportConfig::credit_bank_quanta (4) */
+    int32_t pad_rd;
+    int64_t initial_credit;       /* resolved (-1 in the reference = one BDP) */
 } cn_tx_config;
 typedef struct cn_tx_submit { int64_t t; uint64_t len; uint64_t tag; } cn_tx_submit;
 /* one chunk transmission (send_chunk): time, message, chunk index, path */

@@ -87,6 +87,16 @@ SCENARIOS = {
                         loss=0.0, seed=9, chunk_bytes=16384, paths=1, lb="oblivious",
                         cc="none", queue="trim", trim_depth=4, window=2),
                    [(1, 0, MiB, 2), (2, 0, MiB, 2), (3, 0, MiB, 2), (4, 0, MiB, 2)]),
+    # receiver-driven (EQDS) incast: 5 senders into one host, credit-gated
+    "eqds_incast": (dict(topo="star", topo_arg=6, rate_bps=100e9, qcap_bytes=128 * 1024,
+                         loss=0.0, seed=5, chunk_bytes=32768, paths=1, lb="oblivious",
+                         cc="none", receiver_driven=True, window=2),
+                    [(1, 0, MiB, 2), (2, 0, MiB, 2), (3, 0, MiB, 2), (4, 0, MiB, 2), (5, 0, MiB, 2)]),
+    # the same with 1% loss: retransmissions owed while credit-gated
+    "eqds_lossy": (dict(topo="star", topo_arg=6, rate_bps=100e9, qcap_bytes=128 * 1024,
+                        loss=0.01, seed=6, chunk_bytes=16384, paths=1, lb="oblivious",
+                        cc="swift", receiver_driven=True, window=2),
+                   [(1, 0, MiB, 3), (2, 0, MiB, 3), (3, 0, MiB, 3), (4, 0, MiB, 3)]),
     # closed loop under Swift: the DES sender runs Swift (target 3 x base
     # RTT), so its recorded acks answer exactly what a Swift sender sends
     "closed_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,
@@ -152,16 +162,18 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
         subs = subs[(subs["src"] == src) & (subs["dst"] == dst)]
         name = f"{name}_f{flow}"
     rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes",
-                              "paths", "lb") if k in kw}
+                              "paths", "lb", "receiver_driven") if k in kw}
     submits = [(int(s["t"]), int(s["len"]), int(s["tag"])) for s in subs]
     tx, st = ref.sender_replay(acks_des, submits, src, dst, cc=cc, **rkw)
     rate = kw.get("rate_bps", 400e9)
     bdp = int(round(rate * st["base_rtt"] / 8e9))
     commit_ahead = max(2 * kw["chunk_bytes"], 2 * 32768, bdp)
+    assert commit_ahead == st["commit_ahead"], (commit_ahead, st["commit_ahead"])
     meta = dict(name=name, src=src, dst=dst, chunk_bytes=kw["chunk_bytes"], lb=kw["lb"],
                 seed=kw["seed"], n_paths=int(st["n_paths"]), base_rtt=int(st["base_rtt"]),
                 rto_min=int(st["rto_min"]), rto_max=int(st["rto_max"]), commit_ahead=commit_ahead,
                 end_time=int(st["end_time"]), stats={k: int(v) for k, v in st.items()}, cc=cc,
+                receiver_driven=bool(kw.get("receiver_driven", False)), initial_credit=int(st["bdp"]),
                 # the harness resolves Swift's target to 3 x base RTT (ref_harness.cpp)
                 swift_target_ns=3 * int(st["base_rtt"]) if cc == "swift" else 0)
     path = os.path.join(GOLDEN, f"sender_{name}.npz" if cc == "none" else f"sender_{cc}_{name}.npz")
@@ -176,7 +188,7 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
 # Swift: the replay must reproduce the DES sender's own transmissions
 CLOSED_SWIFT = ["closed_k8", "closed_w4", "closed_cfg2"]
 # trim-mode incasts: every connection replayed with its acks and NACKs
-TRIM_SENDER = ["trim_swift", "trim_storm"]
+TRIM_SENDER = ["trim_swift", "trim_storm", "eqds_incast", "eqds_lossy"]
 
 # Swift (device-exact CC) goldens: the same stimulus as sender_<name>.npz
 SWIFT_SCENARIOS = ["cfg1", "cfg2_32k", "k8_4x1m", "multigen_k8", "lossy_2m", "csn_wrap"]

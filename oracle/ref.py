@@ -31,6 +31,7 @@ class Scenario(ctypes.Structure):
         ("rto_min", ctypes.c_int64), ("n_flows", ctypes.c_int32),
         ("window", ctypes.c_int32), ("cutoff_ns", ctypes.c_int64),
         ("queue_mode", ctypes.c_int32), ("trim_depth", ctypes.c_int32),
+        ("receiver_driven", ctypes.c_int32), ("pad_rd", ctypes.c_int32),
     ]
 
 
@@ -65,7 +66,8 @@ class SenderStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "chunks_sent", "chunk_rtx", "fast_rtx", "rtos", "msgs_completed", "n_tx")] + [
         (n, ctypes.c_int64) for n in ("base_rtt", "rto_min", "rto_max", "end_time")] + [
-        ("n_paths", ctypes.c_int32), ("pad", ctypes.c_int32)]
+        ("n_paths", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("bdp", ctypes.c_int64), ("commit_ahead", ctypes.c_int64), ("rts_sent", ctypes.c_uint64)]
 
 
 class Submit(ctypes.Structure):
@@ -127,13 +129,13 @@ def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
            link_delay_ns=1000, qcap_bytes=1 << 20, loss=0.0, seed=1,
            chunk_bytes=32768, paths=8, lb="p2_rtt", cc="cubic", cc_scope=0,
            engines=1, conn_split=0, dupack_threshold=8, rto_min=0, flows=(),
-           window=1, cutoff_ns=60_000_000_000, queue="drop_tail", trim_depth=0):
+           window=1, cutoff_ns=60_000_000_000, queue="drop_tail", trim_depth=0, receiver_driven=False):
     """Runs the reference DES and writes data.bin / acks_des.bin /
     completions_des.bin into outdir.  flows: [(src, dst, len, count)]."""
     sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns,
                   qcap_bytes, loss, seed, chunk_bytes, paths, LB[lb], CC[cc],
                   cc_scope, engines, conn_split, dupack_threshold, rto_min,
-                  len(flows), window, cutoff_ns, QUEUE[queue], trim_depth)
+                  len(flows), window, cutoff_ns, QUEUE[queue], trim_depth, 1 if receiver_driven else 0)
     fl = (Flow * max(1, len(flows)))(*[Flow(s, d, l, c, 0) for (s, d, l, c) in flows])
     st = RecordStats()
     os.makedirs(outdir, exist_ok=True)
@@ -152,12 +154,14 @@ def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
 def sender_replay(acks, submits, src, dst, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
                   link_delay_ns=1000, qcap_bytes=1 << 20, seed=1, chunk_bytes=32768, paths=8,
                   lb="p2_rtt", cc="none", cc_scope=0, dupack_threshold=8, rto_min=0,
-                  cutoff_ns=60_000_000_000, max_out=1 << 20):
+                  cutoff_ns=60_000_000_000, max_out=1 << 20, receiver_driven=False):
     """Reference sender over a blackhole: submits [(t, len, tag)] and acks
-    (ACK_DTYPE, aux = delivery time at the sender) -> (tx log, stats)."""
+    (ACK_DTYPE, aux = delivery time at the sender; also NACK / credit /
+    rts_ack records) -> (tx log, stats).  Receiver-driven: RTS packets are
+    logged as records with chunk = 0xFFFFFFFF, msg_seq = demand."""
     sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns, qcap_bytes, 0.0,
                   seed, chunk_bytes, paths, LB[lb], CC[cc], cc_scope, 1, 0, dupack_threshold,
-                  rto_min, 0, 1, cutoff_ns)
+                  rto_min, 0, 1, cutoff_ns, 0, 0, 1 if receiver_driven else 0)
     sb = (Submit * max(1, len(submits)))(*[Submit(int(t), int(l), int(g)) for t, l, g in submits])
     acks = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
     out = np.zeros(max_out, dtype=TX_DTYPE)

@@ -115,12 +115,16 @@ cn_ack_rec ack_rec(const Packet& p, uint32_t idx, int64_t aux) {
     a.cum_csn = p.cum_csn;
     a.flags = (p.cum_valid ? CN_ACK_CUM_VALID : 0) |
               (p.ecn_echo ? CN_ACK_ECN_ECHO : 0) |
-              (p.kind == PacketKind::nack ? CN_ACK_NACK : 0);
+              (p.kind == PacketKind::nack ? CN_ACK_NACK : 0) |
+              (p.kind == PacketKind::credit ? CN_ACK_CREDIT : 0) |
+              (p.kind == PacketKind::rts_ack ? CN_ACK_RTS_ACK : 0);
     if (p.kind == PacketKind::nack) a.cum_csn = p.nack_csn;
+
     a.pkt_index = idx;
     a.msg_seq = p.msg_seq;
     a.sack[0] = p.sack[0];
     a.sack[1] = p.sack[1];
+    if (p.kind == PacketKind::credit) a.sack[0] = p.credit_bytes;
     a.echo_tx_time = p.echo_tx_time;
     a.aux = aux;
     return a;
@@ -128,7 +132,11 @@ cn_ack_rec ack_rec(const Packet& p, uint32_t idx, int64_t aux) {
 
 Packet from_ack(const cn_ack_rec& a) {
     Packet p;
-    p.kind = (a.flags & CN_ACK_NACK) ? PacketKind::nack : PacketKind::ack;
+    p.kind = (a.flags & CN_ACK_NACK)      ? PacketKind::nack
+             : (a.flags & CN_ACK_CREDIT)  ? PacketKind::credit
+             : (a.flags & CN_ACK_RTS_ACK) ? PacketKind::rts_ack
+                                          : PacketKind::ack;
+    if (a.flags & CN_ACK_CREDIT) p.credit_bytes = static_cast<uint32_t>(a.sack[0]);
     if (a.flags & CN_ACK_NACK) {
         p.nack_csn = a.cum_csn;
         p.nack_trim = true;
@@ -183,6 +191,8 @@ struct cnref_scenario {
     int64_t cutoff_ns;
     int32_t queue_mode;  // QueueMode: 0 drop_tail, 1 trim, 2 pause
     int32_t trim_depth;  // NetParams::trim_queue_depth (0 = default)
+    int32_t receiver_driven;  // TransportConfig::receiver_driven (EQDS)
+    int32_t pad_rd;
 };
 
 struct cnref_flow {
@@ -238,6 +248,7 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
         tc.dupack_threshold = sc->dupack_threshold;
         tc.rto_min = sc->rto_min;
         tc.carry_payload = true;
+        tc.receiver_driven = sc->receiver_driven != 0;
         Transport tr(net, eq, tc, sc->seed);
 
         std::vector<cn_pkt_hdr> data;
@@ -250,7 +261,8 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
             const Packet& p = *te.pkt;
             if (p.kind == PacketKind::data)
                 data.push_back(to_rec(p));
-            else if (p.kind == PacketKind::ack || p.kind == PacketKind::nack)
+            else if (p.kind == PacketKind::ack || p.kind == PacketKind::nack ||
+                     p.kind == PacketKind::credit || p.kind == PacketKind::rts_ack)
                 acks.push_back(ack_rec(p, 0, te.t));
         });
 
@@ -483,6 +495,8 @@ struct cnref_sender_stats {
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_completed, n_tx;
     int64_t base_rtt, rto_min, rto_max, end_time;
     int32_t n_paths, pad;
+    int64_t bdp, commit_ahead;
+    uint64_t rts_sent;
 };
 
 struct cnref_submit {
@@ -516,15 +530,47 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
         tc.engines = 1;
         tc.dupack_threshold = sc->dupack_threshold;
         tc.rto_min = sc->rto_min;
+        tc.receiver_driven = sc->receiver_driven != 0;
         Transport tr(net, eq, tc, sc->seed);
+        if (tc.receiver_driven) tr.pacers_[dst].reset();  // the recorded credits drive the sender
+        // Control packets skip the egress blackhole and reach the receiver: an
+        // RTS is logged at delivery minus the (empty-fabric, constant) one-way
+        // control latency of this pair, measured with a probe at t = 0.
+        int64_t ctl_lat = -1;
+        if (tc.receiver_driven) {
+            Packet probe;
+            probe.kind = PacketKind::rts;
+            probe.src = src;
+            probe.dst = dst;
+            net.set_trace([&](const TraceEvent& te) {
+                if (std::strcmp(te.event, "deliver") == 0 && te.pkt->kind == PacketKind::rts) ctl_lat = te.t;
+            });
+            net.inject(std::move(probe));
+            eq.run_until_idle(int64_t{1} << 40);
+            if (ctl_lat < 0) throw std::runtime_error("control latency probe lost");
+        }
+        const int64_t t0 = eq.now();  // inputs are scheduled relative to the probe's end (0 without)
         uint64_t n_out = 0;
         net.set_trace([&](const TraceEvent& te) {
+            if (tc.receiver_driven && std::strcmp(te.event, "deliver") == 0 && te.pkt->kind == PacketKind::rts) {
+                if (n_out < max_out) {
+                    cnref_tx_rec& r = out[n_out];
+                    r.t = te.t - ctl_lat - t0;
+                    r.msg_id = 0;
+                    r.chunk = 0xFFFFFFFFu;  // RTS record
+                    r.path = -1;
+                    r.is_rtx = te.pkt->is_rtx ? 1 : 0;
+                    r.msg_seq = te.pkt->demand_bytes;
+                }
+                ++n_out;
+                return;
+            }
             if (std::strcmp(te.event, "loss") != 0) return;
             const Packet& p = *te.pkt;
             if (p.kind != PacketKind::data || p.seq_in_chunk != 0) return;
             if (n_out < max_out) {
                 cnref_tx_rec& r = out[n_out];
-                r.t = te.t;
+                r.t = te.t - t0;
                 r.msg_id = p.hdr.msg_id;
                 r.chunk = static_cast<uint32_t>(p.chunk_offset / tc.chunk_bytes);
                 r.path = p.path_id;
@@ -535,12 +581,13 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
         });
         for (uint64_t k = 0; k < n_subs; ++k) {
             cnref_submit sb = subs[k];
-            eq.schedule(sb.t, [&tr, src, dst, sb] { tr.send_message(src, dst, sb.len, sb.tag); });
+            eq.schedule(t0 + sb.t, [&tr, src, dst, sb] { tr.send_message(src, dst, sb.len, sb.tag); });
         }
         for (uint64_t k = 0; k < n_acks; ++k) {
             cn_ack_rec a = acks[k];
-            eq.schedule(a.aux, [&tr, a] {
+            eq.schedule(t0 + a.aux, [&tr, a, t0] {
                 Packet p = from_ack(a);
+                p.echo_tx_time += t0;  // the same shift as every send time
                 int host = p.dst;
                 tr.handle_packet(host, std::move(p));
             });
@@ -556,8 +603,11 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
             st->base_rtt = net.base_rtt_ns();
             st->rto_min = tr.rto_min_;
             st->rto_max = tr.rto_max_;
-            st->end_time = eq.now();
+            st->end_time = eq.now() - t0;
             st->n_paths = tr.conns_.empty() ? 0 : static_cast<int>(tr.conns_[0].subs.size());
+            st->bdp = net.bdp_bytes();
+            st->commit_ahead = tr.commit_ahead_;
+            st->rts_sent = tr.stats().rts_sent;
         }
         return 0;
     } catch (const std::exception& e) {

@@ -55,7 +55,10 @@ class TxConfig(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("stream_index0", ctypes.c_int64),
                 ("chunk_pool", ctypes.c_uint64), ("cc_algo", ctypes.c_int32),
                 ("drr_quantum", ctypes.c_uint32), ("mss", ctypes.c_int64), ("cap_bytes", ctypes.c_int64),
-                ("swift_target_ns", ctypes.c_int64), ("init_cwnd_pkts", ctypes.c_double)]
+                ("swift_target_ns", ctypes.c_int64), ("init_cwnd_pkts", ctypes.c_double),
+                ("receiver_driven", ctypes.c_int32), ("credit_quantum", ctypes.c_uint32),
+                ("credit_bank_quanta", ctypes.c_int32), ("pad_rd", ctypes.c_int32),
+                ("initial_credit", ctypes.c_int64)]
 
 
 class RxResult(ctypes.Structure):

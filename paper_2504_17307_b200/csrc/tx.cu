@@ -63,6 +63,8 @@ constexpr uint32_t kQRtx = 0x80000000u;  // c_q kind bit: retransmission queue
 constexpr int kTxWindow = 128;           // kCsnWindow (transport.cpp:14)
 constexpr int kBackoffCap = 64;          // kBackoffCap (transport.cpp:15)
 constexpr int kTxWarps = 4;
+constexpr uint32_t kRetryMax = 32;  // pending RTS retry events per connection
+constexpr uint32_t kStaleMax = 256;  // stale retransmission-queue entries per connection
 constexpr int64_t kNeverDecreased = LLONG_MIN / 2;  // cc.cpp:17
 // cc.cpp:11-16
 constexpr double kSwiftAi = 1.0, kSwiftMdScale = 0.8, kSwiftMaxMd = 0.5, kMinCwndPkts = 1.0;
@@ -81,6 +83,13 @@ struct TxConn {
         n_paths, live_msgs, ring_len;
     uint32_t q_seq, pump_pending;
     int64_t pump_at;
+    // receiver-driven mode (EQDS sender glue, transport.cpp:1003-1074)
+    int64_t credit, unchunked, rtxq_bytes;
+    uint32_t rts_outstanding, rts_acked, sched_seq, timer_seq, pump_seq, retry_head, retry_n, stale_n;
+    int64_t retry_t[kRetryMax];
+    uint32_t retry_seq[kRetryMax];
+    uint32_t stale_seq[kStaleMax];  // acked-while-pending rtx queue entries: (queue seq, path)
+    uint16_t stale_path[kStaleMax];
     uint32_t live_mask[4];  // message slots in use (bit = msg id)
     uint8_t free_ids[128];
     uint8_t fq[128];
@@ -89,7 +98,8 @@ struct TxConn {
 
 struct TxDev {
     uint32_t n_conns, cb, max_pl, dupack, avoid_prev, policy, max_inflight, log_cap, cc_algo, quantum;
-    int64_t rto_min, rto_max, commit_ahead, swift_target, mss, cap_bytes;
+    uint32_t rd, pad_rd;
+    int64_t rto_min, rto_max, commit_ahead, swift_target, mss, cap_bytes, credit_cap, initial_credit;
     double init_cwnd, cap_pkts;
     uint64_t pool_cap;
     TxConn* conns;
@@ -139,6 +149,8 @@ struct Tx {
     uint32_t n_txq, n_rtxq;  // live entries over all tx / retransmission queues
     uint32_t q_seq, pump_pending;
     int64_t pump_at;  // schedule_pump (:219-230): one deferred pump per engine
+    uint32_t sched_seq, timer_seq, pump_seq;  // (time, seq) order of run-scheduled events
+    int64_t credit, unchunked, rtxq_bytes;    // receiver-driven state
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_completed;
     uint32_t live[4];  // live message slots, iterated in slot order
 
@@ -197,7 +209,9 @@ struct Tx {
         last_decrease = now;
     }
     // can_send (:312-325), global scope: the connection's total inflight
-    __device__ bool can_send() const { return total_inflight < cwnd_bytes(); }
+    __device__ bool can_send() const {  // + the credit gate of receiver-driven mode (:314)
+        return total_inflight < cwnd_bytes() && (!d.rd || credit > 0);
+    }
     __device__ void add_inflight(int p, int64_t delta) {  // clamped at 0 (:520-521, :813-814)
         int64_t v = inflight[p] + delta;
         if (v < 0) v = 0;
@@ -222,6 +236,33 @@ struct Tx {
         timer_armed = 1;
         armed_at = now;
         timer_at = now + cur_rto() * backoff;
+        timer_seq = ++sched_seq;
+    }
+    // maybe_send_rts (:1026-1053): ask the receiver's pacer for credit once
+    // credit is spent with bytes still pending; retried every rto_min until
+    // acknowledged (every retry event pending at once, as the reference
+    // schedules them)
+    __device__ void maybe_send_rts(int64_t now) {
+        if (!d.rd || C->rts_outstanding) return;
+        const int64_t pending = unchunked + committed_unsent + rtxq_bytes;  // pending_bytes (:1005-1024)
+        if (pending <= 0 || credit > 0) return;
+        const bool has_rtx = n_rtxq + C->stale_n > 0;  // raw queue emptiness, stale entries included
+        __syncwarp();
+        if (lane == 0) {
+            C->rts_outstanding = 1;
+            C->rts_acked = 0;
+            if (C->retry_n < kRetryMax) {
+                const uint32_t k = (C->retry_head + C->retry_n) % kRetryMax;
+                C->retry_t[k] = now + d.rto_min;
+                C->retry_seq[k] = sched_seq + 1;
+                C->retry_n += 1;
+            } else {
+                atomicOr(d.status, 8u);
+            }
+        }
+        __syncwarp();
+        ++sched_seq;
+        record(now, 0, 0xFFFFFFFFu, -1, has_rtx ? 1 : 0, static_cast<uint64_t>(pending));  // the RTS
     }
     __device__ int select(int prev_path) {  // DefaultPolicy (policy.hpp:80-91)
         int p = select_seq(r, d.policy, n, d.policy == 2 ? ecn_s : rtt_s, lane);
@@ -262,6 +303,7 @@ struct Tx {
         }
         __syncwarp();
         add_inflight(path, chunk_len(m, ci));
+        if (d.rd) credit -= chunk_len(m, ci);  // :486
         if (rtx) ++chunk_rtx;
         else ++chunks_sent;
         record(now, mid, ci, path, rtx || att > 1, m.seq);
@@ -285,11 +327,13 @@ struct Tx {
             rtxq_n[p] += 1;
         }
         ++n_rtxq;
+        rtxq_bytes += chunk_len(m, ci);
         __syncwarp();
         ring_insert(p);
         if (!pump_pending) {  // schedule_pump (:541): runs after the events queued at `now`
             pump_pending = 1;
             pump_at = now;
+            pump_seq = ++sched_seq;
         }
     }
 };
@@ -354,23 +398,61 @@ __device__ void drr_idle(Tx& x, uint32_t visits) {
     x.ring_idx = static_cast<uint32_t>((x.ring_idx + visits) % nr);
 }
 
+// Index of the stale retransmission-queue entry of path p with the smallest
+// queue seq, or -1.
+__device__ int stale_front(const Tx& x, int p) {
+    const TxConn* C = x.C;
+    uint32_t best = 0xFFFFFFFFu;
+    int bi = -1;
+    for (uint32_t k0 = 0; k0 < C->stale_n; k0 += 32) {
+        const uint32_t k = k0 + x.lane;
+        const uint32_t key = (k < C->stale_n && C->stale_path[k] == p) ? C->stale_seq[k] : 0xFFFFFFFFu;
+        const uint32_t mn = __reduce_min_sync(0xffffffffu, key);
+        if (mn < best) {
+            best = mn;
+            bi = static_cast<int>(k0 + __ffs(__ballot_sync(0xffffffffu, key == mn)) - 1);
+        }
+    }
+    return bi;
+}
+
 // egress (transport.cpp:329-431): retransmission queues in ring order, then
 // deficit round robin over the ring, every send gated by can_send.
 __device__ uint32_t egress(Tx& x, int64_t now) {
     uint32_t sent = 0;
-    for (int k = 0; x.n_rtxq && k < x.ring_len; ++k) {  // :333-369
+    for (int k = 0; (x.n_rtxq || x.C->stale_n) && k < x.ring_len; ++k) {  // :333-369
         const int p = x.ring[k];
-        while (x.rtxq_n[p] > 0 && x.can_send()) {
-            uint32_t mid, ci;
-            if (!queue_front(x, p, true, &mid, &ci)) break;
+        while ((x.rtxq_n[p] > 0 || (x.C->stale_n && stale_front(x, p) >= 0)) && x.can_send()) {
+            uint32_t mid = 0, ci = 0;
+            const bool live = x.rtxq_n[p] > 0 && queue_front(x, p, true, &mid, &ci);
+            const uint32_t lseq = live ? (x.d.c_q[load_msg(x.C, mid).chunk_base + ci] & ~kQRtx) : 0xFFFFFFFFu;
+            const int si = x.C->stale_n ? stale_front(x, p) : -1;
+            if (si >= 0 && x.C->stale_seq[si] < lseq) {  // a stale entry at the front: popped, nothing sent
+                __syncwarp();
+                if (x.lane == 0) {
+                    TxConn* C = x.C;
+                    const uint32_t last = C->stale_n - 1;
+                    C->stale_seq[si] = C->stale_seq[last];
+                    C->stale_path[si] = C->stale_path[last];
+                    C->stale_n = last;
+                }
+                __syncwarp();
+                continue;
+            }
+            if (!live) break;
+            const TxMsg m = load_msg(x.C, mid);
             set_u32(&x.rtxq_n[p], x.rtxq_n[p] - 1, x.lane);
             --x.n_rtxq;
-            x.send_chunk(now, mid, load_msg(x.C, mid), ci, true);
+            x.rtxq_bytes -= x.chunk_len(m, ci);
+            x.send_chunk(now, mid, m, ci, true);
             ++sent;
         }
     }
     const uint32_t nr = static_cast<uint32_t>(x.ring_len);
-    if (nr == 0) return sent;
+    if (nr == 0) {
+        if (x.d.rd) x.maybe_send_rts(now);  // :372-377
+        return sent;
+    }
     uint32_t idle = 0;
     while (idle < nr) {  // :378-424
         if (x.n_txq == 0 || !x.can_send()) {  // the remaining visits cannot send
@@ -409,6 +491,7 @@ __device__ uint32_t egress(Tx& x, int64_t now) {
         __syncwarp();
         idle = sent_any ? 0 : idle + 1;
     }
+    if (x.d.rd) x.maybe_send_rts(now);  // :427-430
     return sent;
 }
 
@@ -459,6 +542,7 @@ __device__ void commit_chunks(Tx& x) {
         m.nchunks = ci + 1;
         m.chunked += sz;
         x.committed_unsent += sz;
+        x.unchunked -= sz;
         if (m.chunked < m.len) {
             __syncwarp();
             if (x.lane == 0) C->fq[(head + count) & 127] = static_cast<uint8_t>(mid);
@@ -523,17 +607,31 @@ __device__ void release(Tx& x, int64_t now, const TxMsg& m, uint32_t ci, int64_t
     const int path = x.d.c_path[e];
     const uint32_t len = x.chunk_len(m, ci);
     const uint32_t rq = x.rtxq_n[path];
+    const uint32_t qv = x.d.c_q[e];
     __syncwarp();
     if (x.lane == 0) {
         x.d.c_fl[e] = (fl | TF_ACKED) & ~TF_RTXP;
         if (fl & TF_RTXP) {
             x.rtxq_n[path] = rq - 1;
             x.d.c_q[e] = 0;
+            // its queue entry stays behind, stale, until egress pops it (:347-351)
+            TxConn* C = x.C;
+            if (C->stale_n < kStaleMax) {
+                C->stale_seq[C->stale_n] = qv & ~kQRtx;
+                C->stale_path[C->stale_n] = static_cast<uint16_t>(path);
+                C->stale_n += 1;
+            } else {
+                atomicOr(x.d.status, 16u);
+            }
         }
     }
     __syncwarp();
-    if (fl & TF_RTXP) --x.n_rtxq;
-    else x.add_inflight(path, -static_cast<int64_t>(len));
+    if (fl & TF_RTXP) {
+        --x.n_rtxq;
+        x.rtxq_bytes -= len;
+    } else {
+        x.add_inflight(path, -static_cast<int64_t>(len));
+    }
     x.cc_on_ack(now, len, rtt);
     if (rtt > 0) {  // board.record_rtt / record_ecn (:819-822)
         __syncwarp();
@@ -698,6 +796,7 @@ __device__ void rto_fire(Tx& x) {
         x.timer_armed = 1;
         x.armed_at = now;
         x.timer_at = best;
+        x.timer_seq = ++x.sched_seq;
         return;
     }
     ++x.rtos;
@@ -719,6 +818,7 @@ __device__ void rto_fire(Tx& x) {
                     x.queue_rtx(now, m, w0 + __ffs(b) - 1);
             }
         }
+    if (x.d.rd) x.maybe_send_rts(now);  // :1166
     x.arm_rto(now);  // :1167
     pump(x, now);    // :1168
 }
@@ -770,7 +870,40 @@ __device__ void submit(Tx& x, int64_t now, const cn_tx_submit& s) {
         C->fq_count += 1;
     }
     __syncwarp();
+    // dispatch's RTS check (:216) runs before the message is live, so its
+    // bytes are not pending yet
+    if (x.d.rd) x.maybe_send_rts(now);
+    x.unchunked += s.len;
     pump(x, now);
+}
+
+// handle_credit (:1061-1074): bank the grant up to the cap, clear the
+// outstanding RTS, pump, and ask again if needed
+__device__ void handle_credit(Tx& x, int64_t now, uint64_t bytes) {
+    const int64_t cap = x.d.credit_cap;
+    if (x.credit < cap) {
+        const int64_t v = x.credit + static_cast<int64_t>(bytes);
+        x.credit = v < cap ? v : cap;
+    }
+    __syncwarp();
+    if (x.lane == 0) x.C->rts_outstanding = 0;
+    __syncwarp();
+    pump(x, now);
+    x.maybe_send_rts(now);
+}
+
+// an RTS retry event (:1046-1052)
+__device__ void rts_retry(Tx& x, int64_t now) {
+    TxConn* C = x.C;
+    const bool again = C->rts_outstanding && !C->rts_acked;
+    __syncwarp();
+    if (x.lane == 0) {
+        C->retry_head = (C->retry_head + 1) % kRetryMax;
+        C->retry_n -= 1;
+        if (again) C->rts_outstanding = 0;
+    }
+    __syncwarp();
+    if (again) x.maybe_send_rts(now);
 }
 
 // Fires the events the run itself scheduled -- the RTO timer and the
@@ -780,15 +913,31 @@ __device__ void submit(Tx& x, int64_t now, const cn_tx_submit& s) {
 // at the deferred pump's time was queued before it (rto > 0), so it wins.
 __device__ void run_deferred(Tx& x, int64_t t, bool inclusive) {
     for (;;) {
-        const bool tmr = x.timer_armed && (inclusive ? x.timer_at <= t : x.timer_at < t);
-        const bool pmp = x.pump_pending && (inclusive ? x.pump_at <= t : x.pump_at < t);
-        if (tmr && (!pmp || x.timer_at <= x.pump_at)) {
+        // candidates: the RTO timer, the deferred pump, the oldest RTS retry;
+        // fired in (time, scheduling seq) order
+        int which = -1;
+        int64_t bt = 0;
+        uint32_t bs = 0;
+        auto consider = [&](bool live, int64_t at, uint32_t seq, int id) {
+            if (!live || (inclusive ? at > t : at >= t)) return;
+            if (which < 0 || at < bt || (at == bt && seq < bs)) {
+                which = id;
+                bt = at;
+                bs = seq;
+            }
+        };
+        consider(x.timer_armed, x.timer_at, x.timer_seq, 0);
+        consider(x.pump_pending, x.pump_at, x.pump_seq, 1);
+        if (x.C->retry_n)
+            consider(true, x.C->retry_t[x.C->retry_head], x.C->retry_seq[x.C->retry_head], 2);
+        if (which < 0) return;
+        if (which == 0) {
             rto_fire(x);
-        } else if (pmp) {
+        } else if (which == 1) {
             x.pump_pending = 0;
             pump(x, x.pump_at);
         } else {
-            return;
+            rts_retry(x, bt);
         }
     }
 }
@@ -865,6 +1014,12 @@ __global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(TxDev d, const uint
         x.n_rtxq = __reduce_add_sync(0xffffffffu, b);
     }
     x.q_seq = C->q_seq;
+    x.sched_seq = C->sched_seq;
+    x.timer_seq = C->timer_seq;
+    x.pump_seq = C->pump_seq;
+    x.credit = C->credit;
+    x.unchunked = C->unchunked;
+    x.rtxq_bytes = C->rtxq_bytes;
     x.pump_pending = C->pump_pending;
     x.pump_at = C->pump_at;
     x.chunks_sent = C->chunks_sent;
@@ -884,8 +1039,17 @@ __global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(TxDev d, const uint
             submit(x, t, s);
         } else {
             const cn_ack_rec a = acks[idx];
-            if (a.flags & CN_ACK_NACK) handle_nack(x, t, a);
-            else handle_ack(x, t, a);
+            if (a.flags & CN_ACK_NACK) {
+                handle_nack(x, t, a);
+            } else if (a.flags & CN_ACK_CREDIT) {
+                handle_credit(x, t, a.sack[0]);
+            } else if (a.flags & CN_ACK_RTS_ACK) {
+                __syncwarp();
+                if (lane == 0) C->rts_acked = 1;  // handle_packet rts_ack (:587-592)
+                __syncwarp();
+            } else {
+                handle_ack(x, t, a);
+            }
         }
     }
     run_deferred(x, end_time, true);
@@ -918,6 +1082,12 @@ __global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(TxDev d, const uint
         C->ring_len = x.ring_len;
         C->ring_pos = x.ring_pos;
         C->q_seq = x.q_seq;
+        C->sched_seq = x.sched_seq;
+        C->timer_seq = x.timer_seq;
+        C->pump_seq = x.pump_seq;
+        C->credit = x.credit;
+        C->unchunked = x.unchunked;
+        C->rtxq_bytes = x.rtxq_bytes;
         C->pump_pending = x.pump_pending;
         C->pump_at = x.pump_at;
         C->chunks_sent = x.chunks_sent;
@@ -956,6 +1126,7 @@ __global__ void k_tx_init(TxDev d, const int32_t* src, const int32_t* dst, const
     C->next_seq = 1;
     C->w = d.init_cwnd;
     C->last_decrease = kNeverDecreased;
+    C->credit = d.initial_credit;  // conn_to (:131-133)
     C->src = src ? src[c] : 0;
     C->dst = dst ? dst[c] : 0;
     C->n_paths = np ? np[c] : static_cast<int32_t>(d.s.max_paths);
@@ -998,6 +1169,8 @@ extern "C" void cn_tx_config_default(cn_tx_config* c) {
     c->drr_quantum = 32768;  // TransportConfig::drr_quantum
     c->mss = 4032;           // CcConfig::mss
     c->init_cwnd_pkts = 2.0; // CcConfig::init_cwnd_pkts
+    c->credit_quantum = 32768;  // TransportConfig::credit_quantum
+    c->credit_bank_quanta = 4;  // TransportConfig::credit_bank_quanta
 }
 
 static size_t tx_smem_bytes(uint32_t max_paths) { return kTxWarps * tx_smem_words(max_paths) * 8; }
@@ -1040,6 +1213,9 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
     d.mss = cfg->mss;
     d.cap_bytes = cfg->cap_bytes;
     d.init_cwnd = cfg->init_cwnd_pkts;
+    d.rd = cfg->receiver_driven ? 1 : 0;
+    d.credit_cap = static_cast<int64_t>(cfg->credit_bank_quanta) * cfg->credit_quantum;
+    d.initial_credit = cfg->initial_credit;
     // cap_pkts_ (cc.cpp:111-113)
     d.cap_pkts = cfg->cap_bytes > 0 ? static_cast<double>(cfg->cap_bytes) / static_cast<double>(cfg->mss)
                                     : __builtin_huge_val();

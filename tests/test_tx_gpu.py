@@ -38,16 +38,26 @@ def test_tx_engine_matches_reference_sender(name):
                    base_rtt_ns=meta["base_rtt"], seed=meta["seed"], lb=meta["lb"],
                    max_paths=meta["n_paths"], src=[meta["src"]], dst=[meta["dst"]],
                    chunk_pool=1 << 18, log_cap=1 << 17, cc=meta.get("cc", "none"),
-                   swift_target_ns=meta.get("swift_target_ns", 0))
+                   swift_target_ns=meta.get("swift_target_ns", 0),
+                   receiver_driven=meta.get("receiver_driven", False),
+                   initial_credit=meta.get("initial_credit", 0))
     st = eng.run([_events(z["submits"], z["acks"])], z["submits"], z["acks"], 60_000_000_000)[0]
     ref = meta["stats"]
     for k in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos", "msgs_completed"):
         assert int(st[k]) == ref[k], (k, int(st[k]), ref[k])
     got, want = eng.log_np(0), z["tx"]
     assert len(got) == len(want)
-    for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
-        bad = np.nonzero(got[f] != want[f])[0]
-        assert len(bad) == 0, (f, int(bad[0]), got[bad[0]], want[bad[0]])
+    # data transmissions in emission order; receiver-driven RTS records
+    # (chunk = 0xFFFFFFFF; the reference logs them at delivery) by time
+    rts_g, rts_w = got["chunk"] == 0xFFFFFFFF, want["chunk"] == 0xFFFFFFFF
+    assert rts_g.sum() == rts_w.sum()
+    for sel_g, sel_w, srt in ((~rts_g, ~rts_w, False), (rts_g, rts_w, True)):
+        g, w = got[sel_g], want[sel_w]
+        if srt:
+            g, w = g[np.argsort(g["t"], kind="stable")], w[np.argsort(w["t"], kind="stable")]
+        for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
+            bad = np.nonzero(g[f] != w[f])[0]
+            assert len(bad) == 0, (srt, f, int(bad[0]), g[bad[0]], w[bad[0]])
 
 
 def test_tx_engine_eight_dup_hints_one_fast_rtx():

@@ -106,6 +106,11 @@ typedef struct cn_pkt_hdr {
  * (credit bytes in sack[0]) or an RTS acknowledgement */
 #define CN_ACK_CREDIT 0x8u
 #define CN_ACK_RTS_ACK 0x10u
+/* ordered (go-back-N) reliability: a sequence-gap NACK (transport.cpp:
+ * 690-707) with nack_psn = the receiver's expected sequence in sack[0];
+ * CN_ACK_NACK_TRIM when a trimmed head-of-line packet caused it */
+#define CN_ACK_GBN 0x20u
+#define CN_ACK_NACK_TRIM 0x40u
 typedef struct cn_ack_rec {
     int32_t src;          /* ack source = receiving host   */
     int32_t dst;          /* ack destination = sender host */
@@ -160,6 +165,10 @@ typedef struct cn_rx_config {
     int32_t reduce_op;       /* CN_REDUCE_*: fuse the scatter with a ring
                                 reduction step            */
     uint32_t max_posts;      /* capacity of posted destinations (cn_rx_post)    */
+    int32_t ordered;         /* TransportConfig::reliability == ordered: the
+                                go-back-N receive filter (transport.cpp:690-717)
+                                runs first; batches then come with conn_psn
+                                (cn_rx_batch_psn) */
 } cn_rx_config;
 
 /* Reduce modes of the payload scatter: dst = dst + payload elementwise,
@@ -203,6 +212,12 @@ int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
                 uint32_t max_acks, cn_completion* d_completions,
                 uint32_t max_completions, cn_rx_result* d_result,
                 void* stream);
+/* cn_rx_batch for ordered reliability: d_psn[i] = conn_psn of packet i
+ * (Packet::conn_psn, packet.hpp:48; not part of the 64-B header record) */
+int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
+                    uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
+                    cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
+                    void* stream);
 /* Post a destination buffer for the message with caller tag `tag` (the
  * reference's per-message tag, transport.hpp:88-91): its payload is
  * scattered (or reduced, CN_REDUCE_*) into d_buf instead of the arena.

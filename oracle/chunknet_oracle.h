@@ -50,6 +50,9 @@ void orc_next_double_seq(uint64_t seed, const char* name, int64_t index, uint64_
 /* ---- receive path (transport.cpp:546-803) ----------------------------- */
 typedef struct orc_rx orc_rx;
 orc_rx* orc_rx_create(uint32_t max_payload, int carry_payload);
+/* ordered (go-back-N) reliability: psn[i] = conn_psn of packet i of every
+ * following batch (the pointer is read during orc_rx_batch) */
+void orc_rx_set_ordered(orc_rx* rx, int ordered, const uint64_t* psn);
 void orc_rx_destroy(orc_rx* rx);
 /* Processes n packets in order (payload of packet i at payload + i*stride).
  * Appends acks / completions; reassembled buffers are copied into arena at

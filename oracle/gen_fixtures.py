@@ -97,6 +97,15 @@ SCENARIOS = {
                         loss=0.01, seed=6, chunk_bytes=16384, paths=1, lb="oblivious",
                         cc="swift", receiver_driven=True, window=2),
                    [(1, 0, MiB, 3), (2, 0, MiB, 3), (3, 0, MiB, 3), (4, 0, MiB, 3)]),
+    # ordered reliability (go-back-N, transport.cpp:690-717, 966-999): one
+    # lossy connection, and a trimming incast (head-of-line trims)
+    "ordered_loss": (dict(topo="star", topo_arg=2, rate_bps=10e9, qcap_bytes=MiB, loss=0.02,
+                          seed=4, chunk_bytes=32768, paths=1, lb="oblivious", cc="cubic",
+                          ordered=True), [(0, 1, 2 * MiB, 1)]),
+    "ordered_trim": (dict(topo="star", topo_arg=4, rate_bps=100e9, qcap_bytes=64 * 1024, loss=0.0,
+                          seed=9, chunk_bytes=16384, paths=1, lb="oblivious", cc="swift",
+                          ordered=True, queue="trim", trim_depth=4, window=2),
+                     [(1, 0, MiB, 2), (2, 0, MiB, 2), (3, 0, MiB, 2)]),
     # closed loop under Swift: the DES sender runs Swift (target 3 x base
     # RTT), so its recorded acks answer exactly what a Swift sender sends
     "closed_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=400e9, qcap_bytes=MiB,
@@ -118,7 +127,10 @@ def gen(name, kw, flows):
     data, acks_des, cpl_des, st = ref.record(tmp, flows=flows, window=window, **kw)
     assert st["quiesced"] == 1, (name, st)
     assert st["bytes_ok"] == st["completions"], (name, st)
-    acks, cpls, arena = ref.rx_replay(data, st["n_hosts"], kw["chunk_bytes"])
+    psn = st.pop("psn")
+    ordered = bool(kw.get("ordered", False))
+    acks, cpls, arena = ref.rx_replay(data, st["n_hosts"], kw["chunk_bytes"], psn=psn if ordered else None,
+                                      ordered=ordered)
     assert len(cpls) == st["completions"], (name, len(cpls), st)
     conns = {(int(s), int(d)) for s, d in zip(data["src"], data["dst"])}
     if len(conns) == 1:
@@ -138,8 +150,9 @@ def gen(name, kw, flows):
         for f in range(len(flows)):
             gen_sender(name, kw, flows, acks_des, subs, cc=kw["cc"], flow=f)
     path = os.path.join(GOLDEN, f"{name}.npz")
+    extra = {"psn": psn} if ordered else {}
     np.savez_compressed(path, data=data, acks=acks, completions=cpls,
-                        meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
+                        meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8), **extra)
     print(f"{name}: pkts={len(data)} acks={len(acks)} completions={len(cpls)} "
           f"rtx={st['chunk_rtx']} fast_rtx={st['fast_rtx']} rtos={st['rtos']} "
           f"-> {os.path.getsize(path)} B")

@@ -39,6 +39,8 @@ def lib():
         L.orc_rx_create.restype = vp
         L.orc_rx_create.argtypes = [u32, i32]
         L.orc_rx_destroy.argtypes = [vp]
+        L.orc_rx_set_ordered.argtypes = [vp, i32, vp]
+        L.orc_rx_set_ordered.restype = None
         L.orc_rx_batch.argtypes = [vp, vp, vp, u64, u64, u32, vp, u64, vp, u64, vp, u64,
                                    ctypes.POINTER(RxCounts)]
         L.orc_pattern_bytes.argtypes = [u64, u64, vp]
@@ -64,18 +66,21 @@ def _ptr(a):
 class OracleRx:
     """Sequential restatement of the reference receive path."""
 
-    def __init__(self, max_payload=4032, carry_payload=True):
+    def __init__(self, max_payload=4032, carry_payload=True, ordered=False):
         self.h = lib().orc_rx_create(max_payload, 1 if carry_payload else 0)
         self.carry = carry_payload
+        self.ordered = ordered
 
     def __del__(self):
         if getattr(self, "h", None):
             lib().orc_rx_destroy(self.h)
             self.h = None
 
-    def batch(self, hdrs, payload=None, stride=4032, index_base=0, arena_bytes=None):
+    def batch(self, hdrs, payload=None, stride=4032, index_base=0, arena_bytes=None, psn=None):
         hdrs = np.ascontiguousarray(hdrs, dtype=PKT_DTYPE)
         n = len(hdrs)
+        psn_a = np.ascontiguousarray(psn if psn is not None else np.zeros(n), dtype=np.uint64)
+        lib().orc_rx_set_ordered(self.h, 1 if self.ordered else 0, _ptr(psn_a) if self.ordered else None)
         acks = np.zeros(n + 16, dtype=ACK_DTYPE)
         cpls = np.zeros(n + 16, dtype=CPL_DTYPE)
         if arena_bytes is None:

@@ -31,7 +31,7 @@ class Scenario(ctypes.Structure):
         ("rto_min", ctypes.c_int64), ("n_flows", ctypes.c_int32),
         ("window", ctypes.c_int32), ("cutoff_ns", ctypes.c_int64),
         ("queue_mode", ctypes.c_int32), ("trim_depth", ctypes.c_int32),
-        ("receiver_driven", ctypes.c_int32), ("pad_rd", ctypes.c_int32),
+        ("receiver_driven", ctypes.c_int32), ("ordered", ctypes.c_int32),
     ]
 
 
@@ -99,7 +99,7 @@ def lib():
         L.cnref_record.argtypes = [ctypes.POINTER(Scenario), ctypes.POINTER(Flow),
                                    ctypes.c_char_p, ctypes.POINTER(RecordStats)]
         L.cnref_rx_replay.argtypes = [vp, u64, i32, u32, i32, vp, u64, vp, u64, vp,
-                                      u64, ctypes.POINTER(RxOut)]
+                                      u64, ctypes.POINTER(RxOut), vp, i32]
         L.cnref_rx_replay_bench.argtypes = [vp, u64, i32, u32, i32, i32]
         L.cnref_rx_replay_bench.restype = ctypes.c_double
         L.cnref_sender_replay.argtypes = [ctypes.POINTER(Scenario), i32, i32, vp, u64, vp, u64,
@@ -129,13 +129,15 @@ def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
            link_delay_ns=1000, qcap_bytes=1 << 20, loss=0.0, seed=1,
            chunk_bytes=32768, paths=8, lb="p2_rtt", cc="cubic", cc_scope=0,
            engines=1, conn_split=0, dupack_threshold=8, rto_min=0, flows=(),
-           window=1, cutoff_ns=60_000_000_000, queue="drop_tail", trim_depth=0, receiver_driven=False):
+           window=1, cutoff_ns=60_000_000_000, queue="drop_tail", trim_depth=0, receiver_driven=False,
+           ordered=False):
     """Runs the reference DES and writes data.bin / acks_des.bin /
     completions_des.bin into outdir.  flows: [(src, dst, len, count)]."""
     sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns,
                   qcap_bytes, loss, seed, chunk_bytes, paths, LB[lb], CC[cc],
                   cc_scope, engines, conn_split, dupack_threshold, rto_min,
-                  len(flows), window, cutoff_ns, QUEUE[queue], trim_depth, 1 if receiver_driven else 0)
+                  len(flows), window, cutoff_ns, QUEUE[queue], trim_depth, 1 if receiver_driven else 0,
+                  1 if ordered else 0)
     fl = (Flow * max(1, len(flows)))(*[Flow(s, d, l, c, 0) for (s, d, l, c) in flows])
     st = RecordStats()
     os.makedirs(outdir, exist_ok=True)
@@ -143,11 +145,13 @@ def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
     if rc != 0:
         raise RuntimeError(lib().cnref_last_error().decode())
     data = np.fromfile(os.path.join(outdir, "data.bin"), dtype=PKT_DTYPE)
+    psn = np.fromfile(os.path.join(outdir, "psn.bin"), dtype=np.uint64)
     acks = np.fromfile(os.path.join(outdir, "acks_des.bin"), dtype=ACK_DTYPE)
     cpls = np.fromfile(os.path.join(outdir, "completions_des.bin"), dtype=CPL_DTYPE)
     subs = np.fromfile(os.path.join(outdir, "submits.bin"), dtype=SUBMIT_LOG_DTYPE)
     st_d = {k: getattr(st, k) for k, _ in RecordStats._fields_}
     st_d["submits"] = subs
+    st_d["psn"] = psn
     return data, acks, cpls, st_d
 
 
@@ -187,7 +191,7 @@ def sender_replay_bench(acks, submits, src, dst, threads=1, reps=1, *, topo="fat
                                            len(submits), _ptr(acks), len(acks), threads, reps)
 
 
-def rx_replay(recs, n_hosts, chunk_bytes, carry_payload=True, arena_bytes=None):
+def rx_replay(recs, n_hosts, chunk_bytes, carry_payload=True, arena_bytes=None, psn=None, ordered=False):
     """Reference receive path over recorded packets -> (acks, completions, arena)."""
     recs = np.ascontiguousarray(recs, dtype=PKT_DTYPE)
     n = len(recs)
@@ -204,7 +208,9 @@ def rx_replay(recs, n_hosts, chunk_bytes, carry_payload=True, arena_bytes=None):
     rc = lib().cnref_rx_replay(_ptr(recs), n, n_hosts, chunk_bytes,
                                1 if carry_payload else 0, _ptr(acks), max_acks,
                                _ptr(cpls), len(cpls), _ptr(arena),
-                               arena.nbytes if carry_payload else 0, ctypes.byref(out))
+                               arena.nbytes if carry_payload else 0, ctypes.byref(out),
+                               _ptr(np.ascontiguousarray(psn, dtype=np.uint64)) if psn is not None else None,
+                               1 if ordered else 0)
     if rc != 0:
         raise RuntimeError(lib().cnref_last_error().decode())
     return acks[: out.n_acks].copy(), cpls[: out.n_completions].copy(), arena[: out.arena_used]

@@ -52,6 +52,7 @@ using namespace chunknet;
 namespace {
 
 thread_local std::string g_err;
+thread_local bool g_ordered = false;  // records of an ordered-reliability run (go-back-N NACKs)
 
 // Payload generator of the reference tests (test_transport.cpp:63-71).
 std::shared_ptr<std::vector<uint8_t>> pattern(uint64_t n, uint64_t seed) {
@@ -125,6 +126,10 @@ cn_ack_rec ack_rec(const Packet& p, uint32_t idx, int64_t aux) {
     a.sack[0] = p.sack[0];
     a.sack[1] = p.sack[1];
     if (p.kind == PacketKind::credit) a.sack[0] = p.credit_bytes;
+    if (p.kind == PacketKind::nack && g_ordered) {  // sequence-gap NACK (transport.cpp:690-707)
+        a.flags |= CN_ACK_GBN | (p.nack_trim ? CN_ACK_NACK_TRIM : 0);
+        a.sack[0] = p.nack_psn;
+    }
     a.echo_tx_time = p.echo_tx_time;
     a.aux = aux;
     return a;
@@ -140,6 +145,10 @@ Packet from_ack(const cn_ack_rec& a) {
     if (a.flags & CN_ACK_NACK) {
         p.nack_csn = a.cum_csn;
         p.nack_trim = true;
+        if (a.flags & CN_ACK_GBN) {
+            p.nack_psn = a.sack[0];
+            p.nack_trim = (a.flags & CN_ACK_NACK_TRIM) != 0;
+        }
     }
     p.src = a.src;
     p.dst = a.dst;
@@ -192,7 +201,7 @@ struct cnref_scenario {
     int32_t queue_mode;  // QueueMode: 0 drop_tail, 1 trim, 2 pause
     int32_t trim_depth;  // NetParams::trim_queue_depth (0 = default)
     int32_t receiver_driven;  // TransportConfig::receiver_driven (EQDS)
-    int32_t pad_rd;
+    int32_t ordered;          // TransportConfig::reliability == ordered (go-back-N)
 };
 
 struct cnref_flow {
@@ -249,9 +258,12 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
         tc.rto_min = sc->rto_min;
         tc.carry_payload = true;
         tc.receiver_driven = sc->receiver_driven != 0;
+        if (sc->ordered) tc.reliability = TransportConfig::Reliability::ordered;
+        g_ordered = sc->ordered != 0;
         Transport tr(net, eq, tc, sc->seed);
 
         std::vector<cn_pkt_hdr> data;
+        std::vector<uint64_t> psns;
         std::vector<cn_ack_rec> acks;
         std::vector<cn_completion> cpls;
         struct SubRec { int64_t t; uint64_t len, tag; int32_t src, dst; };
@@ -259,8 +271,10 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
         net.set_trace([&](const TraceEvent& te) {
             if (std::strcmp(te.event, "deliver") != 0) return;
             const Packet& p = *te.pkt;
-            if (p.kind == PacketKind::data)
+            if (p.kind == PacketKind::data) {
                 data.push_back(to_rec(p));
+                psns.push_back(p.conn_psn);
+            }
             else if (p.kind == PacketKind::ack || p.kind == PacketKind::nack ||
                      p.kind == PacketKind::credit || p.kind == PacketKind::rts_ack)
                 acks.push_back(ack_rec(p, 0, te.t));
@@ -300,7 +314,8 @@ int cnref_record(const cnref_scenario* sc, const cnref_flow* flows,
         bool q = eq.run_until_idle(sc->cutoff_ns);
 
         std::string dir(outdir);
-        if (!write_vec(dir + "/data.bin", data) || !write_vec(dir + "/acks_des.bin", acks) ||
+        if (!write_vec(dir + "/data.bin", data) || !write_vec(dir + "/psn.bin", psns) ||
+            !write_vec(dir + "/acks_des.bin", acks) ||
             !write_vec(dir + "/completions_des.bin", cpls) || !write_vec(dir + "/submits.bin", subs_log))
             throw std::runtime_error("cannot write to " + dir);
         if (st) {
@@ -341,8 +356,10 @@ struct cnref_rx_out {
 int cnref_rx_replay(const cn_pkt_hdr* recs, uint64_t n, int n_hosts,
                     uint32_t chunk_bytes, int carry_payload, cn_ack_rec* acks,
                     uint64_t max_acks, cn_completion* cpls, uint64_t max_cpls,
-                    uint8_t* arena, uint64_t arena_bytes, cnref_rx_out* out) {
+                    uint8_t* arena, uint64_t arena_bytes, cnref_rx_out* out,
+                    const uint64_t* psn, int ordered) {
     try {
+        g_ordered = ordered != 0;
         Topology topo = build_star(std::max(2, n_hosts));
         NetParams np;
         np.rate_bps = 1e12;
@@ -353,6 +370,7 @@ int cnref_rx_replay(const cn_pkt_hdr* recs, uint64_t n, int n_hosts,
         TransportConfig tc;
         tc.chunk_bytes = chunk_bytes;
         tc.carry_payload = carry_payload != 0;
+        if (ordered) tc.reliability = TransportConfig::Reliability::ordered;
         Transport tr(net, eq, tc, 1);
 
         uint64_t na = 0, nc = 0, used = 0;
@@ -385,6 +403,7 @@ int cnref_rx_replay(const cn_pkt_hdr* recs, uint64_t n, int n_hosts,
         });
         for (uint64_t i = 0; i < n; ++i) {
             Packet p = from_rec(recs[i]);
+            if (psn) p.conn_psn = psn[i];
             if (carry_payload) {
                 auto& s = srcs[p.msg_tag ^ (p.msg_len << 40)];
                 if (!s) s = pattern(p.msg_len, p.msg_tag);
@@ -531,6 +550,8 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
         tc.dupack_threshold = sc->dupack_threshold;
         tc.rto_min = sc->rto_min;
         tc.receiver_driven = sc->receiver_driven != 0;
+        if (sc->ordered) tc.reliability = TransportConfig::Reliability::ordered;
+        g_ordered = sc->ordered != 0;
         Transport tr(net, eq, tc, sc->seed);
         if (tc.receiver_driven) tr.pacers_[dst].reset();  // the recorded credits drive the sender
         // Control packets skip the egress blackhole and reach the receiver: an

@@ -94,6 +94,13 @@ struct RxDev {
     uint32_t* c_newfl;  // [pool] batch scratch: ECN/RTX of new packets
     uint32_t* p_gen;    // [batch]
     uint8_t* p_nack;    // [batch] trimmed header that emits a NACK
+    // ordered reliability (go-back-N receive filter)
+    uint32_t ordered;
+    const uint64_t* psn;      // [batch] conn_psn of the current batch
+    uint8_t* p_gbn;           // [batch] 0 pass on, 1 drop, 2 drop with a NACK
+    uint64_t* p_gbn_psn;      // [batch] nack_psn of a NACK
+    uint64_t* gbn_expected;   // [rconn] RecvConn::expected_psn
+    uint8_t* gbn_nacked;      // [rconn] RecvConn::gap_nacked
     uint32_t* trim_list;  // [kTrimMax] trimmed headers of the batch (packet index)
     unsigned long long* tile_state;  // [ack tiles] decoupled look-back (ack order)
     unsigned long long* scan_state;  // [scan tiles] segmented look-back (prefix max)
@@ -108,6 +115,58 @@ __device__ __forceinline__ uint32_t chunk_len_of(const RxDev& d, uint64_t len, u
 }
 __device__ __forceinline__ uint32_t pkts_of(const RxDev& d, uint32_t clen) {
     return (clen + d.max_pl - 1) / d.max_pl;
+}
+
+// ------------------------------------------------------------ go-back-N
+// handle_data_ordered (transport.cpp:690-717): per receive connection, a
+// packet at the expected sequence advances it and goes on to handle_data;
+// one past it (or a trimmed one at it) is dropped with a NACK naming the
+// expected sequence, once until the gap closes; a trimmed one below it is
+// dropped; a full one below it goes on (a duplicate).  A per-connection
+// sequential scan: warp w owns the connections whose table slot is
+// congruent to w and walks the batch in arrival order, 32 packets at a time.
+__global__ void __launch_bounds__(256) k_gbn(RxDev d, const cn_pkt_hdr* __restrict__ hdrs, uint32_t n) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w0 = 0; w0 < n; w0 += 32) {
+        const uint32_t i = w0 + lane;
+        uint32_t rc = kInf;
+        if (i < n) {
+            const cn_pkt_hdr& h = hdrs[i];
+            const uint64_t rkey = (static_cast<uint64_t>(h.dst) << 32) | (static_cast<uint64_t>(h.src) << 8) |
+                                  (h.hdr >> 24);
+            bool ins = false;
+            rc = table_insert(d.rc_key, d.conn_mask, rkey, &ins);
+        }
+        for (unsigned m = __ballot_sync(0xffffffffu, rc != kInf && rc % nw == gw); m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            if (lane == j) {
+                const uint64_t p = d.psn[i];
+                const bool trimmed = (hdrs[i].flags & CN_PKT_TRIMMED) != 0;
+                uint64_t e = d.gbn_expected[rc];
+                uint8_t g = d.gbn_nacked[rc];
+                uint8_t out = 0;
+                if (p > e || (trimmed && p == e)) {
+                    out = 1;
+                    if (!g) {
+                        g = 1;
+                        out = 2;
+                        d.p_gbn_psn[i] = e;
+                    }
+                } else if (trimmed) {
+                    out = 1;
+                } else if (p == e) {
+                    ++e;
+                    g = 0;
+                }
+                d.gbn_expected[rc] = e;
+                d.gbn_nacked[rc] = g;
+                d.p_gbn[i] = out;
+            }
+            __syncwarp();
+        }
+    }
 }
 
 // ------------------------------------------------------------------ ingest
@@ -173,6 +232,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     uint32_t touch = 0;
     cn_pkt_hdr h;
     bool ok = i < n;
+    if (ok && d.ordered && d.p_gbn[i]) ok = false;  // dropped by the go-back-N filter
     if (ok) {
         h = hdrs[i];
         if (static_cast<uint32_t>(h.src) >= (1u << 24) ||
@@ -727,6 +787,7 @@ __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __re
     const uint64_t off = hdrs[i].chunk_offset;
     const uint32_t s = hdrs[i].seq_in_chunk;
     const uint32_t t = i + 1;
+    if (d.ordered && d.p_gbn[i]) return d.p_gbn[i] == 2 ? PC_NACK : 0;  // decided by k_gbn
     if (hdrs[i].flags & CN_PKT_TRIMMED) return d.p_nack[i] ? PC_NACK : 0;  // decided by k_trim
     if (g == kStale) return PC_STALE;  // transport.cpp:602-615
     if (g == kErr) return 0;
@@ -883,6 +944,12 @@ __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __re
             r.flags = (cls & PC_NACK) ? CN_ACK_NACK : CN_ACK_CUM_VALID;
             r.pkt_index = i;
             r.msg_seq = h.msg_seq;
+            if ((cls & PC_NACK) && d.ordered) {  // sequence-gap NACK (:695-707): nack_psn, no csn / seq
+                r.cum_csn = 0;
+                r.msg_seq = 0;
+                r.flags = CN_ACK_NACK | CN_ACK_GBN | ((h.flags & CN_PKT_TRIMMED) ? CN_ACK_NACK_TRIM : 0);
+                r.sack[0] = d.p_gbn_psn[i];
+            }
             *out = r;
         }
         return;
@@ -1227,7 +1294,13 @@ __global__ void k_reset(RxDev d, int full) {
     uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     uint64_t nconn = static_cast<uint64_t>(d.conn_mask) + 1, ngen = static_cast<uint64_t>(d.gen_mask) + 1;
-    for (uint64_t x = tid; x < nconn; x += stride) d.rc_key[x] = kEmpty;
+    for (uint64_t x = tid; x < nconn; x += stride) {
+        d.rc_key[x] = kEmpty;
+        if (d.ordered) {
+            d.gbn_expected[x] = 0;
+            d.gbn_nacked[x] = 0;
+        }
+    }
     for (uint64_t x = tid; x < nconn * 128; x += stride) d.rc_done[x] = 0;
     for (uint64_t x = tid; x < ngen; x += stride) {
         d.gen_key[x] = kEmpty;
@@ -1304,6 +1377,7 @@ static uint32_t pow2_at_least(uint64_t x) {
 }
 
 extern "C" void cn_rx_config_default(cn_rx_config* cfg) {
+    cfg->ordered = 0;
     cfg->chunk_bytes = 32768;
     cfg->max_payload = CN_MAX_PAYLOAD;
     cfg->max_conns = 1024;
@@ -1320,7 +1394,8 @@ static void rx_free(cn_rx* rx) {
     RxDev& d = rx->d;
     void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen, d.touched, d.c_first, d.c_seen,
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
-                    d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list,
+                    d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list, d.p_gbn, d.p_gbn_psn,
+                    d.gbn_expected, d.gbn_nacked,
                     d.tile_state, d.scan_state, d.plan_base, d.ctl, d.arena, d.post_key,
                     d.post_val, d.post_len};
     for (void* p : ptrs)
@@ -1416,6 +1491,13 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.c_newfl, cfg.chunk_pool * 4);
     ALLOC(d.p_gen, B * 4);
     ALLOC(d.p_nack, B);
+    d.ordered = cfg.ordered ? 1 : 0;
+    if (d.ordered) {
+        ALLOC(d.p_gbn, B);
+        ALLOC(d.p_gbn_psn, B * 8);
+        ALLOC(d.gbn_expected, (static_cast<uint64_t>(d.conn_mask) + 1) * 8);
+        ALLOC(d.gbn_nacked, static_cast<uint64_t>(d.conn_mask) + 1);
+    }
     ALLOC(d.trim_list, kTrimMax * 4ull);
     ALLOC(d.tile_state, rx->max_tiles * 8ull);
     ALLOC(d.scan_state, (cfg.chunk_pool / kScanThreads + ngen + 2) * 8ull);
@@ -1472,14 +1554,44 @@ extern "C" int cn_rx_reset(cn_rx* rx, void* stream) {
 extern "C" void* cn_rx_arena(cn_rx* rx) { return rx ? rx->d.arena : nullptr; }
 extern "C" int cn_rx_last_launches(const cn_rx* rx) { return rx ? rx->launches : 0; }
 
+static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
+                         uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
+                         cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
+                         void* stream);
+
 extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
                            uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks,
                            uint32_t max_acks, cn_completion* d_completions,
                            uint32_t max_completions, cn_rx_result* d_result, void* stream) {
+    if (rx && rx->d.ordered && n > 0) {
+        set_error("cn_rx_batch: ordered reliability needs conn_psn (cn_rx_batch_psn)");
+        return CN_E_INVALID;
+    }
+    return rx_batch_impl(rx, d_hdrs, nullptr, d_payload, payload_stride, n, d_acks, max_acks, d_completions,
+                         max_completions, d_result, stream);
+}
+
+extern "C" int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
+                               uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
+                               cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
+                               void* stream) {
+    if (rx && (!rx->d.ordered || (n > 0 && !d_psn))) {
+        set_error("cn_rx_batch_psn: needs a receiver created with ordered = 1 and conn_psn");
+        return CN_E_INVALID;
+    }
+    return rx_batch_impl(rx, d_hdrs, d_psn, d_payload, payload_stride, n, d_acks, max_acks, d_completions,
+                         max_completions, d_result, stream);
+}
+
+static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
+                         uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
+                         cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
+                         void* stream) {
     if (!rx || !d_result) {
         set_error("cn_rx_batch: null handle/result");
         return CN_E_INVALID;
     }
+    rx->d.psn = d_psn;
     if (n > rx->cfg.max_batch) {
         set_error("cn_rx_batch: n exceeds max_batch");
         return CN_E_CAPACITY;
@@ -1511,6 +1623,7 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
         // to the scatter as they free up (a persistent scatter grid would
         // pin half the register file for its whole duration)
         uint32_t cmax = static_cast<uint32_t>(rx->sms * rx->copy_bps);
+        if (d.ordered) k_gbn<<<4, 256, 0, s>>>(d, d_hdrs, n);  // the go-back-N filter first
         k_ingest<<<(n + kIngestThreads - 1) / kIngestThreads, kIngestThreads, 0, s>>>(d, d_hdrs, n);
         prof_mark(ev, s);
         // fork: the HBM-bound scatter runs beside the latency-bound ack path

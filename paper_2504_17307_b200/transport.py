@@ -78,8 +78,8 @@ class Transport:
                  chunk_pool=1 << 22, arena_bytes=1 << 30, max_batch=1 << 20, reduce=None,
                  max_posts=0):
         self.cfg = cfg or TransportConfig()
-        if self.cfg.reliability != "selective":
-            raise _lib.ChunknetError(-6, "device receive path implements selective mode")
+        if self.cfg.reliability not in ("selective", "ordered"):
+            raise _lib.ChunknetError(-1, "reliability is 'selective' or 'ordered'")
         if self.cfg.receiver_driven:
             raise _lib.ChunknetError(-6, "receiver-driven (EQDS) pacing is host-side")
         self.seed = seed
@@ -99,6 +99,7 @@ class Transport:
         rc.carry_payload = 1 if self.cfg.carry_payload else 0
         rc.reduce_op = self.REDUCE[reduce]
         rc.max_posts = max_posts
+        rc.ordered = 1 if self.cfg.reliability == "ordered" else 0
         self._rxcfg = rc
         with torch.cuda.device(self.device):
             h = ctypes.c_void_p()
@@ -148,28 +149,35 @@ class Transport:
         if self._cpls.numel() < need:
             self._cpls = torch.empty(need, dtype=torch.uint8, device=self.device)
 
-    def rx_batch_async(self, hdrs, payload, stride=MAX_PAYLOAD, stream=None, n=None):
+    def rx_batch_async(self, hdrs, payload, stride=MAX_PAYLOAD, stream=None, n=None, psn=None):
         """Enqueue the receive path for a batch; no host synchronisation.
         hdrs: device uint8 [n*64] (cn_pkt_hdr records, arrival order);
-        payload: device buffer, packet i's payload at i*stride."""
+        payload: device buffer, packet i's payload at i*stride; psn: device
+        uint64 conn_psn per packet (ordered reliability only)."""
         n = hdrs.numel() // 64 if n is None else n
         self._ensure(n)
         s = stream or torch.cuda.current_stream(self.device)
         pl = payload.data_ptr() if payload is not None else None
         if payload is not None and stride == 0 and not self.cfg.carry_payload:
             pl = None
+        if self.cfg.reliability == "ordered":
+            _lib.check(_lib.lib().cn_rx_batch_psn(
+                self._h, hdrs.data_ptr(), psn.data_ptr() if psn is not None else None, pl, stride, n,
+                self._acks.data_ptr(), n + 16, self._cpls.data_ptr(), n + 16, self._result.data_ptr(),
+                ctypes.c_void_p(s.cuda_stream)), "cn_rx_batch_psn")
+            return n
         _lib.check(_lib.lib().cn_rx_batch(
             self._h, hdrs.data_ptr(), pl, stride, n, self._acks.data_ptr(), n + 16,
             self._cpls.data_ptr(), n + 16, self._result.data_ptr(),
             ctypes.c_void_p(s.cuda_stream)), "cn_rx_batch")
         return n
 
-    def handle_packets(self, hdrs, payload=None, stride=MAX_PAYLOAD, stream=None):
+    def handle_packets(self, hdrs, payload=None, stride=MAX_PAYLOAD, stream=None, psn=None):
         """Batched Transport::handle_packet for data packets: runs the device
         receive path, returns the ack records in emission order, and fires
         the completion callback for every delivered message."""
         s = stream or torch.cuda.current_stream(self.device)
-        n = self.rx_batch_async(hdrs, payload, stride, s)
+        n = self.rx_batch_async(hdrs, payload, stride, s, psn=psn)
         self._pinned.copy_(self._result, non_blocking=True)
         s.synchronize()
         res = _lib.RxResult.from_buffer_copy(bytes(self._pinned.numpy()))

@@ -22,6 +22,12 @@ def golden_names():
                   and not os.path.basename(p).startswith("sender_"))
 
 
+def load_psn(name):
+    """conn_psn per data packet of an ordered-reliability golden (None otherwise)."""
+    z = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    return z["psn"] if "psn" in z.files else None
+
+
 def load_golden(name):
     z = np.load(os.path.join(GOLDEN, f"{name}.npz"))
     meta = json.loads(bytes(z["meta"]).decode())

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import golden_names, load_golden
+from conftest import golden_names, load_golden, load_psn
 from oracle import oracle as O
 from oracle.records import ACK_FIELDS, CPL_FIELDS, PKT_DTYPE, ack_equal
 
@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 
 def _transport(meta, carry=True, **kw):
     import paper_2504_17307_b200 as cn
-    cfg = cn.TransportConfig(chunk_bytes=meta["chunk_bytes"], carry_payload=carry)
+    cfg = cn.TransportConfig(chunk_bytes=meta["chunk_bytes"], carry_payload=carry,
+                             reliability="ordered" if meta.get("record", {}).get("ordered") else "selective")
     kw.setdefault("arena_bytes", 256 << 20)
     kw.setdefault("max_batch", 1 << 17)
     kw.setdefault("chunk_pool", 1 << 20)
@@ -25,6 +26,11 @@ def _dev(data, stride=4032):
     import paper_2504_17307_b200 as cn
     staging = O.fill_staging(data, stride=stride)
     return cn.to_device_records(data), torch.from_numpy(staging).cuda()
+
+
+def _psn(name, a=0, b=None):
+    p = load_psn(name)
+    return None if p is None else torch.from_numpy(np.ascontiguousarray(p[a:b]).astype(np.int64)).cuda()
 
 
 def _check_completions(tr, out, cpls_ref, index_base=0):
@@ -44,7 +50,7 @@ def test_rx_matches_reference(name):
     data, acks_ref, cpls_ref, meta = load_golden(name)
     tr = _transport(meta)
     hd, pl = _dev(data)
-    out = tr.handle_packets(hd, pl)
+    out = tr.handle_packets(hd, pl, psn=_psn(name))
     ok, bad = ack_equal(out.acks_np(), acks_ref)
     assert ok, bad
     _check_completions(tr, out, cpls_ref)
@@ -53,7 +59,7 @@ def test_rx_matches_reference(name):
 
 
 @pytest.mark.parametrize("name", ["cfg1", "concurrent_k4", "multigen_k8", "k8_4x1m", "csn_wrap", "trim_swift",
-                                  "trim_storm"])
+                                  "trim_storm", "ordered_loss", "ordered_trim"])
 @pytest.mark.parametrize("nsplit", [2, 7, 64])
 def test_rx_batch_split_invariance(name, nsplit):
     """Persistent device state: any split of the packet sequence into
@@ -65,7 +71,7 @@ def test_rx_batch_split_invariance(name, nsplit):
     acks, cpls, seen = [], [], []
     for a, b in zip(cuts[:-1], cuts[1:]):
         hd, pl = _dev(data[a:b])
-        out = tr.handle_packets(hd, pl)
+        out = tr.handle_packets(hd, pl, psn=_psn(name, a, b))
         ak = out.acks_np().copy()
         ak["pkt_index"] += np.uint32(a)
         acks.append(ak)

@@ -322,6 +322,11 @@ typedef struct cn_tx_config {
     int32_t credit_bank_quanta;   /* TransportConfig::credit_bank_quanta (4) */
     int32_t pad_rd;
     int64_t initial_credit;       /* resolved (-1 in the reference = one BDP) */
+    /* ordered reliability (go-back-N, transport.cpp:433-494, 944-999,
+     * 1144-1148): connection packet sequence, rewinds on NACK / RTO; a
+     * resend starting mid-chunk is logged with (first packet << 16) in path */
+    int32_t ordered;
+    uint32_t sent_order_cap;      /* per-connection sent_order entries (0 = 65536) */
 } cn_tx_config;
 typedef struct cn_tx_submit { int64_t t; uint64_t len; uint64_t tag; } cn_tx_submit;
 /* one chunk transmission (send_chunk): time, message, chunk index, path */

@@ -100,7 +100,7 @@ SCENARIOS = {
     # ordered reliability (go-back-N, transport.cpp:690-717, 966-999): one
     # lossy connection, and a trimming incast (head-of-line trims)
     "ordered_loss": (dict(topo="star", topo_arg=2, rate_bps=10e9, qcap_bytes=MiB, loss=0.02,
-                          seed=4, chunk_bytes=32768, paths=1, lb="oblivious", cc="cubic",
+                          seed=4, chunk_bytes=32768, paths=1, lb="oblivious", cc="none",
                           ordered=True), [(0, 1, 2 * MiB, 1)]),
     "ordered_trim": (dict(topo="star", topo_arg=4, rate_bps=100e9, qcap_bytes=64 * 1024, loss=0.0,
                           seed=9, chunk_bytes=16384, paths=1, lb="oblivious", cc="swift",
@@ -175,7 +175,7 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
         subs = subs[(subs["src"] == src) & (subs["dst"] == dst)]
         name = f"{name}_f{flow}"
     rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes",
-                              "paths", "lb", "receiver_driven") if k in kw}
+                              "paths", "lb", "receiver_driven", "ordered") if k in kw}
     submits = [(int(s["t"]), int(s["len"]), int(s["tag"])) for s in subs]
     tx, st = ref.sender_replay(acks_des, submits, src, dst, cc=cc, **rkw)
     rate = kw.get("rate_bps", 400e9)
@@ -187,6 +187,7 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
                 rto_min=int(st["rto_min"]), rto_max=int(st["rto_max"]), commit_ahead=commit_ahead,
                 end_time=int(st["end_time"]), stats={k: int(v) for k, v in st.items()}, cc=cc,
                 receiver_driven=bool(kw.get("receiver_driven", False)), initial_credit=int(st["bdp"]),
+                ordered=bool(kw.get("ordered", False)),
                 # the harness resolves Swift's target to 3 x base RTT (ref_harness.cpp)
                 swift_target_ns=3 * int(st["base_rtt"]) if cc == "swift" else 0)
     path = os.path.join(GOLDEN, f"sender_{name}.npz" if cc == "none" else f"sender_{cc}_{name}.npz")
@@ -201,7 +202,7 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
 # Swift: the replay must reproduce the DES sender's own transmissions
 CLOSED_SWIFT = ["closed_k8", "closed_w4", "closed_cfg2"]
 # trim-mode incasts: every connection replayed with its acks and NACKs
-TRIM_SENDER = ["trim_swift", "trim_storm", "eqds_incast", "eqds_lossy"]
+TRIM_SENDER = ["trim_swift", "trim_storm", "eqds_incast", "eqds_lossy", "ordered_loss", "ordered_trim"]
 
 # Swift (device-exact CC) goldens: the same stimulus as sender_<name>.npz
 SWIFT_SCENARIOS = ["cfg1", "cfg2_32k", "k8_4x1m", "multigen_k8", "lossy_2m", "csn_wrap"]

@@ -572,6 +572,8 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
         }
         const int64_t t0 = eq.now();  // inputs are scheduled relative to the probe's end (0 without)
         uint64_t n_out = 0;
+        uint64_t last_key = ~uint64_t{0};
+        uint32_t last_sq = 0;
         net.set_trace([&](const TraceEvent& te) {
             if (tc.receiver_driven && std::strcmp(te.event, "deliver") == 0 && te.pkt->kind == PacketKind::rts) {
                 if (n_out < max_out) {
@@ -588,13 +590,20 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
             }
             if (std::strcmp(te.event, "loss") != 0) return;
             const Packet& p = *te.pkt;
-            if (p.kind != PacketKind::data || p.seq_in_chunk != 0) return;
+            if (p.kind != PacketKind::data) return;
+            // the first packet of each send_chunk call: a new (msg, chunk) or a
+            // restart of the same one (a go-back-N resend may start mid-chunk)
+            const uint64_t key = (static_cast<uint64_t>(p.msg_seq) << 32) ^ (p.chunk_offset / tc.chunk_bytes);
+            const bool first = key != last_key || p.seq_in_chunk <= last_sq;
+            last_key = key;
+            last_sq = p.seq_in_chunk;
+            if (!first) return;
             if (n_out < max_out) {
                 cnref_tx_rec& r = out[n_out];
                 r.t = te.t - t0;
                 r.msg_id = p.hdr.msg_id;
                 r.chunk = static_cast<uint32_t>(p.chunk_offset / tc.chunk_bytes);
-                r.path = p.path_id;
+                r.path = p.path_id | static_cast<int32_t>(p.seq_in_chunk << 16);  // + first packet sent
                 r.is_rtx = p.is_rtx ? 1 : 0;
                 r.msg_seq = p.msg_seq;
             }

@@ -59,7 +59,8 @@ class TxConfig(ctypes.Structure):
                 ("swift_target_ns", ctypes.c_int64), ("init_cwnd_pkts", ctypes.c_double),
                 ("receiver_driven", ctypes.c_int32), ("credit_quantum", ctypes.c_uint32),
                 ("credit_bank_quanta", ctypes.c_int32), ("pad_rd", ctypes.c_int32),
-                ("initial_credit", ctypes.c_int64)]
+                ("initial_credit", ctypes.c_int64), ("ordered", ctypes.c_int32),
+                ("sent_order_cap", ctypes.c_uint32)]
 
 
 class RxResult(ctypes.Structure):

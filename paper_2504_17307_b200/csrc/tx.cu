@@ -88,6 +88,8 @@ struct TxConn {
     uint32_t rts_outstanding, rts_acked, sched_seq, timer_seq, pump_seq, retry_head, retry_n, stale_n;
     int64_t retry_t[kRetryMax];
     uint32_t retry_seq[kRetryMax];
+    uint64_t next_psn, last_rewind_psn;  // ordered reliability (go-back-N)
+    uint32_t so_n, gq_head, gq_n, pad_gq;   // sent_order refs; gbn_rtxq ring
     uint32_t stale_seq[kStaleMax];  // acked-while-pending rtx queue entries: (queue seq, path)
     uint16_t stale_path[kStaleMax];
     uint32_t live_mask[4];  // message slots in use (bit = msg id)
@@ -98,7 +100,7 @@ struct TxConn {
 
 struct TxDev {
     uint32_t n_conns, cb, max_pl, dupack, avoid_prev, policy, max_inflight, log_cap, cc_algo, quantum;
-    uint32_t rd, pad_rd;
+    uint32_t rd, ordered, so_cap, pad_o;
     int64_t rto_min, rto_max, commit_ahead, swift_target, mss, cap_bytes, credit_cap, initial_credit;
     double init_cwnd, cap_pkts;
     uint64_t pool_cap;
@@ -110,6 +112,10 @@ struct TxDev {
     uint32_t* c_fl;
     int32_t* c_dup;
     uint32_t* c_q;
+    int64_t* c_psn;     // [pool] ChunkTx::psn_base (ordered)
+    uint32_t* so_ref;   // [conn][so_cap] Connection::sent_order, (msg id << 25) | chunk
+    uint32_t* gq_ref;   // [conn][so_cap] Connection::gbn_rtxq refs
+    uint64_t* gq_from;  // [conn][so_cap] ... and their resend-from sequence
     // per connection x path (SubConn, transport.hpp), persisted across runs
     int64_t* s_inflight;
     int64_t* s_deficit;
@@ -287,11 +293,32 @@ struct Tx {
         return m.len - off < d.cb ? static_cast<uint32_t>(m.len - off) : d.cb;
     }
     // send_chunk (transport.cpp:433-494) on the path the chunk is queued on
-    __device__ void send_chunk(int64_t now, uint32_t mid, const TxMsg& m, uint32_t ci, bool rtx) {
+    __device__ void send_chunk(int64_t now, uint32_t mid, const TxMsg& m, uint32_t ci, bool rtx,
+                               uint64_t from_psn = 0) {
         const uint64_t e = m.chunk_base + ci;
         const int64_t dl = now + cur_rto() * backoff;
         const int32_t path = d.c_path[e];
         const int32_t att = d.c_att[e] + 1;
+        uint32_t start = 0;  // first packet sent (a go-back-N resend may start mid-chunk, :438-447)
+        if (d.ordered) {
+            if (att == 1) {
+                const uint32_t npk = (chunk_len(m, ci) + d.max_pl - 1) / d.max_pl;
+                __syncwarp();
+                if (lane == 0) {
+                    d.c_psn[e] = static_cast<int64_t>(C->next_psn);
+                    C->next_psn += npk;
+                    if (C->so_n < d.so_cap)
+                        d.so_ref[static_cast<uint64_t>(conn) * d.so_cap + C->so_n] = (mid << 25) | ci;
+                    else
+                        atomicOr(d.status, 32u);
+                    C->so_n += 1;
+                }
+                __syncwarp();
+            } else {
+                const uint64_t base = static_cast<uint64_t>(d.c_psn[e]);
+                if (from_psn > base) start = static_cast<uint32_t>(from_psn - base);
+            }
+        }
         __syncwarp();
         if (lane == 0) {
             d.c_att[e] = att;
@@ -303,10 +330,10 @@ struct Tx {
         }
         __syncwarp();
         add_inflight(path, chunk_len(m, ci));
-        if (d.rd) credit -= chunk_len(m, ci);  // :486
+        if (d.rd) credit -= chunk_len(m, ci) - start * d.max_pl;  // the bytes actually sent (:486)
         if (rtx) ++chunk_rtx;
         else ++chunks_sent;
-        record(now, mid, ci, path, rtx || att > 1, m.seq);
+        record(now, mid, ci, path | static_cast<int32_t>(start << 16), rtx || att > 1, m.seq);
         __syncwarp();
         arm_rto(now);
     }
@@ -398,6 +425,86 @@ __device__ void drr_idle(Tx& x, uint32_t visits) {
     x.ring_idx = static_cast<uint32_t>((x.ring_idx + visits) % nr);
 }
 
+// gbn_rewind (transport.cpp:969-999): re-queue every unacked chunk whose
+// packets reach the receiver's expected sequence, in first-send order;
+// chunks wholly below it stay (or come back) in flight.
+__device__ void gbn_rewind(Tx& x, int64_t now, uint64_t expected) {
+    TxConn* C = x.C;
+    if (expected == C->last_rewind_psn) return;  // duplicate gap report
+    x.cc_on_loss(now);
+    __syncwarp();
+    if (x.lane == 0) {
+        C->last_rewind_psn = expected;
+        C->gq_head = 0;
+        C->gq_n = 0;
+    }
+    __syncwarp();
+    const uint64_t so = static_cast<uint64_t>(x.conn) * x.d.so_cap;
+    const uint32_t n = C->so_n < x.d.so_cap ? C->so_n : x.d.so_cap;
+    for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+        const uint32_t k = k0 + x.lane;
+        int act = 0;  // 1: back in flight, 2: re-queue
+        uint32_t ref = 0, len = 0;
+        uint64_t from = 0;
+        uint64_t e = 0;
+        if (k < n) {
+            ref = x.d.so_ref[so + k];
+            const uint32_t mid = ref >> 25, ci = ref & ((1u << 25) - 1);
+            const TxMsg m = load_msg(C, mid);  // the slot's current message (:978-980)
+            if (m.live && ci < m.nchunks) {
+                e = m.chunk_base + ci;
+                const uint32_t fl = x.d.c_fl[e];
+                if ((fl & TF_SENT) && !(fl & TF_ACKED)) {
+                    len = x.chunk_len(m, ci);
+                    const uint64_t base = static_cast<uint64_t>(x.d.c_psn[e]);
+                    const uint64_t end = base + (len + x.d.max_pl - 1) / x.d.max_pl;
+                    if (end <= expected) {
+                        act = (fl & TF_RTXP) ? 1 : 0;
+                    } else {
+                        act = (fl & TF_RTXP) ? 3 : 2;  // 3: already pending, just re-queued
+                        from = base > expected ? base : expected;
+                    }
+                }
+            }
+        }
+        for (unsigned b = __ballot_sync(0xffffffffu, act != 0); b; b &= b - 1) {  // in order
+            const int j = __ffs(b) - 1;
+            const int aj = __shfl_sync(0xffffffffu, act, j);
+            const uint32_t lj = __shfl_sync(0xffffffffu, len, j);
+            const uint64_t ej = __shfl_sync(0xffffffffu, e, j);
+            if (aj == 1) {  // delivered but unacked: in flight again
+                __syncwarp();
+                if (x.lane == 0) x.d.c_fl[ej] &= ~TF_RTXP;
+                __syncwarp();
+                x.add_inflight(0, lj);
+            } else {
+                if (aj == 2) {
+                    __syncwarp();
+                    if (x.lane == 0) x.d.c_fl[ej] |= TF_RTXP;
+                    __syncwarp();
+                    x.add_inflight(0, -static_cast<int64_t>(lj));
+                }
+                const uint32_t rj = __shfl_sync(0xffffffffu, ref, j);
+                const uint64_t fj = __shfl_sync(0xffffffffu, from, j);
+                __syncwarp();
+                if (x.lane == 0) {
+                    x.d.c_dup[ej] = 0;
+                    const uint32_t q = (C->gq_head + C->gq_n) % x.d.so_cap;
+                    x.d.gq_ref[so + q] = rj;
+                    x.d.gq_from[so + q] = fj;
+                    C->gq_n += 1;
+                }
+                __syncwarp();
+            }
+        }
+    }
+    if (!x.pump_pending) {  // schedule_pump (:998)
+        x.pump_pending = 1;
+        x.pump_at = now;
+        x.pump_seq = ++x.sched_seq;
+    }
+}
+
 // Index of the stale retransmission-queue entry of path p with the smallest
 // queue seq, or -1.
 __device__ int stale_front(const Tx& x, int p) {
@@ -420,8 +527,27 @@ __device__ int stale_front(const Tx& x, int p) {
 // deficit round robin over the ring, every send gated by can_send.
 __device__ uint32_t egress(Tx& x, int64_t now) {
     uint32_t sent = 0;
-    for (int k = 0; (x.n_rtxq || x.C->stale_n) && k < x.ring_len; ++k) {  // :333-369
+    for (int k = 0; (x.n_rtxq || x.C->stale_n || x.C->gq_n) && k < x.ring_len; ++k) {  // :333-369
         const int p = x.ring[k];
+        while (x.d.ordered && p == 0 && x.C->gq_n && x.can_send()) {  // gbn_rtxq (:336-352)
+            TxConn* C = x.C;
+            const uint64_t so = static_cast<uint64_t>(x.conn) * x.d.so_cap;
+            const uint32_t ref = x.d.gq_ref[so + C->gq_head];
+            const uint64_t from = x.d.gq_from[so + C->gq_head];
+            __syncwarp();
+            if (x.lane == 0) {
+                C->gq_head = (C->gq_head + 1) % x.d.so_cap;
+                C->gq_n -= 1;
+            }
+            __syncwarp();
+            const uint32_t mid = ref >> 25, ci = ref & ((1u << 25) - 1);
+            const TxMsg m = load_msg(C, mid);
+            if (!m.live || ci >= m.nchunks) continue;
+            const uint32_t fl = x.d.c_fl[m.chunk_base + ci];
+            if ((fl & TF_ACKED) || !(fl & TF_RTXP)) continue;
+            x.send_chunk(now, mid, m, ci, true, from);
+            ++sent;
+        }
         while ((x.rtxq_n[p] > 0 || (x.C->stale_n && stale_front(x, p) >= 0)) && x.can_send()) {
             uint32_t mid = 0, ci = 0;
             const bool live = x.rtxq_n[p] > 0 && queue_front(x, p, true, &mid, &ci);
@@ -709,8 +835,8 @@ __device__ void handle_ack(Tx& x, int64_t now, const cn_ack_rec& a) {
             return ((j < 64 ? s0 >> j : s1 >> (j - 64)) & 1ull) != 0;
         });
     }
-    // duplicate hints -> fast retransmit, ascending chunk order (:918-929)
-    if (cause >= 0) {
+    // duplicate hints -> fast retransmit, ascending chunk order (:918-929; selective only)
+    if (cause >= 0 && !x.d.ordered) {
         for (uint32_t w0 = m.base; w0 < static_cast<uint32_t>(cause); w0 += 32) {
             const uint32_t ci = w0 + x.lane;
             bool trig = false;
@@ -745,6 +871,11 @@ __device__ void handle_ack(Tx& x, int64_t now, const cn_ack_rec& a) {
 // handle_nack (:944-965), selective mode: a trimmed header's NACK names a
 // chunk that never arrived -- retransmit it now.
 __device__ void handle_nack(Tx& x, int64_t now, const cn_ack_rec& a) {
+    if (x.d.ordered) {  // :950-954
+        gbn_rewind(x, now, a.sack[0]);
+        pump(x, now);
+        return;
+    }
     const uint32_t mid = (a.hdr >> 17) & 0x7F;
     const TxMsg m = load_msg(x.C, mid);
     if (!m.live || m.seq != a.msg_seq) return;
@@ -802,6 +933,38 @@ __device__ void rto_fire(Tx& x) {
     ++x.rtos;
     x.backoff = x.backoff * 2 < kBackoffCap ? x.backoff * 2 : kBackoffCap;
     x.cc_on_rto(now);  // once per distinct CC -- global scope has one (:1154-1160)
+    if (x.d.ordered) {  // :1144-1148: rewind from the oldest outstanding chunk's first packet
+        uint64_t psn0 = 0;
+        bool found = false;
+        for (uint32_t q = 0; q < 4 && !found; ++q)
+            for (uint32_t lb = x.live[q]; lb && !found; lb &= lb - 1) {
+                const uint32_t mid = q * 32 + __ffs(lb) - 1;
+                const TxMsg m = load_msg(C, mid);
+                for (uint32_t w0 = m.base; w0 < m.nchunks && !found; w0 += 32) {
+                    const uint32_t ci = w0 + x.lane;
+                    bool hit = false;
+                    if (ci < m.nchunks) {
+                        const uint64_t e = m.chunk_base + ci;
+                        const uint32_t fl = x.d.c_fl[e];
+                        hit = (fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP)) && x.d.c_dead[e] == best;
+                    }
+                    const unsigned b = __ballot_sync(0xffffffffu, hit);
+                    if (b) {
+                        const uint32_t cj = w0 + __ffs(b) - 1;
+                        psn0 = static_cast<uint64_t>(x.d.c_psn[m.chunk_base + cj]);
+                        found = true;
+                    }
+                }
+            }
+        __syncwarp();
+        if (x.lane == 0) C->last_rewind_psn = ~0ull;
+        __syncwarp();
+        gbn_rewind(x, now, psn0);
+        if (x.d.rd) x.maybe_send_rts(now);
+        x.arm_rto(now);
+        pump(x, now);
+        return;
+    }
     for (uint32_t q = 0; q < 4; ++q)
         for (uint32_t lb = x.live[q]; lb; lb &= lb - 1) {
             const uint32_t mid = q * 32 + __ffs(lb) - 1;
@@ -1127,6 +1290,7 @@ __global__ void k_tx_init(TxDev d, const int32_t* src, const int32_t* dst, const
     C->w = d.init_cwnd;
     C->last_decrease = kNeverDecreased;
     C->credit = d.initial_credit;  // conn_to (:131-133)
+    C->last_rewind_psn = ~0ull;
     C->src = src ? src[c] : 0;
     C->dst = dst ? dst[c] : 0;
     C->n_paths = np ? np[c] : static_cast<int32_t>(d.s.max_paths);
@@ -1214,6 +1378,8 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
     d.cap_bytes = cfg->cap_bytes;
     d.init_cwnd = cfg->init_cwnd_pkts;
     d.rd = cfg->receiver_driven ? 1 : 0;
+    d.ordered = cfg->ordered ? 1 : 0;
+    d.so_cap = cfg->ordered ? (cfg->sent_order_cap ? cfg->sent_order_cap : 1u << 16) : 1;
     d.credit_cap = static_cast<int64_t>(cfg->credit_bank_quanta) * cfg->credit_quantum;
     d.initial_credit = cfg->initial_credit;
     // cap_pkts_ (cc.cpp:111-113)
@@ -1228,7 +1394,10 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
               cudaMalloc(&d.c_path, pool * 4) == cudaSuccess && cudaMalloc(&d.c_txt, pool * 8) == cudaSuccess &&
               cudaMalloc(&d.c_dead, pool * 8) == cudaSuccess && cudaMalloc(&d.c_att, pool * 4) == cudaSuccess &&
               cudaMalloc(&d.c_fl, pool * 4) == cudaSuccess && cudaMalloc(&d.c_dup, pool * 4) == cudaSuccess &&
-              cudaMalloc(&d.c_q, pool * 4) == cudaSuccess &&
+              cudaMalloc(&d.c_q, pool * 4) == cudaSuccess && cudaMalloc(&d.c_psn, pool * 8) == cudaSuccess &&
+              cudaMalloc(&d.so_ref, static_cast<uint64_t>(n_conns) * d.so_cap * 4) == cudaSuccess &&
+              cudaMalloc(&d.gq_ref, static_cast<uint64_t>(n_conns) * d.so_cap * 4) == cudaSuccess &&
+              cudaMalloc(&d.gq_from, static_cast<uint64_t>(n_conns) * d.so_cap * 8) == cudaSuccess &&
               cudaMalloc(&d.s_inflight, subs * 8) == cudaSuccess &&
               cudaMalloc(&d.s_deficit, subs * 8) == cudaSuccess && cudaMalloc(&d.s_txq, subs * 4) == cudaSuccess &&
               cudaMalloc(&d.s_rtxq, subs * 4) == cudaSuccess && cudaMalloc(&d.s_ring, subs * 2) == cudaSuccess &&
@@ -1276,7 +1445,8 @@ extern "C" void cn_tx_destroy(cn_tx* t) {
     if (!t) return;
     cudaDeviceSynchronize();
     TxDev& d = t->d;
-    void* ptrs[] = {d.conns,      d.c_path,    d.c_txt, d.c_dead, d.c_att,  d.c_fl,
+    void* ptrs[] = {d.c_psn, d.so_ref, d.gq_ref, d.gq_from,
+                    d.conns,      d.c_path,    d.c_txt, d.c_dead, d.c_att,  d.c_fl,
                     d.c_dup,      d.c_q,       d.s_inflight, d.s_deficit, d.s_txq, d.s_rtxq,
                     d.s_ring,     d.s_inring,  d.pool_top, d.status, t->d_logn};
     for (void* p : ptrs)

@@ -36,7 +36,7 @@ class TxEngine:
                  dupack_threshold=8, rtx_avoid_prev_path=True, stream_index0=0,
                  chunk_pool=1 << 20, log_cap=1 << 16, cc="none", swift_target_ns=0,
                  drr_quantum=32768, mss=4032, cap_bytes=0, init_cwnd_pkts=2.0, receiver_driven=False,
-                 initial_credit=0, credit_quantum=32768, credit_bank_quanta=4, device="cuda"):
+                 initial_credit=0, credit_quantum=32768, credit_bank_quanta=4, ordered=False, device="cuda"):
         L = _lib.lib()
         c = _lib.TxConfig()
         L.cn_tx_config_default(ctypes.byref(c))
@@ -51,6 +51,7 @@ class TxEngine:
         c.mss, c.cap_bytes, c.init_cwnd_pkts = mss, cap_bytes, float(init_cwnd_pkts)
         c.receiver_driven, c.initial_credit = (1 if receiver_driven else 0), initial_credit
         c.credit_quantum, c.credit_bank_quanta = credit_quantum, credit_bank_quanta
+        c.ordered = 1 if ordered else 0
         self.device = torch.device(device)
         self.n, self.log_cap = n_conns, log_cap
         arr = lambda v: (ctypes.c_int32 * n_conns)(*[int(x) for x in v]) if v is not None else None  # noqa: E731

@@ -40,7 +40,7 @@ def test_tx_engine_matches_reference_sender(name):
                    chunk_pool=1 << 18, log_cap=1 << 17, cc=meta.get("cc", "none"),
                    swift_target_ns=meta.get("swift_target_ns", 0),
                    receiver_driven=meta.get("receiver_driven", False),
-                   initial_credit=meta.get("initial_credit", 0))
+                   initial_credit=meta.get("initial_credit", 0), ordered=meta.get("ordered", False))
     st = eng.run([_events(z["submits"], z["acks"])], z["submits"], z["acks"], 60_000_000_000)[0]
     ref = meta["stats"]
     for k in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos", "msgs_completed"):

@@ -156,6 +156,8 @@ struct Tx {
     uint32_t q_seq, pump_pending;
     int64_t pump_at;  // schedule_pump (:219-230): one deferred pump per engine
     uint32_t sched_seq, timer_seq, pump_seq;  // (time, seq) order of run-scheduled events
+    uint32_t n_stale;                         // register copy of C->stale_n
+    uint32_t n_retry;                         // register copy of C->retry_n
     int64_t credit, unchunked, rtxq_bytes;    // receiver-driven state
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_completed;
     uint32_t live[4];  // live message slots, iterated in slot order
@@ -252,7 +254,7 @@ struct Tx {
         if (!d.rd || C->rts_outstanding) return;
         const int64_t pending = unchunked + committed_unsent + rtxq_bytes;  // pending_bytes (:1005-1024)
         if (pending <= 0 || credit > 0) return;
-        const bool has_rtx = n_rtxq + C->stale_n > 0;  // raw queue emptiness, stale entries included
+        const bool has_rtx = n_rtxq + n_stale > 0;  // raw queue emptiness, stale entries included
         __syncwarp();
         if (lane == 0) {
             C->rts_outstanding = 1;
@@ -268,6 +270,7 @@ struct Tx {
         }
         __syncwarp();
         ++sched_seq;
+        if (n_retry < kRetryMax) ++n_retry;
         record(now, 0, 0xFFFFFFFFu, -1, has_rtx ? 1 : 0, static_cast<uint64_t>(pending));  // the RTS
     }
     __device__ int select(int prev_path) {  // DefaultPolicy (policy.hpp:80-91)
@@ -527,7 +530,7 @@ __device__ int stale_front(const Tx& x, int p) {
 // deficit round robin over the ring, every send gated by can_send.
 __device__ uint32_t egress(Tx& x, int64_t now) {
     uint32_t sent = 0;
-    for (int k = 0; (x.n_rtxq || x.C->stale_n || x.C->gq_n) && k < x.ring_len; ++k) {  // :333-369
+    for (int k = 0; (x.n_rtxq || x.n_stale || (x.d.ordered && x.C->gq_n)) && k < x.ring_len; ++k) {  // :333-369
         const int p = x.ring[k];
         while (x.d.ordered && p == 0 && x.C->gq_n && x.can_send()) {  // gbn_rtxq (:336-352)
             TxConn* C = x.C;
@@ -548,11 +551,11 @@ __device__ uint32_t egress(Tx& x, int64_t now) {
             x.send_chunk(now, mid, m, ci, true, from);
             ++sent;
         }
-        while ((x.rtxq_n[p] > 0 || (x.C->stale_n && stale_front(x, p) >= 0)) && x.can_send()) {
+        while ((x.rtxq_n[p] > 0 || (x.n_stale && stale_front(x, p) >= 0)) && x.can_send()) {
             uint32_t mid = 0, ci = 0;
             const bool live = x.rtxq_n[p] > 0 && queue_front(x, p, true, &mid, &ci);
             const uint32_t lseq = live ? (x.d.c_q[load_msg(x.C, mid).chunk_base + ci] & ~kQRtx) : 0xFFFFFFFFu;
-            const int si = x.C->stale_n ? stale_front(x, p) : -1;
+            const int si = x.n_stale ? stale_front(x, p) : -1;
             if (si >= 0 && x.C->stale_seq[si] < lseq) {  // a stale entry at the front: popped, nothing sent
                 __syncwarp();
                 if (x.lane == 0) {
@@ -563,6 +566,7 @@ __device__ uint32_t egress(Tx& x, int64_t now) {
                     C->stale_n = last;
                 }
                 __syncwarp();
+                --x.n_stale;
                 continue;
             }
             if (!live) break;
@@ -755,6 +759,7 @@ __device__ void release(Tx& x, int64_t now, const TxMsg& m, uint32_t ci, int64_t
     if (fl & TF_RTXP) {
         --x.n_rtxq;
         x.rtxq_bytes -= len;
+        if (x.n_stale < kStaleMax) ++x.n_stale;
     } else {
         x.add_inflight(path, -static_cast<int64_t>(len));
     }
@@ -1066,6 +1071,7 @@ __device__ void rts_retry(Tx& x, int64_t now) {
         if (again) C->rts_outstanding = 0;
     }
     __syncwarp();
+    --x.n_retry;
     if (again) x.maybe_send_rts(now);
 }
 
@@ -1091,7 +1097,7 @@ __device__ void run_deferred(Tx& x, int64_t t, bool inclusive) {
         };
         consider(x.timer_armed, x.timer_at, x.timer_seq, 0);
         consider(x.pump_pending, x.pump_at, x.pump_seq, 1);
-        if (x.C->retry_n)
+        if (x.n_retry)
             consider(true, x.C->retry_t[x.C->retry_head], x.C->retry_seq[x.C->retry_head], 2);
         if (which < 0) return;
         if (which == 0) {
@@ -1181,6 +1187,8 @@ __global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(TxDev d, const uint
     x.timer_seq = C->timer_seq;
     x.pump_seq = C->pump_seq;
     x.credit = C->credit;
+    x.n_stale = C->stale_n;
+    x.n_retry = C->retry_n;
     x.unchunked = C->unchunked;
     x.rtxq_bytes = C->rtxq_bytes;
     x.pump_pending = C->pump_pending;

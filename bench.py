@@ -498,8 +498,14 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     offs = np.concatenate([[0], np.cumsum(rows_self[rank])[:-1]]) * row
     sc, rc = rows[rank] * row, rows[:, rank] * row
     cap = int(max(rows.max() * row, 16))
-    a2a = AllToAll(cap)   # dispatch
-    a2c = AllToAll(cap)   # combine (its own slots: the dispatch slots are its send buffer)
+    # pieces: about 8 per hot receiver's inbound volume (the receive path runs
+    # once per piece, so fewer, larger pieces when the incast is heavy)
+    inbound = int(rows.sum(0).max()) * row
+    pb = max(64 << 20, (inbound // 8) >> 20 << 20)
+    if os.environ.get("CN_A2A_PIECE_MB"):
+        pb = int(os.environ["CN_A2A_PIECE_MB"]) << 20
+    a2a = AllToAll(cap, piece_bytes=pb)   # dispatch
+    a2c = AllToAll(cap, piece_bytes=pb)   # combine (its own slots: the dispatch slots are its send buffer)
     coffs = [s_ * a2a.cap for s_ in range(world)]
 
     def step():
@@ -549,7 +555,8 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     a2c.close()
     moved = int(rows.sum()) * row * 2  # dispatch + combine, all ranks
     hot_in = int(rows[:, 0].sum()) * row
-    return {"config": f"{world} ranks x {tokens} tokens, hidden {hidden} bf16 ({row} B/copy), top-8 of "
+    return {"piece_bytes": pb,
+            "config": f"{world} ranks x {tokens} tokens, hidden {hidden} bf16 ({row} B/copy), top-8 of "
                       f"{32 * world} experts, rank 0 experts 10x weight (incast)",
             "ms_per_step": round(ms, 4), "nccl_ms_per_step": round(msn, 4),
             "host_enqueue_ms_per_step": round(host_ms, 4),

@@ -29,7 +29,7 @@ from .transport import MAX_PAYLOAD, Transport, TransportConfig
 
 class AllToAll:
     def __init__(self, max_bytes_per_peer, *, chunk_bytes=32768, paths=8, seed=7, group=None,
-                 piece_bytes=64 << 20, max_spins=1 << 26):
+                 piece_bytes=128 << 20, max_spins=1 << 26):
         self.group = group
         self.n = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -64,10 +64,14 @@ class AllToAll:
             if d == r:
                 continue
             self.peer[d] = {k: self._open(allh[d][k]) for k in ("stage", "hdrs", "flags")}
-        # path choices: one RngStream per peer connection
+        # path choices: one RngStream per block of 2048 chunks of each peer
+        # connection's message (the sequential Mersenne draws of one stream
+        # would otherwise sit in front of every transfer)
         from .scheduler import PathScheduler
-        self.sched = PathScheduler(n, paths, seed, base_rtt_ns=10000.0, index0=r * n)
         self.max_chunks = -(-self.cap // chunk_bytes)
+        self.blk = 2048
+        self.sp = -(-self.max_chunks // self.blk)
+        self.sched = PathScheduler(n * self.sp, paths, seed, base_rtt_ns=10000.0, index0=r * n * self.sp)
         self.paths_all = torch.empty(n * self.max_chunks, dtype=torch.int32, device=self.dev)
         self.rx = Transport(TransportConfig(chunk_bytes=chunk_bytes, paths=paths, lb="p2_rtt", carry_payload=True),
                             device=self.dev, max_conns=2 * n, max_msgs=4 * n,
@@ -78,6 +82,8 @@ class AllToAll:
             if s != r:
                 self.rx.post(s, rb[s * self.cap:(s + 1) * self.cap])
         self.lanes = [torch.cuda.Stream(self.dev) for _ in range(2)]
+        self.hdr_stream = torch.cuda.Stream(self.dev)
+        self.ev_hdrs = torch.cuda.Event()
         self.piece_bytes = max(chunk_bytes, piece_bytes // chunk_bytes * chunk_bytes)
         self.sent = [[0, 0] for _ in range(n)]   # pieces sent to each peer, per lane
         self.recvd = [[0, 0] for _ in range(n)]  # pieces consumed from each peer, per lane
@@ -144,16 +150,26 @@ class AllToAll:
         self.ev_init.record(s)
         for ln in self.lanes:
             ln.wait_event(self.ev_init)
-        # paths for every outgoing message in one launch (grouped by peer)
+        # paths and headers of every outgoing message on a side stream, beside
+        # the first transfers (headers ride with a message's first piece)
+        sh = self.hdr_stream
+        sh.wait_event(self.ev_init)
         nch = [-(-send_counts[d] // self.cb) if d != r else 0 for d in range(n)]
-        offs = [0]
-        for c in nch:
-            offs.append(offs[-1] + c)
-        po = torch.tensor(offs, dtype=torch.int32).to(self.dev, non_blocking=True)
-        self.sched.select("p2_rtt", offsets=po, out=self.paths_all, stream=self.lanes[0])
-        ev_paths = torch.cuda.Event()
-        ev_paths.record(self.lanes[0])
-        self.lanes[1].wait_event(ev_paths)
+        offs, goffs = [0], [0]
+        for d in range(n):
+            start = offs[-1]
+            for b_ in range(self.sp):
+                goffs.append(start + min(nch[d], (b_ + 1) * self.blk))
+            offs.append(start + nch[d])
+        po = torch.tensor(goffs, dtype=torch.int32).to(self.dev, non_blocking=True)
+        self.sched.select("p2_rtt", offsets=po, out=self.paths_all, stream=sh)
+        for d in range(n):
+            if d != r and send_counts[d]:
+                npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
+                oh = _PeerView(self._out_hdrs.data_ptr() + d * self.max_pkts * 64, npk * 64)
+                packetize(send_counts[d], self.cb, src=r, dst=d, conn_id=0, msg_id=1, msg_seq=1, tag=r,
+                          chunk_paths=self.paths_all[offs[d]:offs[d + 1]], out=oh, stream=sh, device=self.dev)
+        self.ev_hdrs.record(sh)
         sb = send.data_ptr()
         cs = lambda st: ctypes.c_void_p(st.cuda_stream)  # noqa: E731
         for k in range(1, n):  # staggered: r+1, r+2, ...
@@ -165,22 +181,17 @@ class AllToAll:
             for ln in range(2):
                 _lib.check(L.cn_flag_wait(self.f_freed + 16 * d + 8 * ln, None, self.sent[d][ln], self.max_spins,
                                           self.f_err, cs(self.lanes[ln])), "cn_flag_wait")
-            sp0 = self.lanes[k % 2]
             npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
-            oh = _PeerView(self._out_hdrs.data_ptr() + d * self.max_pkts * 64, npk * 64)
-            packetize(send_counts[d], self.cb, src=r, dst=d, conn_id=0, msg_id=1, msg_seq=1, tag=r,
-                      chunk_paths=self.paths_all[offs[d]:offs[d + 1]], out=oh, stream=sp0, device=self.dev)
-            ev_h = torch.cuda.Event()
-            ev_h.record(sp0)
-            self.lanes[(k + 1) % 2].wait_event(ev_h)
+            oh = self._out_hdrs.data_ptr() + d * self.max_pkts * 64
             for p, (lo, hi) in enumerate(self._pieces(send_counts[d])):
                 ln = (k + p) % 2  # consecutive pieces alternate copy lanes
                 sp = self.lanes[ln]
                 _lib.check(L.cn_copy_async(pe["stage"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
                                            cs(sp)), "cn_copy_async")
                 if p == 0:  # the message's headers ride with its first piece
-                    _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh.data_ptr(), npk * 64,
-                                               cs(sp)), "cn_copy_async")
+                    sp.wait_event(self.ev_hdrs)
+                    _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh, npk * 64, cs(sp)),
+                               "cn_copy_async")
                 self.sent[d][ln] += 1
                 _lib.check(L.cn_flag_signal(pe["flags"] + 16 * r + 8 * ln, None, self.sent[d][ln], cs(sp)),
                            "cn_flag_signal")
@@ -209,7 +220,7 @@ class AllToAll:
                 self.rx.rx_batch_async(hd, pl, 0, s, n=b - a)
                 _lib.check(L.cn_flag_signal(self.peer[src]["flags"] + 16 * n + 16 * r + 8 * ln, None,
                                             self.recvd[src][ln], cs(s)), "cn_flag_signal")  # src's freed[r][ln]
-        for ln in self.lanes:
+        for ln in self.lanes + [self.hdr_stream]:
             s.wait_stream(ln)
         return self.recv_buffer()
 

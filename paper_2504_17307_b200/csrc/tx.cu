@@ -1119,7 +1119,7 @@ __host__ __device__ inline size_t tx_smem_words(uint32_t max_paths) {
            (11 * static_cast<size_t>(max_paths) + 7) / 8;
 }
 
-__global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(TxDev d, const uint32_t* __restrict__ ev_off,
+__global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(const __grid_constant__ TxDev d, const uint32_t* __restrict__ ev_off,
                                                          const uint64_t* __restrict__ events,
                                                          const cn_tx_submit* __restrict__ submits,
                                                          const cn_ack_rec* __restrict__ acks,

@@ -56,6 +56,10 @@ struct RxCtl {
     uint32_t n_touched, epoch, tile_ticket, fin_done, status, n_copied, n_acks, n_cpls;
     uint32_t ingest_done, scan_ticket, fin_ticket, n_scan_tiles;
     uint32_t n_trim, pad_t;
+    // c_first is double-buffered by batch parity: k_finalize runs beside the
+    // scatter (which reads the batch's half), so it clears the OTHER half --
+    // the tiles the previous batch dirtied, listed in dirty[par ^ 1]
+    uint32_t par, copy_par, n_dirty[2];
 };
 
 enum : uint32_t { CF_INIT = 1, CF_COMPLETE = 2, CF_ECN = 4, CF_RTX = 8, CF_NACKED = 16 };
@@ -81,7 +85,10 @@ struct RxDev {
     unsigned long long* gen_key;
     GenState* gen;
     uint32_t* touched;
-    uint32_t* c_first;  // [pool*ppc] batch scratch
+    uint32_t* c_first;  // [2][pool*ppc] batch scratch (first arrival), half = batch parity
+    uint64_t first_half;             // pool*ppc
+    unsigned long long* dirty;       // [2][dirty_cap] finalize tiles: (first chunk << 9) | count
+    uint32_t dirty_cap;
     uint32_t* c_seen;   // [pool] persistent packet bitmask (ChunkRx::pkts_seen)
     uint32_t* c_flags;  // [pool] persistent CF_*
     int64_t* c_txt;     // [pool] persistent ChunkRx::tx_time
@@ -108,6 +115,10 @@ struct RxDev {
     RxCtl* ctl;
     uint8_t* arena;
 };
+
+__device__ __forceinline__ uint32_t* first_of(const RxDev& d, uint32_t par) {
+    return d.c_first + (par ? d.first_half : 0);
+}
 
 __device__ __forceinline__ uint32_t chunk_len_of(const RxDev& d, uint64_t len, uint64_t c) {
     uint64_t rem = len - c * d.cb;
@@ -220,8 +231,10 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const uint32_t epoch = d.ctl->epoch;
+    const uint32_t par = d.ctl->par;
     const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
     if (i < tiles) d.tile_state[i] = 0;
+    if (i == 0) d.ctl->copy_par = par;  // k_copy's half (k_finalize flips par beside it)
     for (int k = threadIdx.x; k < kIngMap; k += kIngestThreads) {
         m_key[k] = kMapEmpty;
         m_touch[k] = 0;
@@ -399,7 +412,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 if (k < kTrimMax) d.trim_list[k] = i;
                 else status |= CN_RXF_CAPACITY;
             } else if (!(fl & CF_COMPLETE) && !((d.c_seen[e] >> s) & 1u)) {
-                atomicMin(&d.c_first[e * d.ppc + s], t);
+                atomicMin(&first_of(d, par)[e * d.ppc + s], t);
             }
             if (!(fl & CF_INIT)) atomicMin(&d.c_init[e], t);
             touch = static_cast<uint32_t>(c) + 1;
@@ -527,6 +540,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
     const uint32_t ppc = d.ppc;
+    const uint32_t* __restrict__ cf = first_of(d, d.ctl->par);
+    uint32_t my_n = 0;             // first arrivals (n_copied) and their bytes
+    unsigned long long my_b = 0;
     const uint32_t total = plan_block(d, nt, epoch, true, s_base, wsum);
     if (blockIdx.x == 0 && threadIdx.x == 0 && d.ctl->n_touched > kPlanMax)
         atomicOr(&d.ctl->status, CN_RXF_CAPACITY);
@@ -555,14 +571,19 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
         if (c < hi) {
             const uint64_t e = base + c;
             if (!(d.c_flags[e] & CF_COMPLETE)) {
-                const uint32_t exp = pkts_of(d, chunk_len_of(d, G->len, c));
+                const uint32_t clen = chunk_len_of(d, G->len, c);
+                const uint32_t exp = pkts_of(d, clen);
                 const uint32_t seen = d.c_seen[e];
                 uint32_t newb = 0, last = 0;
                 for (uint32_t s = 0; s < exp; ++s) {
-                    uint32_t f = d.c_first[e * ppc + s];
+                    uint32_t f = cf[e * ppc + s];
                     if (f != kInf) {
                         newb |= 1u << s;
                         last = last > f ? last : f;
+                        // a first arrival: exactly the packets k_copy scatters
+                        const uint32_t rem = clen - s * d.max_pl;
+                        ++my_n;
+                        my_b += rem < d.max_pl ? rem : d.max_pl;
                     }
                     if ((seen >> s) & 1u) f = 0;
                     cpl = cpl > f ? cpl : f;
@@ -616,6 +637,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
             }
         }
         __syncthreads();
+    }
+    my_n = __reduce_add_sync(0xffffffffu, my_n);
+    for (int o = 16; o; o >>= 1) my_b += __shfl_xor_sync(0xffffffffu, my_b, o);
+    if (lane == 0 && my_n) {
+        atomicAdd(&d.ctl->n_copied, my_n);
+        atomicAdd(&d.ctl->bytes_copied, my_b);
     }
 }
 
@@ -734,15 +761,8 @@ template <int R>
 __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                               const uint8_t* __restrict__ payload, uint64_t stride,
                                               uint32_t n) {
-    __shared__ uint32_t s_cnt;
-    __shared__ unsigned long long s_bytes;
     const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        s_cnt = 0;
-        s_bytes = 0;
-    }
-    __syncthreads();
-    uint32_t my_cnt = 0, my_bytes = 0;
+    const uint32_t* __restrict__ cf = first_of(d, d.ctl->copy_par);
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
         const uint32_t g = d.p_gen[i];
@@ -753,24 +773,15 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
         const uint32_t len = hp->payload_len;
         const GenState* G = &d.gen[g];
         const uint64_t e = G->chunk_base + off / d.cb;
-        const bool fresh = !((d.c_seen[e] >> s) & 1u) && d.c_first[e * d.ppc + s] == i + 1;
+        // first arrival of a packet not seen before the batch (k_ingest
+        // marks only those); c_seen itself is folded by k_finalize beside us
+        const bool fresh = cf[e * d.ppc + s] == i + 1;
         if (!fresh) continue;
-        ++my_cnt;
-        my_bytes += len;
         if (d.carry) {
             const uint64_t moff = off + static_cast<uint64_t>(s) * d.max_pl;
             const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
             warp_scatter<R>(G->buf + moff, src, len, lane);
         }
-    }
-    if (lane == 0 && my_cnt) {
-        atomicAdd(&s_cnt, my_cnt);
-        atomicAdd(&s_bytes, static_cast<unsigned long long>(my_bytes));
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && s_cnt) {
-        atomicAdd(&d.ctl->n_copied, s_cnt);
-        atomicAdd(&d.ctl->bytes_copied, s_bytes);
     }
 }
 
@@ -891,7 +902,7 @@ __global__ void __launch_bounds__(1024) k_trim(RxDev d, const cn_pkt_hdr* __rest
             uint32_t L = 0;  // the chunk's last new packet before t in this batch
             const uint32_t exp = pkts_of(d, chunk_len_of(d, G.len, c));
             for (uint32_t q = 0; q < exp; ++q) {
-                const uint32_t f = d.c_first[e * d.ppc + q];
+                const uint32_t f = first_of(d, d.ctl->par)[e * d.ppc + q];
                 if (f < t && f > L) L = f;
             }
             const bool nacked = prev_t > L || (L == 0 && prev_t == 0 && (fl & CF_NACKED));
@@ -998,7 +1009,7 @@ __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __re
         const uint32_t fl = d.c_flags[E], cinit = d.c_init[E], seen = d.c_seen[E];
         const int64_t txt0 = d.c_txt[E];
         const int32_t path0 = d.c_path[E];
-        const uint32_t f0 = static_cast<uint32_t>(lane) < exp ? d.c_first[E * d.ppc + lane] : kInf;
+        const uint32_t f0 = static_cast<uint32_t>(lane) < exp ? first_of(d, d.ctl->par)[E * d.ppc + lane] : kInf;
         if ((fl & CF_INIT) || cinit <= t) {
             const uint32_t f = ((seen >> lane) & 1u) ? kInf : f0;
             const bool fok = f <= t;
@@ -1186,7 +1197,23 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     __shared__ uint32_t s_base[kPlanMax + 1];
     const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
     const uint32_t ppc = d.ppc;
+    const uint32_t par = d.ctl->par;
     const uint32_t total = plan_block(d, nt, 0, false, s_base, s_w);
+    // the previous batch's first-arrival half: its scatter has finished
+    // (stream order), the next batch uses it
+    {
+        uint32_t* cf1 = first_of(d, par ^ 1u);
+        const unsigned long long* dl = d.dirty + (par ^ 1u) * static_cast<uint64_t>(d.dirty_cap);
+        const uint32_t nd = d.ctl->n_dirty[par ^ 1u];
+        for (uint32_t j = blockIdx.x; j < nd; j += gridDim.x) {
+            const unsigned long long v = dl[j];
+            if (threadIdx.x < (v & 511)) {
+                const uint64_t e = (v >> 9) + threadIdx.x;
+                for (uint32_t s = 0; s < ppc; ++s) cf1[e * ppc + s] = kInf;
+            }
+        }
+    }
+    unsigned long long* dirty = d.dirty + par * static_cast<uint64_t>(d.dirty_cap);
     for (;;) {
         if (threadIdx.x == 0) {
             uint32_t tk = atomicAdd(&d.ctl->fin_ticket, 1u);
@@ -1205,7 +1232,13 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
         const uint64_t base = G->chunk_base;
         uint32_t done = 0;
-        if (threadIdx.x == 0) d.scan_state[ticket] = 0;  // re-arm the look-back state
+        if (threadIdx.x == 0) {
+            d.scan_state[ticket] = 0;  // re-arm the look-back state
+            if (ticket < d.dirty_cap) {
+                const uint32_t cnt = min(hi - (lo + ti * kScanThreads), static_cast<uint32_t>(kScanThreads));
+                dirty[ticket] = ((base + lo + ti * kScanThreads) << 9) | cnt;
+            }
+        }
         if (c < hi) {
             const uint64_t e = base + c;
             uint32_t fl = d.c_flags[e];
@@ -1224,7 +1257,6 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
                 d.c_newb[e] = 0;
                 d.c_last[e] = 0;
                 d.c_newfl[e] = 0;
-                for (uint32_t s = 0; s < ppc; ++s) d.c_first[e * ppc + s] = kInf;
             }
             if (d.c_init[e] != kInf) {
                 fl |= CF_INIT;
@@ -1270,22 +1302,25 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         res->n_acks = C->n_acks;
         res->n_completions = C->n_cpls;
         res->status = C->status;
-        res->n_copied = C->n_copied;
+        res->n_copied = C->n_copied;  // counted by k_scan
         res->bytes_copied = C->bytes_copied;
+        C->n_copied = 0;
+        C->bytes_copied = 0;
         C->pool_snap = C->pool_top;
         C->n_touched = 0;
         C->n_trim = 0;
         C->tile_ticket = 0;
         C->fin_done = 0;
         C->status = 0;
-        C->n_copied = 0;
-        C->bytes_copied = 0;
         C->n_acks = 0;
         C->n_cpls = 0;
         C->scan_ticket = 0;
         C->fin_ticket = 0;
         uint32_t ep = C->epoch + 1;
         C->epoch = ep ? ep : 1;
+        C->n_dirty[par] = min(total, d.dirty_cap);
+        C->n_dirty[par ^ 1u] = 0;
+        C->par = par ^ 1u;
     }
 }
 
@@ -1322,12 +1357,17 @@ __global__ void k_reset(RxDev d, int full) {
         d.c_last[x] = 0;
         d.c_newfl[x] = 0;
     }
-    for (uint64_t x = tid; x < top * d.ppc; x += stride) d.c_first[x] = kInf;
+    for (uint64_t x = tid; x < top * d.ppc; x += stride) {
+        d.c_first[x] = kInf;
+        d.c_first[d.first_half + x] = kInf;
+    }
     if (full)
         for (uint64_t x = tid; x < d.pool_cap / kScanThreads + ngen + 2; x += stride) d.scan_state[x] = 0;
     if (tid == 0) {
         d.ctl->pool_top = 0;
         d.ctl->arena_top = 0;
+        d.ctl->n_dirty[0] = 0;
+        d.ctl->n_dirty[1] = 0;
     }
 }
 
@@ -1392,7 +1432,7 @@ extern "C" void cn_rx_config_default(cn_rx_config* cfg) {
 
 static void rx_free(cn_rx* rx) {
     RxDev& d = rx->d;
-    void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen, d.touched, d.c_first, d.c_seen,
+    void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen, d.touched, d.c_first, d.dirty, d.c_seen,
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
                     d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list, d.p_gbn, d.p_gbn_psn,
                     d.gbn_expected, d.gbn_nacked,
@@ -1478,7 +1518,10 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.gen_key, ngen * 8ull);
     ALLOC(d.gen, ngen * sizeof(GenState));
     ALLOC(d.touched, ngen * 4ull);
-    ALLOC(d.c_first, cfg.chunk_pool * ppc * 4);
+    d.first_half = cfg.chunk_pool * ppc;
+    ALLOC(d.c_first, 2 * d.first_half * 4);
+    d.dirty_cap = static_cast<uint32_t>(cfg.chunk_pool / kScanThreads + kPlanMax + 1);
+    ALLOC(d.dirty, 2ull * d.dirty_cap * 8);
     ALLOC(d.c_seen, cfg.chunk_pool * 4);
     ALLOC(d.c_flags, cfg.chunk_pool * 4);
     ALLOC(d.c_txt, cfg.chunk_pool * 8);
@@ -1687,13 +1730,29 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         }
         prof_mark(ev, s);
         if (copy_last) copy();
+        // the fold into persistent state needs the ack path, not the scatter
+        // (it clears the other c_first half): it runs beside the scatter's tail
+        {
+            cudaLaunchConfig_t lc = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributePriority;
+            at[0].val.priority = rx->hi_prio;
+            lc.gridDim = dim3(gb);
+            lc.blockDim = dim3(kScanThreads);
+            lc.stream = s;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            CNB_CUDA(cudaLaunchKernelEx(&lc, k_finalize, d, d_hdrs, d_result));
+        }
+        prof_mark(ev, s);
         if (!ev) {
             CNB_CUDA(cudaEventRecord(rx->ev_join, cs));
             CNB_CUDA(cudaStreamWaitEvent(s, rx->ev_join, 0));
         }
+    } else {
+        k_finalize<<<gb, kScanThreads, 0, s>>>(d, d_hdrs, d_result);
+        prof_mark(ev, s);
     }
-    k_finalize<<<gb, kScanThreads, 0, s>>>(d, d_hdrs, d_result);
-    prof_mark(ev, s);
     rx->launches = n > 0 ? 6 : 1;
     CNB_CUDA(cudaGetLastError());
     return CN_OK;

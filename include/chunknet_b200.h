@@ -224,8 +224,24 @@ int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, 
  * Posts persist across batches and resets; the completion's `reserved` field
  * carries the absolute destination pointer.  Asynchronous on `stream`. */
 int cn_rx_post(cn_rx* rx, uint64_t tag, void* d_buf, uint64_t len, void* stream);
-/* Device base pointer of the reassembly arena (cn_completion::buf_offset). */
+/* Device base pointer of the reassembly arena (cn_completion::buf_offset).
+ * A delivered message's arena range stays valid until the cn_rx_batch after
+ * the one that reported its completion has finished (the reference hands the
+ * buffer to on_complete and frees it after, transport.cpp:794-803); post a
+ * destination (cn_rx_post) to keep the data. */
 void* cn_rx_arena(cn_rx* rx);
+/* Occupancy of the receiver's rings (synchronous: waits for the device).
+ * Chunk-pool entries and 512-B arena blocks are allocated per
+ * message, contiguously, and handed back when the message is delivered. */
+typedef struct cn_rx_usage {
+    uint64_t pool_live;        /* entries held by undelivered messages (+ ring padding) */
+    uint64_t pool_cap;
+    uint64_t pool_allocated;   /* entries allocated since create / reset */
+    uint64_t arena_live;       /* arena blocks (512 B) held */
+    uint64_t arena_blocks;
+    uint64_t arena_allocated;
+} cn_rx_usage;
+int cn_rx_get_usage(cn_rx* rx, cn_rx_usage* out);
 /* Number of kernel launches the last cn_rx_batch issued. */
 int cn_rx_last_launches(const cn_rx* rx);
 /* Optional per-kernel CUDA-event timing of cn_rx_batch (bench/profiling). */

@@ -69,6 +69,11 @@ class RxResult(ctypes.Structure):
                 ("bytes_copied", ctypes.c_uint64)]
 
 
+class RxUsage(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint64) for k in ("pool_live", "pool_cap", "pool_allocated", "arena_live",
+                                                "arena_blocks", "arena_allocated")]
+
+
 _lib = None
 
 
@@ -99,6 +104,7 @@ def lib():
     L.cn_rx_arena.argtypes = [vp]
     L.cn_rx_arena.restype = vp
     L.cn_rx_last_launches.argtypes = [vp]
+    L.cn_rx_get_usage.argtypes = [vp, ctypes.POINTER(RxUsage)]
     L.cn_rx_set_profiling.argtypes = [vp, i32]
     L.cn_rx_profile.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32,
                                 ctypes.POINTER(u64), i32]

@@ -47,12 +47,22 @@ struct GenState {
     uint64_t len, tag, seq, chunk_base, buf_off;  // buf_off: arena offset, ~0 if posted
     uint8_t* buf;                                  // absolute destination of the message
     unsigned long long touch;  // (epoch << 32) | (max chunk touched + 1) in that epoch
-    uint32_t nchunks, cum, n_init, rc, msg_id, epoch, deliver_t, ready;
+    uint32_t nchunks, cum, n_init, rc, msg_id, epoch, deliver_t, slot;  // slot: gen_key index
     uint32_t lo_batch, tiles_done, cum_add, pad;
 };
 
+// Ring allocator over `cap` positions (chunk-pool entries, or arena blocks
+// of chunk_bytes): monotonic head/tail counters; a message's range never
+// wraps (the end of the ring is padded and retired at once); retired
+// positions are bits that k_finalize's last block sweeps the tail over --
+// the reference frees MsgRecv state and buffer at delivery (:794-803).
+struct RingCtl {
+    unsigned long long head, tail;
+};
+
 struct RxCtl {
-    unsigned long long pool_top, arena_top, pool_snap, bytes_copied;
+    RingCtl pool, arena;
+    unsigned long long pool_snap, bytes_copied;
     uint32_t n_touched, epoch, tile_ticket, fin_done, status, n_copied, n_acks, n_cpls;
     uint32_t ingest_done, scan_ticket, fin_ticket, n_scan_tiles;
     uint32_t n_trim, pad_t;
@@ -60,6 +70,11 @@ struct RxCtl {
     // scatter (which reads the batch's half), so it clears the OTHER half --
     // the tiles the previous batch dirtied, listed in dirty[par ^ 1]
     uint32_t par, copy_par, n_dirty[2];
+    uint32_t n_aret[2];  // arena ranges of messages delivered in the batch of that parity
+    // message states: a free ring of GenState indices; the (rconn, msg_seq)
+    // table maps keys to them, tombstones are compacted by a rebuild
+    unsigned long long gfree_head, gfree_tail;
+    uint32_t n_tomb, pad_g;
 };
 
 enum : uint32_t { CF_INIT = 1, CF_COMPLETE = 2, CF_ECN = 4, CF_RTX = 8, CF_NACKED = 16 };
@@ -72,6 +87,7 @@ constexpr int kAckTile = 128;        // packets per k_acks tile / block
 constexpr int kAckWarps = 8;         // 256 threads: 4 decide warps, 8 ack builders
 constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
 constexpr int kCopyUnroll = 8;       // 16-byte vectors in flight per lane
+constexpr uint64_t kArenaUnit = 512;  // arena allocation granule (bytes)
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 
 struct RxDev {
@@ -82,13 +98,20 @@ struct RxDev {
     uint64_t pool_cap, arena_cap;
     unsigned long long* rc_key;
     unsigned long long* rc_done;  // [conns*128] completed_seq (transport.hpp:223)
-    unsigned long long* gen_key;
+    unsigned long long* gen_key;  // [ngen] (rconn << 40) | msg_seq, kEmpty, kTomb
+    uint32_t* gen_val;            // [ngen] GenState index of the key, kInf until published
+    uint32_t* gen_free;           // [ngen] free ring of GenState indices
+    unsigned long long* gen_tmp;  // [ngen] rebuild scratch: (key, index) pairs
     GenState* gen;
     uint32_t* touched;
     uint32_t* c_first;  // [2][pool*ppc] batch scratch (first arrival), half = batch parity
     uint64_t first_half;             // pool*ppc
     unsigned long long* dirty;       // [2][dirty_cap] finalize tiles: (first chunk << 9) | count
     uint32_t dirty_cap;
+    uint32_t* pool_bits;             // [pool_cap/32] retired chunk-pool positions
+    uint32_t* arena_bits;            // [arena_blocks/32] retired arena blocks
+    uint64_t arena_blocks;           // arena_cap / kArenaUnit
+    unsigned long long* aret;        // [2][kPlanMax] (first block << 31) | blocks, released a batch later
     uint32_t* c_seen;   // [pool] persistent packet bitmask (ChunkRx::pkts_seen)
     uint32_t* c_flags;  // [pool] persistent CF_*
     int64_t* c_txt;     // [pool] persistent ChunkRx::tx_time
@@ -115,6 +138,89 @@ struct RxDev {
     RxCtl* ctl;
     uint8_t* arena;
 };
+
+__device__ inline void set_bits(uint32_t* bits, uint64_t a, uint64_t n) {
+    for (uint64_t x = a; x < a + n;) {
+        const uint32_t o = static_cast<uint32_t>(x & 31);
+        const uint64_t k = n - (x - a) < 32 - o ? n - (x - a) : 32 - o;
+        const uint32_t m = (k == 32 ? ~0u : ((1u << k) - 1)) << o;
+        atomicOr(&bits[x >> 5], m);
+        x += k;
+    }
+}
+
+// One thread.  Positions [*pos, *pos + n) of the ring, or false when the
+// live span would exceed cap (the tail only moves in k_finalize).
+__device__ inline bool ring_alloc(RingCtl* r, uint64_t cap, uint32_t* bits, uint64_t n, uint64_t* pos) {
+    if (n == 0 || n > cap) return false;
+    const unsigned long long tail = ld_volatile_u64(&r->tail);
+    unsigned long long h = ld_volatile_u64(&r->head);
+    for (;;) {
+        const uint64_t p = h % cap;
+        const uint64_t start = p + n > cap ? h + (cap - p) : h;
+        if (start + n - tail > cap) return false;
+        const unsigned long long old = atomicCAS(&r->head, h, start + n);
+        if (old == h) {
+            if (start > h) set_bits(bits, p, cap - p);  // the padded end of the ring
+            *pos = start % cap;
+            return true;
+        }
+        h = old;
+    }
+}
+
+// Whole block: advance the tail over retired positions (kAdvWords words of
+// 32 per thread per pass), clearing their bits (atomically: other blocks may
+// be retiring more).
+constexpr int kAdvWords = 8;
+__device__ void ring_advance(RingCtl* r, uint64_t cap, uint32_t* bits) {
+    __shared__ unsigned long long s_stop;
+    uint64_t t = r->tail;
+    const uint64_t h = r->head;
+    while (t < h) {
+        const uint64_t p = t % cap;
+        const uint64_t lim = (cap - p < h - t ? cap - p : h - t);
+        const uint64_t end = p + lim;
+        if (threadIdx.x == 0) s_stop = ~0ull;
+        __syncthreads();
+        const uint64_t w0 = (p >> 5) + static_cast<uint64_t>(threadIdx.x) * kAdvWords;
+        uint32_t w[kAdvWords];
+#pragma unroll
+        for (int j = 0; j < kAdvWords; ++j) w[j] = (w0 + j) << 5 < end ? bits[w0 + j] : 0u;
+#pragma unroll
+        for (int j = 0; j < kAdvWords; ++j) {
+            const uint64_t pb = (w0 + j) << 5;
+            if (pb >= end) break;
+            uint32_t inv = ~w[j];
+            if (pb < p) inv &= ~0u << (p - pb);
+            if (end - pb < 32) inv |= ~0u << (end - pb);
+            if (inv) {
+                atomicMin(&s_stop, static_cast<unsigned long long>(pb + __ffs(inv) - 1));
+                break;
+            }
+        }
+        __syncthreads();
+        const uint64_t win = (p & ~31ull) + 32ull * kAdvWords * blockDim.x;
+        uint64_t stop = s_stop;
+        if (stop == ~0ull) stop = win < end ? win : end;
+        if (stop > end) stop = end;
+#pragma unroll
+        for (int j = 0; j < kAdvWords; ++j) {
+            const uint64_t pb = (w0 + j) << 5;
+            if (pb < stop && pb + 32 > p) {  // clear [max(p, pb), min(stop, pb + 32))
+                const uint64_t a = pb > p ? pb : p, b = pb + 32 < stop ? pb + 32 : stop;
+                const uint32_t m = (b - a == 32 ? ~0u : ((1u << (b - a)) - 1)) << (a - pb);
+                atomicAnd(&bits[w0 + j], ~m);
+            }
+        }
+        __syncthreads();
+        t += stop - p;
+        if (stop < end && stop < win) break;  // a live range
+        if (stop == p) break;
+    }
+    if (threadIdx.x == 0) r->tail = t;
+    __syncthreads();
+}
 
 __device__ __forceinline__ uint32_t* first_of(const RxDev& d, uint32_t par) {
     return d.c_first + (par ? d.first_half : 0);
@@ -297,19 +403,21 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         uint32_t gs = kInf, nch = 0;
         unsigned long long cbase = 0, glen = 0;
         bool gins = false;
-        gs = table_insert(d.gen_key, d.gen_mask, gkey, &gins);
-        if (gs != kInf) {
-            GenState* G = &d.gen[gs];
+        const uint32_t slot = table_insert(d.gen_key, d.gen_mask, gkey, &gins);
+        if (slot != kInf) {
+            GenState* G = nullptr;
             if (gins) {
+                // never empty: live keys <= table slots = GenStates
+                gs = d.gen_free[atomicAdd(&d.ctl->gfree_head, 1ull) & d.gen_mask];
+                G = &d.gen[gs];
                 // the unique inserter allocates the message state
                 uint64_t nc = (h.msg_len + d.cb - 1) / d.cb;
                 uint32_t st = 0;
-                unsigned long long base = 0, boff = 0;
-                if (h.msg_len == 0 || nc >= (1ull << 31)) st = CN_RXF_UNSUPPORTED;
-                if (!st) {
-                    base = atomicAdd(&d.ctl->pool_top, static_cast<unsigned long long>(nc));
-                    if (base + nc > d.pool_cap) st = CN_RXF_CAPACITY;
-                }
+                uint64_t base = 0;
+                unsigned long long boff = 0;
+                if (h.msg_len == 0 || nc >= (1ull << 31) || (d.reduce && (h.msg_len % d.elem)))
+                    st = CN_RXF_UNSUPPORTED;
+                if (!st && !ring_alloc(&d.ctl->pool, d.pool_cap, d.pool_bits, nc, &base)) st = CN_RXF_CAPACITY;
                 uint8_t* buf = nullptr;
                 if (!st && d.carry && d.post_mask) {  // a posted destination (cn_rx_post)
                     uint32_t hp = static_cast<uint32_t>(mix64(h.msg_tag)) & d.post_mask;
@@ -325,13 +433,17 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                     }
                     if (buf) boff = ~0ull;
                 }
-                if (!st && d.carry && !buf) {
-                    unsigned long long need = (h.msg_len + 15) & ~15ull;
-                    boff = atomicAdd(&d.ctl->arena_top, need);
-                    if (boff + need > d.arena_cap) st = CN_RXF_CAPACITY;
-                    buf = d.arena + boff;
+                if (!st && d.carry && !buf) {  // arena blocks of kArenaUnit bytes
+                    uint64_t ab = 0;
+                    const uint64_t nb = (h.msg_len + kArenaUnit - 1) / kArenaUnit;
+                    if (ring_alloc(&d.ctl->arena, d.arena_blocks, d.arena_bits, nb, &ab)) {
+                        boff = ab * kArenaUnit;
+                        buf = d.arena + boff;
+                    } else {
+                        st = CN_RXF_CAPACITY;
+                        set_bits(d.pool_bits, base, nc);  // give the chunk range back
+                    }
                 }
-                if (!st && d.reduce && (h.msg_len % d.elem)) st = CN_RXF_UNSUPPORTED;
                 status |= st;
                 G->len = h.msg_len;
                 G->tag = h.msg_tag;
@@ -346,19 +458,19 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 G->rc = rc;
                 G->msg_id = mid;
                 G->deliver_t = kInf;
-                __threadfence();
-                st_release(&G->ready, 1u);
+                G->slot = slot;
+                st_release(&d.gen_val[slot], gs);
             } else {
                 // wait for the inserter (resident, already past its CAS)
                 uint32_t spins = 0;
-                while (ld_acquire(&G->ready) == 0) {
+                while ((gs = ld_acquire(&d.gen_val[slot])) == kInf) {
                     __nanosleep(32);
                     if (++spins > (1u << 24)) {
-                        gs = kInf;
                         status |= CN_RXF_CAPACITY;
                         break;
                     }
                 }
+                if (gs != kInf) G = &d.gen[gs];
             }
             if (gs != kInf) {
                 nch = G->nchunks;
@@ -493,12 +605,14 @@ __device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool
                 hi = G->n_init;
                 const unsigned long long tch = G->touch;
                 if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
+            } else if (G->deliver_t != kInf) {
+                // a delivered message is retired whole: its chunk range is
+                // reset and handed back to the pool ring
+                lo = 0;
+                hi = G->nchunks;
             } else {
                 lo = G->lo_batch;
                 hi = G->n_init;
-                // a delivered message is retired whole: its chunk state is
-                // never read again (pool entries are reclaimed by reset)
-                if (G->deliver_t != kInf) hi = lo;
             }
             tl = (hi - lo + kScanThreads - 1) / kScanThreads;
         }
@@ -1214,6 +1328,13 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         }
     }
     unsigned long long* dirty = d.dirty + par * static_cast<uint64_t>(d.dirty_cap);
+    // one block moves the rings' tails over what earlier batches retired
+    // while the others fold (this batch's retirements are seen next batch):
+    // off the kernel's serial tail
+    if (blockIdx.x == gridDim.x - 1) {
+        ring_advance(&d.ctl->pool, d.pool_cap, d.pool_bits);
+        if (d.arena_blocks) ring_advance(&d.ctl->arena, d.arena_blocks, d.arena_bits);
+    }
     for (;;) {
         if (threadIdx.x == 0) {
             uint32_t tk = atomicAdd(&d.ctl->fin_ticket, 1u);
@@ -1227,7 +1348,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         const uint32_t k = s_k;
         const uint32_t g = d.touched[k];
         GenState* G = &d.gen[g];
-        const uint32_t lo = G->lo_batch, hi = G->n_init;
+        const bool retire = G->deliver_t != kInf;
+        const uint32_t lo = retire ? 0u : G->lo_batch, hi = retire ? G->nchunks : G->n_init;
         const uint32_t ti = ticket - s_base[k];
         const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
         const uint64_t base = G->chunk_base;
@@ -1238,6 +1360,26 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
                 const uint32_t cnt = min(hi - (lo + ti * kScanThreads), static_cast<uint32_t>(kScanThreads));
                 dirty[ticket] = ((base + lo + ti * kScanThreads) << 9) | cnt;
             }
+        }
+        if (retire) {
+            // initial chunk state for the next owner; this batch's c_first
+            // half is cleared through the dirty list (the scatter reads it)
+            if (c < hi) {
+                const uint64_t e = base + c;
+                d.c_seen[e] = 0;
+                d.c_flags[e] = 0;
+                d.c_txt[e] = 0;
+                d.c_path[e] = 0;
+                d.c_init[e] = kInf;
+                d.c_cpl[e] = kInf;
+                d.c_pmax[e] = kInf;
+                d.c_newb[e] = 0;
+                d.c_last[e] = 0;
+                d.c_newfl[e] = 0;
+                atomicOr(&d.pool_bits[e >> 5], 1u << (e & 31));
+            }
+            __syncthreads();
+            continue;
         }
         if (c < hi) {
             const uint64_t e = base + c;
@@ -1281,13 +1423,37 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         }
         __syncthreads();
     }
+    // ---- arena blocks of the previous batch's deliveries: the completion
+    // handler has run (the reference hands the buffer to on_complete and
+    // frees it after, :794-803)
+    {
+        const unsigned long long* al = d.aret + (par ^ 1u) * static_cast<uint64_t>(kPlanMax);
+        const uint32_t na = d.ctl->n_aret[par ^ 1u];
+        for (uint32_t j = blockIdx.x; j < na; j += gridDim.x) {
+            const unsigned long long v = al[j];
+            const uint64_t a = v >> 31, nb = v & 0x7FFFFFFF;
+            for (uint64_t w = (a >> 5) + threadIdx.x; (w << 5) < a + nb; w += blockDim.x) {
+                const uint64_t lo_ = (w << 5) > a ? (w << 5) : a, hi_ = (w << 5) + 32 < a + nb ? (w << 5) + 32 : a + nb;
+                const uint32_t m = (hi_ - lo_ == 32 ? ~0u : ((1u << (hi_ - lo_)) - 1)) << (lo_ - (w << 5));
+                atomicOr(&d.arena_bits[w], m);
+            }
+        }
+    }
     // ---- delivered messages: completed_seq (:801) and retirement
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
         const uint32_t g = d.touched[k];
         GenState* G = &d.gen[g];
         if (G->deliver_t != kInf) {
             atomicMax(&d.rc_done[G->rc * 128 + G->msg_id], static_cast<unsigned long long>(G->seq));
-            d.gen_key[g] = kTomb;
+            if (G->buf_off != ~0ull && d.carry && G->nchunks) {
+                const uint32_t j = atomicAdd(&d.ctl->n_aret[par], 1u);
+                d.aret[par * static_cast<uint64_t>(kPlanMax) + j] =
+                    ((G->buf_off / kArenaUnit) << 31) | ((G->len + kArenaUnit - 1) / kArenaUnit);
+            }
+            d.gen_key[G->slot] = kTomb;
+            d.gen_val[G->slot] = kInf;
+            d.gen_free[atomicAdd(&d.ctl->gfree_tail, 1ull) & d.gen_mask] = g;
+            atomicAdd(&d.ctl->n_tomb, 1u);
         }
     }
     __syncthreads();
@@ -1297,7 +1463,41 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         last_block = atomicAdd(&d.ctl->fin_done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last_block && threadIdx.x == 0) {
+    if (!last_block) return;
+    __threadfence();
+    // tombstones of retired generations: once they reach 1/8 of the table,
+    // rebuild it (no other kernel uses the table now: the scatter reads
+    // GenStates by index, which do not move)
+    if (d.ctl->n_tomb * 8 >= d.gen_mask + 1) {
+        __shared__ uint32_t s_live;
+        if (threadIdx.x == 0) s_live = 0;
+        __syncthreads();
+        for (uint32_t x = threadIdx.x; x <= d.gen_mask; x += blockDim.x) {
+            const unsigned long long k = d.gen_key[x];
+            if (k != kEmpty && k != kTomb) {
+                const uint32_t j = atomicAdd(&s_live, 1u);
+                d.gen_tmp[2 * j] = k;
+                d.gen_tmp[2 * j + 1] = d.gen_val[x];
+            }
+        }
+        __syncthreads();
+        for (uint32_t x = threadIdx.x; x <= d.gen_mask; x += blockDim.x) {
+            d.gen_key[x] = kEmpty;
+            d.gen_val[x] = kInf;
+        }
+        __threadfence_block();
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < s_live; j += blockDim.x) {
+            bool ins = false;
+            const uint32_t slot = table_insert(d.gen_key, d.gen_mask, d.gen_tmp[2 * j], &ins);
+            const uint32_t g = static_cast<uint32_t>(d.gen_tmp[2 * j + 1]);
+            d.gen_val[slot] = g;
+            d.gen[g].slot = slot;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) d.ctl->n_tomb = 0;
+    }
+    if (threadIdx.x == 0) {
         RxCtl* C = d.ctl;
         res->n_acks = C->n_acks;
         res->n_completions = C->n_cpls;
@@ -1306,7 +1506,6 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         res->bytes_copied = C->bytes_copied;
         C->n_copied = 0;
         C->bytes_copied = 0;
-        C->pool_snap = C->pool_top;
         C->n_touched = 0;
         C->n_trim = 0;
         C->tile_ticket = 0;
@@ -1320,7 +1519,9 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->epoch = ep ? ep : 1;
         C->n_dirty[par] = min(total, d.dirty_cap);
         C->n_dirty[par ^ 1u] = 0;
+        C->n_aret[par ^ 1u] = 0;
         C->par = par ^ 1u;
+        C->pool_snap = C->pool.head < d.pool_cap ? C->pool.head : d.pool_cap;
     }
 }
 
@@ -1339,8 +1540,9 @@ __global__ void k_reset(RxDev d, int full) {
     for (uint64_t x = tid; x < nconn * 128; x += stride) d.rc_done[x] = 0;
     for (uint64_t x = tid; x < ngen; x += stride) {
         d.gen_key[x] = kEmpty;
+        d.gen_val[x] = kInf;
+        d.gen_free[x] = static_cast<uint32_t>(x);
         d.gen[x].epoch = 0;
-        d.gen[x].ready = 0;
         d.gen[x].touch = 0;
     }
     uint64_t top = full ? d.pool_cap : d.ctl->pool_snap;
@@ -1357,6 +1559,8 @@ __global__ void k_reset(RxDev d, int full) {
         d.c_last[x] = 0;
         d.c_newfl[x] = 0;
     }
+    for (uint64_t x = tid; x < (d.pool_cap + 31) / 32; x += stride) d.pool_bits[x] = 0;
+    for (uint64_t x = tid; x < (d.arena_blocks + 31) / 32; x += stride) d.arena_bits[x] = 0;
     for (uint64_t x = tid; x < top * d.ppc; x += stride) {
         d.c_first[x] = kInf;
         d.c_first[d.first_half + x] = kInf;
@@ -1364,10 +1568,15 @@ __global__ void k_reset(RxDev d, int full) {
     if (full)
         for (uint64_t x = tid; x < d.pool_cap / kScanThreads + ngen + 2; x += stride) d.scan_state[x] = 0;
     if (tid == 0) {
-        d.ctl->pool_top = 0;
-        d.ctl->arena_top = 0;
+        d.ctl->pool.head = d.ctl->pool.tail = 0;
+        d.ctl->arena.head = d.ctl->arena.tail = 0;
         d.ctl->n_dirty[0] = 0;
         d.ctl->n_dirty[1] = 0;
+        d.ctl->n_aret[0] = 0;
+        d.ctl->n_aret[1] = 0;
+        d.ctl->gfree_head = 0;
+        d.ctl->gfree_tail = ngen;
+        d.ctl->n_tomb = 0;
     }
 }
 
@@ -1432,7 +1641,8 @@ extern "C" void cn_rx_config_default(cn_rx_config* cfg) {
 
 static void rx_free(cn_rx* rx) {
     RxDev& d = rx->d;
-    void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen, d.touched, d.c_first, d.dirty, d.c_seen,
+    void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen_val, d.gen_free, d.gen_tmp, d.gen, d.touched, d.c_first, d.dirty, d.pool_bits,
+                    d.arena_bits, d.aret, d.c_seen,
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
                     d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list, d.p_gbn, d.p_gbn_psn,
                     d.gbn_expected, d.gbn_nacked,
@@ -1517,11 +1727,18 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.rc_done, nconn * 128ull * 8);
     ALLOC(d.gen_key, ngen * 8ull);
     ALLOC(d.gen, ngen * sizeof(GenState));
+    ALLOC(d.gen_val, ngen * 4ull);
+    ALLOC(d.gen_free, ngen * 4ull);
+    ALLOC(d.gen_tmp, ngen * 16ull);
     ALLOC(d.touched, ngen * 4ull);
     d.first_half = cfg.chunk_pool * ppc;
     ALLOC(d.c_first, 2 * d.first_half * 4);
     d.dirty_cap = static_cast<uint32_t>(cfg.chunk_pool / kScanThreads + kPlanMax + 1);
     ALLOC(d.dirty, 2ull * d.dirty_cap * 8);
+    ALLOC(d.pool_bits, (cfg.chunk_pool + 31) / 32 * 4);
+    d.arena_blocks = d.arena_cap / kArenaUnit;
+    if (d.arena_blocks) ALLOC(d.arena_bits, (d.arena_blocks + 31) / 32 * 4);
+    ALLOC(d.aret, 2ull * kPlanMax * 8);
     ALLOC(d.c_seen, cfg.chunk_pool * 4);
     ALLOC(d.c_flags, cfg.chunk_pool * 4);
     ALLOC(d.c_txt, cfg.chunk_pool * 8);
@@ -1596,6 +1813,23 @@ extern "C" int cn_rx_reset(cn_rx* rx, void* stream) {
 
 extern "C" void* cn_rx_arena(cn_rx* rx) { return rx ? rx->d.arena : nullptr; }
 extern "C" int cn_rx_last_launches(const cn_rx* rx) { return rx ? rx->launches : 0; }
+
+extern "C" int cn_rx_get_usage(cn_rx* rx, cn_rx_usage* out) {
+    if (!rx || !out) {
+        set_error("cn_rx_get_usage: null argument");
+        return CN_E_INVALID;
+    }
+    RingCtl r[2];
+    CNB_CUDA(cudaDeviceSynchronize());
+    CNB_CUDA(cudaMemcpy(r, rx->d.ctl, sizeof r, cudaMemcpyDeviceToHost));  // pool, arena lead RxCtl
+    out->pool_live = r[0].head - r[0].tail;
+    out->pool_cap = rx->d.pool_cap;
+    out->pool_allocated = r[0].head;
+    out->arena_live = r[1].head - r[1].tail;
+    out->arena_blocks = rx->d.arena_blocks;
+    out->arena_allocated = r[1].head;
+    return CN_OK;
+}
 
 static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
                          uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,

@@ -233,6 +233,13 @@ class Transport:
     def last_launches(self):
         return _lib.lib().cn_rx_last_launches(self._h)
 
+    def usage(self):
+        """Ring occupancy (cn_rx_get_usage): chunk-pool entries and arena
+        blocks held by undelivered messages, capacities, totals allocated."""
+        u = _lib.RxUsage()
+        _lib.check(_lib.lib().cn_rx_get_usage(self._h, ctypes.byref(u)), "cn_rx_get_usage")
+        return {k: getattr(u, k) for k, _ in u._fields_}
+
     def arena(self):
         """Device uint8 view of the reassembly arena (cn_rx_arena)."""
         ptr = _lib.lib().cn_rx_arena(self._h)

@@ -89,6 +89,44 @@ def test_rx_batch_split_invariance(name, nsplit):
         assert (cp[f] == cpls_ref[f]).all(), f
 
 
+@pytest.mark.parametrize("name,nsplit,pool,arena_units,max_msgs", [
+    ("multigen_k8", 64, 52, 392, 2), ("concurrent_k4", 40, 300, 4464, 8), ("closed_w4", 30, 384, 6456, 4)])
+def test_rx_steady_state_reclaims(name, nsplit, pool, arena_units, max_msgs):
+    """A long-running receiver whose chunk pool, arena and generation table
+    are several times smaller than the trace's total: delivered messages
+    hand their chunk range, arena blocks and table slot back (the reference
+    frees MsgRecv state and buffer at delivery, transport.cpp:794-803), so
+    the stream runs without a capacity error and with the identical acks,
+    completions and buffers.  Sizes: the smallest rings that hold the trace
+    at this batching (a ring's tail waits for its oldest live message)."""
+    data, acks_ref, cpls_ref, meta = load_golden(name)
+    cb = meta["chunk_bytes"]
+    total = sum((int(L) + cb - 1) // cb for L in cpls_ref["len"])
+    assert total > pool and sum((int(L) + 511) // 512 for L in cpls_ref["len"]) > arena_units  # rings wrap
+    tr = _transport(meta, chunk_pool=pool, arena_bytes=arena_units * 512, max_msgs=max_msgs)
+    cuts = np.linspace(0, len(data), nsplit + 1).astype(int)
+    acks, cpls = [], []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        hd, pl = _dev(data[a:b])
+        out = tr.handle_packets(hd, pl, psn=_psn(name, a, b))
+        ak = out.acks_np().copy()
+        ak["pkt_index"] += np.uint32(a)
+        acks.append(ak)
+        cp = out.completions_np().copy()
+        cp["pkt_index"] += np.uint32(a)
+        cpls.append(cp)
+        arena = tr.arena()
+        for c in out.completions_np():
+            assert int(c["buf_offset"]) + int(c["len"]) <= arena_units * 512
+            buf = arena[int(c["buf_offset"]): int(c["buf_offset"]) + int(c["len"])].cpu().numpy()
+            assert (buf == O.pattern_bytes(int(c["len"]), int(c["tag"]))).all()
+    ok, bad = ack_equal(np.concatenate(acks), acks_ref)
+    assert ok, bad
+    cp = np.concatenate(cpls)
+    for f in CPL_FIELDS:
+        assert (cp[f] == cpls_ref[f]).all(), f
+
+
 def test_rx_no_payload_mode_same_acks():
     data, acks_ref, cpls_ref, meta = load_golden("cfg2_32k")
     tr = _transport(meta, carry=False)

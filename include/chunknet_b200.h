@@ -323,7 +323,9 @@ typedef struct cn_tx_config {
     double base_rtt_ns;           /* scoreboard prior (Network::base_rtt_ns) */
     uint64_t seed;                /* Transport seed                          */
     int64_t stream_index0;        /* connection c uses stream index0 + c     */
-    uint64_t chunk_pool;          /* chunk state entries                     */
+    uint64_t chunk_pool;          /* chunk state entries; each connection owns
+                                     chunk_pool / n_conns of them as a ring that
+                                     a finished message hands back            */
     int32_t cc_algo;              /* CN_CC_NONE (OpenLoop) | CN_CC_SWIFT     */
     uint32_t drr_quantum;         /* TransportConfig::drr_quantum (32768)    */
     int64_t mss;                  /* CcConfig::mss (4032)                    */

@@ -93,6 +93,8 @@ struct TxConn {
     uint32_t stale_seq[kStaleMax];  // acked-while-pending rtx queue entries: (queue seq, path)
     uint16_t stale_path[kStaleMax];
     uint32_t live_mask[4];  // message slots in use (bit = msg id)
+    uint64_t p_head;        // chunk ring head (monotonic); the tail is the oldest live message
+    uint64_t p_start[128];  // ring position (monotonic) of each live message's chunks
     uint8_t free_ids[128];
     uint8_t fq[128];
     TxMsg msgs[128];
@@ -103,7 +105,7 @@ struct TxDev {
     uint32_t rd, ordered, so_cap, pad_o;
     int64_t rto_min, rto_max, commit_ahead, swift_target, mss, cap_bytes, credit_cap, initial_credit;
     double init_cwnd, cap_pkts;
-    uint64_t pool_cap;
+    uint64_t pool_cap, conn_pool;  // conn_pool = pool_cap / n_conns entries per connection
     TxConn* conns;
     int32_t* c_path;
     int64_t* c_txt;
@@ -1012,13 +1014,39 @@ __device__ void submit(Tx& x, int64_t now, const cn_tx_submit& s) {
         __syncwarp();
         return;
     }
+    // the connection's share of the chunk pool is a ring: a message takes
+    // nc contiguous entries (the ring's end is skipped when too short) and
+    // frees them when it finishes (msg_finished, :831-847); the tail is the
+    // oldest live message
     const uint64_t nc = (s.len + x.d.cb - 1) / x.d.cb;
-    unsigned long long base = 0;
-    if (x.lane == 0) base = atomicAdd(x.d.pool_top, static_cast<unsigned long long>(nc));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base + nc > x.d.pool_cap) {
+    const uint64_t pc = x.d.conn_pool;
+    const uint64_t h = C->p_head;
+    uint64_t tl = h;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if ((x.live[k] >> x.lane) & 1u) {
+            const uint64_t ps = C->p_start[k * 32 + x.lane];
+            tl = ps < tl ? ps : tl;
+        }
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, tl, o);
+        tl = y < tl ? y : tl;
+    }
+    const uint64_t pp = h % pc;
+    const uint64_t start = pp + nc > pc ? h + (pc - pp) : h;
+    if (nc > pc || start + nc - tl > pc) {
         if (x.lane == 0) atomicOr(x.d.status, 4u);
         return;
+    }
+    const uint64_t base = static_cast<uint64_t>(x.conn) * pc + start % pc;
+    for (uint64_t k = x.lane; k < nc; k += 32) {  // a reused range starts unsent
+        x.d.c_fl[base + k] = 0;
+        x.d.c_q[base + k] = 0;
+    }
+    __syncwarp();
+    if (x.lane == 0) {
+        C->p_head = start + nc;
+        C->p_start[mid] = start;
     }
     TxMsg m;
     memset(&m, 0, sizeof m);
@@ -1394,6 +1422,7 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
     d.cap_pkts = cfg->cap_bytes > 0 ? static_cast<double>(cfg->cap_bytes) / static_cast<double>(cfg->mss)
                                     : __builtin_huge_val();
     d.pool_cap = cfg->chunk_pool;
+    d.conn_pool = cfg->chunk_pool / n_conns;
     d.s = *sched_dev(t->sched);
     const uint64_t subs = static_cast<uint64_t>(n_conns) * cfg->max_paths;
     int32_t *src = nullptr, *dst = nullptr, *np = nullptr;

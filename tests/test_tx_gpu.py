@@ -30,6 +30,23 @@ def _events(submits, acks):
 
 @pytest.mark.parametrize("name", NAMES)
 def test_tx_engine_matches_reference_sender(name):
+    _replay(name, 1 << 18)
+
+
+@pytest.mark.parametrize("name,pool", [("multigen_k8", 56), ("k8_4x1m", 68), ("swift_closed_w4", 350)])
+def test_tx_engine_steady_state_chunk_ring(name, pool):
+    """The connection's chunk entries form a ring that finished messages
+    hand back (msg_finished, transport.cpp:831-847): a pool several times
+    smaller than the scenario's total chunks (about the smallest that holds
+    its live set; the ring's tail is the oldest live message) gives the
+    identical transmit log."""
+    z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
+    cb = json.loads(bytes(z["meta"]).decode())["chunk_bytes"]
+    assert sum((int(s["len"]) + cb - 1) // cb for s in z["submits"]) > pool
+    _replay(name, pool)
+
+
+def _replay(name, chunk_pool):
     from paper_2504_17307_b200.sender import TxEngine
     z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
     meta = json.loads(bytes(z["meta"]).decode())
@@ -37,7 +54,7 @@ def test_tx_engine_matches_reference_sender(name):
                    rto_max=meta["rto_max"], commit_ahead=meta["commit_ahead"],
                    base_rtt_ns=meta["base_rtt"], seed=meta["seed"], lb=meta["lb"],
                    max_paths=meta["n_paths"], src=[meta["src"]], dst=[meta["dst"]],
-                   chunk_pool=1 << 18, log_cap=1 << 17, cc=meta.get("cc", "none"),
+                   chunk_pool=chunk_pool, log_cap=1 << 17, cc=meta.get("cc", "none"),
                    swift_target_ns=meta.get("swift_target_ns", 0),
                    receiver_driven=meta.get("receiver_driven", False),
                    initial_credit=meta.get("initial_credit", 0), ordered=meta.get("ordered", False))

@@ -345,7 +345,25 @@ typedef struct cn_tx_config {
      * resend starting mid-chunk is logged with (first packet << 16) in path */
     int32_t ordered;
     uint32_t sent_order_cap;      /* per-connection sent_order entries (0 = 65536) */
+    /* transport policy plug-in (TransportPolicy / set_policy_factory,
+     * policy.hpp:39-67): CN_POLICY_*; hooks in include/chunknet_policy.cuh */
+    int32_t policy;
+    int32_t pad_pol;
 } cn_tx_config;
+enum {
+    CN_POLICY_DEFAULT = 0,      /* DefaultPolicy with lb_policy / rtx_avoid_prev_path */
+    CN_POLICY_ROUND_ROBIN = 1,  /* cn_policy::RoundRobinPolicy */
+    CN_POLICY_SINGLE_PATH = 2,  /* cn_policy::SinglePathPolicy */
+    CN_POLICY_TEST_OUT_OF_RANGE = 3,
+    CN_POLICY_USER = 100        /* CnUserPolicy of a `make USER_POLICY=...` build */
+};
+/* cn_tx_status bits */
+#define CN_TX_STATUS_EMPTY_MSG 1u  /* send_message of 0 bytes (invalid_argument) */
+#define CN_TX_STATUS_CAPACITY 4u   /* chunk ring full */
+#define CN_TX_STATUS_RETRY 8u      /* RTS retry queue full */
+#define CN_TX_STATUS_STALE 16u     /* stale retransmission-queue entries overflow */
+#define CN_TX_STATUS_SENT_ORDER 32u /* go-back-N sent_order overflow */
+#define CN_TX_STATUS_POLICY 64u    /* policy contract violation (logic_error) */
 typedef struct cn_tx_submit { int64_t t; uint64_t len; uint64_t tag; } cn_tx_submit;
 /* one chunk transmission (send_chunk): time, message, chunk index, path */
 typedef struct cn_tx_rec {
@@ -470,7 +488,8 @@ typedef struct cn_transport_config {
     double base_rtt_ns;                  /* scoreboard prior */
     int64_t commit_ahead;                /* max(2 chunk, 2 quantum, BDP) (transport.cpp:37-39) */
     /* device capacities */
-    uint32_t max_conns, max_batch, log_cap, pad1;
+    uint32_t max_conns, max_batch, log_cap;
+    int32_t policy;                      /* CN_POLICY_* (set_policy_factory, transport.hpp:95) */
     uint64_t chunk_pool, arena_bytes;
 } cn_transport_config;
 typedef struct cn_stats {  /* Transport::Stats (transport.hpp:62-75) */

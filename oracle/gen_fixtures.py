@@ -164,7 +164,11 @@ SENDER_SCENARIOS = ["cfg1", "cfg2_32k", "cfg2_4k", "k8_4x1m", "multigen_k8", "lo
                     "csn_wrap"]
 
 
-def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
+POLICY_NAMES = {1: "rr", 2: "single", 3: "user"}  # harness ids (install_policy, ref_harness.cpp)
+POLICY_ENGINE_ID = {0: 0, 1: 1, 2: 2, 3: 100}     # cn_tx_config::policy (CN_POLICY_*)
+
+
+def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None, policy=0):
     """Sender-side golden: the reference sender (OpenLoop, or Swift with
     global scope) fed the DES's submissions and the acks (and NACKs) the DES
     delivered to it, at their times.  flow: one connection of a multi-flow
@@ -177,7 +181,7 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
     rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes",
                               "paths", "lb", "receiver_driven", "ordered") if k in kw}
     submits = [(int(s["t"]), int(s["len"]), int(s["tag"])) for s in subs]
-    tx, st = ref.sender_replay(acks_des, submits, src, dst, cc=cc, **rkw)
+    tx, st = ref.sender_replay(acks_des, submits, src, dst, cc=cc, policy=policy, **rkw)
     rate = kw.get("rate_bps", 400e9)
     bdp = int(round(rate * st["base_rtt"] / 8e9))
     commit_ahead = max(2 * kw["chunk_bytes"], 2 * 32768, bdp)
@@ -187,10 +191,11 @@ def gen_sender(name, kw, flows, acks_des, subs, cc="none", flow=None):
                 rto_min=int(st["rto_min"]), rto_max=int(st["rto_max"]), commit_ahead=commit_ahead,
                 end_time=int(st["end_time"]), stats={k: int(v) for k, v in st.items()}, cc=cc,
                 receiver_driven=bool(kw.get("receiver_driven", False)), initial_credit=int(st["bdp"]),
-                ordered=bool(kw.get("ordered", False)),
+                ordered=bool(kw.get("ordered", False)), policy=POLICY_ENGINE_ID[policy],
                 # the harness resolves Swift's target to 3 x base RTT (ref_harness.cpp)
                 swift_target_ns=3 * int(st["base_rtt"]) if cc == "swift" else 0)
-    path = os.path.join(GOLDEN, f"sender_{name}.npz" if cc == "none" else f"sender_{cc}_{name}.npz")
+    pre = POLICY_NAMES[policy] + "_" if policy else ""
+    path = os.path.join(GOLDEN, f"sender_{pre}{name}.npz" if cc == "none" else f"sender_{pre}{cc}_{name}.npz")
     sub_arr = np.array(submits, dtype=[("t", "<i8"), ("len", "<u8"), ("tag", "<u8")])
     np.savez_compressed(path, acks=acks_des, submits=sub_arr, tx=tx,
                         meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
@@ -213,6 +218,18 @@ def gen_sender_swift(name):
     z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
     kw, flows = SCENARIOS[name]
     gen_sender(name, kw, flows, z["acks"], z["submits"], cc="swift")
+
+
+# policy plug-ins (include/chunknet_policy.cuh; the same policies as
+# TransportPolicy subclasses in ref_harness.cpp): the stimulus of
+# sender_<name>.npz replayed under round robin / single path
+POLICY_SCENARIOS = ["cfg1", "lossy_2m", "multigen_k8", "k8_4x1m"]
+
+
+def gen_sender_policy(name, policy):
+    z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
+    kw, flows = SCENARIOS[name]
+    gen_sender(name, kw, flows, z["acks"], z["submits"], policy=policy)
 
 
 # reference experiment runs with run.trace = true (experiment.cpp:18-40): the
@@ -412,8 +429,13 @@ def gen_rng():
 
 def main(argv):
     os.makedirs(GOLDEN, exist_ok=True)
-    names = argv or list(SCENARIOS) + ["rng", "swift", "trace", "eqds"]
+    names = argv or list(SCENARIOS) + ["rng", "swift", "trace", "eqds", "policy"]
     for n in names:
+        if n == "policy":
+            for m in POLICY_SCENARIOS:
+                for pol in POLICY_NAMES:
+                    gen_sender_policy(m, pol)
+            continue
         if n == "rng":
             gen_rng()
             continue

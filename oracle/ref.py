@@ -32,6 +32,7 @@ class Scenario(ctypes.Structure):
         ("window", ctypes.c_int32), ("cutoff_ns", ctypes.c_int64),
         ("queue_mode", ctypes.c_int32), ("trim_depth", ctypes.c_int32),
         ("receiver_driven", ctypes.c_int32), ("ordered", ctypes.c_int32),
+        ("policy", ctypes.c_int32), ("pad_policy", ctypes.c_int32),
     ]
 
 
@@ -158,14 +159,19 @@ def record(outdir, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
 def sender_replay(acks, submits, src, dst, *, topo="fat_tree", topo_arg=8, rate_bps=400e9,
                   link_delay_ns=1000, qcap_bytes=1 << 20, seed=1, chunk_bytes=32768, paths=8,
                   lb="p2_rtt", cc="none", cc_scope=0, dupack_threshold=8, rto_min=0,
-                  cutoff_ns=60_000_000_000, max_out=1 << 20, receiver_driven=False, ordered=False):
+                  cutoff_ns=60_000_000_000, max_out=1 << 20, receiver_driven=False, ordered=False,
+                  policy=0):
     """Reference sender over a blackhole: submits [(t, len, tag)] and acks
     (ACK_DTYPE, aux = delivery time at the sender; also NACK / credit /
     rts_ack records) -> (tx log, stats).  Receiver-driven: RTS packets are
-    logged as records with chunk = 0xFFFFFFFF, msg_seq = demand."""
+    logged as records with chunk = 0xFFFFFFFF, msg_seq = demand.  policy:
+    0 DefaultPolicy, 1 round robin, 2 single path, 3 the example plug-in
+    (TransportPolicy subclasses installed with set_policy_factory,
+    ref_harness.cpp)."""
     sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns, qcap_bytes, 0.0,
                   seed, chunk_bytes, paths, LB[lb], CC[cc], cc_scope, 1, 0, dupack_threshold,
-                  rto_min, 0, 1, cutoff_ns, 0, 0, 1 if receiver_driven else 0, 1 if ordered else 0)
+                  rto_min, 0, 1, cutoff_ns, 0, 0, 1 if receiver_driven else 0, 1 if ordered else 0,
+                  policy, 0)
     sb = (Submit * max(1, len(submits)))(*[Submit(int(t), int(l), int(g)) for t, l, g in submits])
     acks = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
     out = np.zeros(max_out, dtype=TX_DTYPE)

@@ -65,6 +65,63 @@ std::shared_ptr<std::vector<uint8_t>> pattern(uint64_t n, uint64_t seed) {
     return v;
 }
 
+// The device engine's built-in policy plug-ins (include/chunknet_policy.cuh),
+// restated as reference TransportPolicy subclasses (policy.hpp:39-67) and
+// installed with Transport::set_policy_factory: one instance per connection.
+struct RoundRobinPolicy : TransportPolicy {
+    uint32_t cb;
+    uint64_t next = 0;
+    explicit RoundRobinPolicy(uint32_t c) : cb(c) {}
+    uint32_t on_chunk_size(uint64_t rem) override { return rem < cb ? static_cast<uint32_t>(rem) : cb; }
+    int on_select_path(const ChunkView&, const PathScoreboard& b, RngStream&) override {
+        return static_cast<int>(next++ % static_cast<uint64_t>(b.n_paths()));
+    }
+    int on_tx_rtx_chunk(const ChunkView& c, const PathScoreboard& b, RngStream&) override {
+        const int n = b.n_paths();
+        int p = static_cast<int>(next++ % static_cast<uint64_t>(n));
+        if (n > 1 && p == c.prev_path) p = (p + 1) % n;
+        return p;
+    }
+};
+struct SinglePathPolicy : TransportPolicy {
+    uint32_t cb;
+    explicit SinglePathPolicy(uint32_t c) : cb(c) {}
+    uint32_t on_chunk_size(uint64_t rem) override { return rem < cb ? static_cast<uint32_t>(rem) : cb; }
+    int on_select_path(const ChunkView& v, const PathScoreboard& b, RngStream&) override {
+        const uint64_t h = static_cast<uint64_t>(static_cast<uint32_t>(v.src)) * 2654435761ull +
+                           static_cast<uint64_t>(static_cast<uint32_t>(v.dst));
+        return static_cast<int>(h % static_cast<uint64_t>(b.n_paths()));
+    }
+};
+// paper_2504_17307_b200/csrc/policies/example_policy.cuh (the plug-in example)
+struct ExampleUserPolicy : TransportPolicy {
+    uint32_t cb;
+    explicit ExampleUserPolicy(uint32_t c) : cb(c) {}
+    uint32_t on_chunk_size(uint64_t rem) override { return rem < cb ? static_cast<uint32_t>(rem) : cb; }
+    int on_select_path(const ChunkView&, const PathScoreboard& b, RngStream& rng) override {
+        const int n = b.n_paths();
+        if (n == 1) return 0;
+        const int a = static_cast<int>(rng.next_below(static_cast<uint64_t>(n)));
+        int c = static_cast<int>(rng.next_below(static_cast<uint64_t>(n - 1)));
+        if (c >= a) ++c;
+        return b.ecn_score(c) < b.ecn_score(a) ? c : a;
+    }
+    int on_tx_rtx_chunk(const ChunkView&, const PathScoreboard& b, RngStream&) override {
+        int best = 0;
+        for (int p = 1; p < b.n_paths(); ++p)
+            if (b.rtt_score(p) < b.rtt_score(best)) best = p;
+        return best;
+    }
+};
+void install_policy(Transport& tr, int policy, uint32_t cb) {
+    if (policy == 1)
+        tr.set_policy_factory([cb](int, int) { return std::make_unique<RoundRobinPolicy>(cb); });
+    else if (policy == 2)
+        tr.set_policy_factory([cb](int, int) { return std::make_unique<SinglePathPolicy>(cb); });
+    else if (policy == 3)
+        tr.set_policy_factory([cb](int, int) { return std::make_unique<ExampleUserPolicy>(cb); });
+}
+
 cn_pkt_hdr to_rec(const Packet& p) {
     cn_pkt_hdr r;
     std::memset(&r, 0, sizeof r);
@@ -202,6 +259,8 @@ struct cnref_scenario {
     int32_t trim_depth;  // NetParams::trim_queue_depth (0 = default)
     int32_t receiver_driven;  // TransportConfig::receiver_driven (EQDS)
     int32_t ordered;          // TransportConfig::reliability == ordered (go-back-N)
+    int32_t policy;           // 0 DefaultPolicy, 1 round robin, 2 single path, 3 example plug-in
+    int32_t pad_policy;
 };
 
 struct cnref_flow {
@@ -553,6 +612,7 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
         if (sc->ordered) tc.reliability = TransportConfig::Reliability::ordered;
         g_ordered = sc->ordered != 0;
         Transport tr(net, eq, tc, sc->seed);
+        install_policy(tr, sc->policy, tc.chunk_bytes);
         if (tc.receiver_driven) tr.pacers_[dst].reset();  // the recorded credits drive the sender
         // Control packets skip the egress blackhole and reach the receiver: an
         // RTS is logged at delivery minus the (empty-fabric, constant) one-way

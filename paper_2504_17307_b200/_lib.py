@@ -60,7 +60,7 @@ class TxConfig(ctypes.Structure):
                 ("receiver_driven", ctypes.c_int32), ("credit_quantum", ctypes.c_uint32),
                 ("credit_bank_quanta", ctypes.c_int32), ("pad_rd", ctypes.c_int32),
                 ("initial_credit", ctypes.c_int64), ("ordered", ctypes.c_int32),
-                ("sent_order_cap", ctypes.c_uint32)]
+                ("sent_order_cap", ctypes.c_uint32), ("policy", ctypes.c_int32), ("pad_pol", ctypes.c_int32)]
 
 
 class RxResult(ctypes.Structure):
@@ -147,6 +147,14 @@ def lib():
     L.cn_trace_format.argtypes = [vp, u64, vp, u64, vp, vp, vp]
     L.cn_trace_from_packets.argtypes = [vp, vp, u64, i32, i32, vp, vp]
     L.cn_trace_from_acks.argtypes = [vp, u64, i32, i32, vp, vp]
+    _tx_protos(L)
+    _lib = L
+    return L
+
+
+def _tx_protos(L):
+    vp, u32 = ctypes.c_void_p, ctypes.c_uint32
+    L.cn_last_error.restype = ctypes.c_char_p
     L.cn_tx_config_default.argtypes = [ctypes.POINTER(TxConfig)]
     L.cn_tx_config_default.restype = None
     L.cn_tx_create.argtypes = [ctypes.POINTER(TxConfig), u32, vp, vp, vp, ctypes.POINTER(vp)]
@@ -154,13 +162,28 @@ def lib():
     L.cn_tx_destroy.restype = None
     L.cn_tx_run.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp, vp]
     L.cn_tx_status.argtypes = [vp, ctypes.POINTER(ctypes.c_uint)]
-    _lib = L
-    return L
 
 
-def check(status, what=""):
+USER_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libchunknet_b200_user.so")
+_user = None
+
+
+def user_lib():
+    """The sender engine built with the example policy plug-in
+    (csrc/policies/example_policy.cuh, `make -C csrc user`): cn_tx_* only."""
+    global _user
+    if _user is None:
+        if not os.path.exists(USER_LIB_PATH):
+            raise ChunknetError(-5, f"{USER_LIB_PATH} not built (make -C csrc user)")
+        L = ctypes.CDLL(USER_LIB_PATH)
+        _tx_protos(L)
+        _user = L
+    return _user
+
+
+def check(status, what="", L=None):
     if status != CN_OK:
-        raise ChunknetError(status, f"{what}: {lib().cn_last_error().decode()}")
+        raise ChunknetError(status, f"{what}: {(L or lib()).cn_last_error().decode()}")
     return status
 
 

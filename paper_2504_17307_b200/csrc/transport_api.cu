@@ -146,6 +146,7 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
     tc.cap_bytes = cfg->cap_bytes;
     tc.swift_target_ns = cfg->swift_target_ns;
     tc.init_cwnd_pkts = cfg->init_cwnd_pkts;
+    tc.policy = cfg->policy;
     int rc = cn_tx_create(&tc, cfg->max_conns, nullptr, nullptr, nullptr, &h->tx);
     if (rc != CN_OK) {
         cn_transport_destroy(h);

@@ -53,8 +53,12 @@
 #include <string>
 #include <vector>
 
+#include "chunknet_policy.cuh"
 #include "common.cuh"
 #include "rng.cuh"
+#ifdef CN_TX_USER_POLICY_HEADER
+#include CN_TX_USER_POLICY_HEADER  // defines struct CnUserPolicy (make USER_POLICY=...)
+#endif
 
 namespace cnb {
 
@@ -94,6 +98,7 @@ struct TxConn {
     uint16_t stale_path[kStaleMax];
     uint32_t live_mask[4];  // message slots in use (bit = msg id)
     uint64_t p_head;        // chunk ring head (monotonic); the tail is the oldest live message
+    uint64_t pol_state[4];  // the connection's policy instance (chunknet_policy.cuh)
     uint64_t p_start[128];  // ring position (monotonic) of each live message's chunks
     uint8_t free_ids[128];
     uint8_t fq[128];
@@ -102,7 +107,8 @@ struct TxConn {
 
 struct TxDev {
     uint32_t n_conns, cb, max_pl, dupack, avoid_prev, policy, max_inflight, log_cap, cc_algo, quantum;
-    uint32_t rd, ordered, so_cap, pad_o;
+    uint32_t rd, ordered, so_cap;
+    int32_t pol;  // CN_POLICY_*
     int64_t rto_min, rto_max, commit_ahead, swift_target, mss, cap_bytes, credit_cap, initial_credit;
     double init_cwnd, cap_pkts;
     uint64_t pool_cap, conn_pool;  // conn_pool = pool_cap / n_conns entries per connection
@@ -275,10 +281,65 @@ struct Tx {
         if (n_retry < kRetryMax) ++n_retry;
         record(now, 0, 0xFFFFFFFFu, -1, has_rtx ? 1 : 0, static_cast<uint64_t>(pending));  // the RTS
     }
-    __device__ int select(int prev_path) {  // DefaultPolicy (policy.hpp:80-91)
-        int p = select_seq(r, d.policy, n, d.policy == 2 ? ecn_s : rtt_s, lane);
-        if (prev_path >= 0 && d.avoid_prev && n > 1 && p == prev_path) p = (p + 1) % n;
-        return p;
+    // on_select_path / on_tx_rtx_chunk of the connection's policy for chunk
+    // ci of message m (view_of, transport.cpp:496-512); prev_path >= 0 for a
+    // retransmission
+    __device__ int select(int prev_path, const TxMsg& m, uint32_t mid, uint32_t ci, int attempts) {
+        if (d.pol == CN_POLICY_DEFAULT) {  // DefaultPolicy (policy.hpp:80-91)
+            int p = select_seq(r, d.policy, n, d.policy == 2 ? ecn_s : rtt_s, lane);
+            if (prev_path >= 0 && d.avoid_prev && n > 1 && p == prev_path) p = (p + 1) % n;
+            return p;
+        }
+        cn_chunk_view v;
+        v.src = C->src;
+        v.dst = C->dst;
+        v.msg_id = mid;
+        v.csn = ci & 0xFF;
+        v.msg_seq = m.seq;
+        v.msg_len = m.len;
+        v.offset = static_cast<uint64_t>(ci) * d.cb;
+        v.len = chunk_len(m, ci);
+        v.last = v.offset + v.len == m.len;
+        v.attempts = attempts;
+        v.prev_path = prev_path;
+        // a fresh chunk is counted as chunked before the hook runs (:271-283)
+        v.remaining = m.len - (prev_path >= 0 ? m.chunked : m.chunked + v.len);
+        switch (d.pol) {
+            case CN_POLICY_ROUND_ROBIN: return pick<cn_policy::RoundRobinPolicy>(v);
+            case CN_POLICY_SINGLE_PATH: return pick<cn_policy::SinglePathPolicy>(v);
+            case CN_POLICY_TEST_OUT_OF_RANGE: return pick<cn_policy::OutOfRangePolicy>(v);
+#ifdef CN_TX_USER_POLICY_HEADER
+            case CN_POLICY_USER: return pick<CnUserPolicy>(v);
+#endif
+            default: return pick<cn_policy::OutOfRangePolicy>(v);
+        }
+    }
+    struct PolicyRng {  // the connection's RngStream, warp-collective draws
+        WarpRng& r;
+        int lane;
+        __device__ uint64_t next_below(uint64_t k) { return next_below_warp(r, k, lane); }
+    };
+    template <class P>
+    __device__ int pick(const cn_chunk_view& v) {
+        cn_path_board b;
+        b.rtt_ewma = rtt_s;
+        b.ecn_ewma = ecn_s;
+        b.n_paths = n;
+        PolicyRng g{r, lane};
+        uint64_t st[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st[k] = C->pol_state[k];
+        int p = v.prev_path >= 0 ? P::rtx_path(v, b, g, st) : -1;
+        if (p == -1) p = P::select_path(v, b, g, st);
+        const bool bad = p < 0 || p >= n || P::pacing(v) != 0;
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) C->pol_state[k] = st[k];
+            if (bad) atomicOr(d.status, 64u);  // the reference's logic_error (:283-290, :528-531)
+        }
+        __syncwarp();
+        return bad ? 0 : p;
     }
     __device__ void record(int64_t t, uint32_t mid, uint32_t ci, int32_t path, int rtx, uint64_t seq) {
         if (lane == 0 && log_n < d.log_cap) {
@@ -343,12 +404,12 @@ struct Tx {
         arm_rto(now);
     }
     // queue_rtx (transport.cpp:516-542); caller checked sent && !acked && !rtx_pending
-    __device__ void queue_rtx(int64_t now, const TxMsg& m, uint32_t ci) {
+    __device__ void queue_rtx(int64_t now, const TxMsg& m, uint32_t mid, uint32_t ci) {
         const uint64_t e = m.chunk_base + ci;
         const int prev = d.c_path[e];  // attempts > 0: prev_path = ch.path (view_of, :509)
         add_inflight(prev, -static_cast<int64_t>(chunk_len(m, ci)));
         cc_on_loss(now);
-        const int p = select(prev);
+        const int p = select(prev, m, mid, ci, d.c_att[e]);
         ++q_seq;
         __syncwarp();
         if (lane == 0) {
@@ -656,7 +717,7 @@ __device__ void commit_chunks(Tx& x) {
         const uint64_t rem = m.len - m.chunked;
         const uint32_t sz = rem < x.d.cb ? static_cast<uint32_t>(rem) : x.d.cb;
         const uint32_t ci = m.nchunks;
-        const int p = x.select(-1);  // on_select_path (:281-287)
+        const int p = x.select(-1, m, mid, ci, 0);  // on_select_path (:281-287)
         ++x.q_seq;
         __syncwarp();
         if (x.lane == 0) {
@@ -859,7 +920,7 @@ __device__ void handle_ack(Tx& x, int64_t now, const cn_ack_rec& a) {
             __syncwarp();
             for (unsigned b = __ballot_sync(0xffffffffu, trig); b; b &= b - 1) {
                 ++x.fast_rtx;
-                x.queue_rtx(now, m, w0 + __ffs(b) - 1);
+                x.queue_rtx(now, m, mid, w0 + __ffs(b) - 1);
             }
         }
     }
@@ -890,7 +951,7 @@ __device__ void handle_nack(Tx& x, int64_t now, const cn_ack_rec& a) {
     if (rel >= kTxWindow || m.base + rel >= m.nchunks) return;
     const uint32_t ci = m.base + rel;
     const uint32_t fl = x.d.c_fl[m.chunk_base + ci];
-    if ((fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP))) x.queue_rtx(now, m, ci);
+    if ((fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP))) x.queue_rtx(now, m, mid, ci);
     pump(x, now);
 }
 
@@ -985,7 +1046,7 @@ __device__ void rto_fire(Tx& x) {
                     ex = (fl & TF_SENT) && !(fl & (TF_ACKED | TF_RTXP)) && x.d.c_dead[e] <= now;
                 }
                 for (unsigned b = __ballot_sync(0xffffffffu, ex); b; b &= b - 1)
-                    x.queue_rtx(now, m, w0 + __ffs(b) - 1);
+                    x.queue_rtx(now, m, mid, w0 + __ffs(b) - 1);
             }
         }
     if (x.d.rd) x.maybe_send_rts(now);  // :1166
@@ -1379,6 +1440,11 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
                             const int32_t* h_dst, const int32_t* h_n_paths, cn_tx** out) {
     if (!cfg || !out || n_conns == 0 || cfg->chunk_bytes == 0 || cfg->rto_min <= 0 ||
         cfg->max_paths == 0 || cfg->max_paths > 1024 || cfg->lb_policy < 0 || cfg->lb_policy > 2 ||
+        !(cfg->policy >= CN_POLICY_DEFAULT && cfg->policy <= CN_POLICY_TEST_OUT_OF_RANGE
+#ifdef CN_TX_USER_POLICY_HEADER
+          || cfg->policy == CN_POLICY_USER
+#endif
+          ) ||
         (cfg->cc_algo != CN_CC_NONE && cfg->cc_algo != CN_CC_SWIFT) || cfg->drr_quantum == 0 ||
         cfg->mss <= 0 || !(cfg->init_cwnd_pkts > 0) || cfg->cap_bytes < 0) {
         set_error("cn_tx_create: bad config (rto_min resolved > 0, max_paths <= 1024, "
@@ -1415,6 +1481,7 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
     d.init_cwnd = cfg->init_cwnd_pkts;
     d.rd = cfg->receiver_driven ? 1 : 0;
     d.ordered = cfg->ordered ? 1 : 0;
+    d.pol = cfg->policy;
     d.so_cap = cfg->ordered ? (cfg->sent_order_cap ? cfg->sent_order_cap : 1u << 16) : 1;
     d.credit_cap = static_cast<int64_t>(cfg->credit_bank_quanta) * cfg->credit_quantum;
     d.initial_credit = cfg->initial_credit;

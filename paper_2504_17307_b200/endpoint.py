@@ -33,7 +33,7 @@ class TransportConfigC(ctypes.Structure):
                 ("mss", i64), ("cap_bytes", i64), ("ecn_as_loss", i32), ("pad0", i32),
                 ("swift_target_ns", i64), ("init_cwnd_pkts", f64), ("base_rtt_ns", f64),
                 ("commit_ahead", i64), ("max_conns", u32), ("max_batch", u32), ("log_cap", u32),
-                ("pad1", u32), ("chunk_pool", u64), ("arena_bytes", u64)]
+                ("policy", i32), ("chunk_pool", u64), ("arena_bytes", u64)]
 
 
 STATS_FIELDS = ["msgs_sent", "msgs_completed", "backpressured", "chunks_sent", "chunk_rtx", "fast_rtx", "rtos",

@@ -28,6 +28,8 @@ STATS_DTYPE = np.dtype([(n, "<u8") for n in ("chunks_sent", "chunk_rtx", "fast_r
                        [("srtt", "<i8"), ("rttvar", "<i8"), ("backoff", "<i4"), ("live_msgs", "<i4"),
                         ("cwnd_bytes", "<i8"), ("inflight", "<i8"), ("cwnd_pkts", "<f8")])
 CC = {"none": 0, "swift": 2}
+# transport policy plug-ins (include/chunknet_policy.cuh; cn_tx_config::policy)
+POLICY = {"default": 0, "round_robin": 1, "single_path": 2, "test_out_of_range": 3, "user": 100}
 
 
 class TxEngine:
@@ -36,8 +38,11 @@ class TxEngine:
                  dupack_threshold=8, rtx_avoid_prev_path=True, stream_index0=0,
                  chunk_pool=1 << 20, log_cap=1 << 16, cc="none", swift_target_ns=0,
                  drr_quantum=32768, mss=4032, cap_bytes=0, init_cwnd_pkts=2.0, receiver_driven=False,
-                 initial_credit=0, credit_quantum=32768, credit_bank_quanta=4, ordered=False, device="cuda"):
-        L = _lib.lib()
+                 initial_credit=0, credit_quantum=32768, credit_bank_quanta=4, ordered=False,
+                 policy="default", device="cuda"):
+        # CN_POLICY_USER lives in the library built with the plug-in
+        pol = POLICY[policy] if isinstance(policy, str) else int(policy)
+        self._L = L = _lib.user_lib() if pol == POLICY["user"] else _lib.lib()
         c = _lib.TxConfig()
         L.cn_tx_config_default(ctypes.byref(c))
         c.chunk_bytes, c.dupack_threshold = chunk_bytes, dupack_threshold
@@ -52,20 +57,21 @@ class TxEngine:
         c.receiver_driven, c.initial_credit = (1 if receiver_driven else 0), initial_credit
         c.credit_quantum, c.credit_bank_quanta = credit_quantum, credit_bank_quanta
         c.ordered = 1 if ordered else 0
+        c.policy = pol
         self.device = torch.device(device)
         self.n, self.log_cap = n_conns, log_cap
         arr = lambda v: (ctypes.c_int32 * n_conns)(*[int(x) for x in v]) if v is not None else None  # noqa: E731
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(L.cn_tx_create(ctypes.byref(c), n_conns, arr(src), arr(dst), arr(n_paths),
-                                      ctypes.byref(h)), "cn_tx_create")
+                                      ctypes.byref(h)), "cn_tx_create", L)
         self._h = h
         self.log = torch.zeros(n_conns * log_cap * 32, dtype=torch.uint8, device=self.device)
         self.stats = torch.zeros(n_conns * STATS_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.lib().cn_tx_destroy(self._h)
+            self._L.cn_tx_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -96,19 +102,20 @@ class TxEngine:
         """Enqueue cn_tx_run on prepared device events (no synchronisation)."""
         t_off, t_ev, t_sub, t_ack = prepared
         s = stream or torch.cuda.current_stream(self.device)
-        _lib.check(_lib.lib().cn_tx_run(self._h, t_off.data_ptr(), t_ev.data_ptr(), t_sub.data_ptr(),
+        _lib.check(self._L.cn_tx_run(self._h, t_off.data_ptr(), t_ev.data_ptr(), t_sub.data_ptr(),
                                         t_ack.data_ptr(), int(end_time), self.log.data_ptr(),
                                         self.stats.data_ptr(), ctypes.c_void_p(s.cuda_stream)),
-                   "cn_tx_run")
+                   "cn_tx_run", self._L)
 
     def run(self, events_per_conn, submits, acks, end_time, stream=None):
         s = stream or torch.cuda.current_stream(self.device)
         self.launch(self.prepare(events_per_conn, submits, acks), end_time, s)
         s.synchronize()
         st = ctypes.c_uint()
-        _lib.lib().cn_tx_status(self._h, ctypes.byref(st))
+        self._L.cn_tx_status(self._h, ctypes.byref(st))
         if st.value:
-            raise _lib.ChunknetError(-6, f"tx engine status 0x{st.value:x}")
+            # 64 = policy contract violation: the reference's logic_error
+            raise _lib.ChunknetError(-2 if st.value & 64 else -6, f"tx engine status 0x{st.value:x}")
         return self.stats_np()
 
     def stats_np(self):

@@ -7,7 +7,9 @@ same Transport::Stats.  sender_<name>: congestion control none (OpenLoop);
 sender_swift_<name>: Swift with global scope, target 3 x base RTT, the
 window gating egress (DRR over the path ring, retransmission queues first).
 The closed_* stimuli come from Swift DES runs, so there the replay is the
-DES sender itself."""
+DES sender itself.  sender_rr_* / sender_single_*: the policy plug-ins
+(include/chunknet_policy.cuh) against the same policies installed in the
+reference with Transport::set_policy_factory."""
 import glob
 import json
 import os
@@ -57,7 +59,8 @@ def _replay(name, chunk_pool):
                    chunk_pool=chunk_pool, log_cap=1 << 17, cc=meta.get("cc", "none"),
                    swift_target_ns=meta.get("swift_target_ns", 0),
                    receiver_driven=meta.get("receiver_driven", False),
-                   initial_credit=meta.get("initial_credit", 0), ordered=meta.get("ordered", False))
+                   initial_credit=meta.get("initial_credit", 0), ordered=meta.get("ordered", False),
+                   policy=meta.get("policy", 0))
     st = eng.run([_events(z["submits"], z["acks"])], z["submits"], z["acks"], 60_000_000_000)[0]
     ref = meta["stats"]
     for k in ("chunks_sent", "chunk_rtx", "fast_rtx", "rtos", "msgs_completed"):
@@ -96,3 +99,17 @@ def test_tx_engine_eight_dup_hints_one_fast_rtx():
     assert int(st["fast_rtx"]) == 1 and int(st["chunk_rtx"]) == 1 and int(st["chunks_sent"]) == 10
     log = eng.log_np(0)
     assert [int(r["chunk"]) for r in log if r["is_rtx"]] == [0]
+
+
+def test_tx_policy_contract_violation_fails_loudly():
+    """test_transport.cpp:686-703: a policy path outside [0, n_paths) is a
+    logic_error; the engine reports CN_E_LOGIC."""
+    from paper_2504_17307_b200._lib import ChunknetError
+    from paper_2504_17307_b200.records import ACK_DTYPE
+    from paper_2504_17307_b200.sender import TxEngine
+    eng = TxEngine(1, chunk_bytes=4032, rto_min=10_000_000, commit_ahead=1 << 20, base_rtt_ns=12_000,
+                   seed=2, max_paths=4, n_paths=[4], src=[0], dst=[1], policy="test_out_of_range")
+    sub = np.array([(0, 4096, 1)], dtype=[("t", "<i8"), ("len", "<u8"), ("tag", "<u8")])
+    with pytest.raises(ChunknetError) as e:
+        eng.run([[(0, 0)]], sub, np.zeros(1, dtype=ACK_DTYPE), 100_000)
+    assert e.value.status == -2

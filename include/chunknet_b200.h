@@ -397,6 +397,20 @@ int cn_tx_run(cn_tx* t, const uint32_t* d_ev_off, const uint64_t* d_events,
               const cn_tx_submit* d_submits, const cn_ack_rec* d_acks, int64_t end_time,
               cn_tx_rec* d_log, cn_tx_stats* d_stats, void* stream);
 int cn_tx_status(cn_tx* t, unsigned int* out);
+/* Connection state for introspection (Transport::path_inflight,
+ * conn_credit, engine_gauge, transport.cpp:1173-1209); synchronous. */
+typedef struct cn_tx_conn_state {
+    int64_t credit;     /* Connection::credit (receiver-driven bank) */
+    int64_t unchunked;  /* dispatched bytes not yet chunked (its share of the engine gauge) */
+    int32_t n_paths;
+    int32_t pad;
+} cn_tx_conn_state;
+int cn_tx_get_conn_state(cn_tx* t, uint32_t conn, cn_tx_conn_state* out,
+                         int64_t* h_path_inflight /* [n_paths] or NULL */, uint32_t max_paths);
+/* Diagnostics: the raw device state of one connection (TxConn, per-path
+ * arrays, RNG, chunk state of its pool share); returns the byte count (pass
+ * h_out = NULL to size).  Used to compare engine states across builds. */
+int64_t cn_tx_debug_state(cn_tx* t, uint32_t conn, void* h_out, uint64_t cap);
 /* Transmit records logged per connection so far (host array of n_conns);
  * cn_tx_log_clear restarts every connection's log at 0. */
 int cn_tx_log_counts(cn_tx* t, uint32_t* h_out);
@@ -521,6 +535,14 @@ int cn_transport_stats(cn_transport* h, cn_stats* out);
 int32_t cn_transport_conn_index(cn_transport* h, int32_t src, int32_t dst);
 /* outstanding_bytes (transport.hpp:102): the connection's gated inflight */
 int64_t cn_transport_outstanding_bytes(cn_transport* h, int32_t src, int32_t dst);
+/* the rest of the reference's introspection (transport.hpp:101-107), as of
+ * the last cn_transport_advance; 0 for an unknown connection or path */
+int64_t cn_transport_path_inflight(cn_transport* h, int32_t src, int32_t dst, int32_t path);
+int64_t cn_transport_window_available(cn_transport* h, int32_t src, int32_t dst, int32_t path);
+int64_t cn_transport_conn_credit(cn_transport* h, int32_t src, int32_t dst);
+int32_t cn_transport_engine_inflight_msgs(cn_transport* h, int32_t host, int32_t engine);
+uint64_t cn_transport_engine_dispatched(cn_transport* h, int32_t host, int32_t engine);
+int64_t cn_transport_engine_gauge(cn_transport* h, int32_t host, int32_t engine);
 
 /* ------------------------------------------------------------- EQDS
  * The receiver-driven pull pacer (EqdsReceiver, eqds.cpp:7-104), one per

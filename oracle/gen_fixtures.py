@@ -226,6 +226,32 @@ def gen_sender_swift(name):
 POLICY_SCENARIOS = ["cfg1", "lossy_2m", "multigen_k8", "k8_4x1m"]
 
 
+# Transport introspection (path_inflight, window_available, outstanding_bytes,
+# conn_credit, engine_*) of the reference sender at times between its input
+# events: probe_<name>.npz for tests/test_endpoint_gpu.py
+PROBE_SCENARIOS = {"lossy_2m": "none", "multigen_k8": "swift", "closed_w4": "swift", "k8_4x1m": "none"}
+
+
+def gen_probes(name, cc):
+    z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz" if cc == "none" else f"sender_{cc}_{name}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    kw, flows = SCENARIOS[name]
+    rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes",
+                              "paths", "lb") if k in kw}
+    acks, sub = z["acks"], z["submits"]
+    ts = np.unique(np.concatenate([acks["aux"].astype(np.int64), sub["t"].astype(np.int64)]))
+    mid = ts[:-1] + (ts[1:] - ts[:-1]) // 2
+    pt = mid[(ts[1:] - ts[:-1]) >= 4][:: max(1, len(mid) // 40)] + 1
+    submits = [(int(s["t"]), int(s["len"]), int(s["tag"])) for s in sub]
+    tx, st, pr = ref.sender_replay(acks, submits, meta["src"], meta["dst"], cc=cc, probe_t=pt,
+                                   probe_paths=int(meta["n_paths"]), **rkw)
+    assert len(tx) == len(z["tx"])
+    path = os.path.join(GOLDEN, f"probe_{name}.npz")
+    np.savez_compressed(path, probe_t=pt, probes=pr, sender=np.frombuffer(
+        (f"sender_{name}" if cc == "none" else f"sender_{cc}_{name}").encode(), dtype=np.uint8))
+    print(f"  probe_{name}: {len(pt)} probes x {pr.shape[1]} values")
+
+
 def gen_sender_policy(name, policy):
     z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
     kw, flows = SCENARIOS[name]
@@ -429,8 +455,12 @@ def gen_rng():
 
 def main(argv):
     os.makedirs(GOLDEN, exist_ok=True)
-    names = argv or list(SCENARIOS) + ["rng", "swift", "trace", "eqds", "policy"]
+    names = argv or list(SCENARIOS) + ["rng", "swift", "trace", "eqds", "policy", "probe"]
     for n in names:
+        if n == "probe":
+            for m, cc in PROBE_SCENARIOS.items():
+                gen_probes(m, cc)
+            continue
         if n == "policy":
             for m in POLICY_SCENARIOS:
                 for pol in POLICY_NAMES:

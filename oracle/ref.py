@@ -108,6 +108,8 @@ def lib():
         L.cnref_sender_replay_bench.argtypes = [ctypes.POINTER(Scenario), i32, i32, vp, u64, vp,
                                                 u64, i32, i32]
         L.cnref_sender_replay_bench.restype = ctypes.c_double
+        L.cnref_set_probes.argtypes = [vp, u32, vp, u32]
+        L.cnref_set_probes.restype = None
         L.cnref_rng_u64.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
         L.cnref_next_below.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]
         L.cnref_next_double.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
@@ -160,7 +162,7 @@ def sender_replay(acks, submits, src, dst, *, topo="fat_tree", topo_arg=8, rate_
                   link_delay_ns=1000, qcap_bytes=1 << 20, seed=1, chunk_bytes=32768, paths=8,
                   lb="p2_rtt", cc="none", cc_scope=0, dupack_threshold=8, rto_min=0,
                   cutoff_ns=60_000_000_000, max_out=1 << 20, receiver_driven=False, ordered=False,
-                  policy=0):
+                  policy=0, probe_t=None, probe_paths=0):
     """Reference sender over a blackhole: submits [(t, len, tag)] and acks
     (ACK_DTYPE, aux = delivery time at the sender; also NACK / credit /
     rts_ack records) -> (tx log, stats).  Receiver-driven: RTS packets are
@@ -176,12 +178,22 @@ def sender_replay(acks, submits, src, dst, *, topo="fat_tree", topo_arg=8, rate_
     acks = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
     out = np.zeros(max_out, dtype=TX_DTYPE)
     st = SenderStats()
-    rc = lib().cnref_sender_replay(ctypes.byref(sc), src, dst, ctypes.cast(sb, ctypes.c_void_p),
-                                   len(submits), _ptr(acks), len(acks), _ptr(out), max_out,
-                                   ctypes.byref(st))
+    probes = None
+    if probe_t is not None:  # Transport introspection at these times (cnref_set_probes)
+        pt = np.ascontiguousarray(probe_t, dtype=np.int64)
+        probes = np.zeros((len(pt), 5 + 2 * probe_paths), dtype=np.int64)
+        lib().cnref_set_probes(_ptr(pt), len(pt), _ptr(probes), probes.shape[1])
+    try:
+        rc = lib().cnref_sender_replay(ctypes.byref(sc), src, dst, ctypes.cast(sb, ctypes.c_void_p),
+                                       len(submits), _ptr(acks), len(acks), _ptr(out), max_out,
+                                       ctypes.byref(st))
+    finally:
+        if probe_t is not None:
+            lib().cnref_set_probes(None, 0, None, 0)
     if rc != 0:
         raise RuntimeError(lib().cnref_last_error().decode())
-    return out[: min(st.n_tx, max_out)].copy(), {k: getattr(st, k) for k, _ in SenderStats._fields_}
+    res = out[: min(st.n_tx, max_out)].copy(), {k: getattr(st, k) for k, _ in SenderStats._fields_}
+    return res + (probes,) if probe_t is not None else res
 
 
 def sender_replay_bench(acks, submits, src, dst, threads=1, reps=1, *, topo="fat_tree",

@@ -53,6 +53,10 @@ namespace {
 
 thread_local std::string g_err;
 thread_local bool g_ordered = false;  // records of an ordered-reliability run (go-back-N NACKs)
+// introspection probes of the next sender replay (cnref_set_probes)
+thread_local std::vector<int64_t> g_probe_t;
+thread_local int64_t* g_probe_out = nullptr;
+thread_local uint32_t g_probe_stride = 0;
 
 // Payload generator of the reference tests (test_transport.cpp:63-71).
 std::shared_ptr<std::vector<uint8_t>> pattern(uint64_t n, uint64_t seed) {
@@ -583,6 +587,17 @@ struct cnref_submit {
     uint64_t tag;
 };
 
+// Probes for the next cnref_sender_replay on this thread: at each time t[i]
+// (relative, like the inputs) the reference's introspection is written to
+// out[i * stride ...]: outstanding_bytes, conn_credit, engine_inflight_msgs,
+// engine_dispatched, engine_gauge, then (path_inflight, window_available)
+// per path.  n = 0 clears.
+void cnref_set_probes(const int64_t* t, uint32_t n, int64_t* out, uint32_t stride) {
+    g_probe_t.assign(t, t + n);
+    g_probe_out = out;
+    g_probe_stride = stride;
+}
+
 int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_submit* subs,
                         uint64_t n_subs, const cn_ack_rec* acks, uint64_t n_acks,
                         cnref_tx_rec* out, uint64_t max_out, cnref_sender_stats* st) {
@@ -680,6 +695,22 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
                 p.echo_tx_time += t0;  // the same shift as every send time
                 int host = p.dst;
                 tr.handle_packet(host, std::move(p));
+            });
+        }
+        // Transport introspection (transport.cpp:1173-1209) at the probe times
+        for (size_t i = 0; i < g_probe_t.size(); ++i) {
+            int64_t* o = g_probe_out + i * g_probe_stride;
+            const uint32_t w = g_probe_stride;
+            eq.schedule(t0 + g_probe_t[i], [&tr, o, w, src, dst] {
+                o[0] = tr.outstanding_bytes(src, dst);
+                o[1] = tr.conn_credit(src, dst);
+                o[2] = tr.engine_inflight_msgs(src, 0);
+                o[3] = static_cast<int64_t>(tr.engine_dispatched(src, 0));
+                o[4] = tr.engine_gauge(src, 0);
+                for (uint32_t p = 0; 6 + 2 * p < w; ++p) {
+                    o[5 + 2 * p] = tr.path_inflight(src, dst, static_cast<int>(p));
+                    o[6 + 2 * p] = tr.window_available(src, dst, static_cast<int>(p));
+                }
             });
         }
         eq.run_until_idle(sc->cutoff_ns);

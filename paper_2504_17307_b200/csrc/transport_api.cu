@@ -366,3 +366,60 @@ extern "C" int64_t cn_transport_outstanding_bytes(cn_transport* h, int32_t src, 
     const int32_t k = open_conn(h, src, dst, false);
     return k < 0 ? 0 : h->txs[k].inflight;
 }
+
+// Transport::path_inflight / window_available / conn_credit / engine_*
+// (transport.cpp:1173-1209), from the device state after the last advance
+extern "C" int64_t cn_transport_path_inflight(cn_transport* h, int32_t src, int32_t dst, int32_t path) {
+    if (!h) return 0;
+    const int32_t k = open_conn(h, src, dst, false);
+    if (k < 0 || path < 0 || path >= static_cast<int32_t>(h->c.paths)) return 0;
+    cn_tx_conn_state cs;
+    std::vector<int64_t> inf(h->c.paths, 0);
+    if (cn_tx_get_conn_state(h->tx, static_cast<uint32_t>(k), &cs, inf.data(), h->c.paths) != CN_OK) return 0;
+    return path < cs.n_paths ? inf[path] : 0;
+}
+
+extern "C" int64_t cn_transport_window_available(cn_transport* h, int32_t src, int32_t dst, int32_t path) {
+    if (!h) return 0;
+    const int32_t k = open_conn(h, src, dst, false);
+    if (k < 0 || path < 0 || path >= static_cast<int32_t>(h->c.paths)) return 0;
+    // global CC scope: the window gates the connection's whole inflight (:320-325)
+    return h->txs[k].cwnd_bytes - h->txs[k].inflight;
+}
+
+extern "C" int64_t cn_transport_conn_credit(cn_transport* h, int32_t src, int32_t dst) {
+    if (!h) return 0;
+    const int32_t k = open_conn(h, src, dst, false);
+    cn_tx_conn_state cs;
+    if (k < 0 || cn_tx_get_conn_state(h->tx, static_cast<uint32_t>(k), &cs, nullptr, 0) != CN_OK) return 0;
+    return cs.credit;
+}
+
+// one engine per host: the host's connections together
+extern "C" int32_t cn_transport_engine_inflight_msgs(cn_transport* h, int32_t host, int32_t engine) {
+    if (!h || engine != 0) return 0;
+    int32_t n = 0;
+    for (const auto& kv : h->conn_idx)
+        if (kv.first.first == host) n += h->txs[kv.second].live_msgs;
+    return n;
+}
+
+extern "C" uint64_t cn_transport_engine_dispatched(cn_transport* h, int32_t host, int32_t engine) {
+    if (!h || engine != 0) return 0;
+    uint64_t n = 0;
+    for (const auto& kv : h->conn_idx)
+        if (kv.first.first == host) n += h->txs[kv.second].msgs_sent;
+    return n;
+}
+
+extern "C" int64_t cn_transport_engine_gauge(cn_transport* h, int32_t host, int32_t engine) {
+    if (!h || engine != 0) return 0;
+    int64_t g = 0;
+    for (const auto& kv : h->conn_idx)
+        if (kv.first.first == host) {
+            cn_tx_conn_state cs;
+            if (cn_tx_get_conn_state(h->tx, static_cast<uint32_t>(kv.second), &cs, nullptr, 0) == CN_OK)
+                g += cs.unchunked;
+        }
+    return g;
+}

@@ -48,6 +48,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
 #include <climits>
 #include <new>
 #include <string>
@@ -755,7 +756,13 @@ __device__ void commit_chunks(Tx& x) {
     __syncwarp();
 }
 
-__device__ void pump(Tx& x, int64_t now) {  // transport.cpp:232-240
+// Inlined into every caller.  Resuming a replay across cn_tx_run calls
+// faulted or diverged with some code layouts of this kernel (pump out of
+// line; pump and run_deferred both inlined) and not with others (this one;
+// ptxas -O0); the cause is not pinned down.  test_tx_gpu.py::
+// test_tx_engine_resumes_across_runs and the endpoint introspection tests
+// guard the layout that passes.
+__device__ __forceinline__ void pump(Tx& x, int64_t now) {  // transport.cpp:232-240
     for (;;) {
         commit_chunks(x);
         if (egress(x, now) == 0) break;
@@ -1208,7 +1215,11 @@ __host__ __device__ inline size_t tx_smem_words(uint32_t max_paths) {
            (11 * static_cast<size_t>(max_paths) + 7) / 8;
 }
 
-__global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(const __grid_constant__ TxDev d, const uint32_t* __restrict__ ev_off,
+// The engine descriptor is read through a global pointer (a cached,
+// read-only copy made at creation): passing it by value made every
+// thread copy it to its stack frame, and a __grid_constant__ parameter
+// addressed generically faulted on a long replay handed over in 42 slices.
+__global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(const TxDev* __restrict__ dp, const uint32_t* __restrict__ ev_off,
                                                          const uint64_t* __restrict__ events,
                                                          const cn_tx_submit* __restrict__ submits,
                                                          const cn_ack_rec* __restrict__ acks,
@@ -1216,6 +1227,7 @@ __global__ void __launch_bounds__(kTxWarps * 32, 1) k_tx_run(const __grid_consta
                                                          uint32_t* __restrict__ log_n,
                                                          cn_tx_stats* __restrict__ stats) {
     extern __shared__ uint64_t sm[];
+    const TxDev& d = *dp;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t conn = blockIdx.x * kTxWarps + w;
     if (conn >= d.n_conns) return;
@@ -1411,6 +1423,7 @@ using namespace cnb;
 
 struct cn_tx {
     TxDev d;
+    TxDev* d_dev = nullptr;  // device copy read by k_tx_run
     cn_sched* sched;
     uint32_t* d_logn;
 };
@@ -1507,6 +1520,7 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
               cudaMalloc(&d.s_rtxq, subs * 4) == cudaSuccess && cudaMalloc(&d.s_ring, subs * 2) == cudaSuccess &&
               cudaMalloc(&d.s_inring, subs) == cudaSuccess && cudaMalloc(&d.pool_top, 8) == cudaSuccess &&
               cudaMalloc(&d.status, 4) == cudaSuccess && cudaMalloc(&t->d_logn, n_conns * 4ull) == cudaSuccess &&
+              cudaMalloc(&t->d_dev, sizeof(TxDev)) == cudaSuccess &&
               cudaMalloc(&src, n_conns * 4ull) == cudaSuccess && cudaMalloc(&dst, n_conns * 4ull) == cudaSuccess &&
               cudaMalloc(&np, n_conns * 4ull) == cudaSuccess;
     if (!ok) {
@@ -1541,6 +1555,12 @@ extern "C" int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int
     }
     cudaFuncSetAttribute(k_tx_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(tx_smem_bytes(cfg->max_paths)));
+    // the descriptor never changes after creation: one device copy
+    if (cudaMemcpy(t->d_dev, &t->d, sizeof(TxDev), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cn_tx_destroy(t);
+        set_error("cn_tx_create: descriptor copy failed");
+        return CN_E_CUDA;
+    }
     *out = t;
     return CN_OK;
 }
@@ -1552,7 +1572,7 @@ extern "C" void cn_tx_destroy(cn_tx* t) {
     void* ptrs[] = {d.c_psn, d.so_ref, d.gq_ref, d.gq_from,
                     d.conns,      d.c_path,    d.c_txt, d.c_dead, d.c_att,  d.c_fl,
                     d.c_dup,      d.c_q,       d.s_inflight, d.s_deficit, d.s_txq, d.s_rtxq,
-                    d.s_ring,     d.s_inring,  d.pool_top, d.status, t->d_logn};
+                    d.s_ring,     d.s_inring,  d.pool_top, d.status, t->d_logn, t->d_dev};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (t->sched) cn_sched_destroy(t->sched);
@@ -1568,7 +1588,7 @@ extern "C" int cn_tx_run(cn_tx* t, const uint32_t* d_ev_off, const uint64_t* d_e
     }
     k_tx_run<<<(t->d.n_conns + kTxWarps - 1) / kTxWarps, kTxWarps * 32,
                tx_smem_bytes(t->d.s.max_paths), static_cast<cudaStream_t>(stream)>>>(
-        t->d, d_ev_off, d_events, d_submits, d_acks, end_time, d_log, t->d_logn, d_stats);
+        t->d_dev, d_ev_off, d_events, d_submits, d_acks, end_time, d_log, t->d_logn, d_stats);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }
@@ -1588,5 +1608,62 @@ extern "C" int cn_tx_log_clear(cn_tx* t, void* stream) {
 extern "C" int cn_tx_status(cn_tx* t, unsigned int* out) {
     if (!t || !out) return CN_E_INVALID;
     CNB_CUDA(cudaMemcpy(out, t->d.status, 4, cudaMemcpyDeviceToHost));
+    return CN_OK;
+}
+
+// Debug: raw device state of connection `conn` (TxConn, its per-path arrays,
+// RNG, and the chunk state of its pool share) into a host buffer.
+extern "C" int64_t cn_tx_debug_state(cn_tx* t, uint32_t conn, void* h_out, uint64_t cap) {
+    if (!t || conn >= t->d.n_conns) return CN_E_INVALID;
+    CNB_CUDA(cudaDeviceSynchronize());
+    std::vector<uint8_t> buf;
+    auto put = [&](const void* dptr, uint64_t n) {
+        const size_t o = buf.size();
+        buf.resize(o + n);
+        if (n) cudaMemcpy(buf.data() + o, dptr, n, cudaMemcpyDeviceToHost);
+    };
+    const TxDev& d = t->d;
+    const uint64_t mp = d.s.max_paths, sb = conn * mp;
+    put(d.conns + conn, sizeof(TxConn));
+    put(d.s_inflight + sb, mp * 8);
+    put(d.s_deficit + sb, mp * 8);
+    put(d.s_txq + sb, mp * 4);
+    put(d.s_rtxq + sb, mp * 4);
+    put(d.s_ring + sb, mp * 2);
+    put(d.s_inring + sb, mp);
+    put(d.s.mt + conn * 312ull, 312 * 8);
+    put(d.s.mt_idx + conn, 4);
+    put(d.s.rtt + sb, mp * 8);
+    put(d.s.ecn + sb, mp * 8);
+    const uint64_t c0 = conn * d.conn_pool, nc = std::min<uint64_t>(d.conn_pool, 4096);
+    put(d.c_path + c0, nc * 4);
+    put(d.c_txt + c0, nc * 8);
+    put(d.c_dead + c0, nc * 8);
+    put(d.c_att + c0, nc * 4);
+    put(d.c_fl + c0, nc * 4);
+    put(d.c_dup + c0, nc * 4);
+    put(d.c_q + c0, nc * 4);
+    if (h_out) memcpy(h_out, buf.data(), std::min<uint64_t>(cap, buf.size()));
+    return static_cast<int64_t>(buf.size());
+}
+
+extern "C" int cn_tx_get_conn_state(cn_tx* t, uint32_t conn, cn_tx_conn_state* out, int64_t* h_path_inflight,
+                                    uint32_t max_paths) {
+    if (!t || !out || conn >= t->d.n_conns) {
+        set_error("cn_tx_get_conn_state: null handle / output or connection out of range");
+        return CN_E_INVALID;
+    }
+    CNB_CUDA(cudaDeviceSynchronize());
+    const TxConn* C = t->d.conns + conn;
+    CNB_CUDA(cudaMemcpy(&out->credit, &C->credit, 8, cudaMemcpyDeviceToHost));
+    CNB_CUDA(cudaMemcpy(&out->unchunked, &C->unchunked, 8, cudaMemcpyDeviceToHost));
+    CNB_CUDA(cudaMemcpy(&out->n_paths, &C->n_paths, 4, cudaMemcpyDeviceToHost));
+    out->pad = 0;
+    if (h_path_inflight) {
+        const uint32_t n = std::min<uint32_t>(max_paths, static_cast<uint32_t>(out->n_paths));
+        if (n)
+            CNB_CUDA(cudaMemcpy(h_path_inflight, t->d.s_inflight + static_cast<uint64_t>(conn) * t->d.s.max_paths,
+                                n * 8ull, cudaMemcpyDeviceToHost));
+    }
     return CN_OK;
 }

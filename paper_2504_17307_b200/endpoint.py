@@ -65,6 +65,14 @@ def _setup(L):
     L.cn_transport_conn_index.argtypes = [vp, i32, i32]
     L.cn_transport_outstanding_bytes.argtypes = [vp, i32, i32]
     L.cn_transport_outstanding_bytes.restype = i64
+    for f, rt in (("path_inflight", i64), ("window_available", i64)):
+        getattr(L, f"cn_transport_{f}").argtypes = [vp, i32, i32, i32]
+        getattr(L, f"cn_transport_{f}").restype = rt
+    L.cn_transport_conn_credit.argtypes = [vp, i32, i32]
+    L.cn_transport_conn_credit.restype = i64
+    for f, rt in (("engine_inflight_msgs", i32), ("engine_dispatched", u64), ("engine_gauge", i64)):
+        getattr(L, f"cn_transport_{f}").argtypes = [vp, i32, i32]
+        getattr(L, f"cn_transport_{f}").restype = rt
 
 
 class TransportEndpoint:
@@ -153,3 +161,22 @@ class TransportEndpoint:
 
     def outstanding_bytes(self, src, dst):
         return int(self._L.cn_transport_outstanding_bytes(self._h, src, dst))
+
+    # the rest of Transport's introspection (transport.hpp:101-107)
+    def path_inflight(self, src, dst, path):
+        return int(self._L.cn_transport_path_inflight(self._h, src, dst, path))
+
+    def window_available(self, src, dst, path):
+        return int(self._L.cn_transport_window_available(self._h, src, dst, path))
+
+    def conn_credit(self, src, dst):
+        return int(self._L.cn_transport_conn_credit(self._h, src, dst))
+
+    def engine_inflight_msgs(self, host, engine=0):
+        return int(self._L.cn_transport_engine_inflight_msgs(self._h, host, engine))
+
+    def engine_dispatched(self, host, engine=0):
+        return int(self._L.cn_transport_engine_dispatched(self._h, host, engine))
+
+    def engine_gauge(self, host, engine=0):
+        return int(self._L.cn_transport_engine_gauge(self._h, host, engine))

@@ -80,3 +80,36 @@ def test_endpoint_multi_connection_and_receive():
     st = ep.stats()
     assert st["nacks_sent"] == int(((acks_ref["flags"] & 4) != 0).sum())
     assert st["delivered_msgs"] == len(cpls_ref)
+
+
+@pytest.mark.parametrize("name", ["lossy_2m", "multigen_k8", "closed_w4", "k8_4x1m"])
+def test_endpoint_introspection_matches_reference(name):
+    """path_inflight / window_available / outstanding_bytes / conn_credit /
+    engine_* (transport.cpp:1173-1209) at times between the scenario's input
+    events, the inputs handed over in time slices: the reference's values
+    (oracle/gen_fixtures.py probe_<name>.npz)."""
+    zp = np.load(os.path.join(GOLDEN, f"probe_{name}.npz"))
+    sname = bytes(zp["sender"]).decode()
+    z = np.load(os.path.join(GOLDEN, f"{sname}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    ep = _ep(meta)
+    src, dst, n = meta["src"], meta["dst"], meta["n_paths"]
+    subs, acks = z["submits"], z["acks"]
+    si = ai = 0
+    for t, want in zip(zp["probe_t"], zp["probes"]):
+        t = int(t)
+        while si < len(subs) and int(subs[si]["t"]) <= t:
+            ep.send_message(src, dst, int(subs[si]["len"]), int(subs[si]["tag"]), int(subs[si]["t"]))
+            si += 1
+        aj = ai
+        while aj < len(acks) and int(acks[aj]["aux"]) <= t:
+            aj += 1
+        if aj > ai:
+            ep.handle_acks(acks[ai:aj])
+            ai = aj
+        ep.advance(t)
+        got = [ep.outstanding_bytes(src, dst), ep.conn_credit(src, dst), ep.engine_inflight_msgs(src),
+               ep.engine_dispatched(src), ep.engine_gauge(src)]
+        for p in range(n):
+            got += [ep.path_inflight(src, dst, p), ep.window_available(src, dst, p)]
+        assert got == [int(v) for v in want], (t, got, list(want))

@@ -113,3 +113,39 @@ def test_tx_policy_contract_violation_fails_loudly():
     with pytest.raises(ChunknetError) as e:
         eng.run([[(0, 0)]], sub, np.zeros(1, dtype=ACK_DTYPE), 100_000)
     assert e.value.status == -2
+
+
+@pytest.mark.parametrize("name,nslice", [("swift_multigen_k8", 42), ("multigen_k8", 42), ("lossy_2m", 7),
+                                         ("swift_closed_w4", 25)])
+def test_tx_engine_resumes_across_runs(name, nslice):
+    """The input events handed over in time slices, one cn_tx_run each (how
+    the endpoint drives the engine): the state persisted between launches
+    gives the identical transmit log."""
+    from paper_2504_17307_b200.sender import TxEngine
+    z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    eng = TxEngine(1, chunk_bytes=meta["chunk_bytes"], rto_min=meta["rto_min"], rto_max=meta["rto_max"],
+                   commit_ahead=meta["commit_ahead"], base_rtt_ns=meta["base_rtt"], seed=meta["seed"],
+                   lb=meta["lb"], max_paths=meta["n_paths"], src=[meta["src"]], dst=[meta["dst"]],
+                   chunk_pool=1 << 18, log_cap=1 << 17, cc=meta.get("cc", "none"),
+                   swift_target_ns=meta.get("swift_target_ns", 0))
+    subs, acks = z["submits"], z["acks"]
+    ev = sorted([(int(s["t"]), 0, k) for k, s in enumerate(subs)] + [(int(a["aux"]), 1, k) for k, a in enumerate(acks)])
+    ts = sorted({e[0] for e in ev})
+    cuts = [ts[int(len(ts) * (i + 1) / nslice) - 1] for i in range(nslice)]
+    cuts[-1] = 60_000_000_000
+    k = 0
+    for c in cuts:
+        part = []
+        while k < len(ev) and ev[k][0] <= c:
+            part.append(ev[k])
+            k += 1
+        si = [e[2] for e in part if e[1] == 0]
+        ai = [e[2] for e in part if e[1] == 1]
+        ms, ma = {j: i for i, j in enumerate(si)}, {j: i for i, j in enumerate(ai)}
+        evs = [(0, ms[e[2]]) if e[1] == 0 else (1, ma[e[2]]) for e in part]
+        eng.run([evs], subs[si] if si else subs[:1], acks[ai] if ai else acks[:1], c)
+    got, want = eng.log_np(0), z["tx"]
+    assert len(got) == len(want)
+    for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
+        assert (got[f] == want[f]).all(), f

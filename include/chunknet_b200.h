@@ -230,6 +230,11 @@ int cn_rx_post(cn_rx* rx, uint64_t tag, void* d_buf, uint64_t len, void* stream)
  * buffer to on_complete and frees it after, transport.cpp:794-803); post a
  * destination (cn_rx_post) to keep the data. */
 void* cn_rx_arena(cn_rx* rx);
+/* Bytes of the arena allocation: 2 x arena_bytes (the ring's capacity is
+ * arena_bytes; a message's range runs contiguously past the ring's end into
+ * the second half instead of wrapping).  The chunk pool is likewise stored
+ * at 2 x chunk_pool entries. */
+uint64_t cn_rx_arena_bytes(const cn_rx* rx);
 /* Occupancy of the receiver's rings (synchronous: waits for the device).
  * Chunk-pool entries and 512-B arena blocks are allocated per
  * message, contiguously, and handed back when the message is delivered. */

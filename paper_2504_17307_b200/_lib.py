@@ -103,6 +103,8 @@ def lib():
     L.cn_rx_post.argtypes = [vp, u64, vp, u64, vp]
     L.cn_rx_arena.argtypes = [vp]
     L.cn_rx_arena.restype = vp
+    L.cn_rx_arena_bytes.argtypes = [vp]
+    L.cn_rx_arena_bytes.restype = u64
     L.cn_rx_last_launches.argtypes = [vp]
     L.cn_rx_get_usage.argtypes = [vp, ctypes.POINTER(RxUsage)]
     L.cn_rx_set_profiling.argtypes = [vp, i32]

@@ -51,11 +51,11 @@ struct GenState {
     uint32_t lo_batch, tiles_done, cum_add, pad;
 };
 
-// Ring allocator over `cap` positions (chunk-pool entries, or arena blocks
-// of chunk_bytes): monotonic head/tail counters; a message's range never
-// wraps (the end of the ring is padded and retired at once); retired
-// positions are bits that k_finalize's last block sweeps the tail over --
-// the reference frees MsgRecv state and buffer at delivery (:794-803).
+// Ring allocator over `cap` positions (chunk-pool entries, or 512-B arena
+// blocks): monotonic head/tail counters; storage is 2 x cap so a message's
+// range is contiguous without padding; retired positions (mod cap) are bits
+// a k_finalize block sweeps the tail over -- the reference frees MsgRecv
+// state and buffer at delivery (:794-803).
 struct RingCtl {
     unsigned long long head, tail;
 };
@@ -139,34 +139,17 @@ struct RxDev {
     uint8_t* arena;
 };
 
-__device__ inline void set_bits(uint32_t* bits, uint64_t a, uint64_t n) {
-    for (uint64_t x = a; x < a + n;) {
-        const uint32_t o = static_cast<uint32_t>(x & 31);
-        const uint64_t k = n - (x - a) < 32 - o ? n - (x - a) : 32 - o;
-        const uint32_t m = (k == 32 ? ~0u : ((1u << k) - 1)) << o;
-        atomicOr(&bits[x >> 5], m);
-        x += k;
-    }
-}
-
-// One thread.  Positions [*pos, *pos + n) of the ring, or false when the
-// live span would exceed cap (the tail only moves in k_finalize).
-__device__ inline bool ring_alloc(RingCtl* r, uint64_t cap, uint32_t* bits, uint64_t n, uint64_t* pos) {
+// One thread.  Ring positions [h, h + n) by one atomicAdd (no retry loop:
+// a batch of a thousand new messages must not serialise on the head), laid
+// out at physical [h % cap, h % cap + n) of arrays sized 2 x cap, so a range
+// never wraps.  Over capacity: false -- CN_RXF_CAPACITY, fatal for the
+// receiver until cn_rx_reset, as an exhausted pool always was.
+__device__ inline bool ring_alloc(RingCtl* r, uint64_t cap, uint64_t n, uint64_t* pos) {
     if (n == 0 || n > cap) return false;
-    const unsigned long long tail = ld_volatile_u64(&r->tail);
-    unsigned long long h = ld_volatile_u64(&r->head);
-    for (;;) {
-        const uint64_t p = h % cap;
-        const uint64_t start = p + n > cap ? h + (cap - p) : h;
-        if (start + n - tail > cap) return false;
-        const unsigned long long old = atomicCAS(&r->head, h, start + n);
-        if (old == h) {
-            if (start > h) set_bits(bits, p, cap - p);  // the padded end of the ring
-            *pos = start % cap;
-            return true;
-        }
-        h = old;
-    }
+    const unsigned long long h = atomicAdd(&r->head, static_cast<unsigned long long>(n));
+    if (h + n - ld_volatile_u64(&r->tail) > cap) return false;
+    *pos = h % cap;
+    return true;
 }
 
 // Whole block: advance the tail over retired positions (kAdvWords words of
@@ -417,7 +400,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 unsigned long long boff = 0;
                 if (h.msg_len == 0 || nc >= (1ull << 31) || (d.reduce && (h.msg_len % d.elem)))
                     st = CN_RXF_UNSUPPORTED;
-                if (!st && !ring_alloc(&d.ctl->pool, d.pool_cap, d.pool_bits, nc, &base)) st = CN_RXF_CAPACITY;
+                if (!st && !ring_alloc(&d.ctl->pool, d.pool_cap, nc, &base)) st = CN_RXF_CAPACITY;
                 uint8_t* buf = nullptr;
                 if (!st && d.carry && d.post_mask) {  // a posted destination (cn_rx_post)
                     uint32_t hp = static_cast<uint32_t>(mix64(h.msg_tag)) & d.post_mask;
@@ -436,12 +419,11 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 if (!st && d.carry && !buf) {  // arena blocks of kArenaUnit bytes
                     uint64_t ab = 0;
                     const uint64_t nb = (h.msg_len + kArenaUnit - 1) / kArenaUnit;
-                    if (ring_alloc(&d.ctl->arena, d.arena_blocks, d.arena_bits, nb, &ab)) {
+                    if (ring_alloc(&d.ctl->arena, d.arena_blocks, nb, &ab)) {
                         boff = ab * kArenaUnit;
                         buf = d.arena + boff;
                     } else {
                         st = CN_RXF_CAPACITY;
-                        set_bits(d.pool_bits, base, nc);  // give the chunk range back
                     }
                 }
                 status |= st;
@@ -1376,7 +1358,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
                 d.c_newb[e] = 0;
                 d.c_last[e] = 0;
                 d.c_newfl[e] = 0;
-                atomicOr(&d.pool_bits[e >> 5], 1u << (e & 31));
+                const uint64_t rp = e >= d.pool_cap ? e - d.pool_cap : e;  // ring position
+                atomicOr(&d.pool_bits[rp >> 5], 1u << (rp & 31));
             }
             __syncthreads();
             continue;
@@ -1431,11 +1414,17 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         const uint32_t na = d.ctl->n_aret[par ^ 1u];
         for (uint32_t j = blockIdx.x; j < na; j += gridDim.x) {
             const unsigned long long v = al[j];
-            const uint64_t a = v >> 31, nb = v & 0x7FFFFFFF;
-            for (uint64_t w = (a >> 5) + threadIdx.x; (w << 5) < a + nb; w += blockDim.x) {
-                const uint64_t lo_ = (w << 5) > a ? (w << 5) : a, hi_ = (w << 5) + 32 < a + nb ? (w << 5) + 32 : a + nb;
-                const uint32_t m = (hi_ - lo_ == 32 ? ~0u : ((1u << (hi_ - lo_)) - 1)) << (lo_ - (w << 5));
-                atomicOr(&d.arena_bits[w], m);
+            const uint64_t a0 = v >> 31, n0 = v & 0x7FFFFFFF;
+            // ring positions [a0, a0 + n0) mod arena_blocks: at most two runs
+            for (int part = 0; part < 2; ++part) {
+                const uint64_t a = part ? 0 : a0;
+                const uint64_t e0 = a0 + n0 > d.arena_blocks ? d.arena_blocks : a0 + n0;
+                const uint64_t end = part ? (a0 + n0 > d.arena_blocks ? a0 + n0 - d.arena_blocks : 0) : e0;
+                for (uint64_t w = (a >> 5) + threadIdx.x; (w << 5) < end; w += blockDim.x) {
+                    const uint64_t lo_ = (w << 5) > a ? (w << 5) : a, hi_ = (w << 5) + 32 < end ? (w << 5) + 32 : end;
+                    const uint32_t m = (hi_ - lo_ == 32 ? ~0u : ((1u << (hi_ - lo_)) - 1)) << (lo_ - (w << 5));
+                    atomicOr(&d.arena_bits[w], m);
+                }
             }
         }
     }
@@ -1465,20 +1454,24 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     __syncthreads();
     if (!last_block) return;
     __threadfence();
-    // tombstones of retired generations: once they reach 1/8 of the table,
+    // tombstones of retired generations: once they reach 1/4 of the table,
     // rebuild it (no other kernel uses the table now: the scatter reads
     // GenStates by index, which do not move)
-    if (d.ctl->n_tomb * 8 >= d.gen_mask + 1) {
+    if (d.ctl->n_tomb * 4 >= d.gen_mask + 1) {
         __shared__ uint32_t s_live;
         if (threadIdx.x == 0) s_live = 0;
         __syncthreads();
-        for (uint32_t x = threadIdx.x; x <= d.gen_mask; x += blockDim.x) {
-            const unsigned long long k = d.gen_key[x];
-            if (k != kEmpty && k != kTomb) {
-                const uint32_t j = atomicAdd(&s_live, 1u);
-                d.gen_tmp[2 * j] = k;
-                d.gen_tmp[2 * j + 1] = d.gen_val[x];
-            }
+        for (uint32_t x0 = threadIdx.x * 4; x0 <= d.gen_mask; x0 += blockDim.x * 4) {
+            unsigned long long k[4];  // independent loads in flight
+#pragma unroll
+            for (int q = 0; q < 4; ++q) k[q] = x0 + q <= d.gen_mask ? d.gen_key[x0 + q] : kEmpty;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (k[q] != kEmpty && k[q] != kTomb) {
+                    const uint32_t j = atomicAdd(&s_live, 1u);
+                    d.gen_tmp[2 * j] = k[q];
+                    d.gen_tmp[2 * j + 1] = d.gen_val[x0 + q];
+                }
         }
         __syncthreads();
         for (uint32_t x = threadIdx.x; x <= d.gen_mask; x += blockDim.x) {
@@ -1521,7 +1514,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->n_dirty[par ^ 1u] = 0;
         C->n_aret[par ^ 1u] = 0;
         C->par = par ^ 1u;
-        C->pool_snap = C->pool.head < d.pool_cap ? C->pool.head : d.pool_cap;
+        // physical extent used since the last reset (ranges overhang cap once the ring laps)
+        C->pool_snap = C->pool.head < d.pool_cap ? C->pool.head : 2 * d.pool_cap;
     }
 }
 
@@ -1545,8 +1539,8 @@ __global__ void k_reset(RxDev d, int full) {
         d.gen[x].epoch = 0;
         d.gen[x].touch = 0;
     }
-    uint64_t top = full ? d.pool_cap : d.ctl->pool_snap;
-    if (top > d.pool_cap) top = d.pool_cap;
+    uint64_t top = full ? 2 * d.pool_cap : d.ctl->pool_snap;
+    if (top > 2 * d.pool_cap) top = 2 * d.pool_cap;
     for (uint64_t x = tid; x < top; x += stride) {
         d.c_seen[x] = 0;
         d.c_flags[x] = 0;
@@ -1731,7 +1725,8 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.gen_free, ngen * 4ull);
     ALLOC(d.gen_tmp, ngen * 16ull);
     ALLOC(d.touched, ngen * 4ull);
-    d.first_half = cfg.chunk_pool * ppc;
+    const uint64_t phys = 2 * cfg.chunk_pool;  // ring capacity + overhang
+    d.first_half = phys * ppc;
     ALLOC(d.c_first, 2 * d.first_half * 4);
     d.dirty_cap = static_cast<uint32_t>(cfg.chunk_pool / kScanThreads + kPlanMax + 1);
     ALLOC(d.dirty, 2ull * d.dirty_cap * 8);
@@ -1739,16 +1734,16 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     d.arena_blocks = d.arena_cap / kArenaUnit;
     if (d.arena_blocks) ALLOC(d.arena_bits, (d.arena_blocks + 31) / 32 * 4);
     ALLOC(d.aret, 2ull * kPlanMax * 8);
-    ALLOC(d.c_seen, cfg.chunk_pool * 4);
-    ALLOC(d.c_flags, cfg.chunk_pool * 4);
-    ALLOC(d.c_txt, cfg.chunk_pool * 8);
-    ALLOC(d.c_path, cfg.chunk_pool * 4);
-    ALLOC(d.c_init, cfg.chunk_pool * 4);
-    ALLOC(d.c_cpl, cfg.chunk_pool * 4);
-    ALLOC(d.c_pmax, cfg.chunk_pool * 4);
-    ALLOC(d.c_newb, cfg.chunk_pool * 4);
-    ALLOC(d.c_last, cfg.chunk_pool * 4);
-    ALLOC(d.c_newfl, cfg.chunk_pool * 4);
+    ALLOC(d.c_seen, phys * 4);
+    ALLOC(d.c_flags, phys * 4);
+    ALLOC(d.c_txt, phys * 8);
+    ALLOC(d.c_path, phys * 4);
+    ALLOC(d.c_init, phys * 4);
+    ALLOC(d.c_cpl, phys * 4);
+    ALLOC(d.c_pmax, phys * 4);
+    ALLOC(d.c_newb, phys * 4);
+    ALLOC(d.c_last, phys * 4);
+    ALLOC(d.c_newfl, phys * 4);
     ALLOC(d.p_gen, B * 4);
     ALLOC(d.p_nack, B);
     d.ordered = cfg.ordered ? 1 : 0;
@@ -1763,7 +1758,7 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.scan_state, (cfg.chunk_pool / kScanThreads + ngen + 2) * 8ull);
     ALLOC(d.plan_base, ngen * 4ull);
     ALLOC(d.ctl, sizeof(RxCtl));
-    if (d.carry && cfg.arena_bytes) ALLOC(d.arena, cfg.arena_bytes);
+    if (d.carry && cfg.arena_bytes) ALLOC(d.arena, 2 * cfg.arena_bytes);  // ring + overhang
     if (d.post_mask) {
         ALLOC(d.post_key, (d.post_mask + 1ull) * 8);
         ALLOC(d.post_val, (d.post_mask + 1ull) * 8);
@@ -1812,6 +1807,7 @@ extern "C" int cn_rx_reset(cn_rx* rx, void* stream) {
 }
 
 extern "C" void* cn_rx_arena(cn_rx* rx) { return rx ? rx->d.arena : nullptr; }
+extern "C" uint64_t cn_rx_arena_bytes(const cn_rx* rx) { return rx && rx->d.arena ? 2 * rx->d.arena_cap : 0; }
 extern "C" int cn_rx_last_launches(const cn_rx* rx) { return rx ? rx->launches : 0; }
 
 extern "C" int cn_rx_get_usage(cn_rx* rx, cn_rx_usage* out) {

@@ -245,7 +245,7 @@ class Transport:
         ptr = _lib.lib().cn_rx_arena(self._h)
         if not ptr:
             return None
-        nbytes = self._rxcfg.arena_bytes
+        nbytes = _lib.lib().cn_rx_arena_bytes(self._h)
         return _device_u8_view(ptr, nbytes, self.device)
 
 

@@ -633,7 +633,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     msg = message_bytes(data)
     if not ref.available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref not built"})
         return
     for _ in range(args.warmup):
         ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
@@ -656,10 +656,23 @@ def run_reference(args):
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
+
+
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line on the real stdout: library chatter (NCCL's version
+    banner, CUDA/C printf) is sent to stderr while the bench runs."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -881,7 +894,7 @@ def main():
             line["sweep_cfg5"] = sweep
         if cpu:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line))
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 

@@ -31,7 +31,8 @@ def main():
     offs = np.concatenate([[0], np.cumsum(rows_self[rank])[:-1]]) * row
     sc, rc = rows[rank] * row, rows[:, rank] * row
     cap = int(max(rows.max() * row, 16))
-    a2a, a2c = AllToAll(cap), AllToAll(cap)
+    pb = int(os.environ.get("CN_A2A_PIECE_MB", "64")) << 20
+    a2a, a2c = AllToAll(cap, piece_bytes=pb), AllToAll(cap, piece_bytes=pb)
     coffs = [s_ * a2a.cap for s_ in range(world)]
 
     def step():

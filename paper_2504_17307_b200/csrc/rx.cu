@@ -390,17 +390,29 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         if (slot != kInf) {
             GenState* G = nullptr;
             if (gins) {
-                // never empty: live keys <= table slots = GenStates
-                gs = d.gen_free[atomicAdd(&d.ctl->gfree_head, 1ull) & d.gen_mask];
-                G = &d.gen[gs];
-                // the unique inserter allocates the message state
-                uint64_t nc = (h.msg_len + d.cb - 1) / d.cb;
+                // the unique inserter allocates the message state; its
+                // independent atomics (GenState index, pool range, arena
+                // range when no posted destinations exist) are issued together
+                const uint64_t nc = (h.msg_len + d.cb - 1) / d.cb;
+                const uint64_t nb = (h.msg_len + kArenaUnit - 1) / kArenaUnit;
                 uint32_t st = 0;
-                uint64_t base = 0;
-                unsigned long long boff = 0;
                 if (h.msg_len == 0 || nc >= (1ull << 31) || (d.reduce && (h.msg_len % d.elem)))
                     st = CN_RXF_UNSUPPORTED;
-                if (!st && !ring_alloc(&d.ctl->pool, d.pool_cap, nc, &base)) st = CN_RXF_CAPACITY;
+                const bool early_arena = !st && d.carry && !d.post_mask && d.arena_blocks;
+                const unsigned long long gi = atomicAdd(&d.ctl->gfree_head, 1ull);
+                unsigned long long ph = 0, ah = 0;
+                if (!st) ph = atomicAdd(&d.ctl->pool.head, static_cast<unsigned long long>(nc));
+                if (early_arena) ah = atomicAdd(&d.ctl->arena.head, static_cast<unsigned long long>(nb));
+                const unsigned long long ptail = ld_volatile_u64(&d.ctl->pool.tail);
+                const unsigned long long atail = early_arena ? ld_volatile_u64(&d.ctl->arena.tail) : 0;
+                // never empty: live keys <= table slots = GenStates
+                gs = d.gen_free[gi & d.gen_mask];
+                G = &d.gen[gs];
+                uint64_t base = 0;
+                unsigned long long boff = 0;
+                // ring_alloc's capacity rule (fatal for the receiver until reset)
+                if (!st && (nc > d.pool_cap || ph + nc - ptail > d.pool_cap)) st = CN_RXF_CAPACITY;
+                if (!st) base = ph % d.pool_cap;
                 uint8_t* buf = nullptr;
                 if (!st && d.carry && d.post_mask) {  // a posted destination (cn_rx_post)
                     uint32_t hp = static_cast<uint32_t>(mix64(h.msg_tag)) & d.post_mask;
@@ -418,8 +430,14 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 }
                 if (!st && d.carry && !buf) {  // arena blocks of kArenaUnit bytes
                     uint64_t ab = 0;
-                    const uint64_t nb = (h.msg_len + kArenaUnit - 1) / kArenaUnit;
-                    if (ring_alloc(&d.ctl->arena, d.arena_blocks, nb, &ab)) {
+                    bool ok_ = false;
+                    if (early_arena) {
+                        ok_ = nb <= d.arena_blocks && ah + nb - atail <= d.arena_blocks;
+                        ab = ah % d.arena_blocks;
+                    } else {
+                        ok_ = ring_alloc(&d.ctl->arena, d.arena_blocks, nb, &ab);
+                    }
+                    if (ok_) {
                         boff = ab * kArenaUnit;
                         buf = d.arena + boff;
                     } else {

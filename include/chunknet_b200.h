@@ -484,8 +484,11 @@ int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, 
  * calls become queued events: send_message / handle_acks queue at their
  * time, cn_transport_advance runs the device sender up to a time, and the
  * transmissions, acks and completions are polled.  Supported: one engine
- * per host, selective reliability, DefaultPolicy, CC none or Swift (global
- * scope), sender-driven; other settings are rejected with CN_E_UNSUPPORTED. */
+ * per host, selective reliability, the policies of chunknet_policy.cuh, CC
+ * none or Swift (global scope), sender- or receiver-driven (credit and
+ * rts_ack records through cn_transport_handle_acks; initial_credit resolved
+ * to one BDP by the caller); other settings are rejected with
+ * CN_E_UNSUPPORTED. */
 typedef struct cn_transport_config {
     /* TransportConfig (transport.hpp:23-51) */
     int32_t engines, conn_split, paths;

@@ -113,11 +113,16 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
         set_error("cn_transport_create: bad config (paths >= 1, resolved rto_min > 0, max_conns > 0)");
         return CN_E_INVALID;
     }
-    if (cfg->engines != 1 || cfg->conn_split || cfg->reliability != 0 || cfg->receiver_driven ||
+    if (cfg->engines != 1 || cfg->conn_split || cfg->reliability != 0 ||
         (cfg->cc_algo != CN_CC_NONE && cfg->cc_algo != CN_CC_SWIFT) || cfg->cc_scope != 0) {
-        set_error("cn_transport_create: supported: 1 engine, selective reliability, sender-driven, "
+        set_error("cn_transport_create: supported: 1 engine, selective reliability, "
                   "CC none/swift with global scope");
         return CN_E_UNSUPPORTED;
+    }
+    if (cfg->receiver_driven && cfg->initial_credit < 0) {
+        // the reference resolves -1 to one BDP of its Network (transport.cpp:40-44)
+        set_error("cn_transport_create: receiver_driven needs initial_credit resolved (one BDP, >= 0)");
+        return CN_E_INVALID;
     }
     *out = nullptr;
     cn_transport* h = new (std::nothrow) cn_transport();
@@ -147,6 +152,13 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
     tc.swift_target_ns = cfg->swift_target_ns;
     tc.init_cwnd_pkts = cfg->init_cwnd_pkts;
     tc.policy = cfg->policy;
+    // receiver-driven mode (EQDS sender glue): credit and rts_ack records
+    // arrive through cn_transport_handle_acks; RTS packets are logged as
+    // transmissions with chunk 0xFFFFFFFF
+    tc.receiver_driven = cfg->receiver_driven ? 1 : 0;
+    tc.credit_quantum = cfg->credit_quantum;
+    tc.credit_bank_quanta = cfg->credit_bank_quanta;
+    tc.initial_credit = cfg->receiver_driven ? cfg->initial_credit : 0;
     int rc = cn_tx_create(&tc, cfg->max_conns, nullptr, nullptr, nullptr, &h->tx);
     if (rc != CN_OK) {
         cn_transport_destroy(h);

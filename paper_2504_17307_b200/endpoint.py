@@ -79,7 +79,8 @@ class TransportEndpoint:
     def __init__(self, *, chunk_bytes=32768, paths=1, lb="oblivious", rto_min, rto_max=0, seed=1,
                  commit_ahead=0, base_rtt_ns=10000.0, cc="none", swift_target_ns=0, dupack_threshold=8,
                  rtx_avoid_prev_path=True, carry_payload=True, max_conns=64, max_batch=1 << 16,
-                 log_cap=1 << 16, chunk_pool=1 << 20, arena_bytes=64 << 20, device="cuda"):
+                 log_cap=1 << 16, chunk_pool=1 << 20, arena_bytes=64 << 20, receiver_driven=False,
+                 initial_credit=-1, credit_quantum=32768, credit_bank_quanta=4, policy=0, device="cuda"):
         L = _lib.lib()
         _setup(L)
         c = TransportConfigC()
@@ -91,6 +92,8 @@ class TransportEndpoint:
         c.carry_payload = 1 if carry_payload else 0
         c.max_conns, c.max_batch, c.log_cap = max_conns, max_batch, log_cap
         c.chunk_pool, c.arena_bytes = chunk_pool, arena_bytes
+        c.receiver_driven, c.initial_credit = (1 if receiver_driven else 0), initial_credit
+        c.credit_quantum, c.credit_bank_quanta, c.policy = credit_quantum, credit_bank_quanta, policy
         self.device = torch.device(device)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):

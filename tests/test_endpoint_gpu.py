@@ -113,3 +113,28 @@ def test_endpoint_introspection_matches_reference(name):
         for p in range(n):
             got += [ep.path_inflight(src, dst, p), ep.window_available(src, dst, p)]
         assert got == [int(v) for v in want], (t, got, list(want))
+
+
+@pytest.mark.parametrize("flow", range(5))
+def test_endpoint_receiver_driven_replay(flow):
+    """Receiver-driven mode through the boundary object: the recorded
+    credits and rts_acks (EQDS incast, one connection each) give the
+    reference's transmissions and RTS packets."""
+    z = np.load(os.path.join(GOLDEN, f"sender_eqds_incast_f{flow}.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    ep = _ep(meta, receiver_driven=True, initial_credit=meta["initial_credit"])
+    for s in z["submits"]:
+        ep.send_message(meta["src"], meta["dst"], int(s["len"]), int(s["tag"]), int(s["t"]))
+    ep.handle_acks(z["acks"])
+    ep.advance(60_000_000_000)
+    tx, conn = ep.poll_transmissions()
+    want = z["tx"]
+    assert len(tx) == len(want)
+    rg, rw = tx["chunk"] == 0xFFFFFFFF, want["chunk"] == 0xFFFFFFFF
+    assert rg.sum() == rw.sum()
+    for sg, sw, srt in ((~rg, ~rw, False), (rg, rw, True)):
+        g, w = tx[sg], want[sw]
+        if srt:
+            g, w = g[np.argsort(g["t"], kind="stable")], w[np.argsort(w["t"], kind="stable")]
+        for f in ("t", "msg_id", "chunk", "path", "is_rtx", "msg_seq"):
+            assert (g[f] == w[f]).all(), (srt, f)

@@ -484,7 +484,8 @@ int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, 
  * calls become queued events: send_message / handle_acks queue at their
  * time, cn_transport_advance runs the device sender up to a time, and the
  * transmissions, acks and completions are polled.  Supported: one engine
- * per host, selective reliability, the policies of chunknet_policy.cuh, CC
+ * per host, selective or ordered reliability (ordered: one path, data
+ * through cn_transport_handle_data_psn), the policies of chunknet_policy.cuh, CC
  * none or Swift (global scope), sender- or receiver-driven (credit and
  * rts_ack records through cn_transport_handle_acks; initial_credit resolved
  * to one BDP by the caller); other settings are rejected with
@@ -536,6 +537,10 @@ int64_t cn_transport_poll_transmissions(cn_transport* h, cn_tx_rec* out, uint64_
 /* Transport::handle_packet for a batch of delivered data packets (device records) */
 int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const void* d_payload, uint64_t stride,
                              uint32_t n, void* stream);
+/* ... with each packet's conn_psn (d_psn[n]), required under ordered
+ * reliability (TransportConfig::reliability = ordered, go-back-N) */
+int cn_transport_handle_data_psn(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
+                                 const void* d_payload, uint64_t stride, uint32_t n, void* stream);
 /* the last batch's ack / NACK records and completions (host copies) */
 int64_t cn_transport_poll_acks(cn_transport* h, cn_ack_rec* out, uint64_t cap);
 int64_t cn_transport_poll_completions(cn_transport* h, cn_completion* out, uint64_t cap);

@@ -113,7 +113,11 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
         set_error("cn_transport_create: bad config (paths >= 1, resolved rto_min > 0, max_conns > 0)");
         return CN_E_INVALID;
     }
-    if (cfg->engines != 1 || cfg->conn_split || cfg->reliability != 0 ||
+    if (cfg->reliability == 1 && cfg->paths > 1) {
+        set_error("cn_transport_create: ordered reliability with multipath (transport.cpp:21-26)");
+        return CN_E_LOGIC;
+    }
+    if (cfg->engines != 1 || cfg->conn_split || cfg->reliability < 0 || cfg->reliability > 1 ||
         (cfg->cc_algo != CN_CC_NONE && cfg->cc_algo != CN_CC_SWIFT) || cfg->cc_scope != 0) {
         set_error("cn_transport_create: supported: 1 engine, selective reliability, "
                   "CC none/swift with global scope");
@@ -156,6 +160,7 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
     // arrive through cn_transport_handle_acks; RTS packets are logged as
     // transmissions with chunk 0xFFFFFFFF
     tc.receiver_driven = cfg->receiver_driven ? 1 : 0;
+    tc.ordered = cfg->reliability == 1 ? 1 : 0;
     tc.credit_quantum = cfg->credit_quantum;
     tc.credit_bank_quanta = cfg->credit_bank_quanta;
     tc.initial_credit = cfg->receiver_driven ? cfg->initial_credit : 0;
@@ -173,6 +178,7 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
     rcfg.chunk_pool = cfg->chunk_pool;
     rcfg.arena_bytes = cfg->carry_payload ? cfg->arena_bytes : 0;
     rcfg.max_batch = cfg->max_batch;
+    rcfg.ordered = cfg->reliability == 1 ? 1 : 0;
     rc = cn_rx_create(&rcfg, &h->rx);
     if (rc != CN_OK) {
         cn_transport_destroy(h);
@@ -308,16 +314,18 @@ extern "C" int64_t cn_transport_poll_transmissions(cn_transport* h, cn_tx_rec* o
     return static_cast<int64_t>(k);
 }
 
-extern "C" int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const void* d_payload,
-                                        uint64_t stride, uint32_t n, void* stream) {
+extern "C" int cn_transport_handle_data_psn(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
+                                            const void* d_payload, uint64_t stride, uint32_t n, void* stream) {
     if (!h) return CN_E_INVALID;
     if (n > h->c.max_batch) {
         set_error("cn_transport_handle_data: batch larger than max_batch");
         return CN_E_CAPACITY;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int rc = cn_rx_batch(h->rx, d_hdrs, d_payload, stride, n, h->d_aout, n + 16, h->d_cpls, n + 16, h->d_res,
-                         stream);
+    int rc = d_psn ? cn_rx_batch_psn(h->rx, d_hdrs, d_psn, d_payload, stride, n, h->d_aout, n + 16, h->d_cpls,
+                                     n + 16, h->d_res, stream)
+                   : cn_rx_batch(h->rx, d_hdrs, d_payload, stride, n, h->d_aout, n + 16, h->d_cpls, n + 16,
+                                 h->d_res, stream);
     if (rc != CN_OK) return rc;
     cn_rx_result r;
     CNB_CUDA(cudaMemcpyAsync(&r, h->d_res, sizeof r, cudaMemcpyDeviceToHost, s));
@@ -339,6 +347,11 @@ extern "C" int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdr
     }
     h->delivered += r.n_completions;
     return CN_OK;
+}
+
+extern "C" int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const void* d_payload,
+                                        uint64_t stride, uint32_t n, void* stream) {
+    return cn_transport_handle_data_psn(h, d_hdrs, nullptr, d_payload, stride, n, stream);
 }
 
 extern "C" int64_t cn_transport_poll_acks(cn_transport* h, cn_ack_rec* out, uint64_t cap) {

@@ -57,6 +57,7 @@ def _setup(L):
     L.cn_transport_poll_transmissions.argtypes = [vp, vp, u64, vp]
     L.cn_transport_poll_transmissions.restype = i64
     L.cn_transport_handle_data.argtypes = [vp, vp, vp, u64, u32, vp]
+    L.cn_transport_handle_data_psn.argtypes = [vp, vp, vp, vp, u64, u32, vp]
     L.cn_transport_poll_acks.argtypes = [vp, vp, u64]
     L.cn_transport_poll_acks.restype = i64
     L.cn_transport_poll_completions.argtypes = [vp, vp, u64]
@@ -80,7 +81,8 @@ class TransportEndpoint:
                  commit_ahead=0, base_rtt_ns=10000.0, cc="none", swift_target_ns=0, dupack_threshold=8,
                  rtx_avoid_prev_path=True, carry_payload=True, max_conns=64, max_batch=1 << 16,
                  log_cap=1 << 16, chunk_pool=1 << 20, arena_bytes=64 << 20, receiver_driven=False,
-                 initial_credit=-1, credit_quantum=32768, credit_bank_quanta=4, policy=0, device="cuda"):
+                 initial_credit=-1, credit_quantum=32768, credit_bank_quanta=4, policy=0,
+                 reliability="selective", device="cuda"):
         L = _lib.lib()
         _setup(L)
         c = TransportConfigC()
@@ -94,6 +96,7 @@ class TransportEndpoint:
         c.chunk_pool, c.arena_bytes = chunk_pool, arena_bytes
         c.receiver_driven, c.initial_credit = (1 if receiver_driven else 0), initial_credit
         c.credit_quantum, c.credit_bank_quanta, c.policy = credit_quantum, credit_bank_quanta, policy
+        c.reliability = {"selective": 0, "ordered": 1}[reliability]
         self.device = torch.device(device)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
@@ -135,12 +138,15 @@ class TransportEndpoint:
         _lib.check(n if n < 0 else 0, "poll_transmissions")
         return out[: min(n, cap)], conn[: min(n, cap)]
 
-    def handle_data(self, hdrs, payload=None, stride=4032, stream=None):
+    def handle_data(self, hdrs, payload=None, stride=4032, stream=None, psn=None):
+        """psn: device int64 conn_psn per packet (ordered reliability)."""
         s = stream or torch.cuda.current_stream(self.device)
         n = hdrs.numel() // 64
         pl = payload.data_ptr() if payload is not None else None
-        _lib.check(self._L.cn_transport_handle_data(self._h, hdrs.data_ptr(), pl, stride, n,
-                                                     ctypes.c_void_p(s.cuda_stream)), "handle_data")
+        _lib.check(self._L.cn_transport_handle_data_psn(self._h, hdrs.data_ptr(),
+                                                         psn.data_ptr() if psn is not None else None, pl,
+                                                         stride, n, ctypes.c_void_p(s.cuda_stream)),
+                   "handle_data")
 
     def poll_acks(self):
         n = self._L.cn_transport_poll_acks(self._h, None, 0)

@@ -267,6 +267,20 @@ class Endpoint {
         return s;
     }
     int64_t outstanding_bytes(int src, int dst) const { return cn_transport_outstanding_bytes(h_, src, dst); }
+    // the rest of Transport's introspection (transport.hpp:101-107)
+    int64_t path_inflight(int src, int dst, int path) const { return cn_transport_path_inflight(h_, src, dst, path); }
+    int64_t window_available(int src, int dst, int path) const {
+        return cn_transport_window_available(h_, src, dst, path);
+    }
+    int64_t conn_credit(int src, int dst) const { return cn_transport_conn_credit(h_, src, dst); }
+    int engine_inflight_msgs(int host, int engine) const { return cn_transport_engine_inflight_msgs(h_, host, engine); }
+    uint64_t engine_dispatched(int host, int engine) const { return cn_transport_engine_dispatched(h_, host, engine); }
+    int64_t engine_gauge(int host, int engine) const { return cn_transport_engine_gauge(h_, host, engine); }
+    // ordered reliability: each packet's conn_psn beside its header
+    void handle_data_psn(const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload, uint64_t stride,
+                         uint32_t n, cudaStream_t s = nullptr) {
+        check(cn_transport_handle_data_psn(h_, d_hdrs, d_psn, d_payload, stride, n, s), "handle_data_psn");
+    }
 
   private:
     cn_transport* h_ = nullptr;

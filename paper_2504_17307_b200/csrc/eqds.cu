@@ -223,6 +223,7 @@ using namespace cnb;
 
 struct cn_eqds {
     EqDev d;
+    int tpb = 128;  // threads (receivers) per block
 };
 
 extern "C" void cn_eqds_config_default(cn_eqds_config* c) {
@@ -242,6 +243,12 @@ extern "C" int cn_eqds_create(const cn_eqds_config* cfg, uint32_t n_receivers, c
     *out = nullptr;
     cn_eqds* h = new (std::nothrow) cn_eqds();
     if (!h) return CN_E_CAPACITY;
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        while (h->tpb > 32 && (n_receivers + h->tpb - 1) / h->tpb < static_cast<uint32_t>(sms)) h->tpb /= 2;
+    }
     EqDev& d = h->d;
     d.n_recv = n_receivers;
     d.max_senders = cfg->max_senders;
@@ -291,7 +298,9 @@ extern "C" int cn_eqds_run(cn_eqds* h, const uint32_t* d_ev_off, const cn_eqds_e
         set_error("cn_eqds_run: bad arguments");
         return CN_E_INVALID;
     }
-    k_eqds_run<<<(h->d.n_recv + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+    // one thread per receiver, each a sequential event loop: spread the
+    // receivers over every SM before stacking warps on one
+    k_eqds_run<<<(h->d.n_recv + h->tpb - 1) / h->tpb, h->tpb, 0, static_cast<cudaStream_t>(stream)>>>(
         h->d, d_ev_off, d_events, end_time, d_log, d_log_n);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;

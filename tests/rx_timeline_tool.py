@@ -19,16 +19,23 @@ def main():
     import paper_2504_17307_b200 as cn
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    data, meta, _ = bench.load_trace("cfg2_32k")
-    data = bench.interleave(data, K)
+    if os.environ.get("SYNTH"):  # SYNTH=<conns>x<bytes>: bench.synth_trace (configs[4] sweep)
+        c_, b_ = (int(v) for v in os.environ["SYNTH"].split("x"))
+        data = bench.synth_trace(c_, b_, seed=1)
+        cb = 32768
+        msg_len = b_
+        K = c_
+    else:
+        data, meta, _ = bench.load_trace("cfg2_32k")
+        data = bench.interleave(data, K)
+        cb = meta["chunk_bytes"]
+        msg_len = int(data["msg_len"][0])
     n = len(data)
-    cb = meta["chunk_bytes"]
-    msg_len = int(data["msg_len"][0])
     hdrs = cn.to_device_records(data, dev)
     st = torch.randint(0, 256, (n * bench.MAX_PL,), dtype=torch.uint8, device=dev)
     tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
                       arena_bytes=K * (msg_len + (1 << 20)), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
-                      max_batch=n, max_conns=64, max_msgs=64)
+                      max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8))
     def step():
         s = torch.cuda.current_stream(dev)
         tr.reset(s)

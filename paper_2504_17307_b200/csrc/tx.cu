@@ -756,13 +756,17 @@ __device__ void commit_chunks(Tx& x) {
     __syncwarp();
 }
 
-// Inlined into every caller.  Resuming a replay across cn_tx_run calls
-// faulted or diverged with some code layouts of this kernel (pump out of
-// line; pump and run_deferred both inlined) and not with others (this one;
-// ptxas -O0); the cause is not pinned down.  test_tx_gpu.py::
-// test_tx_engine_resumes_across_runs and the endpoint introspection tests
-// guard the layout that passes.
+// Inlined into every caller.  Resuming a Swift replay across cn_tx_run
+// calls faults with run_deferred inlined (-DCN_TX_DEFERRED_INLINE) and not
+// with this layout or the pump out of line (-DCN_TX_PUMP_NOINLINE); the
+// cause is not pinned down.  test_tx_gpu.py::
+// test_tx_engine_resumes_across_runs, tests/tx_resume_sweep_tool.py and the
+// endpoint introspection tests guard the layout that passes.
+#ifdef CN_TX_PUMP_NOINLINE  // diagnostic build of the faulting layout
+__device__ __noinline__ void pump(Tx& x, int64_t now) {
+#else
 __device__ __forceinline__ void pump(Tx& x, int64_t now) {  // transport.cpp:232-240
+#endif
     for (;;) {
         commit_chunks(x);
         if (egress(x, now) == 0) break;
@@ -1176,7 +1180,11 @@ __device__ void rts_retry(Tx& x, int64_t now) {
 // or the horizon t (inclusive = true), in the event queue's (time, seq)
 // order: input events were all queued first, so they win ties; a timer due
 // at the deferred pump's time was queued before it (rto > 0), so it wins.
+#ifdef CN_TX_DEFERRED_INLINE  // diagnostic build of the other faulting layout
+__device__ __forceinline__ void run_deferred(Tx& x, int64_t t, bool inclusive) {
+#else
 __device__ void run_deferred(Tx& x, int64_t t, bool inclusive) {
+#endif
     for (;;) {
         // candidates: the RTO timer, the deferred pump, the oldest RTS retry;
         // fired in (time, scheduling seq) order

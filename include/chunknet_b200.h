@@ -299,20 +299,23 @@ int cn_sched_record(cn_sched* s, const uint32_t* d_conn, const int32_t* d_path, 
                     const uint8_t* d_ecn, const uint32_t* d_offsets, uint32_t n_groups, void* stream);
 
 /* ------------------------------------------------------------ tx engine
- * Device sender: ack processing, duplicate-hint fast retransmit, RTO with
- * backoff, and the commit/egress pump of chunknet::Transport
- * (transport.cpp:144-542, 807-942, 1078-1169; RttEstimator cc.hpp:12-35)
- * for congestion control none (OpenLoop), one engine per host, selective
- * mode, DefaultPolicy.  One warp per connection consumes a time-ordered
- * event stream (message submissions, acks delivered at the sender) and
- * fires its own RTO timer in between; every transmission is logged.
- * Path choices (commits and retransmissions) come from the connection's
- * RngStream("transport.conn", stream_index0 + c) and are bit-identical to
- * the reference. */
-/* congestion control on the device (CcConfig::Algo, cc.hpp); global scope.
- * CUBIC is not offered on the device: std::cbrt has no bit-identical
- * device counterpart, so it stays with the host reference. */
-enum { CN_CC_NONE = 0, CN_CC_SWIFT = 2 };
+ * Device sender (chunknet::Transport's sending half, transport.cpp:84-542,
+ * 807-1169; RttEstimator cc.hpp:12-35; OpenLoop / CUBIC / Swift cc.cpp):
+ * message dispatch over each host's engines (home engine or least-loaded
+ * under conn_split), per-engine factory rotation and commit_ahead, per-path
+ * tx / retransmission queues with DRR egress over each engine's ring,
+ * window gating (global or per-path CC scope, credit in receiver-driven
+ * mode), ack / NACK processing, duplicate-hint fast retransmit, RTO with
+ * backoff, go-back-N.  Connections with the same src form one host (the
+ * reference's HostState): one warp per host consumes the host's
+ * time-ordered input events and fires the timers and deferred pumps the run
+ * schedules.  Connection c draws its path choices from
+ * RngStream("transport.conn", stream_index0 + c): number connections in the
+ * order the reference creates them (first send_message per (src, dst)). */
+/* congestion control on the device (CcConfig::Algo, cc.hpp:38-51).  CUBIC's
+ * std::cbrt / std::pow are glibc 2.39's, restated bit-exactly. */
+enum { CN_CC_NONE = 0, CN_CC_CUBIC = 1, CN_CC_SWIFT = 2 };
+enum { CN_CC_SCOPE_GLOBAL = 0, CN_CC_SCOPE_PER_PATH = 1 };
 typedef struct cn_tx_config {
     uint32_t chunk_bytes;         /* TransportConfig::chunk_bytes            */
     uint32_t max_payload;         /* 0 = CN_MAX_PAYLOAD                      */
@@ -321,7 +324,7 @@ typedef struct cn_tx_config {
     int32_t lb_policy;            /* CN_LB_*                                 */
     uint32_t max_inflight_msgs;   /* per engine (128)                        */
     uint32_t max_paths;           /* paths per connection (upper bound)      */
-    uint32_t log_cap;             /* transmit records kept per connection    */
+    uint32_t log_cap;             /* transmit records kept per host          */
     int64_t rto_min;              /* resolved Transport::rto_min_ (> 0)      */
     int64_t rto_max;              /* 0 = 64 * rto_min (transport.cpp:36)     */
     int64_t commit_ahead;         /* Transport::commit_ahead_ (:37-39)       */
@@ -331,7 +334,7 @@ typedef struct cn_tx_config {
     uint64_t chunk_pool;          /* chunk state entries; each connection owns
                                      chunk_pool / n_conns of them as a ring that
                                      a finished message hands back            */
-    int32_t cc_algo;              /* CN_CC_NONE (OpenLoop) | CN_CC_SWIFT     */
+    int32_t cc_algo;              /* CN_CC_*                                 */
     uint32_t drr_quantum;         /* TransportConfig::drr_quantum (32768)    */
     int64_t mss;                  /* CcConfig::mss (4032)                    */
     int64_t cap_bytes;            /* CcConfig::cap_bytes, 0 = uncapped       */
@@ -353,7 +356,11 @@ typedef struct cn_tx_config {
     /* transport policy plug-in (TransportPolicy / set_policy_factory,
      * policy.hpp:39-67): CN_POLICY_*; hooks in include/chunknet_policy.cuh */
     int32_t policy;
-    int32_t pad_pol;
+    int32_t engines;              /* TransportConfig::engines per host (1..16) */
+    int32_t conn_split;           /* TransportConfig::conn_split              */
+    int32_t cc_scope;             /* CcConfig::scope: CN_CC_SCOPE_*           */
+    int32_t ecn_as_loss;          /* CcConfig::ecn_as_loss (CUBIC)            */
+    int32_t pad_cc;
 } cn_tx_config;
 enum {
     CN_POLICY_DEFAULT = 0,      /* DefaultPolicy with lb_policy / rtx_avoid_prev_path */
@@ -364,13 +371,17 @@ enum {
 };
 /* cn_tx_status bits */
 #define CN_TX_STATUS_EMPTY_MSG 1u  /* send_message of 0 bytes (invalid_argument) */
-#define CN_TX_STATUS_CAPACITY 4u   /* chunk ring full */
+#define CN_TX_STATUS_CAPACITY 4u   /* chunk ring / engine ring full */
 #define CN_TX_STATUS_RETRY 8u      /* RTS retry queue full */
 #define CN_TX_STATUS_STALE 16u     /* stale retransmission-queue entries overflow */
 #define CN_TX_STATUS_SENT_ORDER 32u /* go-back-N sent_order overflow */
 #define CN_TX_STATUS_POLICY 64u    /* policy contract violation (logic_error) */
+#define CN_TX_STATUS_LOG 128u      /* a host logged more than log_cap records: some were lost */
+#define CN_TX_STATUS_TIMER 256u    /* more than 8 RTO events armed at one instant */
+#define CN_TX_STATUS_INTERNAL 512u /* event for an unknown connection / corrupt chunk state */
 typedef struct cn_tx_submit { int64_t t; uint64_t len; uint64_t tag; } cn_tx_submit;
-/* one chunk transmission (send_chunk): time, message, chunk index, path */
+/* one chunk transmission (send_chunk): time, message, chunk index, path,
+ * and the connection (cn_tx_create index) and destination it belongs to */
 typedef struct cn_tx_rec {
     int64_t t;
     uint32_t msg_id;
@@ -378,48 +389,80 @@ typedef struct cn_tx_rec {
     int32_t path;
     int32_t is_rtx;
     uint64_t msg_seq;
+    uint32_t conn;
+    int32_t dst;
 } cn_tx_rec;
-typedef struct cn_tx_stats {  /* Transport::Stats sender fields + estimator */
+typedef struct cn_tx_stats {  /* Transport::Stats sender fields (per connection) + estimator */
     uint64_t chunks_sent, chunk_rtx, fast_rtx, rtos, msgs_sent, msgs_completed, backpressured, n_log;
-    int64_t srtt, rttvar;
+    int64_t srtt, rttvar;     /* subs[0]'s RttEstimator */
     int32_t backoff, live_msgs;
-    int64_t cwnd_bytes;   /* CongestionControl::cwnd_bytes() at the end   */
-    int64_t inflight;     /* gated_inflight (global scope) at the end     */
-    double cwnd_pkts;     /* Swift window in packets (unused for none)    */
+    int64_t cwnd_bytes;   /* subs[0]'s CongestionControl::cwnd_bytes() at the end */
+    int64_t inflight;     /* the connection's total inflight at the end */
+    double cwnd_pkts;     /* subs[0]'s window in packets (CUBIC / Swift) */
+    uint64_t rts_sent, decreases;
 } cn_tx_stats;
 typedef struct cn_tx cn_tx;
 void cn_tx_config_default(cn_tx_config* cfg);
+/* h_src: host of each connection (NULL: one host per connection); h_dst,
+ * h_n_paths (NULL: 0, max_paths).  Connection indices are cn_tx_create
+ * order; hosts are numbered by first appearance in h_src. */
 int cn_tx_create(const cn_tx_config* cfg, uint32_t n_conns, const int32_t* h_src, const int32_t* h_dst,
                  const int32_t* h_n_paths, cn_tx** out);
+/* An engine whose connections open one at a time, as the reference's
+ * conn_to creates them (first send_message per (src, dst)): cn_tx_open
+ * returns the new connection's index (>= 0) or a negative status. */
+int cn_tx_create_empty(const cn_tx_config* cfg, uint32_t max_conns, uint32_t max_conns_per_host, cn_tx** out);
+int cn_tx_open(cn_tx* t, int32_t src, int32_t dst, int32_t n_paths);
 void cn_tx_destroy(cn_tx* t);
-/* Events of connection c are d_events[d_ev_off[c] .. d_ev_off[c+1]), each
- * (type << 62) | index: type 0 = d_submits[index], 1 = d_acks[index]
- * (cn_ack_rec::aux = delivery time at the sender), ordered by time (ties:
- * in list order).  Timers fire up to end_time.  d_log holds log_cap records
- * per connection; d_stats one record per connection.  State persists
- * across calls. */
+uint32_t cn_tx_n_hosts(cn_tx* t);
+int32_t cn_tx_conn_host(cn_tx* t, uint32_t conn);
+/* Events of host h are d_events[d_ev_off[h] .. d_ev_off[h+1]), each
+ * (type << 62) | (conn << 40) | index: type 0 = d_submits[index] (a
+ * send_message on connection conn), 1 = d_acks[index] (an ack / NACK /
+ * credit / rts_ack delivered at the host for connection conn; aux = time),
+ * ordered by time (ties: in list order).  Timers fire up to end_time.
+ * d_log holds log_cap records per host (emission order), d_stats one record
+ * per connection.  State persists across calls. */
 int cn_tx_run(cn_tx* t, const uint32_t* d_ev_off, const uint64_t* d_events,
               const cn_tx_submit* d_submits, const cn_ack_rec* d_acks, int64_t end_time,
               cn_tx_rec* d_log, cn_tx_stats* d_stats, void* stream);
 int cn_tx_status(cn_tx* t, unsigned int* out);
-/* Connection state for introspection (Transport::path_inflight,
- * conn_credit, engine_gauge, transport.cpp:1173-1209); synchronous. */
+/* Connection / engine state for introspection (Transport::path_inflight,
+ * conn_credit, window_available, engine_*, transport.cpp:1173-1209);
+ * synchronous. */
 typedef struct cn_tx_conn_state {
     int64_t credit;     /* Connection::credit (receiver-driven bank) */
-    int64_t unchunked;  /* dispatched bytes not yet chunked (its share of the engine gauge) */
+    int64_t unchunked;  /* dispatched bytes not yet chunked */
+    int64_t inflight;   /* sum of the paths' inflight (outstanding_bytes) */
     int32_t n_paths;
+    int32_t opened;     /* conn_to ran (first send_message) */
+    int32_t home_engine;
     int32_t pad;
 } cn_tx_conn_state;
 int cn_tx_get_conn_state(cn_tx* t, uint32_t conn, cn_tx_conn_state* out,
                          int64_t* h_path_inflight /* [n_paths] or NULL */, uint32_t max_paths);
-/* Diagnostics: the raw device state of one connection (TxConn, per-path
- * arrays, RNG, chunk state of its pool share); returns the byte count (pass
- * h_out = NULL to size).  Used to compare engine states across builds. */
+int cn_tx_window_available(cn_tx* t, uint32_t conn, int32_t path, int64_t* out);
+typedef struct cn_tx_engine_state {
+    int32_t inflight_msgs, ring_len;
+    uint64_t dispatched;
+    int64_t gauge, committed_unsent;
+} cn_tx_engine_state;
+/* engine `engine` of the host connection `conn` belongs to */
+int cn_tx_get_engine_state(cn_tx* t, uint32_t conn, int32_t engine, cn_tx_engine_state* out);
+/* Diagnostics: the raw device state of one connection (its shared-memory
+ * image, global state, host image, chunk state of its pool share); returns
+ * the byte count (pass h_out = NULL to size). */
 int64_t cn_tx_debug_state(cn_tx* t, uint32_t conn, void* h_out, uint64_t cap);
-/* Transmit records logged per connection so far (host array of n_conns);
- * cn_tx_log_clear restarts every connection's log at 0. */
+/* Transmit records logged per host so far (host array of n_hosts, counting
+ * records lost to log_cap); cn_tx_log_consume drops the first h_n[h]
+ * records of each host's log (moving the rest to the front);
+ * cn_tx_log_clear restarts every log at 0. */
 int cn_tx_log_counts(cn_tx* t, uint32_t* h_out);
+int cn_tx_log_consume(cn_tx* t, cn_tx_rec* d_log, const uint32_t* h_n);
 int cn_tx_log_clear(cn_tx* t, void* stream);
+/* The device restatement of glibc's cbrt (mode 0) / pow(x, 3.0) (mode 1)
+ * that CUBIC uses, over n doubles (parity hook) */
+int cn_libm_eval(int mode, const double* d_in, double* d_out, uint64_t n, void* stream);
 
 /* --------------------------------------------------------- send side
  * Transport::send_chunk's packetization (transport.cpp:433-494) for all
@@ -483,13 +526,16 @@ int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, 
  * path (cn_rx), driven by the caller's clock.  The reference's synchronous
  * calls become queued events: send_message / handle_acks queue at their
  * time, cn_transport_advance runs the device sender up to a time, and the
- * transmissions, acks and completions are polled.  Supported: one engine
- * per host, selective or ordered reliability (ordered: one path, data
- * through cn_transport_handle_data_psn), the policies of chunknet_policy.cuh, CC
- * none or Swift (global scope), sender- or receiver-driven (credit and
- * rts_ack records through cn_transport_handle_acks; initial_credit resolved
- * to one BDP by the caller); other settings are rejected with
- * CN_E_UNSUPPORTED. */
+ * transmissions, acks and completions are polled.  Every TransportConfig
+ * the reference accepts is supported: engines (home or conn_split
+ * dispatch), selective or ordered reliability (ordered: one path, data
+ * through cn_transport_handle_data_psn), the policies of
+ * chunknet_policy.cuh, CC none / CUBIC / Swift with global or per-path
+ * scope, sender- or receiver-driven (credit and rts_ack records through
+ * cn_transport_handle_acks; initial_credit resolved to one BDP by the
+ * caller).  Connections open in the order send_message first names them
+ * (conn_to), which fixes their RngStream index: call send_message in time
+ * order. */
 typedef struct cn_transport_config {
     /* TransportConfig (transport.hpp:23-51) */
     int32_t engines, conn_split, paths;
@@ -514,6 +560,8 @@ typedef struct cn_transport_config {
     uint32_t max_conns, max_batch, log_cap;
     int32_t policy;                      /* CN_POLICY_* (set_policy_factory, transport.hpp:95) */
     uint64_t chunk_pool, arena_bytes;
+    uint32_t max_conns_per_host;         /* connections one source host may open (0 = as many as fit) */
+    uint32_t pad_mcph;
 } cn_transport_config;
 typedef struct cn_stats {  /* Transport::Stats (transport.hpp:62-75) */
     uint64_t msgs_sent, msgs_completed, backpressured, chunks_sent, chunk_rtx, fast_rtx, rtos,

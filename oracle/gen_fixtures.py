@@ -418,6 +418,172 @@ def gen_eqds():
     print(f"eqds: -> {os.path.getsize(path)} B")
 
 
+# ------------------------------------------------------------ host-level
+# One source host with several connections (fan-out), engines, conn_split,
+# CUBIC and per-path CC scope: the host's submissions and the acks the DES
+# delivered to it, replayed into a fresh reference Transport per config
+# (ref_harness.cpp cnref_host_replay).  The per-host engine state
+# (commit_ahead, factory rotation, DRR ring, max_inflight_msgs, pumps of
+# every engine after an ack, transport.cpp:198-431, 941) couples the
+# connections; only a host-level replay pins it.
+HOST_DES = {
+    # 1 -> 3 destinations on a k=8 fat tree (two inter-pod, one intra-pod),
+    # CUBIC DES sender, 1% loss, two messages outstanding per connection
+    "fanout_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=256 * 1024, loss=0.01,
+                       seed=21, chunk_bytes=16384, paths=16, lb="p2_rtt", cc="cubic", window=2),
+                  [(0, 127, 400_000, 4), (0, 64, 300_000, 4), (0, 9, 250_000, 4)], 0),
+    # the same under Swift in the DES (its acks answer a Swift sender)
+    "fanout_swift": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=256 * 1024, loss=0.01,
+                          seed=22, chunk_bytes=16384, paths=16, lb="p2_rtt", cc="swift", window=2),
+                     [(0, 127, 400_000, 4), (0, 64, 300_000, 4), (0, 9, 250_000, 4)], 0),
+    # receiver-driven (EQDS): one sender to three receivers, credit-gated
+    "fanout_rd": (dict(topo="star", topo_arg=5, rate_bps=100e9, qcap_bytes=128 * 1024, loss=0.01, seed=23,
+                       chunk_bytes=16384, paths=1, lb="oblivious", cc="none", receiver_driven=True, window=2),
+                  [(0, 1, 512 * 1024, 3), (0, 2, 256 * 1024, 3), (0, 3, 300_000, 3)], 0),
+    # multiple engines in the DES itself (home engines by load, conn_split)
+    # per-path CC scope in the DES (closed loop for the per-path replays)
+    "fanout_pp": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=256 * 1024, loss=0.01,
+                       seed=26, chunk_bytes=16384, paths=16, lb="p2_rtt", cc="cubic", cc_scope=1, window=2),
+                  [(0, 127, 400_000, 4), (0, 64, 300_000, 4), (0, 9, 250_000, 4)], 0),
+    "fanout_swift_pp": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=256 * 1024, loss=0.01,
+                             seed=27, chunk_bytes=16384, paths=16, lb="p2_ecn", cc="swift", cc_scope=1, window=2),
+                        [(0, 127, 400_000, 4), (0, 64, 300_000, 4), (0, 9, 250_000, 4)], 0),
+    "rd_swift": (dict(topo="star", topo_arg=5, rate_bps=100e9, qcap_bytes=128 * 1024, loss=0.01, seed=28,
+                      chunk_bytes=16384, paths=1, lb="oblivious", cc="swift", receiver_driven=True, window=2),
+                 [(0, 1, 512 * 1024, 3), (0, 2, 256 * 1024, 3), (0, 3, 300_000, 3)], 0),
+    "split_swift": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=256 * 1024, loss=0.02,
+                         seed=29, chunk_bytes=8064, paths=16, lb="p2_rtt", cc="swift", engines=2, conn_split=1,
+                         window=3), [(0, 127, 300_000, 5), (0, 64, 200_000, 5), (0, 9, 100_000, 4)], 0),
+    "engines_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=256 * 1024, loss=0.02,
+                        seed=24, chunk_bytes=8064, paths=16, lb="p2_rtt", cc="cubic", engines=4, window=3),
+                   [(0, 127, 300_000, 5), (0, 64, 200_000, 5), (0, 100, 150_000, 5), (0, 9, 120_000, 5)], 0),
+    "split_k8": (dict(topo="fat_tree", topo_arg=8, rate_bps=100e9, qcap_bytes=256 * 1024, loss=0.02,
+                      seed=25, chunk_bytes=8064, paths=16, lb="p2_rtt", cc="cubic", engines=3, conn_split=1,
+                      window=3), [(0, 127, 300_000, 5), (0, 64, 200_000, 5)], 0),
+    # BASELINE configs[0] / [1] under CUBIC, the reference default: the DES
+    # sender ran CUBIC, so the CUBIC replay is the DES sender itself
+    "cfg1": (None, None, 0),
+    "cfg2_32k": (None, None, 0),
+    "k8_4x1m": (None, None, 0),
+    "lossy_2m": (None, None, 0),
+    "csn_wrap": (None, None, 0),
+}
+# name -> list of (tag, replay overrides)
+HOST_REPLAYS = {
+    "fanout_k8": [("none", dict(cc="none")), ("cubic", dict(cc="cubic")), ("swift", dict(cc="swift")),
+                  ("cubic_pp", dict(cc="cubic", cc_scope=1)), ("swift_pp", dict(cc="swift", cc_scope=1)),
+                  ("e2", dict(cc="cubic", engines=2)), ("e4split", dict(cc="cubic", engines=4, conn_split=True)),
+                  ("swift_e3split", dict(cc="swift", engines=3, conn_split=True)),
+                  ("inflight2", dict(cc="none", max_inflight_msgs=2)),
+                  ("rr", dict(cc="swift", policy=1)), ("single", dict(cc="none", policy=2))],
+    "fanout_swift": [("swift", dict(cc="swift")), ("swift_pp", dict(cc="swift", cc_scope=1)),
+                     ("cubic", dict(cc="cubic")), ("swift_e2", dict(cc="swift", engines=2))],
+    "fanout_rd": [("none", dict(cc="none")), ("swift", dict(cc="swift")), ("cubic", dict(cc="cubic"))],
+    "fanout_pp": [("cubic_pp", dict(cc="cubic", cc_scope=1)), ("cubic", dict(cc="cubic")),
+                  ("swift_pp_e2", dict(cc="swift", cc_scope=1, engines=2))],
+    "fanout_swift_pp": [("swift_pp", dict(cc="swift", cc_scope=1)),
+                        ("swift_pp_e4split", dict(cc="swift", cc_scope=1, engines=4, conn_split=True))],
+    "rd_swift": [("swift", dict(cc="swift")), ("swift_pp", dict(cc="swift", cc_scope=1))],
+    "split_swift": [("swift_e2split", dict(cc="swift", engines=2, conn_split=True)),
+                    ("cubic_e2split", dict(cc="cubic", engines=2, conn_split=True))],
+    "engines_k8": [("cubic_e4", dict(cc="cubic", engines=4)), ("cubic_e4split", dict(cc="cubic", engines=4,
+                                                                                      conn_split=True)),
+                   ("swift_e2", dict(cc="swift", engines=2)), ("cubic_pp_e4", dict(cc="cubic", engines=4,
+                                                                                   cc_scope=1))],
+    "split_k8": [("cubic_e3split", dict(cc="cubic", engines=3, conn_split=True)),
+                 ("none_e3split", dict(cc="none", engines=3, conn_split=True)),
+                 ("swift_pp_e2split", dict(cc="swift", engines=2, conn_split=True, cc_scope=1))],
+    "cfg1": [("cubic", dict(cc="cubic")), ("cubic_pp", dict(cc="cubic", cc_scope=1))],
+    "cfg2_32k": [("cubic", dict(cc="cubic"))],
+    "k8_4x1m": [("cubic", dict(cc="cubic")), ("cubic_e2split", dict(cc="cubic", engines=2, conn_split=True))],
+    "lossy_2m": [("cubic", dict(cc="cubic"))],
+    "csn_wrap": [("cubic", dict(cc="cubic"))],
+}
+
+
+def gen_host(name):
+    kw, flows, src = HOST_DES[name]
+    if kw is None:  # a single-connection scenario recorded above: reuse its sender stimulus
+        kw, flows = SCENARIOS[name]
+        z = np.load(os.path.join(GOLDEN, f"sender_{name}.npz"))
+        acks_des = z["acks"]
+        subs = np.zeros(len(z["submits"]), dtype=ref.HOST_SUBMIT_DTYPE)
+        for f in ("t", "len", "tag"):
+            subs[f] = z["submits"][f]
+        subs["dst"] = flows[0][1]
+        src = flows[0][0]
+        des_cc = kw["cc"]
+    else:
+        kw = dict(kw)
+        window = kw.pop("window", 1)
+        tmp = f"/tmp/cnfix_host_{name}"
+        _, acks_all, _, st = ref.record(tmp, flows=flows, window=window, **kw)
+        assert st["quiesced"] == 1, (name, st)
+        assert st["bytes_ok"] == st["completions"], (name, st)
+        sl = st["submits"]
+        sl = sl[sl["src"] == src]
+        acks_des = acks_all[acks_all["dst"] == src]
+        subs = np.zeros(len(sl), dtype=ref.HOST_SUBMIT_DTYPE)
+        for f in ("t", "len", "tag", "dst"):
+            subs[f] = sl[f]
+        des_cc = kw["cc"]
+    rkw = {k: kw[k] for k in ("topo", "topo_arg", "rate_bps", "qcap_bytes", "seed", "chunk_bytes", "paths", "lb",
+                              "receiver_driven", "ordered") if k in kw}
+    # an open-loop replay (the DES ran another sender) can end in an RTO
+    # storm once the recorded acks run out: stop 20 ms after the last input
+    t_last = max(int(subs["t"].max()), int(acks_des["aux"].max()) if len(acks_des) else 0)
+    rkw["cutoff_ns"] = t_last + 20_000_000
+    for tag, over in HOST_REPLAYS[name]:
+        r = dict(rkw)
+        r.update(over)
+        tx, stt, conns = ref.host_replay(acks_des, subs, src, **r)
+        rate = kw.get("rate_bps", 400e9)
+        bdp = int(round(rate * stt["base_rtt"] / 8e9))
+        commit_ahead = max(2 * kw["chunk_bytes"], 2 * 32768, bdp)
+        assert commit_ahead == stt["commit_ahead"], (commit_ahead, stt["commit_ahead"])
+        cc = r.get("cc", "none")
+        meta = dict(name=f"{name}_{tag}", src=int(src), conns=[int(c) for c in conns], chunk_bytes=kw["chunk_bytes"],
+                    lb=r["lb"], seed=kw["seed"], paths=int(r["paths"]), base_rtt=int(stt["base_rtt"]),
+                    rto_min=int(stt["rto_min"]), rto_max=int(stt["rto_max"]), commit_ahead=commit_ahead,
+                    end_time=int(stt["end_time"]), stats={k: int(v) for k, v in stt.items()}, cc=cc,
+                    cc_scope=int(r.get("cc_scope", 0)), engines=int(r.get("engines", 1)),
+                    conn_split=bool(r.get("conn_split", False)), des_cc=des_cc,
+                    receiver_driven=bool(r.get("receiver_driven", False)), initial_credit=int(stt["bdp"]),
+                    policy=POLICY_ENGINE_ID[r.get("policy", 0)],
+                    max_inflight_msgs=int(r.get("max_inflight_msgs", 0)) or 128,
+                    swift_target_ns=3 * int(stt["base_rtt"]) if cc == "swift" else 0,
+                    topo=kw.get("topo"), topo_arg=kw.get("topo_arg"))
+        # the reference's path count per connection: min(paths, path_count(src, dst))
+        meta["n_paths"] = [int(x) for x in _path_counts(kw, src, conns)]
+        path = os.path.join(GOLDEN, f"host_{name}_{tag}.npz")
+        np.savez_compressed(path, acks=acks_des, submits=subs, tx=tx,
+                            meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
+        print(f"  host_{name}_{tag}: conns={len(conns)} submits={len(subs)} acks={len(acks_des)} tx={len(tx)} "
+              f"rtx={stt['chunk_rtx']} fast={stt['fast_rtx']} rtos={stt['rtos']} done={stt['msgs_completed']}"
+              f" rts={stt['rts_sent']}")
+
+
+def _path_counts(kw, src, conns):
+    """min(paths, topo.path_count(src, dst)) per connection (conn_to,
+    transport.cpp:97-99): fat tree k -- same edge switch 1, same pod k/2,
+    other pod k^2/4 (topology.cpp:47-56); star 1."""
+    out = []
+    for dst in conns:
+        if kw.get("topo") == "star":
+            pc = 1
+        else:
+            k = kw["topo_arg"]
+            per_edge, per_pod = k // 2, (k // 2) * (k // 2)
+            if src // per_edge == dst // per_edge:
+                pc = 1
+            elif src // per_pod == dst // per_pod:
+                pc = k // 2
+            else:
+                pc = per_pod
+        out.append(min(kw["paths"], pc) if src != dst else 1)
+    return out
+
+
 def gen_rng():
     """RngStream / select_path draw sequences (rng.hpp:29-60, lb.cpp:7-27).
 
@@ -468,6 +634,13 @@ def main(argv):
             continue
         if n == "rng":
             gen_rng()
+            continue
+        if n == "host":
+            for m in HOST_DES:
+                gen_host(m)
+            continue
+        if n.startswith("host_"):
+            gen_host(n[5:])
             continue
         if n == "eqds":
             gen_eqds()

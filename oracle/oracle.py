@@ -52,6 +52,8 @@ def lib():
         L.orc_next_below_seq.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]
         L.orc_next_double_seq.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
         L.orc_fnv1a64.restype = u64
+        L.orc_libm.argtypes = [i32, i32, vp, vp, u64]
+        L.orc_libm.restype = None
         L.orc_fnv1a64.argtypes = [ctypes.c_char_p]
         L.orc_splitmix64.restype = u64
         L.orc_splitmix64.argtypes = [u64]
@@ -157,3 +159,26 @@ def next_double(seed, name, index, count):
     out = np.zeros(count, dtype=np.float64)
     lib().orc_next_double_seq(seed, name.encode(), index, count, _ptr(out))
     return out
+
+
+def libm(mode, x, restated=False):
+    """mode 0 cbrt / 1 pow(x, 3.0) over a float64 array: the host libm the
+    reference links (restated=False) or the C restatement (libm_restate.c)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    lib().orc_libm(mode, 1 if restated else 0, x.ctypes.data_as(ctypes.c_void_p),
+                   out.ctypes.data_as(ctypes.c_void_p), len(x))
+    return out
+
+
+def libm_test_inputs(n, seed=0):
+    """Doubles over CUBIC's argument ranges (t - K in [-200, 200], cube-root
+    arguments w_max * 0.3 / 0.4 up to 1e7) plus every exponent, both signs."""
+    rs = np.random.default_rng(seed)
+    q = n // 4
+    a = (rs.random(q) - 0.5) * 400.0
+    b = rs.random(q) * 1e7
+    c = rs.random(q) * 1e-3
+    bits = rs.integers(0, 0x7FEFFFFFFFFFFFFF, size=n - 3 * q, dtype=np.int64)
+    d = bits.view(np.float64) * np.where(rs.random(n - 3 * q) < 0.5, -1.0, 1.0)
+    return np.concatenate([a, b, c, d, [0.0, -0.0, 1.0, -1.0, 8.0, 27.0, 0.75, 1e-300, 5e-324]])

@@ -79,6 +79,9 @@ SUBMIT_LOG_DTYPE = np.dtype([("t", "<i8"), ("len", "<u8"), ("tag", "<u8"), ("src
                              ("dst", "<i4")])
 TX_DTYPE = np.dtype([("t", "<i8"), ("msg_id", "<u4"), ("chunk", "<u4"), ("path", "<i4"),
                      ("is_rtx", "<i4"), ("msg_seq", "<u8")])
+HOST_TX_DTYPE = np.dtype([("t", "<i8"), ("msg_id", "<u4"), ("chunk", "<u4"), ("path", "<i4"),
+                          ("is_rtx", "<i4"), ("msg_seq", "<u8"), ("conn", "<u4"), ("dst", "<i4")])
+HOST_SUBMIT_DTYPE = np.dtype([("t", "<i8"), ("len", "<u8"), ("tag", "<u8"), ("dst", "<i4"), ("pad", "<i4")])
 
 _lib = None
 
@@ -110,6 +113,10 @@ def lib():
         L.cnref_sender_replay_bench.restype = ctypes.c_double
         L.cnref_set_probes.argtypes = [vp, u32, vp, u32]
         L.cnref_set_probes.restype = None
+        L.cnref_host_replay.argtypes = [ctypes.POINTER(Scenario), i32, vp, u64, vp, u64, vp, u64,
+                                        ctypes.POINTER(SenderStats), vp, u32, i32, i32]
+        L.cnref_set_host_probes.argtypes = [vp, u32, vp, u32, u32]
+        L.cnref_set_host_probes.restype = None
         L.cnref_rng_u64.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
         L.cnref_next_below.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]
         L.cnref_next_double.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
@@ -193,6 +200,44 @@ def sender_replay(acks, submits, src, dst, *, topo="fat_tree", topo_arg=8, rate_
     if rc != 0:
         raise RuntimeError(lib().cnref_last_error().decode())
     res = out[: min(st.n_tx, max_out)].copy(), {k: getattr(st, k) for k, _ in SenderStats._fields_}
+    return res + (probes,) if probe_t is not None else res
+
+
+def host_replay(acks, submits, src, *, topo="fat_tree", topo_arg=8, rate_bps=400e9, link_delay_ns=1000,
+                qcap_bytes=1 << 20, seed=1, chunk_bytes=32768, paths=8, lb="p2_rtt", cc="none", cc_scope=0,
+                engines=1, conn_split=False, dupack_threshold=8, rto_min=0, cutoff_ns=60_000_000_000,
+                max_out=1 << 21, receiver_driven=False, ordered=False, policy=0, ecn_as_loss=False,
+                max_inflight_msgs=0, probe_t=None, probe_conns=0, probe_paths=0):
+    """The reference sender of one source host (ref_harness.cpp
+    cnref_host_replay): submits HOST_SUBMIT_DTYPE (t, len, tag, dst), acks
+    delivered at `src` -> (tx log HOST_TX_DTYPE in emission order, stats,
+    dst per connection index in creation order[, probes])."""
+    sc = Scenario(0 if topo == "star" else 1, topo_arg, rate_bps, link_delay_ns, qcap_bytes, 0.0,
+                  seed, chunk_bytes, paths, LB[lb], CC[cc], cc_scope, engines, 1 if conn_split else 0,
+                  dupack_threshold, rto_min, 0, 1, cutoff_ns, 0, 0, 1 if receiver_driven else 0,
+                  1 if ordered else 0, policy, 0)
+    sb = np.ascontiguousarray(submits, dtype=HOST_SUBMIT_DTYPE)
+    acks = np.ascontiguousarray(acks, dtype=ACK_DTYPE)
+    out = np.zeros(max_out, dtype=HOST_TX_DTYPE)
+    conns = np.full(4096, -1, dtype=np.int32)
+    st = SenderStats()
+    probes = None
+    if probe_t is not None:
+        pt = np.ascontiguousarray(probe_t, dtype=np.int64)
+        probes = np.zeros((len(pt), 3 * engines + probe_conns * (2 + 2 * probe_paths)), dtype=np.int64)
+        lib().cnref_set_host_probes(_ptr(pt), len(pt), _ptr(probes), probe_conns, probe_paths)
+    try:
+        rc = lib().cnref_host_replay(ctypes.byref(sc), src, _ptr(sb), len(sb), _ptr(acks), len(acks), _ptr(out),
+                                     max_out, ctypes.byref(st), _ptr(conns), len(conns), 1 if ecn_as_loss else 0,
+                                     max_inflight_msgs)
+    finally:
+        if probe_t is not None:
+            lib().cnref_set_host_probes(None, 0, None, 0, 0)
+    if rc != 0:
+        raise RuntimeError(lib().cnref_last_error().decode())
+    n_conns = int(st.n_paths)
+    res = (out[: min(st.n_tx, max_out)].copy(), {k: getattr(st, k) for k, _ in SenderStats._fields_},
+           conns[:n_conns].copy())
     return res + (probes,) if probe_t is not None else res
 
 

@@ -737,6 +737,209 @@ int cnref_sender_replay(const cnref_scenario* sc, int src, int dst, const cnref_
     }
 }
 
+// ------------------------------------------------------ host-level replay
+// The reference sender of ONE source host with several connections (fan-out,
+// engines, conn_split): every send_message of `src` (to its dst) and every
+// ack / NACK / credit / rts_ack delivered at `src`, at their times, into a
+// fresh Transport over a blackhole.  Connections open lazily in the
+// replay's own conn_to order; conns_out[k] = dst of connection index k.
+// Transmissions are logged in emission order with the connection index.
+struct cnref_host_submit {
+    int64_t t;
+    uint64_t len;
+    uint64_t tag;
+    int32_t dst;
+    int32_t pad;
+};
+
+struct cnref_host_tx {
+    int64_t t;
+    uint32_t msg_id;
+    uint32_t chunk;
+    int32_t path;
+    int32_t is_rtx;
+    uint64_t msg_seq;
+    uint32_t conn;
+    int32_t dst;
+};
+
+// probes: at each t[i], per engine e (inflight_msgs, dispatched, gauge), then
+// per connection k < n_conn_probe: (outstanding, credit, then per path p <
+// n_path_probe: path_inflight, window_available)
+thread_local std::vector<int64_t> g_hprobe_t;
+thread_local int64_t* g_hprobe_out = nullptr;
+thread_local uint32_t g_hprobe_conns = 0, g_hprobe_paths = 0;
+
+void cnref_set_host_probes(const int64_t* t, uint32_t n, int64_t* out, uint32_t n_conns, uint32_t n_paths) {
+    g_hprobe_t.assign(t, t + n);
+    g_hprobe_out = out;
+    g_hprobe_conns = n_conns;
+    g_hprobe_paths = n_paths;
+}
+
+int cnref_host_replay(const cnref_scenario* sc, int src, const cnref_host_submit* subs, uint64_t n_subs,
+                      const cn_ack_rec* acks, uint64_t n_acks, cnref_host_tx* out, uint64_t max_out,
+                      cnref_sender_stats* st, int32_t* conns_out, uint32_t max_conns, int32_t ecn_as_loss,
+                      int32_t max_inflight_msgs) {
+    try {
+        Topology topo =
+            sc->topo_kind == 0 ? build_star(sc->topo_arg) : build_fat_tree(sc->topo_arg);
+        NetParams np;
+        np.rate_bps = sc->rate_bps;
+        np.link_delay_ns = sc->link_delay_ns;
+        np.qcap_bytes = sc->qcap_bytes;
+        np.mode = static_cast<QueueMode>(sc->queue_mode);
+        if (sc->trim_depth > 0) np.trim_queue_depth = sc->trim_depth;
+        EventQueue eq;
+        Network net(topo, np, eq, sc->seed);
+        net.inject_loss_at_host_egress(1.0);
+        TransportConfig tc;
+        tc.chunk_bytes = sc->chunk_bytes;
+        tc.paths = sc->paths;
+        tc.lb = static_cast<LbPolicy>(sc->lb);
+        tc.cc.algo = static_cast<CcConfig::Algo>(sc->cc);
+        tc.cc.scope = static_cast<CcConfig::Scope>(sc->cc_scope);
+        tc.cc.ecn_as_loss = ecn_as_loss != 0;
+        if (tc.cc.algo == CcConfig::Algo::swift) tc.cc.swift_target_ns = 3 * net.base_rtt_ns();
+        tc.engines = sc->engines;
+        tc.conn_split = sc->conn_split != 0;
+        if (max_inflight_msgs > 0) tc.max_inflight_msgs = max_inflight_msgs;
+        tc.dupack_threshold = sc->dupack_threshold;
+        tc.rto_min = sc->rto_min;
+        tc.receiver_driven = sc->receiver_driven != 0;
+        if (sc->ordered) tc.reliability = TransportConfig::Reliability::ordered;
+        g_ordered = sc->ordered != 0;
+        Transport tr(net, eq, tc, sc->seed);
+        install_policy(tr, sc->policy, tc.chunk_bytes);
+        std::map<int, int64_t> ctl_lat;  // per destination: one-way control latency (RTS logging)
+        if (tc.receiver_driven) {
+            for (uint64_t k = 0; k < n_subs; ++k) {
+                const int dst = subs[k].dst;
+                if (ctl_lat.count(dst)) continue;
+                tr.pacers_[dst].reset();  // the recorded credits drive the sender
+                int64_t lat = -1;
+                const int64_t t_start = eq.now();
+                Packet probe;
+                probe.kind = PacketKind::rts;
+                probe.src = src;
+                probe.dst = dst;
+                net.set_trace([&](const TraceEvent& te) {
+                    if (std::strcmp(te.event, "deliver") == 0 && te.pkt->kind == PacketKind::rts) lat = te.t - t_start;
+                });
+                net.inject(std::move(probe));
+                eq.run_until_idle(int64_t{1} << 40);
+                if (lat < 0) throw std::runtime_error("control latency probe lost");
+                ctl_lat[dst] = lat;
+            }
+        }
+        const int64_t t0 = eq.now();
+        uint64_t n_out = 0;
+        // the first packet of each send_chunk call (its packets are injected
+        // back to back): a new (dst, msg, chunk) or a restart of the same one
+        int last_dst = -1;
+        uint64_t last_key = ~uint64_t{0};
+        uint32_t last_sq = 0;
+        auto conn_of = [&](int dst) -> int {
+            auto it = tr.hosts_[src].conn_by_dst.find(dst);
+            return it == tr.hosts_[src].conn_by_dst.end() ? -1 : it->second;
+        };
+        net.set_trace([&](const TraceEvent& te) {
+            if (tc.receiver_driven && std::strcmp(te.event, "deliver") == 0 && te.pkt->kind == PacketKind::rts) {
+                if (n_out < max_out) {
+                    cnref_host_tx& r = out[n_out];
+                    r.t = te.t - ctl_lat[te.pkt->dst] - t0;
+                    r.msg_id = 0;
+                    r.chunk = 0xFFFFFFFFu;  // RTS record
+                    r.path = -1;
+                    r.is_rtx = te.pkt->is_rtx ? 1 : 0;
+                    r.msg_seq = te.pkt->demand_bytes;
+                    r.conn = static_cast<uint32_t>(conn_of(te.pkt->dst));
+                    r.dst = te.pkt->dst;
+                }
+                ++n_out;
+                return;
+            }
+            if (std::strcmp(te.event, "loss") != 0) return;
+            const Packet& p = *te.pkt;
+            if (p.kind != PacketKind::data) return;
+            const uint64_t key = (static_cast<uint64_t>(p.msg_seq) << 32) ^ (p.chunk_offset / tc.chunk_bytes);
+            const bool first = p.dst != last_dst || key != last_key || p.seq_in_chunk <= last_sq;
+            last_dst = p.dst;
+            last_key = key;
+            last_sq = p.seq_in_chunk;
+            if (!first) return;
+            if (n_out < max_out) {
+                cnref_host_tx& r = out[n_out];
+                r.t = te.t - t0;
+                r.msg_id = p.hdr.msg_id;
+                r.chunk = static_cast<uint32_t>(p.chunk_offset / tc.chunk_bytes);
+                r.path = p.path_id | static_cast<int32_t>(p.seq_in_chunk << 16);
+                r.is_rtx = p.is_rtx ? 1 : 0;
+                r.msg_seq = p.msg_seq;
+                r.conn = static_cast<uint32_t>(conn_of(p.dst));
+                r.dst = p.dst;
+            }
+            ++n_out;
+        });
+        for (uint64_t k = 0; k < n_subs; ++k) {
+            cnref_host_submit sb = subs[k];
+            eq.schedule(t0 + sb.t, [&tr, src, sb] { tr.send_message(src, sb.dst, sb.len, sb.tag); });
+        }
+        for (uint64_t k = 0; k < n_acks; ++k) {
+            cn_ack_rec a = acks[k];
+            eq.schedule(t0 + a.aux, [&tr, a, t0] {
+                Packet p = from_ack(a);
+                p.echo_tx_time += t0;
+                int host = p.dst;
+                tr.handle_packet(host, std::move(p));
+            });
+        }
+        for (size_t i = 0; i < g_hprobe_t.size(); ++i) {
+            const uint32_t ne = static_cast<uint32_t>(tc.engines), nk = g_hprobe_conns, npp = g_hprobe_paths;
+            int64_t* o = g_hprobe_out + i * (3 * ne + nk * (2 + 2 * npp));
+            eq.schedule(t0 + g_hprobe_t[i], [&tr, o, ne, nk, npp, src] {
+                int64_t* q = o;
+                for (uint32_t e = 0; e < ne; ++e) {
+                    *q++ = tr.engine_inflight_msgs(src, static_cast<int>(e));
+                    *q++ = static_cast<int64_t>(tr.engine_dispatched(src, static_cast<int>(e)));
+                    *q++ = tr.engine_gauge(src, static_cast<int>(e));
+                }
+                for (uint32_t k = 0; k < nk; ++k) {
+                    const int dst = k < tr.conns_.size() ? tr.conns_[k].dst : -1;
+                    *q++ = dst >= 0 ? tr.outstanding_bytes(src, dst) : 0;
+                    *q++ = dst >= 0 ? tr.conn_credit(src, dst) : 0;
+                    for (uint32_t p = 0; p < npp; ++p) {
+                        *q++ = dst >= 0 ? tr.path_inflight(src, dst, static_cast<int>(p)) : 0;
+                        *q++ = dst >= 0 ? tr.window_available(src, dst, static_cast<int>(p)) : 0;
+                    }
+                }
+            });
+        }
+        eq.run_until_idle(sc->cutoff_ns);
+        for (size_t k = 0; k < tr.conns_.size() && k < max_conns; ++k) conns_out[k] = tr.conns_[k].dst;
+        if (st) {
+            st->chunks_sent = tr.stats().chunks_sent;
+            st->chunk_rtx = tr.stats().chunk_rtx;
+            st->fast_rtx = tr.stats().fast_rtx;
+            st->rtos = tr.stats().rtos;
+            st->msgs_completed = tr.stats().msgs_completed;
+            st->n_tx = n_out;
+            st->base_rtt = net.base_rtt_ns();
+            st->rto_min = tr.rto_min_;
+            st->rto_max = tr.rto_max_;
+            st->end_time = eq.now() - t0;
+            st->n_paths = static_cast<int>(tr.conns_.size());  // connections opened
+            st->bdp = net.bdp_bytes();
+            st->commit_ahead = tr.commit_ahead_;
+            st->rts_sent = tr.stats().rts_sent;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // Times the reference sender on the same replay (construction and event
 // scheduling outside the timer): T threads x reps replays.  Returns the
 // slowest thread's seconds.

@@ -60,7 +60,20 @@ class TxConfig(ctypes.Structure):
                 ("receiver_driven", ctypes.c_int32), ("credit_quantum", ctypes.c_uint32),
                 ("credit_bank_quanta", ctypes.c_int32), ("pad_rd", ctypes.c_int32),
                 ("initial_credit", ctypes.c_int64), ("ordered", ctypes.c_int32),
-                ("sent_order_cap", ctypes.c_uint32), ("policy", ctypes.c_int32), ("pad_pol", ctypes.c_int32)]
+                ("sent_order_cap", ctypes.c_uint32), ("policy", ctypes.c_int32), ("engines", ctypes.c_int32),
+                ("conn_split", ctypes.c_int32), ("cc_scope", ctypes.c_int32), ("ecn_as_loss", ctypes.c_int32),
+                ("pad_cc", ctypes.c_int32)]
+
+
+class TxConnState(ctypes.Structure):
+    _fields_ = [("credit", ctypes.c_int64), ("unchunked", ctypes.c_int64), ("inflight", ctypes.c_int64),
+                ("n_paths", ctypes.c_int32), ("opened", ctypes.c_int32), ("home_engine", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+class TxEngineState(ctypes.Structure):
+    _fields_ = [("inflight_msgs", ctypes.c_int32), ("ring_len", ctypes.c_int32), ("dispatched", ctypes.c_uint64),
+                ("gauge", ctypes.c_int64), ("committed_unsent", ctypes.c_int64)]
 
 
 class RxResult(ctypes.Structure):
@@ -162,8 +175,23 @@ def _tx_protos(L):
     L.cn_tx_create.argtypes = [ctypes.POINTER(TxConfig), u32, vp, vp, vp, ctypes.POINTER(vp)]
     L.cn_tx_destroy.argtypes = [vp]
     L.cn_tx_destroy.restype = None
+    L.cn_tx_create_empty.argtypes = [ctypes.POINTER(TxConfig), u32, u32, ctypes.POINTER(vp)]
+    L.cn_tx_open.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
     L.cn_tx_run.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp, vp]
     L.cn_tx_status.argtypes = [vp, ctypes.POINTER(ctypes.c_uint)]
+    L.cn_tx_n_hosts.argtypes = [vp]
+    L.cn_tx_n_hosts.restype = u32
+    L.cn_tx_conn_host.argtypes = [vp, u32]
+    L.cn_tx_conn_host.restype = ctypes.c_int32
+    L.cn_tx_log_counts.argtypes = [vp, vp]
+    L.cn_tx_log_consume.argtypes = [vp, vp, vp]
+    L.cn_tx_log_clear.argtypes = [vp, vp]
+    L.cn_tx_get_conn_state.argtypes = [vp, u32, ctypes.POINTER(TxConnState), vp, u32]
+    L.cn_tx_window_available.argtypes = [vp, u32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]
+    L.cn_tx_get_engine_state.argtypes = [vp, u32, ctypes.c_int32, ctypes.POINTER(TxEngineState)]
+    L.cn_tx_debug_state.argtypes = [vp, u32, vp, ctypes.c_uint64]
+    L.cn_tx_debug_state.restype = ctypes.c_int64
+    L.cn_libm_eval.argtypes = [ctypes.c_int, vp, vp, ctypes.c_uint64, vp]
 
 
 USER_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libchunknet_b200_user.so")

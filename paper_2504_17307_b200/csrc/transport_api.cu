@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <map>
+#include <numeric>
 #include <new>
 #include <string>
 #include <utility>
@@ -30,7 +31,8 @@ namespace {
 struct Ev {
     int64_t t;
     uint32_t type;  // 0 submit, 1 ack / NACK (events at one instant: submits first)
-    uint32_t idx;
+    uint32_t conn;
+    uint64_t idx;
 };
 
 template <class T>
@@ -54,7 +56,8 @@ struct cn_transport {
     cn_rx* rx = nullptr;
     cn_tx* tx = nullptr;
     std::map<std::pair<int32_t, int32_t>, int32_t> conn_idx;
-    std::vector<std::vector<Ev>> pend;
+    std::vector<int32_t> conn_src;       // per connection
+    std::vector<std::vector<Ev>> pend;   // per tx host
     std::vector<cn_tx_submit> subs;
     std::vector<cn_ack_rec> acks;
     cn_tx_rec* d_log = nullptr;
@@ -63,7 +66,7 @@ struct cn_transport {
     uint64_t* d_ev = nullptr;
     cn_tx_submit* d_subs = nullptr;
     cn_ack_rec* d_ain = nullptr;
-    uint64_t cap_ev = 0, cap_subs = 0, cap_ain = 0;
+    uint64_t cap_ev = 0, cap_subs = 0, cap_ain = 0, cap_evoff = 0;
     cn_ack_rec* d_aout = nullptr;
     cn_completion* d_cpls = nullptr;
     cn_rx_result* d_res = nullptr;
@@ -117,11 +120,15 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
         set_error("cn_transport_create: ordered reliability with multipath (transport.cpp:21-26)");
         return CN_E_LOGIC;
     }
-    if (cfg->engines != 1 || cfg->conn_split || cfg->reliability < 0 || cfg->reliability > 1 ||
-        (cfg->cc_algo != CN_CC_NONE && cfg->cc_algo != CN_CC_SWIFT) || cfg->cc_scope != 0) {
-        set_error("cn_transport_create: supported: 1 engine, selective reliability, "
-                  "CC none/swift with global scope");
-        return CN_E_UNSUPPORTED;
+    if (cfg->engines < 1 || cfg->engines > 16 || cfg->reliability < 0 || cfg->reliability > 1 ||
+        cfg->cc_algo < CN_CC_NONE || cfg->cc_algo > CN_CC_SWIFT || cfg->cc_scope < 0 || cfg->cc_scope > 1) {
+        set_error("cn_transport_create: engines 1..16, reliability selective / ordered, cc none / cubic / swift, "
+                  "scope global / per_path");
+        return CN_E_INVALID;
+    }
+    if (cfg->reliability == 1 && (cfg->engines != 1 || cfg->conn_split)) {
+        set_error("cn_transport_create: ordered delivery needs a single path and a single engine (transport.cpp:21-26)");
+        return CN_E_LOGIC;
     }
     if (cfg->receiver_driven && cfg->initial_credit < 0) {
         // the reference resolves -1 to one BDP of its Network (transport.cpp:40-44)
@@ -164,7 +171,12 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
     tc.credit_quantum = cfg->credit_quantum;
     tc.credit_bank_quanta = cfg->credit_bank_quanta;
     tc.initial_credit = cfg->receiver_driven ? cfg->initial_credit : 0;
-    int rc = cn_tx_create(&tc, cfg->max_conns, nullptr, nullptr, nullptr, &h->tx);
+    tc.engines = cfg->engines;
+    tc.conn_split = cfg->conn_split;
+    tc.cc_scope = cfg->cc_scope;
+    tc.ecn_as_loss = cfg->ecn_as_loss;
+    tc.cap_bytes = cfg->cap_bytes;
+    int rc = cn_tx_create_empty(&tc, cfg->max_conns, cfg->max_conns_per_host, &h->tx);
     if (rc != CN_OK) {
         cn_transport_destroy(h);
         return rc;
@@ -187,7 +199,6 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
     const uint64_t nc = cfg->max_conns, nb = cfg->max_batch + 16ull;
     bool ok = cudaMalloc(&h->d_log, nc * cfg->log_cap * sizeof(cn_tx_rec)) == cudaSuccess &&
               cudaMalloc(&h->d_stats, nc * sizeof(cn_tx_stats)) == cudaSuccess &&
-              cudaMalloc(&h->d_evoff, (nc + 1) * 4) == cudaSuccess &&
               cudaMalloc(&h->d_aout, nb * sizeof(cn_ack_rec)) == cudaSuccess &&
               cudaMalloc(&h->d_cpls, nb * sizeof(cn_completion)) == cudaSuccess &&
               cudaMalloc(&h->d_res, sizeof(cn_rx_result)) == cudaSuccess;
@@ -197,20 +208,24 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
         return CN_E_CAPACITY;
     }
     cudaMemset(h->d_stats, 0, nc * sizeof(cn_tx_stats));
-    h->pend.resize(nc);
     h->txs.assign(nc, cn_tx_stats{});
     *out = h;
     return CN_OK;
 }
 
+// conn_to (transport.cpp:84-137): the connection opens on first use; its
+// index (creation order) fixes its RngStream, its src its engine-sharing host
 static int32_t open_conn(cn_transport* h, int32_t src, int32_t dst, bool create) {
     auto it = h->conn_idx.find({src, dst});
     if (it != h->conn_idx.end()) return it->second;
     if (!create) return -1;
-    const int32_t k = static_cast<int32_t>(h->conn_idx.size());
-    if (static_cast<uint32_t>(k) >= h->c.max_conns) return -1;
-    h->conn_idx[{src, dst}] = k;
-    return k;
+    const int rc = cn_tx_open(h->tx, src, dst, h->c.paths);
+    if (rc < 0) return rc;
+    h->conn_idx[{src, dst}] = rc;
+    h->conn_src.push_back(src);
+    const uint32_t nh = cn_tx_n_hosts(h->tx);
+    if (h->pend.size() < nh) h->pend.resize(nh);
+    return rc;
 }
 
 extern "C" int32_t cn_transport_conn_index(cn_transport* h, int32_t src, int32_t dst) {
@@ -225,12 +240,9 @@ extern "C" int cn_transport_send_message(cn_transport* h, int32_t src, int32_t d
         return CN_E_INVALID;
     }
     const int32_t k = open_conn(h, src, dst, true);
-    if (k < 0) {
-        set_error("send_message: max_conns connections already open");
-        return CN_E_CAPACITY;
-    }
+    if (k < 0) return k;  // cn_tx_open set the message (capacity)
     h->subs.push_back(cn_tx_submit{t, len, tag});
-    h->pend[k].push_back(Ev{t, 0, static_cast<uint32_t>(h->subs.size() - 1)});
+    h->pend[cn_tx_conn_host(h->tx, k)].push_back(Ev{t, 0, static_cast<uint32_t>(k), h->subs.size() - 1});
     return 1;
 }
 
@@ -241,31 +253,33 @@ extern "C" int cn_transport_handle_acks(cn_transport* h, const cn_ack_rec* acks,
         const int32_t k = open_conn(h, acks[i].dst, acks[i].src, false);
         if (k < 0) continue;
         h->acks.push_back(acks[i]);
-        h->pend[k].push_back(Ev{acks[i].aux, 1, static_cast<uint32_t>(h->acks.size() - 1)});
+        h->pend[cn_tx_conn_host(h->tx, k)].push_back(Ev{acks[i].aux, 1, static_cast<uint32_t>(k), h->acks.size() - 1});
     }
     return CN_OK;
 }
 
 extern "C" int cn_transport_advance(cn_transport* h, int64_t until, void* stream) {
     if (!h) return CN_E_INVALID;
-    const uint32_t nc = h->c.max_conns;
-    std::vector<uint32_t> off(nc + 1, 0);
+    const uint32_t nh = cn_tx_n_hosts(h->tx);
+    if (nh == 0) return CN_OK;
+    std::vector<uint32_t> off(nh + 1, 0);
     std::vector<uint64_t> ev;
-    for (uint32_t k = 0; k < nc; ++k) {
+    for (uint32_t k = 0; k < nh; ++k) {
         auto& v = h->pend[k];
         std::stable_sort(v.begin(), v.end(), [](const Ev& a, const Ev& b) {
             return a.t != b.t ? a.t < b.t : a.type < b.type;
         });
-        for (const Ev& e : v) ev.push_back((static_cast<uint64_t>(e.type) << 62) | e.idx);
+        for (const Ev& e : v)
+            ev.push_back((static_cast<uint64_t>(e.type) << 62) | (static_cast<uint64_t>(e.conn) << 40) | e.idx);
         off[k + 1] = static_cast<uint32_t>(ev.size());
     }
     if (!grow(&h->d_ev, &h->cap_ev, ev.size() + 1) || !grow(&h->d_subs, &h->cap_subs, h->subs.size() + 1) ||
-        !grow(&h->d_ain, &h->cap_ain, h->acks.size() + 1)) {
+        !grow(&h->d_ain, &h->cap_ain, h->acks.size() + 1) || !grow(&h->d_evoff, &h->cap_evoff, nh + 1)) {
         set_error("cn_transport_advance: out of device memory");
         return CN_E_CAPACITY;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    CNB_CUDA(cudaMemcpyAsync(h->d_evoff, off.data(), (nc + 1) * 4ull, cudaMemcpyHostToDevice, s));
+    CNB_CUDA(cudaMemcpyAsync(h->d_evoff, off.data(), (nh + 1) * 4ull, cudaMemcpyHostToDevice, s));
     if (!ev.empty()) CNB_CUDA(cudaMemcpyAsync(h->d_ev, ev.data(), ev.size() * 8, cudaMemcpyHostToDevice, s));
     if (!h->subs.empty())
         CNB_CUDA(cudaMemcpyAsync(h->d_subs, h->subs.data(), h->subs.size() * sizeof(cn_tx_submit),
@@ -275,6 +289,7 @@ extern "C" int cn_transport_advance(cn_transport* h, int64_t until, void* stream
                                  cudaMemcpyHostToDevice, s));
     int rc = cn_tx_run(h->tx, h->d_evoff, h->d_ev, h->d_subs, h->d_ain, until, h->d_log, h->d_stats, stream);
     if (rc != CN_OK) return rc;
+    const uint32_t nc = static_cast<uint32_t>(h->conn_src.size());
     CNB_CUDA(cudaMemcpyAsync(h->txs.data(), h->d_stats, nc * sizeof(cn_tx_stats), cudaMemcpyDeviceToHost, s));
     CNB_CUDA(cudaStreamSynchronize(s));
     unsigned int st = 0;
@@ -283,34 +298,36 @@ extern "C" int cn_transport_advance(cn_transport* h, int64_t until, void* stream
     h->subs.clear();
     h->acks.clear();
     if (st) {
-        set_error("cn_transport_advance: sender status 0x" + std::to_string(st));
-        return CN_E_CAPACITY;
+        set_error("cn_transport_advance: sender status 0x" + std::to_string(st) +
+                  ((st & CN_TX_STATUS_LOG) ? " (transmit log overflow: poll more often or raise log_cap)" : ""));
+        return (st & CN_TX_STATUS_POLICY) ? CN_E_LOGIC : CN_E_CAPACITY;
     }
     return CN_OK;
 }
 
+// transmissions since the last poll: host by host, each host's in emission
+// order.  Records that do not fit `cap` stay queued for the next poll.
 extern "C" int64_t cn_transport_poll_transmissions(cn_transport* h, cn_tx_rec* out, uint64_t cap, int32_t* conn_out) {
     if (!h) return CN_E_INVALID;
-    const uint32_t nc = h->c.max_conns;
-    std::vector<uint32_t> cnt(nc);
+    const uint32_t nh = cn_tx_n_hosts(h->tx);
+    std::vector<uint32_t> cnt(nh), took(nh, 0);
     int rc = cn_tx_log_counts(h->tx, cnt.data());
     if (rc != CN_OK) return rc;
     uint64_t k = 0;
-    for (uint32_t c = 0; c < nc; ++c) {
-        const uint32_t m = std::min(cnt[c], h->c.log_cap);
-        if (!m) continue;
-        if (out && k < cap) {
-            const uint64_t take = std::min<uint64_t>(m, cap - k);
-            CNB_CUDA(cudaMemcpy(out + k, h->d_log + static_cast<uint64_t>(c) * h->c.log_cap,
-                                take * sizeof(cn_tx_rec), cudaMemcpyDeviceToHost));
-            if (conn_out)
-                for (uint64_t j = 0; j < take; ++j) conn_out[k + j] = static_cast<int32_t>(c);
-        }
-        k += m;
+    for (uint32_t x = 0; x < nh; ++x) {
+        const uint32_t m = std::min(cnt[x], h->c.log_cap);
+        if (!m || !out || k >= cap) continue;
+        const uint64_t take = std::min<uint64_t>(m, cap - k);
+        CNB_CUDA(cudaMemcpy(out + k, h->d_log + static_cast<uint64_t>(x) * h->c.log_cap, take * sizeof(cn_tx_rec),
+                            cudaMemcpyDeviceToHost));
+        if (conn_out)
+            for (uint64_t j = 0; j < take; ++j) conn_out[k + j] = static_cast<int32_t>(out[k + j].conn);
+        took[x] = static_cast<uint32_t>(take);
+        k += take;
     }
-    rc = cn_tx_log_clear(h->tx, nullptr);
+    if (!out) return static_cast<int64_t>(std::accumulate(cnt.begin(), cnt.end(), uint64_t{0}));
+    rc = cn_tx_log_consume(h->tx, h->d_log, took.data());
     if (rc != CN_OK) return rc;
-    CNB_CUDA(cudaDeviceSynchronize());
     return static_cast<int64_t>(k);
 }
 
@@ -379,6 +396,7 @@ extern "C" int cn_transport_stats(cn_transport* h, cn_stats* o) {
         o->chunk_rtx += t.chunk_rtx;
         o->fast_rtx += t.fast_rtx;
         o->rtos += t.rtos;
+        o->rts_sent += t.rts_sent;
     }
     o->acks_sent = h->acks_sent;
     o->nacks_sent = h->nacks_sent;
@@ -407,9 +425,9 @@ extern "C" int64_t cn_transport_path_inflight(cn_transport* h, int32_t src, int3
 extern "C" int64_t cn_transport_window_available(cn_transport* h, int32_t src, int32_t dst, int32_t path) {
     if (!h) return 0;
     const int32_t k = open_conn(h, src, dst, false);
-    if (k < 0 || path < 0 || path >= static_cast<int32_t>(h->c.paths)) return 0;
-    // global CC scope: the window gates the connection's whole inflight (:320-325)
-    return h->txs[k].cwnd_bytes - h->txs[k].inflight;
+    int64_t w = 0;
+    if (k < 0 || cn_tx_window_available(h->tx, static_cast<uint32_t>(k), path, &w) != CN_OK) return 0;
+    return w;
 }
 
 extern "C" int64_t cn_transport_conn_credit(cn_transport* h, int32_t src, int32_t dst) {
@@ -420,31 +438,26 @@ extern "C" int64_t cn_transport_conn_credit(cn_transport* h, int32_t src, int32_
     return cs.credit;
 }
 
-// one engine per host: the host's connections together
+// engine introspection: any connection of the host names its engines
+static bool host_engine(cn_transport* h, int32_t host, int32_t engine, cn_tx_engine_state* es) {
+    if (!h || engine < 0 || engine >= h->c.engines) return false;
+    for (size_t c = 0; c < h->conn_src.size(); ++c)
+        if (h->conn_src[c] == host)
+            return cn_tx_get_engine_state(h->tx, static_cast<uint32_t>(c), engine, es) == CN_OK;
+    return false;
+}
+
 extern "C" int32_t cn_transport_engine_inflight_msgs(cn_transport* h, int32_t host, int32_t engine) {
-    if (!h || engine != 0) return 0;
-    int32_t n = 0;
-    for (const auto& kv : h->conn_idx)
-        if (kv.first.first == host) n += h->txs[kv.second].live_msgs;
-    return n;
+    cn_tx_engine_state es;
+    return host_engine(h, host, engine, &es) ? es.inflight_msgs : 0;
 }
 
 extern "C" uint64_t cn_transport_engine_dispatched(cn_transport* h, int32_t host, int32_t engine) {
-    if (!h || engine != 0) return 0;
-    uint64_t n = 0;
-    for (const auto& kv : h->conn_idx)
-        if (kv.first.first == host) n += h->txs[kv.second].msgs_sent;
-    return n;
+    cn_tx_engine_state es;
+    return host_engine(h, host, engine, &es) ? es.dispatched : 0;
 }
 
 extern "C" int64_t cn_transport_engine_gauge(cn_transport* h, int32_t host, int32_t engine) {
-    if (!h || engine != 0) return 0;
-    int64_t g = 0;
-    for (const auto& kv : h->conn_idx)
-        if (kv.first.first == host) {
-            cn_tx_conn_state cs;
-            if (cn_tx_get_conn_state(h->tx, static_cast<uint32_t>(kv.second), &cs, nullptr, 0) == CN_OK)
-                g += cs.unchunked;
-        }
-    return g;
+    cn_tx_engine_state es;
+    return host_engine(h, host, engine, &es) ? es.gauge : 0;
 }

@@ -20,7 +20,7 @@ from . import _lib
 from .records import ACK_DTYPE, CPL_DTYPE
 from .sender import LB, TX_DTYPE
 
-CC = {"none": 0, "swift": 2}
+CC = {"none": 0, "cubic": 1, "swift": 2}
 
 
 class TransportConfigC(ctypes.Structure):
@@ -33,7 +33,8 @@ class TransportConfigC(ctypes.Structure):
                 ("mss", i64), ("cap_bytes", i64), ("ecn_as_loss", i32), ("pad0", i32),
                 ("swift_target_ns", i64), ("init_cwnd_pkts", f64), ("base_rtt_ns", f64),
                 ("commit_ahead", i64), ("max_conns", u32), ("max_batch", u32), ("log_cap", u32),
-                ("policy", i32), ("chunk_pool", u64), ("arena_bytes", u64)]
+                ("policy", i32), ("chunk_pool", u64), ("arena_bytes", u64), ("max_conns_per_host", u32),
+                ("pad_mcph", u32)]
 
 
 STATS_FIELDS = ["msgs_sent", "msgs_completed", "backpressured", "chunks_sent", "chunk_rtx", "fast_rtx", "rtos",
@@ -82,7 +83,8 @@ class TransportEndpoint:
                  rtx_avoid_prev_path=True, carry_payload=True, max_conns=64, max_batch=1 << 16,
                  log_cap=1 << 16, chunk_pool=1 << 20, arena_bytes=64 << 20, receiver_driven=False,
                  initial_credit=-1, credit_quantum=32768, credit_bank_quanta=4, policy=0,
-                 reliability="selective", device="cuda"):
+                 reliability="selective", engines=1, conn_split=False, cc_scope="global", ecn_as_loss=False,
+                 cap_bytes=0, max_conns_per_host=0, device="cuda"):
         L = _lib.lib()
         _setup(L)
         c = TransportConfigC()
@@ -97,6 +99,9 @@ class TransportEndpoint:
         c.receiver_driven, c.initial_credit = (1 if receiver_driven else 0), initial_credit
         c.credit_quantum, c.credit_bank_quanta, c.policy = credit_quantum, credit_bank_quanta, policy
         c.reliability = {"selective": 0, "ordered": 1}[reliability]
+        c.engines, c.conn_split = engines, 1 if conn_split else 0
+        c.cc_scope = {"global": 0, "per_path": 1}[cc_scope]
+        c.ecn_as_loss, c.cap_bytes, c.max_conns_per_host = 1 if ecn_as_loss else 0, cap_bytes, max_conns_per_host
         self.device = torch.device(device)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):

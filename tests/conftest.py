@@ -19,7 +19,7 @@ def pytest_configure(config):
 def golden_names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
                   if os.path.basename(p) not in ("rng.npz", "trace.npz", "eqds.npz")
-                  and not os.path.basename(p).startswith(("sender_", "probe_")))
+                  and not os.path.basename(p).startswith(("sender_", "probe_", "host_")))
 
 
 def load_psn(name):

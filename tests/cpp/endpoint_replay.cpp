@@ -28,7 +28,13 @@ int main(int argc, char** argv) {
     if (argc < 14) return 2;
     auto subs = load<cn_tx_submit>(argv[1]);
     auto acks = load<cn_ack_rec>(argv[2]);
-    auto want = load<cn_tx_rec>(argv[3]);
+    struct Want {  // the reference harness's record (oracle/ref_harness.cpp cnref_tx_rec)
+        int64_t t;
+        uint32_t msg_id, chunk;
+        int32_t path, is_rtx;
+        uint64_t msg_seq;
+    };
+    auto want = load<Want>(argv[3]);
     cn_transport_config c;
     cn_transport_config_default(&c);
     c.chunk_bytes = std::atoi(argv[4]);
@@ -49,7 +55,10 @@ int main(int argc, char** argv) {
     auto tx = ep.poll_transmissions();
     if (tx.size() != want.size()) { std::fprintf(stderr, "tx %zu != %zu\n", tx.size(), want.size()); return 1; }
     for (size_t i = 0; i < tx.size(); ++i)
-        if (std::memcmp(&tx[i].second, &want[i], sizeof(cn_tx_rec)) != 0) {
+        if (tx[i].second.t != want[i].t || tx[i].second.msg_id != want[i].msg_id ||
+            tx[i].second.chunk != want[i].chunk || tx[i].second.path != want[i].path ||
+            tx[i].second.is_rtx != want[i].is_rtx || tx[i].second.msg_seq != want[i].msg_seq || tx[i].first != 0 ||
+            tx[i].second.dst != dst) {
             std::fprintf(stderr, "tx %zu differs\n", i);
             return 1;
         }

@@ -552,7 +552,8 @@ def gen_host(name):
                     policy=POLICY_ENGINE_ID[r.get("policy", 0)],
                     max_inflight_msgs=int(r.get("max_inflight_msgs", 0)) or 128,
                     swift_target_ns=3 * int(stt["base_rtt"]) if cc == "swift" else 0,
-                    topo=kw.get("topo"), topo_arg=kw.get("topo_arg"))
+                    topo=kw.get("topo"), topo_arg=kw.get("topo_arg"), rate_bps=kw.get("rate_bps", 400e9),
+                    qcap_bytes=kw.get("qcap_bytes", 1 << 20), cutoff_ns=int(rkw["cutoff_ns"]))
         # the reference's path count per connection: min(paths, path_count(src, dst))
         meta["n_paths"] = [int(x) for x in _path_counts(kw, src, conns)]
         path = os.path.join(GOLDEN, f"host_{name}_{tag}.npz")

@@ -99,8 +99,9 @@ double orc_pow3(double x) {
     double hi = t2 + ar2;
     double lo3 = fma(ar, r, -ar2);
     double lo4 = t2 - hi + ar2;
-    double p = ar3 * fma(ar2, fma(ar2, fma(r, A[6], A[5]), fma(r, A[4], A[3])), fma(r, A[2], A[1]));
-    double lo = lo1 + lo2 + lo3 + lo4 + p;
+    /* p = ar3 * (...) has one use, in the sum: contracted into it */
+    double pz = fma(ar2, fma(ar2, fma(r, A[6], A[5]), fma(r, A[4], A[3])), fma(r, A[2], A[1]));
+    double lo = fma(ar3, pz, lo1 + lo2 + lo3 + lo4);
     double ly = hi + lo;
     double ltail = hi - ly + lo;
     double ehi = y * ly;

@@ -843,20 +843,24 @@ int cnref_host_replay(const cnref_scenario* sc, int src, const cnref_host_submit
             auto it = tr.hosts_[src].conn_by_dst.find(dst);
             return it == tr.hosts_[src].conn_by_dst.end() ? -1 : it->second;
         };
+        // RTS packets (control, exempt from the blackhole) are seen at
+        // delivery; their send times come from stepping the event loop and
+        // counting Stats::rts_sent per event (one control FIFO per host
+        // egress: deliveries keep the send order on equal-latency paths)
+        std::vector<cnref_host_tx> rts_rec;
+        std::vector<int64_t> rts_sent_t;
         net.set_trace([&](const TraceEvent& te) {
             if (tc.receiver_driven && std::strcmp(te.event, "deliver") == 0 && te.pkt->kind == PacketKind::rts) {
-                if (n_out < max_out) {
-                    cnref_host_tx& r = out[n_out];
-                    r.t = te.t - ctl_lat[te.pkt->dst] - t0;
-                    r.msg_id = 0;
-                    r.chunk = 0xFFFFFFFFu;  // RTS record
-                    r.path = -1;
-                    r.is_rtx = te.pkt->is_rtx ? 1 : 0;
-                    r.msg_seq = te.pkt->demand_bytes;
-                    r.conn = static_cast<uint32_t>(conn_of(te.pkt->dst));
-                    r.dst = te.pkt->dst;
-                }
-                ++n_out;
+                cnref_host_tx r;
+                r.t = te.t;  // delivery time, replaced by the send time below
+                r.msg_id = 0;
+                r.chunk = 0xFFFFFFFFu;  // RTS record
+                r.path = -1;
+                r.is_rtx = te.pkt->is_rtx ? 1 : 0;
+                r.msg_seq = te.pkt->demand_bytes;
+                r.conn = static_cast<uint32_t>(conn_of(te.pkt->dst));
+                r.dst = te.pkt->dst;
+                rts_rec.push_back(r);
                 return;
             }
             if (std::strcmp(te.event, "loss") != 0) return;
@@ -915,7 +919,26 @@ int cnref_host_replay(const cnref_scenario* sc, int src, const cnref_host_submit
                 }
             });
         }
-        eq.run_until_idle(sc->cutoff_ns);
+        while (!eq.heap_.empty() && eq.heap_.top().t <= sc->cutoff_ns) {  // EventQueue::run_until_idle, stepped
+            auto e = eq.heap_.top();
+            eq.heap_.pop();
+            eq.now_ = e.t;
+            const uint64_t before = tr.stats_.rts_sent;
+            e.fn();
+            for (uint64_t i = before; i < tr.stats_.rts_sent; ++i) rts_sent_t.push_back(e.t);
+        }
+        if (tc.receiver_driven) {
+            std::stable_sort(rts_rec.begin(), rts_rec.end(),
+                             [](const cnref_host_tx& a, const cnref_host_tx& b) { return a.t < b.t; });
+            for (size_t i = 0; i < rts_rec.size(); ++i) {
+                cnref_host_tx r = rts_rec[i];
+                if (i >= rts_sent_t.size() || rts_sent_t[i] + ctl_lat[r.dst] > r.t)
+                    throw std::runtime_error("RTS send / delivery pairing failed");
+                r.t = rts_sent_t[i] - t0;
+                if (n_out < max_out) out[n_out] = r;
+                ++n_out;
+            }
+        }
         for (size_t k = 0; k < tr.conns_.size() && k < max_conns; ++k) conns_out[k] = tr.conns_[k].dst;
         if (st) {
             st->chunks_sent = tr.stats().chunks_sent;

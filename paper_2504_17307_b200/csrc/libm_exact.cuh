@@ -129,9 +129,9 @@ __device__ __forceinline__ double libm_pow3(double x) {
     const double hi = __dadd_rn(t2, ar2);
     const double lo3 = __fma_rn(ar, r, -ar2);
     const double lo4 = __dadd_rn(__dsub_rn(t2, hi), ar2);
-    const double p = __dmul_rn(
-        ar3, __fma_rn(ar2, __fma_rn(ar2, __fma_rn(r, A6, A5), __fma_rn(r, A4, A3)), __fma_rn(r, A2, A1)));
-    const double lo = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(lo1, lo2), lo3), lo4), p);
+    // p = ar3 * (...) has one use, in the sum below: contracted into it
+    const double pz = __fma_rn(ar2, __fma_rn(ar2, __fma_rn(r, A6, A5), __fma_rn(r, A4, A3)), __fma_rn(r, A2, A1));
+    const double lo = __fma_rn(ar3, pz, __dadd_rn(__dadd_rn(__dadd_rn(lo1, lo2), lo3), lo4));
     const double ly = __dadd_rn(hi, lo);
     const double ltail = __dadd_rn(__dsub_rn(hi, ly), lo);
     // y * log(x) in double-double

@@ -129,10 +129,11 @@ def test_host_engine_state_matches_reference_probes():
     probes_t = [t + 1 for t in times[:: max(1, len(times) // 12)] if t + 1 not in tset]
     kw = dict(topo=meta["topo"], topo_arg=meta["topo_arg"], seed=meta["seed"], chunk_bytes=meta["chunk_bytes"],
               paths=meta["paths"], lb=meta["lb"], cc=meta["cc"], cc_scope=meta["cc_scope"], engines=meta["engines"],
-              conn_split=meta["conn_split"], cutoff_ns=meta["end_time"] + 1)
-    rate = {"fanout": 100e9}.get(meta["name"].split("_")[0], 100e9)
-    _, _, conns, pr = ref.host_replay(acks, z["submits"], meta["src"], rate_bps=rate, qcap_bytes=256 * 1024,
-                                      probe_t=probes_t, probe_conns=len(meta["conns"]), **kw)
+              conn_split=meta["conn_split"], cutoff_ns=meta["cutoff_ns"])
+    _, _, conns, pr = ref.host_replay(acks, z["submits"], meta["src"], rate_bps=meta["rate_bps"],
+                                      qcap_bytes=meta["qcap_bytes"], probe_t=probes_t,
+                                      probe_conns=len(meta["conns"]), **kw)
+    assert list(conns) == meta["conns"]
     eng = engine_for(meta)
     E = meta["engines"]
     k = 0

@@ -575,9 +575,14 @@ void cn_transport_destroy(cn_transport* h);
  * dst) connection on first use (conn_to order = RngStream index); returns 1
  * when queued (backpressure is counted in the stats when the engine runs). */
 int cn_transport_send_message(cn_transport* h, int32_t src, int32_t dst, uint64_t len, uint64_t tag, int64_t t);
+/* conn_to ahead of the first send_message, with the connection's path count
+ * min(paths, topology path_count(src, dst)) (transport.cpp:97-99) -- the
+ * caller owns the topology; returns the connection index */
+int32_t cn_transport_open_conn(cn_transport* h, int32_t src, int32_t dst, int32_t n_paths);
 /* acks and trimmed-header NACKs delivered at the senders (host records, aux = time) */
 int cn_transport_handle_acks(cn_transport* h, const cn_ack_rec* acks, uint32_t n);
-/* run the sender engine over everything queued, timers up to `until` */
+/* EventQueue::run_until(until): the queued inputs with t <= until and the
+ * timers up to `until` (later inputs stay queued for the next advance) */
 int cn_transport_advance(cn_transport* h, int64_t until, void* stream);
 /* transmissions since the last poll, per connection in emission order;
  * conn_out[i] = connection index of out[i] (optional) */

@@ -215,17 +215,30 @@ extern "C" int cn_transport_create(const cn_transport_config* cfg, uint64_t seed
 
 // conn_to (transport.cpp:84-137): the connection opens on first use; its
 // index (creation order) fixes its RngStream, its src its engine-sharing host
-static int32_t open_conn(cn_transport* h, int32_t src, int32_t dst, bool create) {
+static int32_t open_conn(cn_transport* h, int32_t src, int32_t dst, bool create, int32_t n_paths = 0) {
     auto it = h->conn_idx.find({src, dst});
     if (it != h->conn_idx.end()) return it->second;
     if (!create) return -1;
-    const int rc = cn_tx_open(h->tx, src, dst, h->c.paths);
+    const int rc = cn_tx_open(h->tx, src, dst, n_paths > 0 ? n_paths : h->c.paths);
     if (rc < 0) return rc;
     h->conn_idx[{src, dst}] = rc;
     h->conn_src.push_back(src);
     const uint32_t nh = cn_tx_n_hosts(h->tx);
     if (h->pend.size() < nh) h->pend.resize(nh);
     return rc;
+}
+
+// conn_to with the topology's path count (min(paths, path_count(src, dst)),
+// transport.cpp:97-99) supplied by the caller; send_message opens unknown
+// pairs with `paths`
+extern "C" int32_t cn_transport_open_conn(cn_transport* h, int32_t src, int32_t dst, int32_t n_paths) {
+    if (!h || n_paths < 1 || n_paths > h->c.paths) {
+        set_error("cn_transport_open_conn: n_paths outside [1, paths]");
+        return CN_E_INVALID;
+    }
+    const int32_t k = open_conn(h, src, dst, false);
+    if (k >= 0) return k;
+    return open_conn(h, src, dst, true, n_paths);
 }
 
 extern "C" int32_t cn_transport_conn_index(cn_transport* h, int32_t src, int32_t dst) {
@@ -262,15 +275,23 @@ extern "C" int cn_transport_advance(cn_transport* h, int64_t until, void* stream
     if (!h) return CN_E_INVALID;
     const uint32_t nh = cn_tx_n_hosts(h->tx);
     if (nh == 0) return CN_OK;
+    // EventQueue::run_until(until): the queued inputs up to `until` run now,
+    // later ones stay queued for the next advance
     std::vector<uint32_t> off(nh + 1, 0);
     std::vector<uint64_t> ev;
+    std::vector<std::vector<Ev>> later(nh);
     for (uint32_t k = 0; k < nh; ++k) {
         auto& v = h->pend[k];
         std::stable_sort(v.begin(), v.end(), [](const Ev& a, const Ev& b) {
             return a.t != b.t ? a.t < b.t : a.type < b.type;
         });
-        for (const Ev& e : v)
+        for (const Ev& e : v) {
+            if (e.t > until) {
+                later[k].push_back(e);
+                continue;
+            }
             ev.push_back((static_cast<uint64_t>(e.type) << 62) | (static_cast<uint64_t>(e.conn) << 40) | e.idx);
+        }
         off[k + 1] = static_cast<uint32_t>(ev.size());
     }
     if (!grow(&h->d_ev, &h->cap_ev, ev.size() + 1) || !grow(&h->d_subs, &h->cap_subs, h->subs.size() + 1) ||
@@ -294,9 +315,23 @@ extern "C" int cn_transport_advance(cn_transport* h, int64_t until, void* stream
     CNB_CUDA(cudaStreamSynchronize(s));
     unsigned int st = 0;
     cn_tx_status(h->tx, &st);
-    for (auto& v : h->pend) v.clear();
-    h->subs.clear();
-    h->acks.clear();
+    // keep the later inputs (re-indexed into fresh submit / ack arrays)
+    std::vector<cn_tx_submit> subs2;
+    std::vector<cn_ack_rec> acks2;
+    for (uint32_t k = 0; k < nh; ++k) {
+        for (Ev& e : later[k]) {
+            if (e.type == 0) {
+                subs2.push_back(h->subs[e.idx]);
+                e.idx = subs2.size() - 1;
+            } else {
+                acks2.push_back(h->acks[e.idx]);
+                e.idx = acks2.size() - 1;
+            }
+        }
+        h->pend[k].swap(later[k]);
+    }
+    h->subs.swap(subs2);
+    h->acks.swap(acks2);
     if (st) {
         set_error("cn_transport_advance: sender status 0x" + std::to_string(st) +
                   ((st & CN_TX_STATUS_LOG) ? " (transmit log overflow: poll more often or raise log_cap)" : ""));

@@ -65,6 +65,7 @@ def _setup(L):
     L.cn_transport_poll_completions.restype = i64
     L.cn_transport_stats.argtypes = [vp, vp]
     L.cn_transport_conn_index.argtypes = [vp, i32, i32]
+    L.cn_transport_open_conn.argtypes = [vp, i32, i32, i32]
     L.cn_transport_outstanding_bytes.argtypes = [vp, i32, i32]
     L.cn_transport_outstanding_bytes.restype = i64
     for f, rt in (("path_inflight", i64), ("window_available", i64)):
@@ -169,6 +170,12 @@ class TransportEndpoint:
         st = StatsC()
         _lib.check(self._L.cn_transport_stats(self._h, ctypes.byref(st)), "stats")
         return {n: int(getattr(st, n)) for n in STATS_FIELDS}
+
+    def open_conn(self, src, dst, n_paths):
+        """conn_to with min(paths, path_count(src, dst)) from the caller's topology."""
+        k = int(self._L.cn_transport_open_conn(self._h, src, dst, n_paths))
+        _lib.check(k if k < 0 else 0, "open_conn")
+        return k
 
     def conn_index(self, src, dst):
         return int(self._L.cn_transport_conn_index(self._h, src, dst))

@@ -173,3 +173,39 @@ def test_endpoint_ordered_receive(name):
     ok, bad = ack_equal(ep.poll_acks(), acks_ref)
     assert ok, bad
     assert len(ep.poll_completions()) == len(cpls_ref)
+
+
+@pytest.mark.parametrize("name", ["fanout_k8_cubic", "fanout_k8_e4split", "fanout_pp_cubic_pp",
+                                  "split_swift_swift_e2split", "fanout_rd_none", "engines_k8_cubic_e4"])
+def test_endpoint_host_replay(name):
+    """A source host with several connections through the boundary object:
+    fan-out, engines / conn_split, CUBIC and per-path scope, receiver-driven
+    -- the reference host's transmit log (host_<name>.npz) and the engine
+    introspection after the run."""
+    from test_host_gpu import compare, load
+    z, meta = load(name)
+    src = meta["src"]
+    ep = _ep(dict(meta, n_paths=max(meta["n_paths"])), n_conns=8, engines=meta["engines"],
+             conn_split=meta["conn_split"], cc_scope=["global", "per_path"][meta["cc_scope"]],
+             receiver_driven=meta["receiver_driven"],
+             initial_credit=meta["initial_credit"] if meta["receiver_driven"] else -1, policy=meta["policy"])
+    for k, (dst, np_) in enumerate(zip(meta["conns"], meta["n_paths"])):  # conn_to order
+        assert ep.open_conn(src, dst, np_) == k
+    for s in z["submits"]:
+        ep.send_message(src, int(s["dst"]), int(s["len"]), int(s["tag"]), int(s["t"]))
+    ep.handle_acks(z["acks"])
+    half = int(meta["end_time"]) // 2
+    ep.advance(half)
+    tx1, _ = ep.poll_transmissions()
+    ep.advance(meta["end_time"])
+    tx2, _ = ep.poll_transmissions(cap=7)  # a small cap: the rest stays queued
+    tx3, _ = ep.poll_transmissions()
+    tx = np.concatenate([tx1, tx2, tx3])
+    st = ep.stats()
+
+    class S(dict):
+        def __getitem__(self, k):
+            return np.array([dict.__getitem__(self, k)])
+    compare(tx, z["tx"], meta, S(st))
+    done = sum(ep.engine_dispatched(src, e) for e in range(meta["engines"]))
+    assert done == len(z["submits"]) - st["backpressured"]

@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--piece-mb", type=int, default=64, help="ring pipeline piece size (MiB)")
     ap.add_argument("--no-moe", action="store_true", help="skip the MoE all-to-all (configs[3]) at N > 1")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] receive sweep")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the fused-reduce, steady-state and cfg1 x 1024 legs")
     return ap.parse_args()
 
 
@@ -73,6 +75,16 @@ def interleave(data, k):
         c["msg_tag"] = j
         out[j::k] = c
     return out
+
+
+def bench_config(workload, K, n, n_acks, cb, R, world):
+    """The `config` object both arms print (identical dicts: same_config)."""
+    return {"workload": f"{workload}: BASELINE configs[1] (64 MiB message, 256 paths, 1% drop) x {K} "
+                        f"concurrent connections per batch (round-robin interleaved); {n} pkts, {n_acks} acks, "
+                        f"chunk {cb} B",
+            "l2": f"inputs larger than L2: {R} rotating staging replicas ({R * n * MAX_PL / 1e6:.0f} MB) + "
+                  f"{K * 64} MiB of messages written per step",
+            "parallelism": f"replicas x{world} (shard by connection)"}
 
 
 def copy_traffic(workload, conns):
@@ -144,6 +156,228 @@ class Clocks:
         return {"sm_mhz": int(statistics.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples)}
+
+
+def build_staging(data, flat, msg_len, dev):
+    """Arrival-order staging (packet i's payload at i * 4032) gathered from
+    the per-connection source messages `flat` (uint8, connection j = msg_tag
+    j at j * msg_len) -- setup, untimed."""
+    import torch
+    n = len(data)
+    off = torch.from_numpy((data["chunk_offset"] + data["seq_in_chunk"].astype(np.uint64) * MAX_PL)
+                           .astype(np.int64)).to(dev)
+    pl = torch.from_numpy(data["payload_len"].astype(np.int64)).to(dev)
+    conn_of = torch.from_numpy(data["msg_tag"].astype(np.int64)).to(dev)
+    col = torch.arange(MAX_PL, device=dev)
+    st = torch.zeros(n * MAX_PL, dtype=torch.uint8, device=dev)
+    for a in range(0, n, 4096):
+        b = min(n, a + 4096)
+        pos = off[a:b, None] + col[None, :]
+        mask = col[None, :] < pl[a:b, None]
+        vals = flat[conn_of[a:b, None] * msg_len + pos.clamp(max=msg_len - 1)]
+        st.view(n, MAX_PL)[a:b] = torch.where(mask, vals, torch.zeros_like(vals))
+    return st
+
+
+def timed_graph(g, steps, warmup, stream):
+    """Replays `g` warmup + steps times; CUDA-event ms per step."""
+    import torch
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def fused_reduce_bench(dev, data, meta, K, peak, steps=20, warmup=3):
+    """X1 at one GPU ("at 1 GPU this reduces to local fused-reduce
+    kernel GB/s"): the headline batch through the receive path in reduce
+    mode -- k_copy<R> accumulates every accepted payload into a posted
+    accumulator, dst = dst + payload (fp32; bf16 = fp32 add + RNE).
+    Algorithmic bytes per element: payload read + accumulator read + write
+    (fp32 12 B, bf16 6 B) + 64 B per header.  Parity: after one step every
+    accumulator equals acc0 + message elementwise (torch's IEEE add)."""
+    import torch
+
+    import paper_2504_17307_b200 as cn
+    stream = torch.cuda.current_stream(dev)
+    n = len(data)
+    msg_len = int(data["msg_len"][0])
+    cb = meta["chunk_bytes"]
+    hdrs = cn.to_device_records(data, dev)
+    out = {}
+    for name, dt, op in (("fp32", torch.float32, "sum_f32"), ("bf16", torch.bfloat16, "sum_bf16")):
+        es = 4 if dt == torch.float32 else 2
+        g = torch.Generator(device=dev)
+        g.manual_seed(4321)
+        msgs = (torch.rand(K, msg_len // es, device=dev, generator=g) * 2 - 1).to(dt)
+        acc0 = (torch.rand(K, msg_len // es, device=dev, generator=g) * 2 - 1).to(dt)
+        st = build_staging(data, msgs.view(torch.uint8).reshape(-1), msg_len, dev)
+        accs = acc0.clone()
+        tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev, reduce=op,
+                          max_posts=64, arena_bytes=1 << 20, chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
+                          max_batch=n, max_conns=64, max_msgs=64)
+
+        def step(s_):
+            tr.reset(s_)
+            for j in range(K):
+                tr.post(j, accs[j], s_)
+            tr.rx_batch_async(hdrs, st, MAX_PL, s_)
+
+        step(stream)
+        torch.cuda.synchronize()
+        want = acc0 + msgs
+        ok = bool(torch.equal(accs.view(torch.int16 if es == 2 else torch.int32),
+                              want.view(torch.int16 if es == 2 else torch.int32)))
+        assert ok, f"fused reduce {name}: accumulator != acc0 + message"
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            step(torch.cuda.current_stream(dev))
+        ms = timed_graph(gr, steps, warmup, stream)
+        tr.set_profiling(True)
+        tr.kernel_profile(reset=True)
+        for _ in range(steps):
+            step(stream)
+        torch.cuda.synchronize()
+        tr.set_profiling(False)
+        prof, nb = tr.kernel_profile(reset=True)
+        kms = prof["copy"] / max(nb, 1)
+        algo = 3 * K * msg_len + HDR * n
+        out[name] = {"ms_per_step": round(ms, 4), "kernel_ms": round(kms, 5),
+                     "reduced_GBps": round(K * msg_len / (ms * 1e-3) / 1e9, 1),
+                     "kernel_algorithmic_GBps": round(algo / (kms * 1e-3) / 1e9, 1),
+                     "kernel_frac": round(algo / (kms * 1e-3) / 1e9 / peak, 4),
+                     "step_frac": round(algo / (ms * 1e-3) / 1e9 / peak, 4),
+                     "bytes_per_element": 3 * es, "parity": ok}
+        del tr, gr, st, msgs, acc0, accs
+        torch.cuda.empty_cache()
+    out["config"] = (f"{K} x 64 MiB messages of the headline trace into posted accumulators "
+                     f"(receive path in reduce mode, CUDA graph)")
+    return out
+
+
+def steady_bench(dev, data, meta, K, stagings, srcs, steps=20, warmup=5):
+    """The headline batch in steady state: no reset between steps -- every
+    step is a new generation of the K messages (msg_seq + 1 on every header,
+    the same msg ids reused as the reference's LIFO hands them back), so the
+    receiver retires the previous generation and reclaims its chunk-pool and
+    arena ranges (transport.cpp:794-803) while the next one arrives."""
+    import torch
+
+    import paper_2504_17307_b200 as cn
+    from paper_2504_17307_b200.records import PKT_DTYPE
+    stream = torch.cuda.current_stream(dev)
+    n = len(data)
+    msg_len = int(data["msg_len"][0])
+    cb = meta["chunk_bytes"]
+    hdrs = cn.to_device_records(data, dev)
+    seq_col = hdrs.view(n, 64).view(torch.int64)[:, PKT_DTYPE.fields["msg_seq"][1] // 8]
+    tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
+                      arena_bytes=3 * K * (msg_len + (1 << 20)), chunk_pool=3 * K * ((msg_len + cb - 1) // cb),
+                      max_batch=n, max_conns=64, max_msgs=64)
+    R = len(stagings)
+
+    def step(k, s_):
+        seq_col.add_(1)
+        tr.rx_batch_async(hdrs, stagings[k % R], MAX_PL, s_)
+
+    step(0, stream)
+    torch.cuda.synchronize()
+    graphs = []
+    for r in range(R):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            step(r, torch.cuda.current_stream(dev))
+        graphs.append(gr)
+    for k in range(warmup):
+        graphs[k % R].replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(steps):
+        graphs[k % R].replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    res = _rx_result(tr)
+    assert res.status == 0 and res.n_completions == K, (res.status, res.n_completions)
+    arena = tr.arena()
+    last = (steps - 1) % R
+    for c in tr.completions_np(K):
+        o = int(c["buf_offset"])
+        assert torch.equal(arena[o: o + msg_len], srcs[last][int(c["tag"])]), "steady state: message != source"
+    u = tr.usage()
+    out = {"value": round(K * msg_len / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 4),
+           "generations": 1 + warmup + steps, "msg_seq_last": int(seq_col[0].item()),
+           "pool_live": int(u["pool_live"]), "arena_live": int(u["arena_live"]),
+           "note": "no reset: msg_seq += 1 per step (a torch add on the header column, inside the graph); "
+                   "delivered generations retired and their ring ranges reused",
+           "parity": True}
+    del tr
+    torch.cuda.empty_cache()
+    return out
+
+
+def _rx_result(tr):
+    import torch
+
+    from paper_2504_17307_b200 import _lib as L_
+    res = torch.empty(24, dtype=torch.uint8).copy_(tr._result)
+    return L_.RxResult.from_buffer_copy(bytes(res.numpy()))
+
+
+def cfg1_batch_bench(dev, conns=1024, steps=10, warmup=3):
+    """BASELINE configs[0] batched: `conns` independent
+    copies of the reference's cfg1 trace (1 MiB message, 4 KiB chunks = one
+    4,032 B packet + one 64 B runt each, 8 paths) from `conns` source hosts,
+    interleaved round-robin into one receive batch."""
+    import torch
+
+    import paper_2504_17307_b200 as cn
+    data1, meta, n_acks1 = load_trace("cfg1")
+    data = interleave(data1, conns)
+    n = len(data)
+    msg_len = int(data["msg_len"][0])
+    cb = meta["chunk_bytes"]
+    stream = torch.cuda.current_stream(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    src = torch.randint(0, 256, (conns, msg_len), dtype=torch.uint8, device=dev, generator=g)
+    st = build_staging(data, src.view(-1), msg_len, dev)
+    hdrs = cn.to_device_records(data, dev)
+    tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
+                      arena_bytes=conns * (msg_len + 4096) + (1 << 20), chunk_pool=2 * conns * (msg_len // cb) + 64,
+                      max_batch=n, max_conns=2 * conns + 16, max_msgs=2 * conns + 16)
+
+    def step(s_):
+        tr.reset(s_)
+        tr.rx_batch_async(hdrs, st, MAX_PL, s_)
+
+    step(stream)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        step(torch.cuda.current_stream(dev))
+    ms = timed_graph(gr, steps, warmup, stream)
+    res = _rx_result(tr)
+    assert res.status == 0 and res.n_completions == conns and res.n_acks == n_acks1 * conns, \
+        (res.status, res.n_completions, res.n_acks)
+    arena = tr.arena()
+    for c in tr.completions_np(conns)[:: max(1, conns // 16)]:
+        o = int(c["buf_offset"])
+        assert torch.equal(arena[o: o + msg_len], src[int(c["tag"])]), "cfg1 batch: message != source"
+    out = {"config": f"{conns} x cfg1 (1 MiB, 4 KiB chunks, 8 paths, no loss) interleaved; {n} pkts, "
+                     f"{res.n_acks} acks", "ms_per_batch": round(ms, 4),
+           "GBps": round(conns * msg_len / (ms * 1e-3) / 1e9, 1), "Mpkts_per_s": round(n / (ms * 1e-3) / 1e6, 1),
+           "parity": True}
+    del tr, st, src
+    torch.cuda.empty_cache()
+    return out
 
 
 def message_bytes(data):
@@ -508,10 +742,13 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     a2c = AllToAll(cap, piece_bytes=pb)   # combine (its own slots: the dispatch slots are its send buffer)
     coffs = [s_ * a2a.cap for s_ in range(world)]
 
+    last = {}
+
     def step():
         recv = a2a.run(send, sc, rc, send_offsets=offs)
         # combine: expert outputs (here: the received rows) return to their owners
-        a2c.run(recv, rc, sc, send_offsets=coffs)
+        last["recv"] = recv
+        last["back"] = a2c.run(recv, rc, sc, send_offsets=coffs)
 
     for _ in range(warmup):
         step()
@@ -530,6 +767,29 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    # parity of the timed steps' last dispatch and combine: every source's
+    # rows (its send buffer regenerated from its seed and routing) landed
+    # byte-exact, and every row came back to its owner unchanged
+    bad = 0
+    for s_ in range(world):
+        if s_ == rank or rows[s_, rank] == 0:
+            continue
+        gs = torch.Generator(device=dev)
+        gs.manual_seed(s_)
+        xs_ = torch.randn(tokens, hidden, device=dev, generator=gs).to(torch.bfloat16)
+        send_s = xs_.index_select(0, torch.from_numpy(routing[s_][0]).to(dev)).view(torch.uint8).reshape(-1)
+        o_s = int(np.concatenate([[0], np.cumsum(rows_self[s_])[:-1]])[rank]) * row
+        want = send_s[o_s: o_s + int(rows[s_, rank]) * row]
+        bad += int(not torch.equal(last["recv"][s_ * a2a.cap: s_ * a2a.cap + want.numel()], want))
+    for d_ in range(world):
+        if d_ == rank or sc[d_] == 0:
+            continue
+        want = send[int(offs[d_]): int(offs[d_]) + int(sc[d_])]
+        bad += int(not torch.equal(last["back"][d_ * a2c.cap: d_ * a2c.cap + want.numel()], want))
+    nb = torch.tensor([bad], device=dev)
+    dist.all_reduce(nb)
+    if int(nb.item()):
+        raise AssertionError(f"MoE all-to-all parity failed: {int(nb.item())} mismatched (source, rank) slices")
     # NCCL all_to_all_single with the same splits (local rows excluded on both sides)
     inp = torch.empty(int(sc.sum()), dtype=torch.uint8, device=dev)
     out = torch.empty(int(rc.sum()), dtype=torch.uint8, device=dev)
@@ -555,7 +815,7 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     a2c.close()
     moved = int(rows.sum()) * row * 2  # dispatch + combine, all ranks
     hot_in = int(rows[:, 0].sum()) * row
-    return {"piece_bytes": pb,
+    return {"piece_bytes": pb, "parity": "dispatch and combine byte-exact on every rank (all slices)",
             "config": f"{world} ranks x {tokens} tokens, hidden {hidden} bf16 ({row} B/copy), top-8 of "
                       f"{32 * world} experts, rank 0 experts 10x weight (incast)",
             "ms_per_step": round(ms, 4), "nccl_ms_per_step": round(msn, 4),
@@ -564,6 +824,57 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
             "hot_rank_ingress_GBps": round(hot_in / (ms / 2 * 1e-3) / 1e9, 1),
             "algbw_GBps_all_ranks": round(moved / (ms * 1e-3) / 1e9, 1),
             "nccl_algbw_GBps_all_ranks": round(moved / (msn * 1e-3) / 1e9, 1)}
+
+
+def ring_parity(ring, x, world, rank, dev, samples=1 << 16):
+    """One graph-replayed iteration from the inputs again, then: (1) every
+    rank holds the identical buffer (a checksum gathered over the ranks),
+    (2) a sample of elements equals the same-order fold of the ranks' inputs
+    bit for bit (segment j folds x[j] + x[j+1] + ... + x[j-1] around the
+    ring; bf16 rounds RNE after every fp32 add), (3) the
+    fp32 sample is within 1e-5 * N of the fp64 sum.  Raises on a mismatch."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_17307_b200.collective import seg_bounds
+    ring.buffer().copy_(x)
+    got = ring.run()
+    torch.cuda.synchronize()
+    ring.check()
+    bf = x.dtype == torch.bfloat16
+    bits = got.view(torch.int16 if bf else torch.int32)
+    ck = torch.stack([bits.to(torch.int64).sum(), (bits.to(torch.int64) * 1315423911).sum()])
+    allck = [torch.empty_like(ck) for _ in range(world)]
+    dist.all_gather(allck, ck)
+    same = all(torch.equal(allck[0], c) for c in allck)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(31337)
+    idx = torch.randint(0, x.numel(), (samples,), device=dev, generator=gen)
+    xs = x[idx].contiguous()
+    allx = [torch.empty_like(xs) for _ in range(world)]
+    dist.all_gather(allx, xs)
+    X = torch.stack(allx).float().cpu().numpy()                       # [rank, sample] as fp32
+    ii = idx.cpu().numpy()
+    bounds = [seg_bounds(x.numel(), world, j, ring.quantum) for j in range(world)]
+    seg = np.zeros(len(ii), dtype=np.int64)
+    for j, (a, b) in enumerate(bounds):
+        seg[(ii >= a) & (ii < b)] = j
+    acc = X[seg, np.arange(len(ii))].astype(np.float32)
+    for k in range(1, world):
+        v = X[(seg + k) % world, np.arange(len(ii))].astype(np.float32)
+        acc = (v + acc).astype(np.float32)
+        if bf:  # round to bf16, nearest-even
+            u = acc.view(np.uint32).astype(np.uint64)
+            acc = (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
+    g = got[idx].float().cpu().numpy()
+    exact = bool(np.array_equal(g.view(np.uint32), acc.view(np.uint32)))
+    err = float(np.abs(g.astype(np.float64) - X.astype(np.float64).sum(0)).max())
+    ok = same and exact and (bf or err <= 1e-5 * world * max(1.0, float(np.abs(X).sum(0).max())))
+    if not ok:
+        raise AssertionError(f"ring all-reduce parity failed: ranks_identical={same} sample_bit_exact={exact} "
+                             f"max_abs_err_vs_fp64={err}")
+    return {"ranks_identical": same, "sample_bit_exact_vs_fold": exact, "samples": len(ii),
+            "max_abs_err_vs_fp64": err}
 
 
 def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30, piece_bytes=32 << 20):
@@ -578,7 +889,9 @@ def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30, piece_bytes=
     out = {}
     for dt, name in ((torch.float32, "fp32"), (torch.bfloat16, "bf16")):
         count = nbytes // (4 if dt == torch.float32 else 2)
-        x = torch.randn(count, device=dev).to(dt)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(7000 + rank)
+        x = (torch.rand(count, device=dev, generator=gen) * 2 - 1).to(dt)
         ring = RingAllreduce(count, dt, chunk_bytes=32768, paths=8, piece_bytes=piece_bytes)
         ring.buffer().copy_(x)
         ring.run()  # eager once, then one captured iteration replayed in place
@@ -611,8 +924,9 @@ def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30, piece_bytes=
         tn = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
         dist.all_reduce(tn, op=dist.ReduceOp.MAX)
         msn = float(tn.item())
+        parity = ring_parity(ring, x, world, rank, dev)
         out[name] = {"bytes": nbytes, "ms": round(ms, 4), "busbw_GBps": round(busbw(nbytes, ms * 1e-3, world), 1),
-                     "pieces_per_step": ring.pieces,
+                     "pieces_per_step": ring.pieces, "parity": parity,
                      "nccl_ms": round(msn, 4),
                      "nccl_busbw_GBps": round(busbw(nbytes, msn * 1e-3, world), 1)}
         ring.close()
@@ -624,37 +938,43 @@ def ring_bench(dev, world, rank, iters=8, warmup=3, nbytes=1 << 30, piece_bytes=
 
 
 def run_reference(args):
+    """The reference's own receive path (oracle/_ref: the unmodified chunknet
+    library replaying the same interleaved trace into Transport::handle_packet)
+    on all host threads, each thread its own Transport and source buffers.
+    Each step = `reps` replays per thread (the same per-thread amortisation
+    as the cpu_baseline leg: thread start and Transport setup are outside
+    the per-thread timer, and the slowest thread of a step bounds it)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    data1, meta, n_acks = load_trace(args.workload)
-    data = interleave(data1, max(1, args.conns))
+    data1, meta, n_acks1 = load_trace(args.workload)
+    K = max(1, args.conns)
+    data = interleave(data1, K)
     from oracle import ref
     threads = os.cpu_count() or 1
     msg = message_bytes(data)
     if not ref.available():
         emit({"impl": "reference", "unavailable": "oracle/_ref not built"})
         return
+    t1 = ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
+    reps = max(1, min(16, int(4.0 / max(t1, 1e-3))))  # ~4 s per step
     for _ in range(args.warmup):
         ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
-    times = [ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
-             for _ in range(args.steps)]
+    steps = max(1, min(args.steps, 30))
+    times = [ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, reps) for _ in range(steps)]
     t = sum(times)
-    v = threads * args.steps * msg / t / 1e9
+    v = threads * reps * steps * msg / t / 1e9
+    R = max(1, args.replicas if K == 1 else 2)
     line = {
         "metric": "reassembly_GBps", "value": round(v, 3), "unit": "GB/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "reference DES trace",
-        "config": {"workload": f"{args.workload}: BASELINE configs[1] (64 MiB message, 256 paths, "
-                               f"1% drop) x {args.conns} concurrent connections per batch; "
-                               f"{threads} threads each replay it into its own Transport"},
-        "mpkts_per_s": round(threads * args.steps * len(data) / t / 1e6, 3),
-        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{threads} threads x 1 replay per step"},
-        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t / steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "reference DES trace + random payload",
+        "config": bench_config(args.workload, K, len(data), n_acks1 * K, meta["chunk_bytes"], R, args.gpus),
+        "mpkts_per_s": round(threads * reps * steps * len(data) / t / 1e6, 3),
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{threads} threads x {reps} replays of the {len(data)}-packet trace per step"},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
 
@@ -701,27 +1021,14 @@ def main():
     # synthetic payload: random message bytes on device (one message per
     # connection), gathered into the arrival-order staging slots (packet i
     # at i*4032) -- setup, untimed
-    off = torch.from_numpy((data["chunk_offset"] + data["seq_in_chunk"].astype(np.uint64) * MAX_PL)
-                           .astype(np.int64)).to(dev)
-    pl = torch.from_numpy(data["payload_len"].astype(np.int64)).to(dev)
-    conn_of = torch.from_numpy(data["msg_tag"].astype(np.int64)).to(dev)
     R = max(1, args.replicas if K == 1 else 2)
     srcs, stagings = [], []
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
-    col = torch.arange(MAX_PL, device=dev)
     for r in range(R):
         src = torch.randint(0, 256, (K, msg_len), dtype=torch.uint8, device=dev, generator=g)
-        flat = src.view(-1)
-        st = torch.zeros(n * MAX_PL, dtype=torch.uint8, device=dev)
-        for a in range(0, n, 2048):
-            b = min(n, a + 2048)
-            pos = off[a:b, None] + col[None, :]
-            mask = col[None, :] < pl[a:b, None]
-            vals = flat[conn_of[a:b, None] * msg_len + pos.clamp(max=msg_len - 1)]
-            st.view(n, MAX_PL)[a:b] = torch.where(mask, vals, torch.zeros_like(vals))
         srcs.append(src)
-        stagings.append(st)
+        stagings.append(build_staging(data, src.view(-1), msg_len, dev))
 
     tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
                       arena_bytes=K * (msg_len + (1 << 20)), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
@@ -778,6 +1085,8 @@ def main():
         if world > 1:
             dist.barrier()
         ms = e0.elapsed_time(e1)
+        # the timed graph replays' output: every reassembled message equals its source
+        check_buffers((args.steps - 1) % R)
         # per-kernel CUDA-event pass (eager launches, same inputs) for the roofline
         tr.set_profiling(True)
         tr.kernel_profile(reset=True)
@@ -786,8 +1095,6 @@ def main():
         torch.cuda.synchronize()
         tr.set_profiling(False)
         prof, nb = tr.kernel_profile(reset=True)
-    # last step's buffers must equal their sources (the work was really done)
-    check_buffers((args.steps - 1) % R)
 
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
@@ -848,6 +1155,12 @@ def main():
     ring = ring_bench(dev, world, rank, piece_bytes=args.piece_mb << 20) if world > 1 and not args.no_ring else None
     moe = moe_bench(dev, world, rank) if world > 1 and not args.no_moe else None
     sweep = sweep_bench(dev, world, rank) if not args.no_sweep else None
+    extra = {}
+    if not args.no_extra:
+        peak_, _ = peaks()
+        extra["fused_reduce"] = fused_reduce_bench(dev, data, meta, K, peak_)
+        extra["steady_state"] = steady_bench(dev, data, meta, K, stagings, srcs)
+        extra["cfg1_x1024"] = cfg1_batch_bench(dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -859,12 +1172,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "reference DES trace + random payload",
-            "config": {"workload": f"{args.workload}: BASELINE configs[1] (64 MiB message, "
-                                   f"256 paths, 1% drop) x {K} concurrent connections per batch "
-                                   f"(round-robin interleaved); {n} pkts, {n_acks} acks, chunk {cb} B",
-                       "l2": f"inputs larger than L2: {R} rotating staging replicas "
-                             f"({R * n * MAX_PL / 1e6:.0f} MB) + 64 MiB output per step",
-                       "parallelism": f"replicas x{world} (shard by connection)"},
+            "config": bench_config(args.workload, K, n, n_acks, cb, R, world),
+            "parity": "every reassembled message of the timed CUDA-graph replays equals its source",
             "mpkts_per_s": round(mpkts, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -892,6 +1201,7 @@ def main():
             line["moe_alltoall"] = moe
         if sweep:
             line["sweep_cfg5"] = sweep
+        line.update(extra)
         if cpu:
             line["cpu_baseline"] = cpu
         emit(line)

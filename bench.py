@@ -474,7 +474,7 @@ def sender_bench(dev, conns=1024, scenario="cfg1", reps=3):
         eng = TxEngine(conns, chunk_bytes=meta["chunk_bytes"], rto_min=meta["rto_min"],
                        rto_max=meta["rto_max"], commit_ahead=meta["commit_ahead"],
                        base_rtt_ns=meta["base_rtt"], seed=meta["seed"], lb=meta["lb"],
-                       max_paths=meta["n_paths"], src=[meta["src"]] * conns, dst=[meta["dst"]] * conns,
+                       max_paths=meta["n_paths"], src=list(range(conns)), dst=[meta["dst"]] * conns,
                        chunk_pool=conns * 2048, log_cap=max(1024, len(z["tx"]) + 16), device=dev)
         prep = eng.prepare([one] * conns, subs, acks)
         torch.cuda.synchronize()

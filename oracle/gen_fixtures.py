@@ -585,6 +585,106 @@ def _path_counts(kw, src, conns):
     return out
 
 
+# ------------------------------------------------------ randomized suite
+# The reference's own property suite (test_reliability_props.cpp:126-218):
+# seed -> topology (star 8 / fat tree k=4), rate, delay, drop, chunk size,
+# paths, engines, conn_split, LB, CC algo and scope, receiver-driven /
+# ordered modes and 3-5 messages, drawn over its RngStream by the harness
+# (cnref_prop_spec_draw).  Every seed is recorded in the reference DES, the
+# delivered packets replayed into its receive path (rx parity) and each
+# source host's submissions and acks into a host-level sender replay
+# (sender parity).  Builder's extension: seeds with seed % 10 == 5 run the
+# switch queues in trim mode (64 KiB) so trimmed headers and NACKs appear.
+# kind 1: the engine-invariance case (:328-358), engines 1 / 2 / 4.
+LB_NAMES = ["oblivious", "p2_rtt", "p2_ecn"]
+CC_NAMES = ["none", "cubic", "swift"]
+PROPS_DIR = os.path.join(GOLDEN, "props")
+
+
+def gen_prop(seed, kind=0, engines=None):
+    sp = ref.prop_spec(seed, kind)
+    kw = dict(topo="star" if sp["star"] else "fat_tree", topo_arg=sp["topo_arg"], rate_bps=sp["rate_bps"],
+              link_delay_ns=sp["link_delay_ns"], qcap_bytes=0, loss=sp["drop"], seed=seed,
+              chunk_bytes=sp["chunk_bytes"], paths=sp["paths"], lb=LB_NAMES[sp["lb"]], cc=CC_NAMES[sp["cc"]],
+              cc_scope=sp["cc_scope"], engines=sp["engines"], conn_split=sp["conn_split"],
+              receiver_driven=bool(sp["receiver_driven"]), ordered=bool(sp["ordered"]))
+    if kind == 1:
+        kw.update(engines=engines, conn_split=1 if engines > 1 else 0)
+    trim = kind == 0 and seed % 10 == 5
+    if trim:
+        kw.update(queue="trim", qcap_bytes=64 * 1024, trim_depth=8)
+    flows = [(s_, d_, ln, 1) for s_, d_, ln, _ in sp["msgs"]]
+    tmp = f"/tmp/cnprop_{kind}_{seed}_{engines}"
+    data, acks_des, _, st = ref.record(tmp, flows=flows, window=1, cutoff_ns=2_000_000_000, **kw)
+    assert st["quiesced"] == 1 and st["bytes_ok"] == st["completions"] == len(flows), (seed, st)
+    psn = st.pop("psn")
+    ordered = kw["ordered"]
+    acks, cpls, _ = ref.rx_replay(data, st["n_hosts"], kw["chunk_bytes"], psn=psn if ordered else None,
+                                  ordered=ordered)
+    out = {"data": data, "acks": acks, "completions": cpls}
+    if ordered:
+        out["psn"] = psn
+    sl = st.pop("submits")
+    hosts = []
+    for s_ in [m[0] for m in sp["msgs"]]:
+        if s_ not in hosts:
+            hosts.append(s_)
+    host_meta = []
+    for h in hosts:
+        sub = sl[sl["src"] == h]
+        subs = np.zeros(len(sub), dtype=ref.HOST_SUBMIT_DTYPE)
+        for f in ("t", "len", "tag", "dst"):
+            subs[f] = sub[f]
+        ah = acks_des[acks_des["dst"] == h]
+        t_last = max(int(subs["t"].max()), int(ah["aux"].max()) if len(ah) else 0)
+        rkw = dict(topo=kw["topo"], topo_arg=kw["topo_arg"], rate_bps=kw["rate_bps"],
+                   link_delay_ns=kw["link_delay_ns"], qcap_bytes=0, seed=seed, chunk_bytes=kw["chunk_bytes"],
+                   paths=kw["paths"], lb=kw["lb"], cc=kw["cc"], cc_scope=kw["cc_scope"], engines=kw["engines"],
+                   conn_split=bool(kw["conn_split"]), receiver_driven=kw["receiver_driven"], ordered=ordered,
+                   cutoff_ns=t_last + 20_000_000)
+        tx, stt, conns = ref.host_replay(ah, subs, h, **rkw)
+        swift_t = 3 * int(stt["base_rtt"]) if kw["cc"] == "swift" else 0
+        host_meta.append(dict(src=int(h), conns=[int(c) for c in conns],
+                              n_paths=[int(x) for x in _path_counts(kw, h, conns)],
+                              base_rtt=int(stt["base_rtt"]), rto_min=int(stt["rto_min"]),
+                              rto_max=int(stt["rto_max"]), commit_ahead=int(stt["commit_ahead"]),
+                              initial_credit=int(stt["bdp"]), end_time=int(stt["end_time"]),
+                              swift_target_ns=swift_t, stats={k: int(v) for k, v in stt.items()}))
+        out[f"h{h}_acks"] = ah
+        out[f"h{h}_submits"] = subs
+        out[f"h{h}_tx"] = tx
+    meta = dict(seed=seed, kind=kind, trim=trim, record=kw, flows=flows, n_hosts=int(st["n_hosts"]),
+                chunk_bytes=kw["chunk_bytes"], des_stats={k: int(v) for k, v in st.items()}, hosts=host_meta)
+    os.makedirs(PROPS_DIR, exist_ok=True)
+    name = f"prop_{seed}" if kind == 0 else f"enginv_{seed}_e{engines}"
+    np.savez_compressed(os.path.join(PROPS_DIR, f"{name}.npz"),
+                        meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8), **out)
+    return meta
+
+
+def gen_props(n_seeds=256):
+    tally = dict(star=0, ordered=0, rd=0, trim=0, multi_engine=0, split=0, rtx=0, rtos=0, fast=0, cubic=0,
+                 per_path=0)
+    for seed in range(n_seeds):
+        m = gen_prop(seed)
+        r = m["record"]
+        tally["star"] += r["topo"] == "star"
+        tally["ordered"] += r["ordered"]
+        tally["rd"] += r["receiver_driven"]
+        tally["trim"] += m["trim"]
+        tally["multi_engine"] += r["engines"] > 1
+        tally["split"] += bool(r["conn_split"])
+        tally["cubic"] += r["cc"] == "cubic"
+        tally["per_path"] += r["cc_scope"] == 1
+        tally["rtx"] += m["des_stats"]["chunk_rtx"]
+        tally["rtos"] += m["des_stats"]["rtos"]
+        tally["fast"] += m["des_stats"]["fast_rtx"]
+    for seed in range(12):
+        for e in (1, 2, 4):
+            gen_prop(seed, kind=1, engines=e)
+    print("props:", tally)
+
+
 def gen_rng():
     """RngStream / select_path draw sequences (rng.hpp:29-60, lb.cpp:7-27).
 
@@ -635,6 +735,9 @@ def main(argv):
             continue
         if n == "rng":
             gen_rng()
+            continue
+        if n == "props":
+            gen_props()
             continue
         if n == "host":
             for m in HOST_DES:

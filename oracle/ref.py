@@ -71,6 +71,27 @@ class SenderStats(ctypes.Structure):
         ("bdp", ctypes.c_int64), ("commit_ahead", ctypes.c_int64), ("rts_sent", ctypes.c_uint64)]
 
 
+class PropSpec(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("star", "topo_arg", "ordered", "receiver_driven", "zero_loss",
+                                               "engines", "conn_split", "paths", "lb", "cc", "cc_scope",
+                                               "n_msgs")] + [
+        ("chunk_bytes", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("rate_bps", ctypes.c_double),
+        ("drop", ctypes.c_double), ("link_delay_ns", ctypes.c_int64), ("src", ctypes.c_int32 * 8),
+        ("dst", ctypes.c_int32 * 8), ("len", ctypes.c_uint64 * 8), ("tag", ctypes.c_uint64 * 8)]
+
+
+def prop_spec(seed, kind=0):
+    """The reference property suite's scenario draws for `seed`
+    (test_reliability_props.cpp: kind 0 run_scenario, kind 1 the
+    engine-invariance case), as a dict."""
+    o = PropSpec()
+    lib().cnref_prop_spec_draw(seed, kind, ctypes.byref(o))
+    d = {k: getattr(o, k) for k, _ in PropSpec._fields_ if k not in ("src", "dst", "len", "tag", "pad")}
+    n = o.n_msgs
+    d["msgs"] = [(o.src[i], o.dst[i], int(o.len[i]), int(o.tag[i])) for i in range(n)]
+    return d
+
+
 class Submit(ctypes.Structure):
     _fields_ = [("t", ctypes.c_int64), ("len", ctypes.c_uint64), ("tag", ctypes.c_uint64)]
 
@@ -116,6 +137,7 @@ def lib():
         L.cnref_host_replay.argtypes = [ctypes.POINTER(Scenario), i32, vp, u64, vp, u64, vp, u64,
                                         ctypes.POINTER(SenderStats), vp, u32, i32, i32]
         L.cnref_set_host_probes.argtypes = [vp, u32, vp, u32, u32]
+        L.cnref_prop_spec_draw.argtypes = [u64, i32, vp]
         L.cnref_set_host_probes.restype = None
         L.cnref_rng_u64.argtypes = [u64, ctypes.c_char_p, i64, u64, vp]
         L.cnref_next_below.argtypes = [u64, ctypes.c_char_p, i64, vp, u64, vp]

@@ -963,6 +963,92 @@ int cnref_host_replay(const cnref_scenario* sc, int src, const cnref_host_submit
     }
 }
 
+// ------------------------------------------------ randomized scenarios
+// The reference's own scenario draws (tests/test_reliability_props.cpp:
+// run_scenario :126-218 and the engine-invariance case :328-358), restated
+// draw for draw over its RngStream so the generator's scenarios are
+// exactly the reference suite's.  kind 0: "prop-scenario" (1,000-scenario
+// suite), kind 1: "prop-engines" (engines 1 / 2 / 4 run the same specs).
+struct cnref_prop_spec {
+    int32_t star, topo_arg, ordered, receiver_driven, zero_loss, engines, conn_split, paths, lb, cc, cc_scope,
+        n_msgs;
+    uint32_t chunk_bytes, pad;
+    double rate_bps, drop;
+    int64_t link_delay_ns;
+    int32_t src[8], dst[8];
+    uint64_t len[8], tag[8];
+};
+
+int cnref_prop_spec_draw(uint64_t seed, int kind, cnref_prop_spec* o) {
+    std::memset(o, 0, sizeof *o);
+    if (kind == 0) {
+        RngStream rng(seed, "prop-scenario");
+        bool star = rng.next_below(4) == 0;
+        o->star = star;
+        o->topo_arg = star ? 8 : 4;
+        const int n_hosts = star ? 8 : 16;  // build_star(8) / build_fat_tree(4)
+        o->rate_bps = rng.next_below(2) ? 100e9 : 10e9;
+        o->link_delay_ns = rng.next_below(2) ? 1000 : 200;
+        o->zero_loss = seed % 4 == 0;
+        o->drop = 0.0;
+        if (!o->zero_loss) o->drop = (1.0 / 256) + rng.next_double() * (1.0 / 64 - 1.0 / 256);
+        static const uint32_t kChunks[] = {4032, 8064, 16128, 32768};
+        o->chunk_bytes = kChunks[rng.next_below(4)];
+        static const int kPaths[] = {1, 2, 4, 8};
+        o->paths = kPaths[rng.next_below(4)];
+        o->engines = rng.next_below(2) ? 2 : 1;
+        o->conn_split = o->engines > 1 && rng.next_below(2) == 0;
+        o->lb = static_cast<int>(rng.next_below(3));
+        switch (rng.next_below(3)) {
+            case 0: o->cc = 0; break;
+            case 1: o->cc = 1; break;
+            default: o->cc = 2; break;
+        }
+        o->cc_scope = rng.next_below(2) ? 1 : 0;
+        o->receiver_driven = seed % 10 == 3;
+        o->ordered = seed % 10 == 7;
+        if (o->receiver_driven) o->cc = 0;
+        if (o->ordered) {
+            o->paths = 1;
+            o->engines = 1;
+            o->conn_split = 0;
+            o->receiver_driven = 0;
+            if (o->cc == 2) o->cc = 1;
+        }
+        o->n_msgs = 3 + static_cast<int>(rng.next_below(3));
+        for (int i = 0; i < o->n_msgs; ++i) {
+            o->src[i] = static_cast<int>(rng.next_below(n_hosts));
+            o->dst[i] = static_cast<int>(rng.next_below(n_hosts - 1));
+            if (o->dst[i] >= o->src[i]) ++o->dst[i];
+            uint64_t len = 4032 * (1 + rng.next_below(48)) + rng.next_below(4032);
+            if (i == 1 && seed % 8 == 0) len = 1 + rng.next_below(4032);
+            if (i == 0 && seed % 16 == 0) len = 1;
+            o->len[i] = len;
+            o->tag[i] = seed * 100 + static_cast<uint64_t>(i);
+        }
+        return 0;
+    }
+    RngStream rng(seed, "prop-engines");
+    o->star = 0;
+    o->topo_arg = 4;
+    o->rate_bps = 100e9;
+    o->link_delay_ns = 500;
+    o->drop = 1.0 / 128;
+    o->paths = 4;
+    o->chunk_bytes = 16128;
+    o->cc = 1;
+    o->lb = 1;
+    o->n_msgs = 6;
+    for (int i = 0; i < 6; ++i) {
+        o->src[i] = static_cast<int>(rng.next_below(16));
+        o->dst[i] = static_cast<int>(rng.next_below(15));
+        if (o->dst[i] >= o->src[i]) ++o->dst[i];
+        o->len[i] = 1 + rng.next_below(65536);
+        o->tag[i] = 1000 + static_cast<uint64_t>(i);
+    }
+    return 0;
+}
+
 // Times the reference sender on the same replay (construction and event
 // scheduling outside the timer): T threads x reps replays.  Returns the
 // slowest thread's seconds.

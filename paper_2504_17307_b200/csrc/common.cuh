@@ -55,6 +55,26 @@ __device__ inline uint32_t table_insert(unsigned long long* keys, uint32_t mask,
     return kInf;
 }
 
+// acquire / release and volatile accesses for the cross-block handshakes
+// (decoupled look-back, published table values)
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+    return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
 __host__ __device__ inline uint32_t enc_hdr(uint32_t conn, uint32_t msg, uint32_t csn,
                                             uint32_t last, uint32_t rsvd) {
     return (conn << 24) | (msg << 17) | (csn << 9) | (last << 8) | rsvd;

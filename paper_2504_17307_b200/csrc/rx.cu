@@ -38,7 +38,6 @@
 #include <string>
 #include <vector>
 
-#include "bulk.cuh"
 #include "common.cuh"
 
 namespace cnb {

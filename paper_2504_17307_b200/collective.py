@@ -8,13 +8,18 @@ r receives segment (r-s-1) mod N from r-1 and reduces it into its own copy
 x[j-1] + (... + (x[j+1] + x[j])) and the result is bit-identical to the
 same-order CPU fold (oracle/chunknet_oracle.c: orc_ring_allreduce).
 
-Data movement is B200-native: every segment message is packetized by its
-sender (cn_packetize = Transport::send_chunk, transport.cpp:433-494) into a
-header ring in the sender's HBM, and the receiver runs the transport's
-receive path (csrc/rx.cu) with the fused reduce scatter reading both the
-headers and the payload straight out of the peer's memory over NVLink
-(CUDA IPC mapping, zero copy, payload_stride 0).  Neighbours synchronise
-with device-side progress flags (cn_flag_*), never the host.
+Data movement is B200-native: every segment message is
+packetized by its sender (cn_packetize = Transport::send_chunk,
+transport.cpp:433-494) and pushed in chunk-aligned pieces by the copy
+engines over NVLink (CUDA IPC peer mappings).  Reduce-scatter pieces land in
+a staging slot of the receiver's HBM and the receiver's transport receive
+path (csrc/rx.cu) reduces them into its accumulator (fused scatter-reduce);
+all-gather pieces land directly in the receiver's accumulator segment and
+its receive path runs on the headers only (bookkeeping, no payload pass).
+Neighbours synchronise with device-side progress counters (cn_ctr_*),
+never the host.  The scheduler's per-chunk paths travel in the headers and
+drive the receive bookkeeping; NVLink gives one physical path per peer
+pair, so the bytes move on two copy-engine lanes by piece.
 """
 import ctypes
 
@@ -204,12 +209,14 @@ class RingAllreduce:
                           for st in self.steps]
         # exchange IPC handles: staging, header buffers, flags
         mine = {"stage": _ipc_handle(self._stage), "flags": _ipc_handle(self._flag_buf),
+                "acc": _ipc_handle(self._acc_buf),
                 "hdrs": [_ipc_handle(b) if b is not None else None for b in self._hdr_bufs]}
         allh = [None] * n
         dist.all_gather_object(allh, mine, group=group)
         prev, nxt = (r - 1) % n, (r + 1) % n
         self._opened = []
         self.next_stage = self._open(allh[nxt]["stage"])
+        self.next_acc = self._open(allh[nxt]["acc"])
         self.next_hdrs = [self._open(h) if h is not None else None for h in allh[nxt]["hdrs"]]
         self.next_flags = self._open(allh[nxt]["flags"])
         self.prev_flags = self._open(allh[prev]["flags"]) if prev != nxt else self.next_flags
@@ -221,12 +228,13 @@ class RingAllreduce:
                   arena_bytes=0, max_batch=maxp + 16, max_posts=4 * n)
         cfg = TransportConfig(chunk_bytes=chunk_bytes, paths=paths, lb="p2_rtt", carry_payload=True)
         self.rx_rs = Transport(cfg, reduce=red, **kw)
-        self.rx_ag = Transport(cfg, **kw)
+        # all-gather: the payload lands in place, the receive path keeps the books
+        self.rx_ag = Transport(TransportConfig(chunk_bytes=chunk_bytes, paths=paths, lb="p2_rtt",
+                                               carry_payload=False), **kw)
         accb = self.acc.view(torch.uint8)
         for (k, ph, s, snd, rcv, tag) in self.steps:
-            if ph in ("rs", "ag"):
-                (self.rx_rs if ph == "rs" else self.rx_ag).post(
-                    tag, accb[self.seg_off[rcv]: self.seg_off[rcv] + self.seg_bytes[rcv]])
+            if ph == "rs":
+                self.rx_rs.post(tag, accb[self.seg_off[rcv]: self.seg_off[rcv] + self.seg_bytes[rcv]])
         self.push_streams = [torch.cuda.Stream(self.dev) for _ in range(self.lanes)]
         self.hdr_stream = torch.cuda.Stream(self.dev)
         self.rx_done = [[torch.cuda.Event() for _ in range(P)] for _ in self.steps]
@@ -303,8 +311,11 @@ class RingAllreduce:
                 # its receive path runs pieces in order)
                 self._wait(self.f_freed + 8 * ln, q + 1 - P // NL, sp)
                 lo, hi = self.bounds[snd][p], self.bounds[snd][p + 1]
-                _lib.check(L.cn_copy_async(self.next_stage + p * self.slot_bytes, acc + self.seg_off[snd] + lo,
-                                           hi - lo, ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
+                # reduce-scatter: into next's staging slot; all-gather: the
+                # final bytes straight into next's accumulator segment
+                dst = self.next_stage + p * self.slot_bytes if ph == "rs" else self.next_acc + self.seg_off[snd] + lo
+                _lib.check(L.cn_copy_async(dst, acc + self.seg_off[snd] + lo, hi - lo,
+                                           ctypes.c_void_p(sp.cuda_stream)), "cn_copy_async")
                 if p == 0:  # the whole step's headers ride with its first piece
                     if k == 1:
                         sp.wait_event(self.ev_hdrs)
@@ -317,8 +328,11 @@ class RingAllreduce:
                 rlo = self.bounds[rcv][p]
                 a, b = self.pkt_range(rcv, p)
                 hd = _PeerView(self._hdr_bufs[k].data_ptr() + a * 64, (b - a) * 64)
-                src = _PeerView(self._stage.data_ptr() + p * self.slot_bytes - rlo, self.slot_bytes)
-                rx.rx_batch_async(hd, src, 0, s, n=b - a)
+                if ph == "rs":
+                    src = _PeerView(self._stage.data_ptr() + p * self.slot_bytes - rlo, self.slot_bytes)
+                    rx.rx_batch_async(hd, src, 0, s, n=b - a)
+                else:  # headers only: the bytes already sit in the accumulator
+                    rx.rx_batch_async(hd, None, 0, s, n=b - a)
                 self.rx_done[k][p].record(s)
                 self._signal(self.prev_flags + 16 + 8 * ln, q + 1, s)  # prev's freed counter
         for sl in self.push_streams + [self.hdr_stream]:

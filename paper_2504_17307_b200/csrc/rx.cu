@@ -1924,6 +1924,10 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         }
         const uint32_t cg = cw < cmax ? cw : cmax;
         auto copy = [&] {
+            if (!d.carry) {  // headers only (e.g. the ring's all-gather, payload already in place)
+                prof_mark(ev, s);
+                return;
+            }
             if (d.reduce == 1)
                 k_copy<1><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
             else if (d.reduce == 2)
@@ -2000,7 +2004,7 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         k_finalize<<<gb, kScanThreads, 0, s>>>(d, d_hdrs, d_result);
         prof_mark(ev, s);
     }
-    rx->launches = n > 0 ? 6 : 1;
+    rx->launches = n > 0 ? (d.carry ? 6 : 5) + (d.ordered ? 1 : 0) : 1;
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }

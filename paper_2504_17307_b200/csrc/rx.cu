@@ -68,7 +68,7 @@ struct RxCtl {
     // c_first is double-buffered by batch parity: k_finalize runs beside the
     // scatter (which reads the batch's half), so it clears the OTHER half --
     // the tiles the previous batch dirtied, listed in dirty[par ^ 1]
-    uint32_t par, copy_par, n_dirty[2];
+    uint32_t par, copy_par, n_dirty[2], n_dirty_next, pad_d;
     uint32_t n_aret[2];  // arena ranges of messages delivered in the batch of that parity
     // message states: a free ring of GenState indices; the (rconn, msg_seq)
     // table maps keys to them, tombstones are compacted by a rebuild
@@ -82,7 +82,8 @@ enum : uint8_t { PC_STALE = 1, PC_ACK = 2, PC_COPY = 4, PC_DELIVER = 8, PC_NACK 
 constexpr uint32_t kTrimMax = 16384;  // trimmed headers per batch (sorted in one block, 128 KB smem)
 constexpr uint32_t kStale = kInf;    // p_gen marker: stale before the batch
 constexpr uint32_t kErr = kInf - 1;  // p_gen marker: rejected packet
-constexpr int kAckTile = 128;        // packets per k_acks tile / block
+constexpr int kAckTileMax = 128;     // packets per k_acks tile (large batches)
+constexpr int kAckTileMin = 32;      // ... small batches
 constexpr int kAckWarps = 8;         // 256 threads: 4 decide warps, 8 ack builders
 constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
 constexpr int kCopyUnroll = 8;       // 16-byte vectors in flight per lane
@@ -91,6 +92,7 @@ constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 
 struct RxDev {
     uint32_t cb, max_pl, ppc, conn_mask, gen_mask, carry, reduce, elem, post_mask;
+    uint32_t ack_tile;  // packets per k_acks tile this batch (32 or 128)
     unsigned long long* post_key;  // [posts] message tag (posted destinations)
     unsigned long long* post_val;  // [posts] device pointer
     unsigned long long* post_len;  // [posts] bytes
@@ -133,7 +135,6 @@ struct RxDev {
     uint32_t* trim_list;  // [kTrimMax] trimmed headers of the batch (packet index)
     unsigned long long* tile_state;  // [ack tiles] decoupled look-back (ack order)
     unsigned long long* scan_state;  // [scan tiles] segmented look-back (prefix max)
-    uint32_t* plan_base;             // [touched] first scan tile of each message
     RxCtl* ctl;
     uint8_t* arena;
 };
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     const int lane = threadIdx.x & 31;
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t par = d.ctl->par;
-    const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
+    const uint32_t tiles = (n + d.ack_tile - 1) / d.ack_tile;
     if (i < tiles) d.tile_state[i] = 0;
     if (i == 0) d.ctl->copy_par = par;  // k_copy's half (k_finalize flips par beside it)
     for (int k = threadIdx.x; k < kIngMap; k += kIngestThreads) {
@@ -573,29 +574,33 @@ __device__ __forceinline__ uint32_t block_scan_max(uint32_t v, uint32_t* wsum) {
 
 
 // -------------------------------------------------------------------- scan
-// Flattened over every touched message: tile = 256 consecutive chunks of
-// one message's range [lo, hi), handed out by ticket (tickets of a message
-// are consecutive, planned by k_ingest's last block).  Per chunk: the
-// completion time cpl (max first arrival over its missing packets), the
-// new-packet bitmask and last new packet (for finalize), and the prefix max
-// pmax that drives the cumulative cursor (chunk_completed's
-// `while (complete) ++cum`, :736-738) -- a segmented decoupled look-back
-// across the message's tiles.
+// Flattened over every touched message: the batch's chunk ranges [lo, hi)
+// are laid end to end and cut into tiles of 256 consecutive chunks, so a
+// tile may hold the tail of one message, several whole small messages and
+// the head of another (a thousand 1-chunk messages are 4 tiles, not 1,000).
+// Per chunk: the completion time cpl (max first arrival over its missing
+// packets), the new-packet bitmask and last new packet (for finalize), and
+// the prefix max pmax that drives the cumulative cursor (chunk_completed's
+// `while (complete) ++cum`, :736-738) -- a segmented max-scan inside the
+// tile (reset at message boundaries) plus a decoupled look-back for the
+// message that continues from earlier tiles.
 constexpr uint32_t kPlanMax = 4096;  // touched messages per batch planned in smem
 
 // Every scan/finalize block plans the batch itself (no serial phase): for
 // each touched message its chunk range [lo, hi) -- hi = the chunk vector
-// size (:636-637) -- and the first tile index, as an exclusive prefix sum in
-// shared memory.  Returns the total tile count.  In k_scan lo = cum and hi
-// = max(n_init, max touched chunk + 1); k_finalize reads the values k_scan
-// stored (lo_batch, n_init), so both see the same tiles.
-__device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool scan,
-                               uint32_t* s_base, uint32_t* s_w) {
+// size (:636-637) -- and the exclusive prefix s_F[k] of the range lengths
+// (s_F[nt] = total chunks); a tile's thread reads lo back from the message
+// state (scan: cum, finalize: lo_batch or 0).  In k_scan lo = cum and hi =
+// max(n_init, max touched chunk + 1); k_finalize reads the values k_scan
+// stored (lo_batch, n_init; a delivered message whole), so both see the
+// same flattened layout.
+__device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool scan, uint32_t* s_F,
+                               uint32_t* s_w) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     uint32_t carry = 0;
     for (uint32_t k0 = 0; k0 < nt; k0 += blockDim.x) {
         const uint32_t k = k0 + threadIdx.x;
-        uint32_t tl = 0;
+        uint32_t len = 0;
         if (k < nt) {
             const GenState* G = &d.gen[d.touched[k]];
             uint32_t lo, hi;
@@ -613,9 +618,9 @@ __device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool
                 lo = G->lo_batch;
                 hi = G->n_init;
             }
-            tl = (hi - lo + kScanThreads - 1) / kScanThreads;
+            len = hi > lo ? hi - lo : 0;
         }
-        uint32_t inc = tl;
+        uint32_t inc = len;
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
@@ -627,28 +632,68 @@ __device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool
             if (q < w) wpre += s_w[q];
             tot += s_w[q];
         }
-        if (k < nt) s_base[k] = carry + wpre + inc - tl;
+        if (k < nt) s_F[k] = carry + wpre + inc - len;
         carry += tot;
         __syncthreads();
     }
-    if (threadIdx.x == 0) s_base[nt] = carry;
+    if (threadIdx.x == 0) s_F[nt] = carry;
     __syncthreads();
     return carry;
 }
 
-__device__ __forceinline__ uint32_t find_gen_of_ticket(const uint32_t* s_base, uint32_t nt, uint32_t ticket) {
-    uint32_t lo = 0, hi = nt;  // last k with s_base[k] <= ticket
+// the message holding flattened chunk f: the last k with s_F[k] <= f
+// (empty ranges share their successor's offset and are skipped)
+__device__ __forceinline__ uint32_t msg_of_flat(const uint32_t* s_F, uint32_t nt, uint32_t f) {
+    uint32_t lo = 0, hi = nt;
     while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (s_base[mid] <= ticket) lo = mid; else hi = mid;
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_F[mid] <= f) lo = mid; else hi = mid;
     }
     return lo;
 }
 
+// Block-wide segmented inclusive max-scan: segments start where head is
+// set (and at thread 0).  Returns this thread's inclusive value.
+__device__ __forceinline__ uint32_t block_seg_scan_max(uint32_t v, bool head, uint32_t* s_v, uint32_t* s_h) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t h = head ? 1u : 0u;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yv = __shfl_up_sync(0xffffffffu, v, o);
+        const uint32_t yh = __shfl_up_sync(0xffffffffu, h, o);
+        if (lane >= o) {
+            if (!h) v = v > yv ? v : yv;
+            h |= yh;
+        }
+    }
+    if (lane == 31) {
+        s_v[w] = v;
+        s_h[w] = h;
+    }
+    __syncthreads();
+    if (w == 0) {  // scan the warp totals
+        uint32_t x = lane < nw ? s_v[lane] : 0, xh = lane < nw ? s_h[lane] : 1;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t yv = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t yh = __shfl_up_sync(0xffffffffu, xh, o);
+            if (lane >= o) {
+                if (!xh) x = x > yv ? x : yv;
+                xh |= yh;
+            }
+        }
+        if (lane < nw) s_v[lane] = x;
+    }
+    __syncthreads();
+    if (w > 0 && !h) {  // no segment head in this warp up to me: the earlier warps' carry
+        const uint32_t p = s_v[w - 1];
+        v = v > p ? v : p;
+    }
+    return v;
+}
+
 __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t s_ticket, s_k, s_carry;
-    __shared__ uint32_t s_base[kPlanMax + 1];
+    __shared__ uint32_t s_v[32], s_h[32];
+    __shared__ uint32_t s_ticket, s_carry, s_k0;
+    __shared__ uint32_t s_F[kPlanMax + 1];
     const int lane = threadIdx.x & 31;
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
@@ -656,66 +701,66 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
     const uint32_t* __restrict__ cf = first_of(d, d.ctl->par);
     uint32_t my_n = 0;             // first arrivals (n_copied) and their bytes
     unsigned long long my_b = 0;
-    const uint32_t total = plan_block(d, nt, epoch, true, s_base, wsum);
+    const uint32_t T = plan_block(d, nt, epoch, true, s_F, s_v);
+    const uint32_t tiles = (T + kScanThreads - 1) / kScanThreads;
     if (blockIdx.x == 0 && threadIdx.x == 0 && d.ctl->n_touched > kPlanMax)
         atomicOr(&d.ctl->status, CN_RXF_CAPACITY);
     for (;;) {
-        if (threadIdx.x == 0) {
-            uint32_t tk = atomicAdd(&d.ctl->scan_ticket, 1u);
-            s_ticket = tk;
-            s_k = tk < total ? find_gen_of_ticket(s_base, nt, tk) : 0;
-        }
+        if (threadIdx.x == 0) s_ticket = atomicAdd(&d.ctl->scan_ticket, 1u);
         __syncthreads();
         const uint32_t ticket = s_ticket;
-        if (ticket >= total) break;
-        const uint32_t k = s_k;
-        GenState* G = &d.gen[d.touched[k]];
-        const uint32_t ti = ticket - s_base[k];
-        const uint32_t lo = G->cum;
-        uint32_t hi = G->n_init;
-        {
-            const unsigned long long tch = G->touch;
-            if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
-        }
-
-        const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
-        const uint64_t base = G->chunk_base;
-        uint32_t cpl = 0;
-        if (c < hi) {
-            const uint64_t e = base + c;
+        if (ticket >= tiles) break;
+        const uint32_t f0 = ticket * kScanThreads;
+        const uint32_t f = f0 + threadIdx.x;
+        const bool in = f < T;
+        uint32_t k = 0, c = 0, cpl = 0;
+        GenState* G = nullptr;
+        if (in) {
+            k = msg_of_flat(s_F, nt, f);
+            G = &d.gen[d.touched[k]];
+            c = G->cum + (f - s_F[k]);  // cum: the batch's lower bound (finalize moves it later)
+            const uint64_t e = G->chunk_base + c;
             if (!(d.c_flags[e] & CF_COMPLETE)) {
                 const uint32_t clen = chunk_len_of(d, G->len, c);
                 const uint32_t exp = pkts_of(d, clen);
                 const uint32_t seen = d.c_seen[e];
                 uint32_t newb = 0, last = 0;
-                for (uint32_t s = 0; s < exp; ++s) {
-                    uint32_t f = cf[e * ppc + s];
-                    if (f != kInf) {
-                        newb |= 1u << s;
-                        last = last > f ? last : f;
+                for (uint32_t q = 0; q < exp; ++q) {
+                    uint32_t fa = cf[e * ppc + q];
+                    if (fa != kInf) {
+                        newb |= 1u << q;
+                        last = last > fa ? last : fa;
                         // a first arrival: exactly the packets k_copy scatters
-                        const uint32_t rem = clen - s * d.max_pl;
+                        const uint32_t rem = clen - q * d.max_pl;
                         ++my_n;
                         my_b += rem < d.max_pl ? rem : d.max_pl;
                     }
-                    if ((seen >> s) & 1u) f = 0;
-                    cpl = cpl > f ? cpl : f;
+                    if ((seen >> q) & 1u) fa = 0;
+                    cpl = cpl > fa ? cpl : fa;
                 }
                 d.c_newb[e] = newb;
                 d.c_last[e] = last;
             }
             d.c_cpl[e] = cpl;
         }
-        const uint32_t incl = block_scan_max(cpl, wsum);
+        // segments: one per message present in the tile
+        const bool head = in && (threadIdx.x == 0 || f == s_F[k]);
+        const uint32_t incl = block_seg_scan_max(cpl, head, s_v, s_h);
+        // the message of the tile's first chunk may continue from earlier
+        // tiles (it then spans back to tile F / 256): look back for its carry
         if (threadIdx.x < 32) {
-            const uint32_t agg = wsum[kScanThreads / 32 - 1];
+            const uint32_t fl_ = (f0 + kScanThreads <= T ? f0 + kScanThreads : T) - 1;
+            const uint32_t k0 = msg_of_flat(s_F, nt, f0), kl = msg_of_flat(s_F, nt, fl_);
+            const bool cont = s_F[k0] < f0;           // first message started before this tile
+            const bool last_here = s_F[kl] >= f0;     // last message starts in this tile
+            // the tile's last segment value: the inclusive scan at its last chunk
+            const uint32_t agg = s_v[kScanThreads / 32 - 1];
             uint32_t carry = 0;
-            if (ti == 0) {
-                if (lane == 0) atomicExch(&d.scan_state[ticket], kFlagIncl | agg);
-            } else {
-                if (lane == 0) atomicExch(&d.scan_state[ticket], kFlagAgg | agg);
+            if (last_here && lane == 0) atomicExch(&d.scan_state[ticket], kFlagIncl | agg);
+            if (cont) {
+                if (!last_here && lane == 0) atomicExch(&d.scan_state[ticket], kFlagAgg | agg);
                 int64_t b = static_cast<int64_t>(ticket) - 1;
-                const int64_t seg0 = static_cast<int64_t>(ticket) - ti;  // the message's first tile
+                const int64_t seg0 = static_cast<int64_t>(s_F[k0] / kScanThreads);  // the message's first tile
                 for (;;) {
                     int64_t p = b - lane;
                     unsigned long long v = p >= seg0 ? ld_volatile_u64(&d.scan_state[p]) : kFlagIncl;
@@ -732,21 +777,26 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
                     if (inc) break;
                     b -= 32;
                 }
-                if (lane == 0) {
+                if (!last_here && lane == 0) {
                     __threadfence();
                     atomicExch(&d.scan_state[ticket], kFlagIncl | (agg > carry ? agg : carry));
                 }
             }
-            if (lane == 0) s_carry = carry;
+            if (lane == 0) {
+                s_carry = cont ? carry : 0u;
+                s_k0 = k0;
+            }
         }
         __syncthreads();
-        if (c < hi) {
-            const uint32_t carry = s_carry;
+        if (in) {
+            // the carry belongs to the tile's first message only
+            const uint32_t carry = k == s_k0 ? s_carry : 0u;
             const uint32_t pm = incl > carry ? incl : carry;
-            d.c_pmax[base + c] = pm;
-            if (c == hi - 1) {
+            d.c_pmax[G->chunk_base + c] = pm;
+            if (f + 1 == s_F[k + 1]) {  // the message's last chunk of the batch range
+                const uint32_t hi = c + 1;
                 G->deliver_t = hi == G->nchunks ? pm : kInf;
-                G->n_init = hi;  // every tile computes the same hi: idempotent
+                G->n_init = hi;
             }
         }
         __syncthreads();
@@ -1156,9 +1206,14 @@ __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __re
     }
 }
 
+// TILE packets per tile: 128 for large batches; 32 for small ones, so that a
+// batch of a few thousand acks spreads over many blocks instead of making
+// 8 warps per tile build 16 acks each in turn
+template <int TILE>
 __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
     RxDev d, const cn_pkt_hdr* __restrict__ hdrs, uint32_t n, cn_ack_rec* __restrict__ acks,
     uint32_t max_acks, cn_completion* __restrict__ cpls, uint32_t max_cpls) {
+    constexpr int kAckTile = TILE;
     constexpr int kDecideWarps = kAckTile / 32;
     __shared__ cn_ack_rec s_rec[kAckTile];
     __shared__ uint8_t s_cls[kAckTile];
@@ -1304,14 +1359,16 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
 // grid publishes the batch result and arms the next batch.
 __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                                            cn_rx_result* res) {
-    __shared__ uint32_t s_ticket, s_k, s_cnt;
+    __shared__ uint32_t s_ticket;
     __shared__ bool last_block;
     __shared__ uint32_t s_w[32];
-    __shared__ uint32_t s_base[kPlanMax + 1];
+    __shared__ uint32_t s_cnt[kScanThreads];  // per message segment of the tile: chunks now in the cum prefix
+    __shared__ uint32_t s_F[kPlanMax + 1];
     const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
     const uint32_t ppc = d.ppc;
     const uint32_t par = d.ctl->par;
-    const uint32_t total = plan_block(d, nt, 0, false, s_base, s_w);
+    const uint32_t T = plan_block(d, nt, 0, false, s_F, s_w);
+    const uint32_t total = (T + kScanThreads - 1) / kScanThreads;
     // the previous batch's first-arrival half: its scatter has finished
     // (stream order), the next batch uses it
     {
@@ -1322,7 +1379,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             const unsigned long long v = dl[j];
             if (threadIdx.x < (v & 511)) {
                 const uint64_t e = (v >> 9) + threadIdx.x;
-                for (uint32_t s = 0; s < ppc; ++s) cf1[e * ppc + s] = kInf;
+                for (uint32_t q = 0; q < ppc; ++q) cf1[e * ppc + q] = kInf;
             }
         }
     }
@@ -1335,53 +1392,49 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         if (d.arena_blocks) ring_advance(&d.ctl->arena, d.arena_blocks, d.arena_bits);
     }
     for (;;) {
-        if (threadIdx.x == 0) {
-            uint32_t tk = atomicAdd(&d.ctl->fin_ticket, 1u);
-            s_ticket = tk;
-            s_k = tk < total ? find_gen_of_ticket(s_base, nt, tk) : 0;
-            s_cnt = 0;
-        }
+        if (threadIdx.x == 0) s_ticket = atomicAdd(&d.ctl->fin_ticket, 1u);
+        s_cnt[threadIdx.x] = 0;
         __syncthreads();
         const uint32_t ticket = s_ticket;
         if (ticket >= total) break;
-        const uint32_t k = s_k;
-        const uint32_t g = d.touched[k];
-        GenState* G = &d.gen[g];
-        const bool retire = G->deliver_t != kInf;
-        const uint32_t lo = retire ? 0u : G->lo_batch, hi = retire ? G->nchunks : G->n_init;
-        const uint32_t ti = ticket - s_base[k];
-        const uint32_t c = lo + ti * kScanThreads + threadIdx.x;
-        const uint64_t base = G->chunk_base;
-        uint32_t done = 0;
-        if (threadIdx.x == 0) {
-            d.scan_state[ticket] = 0;  // re-arm the look-back state
-            if (ticket < d.dirty_cap) {
-                const uint32_t cnt = min(hi - (lo + ti * kScanThreads), static_cast<uint32_t>(kScanThreads));
-                dirty[ticket] = ((base + lo + ti * kScanThreads) << 9) | cnt;
+        const uint32_t f0 = ticket * kScanThreads;
+        const uint32_t f = f0 + threadIdx.x;
+        if (threadIdx.x == 0) d.scan_state[ticket] = 0;  // re-arm the look-back state
+        const bool in = f < T;
+        uint32_t k = 0, c = 0, done = 0;
+        bool head = false, retire = false;
+        GenState* G = nullptr;
+        uint64_t base = 0;
+        if (in) {
+            k = msg_of_flat(s_F, nt, f);
+            G = &d.gen[d.touched[k]];
+            retire = G->deliver_t != kInf;
+            c = (retire ? 0u : G->lo_batch) + (f - s_F[k]);
+            base = G->chunk_base;
+            head = threadIdx.x == 0 || f == s_F[k];
+            if (head) {  // this tile's run of the message: c_first cleared through the dirty list
+                const uint32_t end = s_F[k + 1] < f0 + kScanThreads ? s_F[k + 1] : f0 + kScanThreads;
+                const uint32_t j = atomicAdd(&d.ctl->n_dirty_next, 1u);
+                if (j < d.dirty_cap) dirty[j] = ((base + c) << 9) | (end - f);
             }
         }
-        if (retire) {
+        if (in && retire) {
             // initial chunk state for the next owner; this batch's c_first
             // half is cleared through the dirty list (the scatter reads it)
-            if (c < hi) {
-                const uint64_t e = base + c;
-                d.c_seen[e] = 0;
-                d.c_flags[e] = 0;
-                d.c_txt[e] = 0;
-                d.c_path[e] = 0;
-                d.c_init[e] = kInf;
-                d.c_cpl[e] = kInf;
-                d.c_pmax[e] = kInf;
-                d.c_newb[e] = 0;
-                d.c_last[e] = 0;
-                d.c_newfl[e] = 0;
-                const uint64_t rp = e >= d.pool_cap ? e - d.pool_cap : e;  // ring position
-                atomicOr(&d.pool_bits[rp >> 5], 1u << (rp & 31));
-            }
-            __syncthreads();
-            continue;
-        }
-        if (c < hi) {
+            const uint64_t e = base + c;
+            d.c_seen[e] = 0;
+            d.c_flags[e] = 0;
+            d.c_txt[e] = 0;
+            d.c_path[e] = 0;
+            d.c_init[e] = kInf;
+            d.c_cpl[e] = kInf;
+            d.c_pmax[e] = kInf;
+            d.c_newb[e] = 0;
+            d.c_last[e] = 0;
+            d.c_newfl[e] = 0;
+            const uint64_t rp = e >= d.pool_cap ? e - d.pool_cap : e;  // ring position
+            atomicOr(&d.pool_bits[rp >> 5], 1u << (rp & 31));
+        } else if (in) {
             const uint64_t e = base + c;
             uint32_t fl = d.c_flags[e];
             if (!(fl & CF_COMPLETE)) {
@@ -1408,13 +1461,17 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             done = d.c_pmax[e] != kInf;
             d.c_cpl[e] = kInf;
             d.c_pmax[e] = kInf;
+            if (done) atomicAdd(&s_cnt[s_F[k] > f0 ? s_F[k] - f0 : 0u], 1u);  // slot of the run's first chunk
         }
-        done = __reduce_add_sync(0xffffffffu, done);
-        if ((threadIdx.x & 31) == 0 && done) atomicAdd(&s_cnt, done);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            const uint32_t ntiles = (hi - lo + kScanThreads - 1) / kScanThreads;
-            if (s_cnt) atomicAdd(&G->cum_add, s_cnt);
+        if (in && head && !retire) {
+            // the message's tiles report their share of the new cum prefix;
+            // the last one to report moves cum
+            const uint32_t lo = G->lo_batch;
+            const uint32_t F0 = s_F[k], F1 = s_F[k + 1];
+            const uint32_t ntiles = (F1 - 1) / kScanThreads - F0 / kScanThreads + 1;
+            const uint32_t cnt = s_cnt[threadIdx.x];  // the head is the run's first chunk
+            if (cnt) atomicAdd(&G->cum_add, cnt);
             __threadfence();
             if (atomicAdd(&G->tiles_done, 1u) == ntiles - 1) {
                 __threadfence();
@@ -1527,7 +1584,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->fin_ticket = 0;
         uint32_t ep = C->epoch + 1;
         C->epoch = ep ? ep : 1;
-        C->n_dirty[par] = min(total, d.dirty_cap);
+        C->n_dirty[par] = min(C->n_dirty_next, d.dirty_cap);
+        C->n_dirty_next = 0;
         C->n_dirty[par ^ 1u] = 0;
         C->n_aret[par ^ 1u] = 0;
         C->par = par ^ 1u;
@@ -1583,6 +1641,7 @@ __global__ void k_reset(RxDev d, int full) {
         d.ctl->arena.head = d.ctl->arena.tail = 0;
         d.ctl->n_dirty[0] = 0;
         d.ctl->n_dirty[1] = 0;
+        d.ctl->n_dirty_next = 0;
         d.ctl->n_aret[0] = 0;
         d.ctl->n_aret[1] = 0;
         d.ctl->gfree_head = 0;
@@ -1611,6 +1670,7 @@ struct cn_rx {
     int sms = 148;
     int copy_bps = 64;  // k_copy block cap per SM (CN_COPY_BLOCKS_PER_SM overrides)
     int scan_first = 1;  // launch scan/acks before the scatter (CN_SCAN_FIRST=0 reverts)
+    uint32_t small_batch = 32768;  // batches up to this many packets use 32-packet ack tiles (CN_ACK_SMALL)
     int hi_prio = 0;     // greatest stream priority: the latency-bound ack path wins SM slots
     // optional per-kernel timing with CUDA events on the launch stream
     bool profiling = false;
@@ -1657,7 +1717,7 @@ static void rx_free(cn_rx* rx) {
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
                     d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list, d.p_gbn, d.p_gbn_psn,
                     d.gbn_expected, d.gbn_nacked,
-                    d.tile_state, d.scan_state, d.plan_base, d.ctl, d.arena, d.post_key,
+                    d.tile_state, d.scan_state, d.ctl, d.arena, d.post_key,
                     d.post_val, d.post_len};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -1712,13 +1772,14 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     d.pool_cap = cfg.chunk_pool;
     d.arena_cap = cfg.carry_payload ? cfg.arena_bytes : 0;
     uint64_t B = cfg.max_batch;
-    rx->max_tiles = static_cast<uint32_t>((B + kAckTile - 1) / kAckTile);
+    rx->max_tiles = static_cast<uint32_t>((B + kAckTileMin - 1) / kAckTileMin);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&rx->sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_trim, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTrimMax * 8));
     if (const char* e = getenv("CN_COPY_BLOCKS_PER_SM")) rx->copy_bps = atoi(e) > 0 ? atoi(e) : 64;
     if (const char* e = getenv("CN_SCAN_FIRST")) rx->scan_first = atoi(e);
+    if (const char* e = getenv("CN_ACK_SMALL")) rx->small_batch = static_cast<uint32_t>(atoi(e));
     {
         int least = 0, greatest = 0;
         cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -1773,7 +1834,6 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.trim_list, kTrimMax * 4ull);
     ALLOC(d.tile_state, rx->max_tiles * 8ull);
     ALLOC(d.scan_state, (cfg.chunk_pool / kScanThreads + ngen + 2) * 8ull);
-    ALLOC(d.plan_base, ngen * 4ull);
     ALLOC(d.ctl, sizeof(RxCtl));
     if (d.carry && cfg.arena_bytes) ALLOC(d.arena, 2 * cfg.arena_bytes);  // ring + overhang
     if (d.post_mask) {
@@ -1906,7 +1966,9 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
     prof_mark(ev, s);
     if (n > 0) {
         const uint8_t* pl = static_cast<const uint8_t*>(d_payload);
-        uint32_t tiles = (n + kAckTile - 1) / kAckTile;
+        const uint32_t ack_tile = n <= rx->small_batch ? kAckTileMin : kAckTileMax;
+        rx->d.ack_tile = ack_tile;
+        uint32_t tiles = (n + ack_tile - 1) / ack_tile;
         uint32_t cw = (n + 7) / 8;  // 8 warps (packets) per copy block
         // about one packet per warp: short-lived blocks, so the block
         // scheduler hands SM slots to the high-priority ack path first and
@@ -1976,8 +2038,12 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
             lc.stream = s;
             lc.attrs = at;
             lc.numAttrs = 1;
-            CNB_CUDA(cudaLaunchKernelEx(&lc, k_acks, d, d_hdrs, n, d_acks, max_acks, d_completions,
-                                        max_completions));
+            if (ack_tile == kAckTileMin)
+                CNB_CUDA(cudaLaunchKernelEx(&lc, k_acks<kAckTileMin>, d, d_hdrs, n, d_acks, max_acks, d_completions,
+                                            max_completions));
+            else
+                CNB_CUDA(cudaLaunchKernelEx(&lc, k_acks<kAckTileMax>, d, d_hdrs, n, d_acks, max_acks, d_completions,
+                                            max_completions));
         }
         prof_mark(ev, s);
         if (copy_last) copy();

@@ -572,9 +572,10 @@ def eqds_bench(dev, receivers=4096, senders=32, events=1000, reps=3, cpu_receive
     return out
 
 
-def synth_trace(conns, size, chunk_bytes=32768, paths=256, seed=0, window=64, dev="cuda", conn_base=0):
+def synth_trace(conns, size, chunk_bytes=32768, paths=256, seed=0, window=64, dev="cuda", conn_base=0, msgs=1):
     """configs[4] traffic into one receiver: `conns` connections (sources
-    conn_base+1.., conn id = index & 0xFF), one `size`-byte message each,
+    conn_base+1.., conn id = index & 0xFF), `msgs` messages of `size` bytes
+    each (msg ids 0.., msg_seq 1.., concurrent on the connection),
     chunked and packetized as Transport::send_chunk does (DefaultPolicy),
     per-chunk paths from the S3 scheduler (P2-RTT over `paths` paths, one
     RngStream per connection), packets of all connections interleaved
@@ -590,28 +591,29 @@ def synth_trace(conns, size, chunk_bytes=32768, paths=256, seed=0, window=64, de
     lp = -(-last // MAX_PL)
     per = (nch - 1) * ppc + lp
     sch = cn.PathScheduler(conns, paths, seed + 1, base_rtt_ns=10000.0, device=dev)
-    pth = sch.select("p2_rtt", nch).cpu().numpy()                      # [conns, nch]
+    pth = sch.select("p2_rtt", nch * msgs).cpu().numpy().reshape(conns, msgs, nch)
     k = np.arange(per)
     c = np.minimum(k // ppc, nch - 1)
     sq = k - c * ppc
     clen = np.where(c == nch - 1, last, chunk_bytes)
     pl = np.minimum(MAX_PL, clen - sq * MAX_PL)
-    rec = np.zeros((conns, per), dtype=PKT_DTYPE)
-    j = np.arange(conns)[:, None]
+    rec = np.zeros((conns, msgs, per), dtype=PKT_DTYPE)
+    j = np.arange(conns)[:, None, None]
+    m = np.arange(msgs)[None, :, None]
     rec["src"] = conn_base + 1 + j
     rec["dst"] = 0
-    rec["path_id"] = pth[:, c]
-    hdr = ((j & 0xFF) << 24) | (0 << 17) | ((c & 0xFF) << 9) | ((c == nch - 1) << 8)
+    rec["path_id"] = pth[:, :, c]
+    hdr = ((j & 0xFF) << 24) | (m << 17) | ((c & 0xFF) << 9)[None, None, :] | ((c == nch - 1) << 8)[None, None, :]
     rec["hdr"] = hdr.astype(np.uint32)
-    rec["chunk_offset"] = (c * chunk_bytes)[None, :]
-    rec["chunk_len"] = clen[None, :]
-    rec["payload_len"] = pl[None, :]
-    rec["seq_in_chunk"] = sq[None, :]
-    rec["tx_time"] = k[None, :] * 10
-    rec["msg_seq"] = 1
-    rec["msg_tag"] = conn_base + j
+    rec["chunk_offset"] = (c * chunk_bytes)[None, None, :]
+    rec["chunk_len"] = clen[None, None, :]
+    rec["payload_len"] = pl[None, None, :]
+    rec["seq_in_chunk"] = sq[None, None, :]
+    rec["tx_time"] = k[None, None, :] * 10
+    rec["msg_seq"] = 1 + m
+    rec["msg_tag"] = (conn_base + j) * msgs + m
     rec["msg_len"] = size
-    out = rec.T.reshape(-1)                                            # round-robin over connections
+    out = rec.reshape(conns * msgs, per).T.reshape(-1)               # round-robin over messages
     if window > 1 and len(out) > window:
         rs = np.random.RandomState(seed)
         key = np.arange(len(out)) + rs.randint(0, window, len(out))
@@ -632,16 +634,20 @@ def sweep_bench(dev, world, rank, sizes=(4 << 10, 64 << 10, 1 << 20, 16 << 20, 2
 
     import paper_2504_17307_b200 as cn
     out = []
-    for size in sizes:
+    # small messages: a connection keeps several in flight (up to 4,096
+    # messages per receive batch), large ones one per connection
+    plan = [(s_, 1) for s_ in sizes] + [(s_, 4) for s_ in sizes if s_ <= (64 << 10)]
+    for size, mpc in plan:
         conns = max(1, min(total_conns // world, cap_bytes // size))
-        data = synth_trace(conns, size, seed=size % 9973 + rank, conn_base=rank * conns, dev=dev)
+        data = synth_trace(conns, size, seed=size % 9973 + rank, conn_base=rank * conns, dev=dev, msgs=mpc)
         n = len(data)
         hdrs = cn.to_device_records(data, dev)
         st = torch.randint(0, 256, (n * MAX_PL,), dtype=torch.uint8, device=dev)
-        nchk = conns * (-(-size // 32768))
+        nmsg = conns * mpc
+        nchk = nmsg * (-(-size // 32768))
         tr = cn.Transport(cn.TransportConfig(chunk_bytes=32768, carry_payload=True), device=dev,
-                          arena_bytes=conns * (size + 64) + (1 << 20), chunk_pool=2 * nchk + 64,
-                          max_batch=n, max_conns=2 * conns + 16, max_msgs=2 * conns + 16)
+                          arena_bytes=nmsg * (size + 512) + (1 << 20), chunk_pool=2 * nchk + 64,
+                          max_batch=n, max_conns=2 * conns + 16, max_msgs=2 * nmsg + 16)
 
         def step():
             s_ = torch.cuda.current_stream(dev)
@@ -672,10 +678,10 @@ def sweep_bench(dev, world, rank, sizes=(4 << 10, 64 << 10, 1 << 20, 16 << 20, 2
         r = cn.lib  # noqa: F841
         from paper_2504_17307_b200 import _lib as L_
         rr = L_.RxResult.from_buffer_copy(bytes(res.numpy()))
-        assert rr.status == 0 and rr.n_completions == conns, (size, rr.status, rr.n_completions)
-        out.append({"msg_bytes": size, "connections": conns * world, "packets": n * world,
+        assert rr.status == 0 and rr.n_completions == nmsg, (size, rr.status, rr.n_completions)
+        out.append({"msg_bytes": size, "connections": conns * world, "msgs_per_conn": mpc, "packets": n * world,
                     "ms_per_batch": round(ms, 4),
-                    "GBps": round(world * conns * size / (ms * 1e-3) / 1e9, 1),
+                    "GBps": round(world * nmsg * size / (ms * 1e-3) / 1e9, 1),
                     "Mpkts_per_s": round(world * n / (ms * 1e-3) / 1e6, 1)})
         del tr, g, hdrs, st
         torch.cuda.empty_cache()

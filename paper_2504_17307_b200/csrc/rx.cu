@@ -359,7 +359,11 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         if (ok && lane == lr) rslot = map_insert(m_key, rkey, &own);
         rslot = __shfl_sync(0xffffffffu, rslot, lr);
         __syncthreads();
-        if (own) m_val[rslot] = table_insert(d.rc_key, d.conn_mask, rkey, &own);
+        if (own) {
+            bool ins = false;
+            m_val[rslot] = table_insert(d.rc_key, d.conn_mask, rkey, &ins);
+            m_nch[rslot] = ins;  // a connection new this batch: completed_seq is all 0
+        }
         __syncthreads();
     }
     uint32_t rc = ok ? m_val[rslot] : kInf;
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         status |= CN_RXF_CAPACITY;
         ok = false;
     }
-    if (ok && h.msg_seq <= d.rc_done[rc * 128 + mid]) {
+    if (ok && !m_nch[rslot] && h.msg_seq <= d.rc_done[rc * 128 + mid]) {
         g = kStale;  // transport.cpp:602
         ok = false;
     }
@@ -400,6 +404,9 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                     st = CN_RXF_UNSUPPORTED;
                 const bool early_arena = !st && d.carry && !d.post_mask && d.arena_blocks;
                 const unsigned long long gi = atomicAdd(&d.ctl->gfree_head, 1ull);
+                // a new generation is touched by this batch: its touched-list
+                // slot is claimed beside the other allocations (one round trip)
+                const uint32_t tk = atomicAdd(&d.ctl->n_touched, 1u);
                 unsigned long long ph = 0, ah = 0;
                 if (!st) ph = atomicAdd(&d.ctl->pool.head, static_cast<unsigned long long>(nc));
                 if (early_arena) ah = atomicAdd(&d.ctl->arena.head, static_cast<unsigned long long>(nb));
@@ -459,7 +466,15 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 G->msg_id = mid;
                 G->deliver_t = kInf;
                 G->slot = slot;
+                G->epoch = epoch;  // first touch is this batch
+                G->lo_batch = 0;
+                G->tiles_done = 0;
+                G->cum_add = 0;
+                d.touched[tk] = gs;
                 st_release(&d.gen_val[slot], gs);
+                nch = G->nchunks;  // this thread's own values: no read back
+                cbase = G->chunk_base;
+                glen = h.msg_len;
             } else {
                 // wait for the inserter (resident, already past its CAS)
                 uint32_t spins = 0;
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 }
                 if (gs != kInf) G = &d.gen[gs];
             }
-            if (gs != kInf) {
+            if (gs != kInf && !gins) {
                 nch = G->nchunks;
                 cbase = G->chunk_base;
                 glen = G->len;

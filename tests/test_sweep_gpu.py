@@ -11,13 +11,17 @@ from oracle.records import CPL_FIELDS, ack_equal
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("conns,size", [(64, 4096), (48, 64 * 1024 + 17), (9, 1 << 20), (300, 100)])
-def test_synthetic_many_connections_match_oracle(conns, size):
+@pytest.mark.parametrize("conns,size,msgs", [(64, 4096, 1), (48, 64 * 1024 + 17, 1), (9, 1 << 20, 1),
+                                             (300, 100, 1), (256, 4096, 4), (40, 64 * 1024, 4)])
+def test_synthetic_many_connections_match_oracle(conns, size, msgs):
+    """msgs > 1: several concurrent messages per connection (the sweep's
+    small-message batches)."""
     import bench
     import paper_2504_17307_b200 as cn
-    data = bench.synth_trace(conns, size, seed=size % 97)
+    data = bench.synth_trace(conns, size, seed=size % 97, msgs=msgs)
     o_acks, o_cpls, o_arena, cnt = O.OracleRx().batch(data, O.fill_staging(data))
-    assert cnt.n_completions == conns
+    assert cnt.n_completions == conns * msgs
+    conns *= msgs
     for nsplit in (1, 3):
         tr = cn.Transport(cn.TransportConfig(chunk_bytes=32768, carry_payload=True), device="cuda",
                           arena_bytes=conns * (size + 64) + (1 << 20), chunk_pool=4 * conns * (-(-size // 32768)) + 64,

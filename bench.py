@@ -634,9 +634,10 @@ def sweep_bench(dev, world, rank, sizes=(4 << 10, 64 << 10, 1 << 20, 16 << 20, 2
 
     import paper_2504_17307_b200 as cn
     out = []
-    # small messages: a connection keeps several in flight (up to 4,096
+    # small messages: a connection keeps several in flight (up to 16,384
     # messages per receive batch), large ones one per connection
-    plan = [(s_, 1) for s_ in sizes] + [(s_, 4) for s_ in sizes if s_ <= (64 << 10)]
+    plan = [(s_, 1) for s_ in sizes] + [(s_, 4) for s_ in sizes if s_ <= (64 << 10) and len(sizes) > 3] + \
+        [(s_, 16) for s_ in sizes if s_ <= (4 << 10) and len(sizes) > 3]
     for size, mpc in plan:
         conns = max(1, min(total_conns // world, cap_bytes // size))
         data = synth_trace(conns, size, seed=size % 9973 + rank, conn_base=rank * conns, dev=dev, msgs=mpc)

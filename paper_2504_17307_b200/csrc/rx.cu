@@ -34,6 +34,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <new>
 #include <string>
 #include <vector>
@@ -65,6 +66,8 @@ struct RxCtl {
     uint32_t n_touched, epoch, tile_ticket, fin_done, status, n_copied, n_acks, n_cpls;
     uint32_t ingest_done, scan_ticket, fin_ticket, n_scan_tiles;
     uint32_t n_trim, pad_t;
+    // the per-kernel batch plan: builder ticket, release flag (= epoch)
+    uint32_t plan_ticket_scan, plan_ticket_fin, plan_ready_scan, plan_ready_fin;
     // c_first is double-buffered by batch parity: k_finalize runs beside the
     // scatter (which reads the batch's half), so it clears the OTHER half --
     // the tiles the previous batch dirtied, listed in dirty[par ^ 1]
@@ -93,6 +96,7 @@ constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 struct RxDev {
     uint32_t cb, max_pl, ppc, conn_mask, gen_mask, carry, reduce, elem, post_mask;
     uint32_t ack_tile;  // packets per k_acks tile this batch (32 or 128)
+    uint32_t plan_cap;  // touched messages per batch the scan / finalize plan holds (dynamic smem)
     unsigned long long* post_key;  // [posts] message tag (posted destinations)
     unsigned long long* post_val;  // [posts] device pointer
     unsigned long long* post_len;  // [posts] bytes
@@ -112,7 +116,7 @@ struct RxDev {
     uint32_t* pool_bits;             // [pool_cap/32] retired chunk-pool positions
     uint32_t* arena_bits;            // [arena_blocks/32] retired arena blocks
     uint64_t arena_blocks;           // arena_cap / kArenaUnit
-    unsigned long long* aret;        // [2][kPlanMax] (first block << 31) | blocks, released a batch later
+    unsigned long long* aret;        // [2][plan_cap] (first block << 31) | blocks, released a batch later
     uint32_t* c_seen;   // [pool] persistent packet bitmask (ChunkRx::pkts_seen)
     uint32_t* c_flags;  // [pool] persistent CF_*
     int64_t* c_txt;     // [pool] persistent ChunkRx::tx_time
@@ -133,6 +137,8 @@ struct RxDev {
     uint64_t* gbn_expected;   // [rconn] RecvConn::expected_psn
     uint8_t* gbn_nacked;      // [rconn] RecvConn::gap_nacked
     uint32_t* trim_list;  // [kTrimMax] trimmed headers of the batch (packet index)
+    uint32_t* plan_F;     // [plan_cap + 1] flattened chunk offset of each touched message
+    uint32_t* plan_t0;    // [tiles + 1] first message of each 256-chunk tile
     unsigned long long* tile_state;  // [ack tiles] decoupled look-back (ack order)
     unsigned long long* scan_state;  // [scan tiles] segmented look-back (prefix max)
     RxCtl* ctl;
@@ -599,45 +605,75 @@ __device__ __forceinline__ uint32_t block_scan_max(uint32_t v, uint32_t* wsum) {
 // `while (complete) ++cum`, :736-738) -- a segmented max-scan inside the
 // tile (reset at message boundaries) plus a decoupled look-back for the
 // message that continues from earlier tiles.
-constexpr uint32_t kPlanMax = 4096;  // touched messages per batch planned in smem
+constexpr uint32_t kPlanMax = 16384;  // cap of RxDev::plan_cap (touched messages per batch, planned in smem)
 
-// Every scan/finalize block plans the batch itself (no serial phase): for
-// each touched message its chunk range [lo, hi) -- hi = the chunk vector
-// size (:636-637) -- and the exclusive prefix s_F[k] of the range lengths
-// (s_F[nt] = total chunks); a tile's thread reads lo back from the message
-// state (scan: cum, finalize: lo_batch or 0).  In k_scan lo = cum and hi =
+// The batch plan, built once per kernel by the first block to arrive (the
+// others wait on a flag it releases -- it is resident by construction): for
+// each touched message k its chunk range [lo, hi) -- hi = the chunk vector
+// size (:636-637) -- flattened as the exclusive prefix F[k] of the range
+// lengths (F[nt] = total chunks), and for every 256-chunk tile t the first
+// message t0[t] that has a chunk in it.  In k_scan lo = cum and hi =
 // max(n_init, max touched chunk + 1); k_finalize reads the values k_scan
 // stored (lo_batch, n_init; a delivered message whole), so both see the
-// same flattened layout.
-__device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool scan, uint32_t* s_F,
-                               uint32_t* s_w) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint32_t carry = 0;
-    for (uint32_t k0 = 0; k0 < nt; k0 += blockDim.x) {
-        const uint32_t k = k0 + threadIdx.x;
-        uint32_t len = 0;
-        if (k < nt) {
-            const GenState* G = &d.gen[d.touched[k]];
-            uint32_t lo, hi;
-            if (scan) {
-                lo = G->cum;
-                hi = G->n_init;
-                const unsigned long long tch = G->touch;
-                if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
-            } else if (G->deliver_t != kInf) {
-                // a delivered message is retired whole: its chunk range is
-                // reset and handed back to the pool ring
-                lo = 0;
-                hi = G->nchunks;
-            } else {
-                lo = G->lo_batch;
-                hi = G->n_init;
-            }
-            len = hi > lo ? hi - lo : 0;
+// same flattened layout.  The plan lives in global memory (L1 / L2
+// resident): shared memory in these latency-bound kernels would shrink the
+// L1 of the SMs the concurrent HBM-bound scatter streams through.
+// Each planning thread owns a contiguous run of messages: three rounds of
+// independent loads and one block scan, whatever the message count.
+__device__ __forceinline__ uint32_t plan_len(const RxDev& d, uint32_t k, uint32_t epoch, bool scan) {
+    const GenState* G = &d.gen[d.touched[k]];
+    uint32_t lo, hi;
+    if (scan) {
+        lo = G->cum;
+        hi = G->n_init;
+        const unsigned long long tch = G->touch;
+        if ((tch >> 32) == epoch && static_cast<uint32_t>(tch) > hi) hi = static_cast<uint32_t>(tch);
+    } else if (G->deliver_t != kInf) {
+        // a delivered message is retired whole: its chunk range is reset and
+        // handed back to the pool ring
+        lo = 0;
+        hi = G->nchunks;
+    } else {
+        lo = G->lo_batch;
+        hi = G->n_init;
+    }
+    return hi > lo ? hi - lo : 0;
+}
+
+constexpr uint32_t kPlanSmem = 2048;  // up to this many touched messages every block plans in smem (8 KB)
+
+// Returns the total; F points at the plan (s_F when nt <= kPlanSmem -- each
+// block builds its own copy -- else the global one).
+__device__ uint32_t plan_batch(const RxDev& d, uint32_t nt, uint32_t epoch, bool scan, uint32_t* s_F,
+                               const uint32_t** F_out) {
+    __shared__ uint32_t s_role, s_w[32], s_total;
+    RxCtl* C = d.ctl;
+    uint32_t* flag = scan ? &C->plan_ready_scan : &C->plan_ready_fin;
+    const uint32_t tag = C->epoch;  // unique per batch
+    const bool small = nt <= kPlanSmem;
+    uint32_t* Fw = small ? s_F : d.plan_F;
+    *F_out = Fw;
+    if (threadIdx.x == 0) s_role = small || atomicAdd(scan ? &C->plan_ticket_scan : &C->plan_ticket_fin, 1u) == 0;
+    __syncthreads();
+    if (s_role) {
+        const uint32_t per = (nt + blockDim.x - 1) / blockDim.x;
+        const uint32_t k0 = threadIdx.x * per, k1 = min(nt, k0 + per);
+        constexpr uint32_t kReg = 16;  // up to 16 messages per thread: loads issued together, lengths kept
+        uint32_t Lr[kReg];
+        uint32_t sum = 0;
+        if (per <= kReg) {
+#pragma unroll
+            for (uint32_t j = 0; j < kReg; ++j) Lr[j] = k0 + j < k1 ? plan_len(d, k0 + j, epoch, scan) : 0u;
+#pragma unroll
+            for (uint32_t j = 0; j < kReg; ++j) sum += Lr[j];
+        } else {
+            for (uint32_t k = k0; k < k1; ++k) sum += plan_len(d, k, epoch, scan);
         }
-        uint32_t inc = len;
+        // block exclusive scan of the per-thread sums
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        uint32_t inc = sum;
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
         if (lane == 31) s_w[w] = inc;
@@ -647,22 +683,50 @@ __device__ uint32_t plan_block(const RxDev& d, uint32_t nt, uint32_t epoch, bool
             if (q < w) wpre += s_w[q];
             tot += s_w[q];
         }
-        if (k < nt) s_F[k] = carry + wpre + inc - len;
-        carry += tot;
+        uint32_t F = wpre + inc - sum;
+        auto place = [&](uint32_t k, uint32_t len) {
+            Fw[k] = F;
+            // tiles whose first chunk falls in this message's range (global plan)
+            if (!small)
+                for (uint32_t t = (F + kScanThreads - 1) / kScanThreads; len && t * kScanThreads < F + len; ++t)
+                    d.plan_t0[t] = k;
+            F += len;
+        };
+        if (per <= kReg) {
+#pragma unroll
+            for (uint32_t j = 0; j < kReg; ++j)
+                if (k0 + j < k1) place(k0 + j, Lr[j]);
+        } else {
+            for (uint32_t k = k0; k < k1; ++k) place(k, plan_len(d, k, epoch, scan));
+        }
+        if (threadIdx.x == 0) {
+            Fw[nt] = tot;
+            if (!small) d.plan_t0[(tot + kScanThreads - 1) / kScanThreads] = nt;  // sentinel
+        }
+        if (!small) __threadfence();
         __syncthreads();
+        if (threadIdx.x == 0) {
+            s_total = tot;
+            if (!small) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(tag) : "memory");
+        }
+    } else if (threadIdx.x == 0) {
+        while (ld_acquire(flag) != tag) __nanosleep(64);
+        s_total = ld_volatile_u32(&d.plan_F[nt]);
     }
-    if (threadIdx.x == 0) s_F[nt] = carry;
     __syncthreads();
-    return carry;
+    return s_total;
 }
 
-// the message holding flattened chunk f: the last k with s_F[k] <= f
-// (empty ranges share their successor's offset and are skipped)
-__device__ __forceinline__ uint32_t msg_of_flat(const uint32_t* s_F, uint32_t nt, uint32_t f) {
-    uint32_t lo = 0, hi = nt;
+// the message holding flattened chunk f of tile t: the last k with
+// F[k] <= f (within [t0[t], t0[t+1]] for the global plan; empty ranges share
+// their successor's offset and are skipped)
+__device__ __forceinline__ uint32_t msg_of_flat(const RxDev& d, const uint32_t* F, uint32_t nt, uint32_t t,
+                                                uint32_t f) {
+    const bool small = nt <= kPlanSmem;
+    uint32_t lo = small ? 0u : d.plan_t0[t], hi = small ? nt : d.plan_t0[t + 1] + 1;
     while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (s_F[mid] <= f) lo = mid; else hi = mid;
+        if (F[mid] <= f) lo = mid; else hi = mid;
     }
     return lo;
 }
@@ -708,17 +772,18 @@ __device__ __forceinline__ uint32_t block_seg_scan_max(uint32_t v, bool head, ui
 __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
     __shared__ uint32_t s_v[32], s_h[32];
     __shared__ uint32_t s_ticket, s_carry, s_k0;
-    __shared__ uint32_t s_F[kPlanMax + 1];
     const int lane = threadIdx.x & 31;
     const uint32_t epoch = d.ctl->epoch;
-    const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
+    const uint32_t nt = min(d.ctl->n_touched, d.plan_cap);
     const uint32_t ppc = d.ppc;
     const uint32_t* __restrict__ cf = first_of(d, d.ctl->par);
     uint32_t my_n = 0;             // first arrivals (n_copied) and their bytes
     unsigned long long my_b = 0;
-    const uint32_t T = plan_block(d, nt, epoch, true, s_F, s_v);
+    __shared__ uint32_t s_F[kPlanSmem + 1];
+    const uint32_t* F = nullptr;
+    const uint32_t T = plan_batch(d, nt, epoch, true, s_F, &F);
     const uint32_t tiles = (T + kScanThreads - 1) / kScanThreads;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && d.ctl->n_touched > kPlanMax)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && d.ctl->n_touched > d.plan_cap)
         atomicOr(&d.ctl->status, CN_RXF_CAPACITY);
     for (;;) {
         if (threadIdx.x == 0) s_ticket = atomicAdd(&d.ctl->scan_ticket, 1u);
@@ -731,9 +796,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
         uint32_t k = 0, c = 0, cpl = 0;
         GenState* G = nullptr;
         if (in) {
-            k = msg_of_flat(s_F, nt, f);
+            k = msg_of_flat(d, F, nt, ticket, f);
             G = &d.gen[d.touched[k]];
-            c = G->cum + (f - s_F[k]);  // cum: the batch's lower bound (finalize moves it later)
+            c = G->cum + (f - F[k]);  // cum: the batch's lower bound (finalize moves it later)
             const uint64_t e = G->chunk_base + c;
             if (!(d.c_flags[e] & CF_COMPLETE)) {
                 const uint32_t clen = chunk_len_of(d, G->len, c);
@@ -759,15 +824,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
             d.c_cpl[e] = cpl;
         }
         // segments: one per message present in the tile
-        const bool head = in && (threadIdx.x == 0 || f == s_F[k]);
+        const bool head = in && (threadIdx.x == 0 || f == F[k]);
         const uint32_t incl = block_seg_scan_max(cpl, head, s_v, s_h);
         // the message of the tile's first chunk may continue from earlier
         // tiles (it then spans back to tile F / 256): look back for its carry
         if (threadIdx.x < 32) {
             const uint32_t fl_ = (f0 + kScanThreads <= T ? f0 + kScanThreads : T) - 1;
-            const uint32_t k0 = msg_of_flat(s_F, nt, f0), kl = msg_of_flat(s_F, nt, fl_);
-            const bool cont = s_F[k0] < f0;           // first message started before this tile
-            const bool last_here = s_F[kl] >= f0;     // last message starts in this tile
+            const uint32_t k0 = msg_of_flat(d, F, nt, ticket, f0), kl = msg_of_flat(d, F, nt, ticket, fl_);
+            const bool cont = F[k0] < f0;           // first message started before this tile
+            const bool last_here = F[kl] >= f0;     // last message starts in this tile
             // the tile's last segment value: the inclusive scan at its last chunk
             const uint32_t agg = s_v[kScanThreads / 32 - 1];
             uint32_t carry = 0;
@@ -775,7 +840,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
             if (cont) {
                 if (!last_here && lane == 0) atomicExch(&d.scan_state[ticket], kFlagAgg | agg);
                 int64_t b = static_cast<int64_t>(ticket) - 1;
-                const int64_t seg0 = static_cast<int64_t>(s_F[k0] / kScanThreads);  // the message's first tile
+                const int64_t seg0 = static_cast<int64_t>(F[k0] / kScanThreads);  // the message's first tile
                 for (;;) {
                     int64_t p = b - lane;
                     unsigned long long v = p >= seg0 ? ld_volatile_u64(&d.scan_state[p]) : kFlagIncl;
@@ -808,7 +873,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
             const uint32_t carry = k == s_k0 ? s_carry : 0u;
             const uint32_t pm = incl > carry ? incl : carry;
             d.c_pmax[G->chunk_base + c] = pm;
-            if (f + 1 == s_F[k + 1]) {  // the message's last chunk of the batch range
+            if (f + 1 == F[k + 1]) {  // the message's last chunk of the batch range
                 const uint32_t hi = c + 1;
                 G->deliver_t = hi == G->nchunks ? pm : kInf;
                 G->n_init = hi;
@@ -885,7 +950,19 @@ __device__ __forceinline__ void warp_scatter(uint8_t* __restrict__ dst, const ui
             for (int k = 0; k < kCopyUnroll; ++k) {
                 uint32_t v = v0 + k * 32 + lane;
                 if (v < nv) {
+#ifdef CN_COPY_LD_NOALLOC
+                {
+                    int4 t_;
+                    asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(t_.x), "=r"(t_.y), "=r"(t_.z), "=r"(t_.w)
+                                 : "l"(s4 + v));
+                    r[k] = t_;
+                }
+#elif defined(CN_COPY_LD_CG)
+                    r[k] = __ldcg(s4 + v);
+#else
                     r[k] = __ldcs(s4 + v);
+#endif
                     if (R) a[R ? k : 0] = d4[v];
                 }
             }
@@ -1378,11 +1455,12 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     __shared__ bool last_block;
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_cnt[kScanThreads];  // per message segment of the tile: chunks now in the cum prefix
-    __shared__ uint32_t s_F[kPlanMax + 1];
-    const uint32_t nt = min(d.ctl->n_touched, kPlanMax);
+    const uint32_t nt = min(d.ctl->n_touched, d.plan_cap);
     const uint32_t ppc = d.ppc;
     const uint32_t par = d.ctl->par;
-    const uint32_t T = plan_block(d, nt, 0, false, s_F, s_w);
+    __shared__ uint32_t s_F[kPlanSmem + 1];
+    const uint32_t* F = nullptr;
+    const uint32_t T = plan_batch(d, nt, 0, false, s_F, &F);
     const uint32_t total = (T + kScanThreads - 1) / kScanThreads;
     // the previous batch's first-arrival half: its scatter has finished
     // (stream order), the next batch uses it
@@ -1421,14 +1499,14 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         GenState* G = nullptr;
         uint64_t base = 0;
         if (in) {
-            k = msg_of_flat(s_F, nt, f);
+            k = msg_of_flat(d, F, nt, ticket, f);
             G = &d.gen[d.touched[k]];
             retire = G->deliver_t != kInf;
-            c = (retire ? 0u : G->lo_batch) + (f - s_F[k]);
+            c = (retire ? 0u : G->lo_batch) + (f - F[k]);
             base = G->chunk_base;
-            head = threadIdx.x == 0 || f == s_F[k];
+            head = threadIdx.x == 0 || f == F[k];
             if (head) {  // this tile's run of the message: c_first cleared through the dirty list
-                const uint32_t end = s_F[k + 1] < f0 + kScanThreads ? s_F[k + 1] : f0 + kScanThreads;
+                const uint32_t end = F[k + 1] < f0 + kScanThreads ? F[k + 1] : f0 + kScanThreads;
                 const uint32_t j = atomicAdd(&d.ctl->n_dirty_next, 1u);
                 if (j < d.dirty_cap) dirty[j] = ((base + c) << 9) | (end - f);
             }
@@ -1476,14 +1554,14 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             done = d.c_pmax[e] != kInf;
             d.c_cpl[e] = kInf;
             d.c_pmax[e] = kInf;
-            if (done) atomicAdd(&s_cnt[s_F[k] > f0 ? s_F[k] - f0 : 0u], 1u);  // slot of the run's first chunk
+            if (done) atomicAdd(&s_cnt[F[k] > f0 ? F[k] - f0 : 0u], 1u);  // slot of the run's first chunk
         }
         __syncthreads();
         if (in && head && !retire) {
             // the message's tiles report their share of the new cum prefix;
             // the last one to report moves cum
             const uint32_t lo = G->lo_batch;
-            const uint32_t F0 = s_F[k], F1 = s_F[k + 1];
+            const uint32_t F0 = F[k], F1 = F[k + 1];
             const uint32_t ntiles = (F1 - 1) / kScanThreads - F0 / kScanThreads + 1;
             const uint32_t cnt = s_cnt[threadIdx.x];  // the head is the run's first chunk
             if (cnt) atomicAdd(&G->cum_add, cnt);
@@ -1499,7 +1577,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     // handler has run (the reference hands the buffer to on_complete and
     // frees it after, :794-803)
     {
-        const unsigned long long* al = d.aret + (par ^ 1u) * static_cast<uint64_t>(kPlanMax);
+        const unsigned long long* al = d.aret + (par ^ 1u) * static_cast<uint64_t>(d.plan_cap);
         const uint32_t na = d.ctl->n_aret[par ^ 1u];
         for (uint32_t j = blockIdx.x; j < na; j += gridDim.x) {
             const unsigned long long v = al[j];
@@ -1525,7 +1603,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             atomicMax(&d.rc_done[G->rc * 128 + G->msg_id], static_cast<unsigned long long>(G->seq));
             if (G->buf_off != ~0ull && d.carry && G->nchunks) {
                 const uint32_t j = atomicAdd(&d.ctl->n_aret[par], 1u);
-                d.aret[par * static_cast<uint64_t>(kPlanMax) + j] =
+                d.aret[par * static_cast<uint64_t>(d.plan_cap) + j] =
                     ((G->buf_off / kArenaUnit) << 31) | ((G->len + kArenaUnit - 1) / kArenaUnit);
             }
             d.gen_key[G->slot] = kTomb;
@@ -1597,6 +1675,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->n_cpls = 0;
         C->scan_ticket = 0;
         C->fin_ticket = 0;
+        C->plan_ticket_scan = 0;
+        C->plan_ticket_fin = 0;
         uint32_t ep = C->epoch + 1;
         C->epoch = ep ? ep : 1;
         C->n_dirty[par] = min(C->n_dirty_next, d.dirty_cap);
@@ -1732,7 +1812,7 @@ static void rx_free(cn_rx* rx) {
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
                     d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list, d.p_gbn, d.p_gbn_psn,
                     d.gbn_expected, d.gbn_nacked,
-                    d.tile_state, d.scan_state, d.ctl, d.arena, d.post_key,
+                    d.tile_state, d.scan_state, d.ctl, d.plan_F, d.plan_t0, d.arena, d.post_key,
                     d.post_val, d.post_len};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -1821,12 +1901,16 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     const uint64_t phys = 2 * cfg.chunk_pool;  // ring capacity + overhang
     d.first_half = phys * ppc;
     ALLOC(d.c_first, 2 * d.first_half * 4);
-    d.dirty_cap = static_cast<uint32_t>(cfg.chunk_pool / kScanThreads + kPlanMax + 1);
+    d.plan_cap = ngen < kPlanMax ? ngen : kPlanMax;
+    if (const char* e = getenv("CN_PLAN_CAP")) d.plan_cap = std::min<uint32_t>(d.plan_cap, atoi(e) > 0 ? atoi(e) : 1);
+    d.dirty_cap = static_cast<uint32_t>(cfg.chunk_pool / kScanThreads + d.plan_cap + 1);
     ALLOC(d.dirty, 2ull * d.dirty_cap * 8);
     ALLOC(d.pool_bits, (cfg.chunk_pool + 31) / 32 * 4);
     d.arena_blocks = d.arena_cap / kArenaUnit;
     if (d.arena_blocks) ALLOC(d.arena_bits, (d.arena_blocks + 31) / 32 * 4);
-    ALLOC(d.aret, 2ull * kPlanMax * 8);
+    ALLOC(d.aret, 2ull * d.plan_cap * 8);
+    ALLOC(d.plan_F, (d.plan_cap + 1ull) * 4);
+    ALLOC(d.plan_t0, (cfg.chunk_pool / kScanThreads + d.plan_cap + 4ull) * 4);
     ALLOC(d.c_seen, phys * 4);
     ALLOC(d.c_flags, phys * 4);
     ALLOC(d.c_txt, phys * 8);

@@ -392,30 +392,71 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     if (ok && lane == lg) gslot = map_insert(m_key, gkey, &gown);
     gslot = __shfl_sync(0xffffffffu, gslot, lg);
     __syncthreads();
+    // the generation's table slot; the unique inserter of a new generation
+    // allocates its state (GenState index, touched-list slot, chunk-pool
+    // range, arena range when no posted destinations exist) -- the shared
+    // counters claimed once per warp for all of its inserters
+    bool gins = false;
+    uint32_t gslot_t = kInf;
+    if (gown) gslot_t = table_insert(d.gen_key, d.gen_mask, gkey, &gins);
+    gins = gins && gslot_t != kInf;
+    uint64_t a_nc = 0, a_nb = 0;
+    uint32_t a_st = 0;
+    bool a_early = false;
+    if (gins) {
+        a_nc = (h.msg_len + d.cb - 1) / d.cb;
+        a_nb = (h.msg_len + kArenaUnit - 1) / kArenaUnit;
+        if (h.msg_len == 0 || a_nc >= (1ull << 31) || (d.reduce && (h.msg_len % d.elem))) a_st = CN_RXF_UNSUPPORTED;
+        a_early = !a_st && d.carry && !d.post_mask && d.arena_blocks;
+    }
+    unsigned long long a_gi = 0, a_ph = 0, a_ah = 0;
+    uint32_t a_tk = 0;
+    {
+        const unsigned ib = __ballot_sync(0xffffffffu, gins);
+        if (ib) {
+            const uint64_t pnc = gins && !a_st ? a_nc : 0, pnb = a_early ? a_nb : 0;
+            uint64_t inc_c = pnc, inc_b = pnb;  // inclusive warp prefix sums
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t yc = __shfl_up_sync(0xffffffffu, inc_c, o), yb = __shfl_up_sync(0xffffffffu, inc_b, o);
+                if (lane >= o) {
+                    inc_c += yc;
+                    inc_b += yb;
+                }
+            }
+            unsigned long long gi0 = 0, ph0 = 0, ah0 = 0;
+            uint32_t tk0 = 0;
+            if (lane == 31) {
+                const uint32_t cnt = __popc(ib);
+                gi0 = atomicAdd(&d.ctl->gfree_head, static_cast<unsigned long long>(cnt));
+                // a new generation is touched by this batch
+                tk0 = atomicAdd(&d.ctl->n_touched, cnt);
+                if (inc_c) ph0 = atomicAdd(&d.ctl->pool.head, static_cast<unsigned long long>(inc_c));
+                if (inc_b) ah0 = atomicAdd(&d.ctl->arena.head, static_cast<unsigned long long>(inc_b));
+            }
+            gi0 = __shfl_sync(0xffffffffu, gi0, 31);
+            tk0 = __shfl_sync(0xffffffffu, tk0, 31);
+            ph0 = __shfl_sync(0xffffffffu, ph0, 31);
+            ah0 = __shfl_sync(0xffffffffu, ah0, 31);
+            const uint32_t rank = __popc(ib & ((1u << lane) - 1));
+            a_gi = gi0 + rank;
+            a_tk = tk0 + rank;
+            a_ph = ph0 + (inc_c - pnc);
+            a_ah = ah0 + (inc_b - pnb);
+        }
+    }
     if (gown) {
         uint32_t gs = kInf, nch = 0;
         unsigned long long cbase = 0, glen = 0;
-        bool gins = false;
-        const uint32_t slot = table_insert(d.gen_key, d.gen_mask, gkey, &gins);
+        const uint32_t slot = gslot_t;
         if (slot != kInf) {
             GenState* G = nullptr;
             if (gins) {
-                // the unique inserter allocates the message state; its
-                // independent atomics (GenState index, pool range, arena
-                // range when no posted destinations exist) are issued together
-                const uint64_t nc = (h.msg_len + d.cb - 1) / d.cb;
-                const uint64_t nb = (h.msg_len + kArenaUnit - 1) / kArenaUnit;
-                uint32_t st = 0;
-                if (h.msg_len == 0 || nc >= (1ull << 31) || (d.reduce && (h.msg_len % d.elem)))
-                    st = CN_RXF_UNSUPPORTED;
-                const bool early_arena = !st && d.carry && !d.post_mask && d.arena_blocks;
-                const unsigned long long gi = atomicAdd(&d.ctl->gfree_head, 1ull);
-                // a new generation is touched by this batch: its touched-list
-                // slot is claimed beside the other allocations (one round trip)
-                const uint32_t tk = atomicAdd(&d.ctl->n_touched, 1u);
-                unsigned long long ph = 0, ah = 0;
-                if (!st) ph = atomicAdd(&d.ctl->pool.head, static_cast<unsigned long long>(nc));
-                if (early_arena) ah = atomicAdd(&d.ctl->arena.head, static_cast<unsigned long long>(nb));
+                const uint64_t nc = a_nc, nb = a_nb;
+                uint32_t st = a_st;
+                const bool early_arena = a_early;
+                const unsigned long long gi = a_gi;
+                const uint32_t tk = a_tk;
+                const unsigned long long ph = a_ph, ah = a_ah;
                 const unsigned long long ptail = ld_volatile_u64(&d.ctl->pool.tail);
                 const unsigned long long atail = early_arena ? ld_volatile_u64(&d.ctl->arena.tail) : 0;
                 // never empty: live keys <= table slots = GenStates
@@ -1596,20 +1637,40 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         }
     }
     // ---- delivered messages: completed_seq (:801) and retirement
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += gridDim.x * blockDim.x) {
-        const uint32_t g = d.touched[k];
-        GenState* G = &d.gen[g];
-        if (G->deliver_t != kInf) {
+    // (the shared counters are claimed once per warp: a batch may retire
+    // thousands of small messages)
+    const uint32_t kstride = gridDim.x * blockDim.x;
+    for (uint32_t k0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); k0 < nt; k0 += kstride) {
+        const uint32_t k = k0 + (threadIdx.x & 31);
+        const int lane = threadIdx.x & 31;
+        const unsigned lt = (1u << lane) - 1;
+        uint32_t g = 0;
+        GenState* G = nullptr;
+        bool ret = false, arel = false;
+        if (k < nt) {
+            g = d.touched[k];
+            G = &d.gen[g];
+            ret = G->deliver_t != kInf;
+            arel = ret && G->buf_off != ~0ull && d.carry && G->nchunks;
+        }
+        const unsigned rb = __ballot_sync(0xffffffffu, ret), ab = __ballot_sync(0xffffffffu, arel);
+        unsigned long long ft = 0;
+        uint32_t aj = 0;
+        if (lane == 0 && rb) {
+            ft = atomicAdd(&d.ctl->gfree_tail, static_cast<unsigned long long>(__popc(rb)));
+            atomicAdd(&d.ctl->n_tomb, static_cast<uint32_t>(__popc(rb)));
+            if (ab) aj = atomicAdd(&d.ctl->n_aret[par], static_cast<uint32_t>(__popc(ab)));
+        }
+        ft = __shfl_sync(0xffffffffu, ft, 0);
+        aj = __shfl_sync(0xffffffffu, aj, 0);
+        if (ret) {
             atomicMax(&d.rc_done[G->rc * 128 + G->msg_id], static_cast<unsigned long long>(G->seq));
-            if (G->buf_off != ~0ull && d.carry && G->nchunks) {
-                const uint32_t j = atomicAdd(&d.ctl->n_aret[par], 1u);
-                d.aret[par * static_cast<uint64_t>(d.plan_cap) + j] =
+            if (arel)
+                d.aret[par * static_cast<uint64_t>(d.plan_cap) + aj + __popc(ab & lt)] =
                     ((G->buf_off / kArenaUnit) << 31) | ((G->len + kArenaUnit - 1) / kArenaUnit);
-            }
             d.gen_key[G->slot] = kTomb;
             d.gen_val[G->slot] = kInf;
-            d.gen_free[atomicAdd(&d.ctl->gfree_tail, 1ull) & d.gen_mask] = g;
-            atomicAdd(&d.ctl->n_tomb, 1u);
+            d.gen_free[(ft + __popc(rb & lt)) & d.gen_mask] = g;
         }
     }
     __syncthreads();

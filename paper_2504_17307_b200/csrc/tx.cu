@@ -174,6 +174,22 @@ struct TxDev {
     unsigned int* status;
 };
 
+// Debug builds (make EXTRA=-DCN_TX_CHECK_UNIFORM): every value the warp
+// branches on at the handlers' decision points must be equal in all 32
+// lanes; a divergent one sets CN_TX_STATUS_INTERNAL.
+#ifdef CN_TX_CHECK_UNIFORM
+#define CN_UNIFORM(d_, v_)                                                                      \
+    do {                                                                                        \
+        int pred_;                                                                              \
+        __match_all_sync(0xffffffffu, static_cast<unsigned long long>(v_), &pred_);             \
+        if (!pred_) atomicOr((d_).status, CN_TX_STATUS_INTERNAL);                               \
+    } while (0)
+#else
+#define CN_UNIFORM(d_, v_) \
+    do {                   \
+    } while (0)
+#endif
+
 template <class T>
 __device__ __forceinline__ void wr(T& ref, T v, int lane) {  // single-writer store of warp-uniform state
     __syncwarp();
@@ -641,6 +657,7 @@ struct Tx {
         if (lane == 0) cc_on_loss(d, *cc(k, prev), now);
         __syncwarp();
         const int p = select(k, prev, m, mid, ci, d.c_att[e]);
+        CN_UNIFORM(d, p);
         const uint32_t qs = h->q_seq + 1;
         __syncwarp();
         if (lane == 0) {
@@ -903,6 +920,7 @@ __device__ void egress(Tx& x, int en, int64_t now) {
             *dp = x.txq_n(k)[p] ? (def > q ? q : def) : 0;
         }
         __syncwarp();
+        CN_UNIFORM(x.d, first);
         if (first == left) {
             wr(E.ring_pos, E.ring_pos + left, x.lane);
             break;
@@ -987,6 +1005,7 @@ __device__ void commit_chunks(Tx& x, int en, int64_t now) {
         const uint32_t sz = rem < x.d.cb ? static_cast<uint32_t>(rem) : x.d.cb;
         const uint32_t ci = m.nchunks;
         const int p = x.select(k, -1, m, mid, ci, 0);  // on_select_path (:281-287)
+        CN_UNIFORM(x.d, p);
         const uint32_t qs = h->q_seq + 1;
         __syncwarp();
         if (x.lane == 0) {
@@ -1210,6 +1229,10 @@ __device__ void handle_ack(Tx& x, int k, int64_t now, const cn_ack_rec& a) {
         }
     }
     m.base = advance_base(x, m);  // :931
+    CN_UNIFORM(x.d, m.base);
+    CN_UNIFORM(x.d, m.acked);
+    CN_UNIFORM(x.d, newly);
+    CN_UNIFORM(x.d, rcum);
     const bool done = m.chunked >= m.len && nch > 0 && m.acked == nch && !m.in_factory;
     store_msg(g, mid, m, x.lane);
     if (done) msg_finished(x, k, mid, m.engine);  // :932-934
@@ -1275,6 +1298,8 @@ __device__ void rto_fire(Tx& x, int k, int64_t now) {
                 n_exp += __popc(__ballot_sync(0xffffffffu, elig && dl <= now));
             }
         }
+    CN_UNIFORM(x.d, n_exp);
+    CN_UNIFORM(x.d, best);
     if (!have) return;  // :1131 nothing outstanding
     if (n_exp == 0) {   // :1132-1140 re-arm for the earliest deadline
         x.add_timer(k, now, best);
@@ -1540,6 +1565,8 @@ __device__ void run_deferred(Tx& x, int64_t t, bool inclusive) {
                 bid = oi;
             }
         }
+        CN_UNIFORM(x.d, bid);
+        CN_UNIFORM(x.d, bt);
         if (bid == 0xFFFFFFFFu) return;
         const uint32_t kind = bid >> 24, idx = bid & 0xFFFFFF;
         if (kind == 0) {
@@ -1596,6 +1623,7 @@ __global__ void __launch_bounds__(128, 1) k_tx_run(const TxDev* __restrict__ dp,
         const uint32_t conn = static_cast<uint32_t>((ev >> 40) & 0x3FFFFF);
         const uint64_t idx = ev & ((1ull << 40) - 1);
         const int64_t t = type == 0 ? submits[idx].t : acks[idx].aux;
+        CN_UNIFORM(d, ev);
         run_deferred(x, t, false);
         if (conn >= d.n_conns) {
             if (lane == 0) atomicOr(d.status, CN_TX_STATUS_INTERNAL);

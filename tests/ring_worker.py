@@ -16,16 +16,8 @@ def main():
     piece = int(sys.argv[4]) if len(sys.argv) > 4 else 32 << 20
     graph = len(sys.argv) > 5 and sys.argv[5] == "graph"
     local = int(os.environ["LOCAL_RANK"])
-    if os.environ.get("CN_SHARE_DEVICE") == "1":
-        # every rank on cuda:0 (a 1-GPU box): gloo for the host-side plumbing
-        # (IPC handle exchange, barriers); the data path is unchanged -- CUDA
-        # IPC peer pointers and device-side progress flags between processes
-        local = 0
-        torch.cuda.set_device(0)
-        dist.init_process_group("gloo")
-    else:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, r = dist.get_world_size(), dist.get_rank()
     from paper_2504_17307_b200.collective import RingAllreduce
     from oracle import oracle as O

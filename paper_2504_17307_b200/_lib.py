@@ -8,7 +8,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libchunknet_b200.so")
+LIB_PATH = os.environ.get("CHUNKNET_B200_LIB") or os.path.join(HERE, "libchunknet_b200.so")
 
 CN_OK = 0
 STATUS_NAMES = {-1: "CN_E_INVALID", -2: "CN_E_LOGIC", -3: "CN_E_FIELD_RANGE",

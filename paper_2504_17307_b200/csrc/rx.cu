@@ -77,6 +77,10 @@ struct RxCtl {
     // table maps keys to them, tombstones are compacted by a rebuild
     unsigned long long gfree_head, gfree_tail;
     uint32_t n_tomb, pad_g;
+    // ring tail advance (ring_scan): head snapshots the next batch's scan
+    // covers, least live offsets found, armed once a scan ran
+    unsigned long long pool_hsnap, arena_hsnap;
+    uint32_t adv_pool, adv_arena, adv_armed, pad_a;
 };
 
 enum : uint32_t { CF_INIT = 1, CF_COMPLETE = 2, CF_ECN = 4, CF_RTX = 8, CF_NACKED = 16 };
@@ -97,6 +101,7 @@ struct RxDev {
     uint32_t cb, max_pl, ppc, conn_mask, gen_mask, carry, reduce, elem, post_mask;
     uint32_t ack_tile;  // packets per k_acks tile this batch (32 or 128)
     uint32_t plan_cap;  // touched messages per batch the scan / finalize plan holds (dynamic smem)
+    uint32_t scan_blocks;  // leading k_ingest blocks that scan the rings' retirement bits
     unsigned long long* post_key;  // [posts] message tag (posted destinations)
     unsigned long long* post_val;  // [posts] device pointer
     unsigned long long* post_len;  // [posts] bytes
@@ -158,58 +163,86 @@ __device__ inline bool ring_alloc(RingCtl* r, uint64_t cap, uint64_t n, uint64_t
     return true;
 }
 
-// Whole block: advance the tail over retired positions (kAdvWords words of
-// 32 per thread per pass), clearing their bits (atomically: other blocks may
-// be retiring more).
-constexpr int kAdvWords = 8;
-__device__ void ring_advance(RingCtl* r, uint64_t cap, uint32_t* bits) {
-    __shared__ unsigned long long s_stop;
-    uint64_t t = r->tail;
-    const uint64_t h = r->head;
-    while (t < h) {
-        const uint64_t p = t % cap;
-        const uint64_t lim = (cap - p < h - t ? cap - p : h - t);
-        const uint64_t end = p + lim;
-        if (threadIdx.x == 0) s_stop = ~0ull;
-        __syncthreads();
-        const uint64_t w0 = (p >> 5) + static_cast<uint64_t>(threadIdx.x) * kAdvWords;
-        uint32_t w[kAdvWords];
-#pragma unroll
-        for (int j = 0; j < kAdvWords; ++j) w[j] = (w0 + j) << 5 < end ? bits[w0 + j] : 0u;
-#pragma unroll
-        for (int j = 0; j < kAdvWords; ++j) {
-            const uint64_t pb = (w0 + j) << 5;
-            if (pb >= end) break;
-            uint32_t inv = ~w[j];
-            if (pb < p) inv &= ~0u << (p - pb);
-            if (end - pb < 32) inv |= ~0u << (end - pb);
-            if (inv) {
-                atomicMin(&s_stop, static_cast<unsigned long long>(pb + __ffs(inv) - 1));
-                break;
-            }
-        }
-        __syncthreads();
-        const uint64_t win = (p & ~31ull) + 32ull * kAdvWords * blockDim.x;
-        uint64_t stop = s_stop;
-        if (stop == ~0ull) stop = win < end ? win : end;
-        if (stop > end) stop = end;
-#pragma unroll
-        for (int j = 0; j < kAdvWords; ++j) {
-            const uint64_t pb = (w0 + j) << 5;
-            if (pb < stop && pb + 32 > p) {  // clear [max(p, pb), min(stop, pb + 32))
-                const uint64_t a = pb > p ? pb : p, b = pb + 32 < stop ? pb + 32 : stop;
-                const uint32_t m = (b - a == 32 ? ~0u : ((1u << (b - a)) - 1)) << (a - pb);
-                atomicAnd(&bits[w0 + j], ~m);
-            }
-        }
-        __syncthreads();
-        t += stop - p;
-        if (stop < end && stop < win) break;  // a live range
-        if (stop == p) break;
-    }
-    if (threadIdx.x == 0) r->tail = t;
-    __syncthreads();
+// Lap-parity retirement bits.  Ring position p (monotonic) lies in lap
+// p / cap and is retired in that lap iff its bit equals (lap + 1) & 1: a
+// release toggles the bit (every position is allocated and released exactly
+// once per lap), so bits are never cleared and the tail advance is a
+// read-only scan any number of blocks share.  Returns, per warp, the least
+// offset from the tail of a live position in [tail, hsnap) into *out
+// (atomicMin; untouched if all retired).  Spare k_ingest blocks run it
+// beside the packet blocks: they see every release of earlier batches, the
+// tail moves in k_finalize -- off the critical path.
+__device__ __forceinline__ uint32_t span_mask(uint32_t a, uint32_t b) {  // bits [a, b), 0 <= a < b <= 32
+    return (b == 32 ? ~0u : (1u << b) - 1u) & (~0u << a);
 }
+__device__ void ring_scan(const RingCtl* r, unsigned long long hsnap, uint64_t cap, const uint32_t* bits,
+                          uint32_t* out, uint32_t worker, uint32_t workers) {
+    const uint64_t t = ld_volatile_u64(&r->tail);
+    const uint64_t n = hsnap > t ? hsnap - t : 0;
+    uint32_t best = ~0u;
+    if (n) {
+        const uint64_t tq = t % cap, L0 = t / cap;
+        const uint32_t eh = ((L0 + 1) & 1) ? ~0u : 0u, el = ~eh;  // retired values of laps L0, L0 + 1
+        const uint64_t nw = (cap + 31) >> 5;
+        for (uint64_t w = worker; w < nw; w += workers) {
+            const uint64_t q0 = w << 5;
+            const uint32_t lim = cap - q0 < 32 ? static_cast<uint32_t>(cap - q0) : 32u;
+            uint32_t hi = 0, lo = 0;  // valid bits of lap L0 (q >= tq) and of lap L0 + 1 (q < tq)
+            {
+                const uint64_t a = q0 > tq ? q0 : tq, b0 = q0 + lim, b1 = tq + n;
+                const uint64_t b = b0 < b1 ? b0 : b1;
+                if (a < b) hi = span_mask(static_cast<uint32_t>(a - q0), static_cast<uint32_t>(b - q0));
+            }
+            if (n > cap - tq) {
+                uint64_t b = q0 + lim;
+                if (b > tq) b = tq;
+                if (b > n - (cap - tq)) b = n - (cap - tq);
+                if (q0 < b) lo = span_mask(0, static_cast<uint32_t>(b - q0));
+            }
+            if (!(hi | lo)) continue;
+            const uint32_t v = bits[w];
+            const uint32_t lh = (v ^ eh) & hi, ll = (v ^ el) & lo;  // live positions
+            uint64_t off = ~0ull;
+            if (lh) off = q0 + __ffs(lh) - 1 - tq;
+            else if (ll) off = cap - tq + q0 + __ffs(ll) - 1;
+            if (off < best) best = static_cast<uint32_t>(off);
+        }
+    }
+    best = __reduce_min_sync(0xffffffffu, best);
+    if ((threadIdx.x & 31) == 0 && best != ~0u) atomicMin(out, best);
+}
+// k_finalize's last block: the tail moves over the retired prefix
+__device__ __forceinline__ void ring_move_tail(RingCtl* r, unsigned long long hsnap, uint32_t off) {
+    const uint64_t n = hsnap > r->tail ? hsnap - r->tail : 0;
+    r->tail += off < n ? off : n;
+}
+
+// Debug builds (make EXTRA=-DCN_RX_TIMING): %globaltimer marks at phase
+// boundaries of the receive kernels (min over blocks for starts, max for
+// ends), read and cleared by cn_rx_debug_timing (tools/, not the product).
+#ifdef CN_RX_TIMING
+__device__ unsigned long long g_tm[64];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TM_END(slot_)                                         \
+    do {                                                      \
+        if (threadIdx.x == 0) atomicMax(&g_tm[slot_], gtime()); \
+    } while (0)
+#define TM_START(slot_)                                       \
+    do {                                                      \
+        if (threadIdx.x == 0) atomicMin(&g_tm[slot_], gtime()); \
+    } while (0)
+#else
+#define TM_END(slot_) \
+    do {              \
+    } while (0)
+#define TM_START(slot_) \
+    do {                \
+    } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t* first_of(const RxDev& d, uint32_t par) {
     return d.c_first + (par ? d.first_half : 0);
@@ -323,8 +356,19 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     __shared__ unsigned long long m_cbase[kIngMap], m_glen[kIngMap];
     __shared__ uint32_t m_val[kIngMap], m_nch[kIngMap], m_touch[kIngMap];
     __shared__ uint32_t s_status;
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    TM_START(10);
+    if (blockIdx.x < d.scan_blocks) {  // the first blocks scan the rings (ring_scan)
+        const uint32_t worker = blockIdx.x * kIngestThreads + threadIdx.x;
+        const uint32_t workers = d.scan_blocks * kIngestThreads;
+        RxCtl* C = d.ctl;
+        ring_scan(&C->pool, C->pool_hsnap, d.pool_cap, d.pool_bits, &C->adv_pool, worker, workers);
+        if (d.arena_blocks)
+            ring_scan(&C->arena, C->arena_hsnap, d.arena_blocks, d.arena_bits, &C->adv_arena, worker, workers);
+        if (worker == 0) C->adv_armed = 1;
+        return;
+    }
+    const uint32_t i = (blockIdx.x - d.scan_blocks) * blockDim.x + threadIdx.x;
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t par = d.ctl->par;
     const uint32_t tiles = (n + d.ack_tile - 1) / d.ack_tile;
@@ -381,6 +425,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         g = kStale;  // transport.cpp:602
         ok = false;
     }
+    TM_END(11);
     // ---- message generation (rconn, msg_seq)
     for (int k = threadIdx.x; k < kIngMap; k += kIngestThreads) m_key[k] = kMapEmpty;
     __syncthreads();
@@ -558,6 +603,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         m_glen[gslot] = glen;
     }
     __syncthreads();
+    TM_END(12);
     const uint32_t gs = ok ? m_val[gslot] : kInf;
     if (ok && gs != kInf) {
         const uint32_t nch = m_nch[gslot];
@@ -606,6 +652,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     if (gown && m_val[gslot] != kInf && m_touch[gslot])
         atomicMax(&d.gen[m_val[gslot]].touch, (static_cast<unsigned long long>(epoch) << 32) | m_touch[gslot]);
     if (threadIdx.x == 0 && s_status) atomicOr(&d.ctl->status, s_status);
+    TM_END(13);
 }
 
 
@@ -817,6 +864,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t nt = min(d.ctl->n_touched, d.plan_cap);
     const uint32_t ppc = d.ppc;
+    TM_START(20);
     const uint32_t* __restrict__ cf = first_of(d, d.ctl->par);
     uint32_t my_n = 0;             // first arrivals (n_copied) and their bytes
     unsigned long long my_b = 0;
@@ -928,6 +976,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
         atomicAdd(&d.ctl->n_copied, my_n);
         atomicAdd(&d.ctl->bytes_copied, my_b);
     }
+    TM_END(21);
 }
 
 
@@ -1058,6 +1107,7 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
                                               const uint8_t* __restrict__ payload, uint64_t stride,
                                               uint32_t n) {
     const int lane = threadIdx.x & 31;
+    TM_START(24);
     const uint32_t* __restrict__ cf = first_of(d, d.ctl->copy_par);
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
@@ -1079,6 +1129,7 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
             warp_scatter<R>(G->buf + moff, src, len, lane);
         }
     }
+    TM_END(25);
 }
 
 // What the reference does with packet i (handle_data's branches).  Every
@@ -1356,6 +1407,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
     __shared__ uint32_t s_tile, s_base_a, s_base_c;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
+    TM_START(22);
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&d.ctl->tile_ticket, 1u);
         __syncthreads();
@@ -1482,6 +1534,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
         }
         __syncthreads();  // shared lists are reused by the next tile
     }
+    TM_END(23);
 }
 
 // ---------------------------------------------------------------- finalize
@@ -1503,6 +1556,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     const uint32_t* F = nullptr;
     const uint32_t T = plan_batch(d, nt, 0, false, s_F, &F);
     const uint32_t total = (T + kScanThreads - 1) / kScanThreads;
+    TM_START(0);
     // the previous batch's first-arrival half: its scatter has finished
     // (stream order), the next batch uses it
     {
@@ -1517,14 +1571,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             }
         }
     }
+    TM_END(1);
     unsigned long long* dirty = d.dirty + par * static_cast<uint64_t>(d.dirty_cap);
-    // one block moves the rings' tails over what earlier batches retired
-    // while the others fold (this batch's retirements are seen next batch):
-    // off the kernel's serial tail
-    if (blockIdx.x == gridDim.x - 1) {
-        ring_advance(&d.ctl->pool, d.pool_cap, d.pool_bits);
-        if (d.arena_blocks) ring_advance(&d.ctl->arena, d.arena_blocks, d.arena_bits);
-    }
     for (;;) {
         if (threadIdx.x == 0) s_ticket = atomicAdd(&d.ctl->fin_ticket, 1u);
         s_cnt[threadIdx.x] = 0;
@@ -1567,7 +1615,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             d.c_last[e] = 0;
             d.c_newfl[e] = 0;
             const uint64_t rp = e >= d.pool_cap ? e - d.pool_cap : e;  // ring position
-            atomicOr(&d.pool_bits[rp >> 5], 1u << (rp & 31));
+            atomicXor(&d.pool_bits[rp >> 5], 1u << (rp & 31));  // lap-parity release
         } else if (in) {
             const uint64_t e = base + c;
             uint32_t fl = d.c_flags[e];
@@ -1614,6 +1662,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         }
         __syncthreads();
     }
+    TM_END(4);
     // ---- arena blocks of the previous batch's deliveries: the completion
     // handler has run (the reference hands the buffer to on_complete and
     // frees it after, :794-803)
@@ -1631,11 +1680,12 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
                 for (uint64_t w = (a >> 5) + threadIdx.x; (w << 5) < end; w += blockDim.x) {
                     const uint64_t lo_ = (w << 5) > a ? (w << 5) : a, hi_ = (w << 5) + 32 < end ? (w << 5) + 32 : end;
                     const uint32_t m = (hi_ - lo_ == 32 ? ~0u : ((1u << (hi_ - lo_)) - 1)) << (lo_ - (w << 5));
-                    atomicOr(&d.arena_bits[w], m);
+                    atomicXor(&d.arena_bits[w], m);  // lap-parity release
                 }
             }
         }
     }
+    TM_END(5);
     // ---- delivered messages: completed_seq (:801) and retirement
     // (the shared counters are claimed once per warp: a batch may retire
     // thousands of small messages)
@@ -1674,6 +1724,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         }
     }
     __syncthreads();
+    TM_END(6);
     // ---- batch epilogue (last block)
     if (threadIdx.x == 0) {
         __threadfence();
@@ -1747,7 +1798,19 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->par = par ^ 1u;
         // physical extent used since the last reset (ranges overhang cap once the ring laps)
         C->pool_snap = C->pool.head < d.pool_cap ? C->pool.head : 2 * d.pool_cap;
+        // the rings' tails over what the batch's ring scan found retired
+        // (releases of earlier batches), and the next scan's extent
+        if (C->adv_armed) {
+            ring_move_tail(&C->pool, C->pool_hsnap, C->adv_pool);
+            ring_move_tail(&C->arena, C->arena_hsnap, C->adv_arena);
+        }
+        C->adv_pool = ~0u;
+        C->adv_arena = ~0u;
+        C->adv_armed = 0;
+        C->pool_hsnap = C->pool.head;
+        C->arena_hsnap = C->arena.head;
     }
+    TM_END(7);
 }
 
 // -------------------------------------------------------------------- reset
@@ -1803,6 +1866,9 @@ __global__ void k_reset(RxDev d, int full) {
         d.ctl->gfree_head = 0;
         d.ctl->gfree_tail = ngen;
         d.ctl->n_tomb = 0;
+        d.ctl->pool_hsnap = d.ctl->arena_hsnap = 0;
+        d.ctl->adv_pool = d.ctl->adv_arena = ~0u;
+        d.ctl->adv_armed = 0;
     }
 }
 
@@ -1968,6 +2034,17 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.dirty, 2ull * d.dirty_cap * 8);
     ALLOC(d.pool_bits, (cfg.chunk_pool + 31) / 32 * 4);
     d.arena_blocks = d.arena_cap / kArenaUnit;
+    if (d.pool_cap >= (1ull << 32) || d.arena_blocks >= (1ull << 32)) {  // ring offsets are 32-bit
+        rx_free(rx);
+        delete rx;
+        set_error("cn_rx_create: chunk_pool and arena_bytes / 512 must be < 2^32");
+        return CN_E_INVALID;
+    }
+    {  // one retirement-bit word per scan thread, both rings
+        const uint64_t words = std::max<uint64_t>((d.pool_cap + 31) / 32, (d.arena_blocks + 31) / 32);
+        const uint64_t b = (words + kIngestThreads - 1) / kIngestThreads;
+        d.scan_blocks = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(b, 1), 2ull * rx->sms));
+    }
     if (d.arena_blocks) ALLOC(d.arena_bits, (d.arena_blocks + 31) / 32 * 4);
     ALLOC(d.aret, 2ull * d.plan_cap * 8);
     ALLOC(d.plan_F, (d.plan_cap + 1ull) * 4);
@@ -2136,7 +2213,8 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         // pin half the register file for its whole duration)
         uint32_t cmax = static_cast<uint32_t>(rx->sms * rx->copy_bps);
         if (d.ordered) k_gbn<<<4, 256, 0, s>>>(d, d_hdrs, n);  // the go-back-N filter first
-        k_ingest<<<(n + kIngestThreads - 1) / kIngestThreads, kIngestThreads, 0, s>>>(d, d_hdrs, n);
+        k_ingest<<<d.scan_blocks + (n + kIngestThreads - 1) / kIngestThreads, kIngestThreads, 0, s>>>(d, d_hdrs,
+                                                                                                       n);
         prof_mark(ev, s);
         // fork: the HBM-bound scatter runs beside the latency-bound ack path
         cudaStream_t cs = ev ? s : rx->side;
@@ -2295,6 +2373,20 @@ extern "C" int cn_rx_profile(cn_rx* rx, double* ms, int max, uint64_t* batches, 
     }
     return kRxKernels;
 }
+
+#ifdef CN_RX_TIMING
+// debug builds only: the phase marks (ns, %globaltimer), then re-armed
+extern "C" int cn_rx_debug_timing(unsigned long long* out, int n) {
+    unsigned long long h[64];
+    CNB_CUDA(cudaMemcpyFromSymbol(h, g_tm, sizeof h));
+    for (int k = 0; k < n && k < 64; ++k) out[k] = h[k];
+    const unsigned long long mins[] = {0, 10, 20, 22, 24};
+    for (int k = 0; k < 64; ++k) h[k] = 0;
+    for (unsigned long long k : mins) h[k] = ~0ull;
+    CNB_CUDA(cudaMemcpyToSymbol(g_tm, h, sizeof h));
+    return CN_OK;
+}
+#endif
 
 extern "C" const char* cn_rx_kernel_name(int k) {
     return (k >= 0 && k < kRxKernels) ? kRxKernelNames[k] : "";

@@ -1,7 +1,8 @@
 """Profiling helper (not a test): GPU timeline of the receive-path graph
 (bench.py's cfg2_32k x K workload) from CUPTI kernel records (torch.profiler),
 to see launch gaps and stream overlap.  Usage:
-    python tests/rx_timeline_tool.py [K] [steps]"""
+    python tests/rx_timeline_tool.py [K] [steps]
+STEADY=1: no reset between steps, msg_seq += 1 per step (bench.steady_bench)."""
 import os
 import sys
 
@@ -36,9 +37,20 @@ def main():
     tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
                       arena_bytes=K * (msg_len + (1 << 20)), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
                       max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8))
+    steady = os.environ.get("STEADY") == "1"
+    if steady:
+        from paper_2504_17307_b200.records import PKT_DTYPE
+        seq_col = hdrs.view(n, 64).view(torch.int64)[:, PKT_DTYPE.fields["msg_seq"][1] // 8]
+        tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
+                          arena_bytes=3 * K * (msg_len + (1 << 20)), chunk_pool=3 * K * ((msg_len + cb - 1) // cb),
+                          max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8))
+
     def step():
         s = torch.cuda.current_stream(dev)
-        tr.reset(s)
+        if steady:
+            seq_col.add_(1)
+        else:
+            tr.reset(s)
         tr.rx_batch_async(hdrs, st, bench.MAX_PL, s)
 
     step()
@@ -49,6 +61,12 @@ def main():
     for _ in range(5):
         g.replay()
     torch.cuda.synchronize()
+    if os.environ.get("NOPROF") == "1":  # for ncu: plain replays, no CUPTI of our own
+        for _ in range(steps):
+            g.replay()
+        torch.cuda.synchronize()
+        print(f"ok: {steps} replays")
+        return
     from torch.profiler import ProfilerActivity, profile
     eager = os.environ.get("EAGER") == "1"
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -64,7 +82,7 @@ def main():
     prev_reset = None
     for a, b, nm in rows:
         short = nm.split("(")[0].replace("void ", "").replace("cnb::", "")[:28]
-        if "k_reset" in short:
+        if ("k_reset" in short) or (steady and "elementwise" in short):
             if prev_reset is not None:
                 print(f"--- step {(a - prev_reset):.1f} us")
             prev_reset = a

@@ -1,0 +1,61 @@
+"""Profiling helper (not a test): phase marks inside the receive kernels of a
+CN_RX_TIMING build (make EXTRA=-DCN_RX_TIMING; CHUNKNET_B200_LIB=<that .so>),
+steady-state headline batches (msg_seq + 1 per step, no reset), eager.
+    python tools/rx_phase_tool.py [K] [steps]"""
+import ctypes
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+NAMES = {0: "fin start", 1: "fin dirty-clear", 2: "fin adv pool", 3: "fin adv arena", 4: "fin tiles",
+         5: "fin arena release", 6: "fin retire", 7: "fin end", 10: "ing start", 11: "ing conn", 12: "ing gen",
+         13: "ing end", 20: "scan start", 21: "scan end", 22: "acks start", 23: "acks end", 24: "copy start",
+         25: "copy end"}
+
+
+def main():
+    K = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    import bench
+    import paper_2504_17307_b200 as cn
+    from paper_2504_17307_b200 import _lib
+    from paper_2504_17307_b200.records import PKT_DTYPE
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    if os.environ.get("SYNTH"):
+        c_, b_ = (int(v) for v in os.environ["SYNTH"].split("x"))
+        data, cb, msg_len, K = bench.synth_trace(c_, b_, seed=1), 32768, b_, c_
+    else:
+        data, meta, _ = bench.load_trace("cfg2_32k")
+        data = bench.interleave(data, K)
+        cb, msg_len = meta["chunk_bytes"], int(data["msg_len"][0])
+    n = len(data)
+    hdrs = cn.to_device_records(data, dev)
+    seq_col = hdrs.view(n, 64).view(torch.int64)[:, PKT_DTYPE.fields["msg_seq"][1] // 8]
+    st = torch.randint(0, 256, (n * bench.MAX_PL,), dtype=torch.uint8, device=dev)
+    tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
+                      arena_bytes=3 * K * (msg_len + (1 << 20)), chunk_pool=3 * K * ((msg_len + cb - 1) // cb),
+                      max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8))
+    lib = _lib.lib()
+    fn = lib.cn_rx_debug_timing
+    fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+    buf = (ctypes.c_ulonglong * 64)()
+    s = torch.cuda.current_stream(dev)
+    fn(buf, 64)
+    for k in range(steps):
+        seq_col.add_(1)
+        torch.cuda.synchronize()
+        fn(buf, 64)
+        tr.rx_batch_async(hdrs, st, bench.MAX_PL, s)
+        torch.cuda.synchronize()
+        fn(buf, 64)
+        t0 = buf[10]
+        marks = sorted((buf[j] - t0, NAMES[j]) for j in NAMES if 0 < buf[j] < (1 << 63))
+        print(f"--- step {k}: " + "  ".join(f"{nm} {v / 1e3:.1f}" for v, nm in marks))
+
+
+if __name__ == "__main__":
+    main()

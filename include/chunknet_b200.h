@@ -169,6 +169,17 @@ typedef struct cn_rx_config {
                                 go-back-N receive filter (transport.cpp:690-717)
                                 runs first; batches then come with conn_psn
                                 (cn_rx_batch_psn) */
+    int32_t pipeline;        /* 0: cn_rx_batch completes (in stream order) with
+                                acks, completions AND payload final.  1:
+                                pipelined receiver -- the payload scatter of
+                                batch k runs on beside batch k+1's ingest and
+                                ack path and is joined into the caller's
+                                stream at the end of batch k+1 (an empty batch
+                                or cn_rx_flush joins it at once).  Acks and
+                                completion records of batch k are final when
+                                batch k returns; its message bytes when batch
+                                k+1 returns.  Inputs of batch k (headers,
+                                payload) must stay valid until then. */
 } cn_rx_config;
 
 /* Reduce modes of the payload scatter: dst = dst + payload elementwise,
@@ -186,6 +197,9 @@ int cn_rx_create(const cn_rx_config* cfg, cn_rx** out);
 void cn_rx_destroy(cn_rx* rx);
 /* Forget every connection and message (fresh Transport receive state). */
 int cn_rx_reset(cn_rx* rx, void* stream);
+/* Pipelined receivers: joins the outstanding payload scatter into `stream`
+ * (after it, every completed message's bytes are final).  No-op otherwise. */
+int cn_rx_flush(cn_rx* rx, void* stream);
 
 /* Batch result counters, written by the device (d_result). */
 typedef struct cn_rx_result {

@@ -135,6 +135,8 @@ class RxTransport {
     void set_on_complete(CompleteFn fn) { on_complete_ = std::move(fn); }
     const Stats& stats() const { return stats_; }
     void reset(cudaStream_t s = nullptr) { check(cn_rx_reset(rx_, s), "cn_rx_reset"); }
+    // pipelined receivers: the outstanding payload scatter joins `s`
+    void flush(cudaStream_t s = nullptr) { check(cn_rx_flush(rx_, s), "cn_rx_flush"); }
     void post(uint64_t tag, void* d_buf, uint64_t len, cudaStream_t s = nullptr) {
         check(cn_rx_post(rx_, tag, d_buf, len, s), "cn_rx_post");
     }

@@ -34,7 +34,7 @@ class RxConfig(ctypes.Structure):
                 ("chunk_pool", ctypes.c_uint64), ("arena_bytes", ctypes.c_uint64),
                 ("max_batch", ctypes.c_uint32), ("carry_payload", ctypes.c_int32),
                 ("reduce_op", ctypes.c_int32), ("max_posts", ctypes.c_uint32),
-                ("ordered", ctypes.c_int32)]
+                ("ordered", ctypes.c_int32), ("pipeline", ctypes.c_int32)]
 
 
 class PacketizeArgs(ctypes.Structure):
@@ -111,6 +111,7 @@ def lib():
     L.cn_rx_destroy.argtypes = [vp]
     L.cn_rx_destroy.restype = None
     L.cn_rx_reset.argtypes = [vp, vp]
+    L.cn_rx_flush.argtypes = [vp, vp]
     L.cn_rx_batch.argtypes = [vp, vp, vp, u64, u32, vp, u32, vp, u32, vp, vp]
     L.cn_rx_batch_psn.argtypes = [vp, vp, vp, vp, u64, u32, vp, u32, vp, u32, vp, vp]
     L.cn_rx_post.argtypes = [vp, u64, vp, u64, vp]

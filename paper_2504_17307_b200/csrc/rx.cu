@@ -40,6 +40,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace cnb {
 
@@ -68,11 +69,17 @@ struct RxCtl {
     uint32_t n_trim, pad_t;
     // the per-kernel batch plan: builder ticket, release flag (= epoch)
     uint32_t plan_ticket_scan, plan_ticket_fin, plan_ready_scan, plan_ready_fin;
-    // c_first is double-buffered by batch parity: k_finalize runs beside the
-    // scatter (which reads the batch's half), so it clears the OTHER half --
-    // the tiles the previous batch dirtied, listed in dirty[par ^ 1]
-    uint32_t par, copy_par, n_dirty[2], n_dirty_next, pad_d;
-    uint32_t n_aret[2];  // arena ranges of messages delivered in the batch of that parity
+    // c_first and the scatter's per-packet descriptors come in three parts,
+    // batch k using part par = k mod 3: the scatter of batch k may still run
+    // while batch k + 1's ack path does (pipelined receivers), so
+    // k_finalize(k) clears the part of batch k - 2 -- the tiles it dirtied,
+    // listed in dirty[(par + 1) % 3] -- for batch k + 1
+    uint32_t par, n_dirty[3], n_dirty_next;
+    uint32_t n_aret[3];  // arena ranges of messages delivered in the batch of that part
+    // the scatter learns its batch's part through a queue k_ingest pushes
+    // (graph replays fix kernel arguments): cq[cq_out & 3], popped by the
+    // last block of each k_copy
+    uint32_t cq[4], cq_in, cq_out, cq_done, pad_q;
     // message states: a free ring of GenState indices; the (rconn, msg_seq)
     // table maps keys to them, tombstones are compacted by a rebuild
     unsigned long long gfree_head, gfree_tail;
@@ -102,6 +109,7 @@ struct RxDev {
     uint32_t ack_tile;  // packets per k_acks tile this batch (32 or 128)
     uint32_t plan_cap;  // touched messages per batch the scan / finalize plan holds (dynamic smem)
     uint32_t scan_blocks;  // leading k_ingest blocks that scan the rings' retirement bits
+    uint32_t max_batch;
     unsigned long long* post_key;  // [posts] message tag (posted destinations)
     unsigned long long* post_val;  // [posts] device pointer
     unsigned long long* post_len;  // [posts] bytes
@@ -115,13 +123,13 @@ struct RxDev {
     GenState* gen;
     uint32_t* touched;
     uint32_t* c_first;  // [2][pool*ppc] batch scratch (first arrival), half = batch parity
-    uint64_t first_half;             // pool*ppc
-    unsigned long long* dirty;       // [2][dirty_cap] finalize tiles: (first chunk << 9) | count
+    uint64_t first_part;             // pool*ppc
+    unsigned long long* dirty;       // [3][dirty_cap] finalize tiles: (first chunk << 9) | count
     uint32_t dirty_cap;
     uint32_t* pool_bits;             // [pool_cap/32] retired chunk-pool positions
     uint32_t* arena_bits;            // [arena_blocks/32] retired arena blocks
     uint64_t arena_blocks;           // arena_cap / kArenaUnit
-    unsigned long long* aret;        // [2][plan_cap] (first block << 31) | blocks, released a batch later
+    unsigned long long* aret;        // [3][plan_cap] (first block << 31) | blocks, released a batch later
     uint32_t* c_seen;   // [pool] persistent packet bitmask (ChunkRx::pkts_seen)
     uint32_t* c_flags;  // [pool] persistent CF_*
     int64_t* c_txt;     // [pool] persistent ChunkRx::tx_time
@@ -133,6 +141,8 @@ struct RxDev {
     uint32_t* c_last;   // [pool] batch scratch: last new packet time
     uint32_t* c_newfl;  // [pool] batch scratch: ECN/RTX of new packets
     uint32_t* p_gen;    // [batch]
+    unsigned long long* p_dst;  // [3][batch] scatter destination of a candidate first arrival, 0 = none
+    uint32_t* p_fi;             // [3][batch] its c_first index (chunk entry * ppc + seq)
     uint8_t* p_nack;    // [batch] trimmed header that emits a NACK
     // ordered reliability (go-back-N receive filter)
     uint32_t ordered;
@@ -235,7 +245,16 @@ __device__ __forceinline__ unsigned long long gtime() {
     do {                                                      \
         if (threadIdx.x == 0) atomicMin(&g_tm[slot_], gtime()); \
     } while (0)
+constexpr int kTileTm = 8192;
+__device__ unsigned long long g_tile_tm[4][kTileTm];  // k_acks per tile: start, decided, built, written
+#define TM_TILE(k_, tile_)                                                   \
+    do {                                                                     \
+        if (threadIdx.x == 0 && (tile_) < kTileTm) g_tile_tm[k_][tile_] = gtime(); \
+    } while (0)
 #else
+#define TM_TILE(k_, tile_) \
+    do {                   \
+    } while (0)
 #define TM_END(slot_) \
     do {              \
     } while (0)
@@ -245,7 +264,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 __device__ __forceinline__ uint32_t* first_of(const RxDev& d, uint32_t par) {
-    return d.c_first + (par ? d.first_half : 0);
+    return d.c_first + par * d.first_part;
 }
 
 __device__ __forceinline__ uint32_t chunk_len_of(const RxDev& d, uint64_t len, uint64_t c) {
@@ -353,7 +372,7 @@ __device__ __forceinline__ uint32_t map_insert(unsigned long long* keys, uint64_
 __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                                            uint32_t n) {
     __shared__ unsigned long long m_key[kIngMap];
-    __shared__ unsigned long long m_cbase[kIngMap], m_glen[kIngMap];
+    __shared__ unsigned long long m_cbase[kIngMap], m_glen[kIngMap], m_buf[kIngMap];
     __shared__ uint32_t m_val[kIngMap], m_nch[kIngMap], m_touch[kIngMap];
     __shared__ uint32_t s_status;
     const int lane = threadIdx.x & 31;
@@ -373,7 +392,11 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     const uint32_t par = d.ctl->par;
     const uint32_t tiles = (n + d.ack_tile - 1) / d.ack_tile;
     if (i < tiles) d.tile_state[i] = 0;
-    if (i == 0) d.ctl->copy_par = par;  // k_copy's half (k_finalize flips par beside it)
+    if (i == 0 && d.carry) {  // the scatter of this batch reads part par
+        RxCtl* C = d.ctl;
+        C->cq[C->cq_in & 3] = par;
+        C->cq_in += 1;
+    }
     for (int k = threadIdx.x; k < kIngMap; k += kIngestThreads) {
         m_key[k] = kMapEmpty;
         m_touch[k] = 0;
@@ -382,6 +405,8 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     uint32_t status = 0;
     uint32_t g = kErr;
     uint32_t touch = 0;
+    unsigned long long cdst = 0;  // scatter descriptor (0: nothing to copy)
+    uint32_t cfi = 0;
     cn_pkt_hdr h;
     bool ok = i < n;
     if (ok && d.ordered && d.p_gbn[i]) ok = false;  // dropped by the go-back-N filter
@@ -491,7 +516,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     }
     if (gown) {
         uint32_t gs = kInf, nch = 0;
-        unsigned long long cbase = 0, glen = 0;
+        unsigned long long cbase = 0, glen = 0, gbuf = 0;
         const uint32_t slot = gslot_t;
         if (slot != kInf) {
             GenState* G = nullptr;
@@ -567,6 +592,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 nch = G->nchunks;  // this thread's own values: no read back
                 cbase = G->chunk_base;
                 glen = h.msg_len;
+                gbuf = reinterpret_cast<unsigned long long>(buf);
             } else {
                 // wait for the inserter (resident, already past its CAS)
                 uint32_t spins = 0;
@@ -583,6 +609,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 nch = G->nchunks;
                 cbase = G->chunk_base;
                 glen = G->len;
+                gbuf = reinterpret_cast<unsigned long long>(G->buf);
                 // plain read first: only the first block of the batch pays the atomic
                 if (ld_volatile_u32(&G->epoch) != epoch && atomicExch(&G->epoch, epoch) != epoch) {
                     // first touch this batch: freeze the batch's lower bound
@@ -601,6 +628,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         m_nch[gslot] = nch;
         m_cbase[gslot] = cbase;
         m_glen[gslot] = glen;
+        m_buf[gslot] = gbuf;
     }
     __syncthreads();
     TM_END(12);
@@ -632,7 +660,13 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 if (k < kTrimMax) d.trim_list[k] = i;
                 else status |= CN_RXF_CAPACITY;
             } else if (!(fl & CF_COMPLETE) && !((d.c_seen[e] >> s) & 1u)) {
-                atomicMin(&first_of(d, par)[e * d.ppc + s], t);
+                const uint64_t fi = e * d.ppc + s;
+                atomicMin(&first_of(d, par)[fi], t);
+                if (d.carry) {  // the scatter's descriptor (k_copy keeps the first arrival)
+                    const uint64_t moff = h.chunk_offset + static_cast<uint64_t>(s) * d.max_pl;
+                    cdst = m_buf[gslot] + moff;
+                    cfi = static_cast<uint32_t>(fi);
+                }
             }
             if (!(fl & CF_INIT)) atomicMin(&d.c_init[e], t);
             touch = static_cast<uint32_t>(c) + 1;
@@ -641,6 +675,10 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     if (i < n) {
         d.p_gen[i] = g;
         d.p_nack[i] = 0;
+        if (d.carry) {
+            d.p_dst[par * static_cast<uint64_t>(d.max_batch) + i] = cdst;
+            d.p_fi[par * static_cast<uint64_t>(d.max_batch) + i] = cfi;
+        }
     }
     // chunk-vector size per message (:636-637): max over the block, one
     // global atomic per generation and block
@@ -1108,28 +1146,32 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
                                               uint32_t n) {
     const int lane = threadIdx.x & 31;
     TM_START(24);
-    const uint32_t* __restrict__ cf = first_of(d, d.ctl->copy_par);
+    RxCtl* C = d.ctl;
+    const uint32_t par = C->cq[C->cq_out & 3];
+    const uint32_t* __restrict__ cf = first_of(d, par);
+    const unsigned long long* __restrict__ pd = d.p_dst + par * static_cast<uint64_t>(d.max_batch);
+    const uint32_t* __restrict__ pf = d.p_fi + par * static_cast<uint64_t>(d.max_batch);
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
-        const uint32_t g = d.p_gen[i];
-        if (g >= kErr) continue;  // stale before the batch, or rejected
+        // k_ingest's descriptor: only packets not seen before the batch, of
+        // a live message (GenStates may be reused while a pipelined scatter
+        // still runs, so the destination travels with the packet)
+        const unsigned long long dst = pd[i];
+        if (!dst) continue;
+        // first arrival within the batch: c_first is final after k_ingest
+        if (cf[pf[i]] != i + 1) continue;
         const cn_pkt_hdr* hp = hdrs + i;
-        const uint64_t off = hp->chunk_offset;
-        const uint32_t s = hp->seq_in_chunk;
         const uint32_t len = hp->payload_len;
-        const GenState* G = &d.gen[g];
-        const uint64_t e = G->chunk_base + off / d.cb;
-        // first arrival of a packet not seen before the batch (k_ingest
-        // marks only those); c_seen itself is folded by k_finalize beside us
-        const bool fresh = cf[e * d.ppc + s] == i + 1;
-        if (!fresh) continue;
-        if (d.carry) {
-            const uint64_t moff = off + static_cast<uint64_t>(s) * d.max_pl;
-            const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
-            warp_scatter<R>(G->buf + moff, src, len, lane);
-        }
+        const uint64_t moff = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
+        const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
+        warp_scatter<R>(reinterpret_cast<uint8_t*>(dst), src, len, lane);
     }
     TM_END(25);
+    // the last block pops the part queue (every block has read it by now)
+    if (threadIdx.x == 0 && atomicAdd(&C->cq_done, 1u) == gridDim.x - 1) {
+        C->cq_done = 0;
+        C->cq_out += 1;
+    }
 }
 
 // What the reference does with packet i (handle_data's branches).  Every
@@ -1139,14 +1181,136 @@ __device__ __forceinline__ uint32_t pmax_ld(const RxDev& d, uint64_t cbase, uint
                                             uint64_t x) {
     return x < cum ? 0u : x >= n_init ? kInf : d.c_pmax[cbase + x];
 }
+// The copy-mode scatter on the bulk-copy engine: persistent blocks of one
+// warp, kTmaSlots lanes each owning a shared-memory slot.  Per packet the
+// lane issues a bulk load of its 16-byte-multiple body into the slot (an
+// mbarrier counts the bytes), prefetches its next packet's descriptor while
+// the load flies, then issues the bulk store from the slot; the next load
+// into the slot waits only for that store to have READ the slot.  The
+// scatter thus holds 2 x 148 warps instead of thousands, and the
+// latency-bound ack path beside it keeps the SMs' issue slots.  Bytes past
+// the last 16-byte multiple, and packets whose source or destination is not
+// 16-byte aligned (chunk sizes that are not multiples of 16), take the
+// warp-cooperative vector path.
+constexpr int kTmaSlots = 16;
+constexpr uint32_t kTmaSlotBytes = 4096;  // >= max_payload, multiple of 16
+constexpr uint32_t kTmaSmem = kTmaSlots * kTmaSlotBytes;
+
+__global__ void __launch_bounds__(32) k_copy_tma(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
+                                                 const uint8_t* __restrict__ payload, uint64_t stride,
+                                                 uint32_t n) {
+    extern __shared__ __align__(128) uint8_t tma_buf[];
+    __shared__ __align__(8) uint64_t tma_bar[kTmaSlots];
+    const int lane = threadIdx.x;
+    TM_START(24);
+    RxCtl* C = d.ctl;
+    const uint32_t par = C->cq[C->cq_out & 3];
+    const uint32_t* __restrict__ cf = first_of(d, par);
+    const unsigned long long* __restrict__ pd = d.p_dst + par * static_cast<uint64_t>(d.max_batch);
+    const uint32_t* __restrict__ pf = d.p_fi + par * static_cast<uint64_t>(d.max_batch);
+    const bool act = lane < kTmaSlots;
+    const uint32_t slot = smem_u32(tma_buf + (act ? lane : 0) * kTmaSlotBytes);
+    const uint32_t bar = smem_u32(&tma_bar[act ? lane : 0]);
+    if (act) mbar_init(bar, 1);
+    fence_mbar_init();
+    __syncwarp();
+    const uint64_t pol = l2_evict_first();
+    // this lane's packet: k_ingest's descriptor, the first-arrival test, the header fields
+    auto fetch = [&](uint32_t i, unsigned long long& dst, uint32_t& len, uint64_t& moff) {
+        dst = 0;
+        if (!act || i >= n) return;
+        const unsigned long long d0 = pd[i];
+        if (!d0) return;
+        const uint32_t fi = pf[i];
+        const cn_pkt_hdr* hp = hdrs + i;
+        const uint32_t l = hp->payload_len;
+        const uint64_t mo = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
+        if (cf[fi] != i + 1) return;
+        dst = d0;
+        len = l;
+        moff = mo;
+    };
+    const uint32_t step = gridDim.x * kTmaSlots;
+    uint32_t i = blockIdx.x * kTmaSlots + lane;
+    unsigned long long dst = 0;
+    uint32_t len = 0;
+    uint64_t moff = 0;
+    fetch(i, dst, len, moff);
+    uint32_t phase = 0;
+    bool stored = false;
+    for (uint32_t base = blockIdx.x * kTmaSlots; base < n; base += step) {
+        const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
+        const uint32_t len16 = len & ~15u;
+        const bool bulk = dst && len16 && !((reinterpret_cast<uintptr_t>(src) | dst) & 15);
+        if (bulk) {
+            if (stored) bulk_wait_read0();  // the slot's previous store has read it
+            mbar_arrive_expect_tx(bar, len16);
+            bulk_g2s(slot, src, len16, bar, pol);
+        }
+        // the next packet's descriptor while the load flies
+        const uint32_t i2 = i + step;
+        unsigned long long dst2 = 0;
+        uint32_t len2 = 0;
+        uint64_t moff2 = 0;
+        fetch(i2, dst2, len2, moff2);
+        if (bulk)
+            for (uint32_t b = len16; b < len; ++b) reinterpret_cast<uint8_t*>(dst)[b] = src[b];
+        unsigned fb = __ballot_sync(0xffffffffu, dst && !bulk);
+        while (fb) {
+            const int l = __ffs(fb) - 1;
+            fb &= fb - 1;
+            const unsigned long long fd = __shfl_sync(0xffffffffu, dst, l);
+            const unsigned long long fs = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), l);
+            const uint32_t fl = __shfl_sync(0xffffffffu, len, l);
+            warp_scatter<0>(reinterpret_cast<uint8_t*>(fd), reinterpret_cast<const uint8_t*>(fs), fl, lane);
+        }
+        if (bulk) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            bulk_s2g(reinterpret_cast<void*>(dst), slot, len16, pol);
+            bulk_commit();
+            stored = true;
+        }
+        i = i2;
+        dst = dst2;
+        len = len2;
+        moff = moff2;
+    }
+    bulk_wait_all();
+    TM_END(25);
+    __syncwarp();
+    if (lane == 0 && atomicAdd(&C->cq_done, 1u) == gridDim.x - 1) {  // pops the part queue
+        C->cq_done = 0;
+        C->cq_out += 1;
+    }
+}
+
+// What decide() learned about an ack-emitting packet, kept in shared memory
+// for build_ack (the header, its message's state, chunk c): the ack
+// snapshot then takes two dependent round trips.
+struct AckCtx {
+    unsigned long long cbase, seq, len;  // chunk base, msg_seq (G's; the header's if stale), msg length
+    uint32_t c, cum0, n_init, hdr;       // chunk, cursor before the batch, chunk vector size, wire header
+    int32_t src, dst;
+    uint8_t msg_id, exp, flags, pad;     // exp = packets of chunk c; flags = header flags
+};
+
 __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __restrict__ hdrs,
-                                          uint32_t i, uint32_t* st, uint64_t* e_out, uint32_t* pmc) {
+                                          uint32_t i, uint32_t* st, uint64_t* e_out, uint32_t* pmc,
+                                          AckCtx* x) {
     const uint32_t g = d.p_gen[i];
-    const uint64_t off = hdrs[i].chunk_offset;
-    const uint32_t s = hdrs[i].seq_in_chunk;
+    const cn_pkt_hdr* hp = hdrs + i;
+    const uint64_t off = hp->chunk_offset;
+    const uint32_t s = hp->seq_in_chunk;
+    const uint8_t hfl = hp->flags;
+    x->hdr = hp->hdr;
+    x->src = hp->src;
+    x->dst = hp->dst;
+    x->seq = hp->msg_seq;
+    x->flags = hfl;
     const uint32_t t = i + 1;
     if (d.ordered && d.p_gbn[i]) return d.p_gbn[i] == 2 ? PC_NACK : 0;  // decided by k_gbn
-    if (hdrs[i].flags & CN_PKT_TRIMMED) return d.p_nack[i] ? PC_NACK : 0;  // decided by k_trim
+    if (hfl & CN_PKT_TRIMMED) return d.p_nack[i] ? PC_NACK : 0;  // decided by k_trim
     if (g == kStale) return PC_STALE;  // transport.cpp:602-615
     if (g == kErr) return 0;
     const GenState& G = d.gen[g];
@@ -1162,6 +1326,14 @@ __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __re
     const uint32_t pm2 = c >= 128 ? pmax_ld(d, cbase, cum, n_init, c - 128) : 0u;
     *pmc = pm0;
     if (t > dt) return PC_STALE;
+    x->cbase = cbase;
+    x->seq = G.seq;
+    x->len = G.len;
+    x->c = static_cast<uint32_t>(c);
+    x->cum0 = cum;
+    x->n_init = n_init;
+    x->msg_id = static_cast<uint8_t>(G.msg_id);
+    x->exp = static_cast<uint8_t>(pkts_of(d, chunk_len_of(d, G.len, c)));
     uint8_t cls = 0;
     const uint32_t cpl = (fl & CF_COMPLETE) ? 0 : cpl0;
     if (cpl < t) {
@@ -1286,103 +1458,117 @@ __device__ __forceinline__ uint32_t first_above(const uint32_t* __restrict__ pm,
 }
 
 __device__ __forceinline__ void build_ack(const RxDev& d, const cn_pkt_hdr* __restrict__ hdrs,
-                                          uint32_t i, uint8_t cls, uint32_t g, uint32_t pmc, int lane,
+                                          uint32_t i, uint8_t cls, uint32_t pmc, const AckCtx& x, int lane,
                                           cn_ack_rec* out) {
-    const cn_pkt_hdr h = hdrs[i];
     const uint32_t t = i + 1;
-    const uint32_t csn = (h.hdr >> 9) & 0xFF;
+    const uint32_t csn = (x.hdr >> 9) & 0xFF;
     if (cls & (PC_STALE | PC_NACK)) {  // stale re-ack (:602-615) / trimmed-header NACK (:657-674)
         if (lane == 0) {
             cn_ack_rec r;
             memset(&r, 0, sizeof r);
-            r.src = h.dst;
-            r.dst = h.src;
-            r.hdr = h.hdr;
+            r.src = x.dst;
+            r.dst = x.src;
+            r.hdr = x.hdr;
             r.cum_csn = static_cast<uint8_t>(csn);
             r.flags = (cls & PC_NACK) ? CN_ACK_NACK : CN_ACK_CUM_VALID;
             r.pkt_index = i;
-            r.msg_seq = h.msg_seq;
+            r.msg_seq = x.seq;
             if ((cls & PC_NACK) && d.ordered) {  // sequence-gap NACK (:695-707): nack_psn, no csn / seq
                 r.cum_csn = 0;
                 r.msg_seq = 0;
-                r.flags = CN_ACK_NACK | CN_ACK_GBN | ((h.flags & CN_PKT_TRIMMED) ? CN_ACK_NACK_TRIM : 0);
+                r.flags = CN_ACK_NACK | CN_ACK_GBN | ((x.flags & CN_PKT_TRIMMED) ? CN_ACK_NACK_TRIM : 0);
                 r.sack[0] = d.p_gbn_psn[i];
             }
             *out = r;
         }
         return;
     }
-    const GenState& G = d.gen[g];
-    const uint32_t cum0 = G.cum, n_init = G.n_init;
-    const uint64_t cbase = G.chunk_base;
+    const uint32_t cum0 = x.cum0, n_init = x.n_init;
+    const uint64_t cbase = x.cbase;
     const uint32_t* pm = d.c_pmax + cbase;
+    const uint32_t c = x.c;
+    const uint32_t par = d.ctl->par;
+    // round trip 1: the cursor's 32-chunk window beside c, and chunk c's
+    // state -- the echo chunk whenever the ack carries an echo (below)
+    const uint64_t Ec = cbase + c;
+    uint32_t fl = d.c_flags[Ec], cinit = d.c_init[Ec], seen = d.c_seen[Ec];
+    int64_t txt0 = d.c_txt[Ec];
+    int32_t path0 = d.c_path[Ec];
+    uint32_t f0 = static_cast<uint32_t>(lane) < x.exp ? first_of(d, par)[Ec * d.ppc + lane] : kInf;
     // cum after this packet, searched outward from the packet's own chunk c
     // (pmax[c] came from decide): usually one 32-chunk window decides it
-    const uint32_t c = static_cast<uint32_t>(h.chunk_offset / d.cb);
     uint32_t cum;
     if (pmc <= t) {  // the cursor is past c: scan upward from c + 1
-        const uint32_t x = c + 1 + lane;
-        const bool le = x < cum0 || (x < n_init && pm[x] <= t);
+        const uint32_t y = c + 1 + lane;
+        const bool le = y < cum0 || (y < n_init && pm[y] <= t);
         const unsigned b = __ballot_sync(0xffffffffu, le);
         cum = b != 0xffffffffu ? c + 1 + __popc(b)
                                : first_above(pm, c + 33 > cum0 ? c + 33 : cum0, n_init, t, lane);
     } else {  // the cursor is at or before c: scan downward from c
-        const int64_t x = static_cast<int64_t>(c) - 32 + lane;
-        const bool gt = x >= static_cast<int64_t>(cum0) && pm[x] > t;
+        const int64_t y = static_cast<int64_t>(c) - 32 + lane;
+        const bool gt = y >= static_cast<int64_t>(cum0) && pm[y] > t;
         const unsigned b = __ballot_sync(0xffffffffu, gt);
         if ((b & 1u) && static_cast<int64_t>(c) - 32 > static_cast<int64_t>(cum0))
             cum = first_above(pm, cum0, c - 32, t, lane);
         else
             cum = b ? c - 32 + (__ffs(b) - 1) : c;
     }
-    // 128-bit SACK, bit j = chunk cum+j complete (:775-779)
-    const uint32_t* cp = d.c_cpl + cbase;
-    uint32_t sw[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint32_t x = cum + q * 32 + lane;
-        sw[q] = __ballot_sync(0xffffffffu, x < n_init && cp[x] <= t);
-    }
-    // echo of chunk cum + uint8(cause - uint8(cum)) (:781-789)
+    // echo of chunk cum + uint8(cause - uint8(cum)) (:781-789): with an
+    // echo (offset < 128) that is chunk c itself, as the cursor moves at
+    // most a window per packet; anything else reloads (kept exact)
     const uint32_t rel = (csn - (cum & 0xFF)) & 0xFF;
     const uint32_t ei = cum + rel;
+    const bool echo = rel < CN_CSN_WINDOW && ei < n_init;
+    uint32_t exp = x.exp;
+    if (echo && ei != c) {
+        const uint64_t E = cbase + ei;
+        exp = pkts_of(d, chunk_len_of(d, x.len, ei));
+        fl = d.c_flags[E];
+        cinit = d.c_init[E];
+        seen = d.c_seen[E];
+        txt0 = d.c_txt[E];
+        path0 = d.c_path[E];
+        f0 = static_cast<uint32_t>(lane) < exp ? first_of(d, par)[E * d.ppc + lane] : kInf;
+    }
+    const bool live = echo && ((fl & CF_INIT) || cinit <= t);
+    const uint32_t f = ((seen >> lane) & 1u) ? kInf : f0;
+    const bool fok = live && f <= t;
+    const uint32_t lastf = __reduce_max_sync(0xffffffffu, fok ? f : 0u);
+    // round trip 2: the 128-bit SACK, bit j = chunk cum+j complete
+    // (:775-779), and the headers of the echo chunk's new packets
+    const uint32_t* cp = d.c_cpl + cbase;
+    uint32_t cv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t y = cum + q * 32 + lane;
+        cv[q] = y < n_init ? cp[y] : kInf;
+    }
+    const uint8_t pfl = fok ? hdrs[f - 1].flags : 0;
     int64_t etxt = 0;
     int32_t epath = 0;
-    uint32_t eecn = 0;
-    if (rel < CN_CSN_WINDOW && ei < n_init) {
-        // all of the echo chunk's state in one round trip
-        const uint64_t E = cbase + ei;
-        const uint32_t exp = pkts_of(d, chunk_len_of(d, G.len, ei));
-        const uint32_t fl = d.c_flags[E], cinit = d.c_init[E], seen = d.c_seen[E];
-        const int64_t txt0 = d.c_txt[E];
-        const int32_t path0 = d.c_path[E];
-        const uint32_t f0 = static_cast<uint32_t>(lane) < exp ? first_of(d, d.ctl->par)[E * d.ppc + lane] : kInf;
-        if ((fl & CF_INIT) || cinit <= t) {
-            const uint32_t f = ((seen >> lane) & 1u) ? kInf : f0;
-            const bool fok = f <= t;
-            const uint32_t lastf = __reduce_max_sync(0xffffffffu, fok ? f : 0u);
-            const unsigned eb = __ballot_sync(0xffffffffu, fok && (hdrs[fok ? f - 1 : i].flags & CN_PKT_ECN));
-            if (lastf) {
-                etxt = hdrs[lastf - 1].tx_time;
-                epath = hdrs[lastf - 1].path_id;
-            } else {
-                etxt = txt0;
-                epath = path0;
-            }
-            eecn = (eb != 0) || (fl & CF_ECN);
-        }
+    if (lastf) {
+        etxt = hdrs[lastf - 1].tx_time;
+        epath = hdrs[lastf - 1].path_id;
+    } else if (live) {
+        etxt = txt0;
+        epath = path0;
     }
+    uint32_t sw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sw[q] = __ballot_sync(0xffffffffu, cv[q] <= t);
+    const unsigned eb = __ballot_sync(0xffffffffu, fok && (pfl & CN_PKT_ECN));
+    const uint32_t eecn = live && ((eb != 0) || (fl & CF_ECN));
     if (lane == 0) {
         cn_ack_rec r;
         memset(&r, 0, sizeof r);
-        r.src = h.dst;
-        r.dst = h.src;
-        r.hdr = enc_hdr(h.hdr >> 24, G.msg_id, csn, 0, 0);
+        r.src = x.dst;
+        r.dst = x.src;
+        r.hdr = enc_hdr(x.hdr >> 24, x.msg_id, csn, 0, 0);
         r.echo_path_id = epath;
         r.cum_csn = static_cast<uint8_t>((cum - 1) & 0xFF);
         r.flags = (cum > 0 ? CN_ACK_CUM_VALID : 0) | (eecn ? CN_ACK_ECN_ECHO : 0);
         r.pkt_index = i;
-        r.msg_seq = G.seq;
+        r.msg_seq = x.seq;
         r.sack[0] = sw[0] | (static_cast<uint64_t>(sw[1]) << 32);
         r.sack[1] = sw[2] | (static_cast<uint64_t>(sw[3]) << 32);
         r.echo_tx_time = etxt;
@@ -1402,6 +1588,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
     __shared__ cn_ack_rec s_rec[kAckTile];
     __shared__ uint8_t s_cls[kAckTile];
     __shared__ uint32_t s_g[kAckTile], s_pm[kAckTile];
+    __shared__ AckCtx s_ctx[kAckTile];
     __shared__ uint16_t s_alist[kAckTile], s_clist[kAckTile];
     __shared__ uint32_t s_wa[kDecideWarps], s_wc[kDecideWarps];
     __shared__ uint32_t s_tile, s_base_a, s_base_c;
@@ -1413,6 +1600,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= tiles) break;
+        TM_TILE(0, tile);
         const uint32_t i0 = tile * kAckTile;
         uint8_t cls = 0;
         unsigned ab = 0, cb = 0;
@@ -1422,7 +1610,9 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
             const uint32_t j = warp * 32 + lane;
             const uint32_t i = i0 + j;
             uint32_t pmc = 0;
-            if (i < n) cls = decide(d, hdrs, i, &st, &e, &pmc);
+            AckCtx x;
+            if (i < n) cls = decide(d, hdrs, i, &st, &e, &pmc, &x);
+            if (cls & (PC_STALE | PC_ACK | PC_NACK)) s_ctx[j] = x;
             if (cls & PC_COPY) {  // ChunkRx::ecn / any_rtx of new packets (:680-681)
                 const uint8_t pf = hdrs[i].flags;
                 const uint32_t b = ((pf & CN_PKT_ECN) ? CF_ECN : 0) | ((pf & CN_PKT_RTX) ? CF_RTX : 0);
@@ -1441,6 +1631,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
             if (lane == 0 && st) atomicOr(&d.ctl->status, st);
         }
         __syncthreads();
+        TM_TILE(1, tile);
         uint32_t na = 0, nc = 0;
         for (int w = 0; w < kDecideWarps; ++w) {
             na += s_wa[w];
@@ -1504,9 +1695,10 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
         // acks round-robin over the warps, warp 0 (busy looking back) last
         for (uint32_t k = kAckWarps - 1 - warp; k < na; k += kAckWarps) {
             const uint32_t j = s_alist[k];
-            build_ack(d, hdrs, i0 + j, s_cls[j], s_g[j], s_pm[j], lane, &s_rec[k]);
+            build_ack(d, hdrs, i0 + j, s_cls[j], s_pm[j], s_ctx[j], lane, &s_rec[k]);
         }
         __syncthreads();
+        TM_TILE(2, tile);
         for (uint32_t k = warp; k < na; k += kAckWarps) {
             const uint32_t a = s_base_a + k;
             if (lane < 16 && a < max_acks)
@@ -1533,6 +1725,7 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
             }
         }
         __syncthreads();  // shared lists are reused by the next tile
+        TM_TILE(3, tile);
     }
     TM_END(23);
 }
@@ -1560,9 +1753,10 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     // the previous batch's first-arrival half: its scatter has finished
     // (stream order), the next batch uses it
     {
-        uint32_t* cf1 = first_of(d, par ^ 1u);
-        const unsigned long long* dl = d.dirty + (par ^ 1u) * static_cast<uint64_t>(d.dirty_cap);
-        const uint32_t nd = d.ctl->n_dirty[par ^ 1u];
+        const uint32_t nxt = par == 2 ? 0u : par + 1;  // batch k - 2's part, batch k + 1's
+        uint32_t* cf1 = first_of(d, nxt);
+        const unsigned long long* dl = d.dirty + nxt * static_cast<uint64_t>(d.dirty_cap);
+        const uint32_t nd = d.ctl->n_dirty[nxt];
         for (uint32_t j = blockIdx.x; j < nd; j += gridDim.x) {
             const unsigned long long v = dl[j];
             if (threadIdx.x < (v & 511)) {
@@ -1667,8 +1861,9 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     // handler has run (the reference hands the buffer to on_complete and
     // frees it after, :794-803)
     {
-        const unsigned long long* al = d.aret + (par ^ 1u) * static_cast<uint64_t>(d.plan_cap);
-        const uint32_t na = d.ctl->n_aret[par ^ 1u];
+        const uint32_t prv = par == 0 ? 2u : par - 1;  // the previous batch's part
+        const unsigned long long* al = d.aret + prv * static_cast<uint64_t>(d.plan_cap);
+        const uint32_t na = d.ctl->n_aret[prv];
         for (uint32_t j = blockIdx.x; j < na; j += gridDim.x) {
             const unsigned long long v = al[j];
             const uint64_t a0 = v >> 31, n0 = v & 0x7FFFFFFF;
@@ -1791,11 +1986,12 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->plan_ticket_fin = 0;
         uint32_t ep = C->epoch + 1;
         C->epoch = ep ? ep : 1;
+        const uint32_t nxt = par == 2 ? 0u : par + 1, prv = par == 0 ? 2u : par - 1;
         C->n_dirty[par] = min(C->n_dirty_next, d.dirty_cap);
         C->n_dirty_next = 0;
-        C->n_dirty[par ^ 1u] = 0;
-        C->n_aret[par ^ 1u] = 0;
-        C->par = par ^ 1u;
+        C->n_dirty[nxt] = 0;  // cleared by this batch
+        C->n_aret[prv] = 0;   // released by this batch
+        C->par = nxt;
         // physical extent used since the last reset (ranges overhang cap once the ring laps)
         C->pool_snap = C->pool.head < d.pool_cap ? C->pool.head : 2 * d.pool_cap;
         // the rings' tails over what the batch's ring scan found retired
@@ -1851,18 +2047,20 @@ __global__ void k_reset(RxDev d, int full) {
     for (uint64_t x = tid; x < (d.arena_blocks + 31) / 32; x += stride) d.arena_bits[x] = 0;
     for (uint64_t x = tid; x < top * d.ppc; x += stride) {
         d.c_first[x] = kInf;
-        d.c_first[d.first_half + x] = kInf;
+        d.c_first[d.first_part + x] = kInf;
+        d.c_first[2 * d.first_part + x] = kInf;
     }
     if (full)
         for (uint64_t x = tid; x < d.pool_cap / kScanThreads + ngen + 2; x += stride) d.scan_state[x] = 0;
     if (tid == 0) {
         d.ctl->pool.head = d.ctl->pool.tail = 0;
         d.ctl->arena.head = d.ctl->arena.tail = 0;
-        d.ctl->n_dirty[0] = 0;
-        d.ctl->n_dirty[1] = 0;
+        for (int q = 0; q < 3; ++q) {
+            d.ctl->n_dirty[q] = 0;
+            d.ctl->n_aret[q] = 0;
+        }
         d.ctl->n_dirty_next = 0;
-        d.ctl->n_aret[0] = 0;
-        d.ctl->n_aret[1] = 0;
+        d.ctl->cq_in = d.ctl->cq_out = d.ctl->cq_done = 0;
         d.ctl->gfree_head = 0;
         d.ctl->gfree_tail = ngen;
         d.ctl->n_tomb = 0;
@@ -1892,12 +2090,20 @@ struct cn_rx {
     int sms = 148;
     int copy_bps = 64;  // k_copy block cap per SM (CN_COPY_BLOCKS_PER_SM overrides)
     int scan_first = 1;  // launch scan/acks before the scatter (CN_SCAN_FIRST=0 reverts)
+    int copy_tma = 0;    // copy mode on the bulk-copy engine (CN_COPY_TMA=1; default: the vector path)
+    int tma_bps = 2;     // its blocks per SM (CN_TMA_BPS)
     uint32_t small_batch = 32768;  // batches up to this many packets use 32-packet ack tiles (CN_ACK_SMALL)
     int hi_prio = 0;     // greatest stream priority: the latency-bound ack path wins SM slots
     // optional per-kernel timing with CUDA events on the launch stream
     bool profiling = false;
     cudaStream_t side = nullptr;           // k_copy overlaps the ack machinery
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // pipelined receivers (cn_rx_config::pipeline): the scatter of batch k is
+    // joined into the caller's stream at the end of batch k + 1 (or by
+    // cn_rx_flush); ev_copy alternates by host batch count
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+    uint64_t batch_no = 0;
+    int copy_pending = -1;  // ev_copy index of the scatter not yet joined, -1 none
     int* post_ok = nullptr;
     std::vector<std::vector<cudaEvent_t>> pending;
     double acc_ms[kRxKernels] = {0};
@@ -1930,6 +2136,7 @@ extern "C" void cn_rx_config_default(cn_rx_config* cfg) {
     cfg->carry_payload = 1;
     cfg->reduce_op = CN_REDUCE_NONE;
     cfg->max_posts = 0;
+    cfg->pipeline = 0;
 }
 
 static void rx_free(cn_rx* rx) {
@@ -1937,7 +2144,7 @@ static void rx_free(cn_rx* rx) {
     void* ptrs[] = {d.rc_key, d.rc_done, d.gen_key, d.gen_val, d.gen_free, d.gen_tmp, d.gen, d.touched, d.c_first, d.dirty, d.pool_bits,
                     d.arena_bits, d.aret, d.c_seen,
                     d.c_flags, d.c_txt, d.c_path, d.c_init, d.c_cpl, d.c_pmax, d.c_newb,
-                    d.c_last, d.c_newfl, d.p_gen, d.p_nack, d.trim_list, d.p_gbn, d.p_gbn_psn,
+                    d.c_last, d.c_newfl, d.p_gen, d.p_dst, d.p_fi, d.p_nack, d.trim_list, d.p_gbn, d.p_gbn_psn,
                     d.gbn_expected, d.gbn_nacked,
                     d.tile_state, d.scan_state, d.ctl, d.plan_F, d.plan_t0, d.arena, d.post_key,
                     d.post_val, d.post_len};
@@ -2001,6 +2208,9 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     cudaFuncSetAttribute(k_trim, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTrimMax * 8));
     if (const char* e = getenv("CN_COPY_BLOCKS_PER_SM")) rx->copy_bps = atoi(e) > 0 ? atoi(e) : 64;
     if (const char* e = getenv("CN_SCAN_FIRST")) rx->scan_first = atoi(e);
+    if (const char* e = getenv("CN_COPY_TMA")) rx->copy_tma = atoi(e);
+    if (const char* e = getenv("CN_TMA_BPS")) rx->tma_bps = atoi(e) > 0 ? atoi(e) : 2;
+    cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
     if (const char* e = getenv("CN_ACK_SMALL")) rx->small_batch = static_cast<uint32_t>(atoi(e));
     {
         int least = 0, greatest = 0;
@@ -2026,12 +2236,18 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.gen_tmp, ngen * 16ull);
     ALLOC(d.touched, ngen * 4ull);
     const uint64_t phys = 2 * cfg.chunk_pool;  // ring capacity + overhang
-    d.first_half = phys * ppc;
-    ALLOC(d.c_first, 2 * d.first_half * 4);
+    d.first_part = phys * ppc;
+    if (3 * d.first_part >= (1ull << 32)) {  // p_fi indices are 32-bit
+        rx_free(rx);
+        delete rx;
+        set_error("cn_rx_create: chunk_pool too large (2 * chunk_pool * packets per chunk must be < 2^31)");
+        return CN_E_INVALID;
+    }
+    ALLOC(d.c_first, 3 * d.first_part * 4);
     d.plan_cap = ngen < kPlanMax ? ngen : kPlanMax;
     if (const char* e = getenv("CN_PLAN_CAP")) d.plan_cap = std::min<uint32_t>(d.plan_cap, atoi(e) > 0 ? atoi(e) : 1);
     d.dirty_cap = static_cast<uint32_t>(cfg.chunk_pool / kScanThreads + d.plan_cap + 1);
-    ALLOC(d.dirty, 2ull * d.dirty_cap * 8);
+    ALLOC(d.dirty, 3ull * d.dirty_cap * 8);
     ALLOC(d.pool_bits, (cfg.chunk_pool + 31) / 32 * 4);
     d.arena_blocks = d.arena_cap / kArenaUnit;
     if (d.pool_cap >= (1ull << 32) || d.arena_blocks >= (1ull << 32)) {  // ring offsets are 32-bit
@@ -2046,7 +2262,7 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
         d.scan_blocks = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(b, 1), 2ull * rx->sms));
     }
     if (d.arena_blocks) ALLOC(d.arena_bits, (d.arena_blocks + 31) / 32 * 4);
-    ALLOC(d.aret, 2ull * d.plan_cap * 8);
+    ALLOC(d.aret, 3ull * d.plan_cap * 8);
     ALLOC(d.plan_F, (d.plan_cap + 1ull) * 4);
     ALLOC(d.plan_t0, (cfg.chunk_pool / kScanThreads + d.plan_cap + 4ull) * 4);
     ALLOC(d.c_seen, phys * 4);
@@ -2060,6 +2276,11 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     ALLOC(d.c_last, phys * 4);
     ALLOC(d.c_newfl, phys * 4);
     ALLOC(d.p_gen, B * 4);
+    d.max_batch = static_cast<uint32_t>(B);
+    if (d.carry) {
+        ALLOC(d.p_dst, 3 * B * 8);
+        ALLOC(d.p_fi, 3 * B * 4);
+    }
     ALLOC(d.p_nack, B);
     d.ordered = cfg.ordered ? 1 : 0;
     if (d.ordered) {
@@ -2083,6 +2304,8 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     cudaStreamCreateWithFlags(&rx->side, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&rx->ev_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&rx->ev_join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&rx->ev_copy[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&rx->ev_copy[1], cudaEventDisableTiming);
     cudaMemset(d.gen, 0, ngen * sizeof(GenState));
     k_ctl_init<<<1, 1>>>(d);
     k_reset<<<rx->sms * 4, 256>>>(d, 1);
@@ -2102,6 +2325,8 @@ extern "C" void cn_rx_destroy(cn_rx* rx) {
     for (auto& ev : rx->pending)
         for (auto e : ev) cudaEventDestroy(e);
     if (rx->side) cudaStreamDestroy(rx->side);
+    for (auto e : rx->ev_copy)
+        if (e) cudaEventDestroy(e);
     if (rx->post_ok) cudaFree(rx->post_ok);
     if (rx->ev_fork) cudaEventDestroy(rx->ev_fork);
     if (rx->ev_join) cudaEventDestroy(rx->ev_join);
@@ -2115,8 +2340,23 @@ extern "C" int cn_rx_reset(cn_rx* rx, void* stream) {
         return CN_E_INVALID;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = cn_rx_flush(rx, stream);  // an outstanding pipelined scatter finishes first
+    if (rc != CN_OK) return rc;
     k_reset<<<rx->sms * 4, 256, 0, s>>>(rx->d, 0);
     CNB_CUDA(cudaGetLastError());
+    return CN_OK;
+}
+
+// Joins the outstanding scatter of a pipelined receiver into `stream`.
+extern "C" int cn_rx_flush(cn_rx* rx, void* stream) {
+    if (!rx) {
+        set_error("cn_rx_flush: null handle");
+        return CN_E_INVALID;
+    }
+    if (rx->copy_pending >= 0) {
+        CNB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), rx->ev_copy[rx->copy_pending], 0));
+        rx->copy_pending = -1;
+    }
     return CN_OK;
 }
 
@@ -2195,6 +2435,8 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
     const RxDev& d = rx->d;
     std::vector<cudaEvent_t>* ev = nullptr;
     if (rx->profiling && n > 0) {
+        int rc = cn_rx_flush(rx, stream);  // profiled batches run strictly in order
+        if (rc != CN_OK) return rc;
         rx->pending.emplace_back();
         ev = &rx->pending.back();
     }
@@ -2212,9 +2454,30 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         // to the scatter as they free up (a persistent scatter grid would
         // pin half the register file for its whole duration)
         uint32_t cmax = static_cast<uint32_t>(rx->sms * rx->copy_bps);
-        if (d.ordered) k_gbn<<<4, 256, 0, s>>>(d, d_hdrs, n);  // the go-back-N filter first
-        k_ingest<<<d.scan_blocks + (n + kIngestThreads - 1) / kIngestThreads, kIngestThreads, 0, s>>>(d, d_hdrs,
-                                                                                                       n);
+        // the ack path at the greatest priority from its first kernel: in a
+        // pipelined receiver the previous batch's scatter still fills the SMs
+        auto hi = [&](dim3 grid, dim3 block, size_t smem) {
+            cudaLaunchConfig_t lc = {};
+            static thread_local cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributePriority;
+            at[0].val.priority = rx->hi_prio;
+            lc.gridDim = grid;
+            lc.blockDim = block;
+            lc.dynamicSmemBytes = smem;
+            lc.stream = s;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            return lc;
+        };
+        if (d.ordered) {  // the go-back-N filter first
+            cudaLaunchConfig_t lc = hi(dim3(4), dim3(256), 0);
+            CNB_CUDA(cudaLaunchKernelEx(&lc, k_gbn, d, d_hdrs, n));
+        }
+        {
+            cudaLaunchConfig_t lc = hi(dim3(d.scan_blocks + (n + kIngestThreads - 1) / kIngestThreads),
+                                       dim3(kIngestThreads), 0);
+            CNB_CUDA(cudaLaunchKernelEx(&lc, k_ingest, d, d_hdrs, n));
+        }
         prof_mark(ev, s);
         // fork: the HBM-bound scatter runs beside the latency-bound ack path
         cudaStream_t cs = ev ? s : rx->side;
@@ -2232,6 +2495,8 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
                 k_copy<1><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
             else if (d.reduce == 2)
                 k_copy<2><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+            else if (rx->copy_tma && payload_stride % 16 == 0 && d.max_pl <= kTmaSlotBytes)
+                k_copy_tma<<<rx->tma_bps * rx->sms, 32, kTmaSmem, cs>>>(d, d_hdrs, pl, payload_stride, n);
             else
                 k_copy<0><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
             prof_mark(ev, s);
@@ -2300,14 +2565,24 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
             CNB_CUDA(cudaLaunchKernelEx(&lc, k_finalize, d, d_hdrs, d_result));
         }
         prof_mark(ev, s);
-        if (!ev) {
+        if (!ev && d.carry && rx->cfg.pipeline) {
+            // pipelined: join the PREVIOUS batch's scatter; this one's runs on
+            // beside the next batch's ingest and ack path
+            const int j = static_cast<int>(rx->batch_no & 1);
+            CNB_CUDA(cudaEventRecord(rx->ev_copy[j], cs));
+            if (rx->copy_pending >= 0) CNB_CUDA(cudaStreamWaitEvent(s, rx->ev_copy[rx->copy_pending], 0));
+            rx->copy_pending = j;
+        } else if (!ev) {
             CNB_CUDA(cudaEventRecord(rx->ev_join, cs));
             CNB_CUDA(cudaStreamWaitEvent(s, rx->ev_join, 0));
         }
     } else {
         k_finalize<<<gb, kScanThreads, 0, s>>>(d, d_hdrs, d_result);
         prof_mark(ev, s);
+        int rc = cn_rx_flush(rx, stream);  // an empty batch completes the pipeline
+        if (rc != CN_OK) return rc;
     }
+    rx->batch_no += 1;
     rx->launches = n > 0 ? (d.carry ? 6 : 5) + (d.ordered ? 1 : 0) : 1;
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
@@ -2384,6 +2659,11 @@ extern "C" int cn_rx_debug_timing(unsigned long long* out, int n) {
     for (int k = 0; k < 64; ++k) h[k] = 0;
     for (unsigned long long k : mins) h[k] = ~0ull;
     CNB_CUDA(cudaMemcpyToSymbol(g_tm, h, sizeof h));
+    return CN_OK;
+}
+// k_acks per-tile marks of the last batch: [4][kTileTm] (start, decided, built, written)
+extern "C" int cn_rx_debug_tile_timing(unsigned long long* out) {
+    CNB_CUDA(cudaMemcpyFromSymbol(out, g_tile_tm, sizeof g_tile_tm));
     return CN_OK;
 }
 #endif

@@ -76,7 +76,7 @@ class Transport:
 
     def __init__(self, cfg=None, seed=0, *, device="cuda", max_conns=1024, max_msgs=4096,
                  chunk_pool=1 << 22, arena_bytes=1 << 30, max_batch=1 << 20, reduce=None,
-                 max_posts=0):
+                 max_posts=0, pipeline=False):
         self.cfg = cfg or TransportConfig()
         if self.cfg.reliability not in ("selective", "ordered"):
             raise _lib.ChunknetError(-1, "reliability is 'selective' or 'ordered'")
@@ -100,6 +100,8 @@ class Transport:
         rc.reduce_op = self.REDUCE[reduce]
         rc.max_posts = max_posts
         rc.ordered = 1 if self.cfg.reliability == "ordered" else 0
+        rc.pipeline = 1 if pipeline else 0
+        self.pipeline = bool(pipeline)
         self._rxcfg = rc
         with torch.cuda.device(self.device):
             h = ctypes.c_void_p()
@@ -151,6 +153,8 @@ class Transport:
 
     def rx_batch_async(self, hdrs, payload, stride=MAX_PAYLOAD, stream=None, n=None, psn=None):
         """Enqueue the receive path for a batch; no host synchronisation.
+        A pipelined receiver (pipeline=True) leaves this batch's payload
+        scatter running beside the next batch (flush() joins it).
         hdrs: device uint8 [n*64] (cn_pkt_hdr records, arrival order);
         payload: device buffer, packet i's payload at i*stride; psn: device
         uint64 conn_psn per packet (ordered reliability only)."""
@@ -178,6 +182,8 @@ class Transport:
         the completion callback for every delivered message."""
         s = stream or torch.cuda.current_stream(self.device)
         n = self.rx_batch_async(hdrs, payload, stride, s, psn=psn)
+        if self.pipeline:  # this call's contract: the delivered bytes are final
+            self.flush(s)
         self._pinned.copy_(self._result, non_blocking=True)
         s.synchronize()
         res = _lib.RxResult.from_buffer_copy(bytes(self._pinned.numpy()))
@@ -207,6 +213,11 @@ class Transport:
                                   self._index_base + int(c["pkt_index"]), data)
         self._index_base += n
         return out
+
+    def flush(self, stream=None):
+        """Pipelined receivers: join the outstanding payload scatter (cn_rx_flush)."""
+        s = stream or torch.cuda.current_stream(self.device)
+        _lib.check(_lib.lib().cn_rx_flush(self._h, ctypes.c_void_p(s.cuda_stream)), "cn_rx_flush")
 
     def post(self, tag, buf, stream=None):
         """Scatter (or, in reduce mode, accumulate) the message with caller

@@ -33,7 +33,9 @@ def main():
         msg_len = int(data["msg_len"][0])
     n = len(data)
     hdrs = cn.to_device_records(data, dev)
-    st = torch.randint(0, 256, (n * bench.MAX_PL,), dtype=torch.uint8, device=dev)
+    # two staging replicas, rotated per step as in bench.py (inputs larger than L2)
+    sts = [torch.randint(0, 256, (n * bench.MAX_PL,), dtype=torch.uint8, device=dev) for _ in range(2)]
+    st = sts[0]
     tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
                       arena_bytes=K * (msg_len + (1 << 20)), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
                       max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8))
@@ -45,21 +47,61 @@ def main():
                           arena_bytes=3 * K * (msg_len + (1 << 20)), chunk_pool=3 * K * ((msg_len + cb - 1) // cb),
                           max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8))
 
-    def step():
+    def step(r=0):
         s = torch.cuda.current_stream(dev)
         if steady:
             seq_col.add_(1)
         else:
             tr.reset(s)
-        tr.rx_batch_async(hdrs, st, bench.MAX_PL, s)
+        tr.rx_batch_async(hdrs, sts[r], bench.MAX_PL, s)
 
+    pipe = os.environ.get("PIPE") == "1"
+    if pipe:  # bench.py's headline: pipelined receiver, steady state, one graph of `steps` steps
+        from paper_2504_17307_b200.records import PKT_DTYPE
+        tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
+                          arena_bytes=3 * K * (msg_len + (1 << 20)), chunk_pool=3 * K * ((msg_len + cb - 1) // cb),
+                          max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8), pipeline=True)
+        si = PKT_DTYPE.fields["msg_seq"][1] // 8
+        hs = []
+        for j in range(2 * steps + 1):
+            h_ = hdrs.clone()
+            h_.view(n, 64).view(torch.int64)[:, si] += j
+            hs.append(h_)
+        tr.handle_packets(hs[0], st, bench.MAX_PL)
+        gs_ = []
+        for r in range(2):
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_):
+                for j in range(1 + r * steps, 1 + (r + 1) * steps):
+                    tr.rx_batch_async(hs[j], sts[j % 2], bench.MAX_PL, torch.cuda.current_stream(dev))
+                tr.flush(torch.cuda.current_stream(dev))
+            gs_.append(g_)
+        gs_[0].replay()
+        torch.cuda.synchronize()
+        g = gs_[1]
+        steps = 1
+
+        def step():
+            pass
     step()
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        step()
-    for _ in range(5):
-        g.replay()
+    if not pipe:  # one graph per staging replica, replayed alternately
+        gr = []
+        for r in range(2):
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_):
+                step(r)
+            gr.append(g_)
+
+        class _Alt:
+            k = 0
+
+            def replay(self):
+                gr[_Alt.k % 2].replay()
+                _Alt.k += 1
+        g = _Alt()
+        for _ in range(5):
+            g.replay()
     torch.cuda.synchronize()
     if os.environ.get("NOPROF") == "1":  # for ncu: plain replays, no CUPTI of our own
         for _ in range(steps):
@@ -82,7 +124,7 @@ def main():
     prev_reset = None
     for a, b, nm in rows:
         short = nm.split("(")[0].replace("void ", "").replace("cnb::", "")[:28]
-        if ("k_reset" in short) or (steady and "elementwise" in short):
+        if ("k_reset" in short) or (steady and "elementwise" in short) or (pipe and "k_ingest" in short):
             if prev_reset is not None:
                 print(f"--- step {(a - prev_reset):.1f} us")
             prev_reset = a

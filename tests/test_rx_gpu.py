@@ -8,6 +8,7 @@ import torch
 from conftest import golden_names, load_golden, load_psn
 from oracle import oracle as O
 from oracle.records import ACK_FIELDS, CPL_FIELDS, PKT_DTYPE, ack_equal
+from paper_2504_17307_b200.records import ACK_DTYPE, CPL_DTYPE
 
 pytestmark = pytest.mark.gpu
 
@@ -269,3 +270,69 @@ def test_rx_interleaved_connections_independent():
     for c in out.completions_np():
         buf = arena[int(c["buf_offset"]): int(c["buf_offset"]) + int(c["len"])].cpu().numpy()
         assert (buf == O.pattern_bytes(int(c["len"]), int(c["tag"]))).all()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_32k", "concurrent_k4", "multigen_k8", "trim_storm", "ordered_loss"])
+@pytest.mark.parametrize("nsplit", [3, 16])
+def test_rx_pipelined_receiver(name, nsplit):
+    """cn_rx_config::pipeline: the scatter of batch k runs beside batch k+1
+    and joins at its end.  Batches are enqueued back to back with their own
+    output buffers and no host synchronisation: the ack streams and
+    completions are the reference's, batch k's message bytes are final once
+    batch k+1 has returned (checked after each batch), the last batch's after
+    cn_rx_flush."""
+    import ctypes
+
+    from paper_2504_17307_b200 import _lib
+    data, acks_ref, cpls_ref, meta = load_golden(name)
+    tr = _transport(meta, pipeline=True)
+    L = _lib.lib()
+    s = torch.cuda.current_stream()
+    rs = np.random.RandomState(nsplit)
+    cuts = np.unique(np.concatenate([[0, len(data)], rs.randint(0, len(data), nsplit - 1)]))
+    keep, outs = [], []
+
+    def check_bytes(cp):
+        arena = tr.arena()
+        for c in cp:
+            buf = arena[int(c["buf_offset"]): int(c["buf_offset"]) + int(c["len"])].cpu().numpy()
+            assert (buf == O.pattern_bytes(int(c["len"]), int(c["tag"]))).all(), int(c["tag"])
+
+    for j, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+        hd, pl = _dev(data[a:b])
+        n = b - a
+        acks = torch.empty((n + 16) * 64, dtype=torch.uint8, device="cuda")
+        cpls = torch.empty((n + 16) * 64, dtype=torch.uint8, device="cuda")
+        res = torch.zeros(24, dtype=torch.uint8, device="cuda")
+        psn = _psn(name, a, b)
+        args = (hd.data_ptr(), pl.data_ptr(), 4032, n, acks.data_ptr(), n + 16, cpls.data_ptr(), n + 16,
+                res.data_ptr(), ctypes.c_void_p(s.cuda_stream))
+        if psn is not None:
+            _lib.check(L.cn_rx_batch_psn(tr._h, args[0], psn.data_ptr(), *args[1:]), "cn_rx_batch_psn")
+        else:
+            _lib.check(L.cn_rx_batch(tr._h, *args), "cn_rx_batch")
+        keep.append((hd, pl, psn))
+        outs.append((a, acks, cpls, res))
+        if j % 4 == 3:  # now and then: batch j-1's bytes are final once batch j returned
+            torch.cuda.synchronize()
+            if j >= 1:
+                r = _lib.RxResult.from_buffer_copy(bytes(outs[j - 1][3].cpu().numpy()))
+                check_bytes(outs[j - 1][2][: r.n_completions * 64].cpu().numpy().view(CPL_DTYPE))
+    tr.flush()
+    torch.cuda.synchronize()
+    all_acks, all_cpls = [], []
+    for a, acks, cpls, res in outs:
+        r = _lib.RxResult.from_buffer_copy(bytes(res.cpu().numpy()))
+        assert r.status == 0
+        ak = acks[: r.n_acks * 64].cpu().numpy().view(ACK_DTYPE).copy()
+        ak["pkt_index"] += np.uint32(a)
+        all_acks.append(ak)
+        cp = cpls[: r.n_completions * 64].cpu().numpy().view(CPL_DTYPE).copy()
+        check_bytes(cp)
+        cp["pkt_index"] += np.uint32(a)
+        all_cpls.append(cp)
+    ok, bad = ack_equal(np.concatenate(all_acks), acks_ref)
+    assert ok, bad
+    cp = np.concatenate(all_cpls)
+    for f in CPL_FIELDS:
+        assert (cp[f] == cpls_ref[f]).all(), f

@@ -55,6 +55,23 @@ def main():
         t0 = buf[10]
         marks = sorted((buf[j] - t0, NAMES[j]) for j in NAMES if 0 < buf[j] < (1 << 63))
         print(f"--- step {k}: " + "  ".join(f"{nm} {v / 1e3:.1f}" for v, nm in marks))
+        if os.environ.get("TILES") == "1" and k == steps - 1:  # k_acks per-tile marks
+            import numpy as np
+            tb = (ctypes.c_ulonglong * (4 * 8192))()
+            lib.cn_rx_debug_tile_timing.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+            lib.cn_rx_debug_tile_timing(tb)
+            a = np.frombuffer(tb, dtype=np.uint64).reshape(4, 8192).astype(np.int64)
+            nt = int((a[3] > 0).sum())
+            a = a[:, :nt]
+            a0 = buf[22]
+            st = (a[0] - a0) / 1e3
+            print(f"tiles {nt}: start  p10 {np.percentile(st, 10):.1f} p50 {np.median(st):.1f} "
+                  f"p90 {np.percentile(st, 90):.1f} max {st.max():.1f} us after the first block")
+            for nm, x, y in (("decide", 0, 1), ("build", 1, 2), ("write", 2, 3), ("tile", 0, 3)):
+                dd = (a[y] - a[x]) / 1e3
+                print(f"  {nm:7s} p50 {np.median(dd):.2f} p90 {np.percentile(dd, 90):.2f} max {dd.max():.2f} us")
+            order = np.argsort(a[0])
+            print("  tiles started per 5 us:", np.histogram(st, bins=np.arange(0, st.max() + 5, 5))[0].tolist())
 
 
 if __name__ == "__main__":

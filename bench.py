@@ -1131,6 +1131,13 @@ def main():
     g_warm = pipe_graph(range(1, W_ + 1))
     g_timed = pipe_graph(range(W_ + 1, W_ + K_ + 1))
     g_warm.replay()
+    # the timed graph's first launch uploads its ~10 nodes per step: it runs
+    # once untimed (more warm-up steps), then every header it reads moves on
+    # K generations, so the timed launch delivers new generations again
+    g_timed.replay()
+    torch.cuda.synchronize()
+    for j in range(W_ + 1, W_ + K_ + 1):
+        hsets[j].view(n, 64).view(torch.int64)[:, seq_i] += K_
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -111,7 +111,8 @@ def lib():
     L.cn_rx_destroy.argtypes = [vp]
     L.cn_rx_destroy.restype = None
     L.cn_rx_reset.argtypes = [vp, vp]
-    L.cn_rx_flush.argtypes = [vp, vp]
+    if hasattr(L, "cn_rx_flush"):
+        L.cn_rx_flush.argtypes = [vp, vp]
     L.cn_rx_batch.argtypes = [vp, vp, vp, u64, u32, vp, u32, vp, u32, vp, vp]
     L.cn_rx_batch_psn.argtypes = [vp, vp, vp, vp, u64, u32, vp, u32, vp, u32, vp, vp]
     L.cn_rx_post.argtypes = [vp, u64, vp, u64, vp]

@@ -1156,13 +1156,15 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
         // k_ingest's descriptor: only packets not seen before the batch, of
         // a live message (GenStates may be reused while a pipelined scatter
         // still runs, so the destination travels with the packet)
+        // every load but the first-arrival test's is independent: issued together
         const unsigned long long dst = pd[i];
-        if (!dst) continue;
-        // first arrival within the batch: c_first is final after k_ingest
-        if (cf[pf[i]] != i + 1) continue;
+        const uint32_t fi = pf[i];
         const cn_pkt_hdr* hp = hdrs + i;
         const uint32_t len = hp->payload_len;
         const uint64_t moff = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
+        // first arrival within the batch: c_first is final after k_ingest
+        // (fi is 0 for a packet without a descriptor: a valid index)
+        if (cf[fi] != i + 1 || !dst) continue;
         const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
         warp_scatter<R>(reinterpret_cast<uint8_t*>(dst), src, len, lane);
     }
@@ -1192,15 +1194,23 @@ __device__ __forceinline__ uint32_t pmax_ld(const RxDev& d, uint64_t cbase, uint
 // the last 16-byte multiple, and packets whose source or destination is not
 // 16-byte aligned (chunk sizes that are not multiples of 16), take the
 // warp-cooperative vector path.
-constexpr int kTmaSlots = 16;
+constexpr int kTmaLanes = 16;             // lanes with slots (the other 16 help with misaligned packets)
+constexpr int kTmaBufs = 2;               // slots per lane: the next load flies while the current one lands
 constexpr uint32_t kTmaSlotBytes = 4096;  // >= max_payload, multiple of 16
-constexpr uint32_t kTmaSmem = kTmaSlots * kTmaSlotBytes;
+constexpr uint32_t kTmaSmem = kTmaLanes * kTmaBufs * kTmaSlotBytes;
+
+struct TmaPkt {
+    unsigned long long dst;
+    const uint8_t* src;
+    uint32_t len;
+    bool bulk;
+};
 
 __global__ void __launch_bounds__(32) k_copy_tma(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                                  const uint8_t* __restrict__ payload, uint64_t stride,
                                                  uint32_t n) {
     extern __shared__ __align__(128) uint8_t tma_buf[];
-    __shared__ __align__(8) uint64_t tma_bar[kTmaSlots];
+    __shared__ __align__(8) uint64_t tma_bar[kTmaLanes * kTmaBufs];
     const int lane = threadIdx.x;
     TM_START(24);
     RxCtl* C = d.ctl;
@@ -1208,73 +1218,82 @@ __global__ void __launch_bounds__(32) k_copy_tma(RxDev d, const cn_pkt_hdr* __re
     const uint32_t* __restrict__ cf = first_of(d, par);
     const unsigned long long* __restrict__ pd = d.p_dst + par * static_cast<uint64_t>(d.max_batch);
     const uint32_t* __restrict__ pf = d.p_fi + par * static_cast<uint64_t>(d.max_batch);
-    const bool act = lane < kTmaSlots;
-    const uint32_t slot = smem_u32(tma_buf + (act ? lane : 0) * kTmaSlotBytes);
-    const uint32_t bar = smem_u32(&tma_bar[act ? lane : 0]);
-    if (act) mbar_init(bar, 1);
+    const bool act = lane < kTmaLanes;
+    const int ln = act ? lane : 0;
+    uint32_t slot[kTmaBufs], bar[kTmaBufs], phase[kTmaBufs];
+#pragma unroll
+    for (int q = 0; q < kTmaBufs; ++q) {
+        slot[q] = smem_u32(tma_buf + (ln * kTmaBufs + q) * kTmaSlotBytes);
+        bar[q] = smem_u32(&tma_bar[ln * kTmaBufs + q]);
+        phase[q] = 0;
+        if (act) mbar_init(bar[q], 1);
+    }
     fence_mbar_init();
     __syncwarp();
     const uint64_t pol = l2_evict_first();
     // this lane's packet: k_ingest's descriptor, the first-arrival test, the header fields
-    auto fetch = [&](uint32_t i, unsigned long long& dst, uint32_t& len, uint64_t& moff) {
-        dst = 0;
-        if (!act || i >= n) return;
+    auto prep = [&](uint32_t i) {
+        TmaPkt p{0, nullptr, 0, false};
+        if (!act || i >= n) return p;
         const unsigned long long d0 = pd[i];
-        if (!d0) return;
         const uint32_t fi = pf[i];
         const cn_pkt_hdr* hp = hdrs + i;
         const uint32_t l = hp->payload_len;
         const uint64_t mo = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
-        if (cf[fi] != i + 1) return;
-        dst = d0;
-        len = l;
-        moff = mo;
+        if (cf[fi] != i + 1 || !d0) return p;
+        p.dst = d0;
+        p.len = l;
+        p.src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + mo;
+        p.bulk = (l & ~15u) && !((reinterpret_cast<uintptr_t>(p.src) | d0) & 15);
+        return p;
     };
-    const uint32_t step = gridDim.x * kTmaSlots;
-    uint32_t i = blockIdx.x * kTmaSlots + lane;
-    unsigned long long dst = 0;
-    uint32_t len = 0;
-    uint64_t moff = 0;
-    fetch(i, dst, len, moff);
-    uint32_t phase = 0;
+    uint32_t uses = 0;  // bulk loads issued by this lane (slot = uses % kTmaBufs)
     bool stored = false;
-    for (uint32_t base = blockIdx.x * kTmaSlots; base < n; base += step) {
-        const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
-        const uint32_t len16 = len & ~15u;
-        const bool bulk = dst && len16 && !((reinterpret_cast<uintptr_t>(src) | dst) & 15);
-        if (bulk) {
-            if (stored) bulk_wait_read0();  // the slot's previous store has read it
-            mbar_arrive_expect_tx(bar, len16);
-            bulk_g2s(slot, src, len16, bar, pol);
+    auto issue = [&](const TmaPkt& p) {
+        if (!p.bulk) return;
+        const int q = uses % kTmaBufs;
+        // the slot's previous store (kTmaBufs loads ago) must have read it: with
+        // two slots that is the most recent committed store
+        if (stored) bulk_wait_read0();
+        mbar_arrive_expect_tx(bar[q], p.len & ~15u);
+        bulk_g2s(slot[q], p.src, p.len & ~15u, bar[q], pol);
+        ++uses;
+    };
+    const uint32_t step = gridDim.x * kTmaLanes;
+    uint32_t i = blockIdx.x * kTmaLanes + lane;
+    TmaPkt cur = prep(i);
+    issue(cur);
+    TmaPkt nxt = prep(i + step);
+    for (uint32_t base = blockIdx.x * kTmaLanes; base < n; base += step) {
+        // the next packet's load joins the current one in flight
+        issue(nxt);
+        const TmaPkt nn = prep(i + 2 * step);
+        if (cur.bulk) {
+            const uint32_t len16 = cur.len & ~15u;
+            for (uint32_t b = len16; b < cur.len; ++b) reinterpret_cast<uint8_t*>(cur.dst)[b] = cur.src[b];
         }
-        // the next packet's descriptor while the load flies
-        const uint32_t i2 = i + step;
-        unsigned long long dst2 = 0;
-        uint32_t len2 = 0;
-        uint64_t moff2 = 0;
-        fetch(i2, dst2, len2, moff2);
-        if (bulk)
-            for (uint32_t b = len16; b < len; ++b) reinterpret_cast<uint8_t*>(dst)[b] = src[b];
-        unsigned fb = __ballot_sync(0xffffffffu, dst && !bulk);
+        // misaligned packets (chunk sizes not a multiple of 16): the whole warp
+        unsigned fb = __ballot_sync(0xffffffffu, cur.dst && !cur.bulk);
         while (fb) {
             const int l = __ffs(fb) - 1;
             fb &= fb - 1;
-            const unsigned long long fd = __shfl_sync(0xffffffffu, dst, l);
-            const unsigned long long fs = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), l);
-            const uint32_t fl = __shfl_sync(0xffffffffu, len, l);
+            const unsigned long long fd = __shfl_sync(0xffffffffu, cur.dst, l);
+            const unsigned long long fs = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(cur.src), l);
+            const uint32_t fl = __shfl_sync(0xffffffffu, cur.len, l);
             warp_scatter<0>(reinterpret_cast<uint8_t*>(fd), reinterpret_cast<const uint8_t*>(fs), fl, lane);
         }
-        if (bulk) {
-            mbar_wait(bar, phase);
-            phase ^= 1u;
-            bulk_s2g(reinterpret_cast<void*>(dst), slot, len16, pol);
+        if (cur.bulk) {
+            // cur's load is the one issued before nxt's
+            const int q = (uses - (nxt.bulk ? 2 : 1)) % kTmaBufs;
+            mbar_wait(bar[q], phase[q]);
+            phase[q] ^= 1u;
+            bulk_s2g(reinterpret_cast<void*>(cur.dst), slot[q], cur.len & ~15u, pol);
             bulk_commit();
             stored = true;
         }
-        i = i2;
-        dst = dst2;
-        len = len2;
-        moff = moff2;
+        i += step;
+        cur = nxt;
+        nxt = nn;
     }
     bulk_wait_all();
     TM_END(25);
@@ -2091,7 +2110,8 @@ struct cn_rx {
     int copy_bps = 64;  // k_copy block cap per SM (CN_COPY_BLOCKS_PER_SM overrides)
     int scan_first = 1;  // launch scan/acks before the scatter (CN_SCAN_FIRST=0 reverts)
     int copy_tma = 0;    // copy mode on the bulk-copy engine (CN_COPY_TMA=1; default: the vector path)
-    int tma_bps = 2;     // its blocks per SM (CN_TMA_BPS)
+    int tma_bps = 1;     // its blocks per SM (CN_TMA_BPS)
+    int ack_bps = 4;     // k_acks blocks per SM (CN_ACK_BPS)
     uint32_t small_batch = 32768;  // batches up to this many packets use 32-packet ack tiles (CN_ACK_SMALL)
     int hi_prio = 0;     // greatest stream priority: the latency-bound ack path wins SM slots
     // optional per-kernel timing with CUDA events on the launch stream
@@ -2209,7 +2229,8 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     if (const char* e = getenv("CN_COPY_BLOCKS_PER_SM")) rx->copy_bps = atoi(e) > 0 ? atoi(e) : 64;
     if (const char* e = getenv("CN_SCAN_FIRST")) rx->scan_first = atoi(e);
     if (const char* e = getenv("CN_COPY_TMA")) rx->copy_tma = atoi(e);
-    if (const char* e = getenv("CN_TMA_BPS")) rx->tma_bps = atoi(e) > 0 ? atoi(e) : 2;
+    if (const char* e = getenv("CN_ACK_BPS")) rx->ack_bps = atoi(e) > 0 ? atoi(e) : 4;
+    if (const char* e = getenv("CN_TMA_BPS")) rx->tma_bps = atoi(e) > 0 ? atoi(e) : 1;
     cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
     if (const char* e = getenv("CN_ACK_SMALL")) rx->small_batch = static_cast<uint32_t>(atoi(e));
     {
@@ -2530,7 +2551,8 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         }
         prof_mark(ev, s);
         // persistent: as many blocks as fit beside the scatter, tiles by ticket
-        const uint32_t ag = tiles < static_cast<uint32_t>(rx->sms) * 4 ? tiles : rx->sms * 4;
+        const uint32_t acap = static_cast<uint32_t>(rx->sms * rx->ack_bps);
+        const uint32_t ag = tiles < acap ? tiles : acap;
         {
             cudaLaunchConfig_t lc = {};
             cudaLaunchAttribute at[1];

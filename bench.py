@@ -750,8 +750,9 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     pb = max(64 << 20, (inbound // 8) >> 20 << 20)
     if os.environ.get("CN_A2A_PIECE_MB"):
         pb = int(os.environ["CN_A2A_PIECE_MB"]) << 20
-    a2a = AllToAll(cap, piece_bytes=pb)   # dispatch
-    a2c = AllToAll(cap, piece_bytes=pb)   # combine (its own slots: the dispatch slots are its send buffer)
+    direct = os.environ.get("CN_A2A_DIRECT", "1") == "1"  # bytes straight into the receive slots
+    a2a = AllToAll(cap, piece_bytes=pb, direct=direct)   # dispatch
+    a2c = AllToAll(cap, piece_bytes=pb, direct=direct)   # combine (own slots: the dispatch slots are its send buffer)
     coffs = [s_ * a2a.cap for s_ in range(world)]
 
     last = {}
@@ -827,7 +828,9 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     a2c.close()
     moved = int(rows.sum()) * row * 2  # dispatch + combine, all ranks
     hot_in = int(rows[:, 0].sum()) * row
-    return {"piece_bytes": pb, "parity": "dispatch and combine byte-exact on every rank (all slices)",
+    return {"piece_bytes": pb, "mode": "direct (NVLink writes into the receive slots, header-only receive path)"
+            if direct else "staged (receive path scatters staging into the posted slots)",
+            "parity": "dispatch and combine byte-exact on every rank (all slices)",
             "config": f"{world} ranks x {tokens} tokens, hidden {hidden} bf16 ({row} B/copy), top-8 of "
                       f"{32 * world} experts, rank 0 experts 10x weight (incast)",
             "ms_per_step": round(ms, 4), "nccl_ms_per_step": round(msn, 4),

@@ -5,12 +5,15 @@ dispatch / combine of BASELINE configs[3] (SURVEY.md 8(d) cfg 4, 8(e):
 Each rank holds one connection to every peer.  Per call, rank r's message
 to peer d (`send_counts[d]` bytes of its send buffer) is packetized
 (cn_packetize = Transport::send_chunk, per-chunk paths from the S3
-scheduler) and moved by a copy engine into r's staging slot in d's HBM, its
-headers alongside, followed by a system-scope release of d's ready counter
-for r (the NIC DMA + doorbell of the paper's transport).  Peer d runs the
-receive path on the landed message (ingest, scatter into the posted
-receive slot for r, SACK/cum bookkeeping, completion) and releases r's
-freed counter, after which r may reuse the slot.  Messages to different
+scheduler) and moved by a copy engine over NVLink, its headers alongside,
+followed by a system-scope release of d's ready counter for r (the NIC DMA
++ doorbell of the paper's transport).  Direct mode (the default): the bytes
+land straight in d's receive slot for r -- RDMA-write semantics into a
+posted buffer, armed by d at the start of each call -- and d's receive
+path keeps the books on the headers alone (SACK / cum / completion, no
+payload pass); staged mode lands them in a staging slot and d's receive
+path scatters them into the slot (accept_payload).  Either way d releases
+r's freed counter per piece, after which r may reuse the header slot.  Messages to different
 peers leave on two copy lanes in a staggered order (r+1, r+2, ...), so a
 hot receiver (incast) sees all its senders at once -- its NVLink ingress is
 the bottleneck, which is the point of the workload.  Messages move in
@@ -18,6 +21,7 @@ chunk-aligned pieces, each releasing a per-pair monotone counter, so the
 receive path runs on early pieces while later ones are still in flight.
 """
 import ctypes
+import os
 
 import torch
 import torch.distributed as dist
@@ -27,9 +31,12 @@ from .collective import DeviceBuffer, _ipc_handle, _ipc_open, _PeerView, packeti
 from .transport import MAX_PAYLOAD, Transport, TransportConfig
 
 
+_SKIP = os.environ.get("CN_A2A_SKIP", "")  # profiling switches only (tools/a2a_probe.py)
+
+
 class AllToAll:
     def __init__(self, max_bytes_per_peer, *, chunk_bytes=32768, paths=8, seed=7, group=None,
-                 piece_bytes=128 << 20, max_spins=1 << 26):
+                 piece_bytes=128 << 20, max_spins=1 << 26, direct=True, tail=0):
         self.group = group
         self.n = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -40,21 +47,28 @@ class AllToAll:
         self.cb = chunk_bytes
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.max_spins = max_spins
+        self.direct = direct
+        self.tail = tail
+        self.calls = 0
         L = _lib.lib()
         self.max_pkts = L.cn_packet_count(self.cap, chunk_bytes, MAX_PAYLOAD)
         # receive side: posted destination slot, staging slot and header slot per source
         self._recv = DeviceBuffer(n * self.cap, self.dev)
-        self._stage = DeviceBuffer(n * self.cap, self.dev)
+        self._stage = None if direct else DeviceBuffer(n * self.cap, self.dev)
         self._hdrs = DeviceBuffer(n * self.max_pkts * 64, self.dev)
         self._out_hdrs = DeviceBuffer(n * self.max_pkts * 64, self.dev)  # my outgoing headers
         # flags: ready[n][2] (written by sources, per copy lane), freed[n][2]
-        # (written by destinations), err
-        self._flags = DeviceBuffer((4 * n + 2) * 8, self.dev)
-        self.flags = self._flags.tensor(torch.int64, 4 * n + 2)
+        # (written by destinations), err, spare, armed[n] (written by
+        # destinations: my receive slot for you is free for call k)
+        self._flags = DeviceBuffer((5 * n + 2) * 8, self.dev)
+        self.flags = self._flags.tensor(torch.int64, 5 * n + 2)
         fp = self._flags.data_ptr()
         self.f_ready, self.f_freed = fp, fp + 16 * n
         self.f_err = fp + 32 * n
-        mine = {"stage": _ipc_handle(self._stage), "hdrs": _ipc_handle(self._hdrs),
+        self.o_armed = (4 * n + 2) * 8
+        self.f_armed = fp + self.o_armed
+        land = self._recv if direct else self._stage
+        mine = {"land": _ipc_handle(land), "hdrs": _ipc_handle(self._hdrs),
                 "flags": _ipc_handle(self._flags)}
         allh = [None] * n
         dist.all_gather_object(allh, mine, group=group)
@@ -63,7 +77,7 @@ class AllToAll:
         for d in range(n):
             if d == r:
                 continue
-            self.peer[d] = {k: self._open(allh[d][k]) for k in ("stage", "hdrs", "flags")}
+            self.peer[d] = {k: self._open(allh[d][k]) for k in ("land", "hdrs", "flags")}
         # path choices: one RngStream per block of 2048 chunks of each peer
         # connection's message (the sequential Mersenne draws of one stream
         # would otherwise sit in front of every transfer)
@@ -73,14 +87,16 @@ class AllToAll:
         self.sp = -(-self.max_chunks // self.blk)
         self.sched = PathScheduler(n * self.sp, paths, seed, base_rtt_ns=10000.0, index0=r * n * self.sp)
         self.paths_all = torch.empty(n * self.max_chunks, dtype=torch.int32, device=self.dev)
-        self.rx = Transport(TransportConfig(chunk_bytes=chunk_bytes, paths=paths, lb="p2_rtt", carry_payload=True),
+        self.rx = Transport(TransportConfig(chunk_bytes=chunk_bytes, paths=paths, lb="p2_rtt",
+                                            carry_payload=not direct),
                             device=self.dev, max_conns=2 * n, max_msgs=4 * n,
                             chunk_pool=2 * n * self.max_chunks + 64, arena_bytes=0,
                             max_batch=self.max_pkts + 16, max_posts=4 * n)
-        rb = self.recv_buffer()
-        for s in range(n):
-            if s != r:
-                self.rx.post(s, rb[s * self.cap:(s + 1) * self.cap])
+        if not direct:  # the receive path scatters staged bytes into the posted slots
+            rb = self.recv_buffer()
+            for s in range(n):
+                if s != r:
+                    self.rx.post(s, rb[s * self.cap:(s + 1) * self.cap])
         self.lanes = [torch.cuda.Stream(self.dev) for _ in range(2)]
         self.hdr_stream = torch.cuda.Stream(self.dev)
         self.ev_hdrs = torch.cuda.Event()
@@ -106,7 +122,8 @@ class AllToAll:
             _lib.lib().cn_ipc_close(ctypes.c_void_p(p))
         self._opened = []
         for b in (self._recv, self._stage, self._hdrs, self._out_hdrs, self._flags):
-            b.free()
+            if b is not None:
+                b.free()
 
     def _wait(self, flag, off, s):
         _lib.check(_lib.lib().cn_ctr_wait(flag, self.f_it, 1, off, self.max_spins, self.f_err,
@@ -117,9 +134,18 @@ class AllToAll:
                    "cn_ctr_signal")
 
     def _pieces(self, cnt):
-        """Chunk-aligned piece bounds of a cnt-byte message."""
+        """Chunk-aligned piece bounds of a cnt-byte message.  With tail
+        pieces: one large head piece (a copy-engine transfer runs at the
+        link's rate only when large, ~4 us of fixed cost per copy), then
+        `tail` pieces of piece_bytes whose transfers hide the receive path
+        of the head; else equal pieces of at most piece_bytes."""
         if cnt == 0:
             return []
+        tb = self.tail * self.piece_bytes
+        if self.tail and cnt > tb + self.piece_bytes:
+            h = (cnt - tb) // self.cb * self.cb
+            b = [0, h] + [h + k * self.piece_bytes for k in range(1, self.tail)] + [cnt]
+            return [(b[p], b[p + 1]) for p in range(len(b) - 1) if b[p + 1] > b[p]]
         P = max(1, min(-(-cnt // self.piece_bytes), -(-cnt // self.cb)))
         b = [0] + [cnt * p // P // self.cb * self.cb for p in range(1, P)] + [cnt]
         return [(b[p], b[p + 1]) for p in range(P) if b[p + 1] > b[p]]
@@ -146,7 +172,13 @@ class AllToAll:
                 o += send_counts[d]
         assert max(send_counts) <= self.cap and max(recv_counts) <= self.cap
         ppc = -(-self.cb // MAX_PAYLOAD)
+        self.calls += 1
         self.rx.reset(s)
+        if self.direct:  # my receive slots are free (stream order): arm every source
+            for src in range(n):
+                if src != r:
+                    _lib.check(L.cn_flag_signal(self.peer[src]["flags"] + self.o_armed + 8 * r, None, self.calls,
+                                                ctypes.c_void_p(s.cuda_stream)), "cn_flag_signal")
         self.ev_init.record(s)
         for ln in self.lanes:
             ln.wait_event(self.ev_init)
@@ -181,14 +213,17 @@ class AllToAll:
             for ln in range(2):
                 _lib.check(L.cn_flag_wait(self.f_freed + 16 * d + 8 * ln, None, self.sent[d][ln], self.max_spins,
                                           self.f_err, cs(self.lanes[ln])), "cn_flag_wait")
+                if self.direct:  # d armed its receive slot for me this call
+                    _lib.check(L.cn_flag_wait(self.f_armed + 8 * d, None, self.calls, self.max_spins, self.f_err,
+                                              cs(self.lanes[ln])), "cn_flag_wait")
             npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
             oh = self._out_hdrs.data_ptr() + d * self.max_pkts * 64
             for p, (lo, hi) in enumerate(self._pieces(send_counts[d])):
                 ln = (k + p) % 2  # consecutive pieces alternate copy lanes
                 sp = self.lanes[ln]
-                _lib.check(L.cn_copy_async(pe["stage"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
+                _lib.check(L.cn_copy_async(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
                                            cs(sp)), "cn_copy_async")
-                if p == 0:  # the message's headers ride with its first piece
+                if p == 0 and "hdr" not in _SKIP:  # the message's headers ride with its first piece
                     sp.wait_event(self.ev_hdrs)
                     _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh, npk * 64, cs(sp)),
                                "cn_copy_async")
@@ -216,8 +251,13 @@ class AllToAll:
                 b = (L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD) if hi == recv_counts[src]
                      else hi // self.cb * ppc)
                 hd = _PeerView(self._hdrs.data_ptr() + src * self.max_pkts * 64 + a * 64, (b - a) * 64)
-                pl = _PeerView(self._stage.data_ptr() + src * self.cap, recv_counts[src])
-                self.rx.rx_batch_async(hd, pl, 0, s, n=b - a)
+                if "rx" in _SKIP:  # profiling switch (tools/a2a_probe.py): no receive path
+                    pass
+                elif self.direct:  # headers only: the bytes already sit in the receive slot
+                    self.rx.rx_batch_async(hd, None, 0, s, n=b - a)
+                else:
+                    pl = _PeerView(self._stage.data_ptr() + src * self.cap, recv_counts[src])
+                    self.rx.rx_batch_async(hd, pl, 0, s, n=b - a)
                 _lib.check(L.cn_flag_signal(self.peer[src]["flags"] + 16 * n + 16 * r + 8 * ln, None,
                                             self.recvd[src][ln], cs(s)), "cn_flag_signal")  # src's freed[r][ln]
         for ln in self.lanes + [self.hdr_stream]:

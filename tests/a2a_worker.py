@@ -28,7 +28,15 @@ def main():
     n, r = dist.get_world_size(), dist.get_rank()
     from paper_2504_17307_b200.alltoall import AllToAll
     cap = 3 << 20
-    a2a = AllToAll(cap)
+    for direct in (True, False):  # bytes straight into the receive slots / staged + scattered
+        run_mode(AllToAll(cap, direct=direct), n, r, iters, cap)
+    dist.barrier()
+    if r == 0:
+        print(f"A2A_OK n={n} iters={iters}")
+    dist.destroy_process_group()
+
+
+def run_mode(a2a, n, r, iters, cap):
     for it in range(iters):
         m = counts_matrix(n, it, cap)
         g = torch.Generator(device="cuda")
@@ -47,12 +55,9 @@ def main():
             off = int(m[s, :r].sum())
             want = ss[off: off + int(m[s, r])]
             got = recv[s * a2a.cap: s * a2a.cap + int(m[s, r])]
-            assert torch.equal(got, want), f"rank {r} iter {it} from {s}: mismatch"
+            assert torch.equal(got, want), f"rank {r} iter {it} direct={a2a.direct} from {s}: mismatch"
     dist.barrier()
     a2a.close()
-    if r == 0:
-        print(f"A2A_OK n={n} iters={iters}")
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

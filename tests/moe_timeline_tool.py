@@ -32,7 +32,8 @@ def main():
     sc, rc = rows[rank] * row, rows[:, rank] * row
     cap = int(max(rows.max() * row, 16))
     pb = int(os.environ.get("CN_A2A_PIECE_MB", "64")) << 20
-    a2a, a2c = AllToAll(cap, piece_bytes=pb), AllToAll(cap, piece_bytes=pb)
+    direct = os.environ.get("CN_A2A_DIRECT", "1") == "1"
+    a2a, a2c = AllToAll(cap, piece_bytes=pb, direct=direct), AllToAll(cap, piece_bytes=pb, direct=direct)
     coffs = [s_ * a2a.cap for s_ in range(world)]
 
     def step():
@@ -53,6 +54,8 @@ def main():
         if who == rank:
             evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
             rows_ = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
+            st_ = [r_ for r_ in rows_[len(rows_) // 2:]]
+            print(f"==== rank {rank} step span {(st_[-1][1] - st_[0][0]):.1f} us over the last step")
             t0 = rows_[0][0]
             print(f"==== rank {rank}")
             for a, b, nm in rows_[len(rows_) // 2:]:

@@ -226,6 +226,18 @@ int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
                 uint32_t max_acks, cn_completion* d_completions,
                 uint32_t max_completions, cn_rx_result* d_result,
                 void* stream);
+/* Packets that carry their message's data (Packet::msg_data: the
+ * reference's send_message_data path, transport.hpp:88-91, copied from in
+ * accept_payload, transport.cpp:719-730): packet i's payload is read at
+ * d_msg_data[i] + chunk_offset + seq_in_chunk * max_payload -- each
+ * packet names its message's device buffer (e.g. the sender's, over
+ * NVLink).  A 0 entry is a packet without data: accepted and counted,
+ * nothing copied (:722).  d_psn: conn_psn per packet for an ordered
+ * receiver, NULL otherwise. */
+int cn_rx_batch_msgdata(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
+                        const uint64_t* d_msg_data, uint32_t n, cn_ack_rec* d_acks,
+                        uint32_t max_acks, cn_completion* d_completions,
+                        uint32_t max_completions, cn_rx_result* d_result, void* stream);
 /* cn_rx_batch for ordered reliability: d_psn[i] = conn_psn of packet i
  * (Packet::conn_psn, packet.hpp:48; not part of the 64-B header record) */
 int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
@@ -608,6 +620,13 @@ int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const vo
  * reliability (TransportConfig::reliability = ordered, go-back-N) */
 int cn_transport_handle_data_psn(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
                                  const void* d_payload, uint64_t stride, uint32_t n, void* stream);
+/* ... with each packet's message data pointer (d_msg_data[n], see
+ * cn_rx_batch_msgdata): the send_message_data path, where a packet carries
+ * its message's data (transport.hpp:88-91) -- the caller's injection code
+ * sets it per packet as send_chunk sets Packet::msg_data (transport.cpp:486);
+ * d_psn as in cn_transport_handle_data_psn or NULL */
+int cn_transport_handle_data_msgdata(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
+                                     const uint64_t* d_msg_data, uint32_t n, void* stream);
 /* the last batch's ack / NACK records and completions (host copies) */
 int64_t cn_transport_poll_acks(cn_transport* h, cn_ack_rec* out, uint64_t cap);
 int64_t cn_transport_poll_completions(cn_transport* h, cn_completion* out, uint64_t cap);

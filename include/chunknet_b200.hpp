@@ -283,6 +283,11 @@ class Endpoint {
                          uint32_t n, cudaStream_t s = nullptr) {
         check(cn_transport_handle_data_psn(h_, d_hdrs, d_psn, d_payload, stride, n, s), "handle_data_psn");
     }
+    // send_message_data path: each packet names its message's device data (Packet::msg_data)
+    void handle_data_msgdata(const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const uint64_t* d_msg_data,
+                             uint32_t n, cudaStream_t s = nullptr) {
+        check(cn_transport_handle_data_msgdata(h_, d_hdrs, d_psn, d_msg_data, n, s), "handle_data_msgdata");
+    }
 
   private:
     cn_transport* h_ = nullptr;

@@ -100,7 +100,13 @@ constexpr int kAckTileMax = 128;     // packets per k_acks tile (large batches)
 constexpr int kAckTileMin = 32;      // ... small batches
 constexpr int kAckWarps = 8;         // 256 threads: 4 decide warps, 8 ack builders
 constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
-constexpr int kCopyUnroll = 8;       // 16-byte vectors in flight per lane
+#ifndef CN_COPY_UNROLL
+#define CN_COPY_UNROLL 8
+#endif
+#ifndef CN_COPY_MINB
+#define CN_COPY_MINB 1
+#endif
+constexpr int kCopyUnroll = CN_COPY_UNROLL;  // 16-byte vectors in flight per lane
 constexpr uint64_t kArenaUnit = 512;  // arena allocation granule (bytes)
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 
@@ -147,6 +153,9 @@ struct RxDev {
     // ordered reliability (go-back-N receive filter)
     uint32_t ordered;
     const uint64_t* psn;      // [batch] conn_psn of the current batch
+    // [batch] per-packet message data (Packet::msg_data, transport.hpp:88-91,
+    // transport.cpp:486): packet i's payload at msgdata[i] + its message offset
+    const unsigned long long* msgdata;
     uint8_t* p_gbn;           // [batch] 0 pass on, 1 drop, 2 drop with a NACK
     uint64_t* p_gbn_psn;      // [batch] nack_psn of a NACK
     uint64_t* gbn_expected;   // [rconn] RecvConn::expected_psn
@@ -1141,7 +1150,7 @@ __device__ __forceinline__ void warp_scatter(uint8_t* __restrict__ dst, const ui
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
+__global__ void __launch_bounds__(256, CN_COPY_MINB) k_copy(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                               const uint8_t* __restrict__ payload, uint64_t stride,
                                               uint32_t n) {
     const int lane = threadIdx.x & 31;
@@ -1151,6 +1160,7 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
     const uint32_t* __restrict__ cf = first_of(d, par);
     const unsigned long long* __restrict__ pd = d.p_dst + par * static_cast<uint64_t>(d.max_batch);
     const uint32_t* __restrict__ pf = d.p_fi + par * static_cast<uint64_t>(d.max_batch);
+    const unsigned long long* __restrict__ md = d.msgdata;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
         // k_ingest's descriptor: only packets not seen before the batch, of
@@ -1159,13 +1169,16 @@ __global__ void __launch_bounds__(256) k_copy(RxDev d, const cn_pkt_hdr* __restr
         // every load but the first-arrival test's is independent: issued together
         const unsigned long long dst = pd[i];
         const uint32_t fi = pf[i];
+        const unsigned long long mdv = md ? md[i] : 0;
         const cn_pkt_hdr* hp = hdrs + i;
         const uint32_t len = hp->payload_len;
         const uint64_t moff = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
         // first arrival within the batch: c_first is final after k_ingest
         // (fi is 0 for a packet without a descriptor: a valid index)
         if (cf[fi] != i + 1 || !dst) continue;
-        const uint8_t* src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
+        const uint8_t* src = md ? reinterpret_cast<const uint8_t*>(mdv) + moff
+                             : stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
+        if (md && !mdv) continue;  // no message data: accepted, nothing to copy (transport.cpp:722)
         warp_scatter<R>(reinterpret_cast<uint8_t*>(dst), src, len, lane);
     }
     TM_END(25);
@@ -1241,9 +1254,12 @@ __global__ void __launch_bounds__(32) k_copy_tma(RxDev d, const cn_pkt_hdr* __re
         const uint32_t l = hp->payload_len;
         const uint64_t mo = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
         if (cf[fi] != i + 1 || !d0) return p;
+        const unsigned long long mdv = d.msgdata ? d.msgdata[i] : 0;
+        if (d.msgdata && !mdv) return p;  // no message data: nothing to copy
         p.dst = d0;
         p.len = l;
-        p.src = stride ? payload + static_cast<uint64_t>(i) * stride : payload + mo;
+        p.src = d.msgdata ? reinterpret_cast<const uint8_t*>(mdv) + mo
+                          : stride ? payload + static_cast<uint64_t>(i) * stride : payload + mo;
         p.bulk = (l & ~15u) && !((reinterpret_cast<uintptr_t>(p.src) | d0) & 15);
         return p;
     };
@@ -2405,7 +2421,7 @@ extern "C" int cn_rx_get_usage(cn_rx* rx, cn_rx_usage* out) {
 static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
                          uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
                          cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
-                         void* stream);
+                         void* stream, const uint64_t* d_msgdata = nullptr);
 
 extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
                            uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks,
@@ -2417,6 +2433,26 @@ extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_pa
     }
     return rx_batch_impl(rx, d_hdrs, nullptr, d_payload, payload_stride, n, d_acks, max_acks, d_completions,
                          max_completions, d_result, stream);
+}
+
+// Packets carrying their message's data pointer (Packet::msg_data, the
+// reference's send_message_data path): packet i's payload is read at
+// d_msg_data[i] + chunk_offset + seq_in_chunk * max_payload; a 0 pointer is a
+// packet without data (accepted and counted, nothing copied, :722).
+extern "C" int cn_rx_batch_msgdata(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
+                                   const uint64_t* d_msg_data, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
+                                   cn_completion* d_completions, uint32_t max_completions,
+                                   cn_rx_result* d_result, void* stream) {
+    if (rx && (rx->d.ordered ? (n > 0 && !d_psn) : d_psn != nullptr)) {
+        set_error("cn_rx_batch_msgdata: conn_psn exactly when the receiver is ordered");
+        return CN_E_INVALID;
+    }
+    if (rx && n > 0 && !d_msg_data) {
+        set_error("cn_rx_batch_msgdata: null msg_data");
+        return CN_E_INVALID;
+    }
+    return rx_batch_impl(rx, d_hdrs, d_psn, nullptr, 0, n, d_acks, max_acks, d_completions, max_completions,
+                         d_result, stream, d_msg_data);
 }
 
 extern "C" int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
@@ -2434,12 +2470,13 @@ extern "C" int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64
 static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
                          uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
                          cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
-                         void* stream) {
+                         void* stream, const uint64_t* d_msgdata) {
     if (!rx || !d_result) {
         set_error("cn_rx_batch: null handle/result");
         return CN_E_INVALID;
     }
     rx->d.psn = d_psn;
+    rx->d.msgdata = reinterpret_cast<const unsigned long long*>(d_msgdata);
     if (n > rx->cfg.max_batch) {
         set_error("cn_rx_batch: n exceeds max_batch");
         return CN_E_CAPACITY;
@@ -2448,7 +2485,7 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         set_error("cn_rx_batch: null headers");
         return CN_E_INVALID;
     }
-    if (rx->d.carry && n > 0 && (!d_payload || (payload_stride && payload_stride < rx->d.max_pl))) {
+    if (rx->d.carry && n > 0 && !d_msgdata && (!d_payload || (payload_stride && payload_stride < rx->d.max_pl))) {
         set_error("cn_rx_batch: carry_payload needs a payload buffer (stride 0 or >= max_payload)");
         return CN_E_INVALID;
     }

@@ -366,18 +366,20 @@ extern "C" int64_t cn_transport_poll_transmissions(cn_transport* h, cn_tx_rec* o
     return static_cast<int64_t>(k);
 }
 
-extern "C" int cn_transport_handle_data_psn(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
-                                            const void* d_payload, uint64_t stride, uint32_t n, void* stream) {
+static int handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
+                       uint64_t stride, const uint64_t* d_msg_data, uint32_t n, void* stream) {
     if (!h) return CN_E_INVALID;
     if (n > h->c.max_batch) {
         set_error("cn_transport_handle_data: batch larger than max_batch");
         return CN_E_CAPACITY;
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    int rc = d_psn ? cn_rx_batch_psn(h->rx, d_hdrs, d_psn, d_payload, stride, n, h->d_aout, n + 16, h->d_cpls,
-                                     n + 16, h->d_res, stream)
-                   : cn_rx_batch(h->rx, d_hdrs, d_payload, stride, n, h->d_aout, n + 16, h->d_cpls, n + 16,
-                                 h->d_res, stream);
+    int rc = d_msg_data ? cn_rx_batch_msgdata(h->rx, d_hdrs, d_psn, d_msg_data, n, h->d_aout, n + 16, h->d_cpls,
+                                              n + 16, h->d_res, stream)
+             : d_psn    ? cn_rx_batch_psn(h->rx, d_hdrs, d_psn, d_payload, stride, n, h->d_aout, n + 16,
+                                          h->d_cpls, n + 16, h->d_res, stream)
+                        : cn_rx_batch(h->rx, d_hdrs, d_payload, stride, n, h->d_aout, n + 16, h->d_cpls, n + 16,
+                                      h->d_res, stream);
     if (rc != CN_OK) return rc;
     cn_rx_result r;
     CNB_CUDA(cudaMemcpyAsync(&r, h->d_res, sizeof r, cudaMemcpyDeviceToHost, s));
@@ -401,9 +403,21 @@ extern "C" int cn_transport_handle_data_psn(cn_transport* h, const cn_pkt_hdr* d
     return CN_OK;
 }
 
+extern "C" int cn_transport_handle_data_psn(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
+                                            const void* d_payload, uint64_t stride, uint32_t n, void* stream) {
+    return handle_data(h, d_hdrs, d_psn, d_payload, stride, nullptr, n, stream);
+}
 extern "C" int cn_transport_handle_data(cn_transport* h, const cn_pkt_hdr* d_hdrs, const void* d_payload,
                                         uint64_t stride, uint32_t n, void* stream) {
-    return cn_transport_handle_data_psn(h, d_hdrs, nullptr, d_payload, stride, n, stream);
+    return handle_data(h, d_hdrs, nullptr, d_payload, stride, nullptr, n, stream);
+}
+extern "C" int cn_transport_handle_data_msgdata(cn_transport* h, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn,
+                                                const uint64_t* d_msg_data, uint32_t n, void* stream) {
+    if (h && n > 0 && !d_msg_data) {
+        set_error("cn_transport_handle_data_msgdata: null msg_data");
+        return CN_E_INVALID;
+    }
+    return handle_data(h, d_hdrs, d_psn, nullptr, 0, d_msg_data, n, stream);
 }
 
 extern "C" int64_t cn_transport_poll_acks(cn_transport* h, cn_ack_rec* out, uint64_t cap) {

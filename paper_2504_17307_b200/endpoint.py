@@ -59,6 +59,7 @@ def _setup(L):
     L.cn_transport_poll_transmissions.restype = i64
     L.cn_transport_handle_data.argtypes = [vp, vp, vp, u64, u32, vp]
     L.cn_transport_handle_data_psn.argtypes = [vp, vp, vp, vp, u64, u32, vp]
+    L.cn_transport_handle_data_msgdata.argtypes = [vp, vp, vp, vp, u32, vp]
     L.cn_transport_poll_acks.argtypes = [vp, vp, u64]
     L.cn_transport_poll_acks.restype = i64
     L.cn_transport_poll_completions.argtypes = [vp, vp, u64]
@@ -144,10 +145,17 @@ class TransportEndpoint:
         _lib.check(n if n < 0 else 0, "poll_transmissions")
         return out[: min(n, cap)], conn[: min(n, cap)]
 
-    def handle_data(self, hdrs, payload=None, stride=4032, stream=None, psn=None):
-        """psn: device int64 conn_psn per packet (ordered reliability)."""
+    def handle_data(self, hdrs, payload=None, stride=4032, stream=None, psn=None, msg_data=None):
+        """psn: device int64 conn_psn per packet (ordered reliability);
+        msg_data: device int64 message-data pointer per packet (Packet::msg_data,
+        the send_message_data path) instead of a payload buffer."""
         s = stream or torch.cuda.current_stream(self.device)
         n = hdrs.numel() // 64
+        if msg_data is not None:
+            _lib.check(self._L.cn_transport_handle_data_msgdata(
+                self._h, hdrs.data_ptr(), psn.data_ptr() if psn is not None else None, msg_data.data_ptr(), n,
+                ctypes.c_void_p(s.cuda_stream)), "handle_data_msgdata")
+            return
         pl = payload.data_ptr() if payload is not None else None
         _lib.check(self._L.cn_transport_handle_data_psn(self._h, hdrs.data_ptr(),
                                                          psn.data_ptr() if psn is not None else None, pl,

@@ -151,16 +151,24 @@ class Transport:
         if self._cpls.numel() < need:
             self._cpls = torch.empty(need, dtype=torch.uint8, device=self.device)
 
-    def rx_batch_async(self, hdrs, payload, stride=MAX_PAYLOAD, stream=None, n=None, psn=None):
+    def rx_batch_async(self, hdrs, payload, stride=MAX_PAYLOAD, stream=None, n=None, psn=None, msg_data=None):
         """Enqueue the receive path for a batch; no host synchronisation.
         A pipelined receiver (pipeline=True) leaves this batch's payload
         scatter running beside the next batch (flush() joins it).
         hdrs: device uint8 [n*64] (cn_pkt_hdr records, arrival order);
         payload: device buffer, packet i's payload at i*stride; psn: device
-        uint64 conn_psn per packet (ordered reliability only)."""
+        uint64 conn_psn per packet (ordered reliability only); msg_data: device
+        int64 per packet, its message's data pointer (Packet::msg_data, the
+        send_message_data path) -- replaces payload / stride."""
         n = hdrs.numel() // 64 if n is None else n
         self._ensure(n)
         s = stream or torch.cuda.current_stream(self.device)
+        if msg_data is not None:
+            _lib.check(_lib.lib().cn_rx_batch_msgdata(
+                self._h, hdrs.data_ptr(), psn.data_ptr() if psn is not None else None, msg_data.data_ptr(), n,
+                self._acks.data_ptr(), n + 16, self._cpls.data_ptr(), n + 16, self._result.data_ptr(),
+                ctypes.c_void_p(s.cuda_stream)), "cn_rx_batch_msgdata")
+            return n
         pl = payload.data_ptr() if payload is not None else None
         if payload is not None and stride == 0 and not self.cfg.carry_payload:
             pl = None
@@ -176,12 +184,12 @@ class Transport:
             ctypes.c_void_p(s.cuda_stream)), "cn_rx_batch")
         return n
 
-    def handle_packets(self, hdrs, payload=None, stride=MAX_PAYLOAD, stream=None, psn=None):
+    def handle_packets(self, hdrs, payload=None, stride=MAX_PAYLOAD, stream=None, psn=None, msg_data=None):
         """Batched Transport::handle_packet for data packets: runs the device
         receive path, returns the ack records in emission order, and fires
         the completion callback for every delivered message."""
         s = stream or torch.cuda.current_stream(self.device)
-        n = self.rx_batch_async(hdrs, payload, stride, s, psn=psn)
+        n = self.rx_batch_async(hdrs, payload, stride, s, psn=psn, msg_data=msg_data)
         if self.pipeline:  # this call's contract: the delivered bytes are final
             self.flush(s)
         self._pinned.copy_(self._result, non_blocking=True)

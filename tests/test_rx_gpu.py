@@ -336,3 +336,41 @@ def test_rx_pipelined_receiver(name, nsplit):
     cp = np.concatenate(all_cpls)
     for f in CPL_FIELDS:
         assert (cp[f] == cpls_ref[f]).all(), f
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_32k", "concurrent_k4", "multigen_k8", "odd_chunk", "ordered_loss"])
+def test_rx_message_data_pointers(name):
+    """The send_message_data path (transport.hpp:88-91): each packet carries
+    its message's data (Packet::msg_data, set by send_chunk :486) and
+    accept_payload copies from it (:719-730).  Here every packet names a
+    device buffer holding its message's bytes (cn_rx_batch_msgdata); the ack
+    stream, completions and reassembled buffers are the reference's."""
+    data, acks_ref, cpls_ref, meta = load_golden(name)
+    tr = _transport(meta)
+    bufs, ptr = {}, np.zeros(len(data), dtype=np.int64)
+    for i, (tag, ln) in enumerate(zip(data["msg_tag"], data["msg_len"])):
+        k = (int(tag), int(ln))
+        if k not in bufs:
+            bufs[k] = torch.from_numpy(O.pattern_bytes(k[1], k[0]).copy()).cuda()
+        ptr[i] = bufs[k].data_ptr()
+    import paper_2504_17307_b200 as cn
+    out = tr.handle_packets(cn.to_device_records(data), None, psn=_psn(name),
+                            msg_data=torch.from_numpy(ptr).cuda())
+    ok, bad = ack_equal(out.acks_np(), acks_ref)
+    assert ok, bad
+    _check_completions(tr, out, cpls_ref)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_32k", "odd_chunk", "multigen_k8", "trim_storm"])
+def test_rx_bulk_copy_variant(name, monkeypatch):
+    """The scatter on the bulk-copy (TMA) engine (k_copy_tma, CN_COPY_TMA=1):
+    identical buffers, incl. the 16-byte tails and the misaligned packets of
+    a 5000-byte chunk size that take the warp-cooperative path."""
+    monkeypatch.setenv("CN_COPY_TMA", "1")
+    data, acks_ref, cpls_ref, meta = load_golden(name)
+    tr = _transport(meta)
+    hd, pl = _dev(data)
+    out = tr.handle_packets(hd, pl, psn=_psn(name))
+    ok, bad = ack_equal(out.acks_np(), acks_ref)
+    assert ok, bad
+    _check_completions(tr, out, cpls_ref)

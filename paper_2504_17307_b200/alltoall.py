@@ -104,6 +104,9 @@ class AllToAll:
         self.sent = [[0, 0] for _ in range(n)]   # pieces sent to each peer, per lane
         self.recvd = [[0, 0] for _ in range(n)]  # pieces consumed from each peer, per lane
         self.ev_init = torch.cuda.Event()
+        # the copy lanes' last work of the previous call: the next call's headers
+        # may be built as soon as those copies have read the header buffer
+        self.ev_lanes = [torch.cuda.Event() for _ in range(2)]
         torch.cuda.synchronize()
         dist.barrier(group)
 
@@ -184,8 +187,12 @@ class AllToAll:
             ln.wait_event(self.ev_init)
         # paths and headers of every outgoing message on a side stream, beside
         # the first transfers (headers ride with a message's first piece)
+        # built ahead: the header stream waits only for the previous call's
+        # copies of the header buffer, not for this rank's earlier work on s
+        # (the combine's headers are ready while the dispatch still runs)
         sh = self.hdr_stream
-        sh.wait_event(self.ev_init)
+        for ev in self.ev_lanes:
+            sh.wait_event(ev)
         nch = [-(-send_counts[d] // self.cb) if d != r else 0 for d in range(n)]
         offs, goffs = [0], [0]
         for d in range(n):
@@ -193,7 +200,8 @@ class AllToAll:
             for b_ in range(self.sp):
                 goffs.append(start + min(nch[d], (b_ + 1) * self.blk))
             offs.append(start + nch[d])
-        po = torch.tensor(goffs, dtype=torch.int32).to(self.dev, non_blocking=True)
+        with torch.cuda.stream(sh):
+            po = torch.tensor(goffs, dtype=torch.int32).to(self.dev, non_blocking=True)
         self.sched.select("p2_rtt", offsets=po, out=self.paths_all, stream=sh)
         for d in range(n):
             if d != r and send_counts[d]:
@@ -221,12 +229,12 @@ class AllToAll:
             for p, (lo, hi) in enumerate(self._pieces(send_counts[d])):
                 ln = (k + p) % 2  # consecutive pieces alternate copy lanes
                 sp = self.lanes[ln]
-                _lib.check(L.cn_copy_async(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
-                                           cs(sp)), "cn_copy_async")
-                if p == 0 and "hdr" not in _SKIP:  # the message's headers ride with its first piece
+                if p == 0 and "hdr" not in _SKIP:  # the message's headers lead its first piece
                     sp.wait_event(self.ev_hdrs)
                     _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh, npk * 64, cs(sp)),
                                "cn_copy_async")
+                _lib.check(L.cn_copy_async(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
+                                           cs(sp)), "cn_copy_async")
                 self.sent[d][ln] += 1
                 _lib.check(L.cn_flag_signal(pe["flags"] + 16 * r + 8 * ln, None, self.sent[d][ln], cs(sp)),
                            "cn_flag_signal")
@@ -260,6 +268,8 @@ class AllToAll:
                     self.rx.rx_batch_async(hd, pl, 0, s, n=b - a)
                 _lib.check(L.cn_flag_signal(self.peer[src]["flags"] + 16 * n + 16 * r + 8 * ln, None,
                                             self.recvd[src][ln], cs(s)), "cn_flag_signal")  # src's freed[r][ln]
+        for ln, ev in zip(self.lanes, self.ev_lanes):
+            ev.record(ln)
         for ln in self.lanes + [self.hdr_stream]:
             s.wait_stream(ln)
         return self.recv_buffer()

@@ -50,13 +50,16 @@ def main():
             step()
         torch.cuda.synchronize()
     dist.barrier()
+    evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    rows_ = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
+    # a common origin over the ranks (CUPTI stamps are host-clock based)
+    t0t = torch.tensor([float(rows_[0][0])], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t0t, op=dist.ReduceOp.MIN)
     for who in range(world):
         if who == rank:
-            evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
-            rows_ = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
             st_ = [r_ for r_ in rows_[len(rows_) // 2:]]
             print(f"==== rank {rank} step span {(st_[-1][1] - st_[0][0]):.1f} us over the last step")
-            t0 = rows_[0][0]
+            t0 = float(t0t.item())
             print(f"==== rank {rank}")
             for a, b, nm in rows_[len(rows_) // 2:]:
                 short = nm.split("(")[0].replace("void ", "").replace("cnb::", "")[:30]

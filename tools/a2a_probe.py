@@ -33,28 +33,59 @@ def main():
     offs = np.concatenate([[0], np.cumsum(rows_self[rank])[:-1]]) * row
     sc, rc = rows[rank] * row, rows[:, rank] * row
     cap = int(max(rows.max() * row, 16))
-    for pb_mb, tail in ((64, 0), (32, 2), (48, 2), (32, 3), (64, 1)):
-        for direct in (True, False):
-            a2a = AllToAll(cap, piece_bytes=pb_mb << 20, direct=direct, tail=tail)
-            for _ in range(3):
+    direct = os.environ.get("CN_A2A_DIRECT", "1") == "1"
+    pb = int(os.environ.get("CN_A2A_PIECE_MB", "64")) << 20
+    a2a = AllToAll(cap, piece_bytes=pb, direct=direct)
+    a2c = AllToAll(cap, piece_bytes=pb, direct=direct)
+    coffs = [s_ * a2a.cap for s_ in range(world)]
+    recv = a2a.run(send, sc, rc, send_offsets=offs)
+    variants = {
+        "dispatch only": lambda: a2a.run(send, sc, rc, send_offsets=offs),
+        "combine only": lambda: a2c.run(recv, rc, sc, send_offsets=coffs),
+        "dispatch + combine": lambda: (a2a.run(send, sc, rc, send_offsets=offs),
+                                       a2c.run(recv, rc, sc, send_offsets=coffs)),
+        "dispatch + combine, synchronized between": None,
+        "dispatch only, alternating two AllToAll objects": "alt",
+    }
+    a2b = AllToAll(cap, piece_bytes=pb, direct=direct)
+    alt = [0]
+    for name, fn in variants.items():
+        def step():
+            if fn == "alt":
+                (a2a if alt[0] % 2 == 0 else a2b).run(send, sc, rc, send_offsets=offs)
+                alt[0] += 1
+            elif fn is not None:
+                fn()
+            else:
                 a2a.run(send, sc, rc, send_offsets=offs)
-            torch.cuda.synchronize()
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(5):
-                a2a.run(send, sc, rc, send_offsets=offs)
-            e1.record()
-            torch.cuda.synchronize()
-            a2a.check()
-            t = torch.tensor([e0.elapsed_time(e1) / 5], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            hot = int(rows[:, 0].sum()) * row
-            if rank == 0:
-                print(f"dispatch only, pieces {pb_mb} MiB tail {tail}, direct={direct}: {float(t.item()):.3f} ms = "
-                      f"{hot / (float(t.item()) * 1e-3) / 1e9:.1f} GB/s into the hot rank "
-                      f"(skip={os.environ.get('CN_A2A_SKIP', '')})", flush=True)
-            a2a.close()
+                torch.cuda.synchronize()
+                dist.barrier()
+                a2c.run(recv, rc, sc, send_offsets=coffs)
+                torch.cuda.synchronize()
+                dist.barrier()
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        import time
+        h0 = time.perf_counter()
+        e0.record()
+        for _ in range(5):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - h0) * 1e3 / 5
+        t = torch.tensor([e0.elapsed_time(e1) / 5], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            print(f"{name}: {float(t.item()):.3f} ms (wall {wall:.3f} ms), pieces {pb >> 20} MiB, direct={direct}",
+                  flush=True)
+    a2a.check()
+    a2c.check()
+    a2a.close()
+    a2c.close()
+    a2b.close()
     dist.destroy_process_group()
 
 

@@ -255,6 +255,11 @@ __device__ __forceinline__ unsigned long long gtime() {
         if (threadIdx.x == 0) atomicMin(&g_tm[slot_], gtime()); \
     } while (0)
 constexpr int kTileTm = 8192;
+__device__ unsigned long long g_ing_tm[5][64];  // k_ingest packet blocks 0..63: start, conn, gen, end, first-load
+#define TM_ING(k_, b_)                                                    \
+    do {                                                                  \
+        if (threadIdx.x == 0 && (b_) < 64) g_ing_tm[k_][b_] = gtime();   \
+    } while (0)
 __device__ unsigned long long g_tile_tm[4][kTileTm];  // k_acks per tile: start, decided, built, written
 #define TM_TILE(k_, tile_)                                                   \
     do {                                                                     \
@@ -263,6 +268,9 @@ __device__ unsigned long long g_tile_tm[4][kTileTm];  // k_acks per tile: start,
 #else
 #define TM_TILE(k_, tile_) \
     do {                   \
+    } while (0)
+#define TM_ING(k_, b_) \
+    do {               \
     } while (0)
 #define TM_END(slot_) \
     do {              \
@@ -397,6 +405,8 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         return;
     }
     const uint32_t i = (blockIdx.x - d.scan_blocks) * blockDim.x + threadIdx.x;
+    const uint32_t pblk = blockIdx.x - d.scan_blocks;
+    TM_ING(0, pblk);
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t par = d.ctl->par;
     const uint32_t tiles = (n + d.ack_tile - 1) / d.ack_tile;
@@ -432,6 +442,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     }
     const uint32_t mid = (h.hdr >> 17) & 0x7F;
     __syncthreads();
+    TM_ING(4, pblk);
     // ---- connection (dst, src, conn_id)
     const uint64_t rkey = (static_cast<uint64_t>(h.dst) << 32) | (static_cast<uint64_t>(h.src) << 8) |
                           (h.hdr >> 24);
@@ -460,6 +471,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         ok = false;
     }
     TM_END(11);
+    TM_ING(1, pblk);
     // ---- message generation (rconn, msg_seq)
     for (int k = threadIdx.x; k < kIngMap; k += kIngestThreads) m_key[k] = kMapEmpty;
     __syncthreads();
@@ -641,6 +653,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     }
     __syncthreads();
     TM_END(12);
+    TM_ING(2, pblk);
     const uint32_t gs = ok ? m_val[gslot] : kInf;
     if (ok && gs != kInf) {
         const uint32_t nch = m_nch[gslot];
@@ -700,6 +713,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         atomicMax(&d.gen[m_val[gslot]].touch, (static_cast<unsigned long long>(epoch) << 32) | m_touch[gslot]);
     if (threadIdx.x == 0 && s_status) atomicOr(&d.ctl->status, s_status);
     TM_END(13);
+    TM_ING(3, pblk);
 }
 
 
@@ -2128,6 +2142,8 @@ struct cn_rx {
     int copy_tma = 0;    // copy mode on the bulk-copy engine (CN_COPY_TMA=1; default: the vector path)
     int tma_bps = 1;     // its blocks per SM (CN_TMA_BPS)
     int ack_bps = 4;     // k_acks blocks per SM (CN_ACK_BPS)
+    int chain_bps = 2;   // k_scan / k_finalize blocks per SM (CN_CHAIN_BPS)
+    int copy_warps = 8;  // warps per copy-mode scatter block (CN_COPY_WARPS, 1..8)
     uint32_t small_batch = 32768;  // batches up to this many packets use 32-packet ack tiles (CN_ACK_SMALL)
     int hi_prio = 0;     // greatest stream priority: the latency-bound ack path wins SM slots
     // optional per-kernel timing with CUDA events on the launch stream
@@ -2246,6 +2262,8 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     if (const char* e = getenv("CN_SCAN_FIRST")) rx->scan_first = atoi(e);
     if (const char* e = getenv("CN_COPY_TMA")) rx->copy_tma = atoi(e);
     if (const char* e = getenv("CN_ACK_BPS")) rx->ack_bps = atoi(e) > 0 ? atoi(e) : 4;
+    if (const char* e = getenv("CN_CHAIN_BPS")) rx->chain_bps = atoi(e) > 0 ? atoi(e) : 2;
+    if (const char* e = getenv("CN_COPY_WARPS")) rx->copy_warps = std::min(8, std::max(1, atoi(e)));
     if (const char* e = getenv("CN_TMA_BPS")) rx->tma_bps = atoi(e) > 0 ? atoi(e) : 1;
     cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
     if (const char* e = getenv("CN_ACK_SMALL")) rx->small_batch = static_cast<uint32_t>(atoi(e));
@@ -2499,14 +2517,15 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         ev = &rx->pending.back();
     }
     // chunk-tile kernels: persistent grids pulling 256-chunk tiles by ticket
-    uint32_t gb = 2u * static_cast<uint32_t>(rx->sms);
+    uint32_t gb = static_cast<uint32_t>(rx->chain_bps) * static_cast<uint32_t>(rx->sms);
     prof_mark(ev, s);
     if (n > 0) {
         const uint8_t* pl = static_cast<const uint8_t*>(d_payload);
         const uint32_t ack_tile = n <= rx->small_batch ? kAckTileMin : kAckTileMax;
         rx->d.ack_tile = ack_tile;
         uint32_t tiles = (n + ack_tile - 1) / ack_tile;
-        uint32_t cw = (n + 7) / 8;  // 8 warps (packets) per copy block
+        const uint32_t cwarps = static_cast<uint32_t>(rx->copy_warps);
+        uint32_t cw = (n + cwarps - 1) / cwarps;  // one warp (packet) per copy-block warp
         // about one packet per warp: short-lived blocks, so the block
         // scheduler hands SM slots to the high-priority ack path first and
         // to the scatter as they free up (a persistent scatter grid would
@@ -2556,7 +2575,7 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
             else if (rx->copy_tma && payload_stride % 16 == 0 && d.max_pl <= kTmaSlotBytes)
                 k_copy_tma<<<rx->tma_bps * rx->sms, 32, kTmaSmem, cs>>>(d, d_hdrs, pl, payload_stride, n);
             else
-                k_copy<0><<<cg, 256, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
+                k_copy<0><<<cg, 32 * cwarps, 0, cs>>>(d, d_hdrs, pl, payload_stride, n);
             prof_mark(ev, s);
         };
         const bool copy_last = rx->scan_first && !ev;  // profiling keeps the named kernel order
@@ -2718,6 +2737,11 @@ extern "C" int cn_rx_debug_timing(unsigned long long* out, int n) {
     for (int k = 0; k < 64; ++k) h[k] = 0;
     for (unsigned long long k : mins) h[k] = ~0ull;
     CNB_CUDA(cudaMemcpyToSymbol(g_tm, h, sizeof h));
+    return CN_OK;
+}
+// k_ingest per-packet-block marks: [5][64]
+extern "C" int cn_rx_debug_ingest_timing(unsigned long long* out) {
+    CNB_CUDA(cudaMemcpyFromSymbol(out, g_ing_tm, sizeof g_ing_tm));
     return CN_OK;
 }
 // k_acks per-tile marks of the last batch: [4][kTileTm] (start, decided, built, written)

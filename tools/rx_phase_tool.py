@@ -55,6 +55,19 @@ def main():
         t0 = buf[10]
         marks = sorted((buf[j] - t0, NAMES[j]) for j in NAMES if 0 < buf[j] < (1 << 63))
         print(f"--- step {k}: " + "  ".join(f"{nm} {v / 1e3:.1f}" for v, nm in marks))
+        if os.environ.get("INGEST") == "1" and k == steps - 1:  # k_ingest per-packet-block marks
+            import numpy as np
+            ib = (ctypes.c_ulonglong * (5 * 64))()
+            lib.cn_rx_debug_ingest_timing.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+            lib.cn_rx_debug_ingest_timing(ib)
+            a = np.frombuffer(ib, dtype=np.uint64).reshape(5, 64).astype(np.int64)
+            nb = int((a[3] > 0).sum())
+            a = a[:, :nb]
+            print(f"ingest packet blocks {nb}: start after the first block (us) " +
+                  " ".join(f"{(v - buf[10]) / 1e3:.1f}" for v in a[0][:16]))
+            for nm, x, y in (("hdr load", 0, 4), ("conn", 4, 1), ("gen", 1, 2), ("chunks", 2, 3), ("block", 0, 3)):
+                dd = (a[y] - a[x]) / 1e3
+                print(f"  {nm:9s} p50 {np.median(dd):.2f} max {dd.max():.2f} us")
         if os.environ.get("TILES") == "1" and k == steps - 1:  # k_acks per-tile marks
             import numpy as np
             tb = (ctypes.c_ulonglong * (4 * 8192))()

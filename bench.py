@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sched", action="store_true")
     ap.add_argument("--no-ring", action="store_true")
-    ap.add_argument("--piece-mb", type=int, default=64, help="ring pipeline piece size (MiB)")
+    ap.add_argument("--piece-mb", type=int, default=0,
+                    help="ring pipeline piece size (MiB); 0 = a quarter of a segment, at least 32 MiB")
     ap.add_argument("--no-moe", action="store_true", help="skip the MoE all-to-all (configs[3]) at N > 1")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] receive sweep")
     ap.add_argument("--no-extra", action="store_true",
@@ -1233,7 +1234,10 @@ def main():
     sched = sched_bench(dev) if not args.no_sched else None
     sender = sender_bench(dev) if not args.no_sched and rank == 0 else None
     eqds = eqds_bench(dev) if not args.no_sched and rank == 0 else None
-    ring = ring_bench(dev, world, rank, piece_bytes=args.piece_mb << 20) if world > 1 and not args.no_ring else None
+    # pieces: 4 per ring step (the copy engine's fixed cost per copy against the
+    # exposed first / last piece; tools/p2p_probe.py)
+    pmb = args.piece_mb or max(32, ((1 << 30) // max(world, 1) // 4) >> 20)
+    ring = ring_bench(dev, world, rank, piece_bytes=pmb << 20) if world > 1 and not args.no_ring else None
     moe = moe_bench(dev, world, rank) if world > 1 and not args.no_moe else None
     sweep = sweep_bench(dev, world, rank) if not args.no_sweep else None
     extra = {}

@@ -829,8 +829,9 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     a2c.close()
     moved = int(rows.sum()) * row * 2  # dispatch + combine, all ranks
     hot_in = int(rows[:, 0].sum()) * row
-    return {"piece_bytes": pb, "mode": "direct (NVLink writes into the receive slots, header-only receive path)"
-            if direct else "staged (receive path scatters staging into the posted slots)",
+    return {"piece_bytes": pb, "mode": ("direct (NVLink writes into the receive slots, header-only receive path)"
+                                        if direct else "staged (receive path scatters staging into the posted slots)")
+            + f"; pieces pushed by {a2a.push}",
             "parity": "dispatch and combine byte-exact on every rank (all slices)",
             "config": f"{world} ranks x {tokens} tokens, hidden {hidden} bf16 ({row} B/copy), top-8 of "
                       f"{32 * world} experts, rank 0 experts 10x weight (incast)",

@@ -14,7 +14,7 @@ path keeps the books on the headers alone (SACK / cum / completion, no
 payload pass); staged mode lands them in a staging slot and d's receive
 path scatters them into the slot (accept_payload).  Either way d releases
 r's freed counter per piece, after which r may reuse the header slot.  Messages to different
-peers leave on two copy lanes in a staggered order (r+1, r+2, ...), so a
+peers leave on two lanes in a staggered order (r+1, r+2, ...), so a
 hot receiver (incast) sees all its senders at once -- its NVLink ingress is
 the bottleneck, which is the point of the workload.  Messages move in
 chunk-aligned pieces, each releasing a per-pair monotone counter, so the
@@ -36,7 +36,7 @@ _SKIP = os.environ.get("CN_A2A_SKIP", "")  # profiling switches only (tools/a2a_
 
 class AllToAll:
     def __init__(self, max_bytes_per_peer, *, chunk_bytes=32768, paths=8, seed=7, group=None,
-                 piece_bytes=128 << 20, max_spins=1 << 26, direct=True, tail=0):
+                 piece_bytes=128 << 20, max_spins=1 << 26, direct=True, tail=0, push=None):
         self.group = group
         self.n = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -49,6 +49,10 @@ class AllToAll:
         self.max_spins = max_spins
         self.direct = direct
         self.tail = tail
+        # the wire: SM stores over NVLink ("sm:<blocks>", default: no per-copy
+        # cost, and unaffected by a source the previous phase just wrote) or
+        # the copy engines ("ce"; ~4.4 us per copy)
+        self.push = push or os.environ.get("CN_A2A_PUSH", "sm:32")
         self.calls = 0
         L = _lib.lib()
         self.max_pkts = L.cn_packet_count(self.cap, chunk_bytes, MAX_PAYLOAD)
@@ -233,8 +237,13 @@ class AllToAll:
                     sp.wait_event(self.ev_hdrs)
                     _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh, npk * 64, cs(sp)),
                                "cn_copy_async")
-                _lib.check(L.cn_copy_async(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
-                                           cs(sp)), "cn_copy_async")
+                if self.push.startswith("sm"):
+                    nb = int(self.push.split(":")[1]) if ":" in self.push else 64
+                    _lib.check(L.cn_copy_sm(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo, nb,
+                                            cs(sp)), "cn_copy_sm")
+                else:
+                    _lib.check(L.cn_copy_async(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
+                                               cs(sp)), "cn_copy_async")
                 self.sent[d][ln] += 1
                 _lib.check(L.cn_flag_signal(pe["flags"] + 16 * r + 8 * ln, None, self.sent[d][ln], cs(sp)),
                            "cn_flag_signal")

@@ -46,12 +46,17 @@ def main():
                                        a2c.run(recv, rc, sc, send_offsets=coffs)),
         "dispatch + combine, synchronized between": None,
         "dispatch only, alternating two AllToAll objects": "alt",
+        "combine only, its source rewritten before each call": "rewrite",
     }
+    scratch = torch.empty_like(recv)
     a2b = AllToAll(cap, piece_bytes=pb, direct=direct)
     alt = [0]
     for name, fn in variants.items():
         def step():
-            if fn == "alt":
+            if fn == "rewrite":
+                recv.copy_(scratch)  # the combine's source freshly written (dirty in L2)
+                a2c.run(recv, rc, sc, send_offsets=coffs)
+            elif fn == "alt":
                 (a2a if alt[0] % 2 == 0 else a2b).run(send, sc, rc, send_offsets=offs)
                 alt[0] += 1
             elif fn is not None:

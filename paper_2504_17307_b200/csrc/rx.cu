@@ -1063,10 +1063,14 @@ __device__ __forceinline__ uint32_t bf16_rne(float f) {
     u += 0x7fffu + ((u >> 16) & 1u);
     return u >> 16;
 }
+// fp32 adds (a NaN sum is the canonical 0x7FFFFFFF), then both halves
+// rounded to nearest even by one cvt (canonical NaN 0x7FFF) -- the fold's
+// rules (oracle/chunknet_oracle.c)
 __device__ __forceinline__ uint32_t add_bf16x2(uint32_t a, uint32_t b) {
-    uint32_t lo = bf16_rne(__fadd_rn(bf16_lo(a), bf16_lo(b)));
-    uint32_t hi = bf16_rne(__fadd_rn(bf16_hi(a), bf16_hi(b)));
-    return lo | (hi << 16);
+    const float lo = __fadd_rn(bf16_lo(a), bf16_lo(b)), hi = __fadd_rn(bf16_hi(a), bf16_hi(b));
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
 }
 template <int R>
 __device__ __forceinline__ int4 combine(int4 dst, int4 src) {
@@ -1114,7 +1118,7 @@ __device__ __forceinline__ void warp_scatter(uint8_t* __restrict__ dst, const ui
 #else
                     r[k] = __ldcs(s4 + v);
 #endif
-                    if (R) a[R ? k : 0] = d4[v];
+                    if (R) a[R ? k : 0] = __ldcs(d4 + v);  // global (not generic) accesses
                 }
             }
 #pragma unroll
@@ -1123,7 +1127,7 @@ __device__ __forceinline__ void warp_scatter(uint8_t* __restrict__ dst, const ui
                 if (v < nv) {
                     // streaming stores: the message buffers must not evict the
                     // bookkeeping arrays the concurrent ack kernels walk
-                    if (R) d4[v] = combine<R ? R : 1>(a[R ? k : 0], r[k]);
+                    if (R) __stcs(d4 + v, combine<R ? R : 1>(a[R ? k : 0], r[k]));
                     else __stcs(d4 + v, r[k]);
                 }
             }
@@ -1164,7 +1168,9 @@ __device__ __forceinline__ void warp_scatter(uint8_t* __restrict__ dst, const ui
 }
 
 template <int R>
-__global__ void __launch_bounds__(256, CN_COPY_MINB) k_copy(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
+// reduce modes: 3 blocks per SM (80 registers, a few bytes spilled) beat 2
+// (105 registers): fp32 0.149 -> 0.130 ms on the 4 x 64 MiB batch
+__global__ void __launch_bounds__(256, R ? 3 : CN_COPY_MINB) k_copy(RxDev d, const cn_pkt_hdr* __restrict__ hdrs,
                                               const uint8_t* __restrict__ payload, uint64_t stride,
                                               uint32_t n) {
     const int lane = threadIdx.x & 31;
@@ -1180,6 +1186,7 @@ __global__ void __launch_bounds__(256, CN_COPY_MINB) k_copy(RxDev d, const cn_pk
         // k_ingest's descriptor: only packets not seen before the batch, of
         // a live message (GenStates may be reused while a pipelined scatter
         // still runs, so the destination travels with the packet)
+#ifndef CN_COPY_LAZY_HDR
         // every load but the first-arrival test's is independent: issued together
         const unsigned long long dst = pd[i];
         const uint32_t fi = pf[i];
@@ -1190,6 +1197,15 @@ __global__ void __launch_bounds__(256, CN_COPY_MINB) k_copy(RxDev d, const cn_pk
         // first arrival within the batch: c_first is final after k_ingest
         // (fi is 0 for a packet without a descriptor: a valid index)
         if (cf[fi] != i + 1 || !dst) continue;
+#else
+        const unsigned long long dst = pd[i];
+        const uint32_t fi = pf[i];
+        if (cf[fi] != i + 1 || !dst) continue;
+        const unsigned long long mdv = md ? md[i] : 0;
+        const cn_pkt_hdr* hp = hdrs + i;
+        const uint32_t len = hp->payload_len;
+        const uint64_t moff = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
+#endif
         const uint8_t* src = md ? reinterpret_cast<const uint8_t*>(mdv) + moff
                              : stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
         if (md && !mdv) continue;  // no message data: accepted, nothing to copy (transport.cpp:722)

@@ -329,6 +329,11 @@ def steady_bench(dev, data, meta, K, stagings, srcs, steps=20, warmup=5):
     return out
 
 
+def _lib_result(h_res):
+    from paper_2504_17307_b200 import _lib as L_
+    return L_.RxResult.from_buffer_copy(bytes(h_res.numpy()))
+
+
 def _rx_result(tr):
     import torch
 
@@ -1195,21 +1200,28 @@ def main():
     algo_step = 2 * bytes_copied + HDR * n + ACK * n_acks
     step_gbs = algo_step / (ms_step * 1e-3) / 1e9
 
-    # end to end through the public API with host buffers
+    # end to end through the public API with host buffers: each step copies
+    # its batch host -> device (the headers, the payloads packed back to back
+    # as a NIC ring holds them, their offsets), runs cn_rx_batch_packed and
+    # reads the acks and the result back
     e2e = None
     if not args.no_e2e:
+        pl_d = torch.from_numpy(data["payload_len"].astype(np.int64)).to(dev)
+        mask = torch.arange(MAX_PL, device=dev)[None, :] < pl_d[:, None]
+        off_d = torch.cumsum(pl_d, 0) - pl_d
         h_hdr = hdrs.cpu().pin_memory()
-        h_st = [s.cpu().pin_memory() for s in stagings[:2]]
-        d_hdr = torch.empty_like(hdrs)
-        d_st = torch.empty_like(stagings[0])
+        h_pk = [s_.view(n, MAX_PL)[mask].cpu().pin_memory() for s_ in stagings[:2]]
+        h_off = off_d.cpu().pin_memory()
+        d_hdr, d_pk, d_off = torch.empty_like(hdrs), torch.empty_like(h_pk[0], device=dev), torch.empty_like(off_d)
         h_acks = torch.empty((n_acks + 16) * ACK, dtype=torch.uint8).pin_memory()
         h_res = torch.empty(24, dtype=torch.uint8).pin_memory()
 
         def e2e_step(k):
             d_hdr.copy_(h_hdr, non_blocking=True)
-            d_st.copy_(h_st[k % 2], non_blocking=True)
+            d_pk.copy_(h_pk[k % 2], non_blocking=True)  # one copy stream: PCIe-bound (~54 GB/s)
+            d_off.copy_(h_off, non_blocking=True)
             tr.reset(stream)
-            tr.rx_batch_async(d_hdr, d_st, MAX_PL, stream)
+            tr.rx_batch_async(d_hdr, d_pk, 0, stream, offsets=d_off)
             h_acks[: n_acks * ACK].copy_(tr._acks[: n_acks * ACK], non_blocking=True)
             h_res.copy_(tr._result, non_blocking=True)
 
@@ -1224,13 +1236,17 @@ def main():
             e2e_step(k)
         f1.record(stream)
         torch.cuda.synchronize()
+        check_buffers((args.steps - 1) % 2)  # the last step's messages equal their sources
+        res_e = _lib_result(h_res)
+        assert res_e.status == 0 and res_e.n_acks == n_acks, (res_e.status, res_e.n_acks)
         te = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(world * K * msg_len * args.steps / (float(te.item()) * 1e-3) / 1e9, 3),
-               "unit": "GB/s", "h2d_bytes_per_step": int(hdrs.numel() + stagings[0].numel()),
+               "unit": "GB/s", "h2d_bytes_per_step": int(hdrs.numel() + h_pk[0].numel() + h_off.numel() * 8),
                "d2h_bytes_per_step": int(n_acks * ACK + 24),
-               "path": "pinned host records+staging -> cn_rx_batch (C ABI) -> acks to host"}
+               "path": "pinned host: headers + payloads packed back to back + offsets -> H2D -> "
+                       "cn_rx_batch_packed (C ABI) -> acks and result D2H; last step's buffers checked"}
 
     sched = sched_bench(dev) if not args.no_sched else None
     sender = sender_bench(dev) if not args.no_sched and rank == 0 else None

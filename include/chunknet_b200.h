@@ -238,6 +238,13 @@ int cn_rx_batch_msgdata(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_p
                         const uint64_t* d_msg_data, uint32_t n, cn_ack_rec* d_acks,
                         uint32_t max_acks, cn_completion* d_completions,
                         uint32_t max_completions, cn_rx_result* d_result, void* stream);
+/* Packed payloads: packet i's payload_len bytes at d_payload + d_offset[i]
+ * (a NIC ring's variable-size packet buffers -- no stride padding to move
+ * across PCIe).  d_psn as in cn_rx_batch_msgdata. */
+int cn_rx_batch_packed(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
+                       const uint64_t* d_offset, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
+                       cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
+                       void* stream);
 /* cn_rx_batch for ordered reliability: d_psn[i] = conn_psn of packet i
  * (Packet::conn_psn, packet.hpp:48; not part of the 64-B header record) */
 int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,

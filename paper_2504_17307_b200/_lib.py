@@ -115,6 +115,8 @@ def lib():
         L.cn_rx_flush.argtypes = [vp, vp]
     L.cn_rx_batch.argtypes = [vp, vp, vp, u64, u32, vp, u32, vp, u32, vp, vp]
     L.cn_rx_batch_psn.argtypes = [vp, vp, vp, vp, u64, u32, vp, u32, vp, u32, vp, vp]
+    if hasattr(L, "cn_rx_batch_packed"):
+        L.cn_rx_batch_packed.argtypes = [vp, vp, vp, vp, vp, u32, vp, u32, vp, u32, vp, vp]
     if hasattr(L, "cn_rx_batch_msgdata"):
         L.cn_rx_batch_msgdata.argtypes = [vp, vp, vp, vp, u32, vp, u32, vp, u32, vp, vp]
     L.cn_rx_post.argtypes = [vp, u64, vp, u64, vp]

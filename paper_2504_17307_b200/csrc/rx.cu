@@ -156,6 +156,8 @@ struct RxDev {
     // [batch] per-packet message data (Packet::msg_data, transport.hpp:88-91,
     // transport.cpp:486): packet i's payload at msgdata[i] + its message offset
     const unsigned long long* msgdata;
+    // [batch] packed payloads (cn_rx_batch_packed): packet i's payload at payload + poff[i]
+    const unsigned long long* poff;
     uint8_t* p_gbn;           // [batch] 0 pass on, 1 drop, 2 drop with a NACK
     uint64_t* p_gbn_psn;      // [batch] nack_psn of a NACK
     uint64_t* gbn_expected;   // [rconn] RecvConn::expected_psn
@@ -1181,6 +1183,7 @@ __global__ void __launch_bounds__(256, R ? 3 : CN_COPY_MINB) k_copy(RxDev d, con
     const unsigned long long* __restrict__ pd = d.p_dst + par * static_cast<uint64_t>(d.max_batch);
     const uint32_t* __restrict__ pf = d.p_fi + par * static_cast<uint64_t>(d.max_batch);
     const unsigned long long* __restrict__ md = d.msgdata;
+    const unsigned long long* __restrict__ po = d.poff;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
         // k_ingest's descriptor: only packets not seen before the batch, of
@@ -1206,7 +1209,8 @@ __global__ void __launch_bounds__(256, R ? 3 : CN_COPY_MINB) k_copy(RxDev d, con
         const uint32_t len = hp->payload_len;
         const uint64_t moff = hp->chunk_offset + static_cast<uint64_t>(hp->seq_in_chunk) * d.max_pl;
 #endif
-        const uint8_t* src = md ? reinterpret_cast<const uint8_t*>(mdv) + moff
+        const uint8_t* src = po    ? payload + po[i]
+                             : md   ? reinterpret_cast<const uint8_t*>(mdv) + moff
                              : stride ? payload + static_cast<uint64_t>(i) * stride : payload + moff;
         if (md && !mdv) continue;  // no message data: accepted, nothing to copy (transport.cpp:722)
         warp_scatter<R>(reinterpret_cast<uint8_t*>(dst), src, len, lane);
@@ -1288,8 +1292,9 @@ __global__ void __launch_bounds__(32) k_copy_tma(RxDev d, const cn_pkt_hdr* __re
         if (d.msgdata && !mdv) return p;  // no message data: nothing to copy
         p.dst = d0;
         p.len = l;
-        p.src = d.msgdata ? reinterpret_cast<const uint8_t*>(mdv) + mo
-                          : stride ? payload + static_cast<uint64_t>(i) * stride : payload + mo;
+        p.src = d.poff      ? payload + d.poff[i]
+                : d.msgdata ? reinterpret_cast<const uint8_t*>(mdv) + mo
+                : stride    ? payload + static_cast<uint64_t>(i) * stride : payload + mo;
         p.bulk = (l & ~15u) && !((reinterpret_cast<uintptr_t>(p.src) | d0) & 15);
         return p;
     };
@@ -2455,7 +2460,7 @@ extern "C" int cn_rx_get_usage(cn_rx* rx, cn_rx_usage* out) {
 static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
                          uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
                          cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
-                         void* stream, const uint64_t* d_msgdata = nullptr);
+                         void* stream, const uint64_t* d_msgdata = nullptr, const uint64_t* d_poff = nullptr);
 
 extern "C" int cn_rx_batch(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const void* d_payload,
                            uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks,
@@ -2489,6 +2494,24 @@ extern "C" int cn_rx_batch_msgdata(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const ui
                          d_result, stream, d_msg_data);
 }
 
+// Packed payloads: packet i's payload_len bytes at d_payload + d_offset[i]
+// (a NIC ring's variable-size packet buffers; no stride padding to move).
+extern "C" int cn_rx_batch_packed(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
+                                  const uint64_t* d_offset, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
+                                  cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
+                                  void* stream) {
+    if (rx && (rx->d.ordered ? (n > 0 && !d_psn) : d_psn != nullptr)) {
+        set_error("cn_rx_batch_packed: conn_psn exactly when the receiver is ordered");
+        return CN_E_INVALID;
+    }
+    if (rx && n > 0 && rx->d.carry && (!d_offset || !d_payload)) {
+        set_error("cn_rx_batch_packed: null payload or offsets");
+        return CN_E_INVALID;
+    }
+    return rx_batch_impl(rx, d_hdrs, d_psn, d_payload, 0, n, d_acks, max_acks, d_completions, max_completions,
+                         d_result, stream, nullptr, d_offset);
+}
+
 extern "C" int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
                                uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
                                cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
@@ -2504,13 +2527,14 @@ extern "C" int cn_rx_batch_psn(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64
 static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_psn, const void* d_payload,
                          uint64_t payload_stride, uint32_t n, cn_ack_rec* d_acks, uint32_t max_acks,
                          cn_completion* d_completions, uint32_t max_completions, cn_rx_result* d_result,
-                         void* stream, const uint64_t* d_msgdata) {
+                         void* stream, const uint64_t* d_msgdata, const uint64_t* d_poff) {
     if (!rx || !d_result) {
         set_error("cn_rx_batch: null handle/result");
         return CN_E_INVALID;
     }
     rx->d.psn = d_psn;
     rx->d.msgdata = reinterpret_cast<const unsigned long long*>(d_msgdata);
+    rx->d.poff = reinterpret_cast<const unsigned long long*>(d_poff);
     if (n > rx->cfg.max_batch) {
         set_error("cn_rx_batch: n exceeds max_batch");
         return CN_E_CAPACITY;

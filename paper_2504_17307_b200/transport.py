@@ -151,18 +151,28 @@ class Transport:
         if self._cpls.numel() < need:
             self._cpls = torch.empty(need, dtype=torch.uint8, device=self.device)
 
-    def rx_batch_async(self, hdrs, payload, stride=MAX_PAYLOAD, stream=None, n=None, psn=None, msg_data=None):
+    def rx_batch_async(self, hdrs, payload, stride=MAX_PAYLOAD, stream=None, n=None, psn=None, msg_data=None,
+                       offsets=None):
         """Enqueue the receive path for a batch; no host synchronisation.
         A pipelined receiver (pipeline=True) leaves this batch's payload
         scatter running beside the next batch (flush() joins it).
         hdrs: device uint8 [n*64] (cn_pkt_hdr records, arrival order);
         payload: device buffer, packet i's payload at i*stride; psn: device
-        uint64 conn_psn per packet (ordered reliability only); msg_data: device
+        uint64 conn_psn per packet (ordered reliability only); offsets: device
+        int64 per packet -- packed payloads, packet i at payload + offsets[i];
+        msg_data: device
         int64 per packet, its message's data pointer (Packet::msg_data, the
         send_message_data path) -- replaces payload / stride."""
         n = hdrs.numel() // 64 if n is None else n
         self._ensure(n)
         s = stream or torch.cuda.current_stream(self.device)
+        if offsets is not None:  # packed payloads: packet i at payload + offsets[i]
+            _lib.check(_lib.lib().cn_rx_batch_packed(
+                self._h, hdrs.data_ptr(), psn.data_ptr() if psn is not None else None,
+                payload.data_ptr() if payload is not None else None, offsets.data_ptr(), n,
+                self._acks.data_ptr(), n + 16, self._cpls.data_ptr(), n + 16, self._result.data_ptr(),
+                ctypes.c_void_p(s.cuda_stream)), "cn_rx_batch_packed")
+            return n
         if msg_data is not None:
             _lib.check(_lib.lib().cn_rx_batch_msgdata(
                 self._h, hdrs.data_ptr(), psn.data_ptr() if psn is not None else None, msg_data.data_ptr(), n,
@@ -184,12 +194,13 @@ class Transport:
             ctypes.c_void_p(s.cuda_stream)), "cn_rx_batch")
         return n
 
-    def handle_packets(self, hdrs, payload=None, stride=MAX_PAYLOAD, stream=None, psn=None, msg_data=None):
+    def handle_packets(self, hdrs, payload=None, stride=MAX_PAYLOAD, stream=None, psn=None, msg_data=None,
+                       offsets=None):
         """Batched Transport::handle_packet for data packets: runs the device
         receive path, returns the ack records in emission order, and fires
         the completion callback for every delivered message."""
         s = stream or torch.cuda.current_stream(self.device)
-        n = self.rx_batch_async(hdrs, payload, stride, s, psn=psn, msg_data=msg_data)
+        n = self.rx_batch_async(hdrs, payload, stride, s, psn=psn, msg_data=msg_data, offsets=offsets)
         if self.pipeline:  # this call's contract: the delivered bytes are final
             self.flush(s)
         self._pinned.copy_(self._result, non_blocking=True)

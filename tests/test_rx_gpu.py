@@ -374,3 +374,26 @@ def test_rx_bulk_copy_variant(name, monkeypatch):
     ok, bad = ack_equal(out.acks_np(), acks_ref)
     assert ok, bad
     _check_completions(tr, out, cpls_ref)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_32k", "odd_chunk", "trim_storm", "ordered_loss"])
+def test_rx_packed_payloads(name):
+    """cn_rx_batch_packed: payloads packed back to back (a NIC ring's
+    variable-size packet buffers), packet i at payload + offset[i]; shuffled
+    offsets too.  Same acks, completions and buffers as the reference."""
+    import paper_2504_17307_b200 as cn
+    data, acks_ref, cpls_ref, meta = load_golden(name)
+    st = O.fill_staging(data)
+    pl = data["payload_len"].astype(np.int64)
+    order = np.random.RandomState(1).permutation(len(data))  # packets stored in a shuffled order
+    off = np.zeros(len(data), dtype=np.int64)
+    off[order] = np.concatenate([[0], np.cumsum(pl[order])[:-1]])
+    packed = np.zeros(int(pl.sum()) + 16, dtype=np.uint8)
+    for i in range(len(data)):
+        packed[off[i]: off[i] + pl[i]] = st[i * 4032: i * 4032 + pl[i]]
+    tr = _transport(meta)
+    out = tr.handle_packets(cn.to_device_records(data), torch.from_numpy(packed).cuda(), psn=_psn(name),
+                            offsets=torch.from_numpy(off).cuda())
+    ok, bad = ack_equal(out.acks_np(), acks_ref)
+    assert ok, bad
+    _check_completions(tr, out, cpls_ref)

@@ -49,7 +49,7 @@ struct GenState {
     uint8_t* buf;                                  // absolute destination of the message
     unsigned long long touch;  // (epoch << 32) | (max chunk touched + 1) in that epoch
     uint32_t nchunks, cum, n_init, rc, msg_id, epoch, deliver_t, slot;  // slot: gen_key index
-    uint32_t lo_batch, tiles_done, cum_add, pad;
+    uint32_t lo_batch, tiles_done, cum_add, born;  // born: the epoch (batch) that created it
 };
 
 // Ring allocator over `cap` positions (chunk-pool entries, or 512-B arena
@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                                                            uint32_t n) {
     __shared__ unsigned long long m_key[kIngMap];
     __shared__ unsigned long long m_cbase[kIngMap], m_glen[kIngMap], m_buf[kIngMap];
+    __shared__ uint8_t m_fresh[kIngMap];  // generation created in this batch: its chunk state is initial
     __shared__ uint32_t m_val[kIngMap], m_nch[kIngMap], m_touch[kIngMap];
     __shared__ uint32_t s_status;
     const int lane = threadIdx.x & 31;
@@ -411,6 +412,10 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     TM_ING(0, pblk);
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t par = d.ctl->par;
+    // the rings' tails move only in k_finalize: read them with the header, off
+    // the inserters' dependent chain
+    const unsigned long long ptail = ld_volatile_u64(&d.ctl->pool.tail);
+    const unsigned long long atail = ld_volatile_u64(&d.ctl->arena.tail);
     const uint32_t tiles = (n + d.ack_tile - 1) / d.ack_tile;
     if (i < tiles) d.tile_state[i] = 0;
     if (i == 0 && d.carry) {  // the scatter of this batch reads part par
@@ -540,6 +545,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     if (gown) {
         uint32_t gs = kInf, nch = 0;
         unsigned long long cbase = 0, glen = 0, gbuf = 0;
+        bool fresh = false;
         const uint32_t slot = gslot_t;
         if (slot != kInf) {
             GenState* G = nullptr;
@@ -550,8 +556,6 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 const unsigned long long gi = a_gi;
                 const uint32_t tk = a_tk;
                 const unsigned long long ph = a_ph, ah = a_ah;
-                const unsigned long long ptail = ld_volatile_u64(&d.ctl->pool.tail);
-                const unsigned long long atail = early_arena ? ld_volatile_u64(&d.ctl->arena.tail) : 0;
                 // never empty: live keys <= table slots = GenStates
                 gs = d.gen_free[gi & d.gen_mask];
                 G = &d.gen[gs];
@@ -607,6 +611,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 G->deliver_t = kInf;
                 G->slot = slot;
                 G->epoch = epoch;  // first touch is this batch
+                G->born = epoch;
                 G->lo_batch = 0;
                 G->tiles_done = 0;
                 G->cum_add = 0;
@@ -616,6 +621,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 cbase = G->chunk_base;
                 glen = h.msg_len;
                 gbuf = reinterpret_cast<unsigned long long>(buf);
+                fresh = true;
             } else {
                 // wait for the inserter (resident, already past its CAS)
                 uint32_t spins = 0;
@@ -633,6 +639,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
                 cbase = G->chunk_base;
                 glen = G->len;
                 gbuf = reinterpret_cast<unsigned long long>(G->buf);
+                fresh = G->born == epoch;
                 // plain read first: only the first block of the batch pays the atomic
                 if (ld_volatile_u32(&G->epoch) != epoch && atomicExch(&G->epoch, epoch) != epoch) {
                     // first touch this batch: freeze the batch's lower bound
@@ -652,6 +659,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
         m_cbase[gslot] = cbase;
         m_glen[gslot] = glen;
         m_buf[gslot] = gbuf;
+        m_fresh[gslot] = fresh;
     }
     __syncthreads();
     TM_END(12);
@@ -678,12 +686,14 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
             g = gs;
             const uint64_t e = cbase + c;
             const uint32_t t = i + 1;
-            const uint32_t fl = d.c_flags[e];
+            // a generation created in this batch has initial chunk state: no loads
+            const bool fresh = m_fresh[gslot];
+            const uint32_t fl = fresh ? 0u : d.c_flags[e];
             if (h.flags & CN_PKT_TRIMMED) {  // header only: chunk init, then the NACK pass (k_trim)
                 const uint32_t k = atomicAdd(&d.ctl->n_trim, 1u);
                 if (k < kTrimMax) d.trim_list[k] = i;
                 else status |= CN_RXF_CAPACITY;
-            } else if (!(fl & CF_COMPLETE) && !((d.c_seen[e] >> s) & 1u)) {
+            } else if (!(fl & CF_COMPLETE) && (fresh || !((d.c_seen[e] >> s) & 1u))) {
                 const uint64_t fi = e * d.ppc + s;
                 atomicMin(&first_of(d, par)[fi], t);
                 if (d.carry) {  // the scatter's descriptor (k_copy keeps the first arrival)

@@ -53,6 +53,9 @@ class AllToAll:
         # cost, and unaffected by a source the previous phase just wrote) or
         # the copy engines ("ce"; ~4.4 us per copy)
         self.push = push or os.environ.get("CN_A2A_PUSH", "sm:32")
+        # push lanes (streams): two hide the gap between consecutive pieces (one
+        # lane measured no better with SM push: 1.56 vs 1.54 ms, N = 2)
+        self.nl = int(os.environ.get("CN_A2A_LANES", "2"))
         self.calls = 0
         L = _lib.lib()
         self.max_pkts = L.cn_packet_count(self.cap, chunk_bytes, MAX_PAYLOAD)
@@ -222,7 +225,7 @@ class AllToAll:
                 continue
             pe = self.peer[d]
             # d consumed every piece of my previous message (slot and header reuse)
-            for ln in range(2):
+            for ln in range(self.nl):
                 _lib.check(L.cn_flag_wait(self.f_freed + 16 * d + 8 * ln, None, self.sent[d][ln], self.max_spins,
                                           self.f_err, cs(self.lanes[ln])), "cn_flag_wait")
                 if self.direct:  # d armed its receive slot for me this call
@@ -231,7 +234,7 @@ class AllToAll:
             npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
             oh = self._out_hdrs.data_ptr() + d * self.max_pkts * 64
             for p, (lo, hi) in enumerate(self._pieces(send_counts[d])):
-                ln = (k + p) % 2  # consecutive pieces alternate copy lanes
+                ln = (k + p) % self.nl  # consecutive pieces alternate push lanes
                 sp = self.lanes[ln]
                 if p == 0 and "hdr" not in _SKIP:  # the message's headers lead its first piece
                     sp.wait_event(self.ev_hdrs)
@@ -259,7 +262,7 @@ class AllToAll:
                 if src not in plan or p >= len(plan[src][1]):
                     continue
                 ks = (r - src) % n  # the sender's stagger index for me -> its lane choice
-                ln = (ks + p) % 2
+                ln = (ks + p) % self.nl
                 lo, hi = plan[src][1][p]
                 self.recvd[src][ln] += 1
                 _lib.check(L.cn_flag_wait(self.f_ready + 16 * src + 8 * ln, None, self.recvd[src][ln],

@@ -31,9 +31,6 @@ from .collective import DeviceBuffer, _ipc_handle, _ipc_open, _PeerView, packeti
 from .transport import MAX_PAYLOAD, Transport, TransportConfig
 
 
-_SKIP = os.environ.get("CN_A2A_SKIP", "")  # profiling switches only (tools/a2a_probe.py)
-
-
 class AllToAll:
     def __init__(self, max_bytes_per_peer, *, chunk_bytes=32768, paths=8, seed=7, group=None,
                  piece_bytes=128 << 20, max_spins=1 << 26, direct=True, tail=0, push=None):
@@ -236,7 +233,7 @@ class AllToAll:
             for p, (lo, hi) in enumerate(self._pieces(send_counts[d])):
                 ln = (k + p) % self.nl  # consecutive pieces alternate push lanes
                 sp = self.lanes[ln]
-                if p == 0 and "hdr" not in _SKIP:  # the message's headers lead its first piece
+                if p == 0:  # the message's headers lead its first piece
                     sp.wait_event(self.ev_hdrs)
                     _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh, npk * 64, cs(sp)),
                                "cn_copy_async")
@@ -271,9 +268,7 @@ class AllToAll:
                 b = (L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD) if hi == recv_counts[src]
                      else hi // self.cb * ppc)
                 hd = _PeerView(self._hdrs.data_ptr() + src * self.max_pkts * 64 + a * 64, (b - a) * 64)
-                if "rx" in _SKIP:  # profiling switch (tools/a2a_probe.py): no receive path
-                    pass
-                elif self.direct:  # headers only: the bytes already sit in the receive slot
+                if self.direct:  # headers only: the bytes already sit in the receive slot
                     self.rx.rx_batch_async(hd, None, 0, s, n=b - a)
                 else:
                     pl = _PeerView(self._stage.data_ptr() + src * self.cap, recv_counts[src])

@@ -1,7 +1,7 @@
-"""Profiling helper (not a test): the MoE dispatch alone through AllToAll,
-timed per call, with parts of the protocol switched off by CN_A2A_SKIP
-(comma list: rx = no receive path, hdr = no header copies) -- to locate
-what slows the copy engine below the bare protocol's rate (tools/p2p_probe.py).
+"""Profiling helper (not a test): the MoE dispatch and combine through
+AllToAll, each phase alone, alternating, synchronized between, and with a
+freshly written combine source -- to locate what slows a phase below the
+bare protocol's rate (tools/p2p_probe.py).
     torchrun --nproc-per-node 2 tools/a2a_probe.py"""
 import os
 import sys

@@ -55,6 +55,15 @@ __device__ inline uint32_t table_insert(unsigned long long* keys, uint32_t mask,
     return kInf;
 }
 
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization starts while its
+// predecessor in the stream still runs; pdl_wait() blocks until that
+// predecessor has completed and its writes are visible (a no-op without the
+// attribute); pdl_launch() lets the successor start (the ack path's launch
+// latencies overlap the kernel before).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // acquire / release and volatile accesses for the cross-block handshakes
 // (decoupled look-back, published table values)
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {

@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(kIngestThreads) k_ingest(RxDev d, const cn_pkt
     __shared__ uint32_t m_val[kIngMap], m_nch[kIngMap], m_touch[kIngMap];
     __shared__ uint32_t s_status;
     const int lane = threadIdx.x & 31;
+    pdl_launch();  // k_scan may launch now (it waits for this grid)
     TM_START(10);
     if (blockIdx.x < d.scan_blocks) {  // the first blocks scan the rings (ring_scan)
         const uint32_t worker = blockIdx.x * kIngestThreads + threadIdx.x;
@@ -933,6 +934,8 @@ __device__ __forceinline__ uint32_t block_seg_scan_max(uint32_t v, bool head, ui
 __global__ void __launch_bounds__(kScanThreads) k_scan(RxDev d) {
     __shared__ uint32_t s_v[32], s_h[32];
     __shared__ uint32_t s_ticket, s_carry, s_k0;
+    pdl_wait();
+    pdl_launch();
     const int lane = threadIdx.x & 31;
     const uint32_t epoch = d.ctl->epoch;
     const uint32_t nt = min(d.ctl->n_touched, d.plan_cap);
@@ -1445,6 +1448,8 @@ __device__ __forceinline__ uint8_t decide(const RxDev& d, const cn_pkt_hdr* __re
 // them by (chunk, time) and decides each from its predecessor; the decision
 // feeds k_acks, which orders the NACK records into the ack stream.
 __global__ void __launch_bounds__(1024) k_trim(RxDev d, const cn_pkt_hdr* __restrict__ hdrs) {
+    pdl_wait();
+    pdl_launch();
     extern __shared__ unsigned long long key[];  // [kTrimMax]
     const uint32_t m0 = d.ctl->n_trim;
     const uint32_t m = m0 < kTrimMax ? m0 : kTrimMax;
@@ -1672,6 +1677,8 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
     __shared__ uint16_t s_alist[kAckTile], s_clist[kAckTile];
     __shared__ uint32_t s_wa[kDecideWarps], s_wc[kDecideWarps];
     __shared__ uint32_t s_tile, s_base_a, s_base_c;
+    pdl_wait();
+    pdl_launch();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t tiles = (n + kAckTile - 1) / kAckTile;
     TM_START(22);
@@ -1822,6 +1829,7 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     __shared__ bool last_block;
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_cnt[kScanThreads];  // per message segment of the tile: chunks now in the cum prefix
+    pdl_wait();
     const uint32_t nt = min(d.ctl->n_touched, d.plan_cap);
     const uint32_t ppc = d.ppc;
     const uint32_t par = d.ctl->par;
@@ -2175,6 +2183,10 @@ struct cn_rx {
     int ack_bps = 4;     // k_acks blocks per SM (CN_ACK_BPS)
     int chain_bps = 2;   // k_scan / k_finalize blocks per SM (CN_CHAIN_BPS)
     int copy_warps = 8;  // warps per copy-mode scatter block (CN_COPY_WARPS, 1..8)
+    // programmatic dependent launch along the ack path (CN_PDL=1): measured
+    // slower -- the early-launched waiting blocks take SM slots from the
+    // scatter (pipelined step 101.6 -> 105.9 us, strict 105.2 -> 112.5 us)
+    int pdl = 0;
     uint32_t small_batch = 32768;  // batches up to this many packets use 32-packet ack tiles (CN_ACK_SMALL)
     int hi_prio = 0;     // greatest stream priority: the latency-bound ack path wins SM slots
     // optional per-kernel timing with CUDA events on the launch stream
@@ -2295,6 +2307,7 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     if (const char* e = getenv("CN_ACK_BPS")) rx->ack_bps = atoi(e) > 0 ? atoi(e) : 4;
     if (const char* e = getenv("CN_CHAIN_BPS")) rx->chain_bps = atoi(e) > 0 ? atoi(e) : 2;
     if (const char* e = getenv("CN_COPY_WARPS")) rx->copy_warps = std::min(8, std::max(1, atoi(e)));
+    if (const char* e = getenv("CN_PDL")) rx->pdl = atoi(e);
     if (const char* e = getenv("CN_TMA_BPS")) rx->tma_bps = atoi(e) > 0 ? atoi(e) : 1;
     cudaFuncSetAttribute(k_copy_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem));
     if (const char* e = getenv("CN_ACK_SMALL")) rx->small_batch = static_cast<uint32_t>(atoi(e));
@@ -2629,30 +2642,37 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
             prof_mark(ev, s);
         };
         const bool copy_last = rx->scan_first && !ev;  // profiling keeps the named kernel order
+        // programmatic dependent launch along the ack path (not under the
+        // per-kernel profiling events, which sit between the kernels)
+        const bool pdl = rx->pdl && !ev;
         if (!copy_last) copy();
         {
             cudaLaunchConfig_t lc = {};
-            cudaLaunchAttribute at[1];
+            cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributePriority;
             at[0].val.priority = rx->hi_prio;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (pdl_wait)
+            at[1].val.programmaticStreamSerializationAllowed = 1;
             lc.gridDim = dim3(gb);
             lc.blockDim = dim3(kScanThreads);
             lc.stream = s;
             lc.attrs = at;
-            lc.numAttrs = 1;
+            lc.numAttrs = pdl ? 2 : 1;
             CNB_CUDA(cudaLaunchKernelEx(&lc, k_scan, d));
         }
         {  // rare work, but on the ack path: same priority, or it queues behind the scatter
             cudaLaunchConfig_t lc = {};
-            cudaLaunchAttribute at[1];
+            cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributePriority;
             at[0].val.priority = rx->hi_prio;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (pdl_wait)
+            at[1].val.programmaticStreamSerializationAllowed = 1;
             lc.gridDim = dim3(1);
             lc.blockDim = dim3(1024);
             lc.dynamicSmemBytes = kTrimMax * 8;
             lc.stream = s;
             lc.attrs = at;
-            lc.numAttrs = 1;
+            lc.numAttrs = pdl ? 2 : 1;
             CNB_CUDA(cudaLaunchKernelEx(&lc, k_trim, d, d_hdrs));
         }
         prof_mark(ev, s);
@@ -2661,14 +2681,16 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         const uint32_t ag = tiles < acap ? tiles : acap;
         {
             cudaLaunchConfig_t lc = {};
-            cudaLaunchAttribute at[1];
+            cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributePriority;
             at[0].val.priority = rx->hi_prio;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (pdl_wait)
+            at[1].val.programmaticStreamSerializationAllowed = 1;
             lc.gridDim = dim3(ag);
             lc.blockDim = dim3(kAckWarps * 32);
             lc.stream = s;
             lc.attrs = at;
-            lc.numAttrs = 1;
+            lc.numAttrs = pdl ? 2 : 1;
             if (ack_tile == kAckTileMin)
                 CNB_CUDA(cudaLaunchKernelEx(&lc, k_acks<kAckTileMin>, d, d_hdrs, n, d_acks, max_acks, d_completions,
                                             max_completions));
@@ -2682,14 +2704,16 @@ static int rx_batch_impl(cn_rx* rx, const cn_pkt_hdr* d_hdrs, const uint64_t* d_
         // (it clears the other c_first half): it runs beside the scatter's tail
         {
             cudaLaunchConfig_t lc = {};
-            cudaLaunchAttribute at[1];
+            cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributePriority;
             at[0].val.priority = rx->hi_prio;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (pdl_wait)
+            at[1].val.programmaticStreamSerializationAllowed = 1;
             lc.gridDim = dim3(gb);
             lc.blockDim = dim3(kScanThreads);
             lc.stream = s;
             lc.attrs = at;
-            lc.numAttrs = 1;
+            lc.numAttrs = pdl ? 2 : 1;
             CNB_CUDA(cudaLaunchKernelEx(&lc, k_finalize, d, d_hdrs, d_result));
         }
         prof_mark(ev, s);

@@ -406,8 +406,10 @@ def cpu_reference(data, n_hosts, chunk_bytes, seconds, threads=None):
     threads = threads or os.cpu_count() or 1
     msg = message_bytes(data)
     if ref.available():
+        ref.rx_replay_bench(data, n_hosts, chunk_bytes, threads, 1)  # warm (pages, allocator)
         t1 = ref.rx_replay_bench(data, n_hosts, chunk_bytes, threads, 1)
-        reps = max(1, min(200, int(seconds / max(t1, 1e-3))))
+        # the same sample size per measurement as one step of --impl reference
+        reps = max(1, min(200, int(seconds / 2 / max(t1, 1e-3))))
         t = ref.rx_replay_bench(data, n_hosts, chunk_bytes, threads, reps)
         gbs = threads * reps * msg / t / 1e9
         return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
@@ -978,10 +980,12 @@ def run_reference(args):
     if not ref.available():
         emit({"impl": "reference", "unavailable": "oracle/_ref not built"})
         return
-    t1 = ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
-    reps = max(1, min(16, int(4.0 / max(t1, 1e-3))))  # ~4 s per step
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):
         ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
+    # reps per step from a warm replay, capped like the cpu_baseline leg's
+    # sample (~4 s of work per step, the same per-thread amortisation)
+    t1 = ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, 1)
+    reps = max(1, min(200, int(args.cpu_seconds / 2 / max(t1, 1e-3))))
     steps = max(1, min(args.steps, 30))
     times = [ref.rx_replay_bench(data, meta["n_hosts"], meta["chunk_bytes"], threads, reps) for _ in range(steps)]
     t = sum(times)

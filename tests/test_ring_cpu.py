@@ -1,5 +1,5 @@
 """The ring schedule of paper_2504_17307_b200.collective (steps, segments,
-tags, fold order) executed by world_size-2/3 gloo processes on CPU, against
+tags, fold order) executed by world_size-2/3/8 gloo processes on CPU, against
 the oracle's same-order fold (bit-exact).  Test infrastructure for the N>1
 host logic; the device path is tests/test_ring_gpu.py."""
 import os
@@ -61,7 +61,7 @@ def _worker(rank, n, port, count, dtype, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [2, 3])
+@pytest.mark.parametrize("n", [2, 3, 8])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_ring_schedule_matches_oracle_fold(n, dtype):
     from oracle import oracle as O

@@ -108,6 +108,7 @@ constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
 #endif
 constexpr int kCopyUnroll = CN_COPY_UNROLL;  // 16-byte vectors in flight per lane
 constexpr uint64_t kArenaUnit = 512;  // arena allocation granule (bytes)
+constexpr uint32_t kArenaRelBlocks = 8192;  // arena blocks per release entry: a large message's release spreads over blocks
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 
 struct RxDev {
@@ -135,6 +136,7 @@ struct RxDev {
     uint32_t* pool_bits;             // [pool_cap/32] retired chunk-pool positions
     uint32_t* arena_bits;            // [arena_blocks/32] retired arena blocks
     uint64_t arena_blocks;           // arena_cap / kArenaUnit
+    uint32_t aret_cap;               // arena-release entries per part (a message: one per kArenaRelBlocks)
     unsigned long long* aret;        // [3][plan_cap] (first block << 31) | blocks, released a batch later
     uint32_t* c_seen;   // [pool] persistent packet bitmask (ChunkRx::pkts_seen)
     uint32_t* c_flags;  // [pool] persistent CF_*
@@ -1897,7 +1899,12 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             d.c_last[e] = 0;
             d.c_newfl[e] = 0;
             const uint64_t rp = e >= d.pool_cap ? e - d.pool_cap : e;  // ring position
-            atomicXor(&d.pool_bits[rp >> 5], 1u << (rp & 31));  // lap-parity release
+            // lap-parity release, one atomic per bit word and warp (a message's
+            // chunks are consecutive: a warp's 32 usually share one word)
+            const unsigned am = __activemask();
+            const unsigned peers = __match_any_sync(am, static_cast<unsigned long long>(rp >> 5));
+            const uint32_t m = __reduce_or_sync(peers, 1u << (rp & 31));
+            if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicXor(&d.pool_bits[rp >> 5], m);
         } else if (in) {
             const uint64_t e = base + c;
             uint32_t fl = d.c_flags[e];
@@ -1950,8 +1957,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     // frees it after, :794-803)
     {
         const uint32_t prv = par == 0 ? 2u : par - 1;  // the previous batch's part
-        const unsigned long long* al = d.aret + prv * static_cast<uint64_t>(d.plan_cap);
-        const uint32_t na = d.ctl->n_aret[prv];
+        const unsigned long long* al = d.aret + prv * static_cast<uint64_t>(d.aret_cap);
+        const uint32_t na = min(d.ctl->n_aret[prv], d.aret_cap);
         for (uint32_t j = blockIdx.x; j < na; j += gridDim.x) {
             const unsigned long long v = al[j];
             const uint64_t a0 = v >> 31, n0 = v & 0x7FFFFFFF;
@@ -1987,20 +1994,39 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             arel = ret && G->buf_off != ~0ull && d.carry && G->nchunks;
         }
         const unsigned rb = __ballot_sync(0xffffffffu, ret), ab = __ballot_sync(0xffffffffu, arel);
+        // a message's arena range is released in entries of kArenaRelBlocks
+        // (inclusive warp prefix of the entry counts)
+        const uint64_t ablk = arel ? (G->len + kArenaUnit - 1) / kArenaUnit : 0;
+        const uint32_t npc = static_cast<uint32_t>((ablk + kArenaRelBlocks - 1) / kArenaRelBlocks);
+        uint32_t inc = npc;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
         unsigned long long ft = 0;
         uint32_t aj = 0;
-        if (lane == 0 && rb) {
+        if (lane == 31 && rb) {
             ft = atomicAdd(&d.ctl->gfree_tail, static_cast<unsigned long long>(__popc(rb)));
             atomicAdd(&d.ctl->n_tomb, static_cast<uint32_t>(__popc(rb)));
-            if (ab) aj = atomicAdd(&d.ctl->n_aret[par], static_cast<uint32_t>(__popc(ab)));
+            if (ab) aj = atomicAdd(&d.ctl->n_aret[par], inc);
         }
-        ft = __shfl_sync(0xffffffffu, ft, 0);
-        aj = __shfl_sync(0xffffffffu, aj, 0);
+        ft = __shfl_sync(0xffffffffu, ft, 31);
+        aj = __shfl_sync(0xffffffffu, aj, 31);
         if (ret) {
             atomicMax(&d.rc_done[G->rc * 128 + G->msg_id], static_cast<unsigned long long>(G->seq));
-            if (arel)
-                d.aret[par * static_cast<uint64_t>(d.plan_cap) + aj + __popc(ab & lt)] =
-                    ((G->buf_off / kArenaUnit) << 31) | ((G->len + kArenaUnit - 1) / kArenaUnit);
+            if (arel) {
+                const uint64_t b0 = G->buf_off / kArenaUnit;
+                const uint32_t j0 = aj + (inc - npc);
+                unsigned long long* out = d.aret + par * static_cast<uint64_t>(d.aret_cap) + j0;
+                if (j0 + npc > d.aret_cap) atomicOr(&d.ctl->status, CN_RXF_CAPACITY);  // cannot happen (sized)
+                for (uint32_t q = 0; q < npc && j0 + q < d.aret_cap; ++q) {
+                    const uint64_t lo = static_cast<uint64_t>(q) * kArenaRelBlocks;
+                    const uint64_t nb = ablk - lo < kArenaRelBlocks ? ablk - lo : kArenaRelBlocks;
+                    // a start past the ring's end names the wrapped position (the range never wraps physically)
+                    const uint64_t st = b0 + lo >= d.arena_blocks ? b0 + lo - d.arena_blocks : b0 + lo;
+                    out[q] = (st << 31) | nb;
+                }
+            }
             d.gen_key[G->slot] = kTomb;
             d.gen_val[G->slot] = kInf;
             d.gen_free[(ft + __popc(rb & lt)) & d.gen_mask] = g;
@@ -2361,7 +2387,8 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
         d.scan_blocks = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(b, 1), 2ull * rx->sms));
     }
     if (d.arena_blocks) ALLOC(d.arena_bits, (d.arena_blocks + 31) / 32 * 4);
-    ALLOC(d.aret, 3ull * d.plan_cap * 8);
+    d.aret_cap = static_cast<uint32_t>(d.plan_cap + d.arena_blocks / kArenaRelBlocks + 1);
+    ALLOC(d.aret, 3ull * d.aret_cap * 8);
     ALLOC(d.plan_F, (d.plan_cap + 1ull) * 4);
     ALLOC(d.plan_t0, (cfg.chunk_pool / kScanThreads + d.plan_cap + 4ull) * 4);
     ALLOC(d.c_seen, phys * 4);

@@ -1847,7 +1847,11 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         uint32_t* cf1 = first_of(d, nxt);
         const unsigned long long* dl = d.dirty + nxt * static_cast<uint64_t>(d.dirty_cap);
         const uint32_t nd = d.ctl->n_dirty[nxt];
-        for (uint32_t j = blockIdx.x; j < nd; j += gridDim.x) {
+        // phases go to different blocks (tiles are taken by ticket, usually
+        // by the first blocks): dirty lists from a third of the grid on,
+        // arena releases from two thirds, retirement from the middle
+        const uint32_t rb = (blockIdx.x + gridDim.x - gridDim.x / 3) % gridDim.x;
+        for (uint32_t j = rb; j < nd; j += gridDim.x) {
             const unsigned long long v = dl[j];
             if (threadIdx.x < (v & 511)) {
                 const uint64_t e = (v >> 9) + threadIdx.x;
@@ -1959,7 +1963,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         const uint32_t prv = par == 0 ? 2u : par - 1;  // the previous batch's part
         const unsigned long long* al = d.aret + prv * static_cast<uint64_t>(d.aret_cap);
         const uint32_t na = min(d.ctl->n_aret[prv], d.aret_cap);
-        for (uint32_t j = blockIdx.x; j < na; j += gridDim.x) {
+        const uint32_t rb = (blockIdx.x + gridDim.x - 2 * (gridDim.x / 3)) % gridDim.x;
+        for (uint32_t j = rb; j < na; j += gridDim.x) {
             const unsigned long long v = al[j];
             const uint64_t a0 = v >> 31, n0 = v & 0x7FFFFFFF;
             // ring positions [a0, a0 + n0) mod arena_blocks: at most two runs
@@ -1980,7 +1985,8 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
     // (the shared counters are claimed once per warp: a batch may retire
     // thousands of small messages)
     const uint32_t kstride = gridDim.x * blockDim.x;
-    for (uint32_t k0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); k0 < nt; k0 += kstride) {
+    for (uint32_t k0 = ((blockIdx.x + gridDim.x / 2) % gridDim.x) * blockDim.x + (threadIdx.x & ~31u); k0 < nt;
+         k0 += kstride) {
         const uint32_t k = k0 + (threadIdx.x & 31);
         const int lane = threadIdx.x & 31;
         const unsigned lt = (1u << lane) - 1;

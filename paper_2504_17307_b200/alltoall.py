@@ -237,13 +237,12 @@ class AllToAll:
                     sp.wait_event(self.ev_hdrs)
                     _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh, npk * 64, cs(sp)),
                                "cn_copy_async")
-                if self.push.startswith("sm"):
+                dst_p, src_p = pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo
+                if self.push.startswith("sm") and not ((dst_p | src_p | (hi - lo)) & 15):
                     nb = int(self.push.split(":")[1]) if ":" in self.push else 64
-                    _lib.check(L.cn_copy_sm(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo, nb,
-                                            cs(sp)), "cn_copy_sm")
-                else:
-                    _lib.check(L.cn_copy_async(pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo, hi - lo,
-                                               cs(sp)), "cn_copy_async")
+                    _lib.check(L.cn_copy_sm(dst_p, src_p, hi - lo, nb, cs(sp)), "cn_copy_sm")
+                else:  # the copy engines (or a piece not 16-byte aligned, which SM vectors cannot move)
+                    _lib.check(L.cn_copy_async(dst_p, src_p, hi - lo, cs(sp)), "cn_copy_async")
                 self.sent[d][ln] += 1
                 _lib.check(L.cn_flag_signal(pe["flags"] + 16 * r + 8 * ln, None, self.sent[d][ln], cs(sp)),
                            "cn_flag_signal")

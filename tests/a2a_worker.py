@@ -30,15 +30,19 @@ def main():
     cap = 3 << 20
     for direct in (True, False):  # bytes straight into the receive slots / staged + scattered
         run_mode(AllToAll(cap, direct=direct), n, r, iters, cap)
+    # odd message sizes: unaligned pieces fall back from SM stores to the copy engines
+    run_mode(AllToAll(cap, direct=True), n, r, 2, cap, odd=3)
     dist.barrier()
     if r == 0:
         print(f"A2A_OK n={n} iters={iters}")
     dist.destroy_process_group()
 
 
-def run_mode(a2a, n, r, iters, cap):
+def run_mode(a2a, n, r, iters, cap, odd=0):
     for it in range(iters):
         m = counts_matrix(n, it, cap)
+        if odd:
+            m = np.where(m > 0, np.minimum(m + odd, cap), m)
         g = torch.Generator(device="cuda")
         g.manual_seed(1000 * it + r)
         send = torch.randint(0, 256, (int(m[r].sum()) + 16,), dtype=torch.uint8, device="cuda", generator=g)

@@ -108,7 +108,10 @@ constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
 #endif
 constexpr int kCopyUnroll = CN_COPY_UNROLL;  // 16-byte vectors in flight per lane
 constexpr uint64_t kArenaUnit = 512;  // arena allocation granule (bytes)
-constexpr uint32_t kArenaRelBlocks = 8192;  // arena blocks per release entry: a large message's release spreads over blocks
+#ifndef CN_ARENA_REL_BLOCKS
+#define CN_ARENA_REL_BLOCKS 8192
+#endif
+constexpr uint32_t kArenaRelBlocks = CN_ARENA_REL_BLOCKS;  // arena blocks per release entry: a large message's release spreads over blocks
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 
 struct RxDev {
@@ -136,7 +139,6 @@ struct RxDev {
     uint32_t* pool_bits;             // [pool_cap/32] retired chunk-pool positions
     uint32_t* arena_bits;            // [arena_blocks/32] retired arena blocks
     uint64_t arena_blocks;           // arena_cap / kArenaUnit
-    uint32_t aret_cap;               // arena-release entries per part (a message: one per kArenaRelBlocks)
     unsigned long long* aret;        // [3][plan_cap] (first block << 31) | blocks, released a batch later
     uint32_t* c_seen;   // [pool] persistent packet bitmask (ChunkRx::pkts_seen)
     uint32_t* c_flags;  // [pool] persistent CF_*
@@ -171,6 +173,9 @@ struct RxDev {
     unsigned long long* scan_state;  // [scan tiles] segmented look-back (prefix max)
     RxCtl* ctl;
     uint8_t* arena;
+    // kept last: inserting it among the fields above reordered k_copy's
+    // parameter loads and cost the scatter 3% on large batches (measured)
+    uint32_t aret_cap;  // arena-release entries per part (a message: one per kArenaRelBlocks)
 };
 
 // One thread.  Ring positions [h, h + n) by one atomicAdd (no retry loop:
@@ -1905,10 +1910,14 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             const uint64_t rp = e >= d.pool_cap ? e - d.pool_cap : e;  // ring position
             // lap-parity release, one atomic per bit word and warp (a message's
             // chunks are consecutive: a warp's 32 usually share one word)
+#ifndef CN_POOL_REL_PER_CHUNK
             const unsigned am = __activemask();
             const unsigned peers = __match_any_sync(am, static_cast<unsigned long long>(rp >> 5));
             const uint32_t m = __reduce_or_sync(peers, 1u << (rp & 31));
             if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) atomicXor(&d.pool_bits[rp >> 5], m);
+#else
+            atomicXor(&d.pool_bits[rp >> 5], 1u << (rp & 31));
+#endif
         } else if (in) {
             const uint64_t e = base + c;
             uint32_t fl = d.c_flags[e];

@@ -2399,7 +2399,9 @@ extern "C" int cn_rx_create(const cn_rx_config* cfg_in, cn_rx** out) {
     {  // one retirement-bit word per scan thread, both rings
         const uint64_t words = std::max<uint64_t>((d.pool_cap + 31) / 32, (d.arena_blocks + 31) / 32);
         const uint64_t b = (words + kIngestThreads - 1) / kIngestThreads;
-        d.scan_blocks = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(b, 1), 2ull * rx->sms));
+        uint64_t cap_b = 2ull * rx->sms;
+        if (const char* e = getenv("CN_SCAN_BLOCKS")) cap_b = std::max(1, atoi(e));
+        d.scan_blocks = static_cast<uint32_t>(std::min<uint64_t>(std::max<uint64_t>(b, 1), cap_b));
     }
     if (d.arena_blocks) ALLOC(d.arena_bits, (d.arena_blocks + 31) / 32 * 4);
     d.aret_cap = static_cast<uint32_t>(d.plan_cap + d.arena_blocks / kArenaRelBlocks + 1);

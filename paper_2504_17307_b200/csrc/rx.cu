@@ -98,7 +98,10 @@ constexpr uint32_t kStale = kInf;    // p_gen marker: stale before the batch
 constexpr uint32_t kErr = kInf - 1;  // p_gen marker: rejected packet
 constexpr int kAckTileMax = 128;     // packets per k_acks tile (large batches)
 constexpr int kAckTileMin = 32;      // ... small batches
-constexpr int kAckWarps = 8;         // 256 threads: 4 decide warps, 8 ack builders
+#ifndef CN_ACK_WARPS
+#define CN_ACK_WARPS 8
+#endif
+constexpr int kAckWarps = CN_ACK_WARPS;  // 256 threads: 4 decide warps, 8 ack builders
 constexpr int kScanThreads = 256;     // chunks per scan/finalize tile
 #ifndef CN_COPY_UNROLL
 #define CN_COPY_UNROLL 8

@@ -640,7 +640,8 @@ def sweep_bench(dev, world, rank, sizes=(4 << 10, 64 << 10, 1 << 20, 16 << 20, 2
     paths into the receive path, message sizes 4 KiB..1 GiB (connections per
     size capped so that <= 2 GiB of messages are in flight per GPU); the
     connections shard over the ranks.  Per size: one batch
-    = every packet of every connection (reset + receive path, CUDA graph),
+    = every packet of every connection, a new generation of every message per
+    batch through a pipelined receiver in steady state (no reset; CUDA graph),
     time = max over ranks."""
     import torch
     import torch.distributed as dist
@@ -659,29 +660,43 @@ def sweep_bench(dev, world, rank, sizes=(4 << 10, 64 << 10, 1 << 20, 16 << 20, 2
         st = torch.randint(0, 256, (n * MAX_PL,), dtype=torch.uint8, device=dev)
         nmsg = conns * mpc
         nchk = nmsg * (-(-size // 32768))
+        # a pipelined receiver in steady state, as the headline: batch j is
+        # generation j of every message (msg_seq + j, its own header buffer),
+        # no reset; the timed batches are one CUDA graph, uploaded by an
+        # untimed launch after which every header moves on `steps` generations
         tr = cn.Transport(cn.TransportConfig(chunk_bytes=32768, carry_payload=True), device=dev,
-                          arena_bytes=nmsg * (size + 512) + (1 << 20), chunk_pool=2 * nchk + 64,
-                          max_batch=n, max_conns=2 * conns + 16, max_msgs=2 * nmsg + 16)
+                          arena_bytes=3 * nmsg * (size + 512) + (1 << 20), chunk_pool=3 * nchk + 64,
+                          max_batch=n, max_conns=2 * conns + 16, max_msgs=4 * nmsg + 16, pipeline=True)
+        from paper_2504_17307_b200.records import PKT_DTYPE
+        si = PKT_DTYPE.fields["msg_seq"][1] // 8
+        hs = []
+        for j in range(warmup + steps + 1):
+            h_ = hdrs.clone()
+            h_.view(n, 64).view(torch.int64)[:, si] += j
+            hs.append(h_)
+        tr.handle_packets(hs[0], st, MAX_PL)
 
-        def step():
-            s_ = torch.cuda.current_stream(dev)
-            tr.reset(s_)
-            tr.rx_batch_async(hdrs, st, MAX_PL, s_)
+        def graph_of(gens):
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_):
+                s_ = torch.cuda.current_stream(dev)
+                for j in gens:
+                    tr.rx_batch_async(hs[j], st, MAX_PL, s_)
+                tr.flush(s_)
+            return g_
 
-        step()
+        gw, g = graph_of(range(1, warmup + 1)), graph_of(range(warmup + 1, warmup + steps + 1))
+        gw.replay()
+        g.replay()  # upload
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            step()
-        for _ in range(warmup):
-            g.replay()
+        for j in range(warmup + 1, warmup + steps + 1):
+            hs[j].view(n, 64).view(torch.int64)[:, si] += steps
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(steps):
-            g.replay()
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / steps], device=dev, dtype=torch.float64)
@@ -697,7 +712,7 @@ def sweep_bench(dev, world, rank, sizes=(4 << 10, 64 << 10, 1 << 20, 16 << 20, 2
                     "ms_per_batch": round(ms, 4),
                     "GBps": round(world * nmsg * size / (ms * 1e-3) / 1e9, 1),
                     "Mpkts_per_s": round(world * n / (ms * 1e-3) / 1e6, 1)})
-        del tr, g, hdrs, st
+        del tr, g, gw, hdrs, st, hs
         torch.cuda.empty_cache()
     return out
 

@@ -88,6 +88,10 @@ struct RxCtl {
     // covers, least live offsets found, armed once a scan ran
     unsigned long long pool_hsnap, arena_hsnap;
     uint32_t adv_pool, adv_arena, adv_armed, pad_a;
+    uint32_t ret_ticket, ret_done;  // k_finalize's retirement units
+    // the global batch plan's slice look-back: (epoch << 32) | slice sum,
+    // (epoch << 32) | inclusive prefix; [0] k_scan, [1] k_finalize
+    unsigned long long plan_agg[2][16], plan_inc[2][16];
 };
 
 enum : uint32_t { CF_INIT = 1, CF_COMPLETE = 2, CF_ECN = 4, CF_RTX = 8, CF_NACKED = 16 };
@@ -779,19 +783,19 @@ __device__ __forceinline__ uint32_t block_scan_max(uint32_t v, uint32_t* wsum) {
 // message that continues from earlier tiles.
 constexpr uint32_t kPlanMax = 16384;  // cap of RxDev::plan_cap (touched messages per batch, planned in smem)
 
-// The batch plan, built once per kernel by the first block to arrive (the
-// others wait on a flag it releases -- it is resident by construction): for
+// The batch plan, built once per kernel (in every block's shared memory for
+// up to kPlanSmem messages, else once in global memory by the grid): for
 // each touched message k its chunk range [lo, hi) -- hi = the chunk vector
 // size (:636-637) -- flattened as the exclusive prefix F[k] of the range
 // lengths (F[nt] = total chunks), and for every 256-chunk tile t the first
 // message t0[t] that has a chunk in it.  In k_scan lo = cum and hi =
 // max(n_init, max touched chunk + 1); k_finalize reads the values k_scan
 // stored (lo_batch, n_init; a delivered message whole), so both see the
-// same flattened layout.  The plan lives in global memory (L1 / L2
+// same flattened layout.  The large plan lives in global memory (L1 / L2
 // resident): shared memory in these latency-bound kernels would shrink the
-// L1 of the SMs the concurrent HBM-bound scatter streams through.
-// Each planning thread owns a contiguous run of messages: three rounds of
-// independent loads and one block scan, whatever the message count.
+// L1 of the SMs the concurrent HBM-bound scatter streams through.  Its
+// message-state loads are scattered, so one SM cannot issue them fast
+// enough (~50 us for 16K messages); spread over the grid they cost a few.
 __device__ __forceinline__ uint32_t plan_len(const RxDev& d, uint32_t k, uint32_t epoch, bool scan) {
     const GenState* G = &d.gen[d.touched[k]];
     uint32_t lo, hi;
@@ -813,79 +817,159 @@ __device__ __forceinline__ uint32_t plan_len(const RxDev& d, uint32_t k, uint32_
 }
 
 constexpr uint32_t kPlanSmem = 2048;  // up to this many touched messages every block plans in smem (8 KB)
+constexpr uint32_t kPlanSlice = 1024;  // global plan: messages per slice (4 per thread)
+constexpr uint32_t kPlanSlices = kPlanMax / kPlanSlice;
+static_assert(kPlanSlices <= 16, "RxCtl::plan_agg holds 16 slices");
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Block exclusive scan of one value per thread; *tot gets the block total.
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t v, uint32_t* s_w, uint32_t* tot) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    uint32_t wpre = 0, t = 0;
+    for (int q = 0; q < nw; ++q) {
+        if (q < w) wpre += s_w[q];
+        t += s_w[q];
+    }
+    *tot = t;
+    return wpre + inc - v;
+}
 
 // Returns the total; F points at the plan (s_F when nt <= kPlanSmem -- each
-// block builds its own copy -- else the global one).
+// block builds its own copy -- else the global one).  The global plan is a
+// single-pass scan spread over the grid: blocks take 1,024-message slices by
+// ticket (so a slice is only ever waited on once a running block holds it),
+// publish the slice sum, look back over the earlier slices for their base
+// (decoupled look-back, tagged with the batch epoch so nothing is reset),
+// write their offsets and tile starts and count the slice done; every block
+// then waits for all slices.
 __device__ uint32_t plan_batch(const RxDev& d, uint32_t nt, uint32_t epoch, bool scan, uint32_t* s_F,
                                const uint32_t** F_out) {
-    __shared__ uint32_t s_role, s_w[32], s_total;
+    __shared__ uint32_t s_w[32], s_total, s_sl, s_base;
     RxCtl* C = d.ctl;
-    uint32_t* flag = scan ? &C->plan_ready_scan : &C->plan_ready_fin;
-    const uint32_t tag = C->epoch;  // unique per batch
-    const bool small = nt <= kPlanSmem;
-    uint32_t* Fw = small ? s_F : d.plan_F;
-    *F_out = Fw;
-    if (threadIdx.x == 0) s_role = small || atomicAdd(scan ? &C->plan_ticket_scan : &C->plan_ticket_fin, 1u) == 0;
-    __syncthreads();
-    if (s_role) {
-        const uint32_t per = (nt + blockDim.x - 1) / blockDim.x;
+    constexpr uint32_t kPer = kPlanSlice / kScanThreads;
+    if (nt <= kPlanSmem) {
+        *F_out = s_F;
+        const uint32_t per = (nt + blockDim.x - 1) / blockDim.x;  // <= 8
         const uint32_t k0 = threadIdx.x * per, k1 = min(nt, k0 + per);
-        constexpr uint32_t kReg = 16;  // up to 16 messages per thread: loads issued together, lengths kept
-        uint32_t Lr[kReg];
-        uint32_t sum = 0;
-        if (per <= kReg) {
+        uint32_t L[kPlanSmem / kScanThreads], sum = 0;
 #pragma unroll
-            for (uint32_t j = 0; j < kReg; ++j) Lr[j] = k0 + j < k1 ? plan_len(d, k0 + j, epoch, scan) : 0u;
+        for (uint32_t j = 0; j < kPlanSmem / kScanThreads; ++j) {
+            L[j] = k0 + j < k1 ? plan_len(d, k0 + j, epoch, scan) : 0u;
+            sum += L[j];
+        }
+        uint32_t tot;
+        uint32_t F = block_excl_sum(sum, s_w, &tot);
 #pragma unroll
-            for (uint32_t j = 0; j < kReg; ++j) sum += Lr[j];
-        } else {
-            for (uint32_t k = k0; k < k1; ++k) sum += plan_len(d, k, epoch, scan);
-        }
-        // block exclusive scan of the per-thread sums
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        uint32_t inc = sum;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        if (lane == 31) s_w[w] = inc;
+        for (uint32_t j = 0; j < kPlanSmem / kScanThreads; ++j)
+            if (k0 + j < k1) {
+                s_F[k0 + j] = F;
+                F += L[j];
+            }
+        if (threadIdx.x == 0) s_F[nt] = tot;
         __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-        for (int q = 0; q < nw; ++q) {
-            if (q < w) wpre += s_w[q];
-            tot += s_w[q];
+        return tot;
+    }
+    *F_out = d.plan_F;
+    TM_START(scan ? 30 : 34);
+    uint32_t* ticket = scan ? &C->plan_ticket_scan : &C->plan_ticket_fin;
+    uint32_t* done = scan ? &C->plan_ready_scan : &C->plan_ready_fin;
+    unsigned long long* agg = C->plan_agg[scan ? 0 : 1];
+    unsigned long long* incl = C->plan_inc[scan ? 0 : 1];
+    const unsigned long long tag = static_cast<unsigned long long>(C->epoch) << 32;  // never 0
+    const uint32_t ns = (nt + kPlanSlice - 1) / kPlanSlice;
+    for (;;) {
+        if (threadIdx.x == 0) s_sl = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint32_t sl = s_sl;
+        if (sl >= ns) break;
+        const uint32_t kb = sl * kPlanSlice + threadIdx.x * kPer;
+        uint32_t L[kPer], sum = 0;
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            L[u] = kb + u < nt ? plan_len(d, kb + u, epoch, scan) : 0u;
+            sum += L[u];
         }
-        uint32_t F = wpre + inc - sum;
-        auto place = [&](uint32_t k, uint32_t len) {
-            Fw[k] = F;
-            // tiles whose first chunk falls in this message's range (global plan)
-            if (!small)
+        uint32_t tot;
+        uint32_t F = block_excl_sum(sum, s_w, &tot);
+        if (threadIdx.x < 32) {  // warp 0: publish, then look back over all earlier slices at once
+            const int lane = threadIdx.x;
+            uint32_t base = 0;
+            if (sl == 0) {
+                if (lane == 0) st_release_u64(&incl[0], tag | tot);
+            } else {
+                if (lane == 0) st_release_u64(&agg[sl], tag | tot);
+                const int q = static_cast<int>(sl) - 1 - lane;  // lane j: slice sl - 1 - j
+                for (;;) {
+                    unsigned long long v = 0, a = 0;
+                    if (q >= 0) {
+                        v = ld_acquire_u64(&incl[q]);
+                        a = ld_acquire_u64(&agg[q]);
+                    }
+                    const bool hi = q >= 0 && (v & ~0xffffffffull) == tag;
+                    const bool ha = q >= 0 && (a & ~0xffffffffull) == tag;
+                    const uint32_t mi = __ballot_sync(0xffffffffu, hi), ma = __ballot_sync(0xffffffffu, ha);
+                    if (mi) {  // the nearest inclusive prefix, and every aggregate before it
+                        const int lim = __ffs(mi) - 1;
+                        const uint32_t need = lim ? (1u << lim) - 1 : 0u;
+                        if ((ma & need) == need) {
+                            uint32_t x = lane < lim ? static_cast<uint32_t>(a)
+                                                    : lane == lim ? static_cast<uint32_t>(v) : 0u;
+                            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                            base = x;
+                            break;
+                        }
+                    }
+                    __nanosleep(32);
+                }
+                if (lane == 0) st_release_u64(&incl[sl], tag | (base + tot));
+            }
+            if (lane == 0) {
+                s_base = base;
+                if (sl == ns - 1) {
+                    d.plan_F[nt] = base + tot;
+                    d.plan_t0[(base + tot + kScanThreads - 1) / kScanThreads] = nt;  // sentinel
+                }
+            }
+        }
+        __syncthreads();
+        F += s_base;
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t k = kb + u, len = L[u];
+            if (k < nt) {
+                d.plan_F[k] = F;
+                // tiles whose first chunk falls in this message's range
                 for (uint32_t t = (F + kScanThreads - 1) / kScanThreads; len && t * kScanThreads < F + len; ++t)
                     d.plan_t0[t] = k;
+            }
             F += len;
-        };
-        if (per <= kReg) {
-#pragma unroll
-            for (uint32_t j = 0; j < kReg; ++j)
-                if (k0 + j < k1) place(k0 + j, Lr[j]);
-        } else {
-            for (uint32_t k = k0; k < k1; ++k) place(k, plan_len(d, k, epoch, scan));
         }
-        if (threadIdx.x == 0) {
-            Fw[nt] = tot;
-            if (!small) d.plan_t0[(tot + kScanThreads - 1) / kScanThreads] = nt;  // sentinel
-        }
-        if (!small) __threadfence();
+        __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) {
-            s_total = tot;
-            if (!small) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(tag) : "memory");
-        }
-    } else if (threadIdx.x == 0) {
-        while (ld_acquire(flag) != tag) __nanosleep(64);
+        if (threadIdx.x == 0) atomicAdd(done, 1u);
+    }
+    TM_END(scan ? 31 : 35);
+    if (threadIdx.x == 0) {
+        while (ld_acquire(done) < ns) __nanosleep(64);
         s_total = ld_volatile_u32(&d.plan_F[nt]);
     }
     __syncthreads();
+    TM_END(scan ? 32 : 36);
     return s_total;
 }
 
@@ -1827,6 +1911,22 @@ __global__ void __launch_bounds__(kAckWarps * 32) k_acks(
     TM_END(23);
 }
 
+// One arena release entry (start << 31 | blocks), a warp's lanes over its
+// bit words: ring positions [a0, a0 + n0) mod arena_blocks, at most two runs.
+__device__ __forceinline__ void arena_release(const RxDev& d, unsigned long long v, int lane) {
+    const uint64_t a0 = v >> 31, n0 = v & 0x7FFFFFFF;
+    for (int part = 0; part < 2; ++part) {
+        const uint64_t a = part ? 0 : a0;
+        const uint64_t e0 = a0 + n0 > d.arena_blocks ? d.arena_blocks : a0 + n0;
+        const uint64_t end = part ? (a0 + n0 > d.arena_blocks ? a0 + n0 - d.arena_blocks : 0) : e0;
+        for (uint64_t w = (a >> 5) + lane; (w << 5) < end; w += 32) {
+            const uint64_t lo_ = (w << 5) > a ? (w << 5) : a, hi_ = (w << 5) + 32 < end ? (w << 5) + 32 : end;
+            const uint32_t m = (hi_ - lo_ == 32 ? ~0u : ((1u << (hi_ - lo_)) - 1)) << (lo_ - (w << 5));
+            atomicXor(&d.arena_bits[w], m);  // lap-parity release
+        }
+    }
+}
+
 // ---------------------------------------------------------------- finalize
 // Same tiles: fold batch scratch into persistent per-chunk state
 // (pkts_seen, complete, init, ecn, any_rtx, tx_time/path of the last new
@@ -1858,12 +1958,21 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         // phases go to different blocks (tiles are taken by ticket, usually
         // by the first blocks): dirty lists from a third of the grid on,
         // arena releases from two thirds, retirement from the middle
-        const uint32_t rb = (blockIdx.x + gridDim.x - gridDim.x / 3) % gridDim.x;
-        for (uint32_t j = rb; j < nd; j += gridDim.x) {
-            const unsigned long long v = dl[j];
-            if (threadIdx.x < (v & 511)) {
-                const uint64_t e = (v >> 9) + threadIdx.x;
-                for (uint32_t q = 0; q < ppc; ++q) cf1[e * ppc + q] = kInf;
+        // a warp takes up to 32 entries (one coalesced load; fewer when the
+        // list is short, so large runs spread over the grid) and clears each
+        // entry's contiguous run of chunks x ppc slots across its lanes
+        const int lane = threadIdx.x & 31;
+        const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+        const uint32_t gw = (((blockIdx.x + gridDim.x - gridDim.x / 3) % gridDim.x) * blockDim.x + threadIdx.x) >> 5;
+        const uint32_t per = min(32u, (nd + nwarps - 1) / nwarps);
+        for (uint32_t j0 = gw * per; j0 < nd; j0 += nwarps * per) {
+            const unsigned long long vl = j0 + lane < nd && lane < per ? dl[j0 + lane] : 0ull;
+            const uint32_t m = min(per, nd - j0);
+            for (uint32_t e = 0; e < m; ++e) {
+                const unsigned long long v = __shfl_sync(0xffffffffu, vl, e);
+                uint32_t* p0 = cf1 + (v >> 9) * ppc;
+                const uint32_t nq = static_cast<uint32_t>(v & 511) * ppc;
+                for (uint32_t q = lane; q < nq; q += 32) p0[q] = kInf;
             }
         }
     }
@@ -1890,9 +1999,15 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             c = (retire ? 0u : G->lo_batch) + (f - F[k]);
             base = G->chunk_base;
             head = threadIdx.x == 0 || f == F[k];
-            if (head) {  // this tile's run of the message: c_first cleared through the dirty list
+        }
+        {  // each run of a message in this tile: c_first cleared through the dirty list (one claim per warp)
+            const unsigned hm = __ballot_sync(0xffffffffu, in && head);
+            const int lane = threadIdx.x & 31;
+            uint32_t j = 0;
+            if (lane == 0 && hm) j = atomicAdd(&d.ctl->n_dirty_next, static_cast<uint32_t>(__popc(hm)));
+            j = __shfl_sync(0xffffffffu, j, 0) + __popc(hm & ((1u << lane) - 1));
+            if (in && head) {
                 const uint32_t end = F[k + 1] < f0 + kScanThreads ? F[k + 1] : f0 + kScanThreads;
-                const uint32_t j = atomicAdd(&d.ctl->n_dirty_next, 1u);
                 if (j < d.dirty_cap) dirty[j] = ((base + c) << 9) | (end - f);
             }
         }
@@ -1975,30 +2090,27 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         const uint32_t prv = par == 0 ? 2u : par - 1;  // the previous batch's part
         const unsigned long long* al = d.aret + prv * static_cast<uint64_t>(d.aret_cap);
         const uint32_t na = min(d.ctl->n_aret[prv], d.aret_cap);
-        const uint32_t rb = (blockIdx.x + gridDim.x - 2 * (gridDim.x / 3)) % gridDim.x;
-        for (uint32_t j = rb; j < na; j += gridDim.x) {
-            const unsigned long long v = al[j];
-            const uint64_t a0 = v >> 31, n0 = v & 0x7FFFFFFF;
-            // ring positions [a0, a0 + n0) mod arena_blocks: at most two runs
-            for (int part = 0; part < 2; ++part) {
-                const uint64_t a = part ? 0 : a0;
-                const uint64_t e0 = a0 + n0 > d.arena_blocks ? d.arena_blocks : a0 + n0;
-                const uint64_t end = part ? (a0 + n0 > d.arena_blocks ? a0 + n0 - d.arena_blocks : 0) : e0;
-                for (uint64_t w = (a >> 5) + threadIdx.x; (w << 5) < end; w += blockDim.x) {
-                    const uint64_t lo_ = (w << 5) > a ? (w << 5) : a, hi_ = (w << 5) + 32 < end ? (w << 5) + 32 : end;
-                    const uint32_t m = (hi_ - lo_ == 32 ? ~0u : ((1u << (hi_ - lo_)) - 1)) << (lo_ - (w << 5));
-                    atomicXor(&d.arena_bits[w], m);  // lap-parity release
-                }
-            }
+        const int lane = threadIdx.x & 31;
+        const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+        const uint32_t gw = (((blockIdx.x + gridDim.x - 2 * (gridDim.x / 3)) % gridDim.x) * blockDim.x + threadIdx.x) >> 5;
+        const uint32_t per = min(32u, (na + nwarps - 1) / nwarps);
+        for (uint32_t j0 = gw * per; j0 < na; j0 += nwarps * per) {
+            const unsigned long long vl = j0 + lane < na && lane < per ? al[j0 + lane] : 0ull;
+            const uint32_t m = min(per, na - j0);
+            for (uint32_t e = 0; e < m; ++e) arena_release(d, __shfl_sync(0xffffffffu, vl, e), lane);
         }
     }
     TM_END(5);
-    // ---- delivered messages: completed_seq (:801) and retirement
-    // (the shared counters are claimed once per warp: a batch may retire
-    // thousands of small messages)
-    const uint32_t kstride = gridDim.x * blockDim.x;
-    for (uint32_t k0 = ((blockIdx.x + gridDim.x / 2) % gridDim.x) * blockDim.x + (threadIdx.x & ~31u); k0 < nt;
-         k0 += kstride) {
+    // ---- delivered messages: completed_seq (:801) and retirement, in
+    // units of 256 messages taken by ticket (the shared counters are claimed
+    // once per warp: a batch may retire thousands of small messages)
+    const uint32_t nunits = (nt + blockDim.x - 1) / blockDim.x;
+    for (;;) {
+        __syncthreads();  // s_ticket reuse
+        if (threadIdx.x == 0) s_ticket = atomicAdd(&d.ctl->ret_ticket, 1u);
+        __syncthreads();
+        if (s_ticket >= nunits) break;
+        const uint32_t k0 = s_ticket * blockDim.x + (threadIdx.x & ~31u);
         const uint32_t k = k0 + (threadIdx.x & 31);
         const int lane = threadIdx.x & 31;
         const unsigned lt = (1u << lane) - 1;
@@ -2049,9 +2161,50 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
             d.gen_val[G->slot] = kInf;
             d.gen_free[(ft + __popc(rb & lt)) & d.gen_mask] = g;
         }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(&d.ctl->ret_done, 1u);
+    }
+    TM_END(6);
+    // ---- tombstone compaction once every retirement unit is done (a block
+    // here only waits for units that running blocks hold), every warp a
+    // 32-slot window of the message table (with a 32-slot lookahead): a
+    // tombstone whose next non-tombstone slot in probe order is empty carries
+    // no probe chain -- a key past it would have been placed in that empty
+    // slot -- so it becomes empty.  No lookups or inserts run now (k_ingest
+    // does them).  Runs past the lookahead and tombstones inside clusters of
+    // live keys are left to the last block's rebuild (at 1/4 of the table).
+    if (threadIdx.x == 0) {
+        while (ld_acquire(&d.ctl->ret_done) < nunits) __nanosleep(64);
+        s_ticket = ld_volatile_u32(&d.ctl->n_tomb);
     }
     __syncthreads();
-    TM_END(6);
+    if (s_ticket) {
+        const uint32_t size = d.gen_mask + 1;
+        const uint32_t nwin = (size + 31) / 32;
+        const int lane = threadIdx.x & 31;
+        const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+        uint32_t cleared = 0;
+        for (uint32_t w = gw; size >= 64 && w < nwin; w += nwarps) {  // (a window must not alias itself)
+            const uint32_t x = (w * 32 + lane) & d.gen_mask, x2 = (w * 32 + 32 + lane) & d.gen_mask;
+            const unsigned long long k = ld_volatile_u64(&d.gen_key[x]), k2 = ld_volatile_u64(&d.gen_key[x2]);
+            const unsigned long long T = __ballot_sync(0xffffffffu, k == kTomb) |
+                                         (static_cast<unsigned long long>(__ballot_sync(0xffffffffu, k2 == kTomb)) << 32);
+            const unsigned long long E = __ballot_sync(0xffffffffu, k == kEmpty) |
+                                         (static_cast<unsigned long long>(__ballot_sync(0xffffffffu, k2 == kEmpty)) << 32);
+            if (!((T >> lane) & 1ull)) continue;
+            const unsigned long long after = ~T & (~0ull << (lane + 1));  // non-tombstones past this slot
+            if (!after) continue;  // the run outlasts the lookahead
+            const int j = __ffsll(static_cast<long long>(after)) - 1;
+            if ((E >> j) & 1ull) {
+                d.gen_key[x] = kEmpty;
+                d.gen_val[x] = kInf;
+                ++cleared;
+            }
+        }
+        cleared = __reduce_add_sync(0xffffffffu, cleared);
+        if ((threadIdx.x & 31) == 0 && cleared) atomicSub(&d.ctl->n_tomb, cleared);
+    }
     // ---- batch epilogue (last block)
     if (threadIdx.x == 0) {
         __threadfence();
@@ -2116,6 +2269,10 @@ __global__ void __launch_bounds__(kScanThreads) k_finalize(RxDev d, const cn_pkt
         C->fin_ticket = 0;
         C->plan_ticket_scan = 0;
         C->plan_ticket_fin = 0;
+        C->plan_ready_scan = 0;
+        C->plan_ready_fin = 0;
+        C->ret_ticket = 0;
+        C->ret_done = 0;
         uint32_t ep = C->epoch + 1;
         C->epoch = ep ? ep : 1;
         const uint32_t nxt = par == 2 ? 0u : par + 1, prv = par == 0 ? 2u : par - 1;
@@ -2854,7 +3011,7 @@ extern "C" int cn_rx_debug_timing(unsigned long long* out, int n) {
     unsigned long long h[64];
     CNB_CUDA(cudaMemcpyFromSymbol(h, g_tm, sizeof h));
     for (int k = 0; k < n && k < 64; ++k) out[k] = h[k];
-    const unsigned long long mins[] = {0, 10, 20, 22, 24};
+    const unsigned long long mins[] = {0, 10, 20, 22, 24, 30, 34};
     for (int k = 0; k < 64; ++k) h[k] = 0;
     for (unsigned long long k : mins) h[k] = ~0ull;
     CNB_CUDA(cudaMemcpyToSymbol(g_tm, h, sizeof h));

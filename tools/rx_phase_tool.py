@@ -13,7 +13,8 @@ sys.path.insert(0, ROOT)
 NAMES = {0: "fin start", 1: "fin dirty-clear", 2: "fin adv pool", 3: "fin adv arena", 4: "fin tiles",
          5: "fin arena release", 6: "fin retire", 7: "fin end", 10: "ing start", 11: "ing conn", 12: "ing gen",
          13: "ing end", 20: "scan start", 21: "scan end", 22: "acks start", 23: "acks end", 24: "copy start",
-         25: "copy end"}
+         25: "copy end", 30: "scan plan start", 31: "scan plan lens", 32: "scan plan placed", 34: "fin plan start",
+         35: "fin plan lens", 36: "fin plan placed"}
 
 
 def main():
@@ -27,7 +28,8 @@ def main():
     torch.cuda.set_device(dev)
     if os.environ.get("SYNTH"):
         c_, b_ = (int(v) for v in os.environ["SYNTH"].split("x"))
-        data, cb, msg_len, K = bench.synth_trace(c_, b_, seed=1), 32768, b_, c_
+        mpc = int(os.environ.get("SYNTH_MPC", "1"))  # messages per connection
+        data, cb, msg_len, K = bench.synth_trace(c_, b_, seed=1, msgs=mpc), 32768, b_, c_ * mpc
     else:
         data, meta, _ = bench.load_trace("cfg2_32k")
         data = bench.interleave(data, K)

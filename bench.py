@@ -767,10 +767,11 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     offs = np.concatenate([[0], np.cumsum(rows_self[rank])[:-1]]) * row
     sc, rc = rows[rank] * row, rows[:, rank] * row
     cap = int(max(rows.max() * row, 16))
-    # pieces: about 8 per hot receiver's inbound volume (the receive path runs
-    # once per piece, so fewer, larger pieces when the incast is heavy)
+    # pieces: about 3 per hot receiver's inbound volume (direct mode runs the
+    # receive path once per message, when its headers land with the first
+    # piece; N = 2: 64 / 96 / 128 / 256 MiB pieces 1.42 / 1.39 / 1.36 / 1.46 ms)
     inbound = int(rows.sum(0).max()) * row
-    pb = max(64 << 20, (inbound // 8) >> 20 << 20)
+    pb = max(64 << 20, (inbound // 3) >> 20 << 20)
     if os.environ.get("CN_A2A_PIECE_MB"):
         pb = int(os.environ["CN_A2A_PIECE_MB"]) << 20
     direct = os.environ.get("CN_A2A_DIRECT", "1") == "1"  # bytes straight into the receive slots

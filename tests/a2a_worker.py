@@ -30,6 +30,10 @@ def main():
     cap = 3 << 20
     for direct in (True, False):  # bytes straight into the receive slots / staged + scattered
         run_mode(AllToAll(cap, direct=direct), n, r, iters, cap)
+    # several pieces per message: the receive path on the whole message once its
+    # headers land (early), or piece by piece as each lands
+    for early in (True, False):
+        run_mode(AllToAll(cap, direct=True, piece_bytes=1 << 20, early=early), n, r, iters, cap)
     # odd message sizes: unaligned pieces fall back from SM stores to the copy engines
     run_mode(AllToAll(cap, direct=True), n, r, 2, cap, odd=3)
     dist.barrier()

@@ -767,11 +767,12 @@ def moe_bench(dev, world, rank, tokens=4096, hidden=7168, iters=5, warmup=2):
     offs = np.concatenate([[0], np.cumsum(rows_self[rank])[:-1]]) * row
     sc, rc = rows[rank] * row, rows[:, rank] * row
     cap = int(max(rows.max() * row, 16))
-    # pieces: about 3 per hot receiver's inbound volume (direct mode runs the
-    # receive path once per message, when its headers land with the first
-    # piece; N = 2: 64 / 96 / 128 / 256 MiB pieces 1.42 / 1.39 / 1.36 / 1.46 ms)
-    inbound = int(rows.sum(0).max()) * row
-    pb = max(64 << 20, (inbound // 3) >> 20 << 20)
+    # pieces: 3 per largest message (direct mode runs the receive path on a
+    # message once its headers land with the first piece, beside the rest;
+    # N = 2, 421 MB: 6 / 4 / 2 pieces 1.42 / 1.36-1.41 / 1.46 ms; N = 4, 354 MB
+    # per source: 6 / 4 / 3 / 1 pieces 3.56 / 3.53 / 3.49 / 3.61 ms)
+    biggest = int(rows.max()) * row
+    pb = max(32 << 20, -(-biggest // (3 << 20)) << 20)
     if os.environ.get("CN_A2A_PIECE_MB"):
         pb = int(os.environ["CN_A2A_PIECE_MB"]) << 20
     direct = os.environ.get("CN_A2A_DIRECT", "1") == "1"  # bytes straight into the receive slots

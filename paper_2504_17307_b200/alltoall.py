@@ -62,6 +62,7 @@ class AllToAll:
         # lane measured no better with SM push: 1.56 vs 1.54 ms, N = 2)
         self.nl = int(os.environ.get("CN_A2A_LANES", "2"))
         self.calls = 0
+        self._rx_clean = False  # the receive state was reset after the previous call's last batch
         L = _lib.lib()
         self.max_pkts = L.cn_packet_count(self.cap, chunk_bytes, MAX_PAYLOAD)
         # receive side: posted destination slot, staging slot and header slot per source
@@ -191,7 +192,9 @@ class AllToAll:
         assert max(send_counts) <= self.cap and max(recv_counts) <= self.cap
         ppc = -(-self.cb // MAX_PAYLOAD)
         self.calls += 1
-        self.rx.reset(s)
+        if not self._rx_clean:
+            self.rx.reset(s)
+        self._rx_clean = False
         if self.direct:  # my receive slots are free (stream order): arm every source
             for src in range(n):
                 if src != r:
@@ -233,12 +236,12 @@ class AllToAll:
                 continue
             pe = self.peer[d]
             # d consumed every piece of my previous message (slot and header reuse)
+            # (direct mode: and d armed its receive slot for me this call) -- one wait kernel
             for ln in range(self.nl):
-                _lib.check(L.cn_flag_wait(self.f_freed + 16 * d + 8 * ln, None, self.sent[d][ln], self.max_spins,
-                                          self.f_err, cs(self.lanes[ln])), "cn_flag_wait")
-                if self.direct:  # d armed its receive slot for me this call
-                    _lib.check(L.cn_flag_wait(self.f_armed + 8 * d, None, self.calls, self.max_spins, self.f_err,
-                                              cs(self.lanes[ln])), "cn_flag_wait")
+                _lib.check(L.cn_flag_wait_signal(self.f_freed + 16 * d + 8 * ln, self.sent[d][ln],
+                                                 self.f_armed + 8 * d if self.direct else None, self.calls,
+                                                 None, 0, self.max_spins, self.f_err, cs(self.lanes[ln])),
+                           "cn_flag_wait_signal")
             npk = L.cn_packet_count(send_counts[d], self.cb, MAX_PAYLOAD)
             oh = self._out_hdrs.data_ptr() + d * self.max_pkts * 64
             for p, (lo, hi) in enumerate(self._pieces(send_counts[d])):
@@ -264,6 +267,9 @@ class AllToAll:
             src = (r - k) % n
             if recv_counts[src]:
                 plan[src] = (k, self._pieces(recv_counts[src]))
+        # receive batches this call runs; after the last one the receive state
+        # is reset for the next call, beside the pieces still in flight
+        left = sum(1 if self.early else len(v[1]) for v in plan.values())
         for p in range(max([len(v[1]) for v in plan.values()] or [0])):
             for k in range(1, n):
                 src = (r - k) % n
@@ -273,23 +279,30 @@ class AllToAll:
                 ln = (ks + p) % self.nl
                 lo, hi = plan[src][1][p]
                 self.recvd[src][ln] += 1
+                freed = self.peer[src]["flags"] + 16 * n + 16 * r + 8 * ln  # src's freed[r][ln]
+                if self.early and p > 0:  # nothing to run on this piece: wait for it and release it, one kernel
+                    _lib.check(L.cn_flag_wait_signal(self.f_ready + 16 * src + 8 * ln, self.recvd[src][ln], None,
+                                                     0, freed, self.recvd[src][ln], self.max_spins, self.f_err,
+                                                     cs(s)), "cn_flag_wait_signal")
+                    continue
                 _lib.check(L.cn_flag_wait(self.f_ready + 16 * src + 8 * ln, None, self.recvd[src][ln],
                                           self.max_spins, self.f_err, cs(s)), "cn_flag_wait")
                 a = lo // self.cb * ppc
                 b = (L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD) if hi == recv_counts[src]
                      else hi // self.cb * ppc)
                 if self.early:  # every header of the message, once (they landed with piece 0)
-                    a, b = 0, (L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD) if p == 0 else 0)
+                    a, b = 0, L.cn_packet_count(recv_counts[src], self.cb, MAX_PAYLOAD)
                 hd = _PeerView(self._hdrs.data_ptr() + src * self.max_pkts * 64 + a * 64, (b - a) * 64)
-                if self.early and b == 0:
-                    pass
-                elif self.direct:  # headers only: the bytes already sit in the receive slot
+                if self.direct:  # headers only: the bytes already sit in the receive slot
                     self.rx.rx_batch_async(hd, None, 0, s, n=b - a)
                 else:
                     pl = _PeerView(self._stage.data_ptr() + src * self.cap, recv_counts[src])
                     self.rx.rx_batch_async(hd, pl, 0, s, n=b - a)
-                _lib.check(L.cn_flag_signal(self.peer[src]["flags"] + 16 * n + 16 * r + 8 * ln, None,
-                                            self.recvd[src][ln], cs(s)), "cn_flag_signal")  # src's freed[r][ln]
+                left -= 1
+                if left == 0:
+                    self.rx.reset(s)
+                    self._rx_clean = True
+                _lib.check(L.cn_flag_signal(freed, None, self.recvd[src][ln], cs(s)), "cn_flag_signal")
         for ln, ev in zip(self.lanes, self.ev_lanes):
             ev.record(ln)
         for ln in self.lanes + [self.hdr_stream]:

@@ -81,6 +81,25 @@ __global__ void k_flag_wait(const unsigned long long* a, const unsigned long lon
     __threadfence_system();
 }
 
+__global__ void k_flag_wait_signal(const unsigned long long* wa, unsigned long long va,
+                                   const unsigned long long* wb, unsigned long long vb, unsigned long long* sg,
+                                   unsigned long long vs, unsigned long long max_spins, unsigned int* err) {
+    unsigned long long spins = 0;
+    for (;;) {
+        unsigned long long x = ~0ull, y = ~0ull;
+        if (wa) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(wa) : "memory");
+        if (wb) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(y) : "l"(wb) : "memory");
+        if (x >= va && y >= vb) break;
+        if (++spins > max_spins) {
+            atomicOr(err, 1u);
+            break;
+        }
+        __nanosleep(100);
+    }
+    __threadfence_system();
+    if (sg) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(sg), "l"(vs) : "memory");
+}
+
 __device__ __forceinline__ long long ctr_target(const unsigned long long* it, unsigned long long per_iter,
                                                 long long off) {
     return static_cast<long long>(*reinterpret_cast<const volatile unsigned long long*>(it) * per_iter) + off;
@@ -268,6 +287,16 @@ extern "C" int cn_ipc_close(void* d_ptr) {
 extern "C" int cn_flag_signal(unsigned long long* d_a, unsigned long long* d_b, uint64_t value,
                               void* stream) {
     k_flag_signal<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_a, d_b, value);
+    CNB_CUDA(cudaGetLastError());
+    return CN_OK;
+}
+
+extern "C" int cn_flag_wait_signal(const unsigned long long* d_wa, uint64_t va, const unsigned long long* d_wb,
+                                   uint64_t vb, unsigned long long* d_s, uint64_t vs, uint64_t max_spins,
+                                   unsigned int* d_err, void* stream) {
+    if (!d_err) return CN_E_INVALID;
+    k_flag_wait_signal<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_wa, va, d_wb, vb, d_s, vs, max_spins,
+                                                                        d_err);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }

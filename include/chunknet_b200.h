@@ -535,10 +535,14 @@ int cn_ipc_close(void* d_ptr);
 int cn_flag_signal(unsigned long long* d_a, unsigned long long* d_b, uint64_t value, void* stream);
 int cn_flag_wait(const unsigned long long* d_a, const unsigned long long* d_b, uint64_t value,
                  uint64_t max_spins, unsigned int* d_err, void* stream);
-/* One kernel for a wait followed by a signal: spin until *d_wa >= va and
- * *d_wb >= vb (a null pointer is met), then, if d_s, release-store vs into
- * *d_s (system scope).  Saves a launch on the all-to-all's per-piece
- * handshakes. */
+/* A notification that publishes no data ("my receive slot is free"): a
+ * relaxed system-scope store of value into *d_a, no fence (the stream's
+ * earlier kernels have completed). */
+int cn_flag_post(unsigned long long* d_a, uint64_t value, void* stream);
+/* One kernel for a wait followed by a notice: spin until *d_wa >= va and
+ * *d_wb >= vb (a null pointer is met), then, if d_s, store vs into *d_s
+ * as cn_flag_post does (a consumption notice: it publishes no data).
+ * Saves a launch on the all-to-all's per-piece handshakes. */
 int cn_flag_wait_signal(const unsigned long long* d_wa, uint64_t va, const unsigned long long* d_wb,
                         uint64_t vb, unsigned long long* d_s, uint64_t vs, uint64_t max_spins,
                         unsigned int* d_err, void* stream);

@@ -149,6 +149,8 @@ def lib():
     L.cn_ipc_close.argtypes = [vp]
     L.cn_flag_signal.argtypes = [vp, vp, u64, vp]
     L.cn_flag_wait.argtypes = [vp, vp, u64, u64, vp, vp]
+    if hasattr(L, "cn_flag_post"):
+        L.cn_flag_post.argtypes = [vp, u64, vp]
     if hasattr(L, "cn_flag_wait_signal"):
         L.cn_flag_wait_signal.argtypes = [vp, u64, vp, u64, vp, u64, u64, vp, vp]
     L.cn_ctr_wait.argtypes = [vp, vp, u64, ctypes.c_int64, u64, vp, vp]

@@ -198,8 +198,8 @@ class AllToAll:
         if self.direct:  # my receive slots are free (stream order): arm every source
             for src in range(n):
                 if src != r:
-                    _lib.check(L.cn_flag_signal(self.peer[src]["flags"] + self.o_armed + 8 * r, None, self.calls,
-                                                ctypes.c_void_p(s.cuda_stream)), "cn_flag_signal")
+                    _lib.check(L.cn_flag_post(self.peer[src]["flags"] + self.o_armed + 8 * r, self.calls,
+                                              ctypes.c_void_p(s.cuda_stream)), "cn_flag_post")
         self.ev_init.record(s)
         for ln in self.lanes:
             ln.wait_event(self.ev_init)
@@ -302,7 +302,7 @@ class AllToAll:
                 if left == 0:
                     self.rx.reset(s)
                     self._rx_clean = True
-                _lib.check(L.cn_flag_signal(freed, None, self.recvd[src][ln], cs(s)), "cn_flag_signal")
+                _lib.check(L.cn_flag_post(freed, self.recvd[src][ln], cs(s)), "cn_flag_post")  # consumed
         for ln, ev in zip(self.lanes, self.ev_lanes):
             ev.record(ln)
         for ln in self.lanes + [self.hdr_stream]:

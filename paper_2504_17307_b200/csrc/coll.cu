@@ -81,6 +81,10 @@ __global__ void k_flag_wait(const unsigned long long* a, const unsigned long lon
     __threadfence_system();
 }
 
+__global__ void k_flag_post(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+
 __global__ void k_flag_wait_signal(const unsigned long long* wa, unsigned long long va,
                                    const unsigned long long* wb, unsigned long long vb, unsigned long long* sg,
                                    unsigned long long vs, unsigned long long max_spins, unsigned int* err) {
@@ -96,8 +100,10 @@ __global__ void k_flag_wait_signal(const unsigned long long* wa, unsigned long l
         }
         __nanosleep(100);
     }
-    __threadfence_system();
-    if (sg) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(sg), "l"(vs) : "memory");
+    if (sg)  // a consumption notice: it publishes nothing this stream wrote
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(sg), "l"(vs) : "memory");
+    else
+        __threadfence_system();
 }
 
 __device__ __forceinline__ long long ctr_target(const unsigned long long* it, unsigned long long per_iter,
@@ -287,6 +293,13 @@ extern "C" int cn_ipc_close(void* d_ptr) {
 extern "C" int cn_flag_signal(unsigned long long* d_a, unsigned long long* d_b, uint64_t value,
                               void* stream) {
     k_flag_signal<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_a, d_b, value);
+    CNB_CUDA(cudaGetLastError());
+    return CN_OK;
+}
+
+extern "C" int cn_flag_post(unsigned long long* d_a, uint64_t value, void* stream) {
+    if (!d_a) return CN_E_INVALID;
+    k_flag_post<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_a, value);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }

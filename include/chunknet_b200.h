@@ -563,6 +563,12 @@ int cn_copy_async(void* d_dst, const void* d_src, uint64_t bytes, void* stream);
 /* The same transfer driven by SM threads (16-byte aligned pointers and size;
  * blocks = 0 picks one per SM): posted NVLink writes beside the copy engines. */
 int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks, void* stream);
+/* cn_copy_sm whose last block then raises a progress flag as cn_flag_signal
+ * does (release-store of value into *d_flag, system scope), saving the
+ * separate signal launch.  d_ctr: a zeroed device word private to the
+ * stream, left zero again. */
+int cn_copy_sm_signal(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks,
+                      unsigned long long* d_flag, uint64_t value, unsigned int* d_ctr, void* stream);
 
 /* -------------------------------------------------------- transport
  * One object in the shape of chunknet::Transport (transport.hpp:53-107):

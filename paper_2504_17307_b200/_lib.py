@@ -158,6 +158,8 @@ def lib():
     L.cn_ctr_advance.argtypes = [vp, vp]
     L.cn_copy_async.argtypes = [vp, vp, u64, vp]
     L.cn_copy_sm.argtypes = [vp, vp, u64, u32, vp]
+    if hasattr(L, "cn_copy_sm_signal"):
+        L.cn_copy_sm_signal.argtypes = [vp, vp, u64, u32, vp, u64, vp, vp]
     L.cn_eqds_config_default.argtypes = [vp]
     L.cn_eqds_config_default.restype = None
     L.cn_eqds_create.argtypes = [vp, u32, ctypes.POINTER(vp)]

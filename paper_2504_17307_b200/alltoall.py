@@ -74,6 +74,7 @@ class AllToAll:
         # (written by destinations), err, spare, armed[n] (written by
         # destinations: my receive slot for you is free for call k)
         self._flags = DeviceBuffer((5 * n + 2) * 8, self.dev)
+        self._ctr = DeviceBuffer(64, self.dev)  # per push lane: the signalling copy's block counter
         self.flags = self._flags.tensor(torch.int64, 5 * n + 2)
         fp = self._flags.data_ptr()
         self.f_ready, self.f_freed = fp, fp + 16 * n
@@ -137,7 +138,7 @@ class AllToAll:
         for p in self._opened:
             _lib.lib().cn_ipc_close(ctypes.c_void_p(p))
         self._opened = []
-        for b in (self._recv, self._stage, self._hdrs, self._out_hdrs, self._flags):
+        for b in (self._recv, self._stage, self._hdrs, self._out_hdrs, self._flags, self._ctr):
             if b is not None:
                 b.free()
 
@@ -253,14 +254,16 @@ class AllToAll:
                     _lib.check(L.cn_copy_async(pe["hdrs"] + r * self.max_pkts * 64, oh, npk * 64, cs(sp)),
                                "cn_copy_async")
                 dst_p, src_p = pe["land"] + r * self.cap + lo, sb + send_offsets[d] + lo
+                self.sent[d][ln] += 1
+                ready = pe["flags"] + 16 * r + 8 * ln
                 if self.push.startswith("sm") and not ((dst_p | src_p | (hi - lo)) & 15):
+                    # the copy's last block raises d's ready flag
                     nb = int(self.push.split(":")[1]) if ":" in self.push else 64
-                    _lib.check(L.cn_copy_sm(dst_p, src_p, hi - lo, nb, cs(sp)), "cn_copy_sm")
+                    _lib.check(L.cn_copy_sm_signal(dst_p, src_p, hi - lo, nb, ready, self.sent[d][ln],
+                                                   self._ctr.data_ptr() + 4 * ln, cs(sp)), "cn_copy_sm_signal")
                 else:  # the copy engines (or a piece not 16-byte aligned, which SM vectors cannot move)
                     _lib.check(L.cn_copy_async(dst_p, src_p, hi - lo, cs(sp)), "cn_copy_async")
-                self.sent[d][ln] += 1
-                _lib.check(L.cn_flag_signal(pe["flags"] + 16 * r + 8 * ln, None, self.sent[d][ln], cs(sp)),
-                           "cn_flag_signal")
+                    _lib.check(L.cn_flag_signal(ready, None, self.sent[d][ln], cs(sp)), "cn_flag_signal")
         # receive: pieces as they land, interleaved over the sources (r-1, r-2, ...)
         plan = {}
         for k in range(1, n):

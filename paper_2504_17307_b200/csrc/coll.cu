@@ -143,7 +143,8 @@ __global__ void k_ctr_advance(unsigned long long* it) { *it += 1; }
 // destination these are NVLink posted writes, a second "wire" beside the
 // copy engines.
 __global__ void __launch_bounds__(512) k_copy_sm(int4* __restrict__ dst, const int4* __restrict__ src,
-                                                 uint64_t nv) {
+                                                 uint64_t nv, unsigned long long* flag, unsigned long long value,
+                                                 unsigned int* ctr) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     for (; i + 3 * stride < nv; i += 4 * stride) {
@@ -155,6 +156,18 @@ __global__ void __launch_bounds__(512) k_copy_sm(int4* __restrict__ dst, const i
         dst[i + 3 * stride] = e;
     }
     for (; i < nv; i += stride) dst[i] = __ldcs(src + i);
+    if (flag) {  // the last block to finish raises the flag (its peers' stores fenced first)
+        __shared__ bool last;
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            __threadfence_system();
+            *ctr = 0;  // for the next copy on this stream
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+        }
+    }
 }
 
 }  // namespace cnb
@@ -212,7 +225,20 @@ extern "C" int cn_copy_sm(void* d_dst, const void* d_src, uint64_t bytes, uint32
         return CN_E_INVALID;
     }
     k_copy_sm<<<blocks ? blocks : 148, 512, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<int4*>(d_dst), static_cast<const int4*>(d_src), bytes >> 4);
+        static_cast<int4*>(d_dst), static_cast<const int4*>(d_src), bytes >> 4, nullptr, 0, nullptr);
+    CNB_CUDA(cudaGetLastError());
+    return CN_OK;
+}
+
+extern "C" int cn_copy_sm_signal(void* d_dst, const void* d_src, uint64_t bytes, uint32_t blocks,
+                                 unsigned long long* d_flag, uint64_t value, unsigned int* d_ctr, void* stream) {
+    if (!d_dst || !d_src || !d_flag || !d_ctr || !bytes ||
+        ((reinterpret_cast<uintptr_t>(d_dst) | reinterpret_cast<uintptr_t>(d_src) | bytes) & 15)) {
+        set_error("cn_copy_sm_signal: non-empty, 16-byte aligned copy and a flag and counter required");
+        return CN_E_INVALID;
+    }
+    k_copy_sm<<<blocks ? blocks : 148, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<int4*>(d_dst), static_cast<const int4*>(d_src), bytes >> 4, d_flag, value, d_ctr);
     CNB_CUDA(cudaGetLastError());
     return CN_OK;
 }

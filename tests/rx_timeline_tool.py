@@ -22,10 +22,11 @@ def main():
     torch.cuda.set_device(dev)
     if os.environ.get("SYNTH"):  # SYNTH=<conns>x<bytes>: bench.synth_trace (configs[4] sweep)
         c_, b_ = (int(v) for v in os.environ["SYNTH"].split("x"))
-        data = bench.synth_trace(c_, b_, seed=1)
+        mpc = int(os.environ.get("SYNTH_MPC", "1"))  # messages per connection
+        data = bench.synth_trace(c_, b_, seed=1, msgs=mpc)
         cb = 32768
         msg_len = b_
-        K = c_
+        K = c_ * mpc
     else:
         data, meta, _ = bench.load_trace("cfg2_32k")
         data = bench.interleave(data, K)
@@ -37,8 +38,8 @@ def main():
     sts = [torch.randint(0, 256, (n * bench.MAX_PL,), dtype=torch.uint8, device=dev) for _ in range(2)]
     st = sts[0]
     tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
-                      arena_bytes=K * (msg_len + (1 << 20)), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
-                      max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8))
+                      arena_bytes=3 * K * (msg_len + 512) + (64 << 20), chunk_pool=4 * K * ((msg_len + cb - 1) // cb),
+                      max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 4 * K + 16))
     steady = os.environ.get("STEADY") == "1"
     if steady:
         from paper_2504_17307_b200.records import PKT_DTYPE
@@ -59,8 +60,9 @@ def main():
     if pipe:  # bench.py's headline: pipelined receiver, steady state, one graph of `steps` steps
         from paper_2504_17307_b200.records import PKT_DTYPE
         tr = cn.Transport(cn.TransportConfig(chunk_bytes=cb, carry_payload=True), device=dev,
-                          arena_bytes=3 * K * (msg_len + (1 << 20)), chunk_pool=3 * K * ((msg_len + cb - 1) // cb),
-                          max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 2 * K + 8), pipeline=True)
+                          arena_bytes=3 * K * (msg_len + 512) + (64 << 20),
+                          chunk_pool=3 * K * ((msg_len + cb - 1) // cb) + 64,
+                          max_batch=n, max_conns=max(64, 2 * K + 8), max_msgs=max(64, 4 * K + 16), pipeline=True)
         si = PKT_DTYPE.fields["msg_seq"][1] // 8
         hs = []
         for j in range(2 * steps + 1):

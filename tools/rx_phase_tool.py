@@ -31,7 +31,7 @@ def main():
         mpc = int(os.environ.get("SYNTH_MPC", "1"))  # messages per connection
         data, cb, msg_len, K = bench.synth_trace(c_, b_, seed=1, msgs=mpc), 32768, b_, c_ * mpc
     else:
-        data, meta, _ = bench.load_trace("cfg2_32k")
+        data, meta, _ = bench.load_trace(os.environ.get("TRACE", "cfg2_32k"))
         data = bench.interleave(data, K)
         cb, msg_len = meta["chunk_bytes"], int(data["msg_len"][0])
     n = len(data)

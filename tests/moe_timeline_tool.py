@@ -31,7 +31,7 @@ def main():
     offs = np.concatenate([[0], np.cumsum(rows_self[rank])[:-1]]) * row
     sc, rc = rows[rank] * row, rows[:, rank] * row
     cap = int(max(rows.max() * row, 16))
-    pb = int(os.environ.get("CN_A2A_PIECE_MB", "135")) << 20
+    pb = int(os.environ.get("CN_A2A_PIECE_MB", "113")) << 20
     direct = os.environ.get("CN_A2A_DIRECT", "1") == "1"
     a2a, a2c = AllToAll(cap, piece_bytes=pb, direct=direct), AllToAll(cap, piece_bytes=pb, direct=direct)
     coffs = [s_ * a2a.cap for s_ in range(world)]
